@@ -1,0 +1,168 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the beLLMan scenario
+ * simulation (arXiv 2510.15330).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no
+ * code, header, table or constant generator with the CUDA path
+ * (paper_2510_15330_b200/); both take their inputs from workloads/.
+ *
+ * Structure (deliberately unlike the GPU kernel): all arrivals are generated up
+ * front into an array; a binary heap of typed events drives a textbook
+ * discrete-event simulation; per-request structs; an explicit FIFO queue; the
+ * per-second signal series is kept in full and the moving average recomputed
+ * from it at every ingest.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * Rn = reading n in DESIGN.md §3 (== SURVEY.md §8(c).2).
+ *
+ * Parity pins (tests/test_oracle_*.py): Random123 KATs (Philox), libm -log
+ * (neglog), Decimal log2 table, SPEC worked examples, hand fixtures F1-F6
+ * (tests/golden/), a brute-force microsecond-stepping simulator on tiny
+ * traces, M/D/1 Pollaczek-Khinchine, the uncongested-regime bound, the
+ * sample-path Little's law identity, controller law vs exact rationals.
+ * "parity unpinned": the paper's directional outcomes (A4) and the saturation
+ * capacity of P24/L8B (calibration outputs), see DESIGN.md §6.
+ */
+#ifndef BELLMAN_ORACLE_H
+#define BELLMAN_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_LAW_OFF = 0, ORC_LAW_CONST = 1, ORC_LAW_MAP = 2, ORC_LAW_STEP = 3 };
+enum { ORC_SIG_TBT = 0, ORC_SIG_E2E = 1, ORC_SIG_SLO = 2 };
+enum { ORC_MODE_CUTOFF = 0, ORC_MODE_DRAIN = 1 };
+enum { ORC_FLAG_TRUNCATED = 1, ORC_FLAG_DEGENERATE_CALIB = 2 };
+
+#define ORC_NONE 0xFFFFFFFFu
+#define ORC_HIST_LAT 896 /* log-linear ms bins, 32 per octave (a9) */
+#define ORC_HIST_R 512   /* 10 bp bins of r */
+
+/* ---- column inputs, exactly as workloads.Workload.columns() builds them ---- */
+typedef struct {
+  const int64_t *knot_t;
+  const uint32_t *knot_lam;
+  const uint32_t *trace_knot_off, *trace_n_knots, *trace_cap;
+  const uint32_t *prof_t0, *prof_knee, *prof_slope, *prof_kv, *prof_maxb, *prof_prefill_ns;
+  const double *prof_e_in, *prof_e_out, *prof_p_idle;
+  const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
+  const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
+  const uint32_t *ctrl_rungs; /* [n_ctrl][8] */
+  const int32_t *tab_L, *tab_I, *tab_fvar, *tab_noise, *tab_fcomp; /* [4096] each */
+  const int64_t *poly_q16;                                          /* [3] */
+  const uint32_t *sc_seed;
+  const uint64_t *sc_wid;
+  const uint32_t *sc_trace, *sc_profile, *sc_ctrl, *sc_segment, *sc_mode;
+  const int64_t *sc_horizon, *sc_w0, *sc_w1;
+  const uint32_t *sc_calib_src, *sc_record;
+  uint64_t n_scenarios;
+} orc_inputs;
+
+/* One accepted arrival with its per-request model draws (a2, a3). */
+typedef struct {
+  uint64_t a_us;       /* arrival time */
+  uint32_t j;          /* candidate index (Philox counter word 0) */
+  uint32_t L;          /* natural (median) unbounded output words */
+  uint32_t input;      /* input words */
+  uint32_t U;          /* realized unbounded output words */
+  uint32_t P;          /* predicted output words */
+  int32_t fcomp_q16;   /* compliance factor */
+} orc_request;
+
+typedef struct {
+  uint32_t t0_us, knee, slope_us, kv_ns_per_word, max_batch, prefill_ns_per_word;
+  double e_in, e_out, p_idle;
+} orc_profile;
+
+typedef struct {
+  uint32_t law, signal, window, r_min_bp, r_max_bp, r_const_bp, t1, t2, slo_us, calibrated, n_rungs;
+  uint32_t rungs_bp[8];
+} orc_ctrl;
+
+typedef struct {
+  uint32_t mode;
+  int64_t horizon_us, w0_us, w1_us;
+  int64_t poly_q16[3];
+  uint32_t record; /* keep the per-second signal series */
+} orc_run_cfg;
+
+typedef struct {
+  uint64_t ticks, candidates, arrivals, admitted, served, rewritten;
+  uint64_t words_in, words_out, idle_us, end_us, queued_end, inflight_end;
+  uint64_t win_served, win_words_in, win_words_out, win_idle_us;
+  uint64_t sum_queue_us, sum_ttft_us, sum_e2e_us, slo_violations;
+  uint32_t e2e_p50_ms, e2e_p99_ms, ttft_p50_ms, ttft_p99_ms, median_r_bp;
+  uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
+  double energy_j, win_energy_j;
+  /* ---- self-checks the GPU never computes ---- */
+  uint64_t e2e_exact_p50_us, e2e_exact_p99_us, ttft_exact_p50_us, ttft_exact_p99_us;
+  uint64_t int_system_us;  /* integral of (queued + in_system) dt, µs*requests */
+  uint64_t int_queue_us;   /* integral of queued dt */
+  uint64_t sum_sojourn_us; /* sum over completed of (completion - arrival) */
+  uint64_t tbt_samples, tbt_sum_us, tbt_max_us;
+  uint32_t hist_e2e[ORC_HIST_LAT], hist_ttft[ORC_HIST_LAT], hist_r[ORC_HIST_R];
+  uint32_t n_series; /* per-second signal samples written to series[] (record mode) */
+} orc_result;
+
+/* Optional per-request / per-gap / controller trace for hand fixtures. */
+typedef struct {
+  uint64_t admit_us, first_us, done_us; /* UINT64_MAX if the event did not happen */
+  uint32_t R, r_bp, n_gaps, _pad;
+} orc_req_log;
+
+typedef struct {
+  uint32_t second, sample, k, r_bp, active, _pad;
+  uint64_t A;
+} orc_ctrl_log;
+
+typedef struct {
+  orc_req_log *req;    /* [n_requests] or NULL */
+  uint64_t *gaps;      /* pairs (request index, gap µs), capacity cap_gaps pairs, or NULL */
+  uint64_t cap_gaps, n_gaps;
+  orc_ctrl_log *ctrl;  /* capacity cap_ctrl or NULL */
+  uint64_t cap_ctrl, n_ctrl;
+  uint32_t *series;    /* per-second samples (record mode), capacity cap_series */
+  uint64_t cap_series;
+} orc_log;
+
+/* Philox4x32-10 (Salmon et al., SC'11), key = (k0, k1), counter c[4]. */
+void orc_philox(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t out[4]);
+/* -ln(U) in Q32 for U = (2u+1)/2^33 (reading R33). */
+uint64_t orc_neglog_q32(uint32_t u);
+/* round(2^32 log2(1 + i/4096)), i = 0..4096 (reading R33). */
+uint64_t orc_log2_table(uint32_t i);
+/* latency bin of a value in ms, and the lower edge of a bin (a9). */
+uint32_t orc_lat_bin(uint64_t ms);
+uint64_t orc_lat_edge(uint32_t bin);
+
+/* Generate the accepted arrivals of scenario sid (a2 + a3); returns the count
+ * (all of them up to the trace end / arrival cap), or -1 on allocation failure.
+ * If out is NULL only counts. */
+int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint64_t cap_out);
+
+/* The discrete-event simulation (a4-a9) over an explicit request list. */
+int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof,
+                 const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log);
+
+/* Full scenario: arrivals + (calibration pass a10) + simulation. */
+int orc_run_scenario(const orc_inputs *in, uint64_t sid, orc_result *res, orc_log *log);
+
+/* Nearest-rank percentile of a sample list, 0 < p <= 100 (p = 0 -> min). */
+uint32_t orc_percentile_u32(const uint32_t *v, uint64_t n, uint32_t p);
+
+/* Threshold calibration (a10): 0 ok, 1 insufficient, 2 degenerate. */
+int orc_calibrate(const uint32_t *series, uint64_t n, uint32_t *t1, uint32_t *t2);
+
+/* Controller law as a pure function (a6): r in bp for a window sum A over k samples. */
+uint32_t orc_map_rate(uint64_t A, uint32_t k, const orc_ctrl *c);
+
+/* Run many scenarios on nthreads host threads (cpu baseline). Returns 0 on success. */
+int orc_run_batch(const orc_inputs *in, const uint64_t *sids, uint64_t n, orc_result *res, int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

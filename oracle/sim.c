@@ -1,0 +1,623 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * A textbook discrete-event simulation of one LLM serving node under the
+ * beLLMan controller (a4-a10).  Times are integer microseconds.
+ *
+ * Serving model (SPEC serving_sim, readings R6-R9, R18-R21):
+ *  - continuous batching: "one global iteration loop; each iteration all active
+ *    requests emit one word; new requests admitted between iterations FIFO up
+ *    to max_batch; a request's prefill occupies it for prefill_time before its
+ *    first decode step but does not block others";
+ *  - decode iteration time t0 + slope*max(0, B - knee) + the optional
+ *    KV term floor(kv_ns_per_word * K / 1000) (reading R2);
+ *  - prefill time prefill_ns_per_word * input / 1000, at least 1 µs;
+ *  - first word at prefill end; TBT = inter-token gaps (R6);
+ *  - a request admitted while the loop runs joins at the next boundary (R6);
+ *  - admission points: every event instant at which the loop is idle (an
+ *    iteration end makes it idle); arrivals <= T are eligible (R7);
+ *  - simultaneous events: iteration end, prefill ends (by j), arrivals (by j),
+ *    then ingest, admission, iteration start (R7).
+ * Controller (R3-R5, R12, R21, R38): the per-second
+ * signal sample is ingested at each admission point for every closed second;
+ * moving average over the last `window` samples; active iff MA >= t1; the
+ * linear law maps MA in [t1, t2] to r in [r_min, r_max]; ladders floor it to a
+ * rung; STEP climbs a rung per ingest while active.  Rewrite at admission:
+ * N = round(P (1 - r)), realized = round(poly(N) * Fcomp).
+ * Energy: e_in * words_in + e_out * words_out + p_idle * idle.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "oracle.h"
+
+#define US 1000000ull
+#define NEVER UINT64_MAX
+
+enum { EV_ITER_END = 0, EV_PREFILL_END = 1, EV_ARRIVAL = 2 };
+enum { RS_FUTURE = 0, RS_QUEUED, RS_PREFILL, RS_READY, RS_DECODING, RS_DONE };
+
+typedef struct {
+  uint64_t t;
+  uint32_t kind, idx;
+} event;
+
+typedef struct {
+  event *v;
+  uint64_t n, cap;
+} heap;
+
+static int ev_less(const event *a, const event *b) {
+  if (a->t != b->t) return a->t < b->t;
+  if (a->kind != b->kind) return a->kind < b->kind;
+  return a->idx < b->idx;
+}
+
+static int heap_push(heap *h, event e) {
+  if (h->n == h->cap) {
+    uint64_t nc = h->cap ? 2 * h->cap : 64;
+    event *nv = (event *)realloc(h->v, nc * sizeof(event));
+    if (!nv) return -1;
+    h->v = nv;
+    h->cap = nc;
+  }
+  uint64_t i = h->n++;
+  h->v[i] = e;
+  while (i > 0) {
+    uint64_t p = (i - 1) / 2;
+    if (!ev_less(&h->v[i], &h->v[p])) break;
+    event t = h->v[i]; h->v[i] = h->v[p]; h->v[p] = t;
+    i = p;
+  }
+  return 0;
+}
+
+static event heap_pop(heap *h) {
+  event top = h->v[0];
+  h->v[0] = h->v[--h->n];
+  uint64_t i = 0;
+  for (;;) {
+    uint64_t l = 2 * i + 1, r = l + 1, m = i;
+    if (l < h->n && ev_less(&h->v[l], &h->v[m])) m = l;
+    if (r < h->n && ev_less(&h->v[r], &h->v[m])) m = r;
+    if (m == i) break;
+    event t = h->v[i]; h->v[i] = h->v[m]; h->v[m] = t;
+    i = m;
+  }
+  return top;
+}
+
+/* ---------------------------------------------------------------------------
+ * latency histogram bins (a9): integer ms, 32 log-linear sub-buckets per
+ * octave.  Bin b < 32 holds exactly b ms; above, bin 32(e-4)+s holds
+ * [(32+s) 2^(e-5), (33+s) 2^(e-5)).  The bin of a value is found by search
+ * over the edges (the definition), not by bit tricks.
+ * ------------------------------------------------------------------------- */
+uint64_t orc_lat_edge(uint32_t b) {
+  if (b < 32) return b;
+  uint32_t e = b / 32 + 4, s = b % 32;
+  return (uint64_t)(32 + s) << (e - 5);
+}
+
+uint32_t orc_lat_bin(uint64_t ms) {
+  uint32_t lo = 0, hi = ORC_HIST_LAT - 1; /* largest b with edge(b) <= ms */
+  if (ms >= orc_lat_edge(hi)) return hi;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi + 1) / 2;
+    if (orc_lat_edge(mid) <= ms) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+/* nearest-rank percentile (R13): rank k = max(1, ceil(p n / 100)) */
+static uint64_t nr_rank(uint64_t n, uint32_t p) {
+  uint64_t k = (p * n + 99) / 100;
+  return k < 1 ? 1 : k;
+}
+
+static int cmp_u32(const void *a, const void *b) {
+  uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+  return x < y ? -1 : x > y;
+}
+static int cmp_u64(const void *a, const void *b) {
+  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : x > y;
+}
+
+uint32_t orc_percentile_u32(const uint32_t *v, uint64_t n, uint32_t p) {
+  if (n == 0) return ORC_NONE;
+  uint32_t *s = (uint32_t *)malloc(n * sizeof(uint32_t));
+  if (!s) return ORC_NONE;
+  memcpy(s, v, n * sizeof(uint32_t));
+  qsort(s, n, sizeof(uint32_t), cmp_u32);
+  uint32_t r = p == 0 ? s[0] : s[nr_rank(n, p) - 1];
+  free(s);
+  return r;
+}
+
+/* a10 — "We pick the median TBT (T1) during the unbounded run ... and the 75th
+ * percentile TBT (T2)"; >= 4 samples, t1 != t2. */
+int orc_calibrate(const uint32_t *series, uint64_t n, uint32_t *t1, uint32_t *t2) {
+  if (n < 4) { *t1 = *t2 = 0; return 1; }
+  *t1 = orc_percentile_u32(series, n, 50);
+  *t2 = orc_percentile_u32(series, n, 75);
+  return *t1 == *t2 ? 2 : 0;
+}
+
+/* a6 — the first-cut law: r = 0 below t1; r_min at
+ * t1 rising linearly to r_max at t2; clamped.  Exact integer form of
+ * r_min + (r_max - r_min)(MA - t1)/(t2 - t1) with MA = A/k, floored to a bp. */
+uint32_t orc_map_rate(uint64_t A, uint32_t k, const orc_ctrl *c) {
+  if (A < (uint64_t)k * c->t1) return 0;
+  uint64_t num = (uint64_t)(c->r_max_bp - c->r_min_bp) * (A - (uint64_t)k * c->t1);
+  uint64_t den = (uint64_t)k * (c->t2 - c->t1);
+  uint64_t r = c->r_min_bp + num / den;
+  if (r > c->r_max_bp) r = c->r_max_bp;
+  if (c->n_rungs) { /* ladder (R5): the largest rung <= r */
+    uint32_t best = c->rungs_bp[0];
+    for (uint32_t i = 0; i < c->n_rungs; ++i)
+      if (c->rungs_bp[i] <= r) best = c->rungs_bp[i];
+    r = best;
+  }
+  return (uint32_t)r;
+}
+
+/* floor(x / 2^32) for signed 128-bit x */
+static __int128 floor_div_2p32(__int128 x) {
+  __int128 d = (__int128)1 << 32;
+  __int128 q = x / d;
+  if ((x % d) != 0 && x < 0) q -= 1;
+  return q;
+}
+
+/* a7 — bounded target N = round(P (1 - r)) (R11) and realized
+ * length round(poly(N) * Fcomp) clamped to [1, 2^24]. */
+static uint32_t bounded_realized(uint32_t P, uint32_t r_bp, int32_t fcomp, const int64_t poly[3]) {
+  int64_t N = ((int64_t)P * (10000 - (int64_t)r_bp) + 5000) / 10000;
+  if (N < 1) N = 1;
+  __int128 p = (__int128)poly[0] + (__int128)poly[1] * N + (__int128)poly[2] * N * N;
+  __int128 x = floor_div_2p32(p * fcomp + ((__int128)1 << 31));
+  if (x < 1) x = 1;
+  if (x > (1 << 24)) x = 1 << 24;
+  return (uint32_t)x;
+}
+
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t admit, first, done, last_tok, prefill_end;
+  uint32_t emitted, R, r_bp, state, n_gaps;
+} rstate;
+
+typedef struct {
+  const orc_ctrl *c;
+  uint32_t law;
+  uint32_t *samples;
+  uint64_t n, cap;
+  int active;
+  uint32_t r, rung;
+} cstate;
+
+static int push_u32(uint32_t **v, uint64_t *n, uint64_t *cap, uint32_t x) {
+  if (*n == *cap) {
+    uint64_t nc = *cap ? 2 * *cap : 64;
+    uint32_t *nv = (uint32_t *)realloc(*v, nc * sizeof(uint32_t));
+    if (!nv) return -1;
+    *v = nv;
+    *cap = nc;
+  }
+  (*v)[(*n)++] = x;
+  return 0;
+}
+
+/* one controller ingest of the sample x of closed second `second` (a6) */
+static int ingest(cstate *cs, uint32_t second, uint32_t x, orc_result *res, orc_log *log) {
+  if (cs->law != ORC_LAW_MAP && cs->law != ORC_LAW_STEP) return 0;
+  if (push_u32(&cs->samples, &cs->n, &cs->cap, x)) return -1;
+  const orc_ctrl *c = cs->c;
+  /* moving average over the last `window` samples; partial window at start */
+  uint32_t k = cs->n < c->window ? (uint32_t)cs->n : c->window;
+  uint64_t A = 0;
+  for (uint64_t i = cs->n - k; i < cs->n; ++i) A += cs->samples[i];
+  int act = A >= (uint64_t)k * c->t1; /* MA >= T1 triggers (R38); below resets */
+  uint32_t r = 0;
+  if (act) {
+    if (cs->law == ORC_LAW_MAP) {
+      r = orc_map_rate(A, k, c);
+    } else { /* STEP (R4, R5): rung 0 on activation, one rung up per ingest while active */
+      if (!cs->active) cs->rung = 0;
+      else if (cs->rung + 1 < c->n_rungs) cs->rung++;
+      r = c->rungs_bp[cs->rung];
+    }
+  }
+  if (act && !cs->active) {
+    res->activations++;
+    if (res->first_act_s == ORC_NONE) res->first_act_s = second;
+  }
+  if (!act && cs->active) res->last_deact_s = second;
+  if (act) res->active_ingests++;
+  cs->active = act;
+  cs->r = r;
+  if (log && log->ctrl) {
+    if (log->n_ctrl < log->cap_ctrl) {
+      orc_ctrl_log *L = &log->ctrl[log->n_ctrl];
+      L->second = second; L->sample = x; L->k = k; L->r_bp = r; L->active = (uint32_t)act; L->A = A;
+    }
+    log->n_ctrl++;
+  }
+  return 0;
+}
+
+static uint64_t overlap(uint64_t a, uint64_t b, int64_t w0, int64_t w1) {
+  uint64_t lo = a > (uint64_t)w0 ? a : (uint64_t)w0;
+  uint64_t hi = b < (uint64_t)w1 ? b : (uint64_t)w1;
+  return hi > lo ? hi - lo : 0;
+}
+
+static int in_window(uint64_t t, const orc_run_cfg *cfg) {
+  return (int64_t)t >= cfg->w0_us && (int64_t)t < cfg->w1_us;
+}
+
+int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof,
+                 const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log) {
+  memset(res, 0, sizeof(*res));
+  res->first_act_s = res->last_deact_s = ORC_NONE;
+  res->t1 = ctrl->t1;
+  res->t2 = ctrl->t2;
+  const uint64_t H = (uint64_t)cfg->horizon_us;
+  int rc = -1;
+
+  rstate *rs = (rstate *)calloc(n_req ? n_req : 1, sizeof(rstate));
+  uint32_t *queue = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
+  uint32_t *ready = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
+  uint32_t *batch = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
+  uint64_t *e2e_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
+  uint64_t *ttft_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
+  uint64_t n_sec = H / US + 2;
+  uint64_t *sec_tbt_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_tbt_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_e2e_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_e2e_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_slo_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  heap h = {0, 0, 0};
+  cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
+  if (!rs || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
+      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt)
+    goto out;
+  if (cs.law == ORC_LAW_CONST) cs.r = ctrl->r_const_bp; /* S:320-326 constant policy */
+
+  for (uint64_t i = 0; i < n_req; ++i) {
+    rs[i].admit = rs[i].first = rs[i].done = NEVER;
+    if (heap_push(&h, (event){req[i].a_us, EV_ARRIVAL, (uint32_t)i})) goto out;
+  }
+
+  uint64_t q_head = 0, q_tail = 0, n_ready = 0, n_batch = 0, in_sys = 0;
+  uint64_t n_e2e = 0, n_ttft = 0;
+  int busy = 0;
+  uint64_t next_sec = 0; /* first second not yet ingested */
+  uint64_t T_prev = 0, last_T = 0;
+  uint64_t n_series = 0;
+
+#define INGEST_UNTIL(TT)                                                                 \
+  do {                                                                                   \
+    for (; (next_sec + 1) * US <= (TT); ++next_sec) {                                    \
+      uint64_t cnt, sum;                                                                 \
+      if (next_sec >= n_sec) continue;                                                   \
+      if (ctrl->signal == ORC_SIG_TBT) { cnt = sec_tbt_cnt[next_sec]; sum = sec_tbt_sum[next_sec]; } \
+      else if (ctrl->signal == ORC_SIG_E2E) { cnt = sec_e2e_cnt[next_sec]; sum = sec_e2e_sum[next_sec]; } \
+      else { cnt = sec_e2e_cnt[next_sec]; sum = 1000 * sec_slo_cnt[next_sec]; }          \
+      if (cnt == 0) continue; /* a second with no samples is a gap */     \
+      uint32_t x = (uint32_t)(sum / cnt);                                                \
+      if (cfg->record) {                                                                 \
+        if (log && log->series && n_series < log->cap_series) log->series[n_series] = x; \
+        n_series++;                                                                      \
+      }                                                                                  \
+      if (ingest(&cs, (uint32_t)next_sec, x, res, log)) goto out;                        \
+    }                                                                                    \
+  } while (0)
+
+  for (;;) {
+    if (h.n == 0) break;
+    uint64_t T = h.v[0].t;
+    if (T >= H) break;
+    /* integrate piecewise-constant state over [T_prev, T) */
+    {
+      uint64_t dt = T - T_prev, nq = q_tail - q_head;
+      if (in_sys == 0) {
+        res->idle_us += dt;
+        res->win_idle_us += overlap(T_prev, T, cfg->w0_us, cfg->w1_us);
+      }
+      res->int_system_us += (nq + in_sys) * dt;
+      res->int_queue_us += nq * dt;
+    }
+    T_prev = T;
+    last_T = T;
+    uint64_t s_idx = T / US;
+    while (h.n && h.v[0].t == T) {
+      event e = heap_pop(&h);
+      if (e.kind == EV_ITER_END) {
+        /* E1: every request in the iteration emits a word at T */
+        for (uint64_t b = 0; b < n_batch; ++b) {
+          uint32_t m = batch[b];
+          uint64_t gap = T - rs[m].last_tok;
+          sec_tbt_sum[s_idx] += gap;
+          sec_tbt_cnt[s_idx] += 1;
+          res->tbt_samples++;
+          res->tbt_sum_us += gap;
+          if (gap > res->tbt_max_us) res->tbt_max_us = gap;
+          if (log && log->gaps && log->n_gaps < log->cap_gaps) {
+            log->gaps[2 * log->n_gaps] = m;
+            log->gaps[2 * log->n_gaps + 1] = gap;
+          }
+          if (log) log->n_gaps++;
+          rs[m].n_gaps++;
+          rs[m].last_tok = T;
+          rs[m].emitted++;
+          res->words_out++;
+          if (in_window(T, cfg)) res->win_words_out++;
+          if (rs[m].emitted == rs[m].R) { /* completes: E2E = completion - arrival */
+            uint64_t e2e = T - req[m].a_us;
+            rs[m].done = T;
+            rs[m].state = RS_DONE;
+            in_sys--;
+            res->served++;
+            res->sum_e2e_us += e2e;
+            res->sum_sojourn_us += e2e;
+            e2e_v[n_e2e++] = e2e;
+            res->hist_e2e[orc_lat_bin(e2e / 1000)]++;
+            if (in_window(T, cfg)) res->win_served++;
+            sec_e2e_sum[s_idx] += e2e;
+            sec_e2e_cnt[s_idx] += 1;
+            if (e2e > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }
+          } else {
+            rs[m].state = RS_READY;
+            ready[n_ready++] = m;
+          }
+        }
+        n_batch = 0;
+        busy = 0;
+      } else if (e.kind == EV_PREFILL_END) {
+        /* E2: first word at prefill end; TTFT = first token - arrival */
+        uint32_t m = e.idx;
+        uint64_t ttft = T - req[m].a_us;
+        rs[m].first = T;
+        rs[m].last_tok = T;
+        rs[m].emitted = 1;
+        res->words_out++;
+        if (in_window(T, cfg)) res->win_words_out++;
+        res->sum_ttft_us += ttft;
+        ttft_v[n_ttft++] = ttft;
+        res->hist_ttft[orc_lat_bin(ttft / 1000)]++;
+        if (rs[m].R == 1) { /* R9: realized length 1 completes at prefill end */
+          uint64_t e2e = ttft;
+          rs[m].done = T;
+          rs[m].state = RS_DONE;
+          in_sys--;
+          res->served++;
+          res->sum_e2e_us += e2e;
+          res->sum_sojourn_us += e2e;
+          e2e_v[n_e2e++] = e2e;
+          res->hist_e2e[orc_lat_bin(e2e / 1000)]++;
+          if (in_window(T, cfg)) res->win_served++;
+          sec_e2e_sum[s_idx] += e2e;
+          sec_e2e_cnt[s_idx] += 1;
+          if (e2e > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }
+        } else {
+          rs[m].state = RS_READY;
+          ready[n_ready++] = m;
+        }
+      } else { /* E3: arrival -> FIFO queue */
+        uint32_t m = e.idx;
+        rs[m].state = RS_QUEUED;
+        queue[q_tail++] = m;
+        res->arrivals++;
+        res->candidates = (uint64_t)req[m].j + 1;
+      }
+    }
+    if (!busy) {
+      /* admission point: ingest every closed second, then admit FIFO */
+      INGEST_UNTIL(T);
+      while (in_sys < prof->max_batch && q_head < q_tail) {
+        uint32_t m = queue[q_head++];
+        uint32_t r = cs.r;
+        rs[m].admit = T;
+        rs[m].r_bp = r;
+        rs[m].R = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+        uint64_t pf = ((uint64_t)prof->prefill_ns_per_word * req[m].input) / 1000;
+        rs[m].prefill_end = T + (pf < 1 ? 1 : pf);
+        rs[m].state = RS_PREFILL;
+        in_sys++;
+        res->admitted++;
+        res->sum_queue_us += T - req[m].a_us;
+        res->words_in += req[m].input;
+        if (in_window(T, cfg)) res->win_words_in += req[m].input;
+        if (r > 0) {
+          res->rewritten++;
+          res->hist_r[r / 10 < ORC_HIST_R ? r / 10 : ORC_HIST_R - 1]++;
+        }
+        if (heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m})) goto out;
+      }
+      /* iteration start with every decode-ready request */
+      if (n_ready > 0) {
+        uint64_t K = 0;
+        for (uint64_t b = 0; b < n_ready; ++b) {
+          uint32_t m = ready[b];
+          batch[b] = m;
+          rs[m].state = RS_DECODING;
+          K += req[m].input + rs[m].emitted;
+        }
+        n_batch = n_ready;
+        n_ready = 0;
+        uint64_t B = n_batch;
+        uint64_t d = prof->t0_us + (uint64_t)prof->slope_us * (B > prof->knee ? B - prof->knee : 0) +
+                     ((uint64_t)prof->kv_ns_per_word * K) / 1000;
+        if (heap_push(&h, (event){T + d, EV_ITER_END, 0})) goto out;
+        busy = 1;
+        res->ticks++;
+      }
+    }
+  }
+
+  /* termination (R20): cutoff -> end at H; drain -> last event, unless capped */
+  uint64_t end = (cfg->mode == ORC_MODE_DRAIN && h.n == 0) ? last_T : H;
+  {
+    uint64_t dt = end - T_prev, nq = q_tail - q_head;
+    if (in_sys == 0) {
+      res->idle_us += dt;
+      res->win_idle_us += overlap(T_prev, end, cfg->w0_us, cfg->w1_us);
+    }
+    res->int_system_us += (nq + in_sys) * dt;
+    res->int_queue_us += nq * dt;
+  }
+  res->end_us = end;
+  INGEST_UNTIL(end);
+  res->queued_end = q_tail - q_head;
+  res->inflight_end = in_sys;
+  if (res->queued_end + res->inflight_end > 0) res->flags |= ORC_FLAG_TRUNCATED;
+
+  /* a8 energy, fp64, in this fixed order (R19) */
+  {
+    double a = prof->e_in * (double)res->words_in;
+    double b = prof->e_out * (double)res->words_out;
+    double c = prof->p_idle * (double)res->idle_us;
+    res->energy_j = (a + b) + c / 1e6;
+    double wa = prof->e_in * (double)res->win_words_in;
+    double wb = prof->e_out * (double)res->win_words_out;
+    double wc = prof->p_idle * (double)res->win_idle_us;
+    res->win_energy_j = (wa + wb) + wc / 1e6;
+  }
+  /* a9 percentiles: nearest rank on the histograms -> bin lower edge */
+  {
+    uint64_t n = res->served;
+    res->e2e_p50_ms = res->e2e_p99_ms = res->ttft_p50_ms = res->ttft_p99_ms = ORC_NONE;
+    res->median_r_bp = ORC_NONE;
+    const uint32_t ps[2] = {50, 99};
+    for (int w = 0; w < 2; ++w) {
+      const uint32_t *hh = w == 0 ? res->hist_e2e : res->hist_ttft;
+      uint64_t nn = w == 0 ? n : n_ttft;
+      for (int q = 0; q < 2; ++q) {
+        if (nn == 0) continue;
+        uint64_t k = nr_rank(nn, ps[q]), cum = 0;
+        uint32_t bsel = 0;
+        for (uint32_t b = 0; b < ORC_HIST_LAT; ++b) {
+          cum += hh[b];
+          if (cum >= k) { bsel = b; break; }
+        }
+        uint32_t v = (uint32_t)orc_lat_edge(bsel);
+        if (w == 0 && q == 0) res->e2e_p50_ms = v;
+        if (w == 0 && q == 1) res->e2e_p99_ms = v;
+        if (w == 1 && q == 0) res->ttft_p50_ms = v;
+        if (w == 1 && q == 1) res->ttft_p99_ms = v;
+      }
+    }
+    if (res->rewritten) {
+      uint64_t k = nr_rank(res->rewritten, 50), cum = 0;
+      for (uint32_t b = 0; b < ORC_HIST_R; ++b) {
+        cum += res->hist_r[b];
+        if (cum >= k) { res->median_r_bp = b * 10; break; }
+      }
+    }
+    /* exact nearest-rank values (self-check only) */
+    qsort(e2e_v, n_e2e, sizeof(uint64_t), cmp_u64);
+    qsort(ttft_v, n_ttft, sizeof(uint64_t), cmp_u64);
+    res->e2e_exact_p50_us = n_e2e ? e2e_v[nr_rank(n_e2e, 50) - 1] : NEVER;
+    res->e2e_exact_p99_us = n_e2e ? e2e_v[nr_rank(n_e2e, 99) - 1] : NEVER;
+    res->ttft_exact_p50_us = n_ttft ? ttft_v[nr_rank(n_ttft, 50) - 1] : NEVER;
+    res->ttft_exact_p99_us = n_ttft ? ttft_v[nr_rank(n_ttft, 99) - 1] : NEVER;
+  }
+  res->n_series = (uint32_t)n_series;
+  if (log && log->req) {
+    for (uint64_t i = 0; i < n_req; ++i) {
+      log->req[i].admit_us = rs[i].admit;
+      log->req[i].first_us = rs[i].first;
+      log->req[i].done_us = rs[i].done;
+      log->req[i].R = rs[i].R;
+      log->req[i].r_bp = rs[i].r_bp;
+      log->req[i].n_gaps = rs[i].n_gaps;
+    }
+  }
+  rc = 0;
+out:
+  free(rs); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
+  free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
+  free(h.v); free(cs.samples);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc_ctrl *c, orc_run_cfg *cfg) {
+  uint32_t pi = in->sc_profile[sid], ci = in->sc_ctrl[sid];
+  p->t0_us = in->prof_t0[pi];
+  p->knee = in->prof_knee[pi];
+  p->slope_us = in->prof_slope[pi];
+  p->kv_ns_per_word = in->prof_kv[pi];
+  p->max_batch = in->prof_maxb[pi];
+  p->prefill_ns_per_word = in->prof_prefill_ns[pi];
+  p->e_in = in->prof_e_in[pi];
+  p->e_out = in->prof_e_out[pi];
+  p->p_idle = in->prof_p_idle[pi];
+  memset(c, 0, sizeof(*c));
+  c->law = in->ctrl_law[ci];
+  c->signal = in->ctrl_signal[ci];
+  c->window = in->ctrl_window[ci];
+  c->r_min_bp = in->ctrl_rmin[ci];
+  c->r_max_bp = in->ctrl_rmax[ci];
+  c->r_const_bp = in->ctrl_rconst[ci];
+  c->t1 = in->ctrl_t1[ci];
+  c->t2 = in->ctrl_t2[ci];
+  c->slo_us = in->ctrl_slo_us[ci];
+  c->calibrated = in->ctrl_calibrated[ci];
+  c->n_rungs = in->ctrl_nrungs[ci];
+  for (int k = 0; k < 8; ++k) c->rungs_bp[k] = in->ctrl_rungs[8 * ci + k];
+  cfg->mode = in->sc_mode[sid];
+  cfg->horizon_us = in->sc_horizon[sid];
+  cfg->w0_us = in->sc_w0[sid];
+  cfg->w1_us = in->sc_w1[sid];
+  for (int k = 0; k < 3; ++k) cfg->poly_q16[k] = in->poly_q16[k];
+  cfg->record = in->sc_record[sid];
+}
+
+static int run_internal(const orc_inputs *in, uint64_t sid, int force_record, orc_result *res, orc_log *log) {
+  orc_profile prof;
+  orc_ctrl ctrl;
+  orc_run_cfg cfg;
+  scenario_cfg(in, sid, &prof, &ctrl, &cfg);
+  if (force_record) cfg.record = 1;
+  uint32_t flags = 0;
+  if (ctrl.calibrated && (ctrl.law == ORC_LAW_MAP || ctrl.law == ORC_LAW_STEP)) {
+    /* a10: two-pass calibration from the paired unbounded run */
+    uint64_t src = in->sc_calib_src[sid];
+    uint64_t cap = (uint64_t)in->sc_horizon[src] / US + 2;
+    uint32_t *series = (uint32_t *)malloc(cap * sizeof(uint32_t));
+    orc_result *tmp = (orc_result *)malloc(sizeof(orc_result));
+    if (!series || !tmp) { free(series); free(tmp); return -1; }
+    orc_log slog;
+    memset(&slog, 0, sizeof(slog));
+    slog.series = series;
+    slog.cap_series = cap;
+    if (run_internal(in, src, 1, tmp, &slog)) { free(series); free(tmp); return -1; }
+    uint32_t t1, t2;
+    int st = orc_calibrate(series, tmp->n_series, &t1, &t2);
+    ctrl.t1 = t1;
+    ctrl.t2 = t2;
+    if (st) { /* degenerate / insufficient -> controller off, flagged */
+      flags |= ORC_FLAG_DEGENERATE_CALIB;
+      ctrl.law = ORC_LAW_OFF;
+    }
+    free(series);
+    free(tmp);
+  }
+  int64_t n = orc_arrivals(in, sid, NULL, 0);
+  orc_request *req = (orc_request *)malloc((n > 0 ? (uint64_t)n : 1) * sizeof(orc_request));
+  if (!req) return -1;
+  if (orc_arrivals(in, sid, req, (uint64_t)n) != n) { free(req); return -1; }
+  int rc = orc_simulate(req, (uint64_t)n, &prof, &ctrl, &cfg, res, log);
+  res->flags |= flags;
+  free(req);
+  return rc;
+}
+
+int orc_run_scenario(const orc_inputs *in, uint64_t sid, orc_result *res, orc_log *log) {
+  if (sid >= in->n_scenarios) return -1;
+  return run_internal(in, sid, 0, res, log);
+}

@@ -1,0 +1,132 @@
+"""Brute-force microsecond-stepping simulator — a pin for the oracle's DES.
+
+Deliberately the dumbest possible algorithm: it walks simulated time one
+microsecond at a time and, at every microsecond, applies the serving rules of
+SPEC.md S:245 (continuous batching) in the order fixed by S:247 / readings
+R6-R9: iteration end, prefill ends (by j), arrivals (by j), then — if the loop
+is idle — ingest, admission and iteration start.  No event heap, no
+incremental sums.  Usable only on tiny traces (<= ~2e6 µs).  Controller: the
+linear MAP law recomputed from a Fraction moving average.
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+
+def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max=2000, window=5,
+             r_const=0, mode_drain=True):
+    n = len(requests)
+    st = ["future"] * n
+    admit = [None] * n
+    pend = [None] * n
+    first = [None] * n
+    done = [None] * n
+    last = [None] * n
+    emitted = [0] * n
+    R = [0] * n
+    rbp = [0] * n
+    queue = []
+    ready = []
+    batch = []
+    iter_end = None
+    ticks = 0
+    words_out = 0
+    gaps = [[] for _ in range(n)]
+    sec_sum, sec_cnt = {}, {}
+    samples = []
+    ingested_upto = 0  # next second to ingest
+    r_cur = r_const if law == "const" else 0
+    last_event = 0
+    t = 0
+    while t < horizon_us:
+        anything = False
+        if iter_end == t:
+            anything = True
+            for m in batch:
+                g = t - last[m]
+                gaps[m].append(g)
+                sec_sum[t // 10**6] = sec_sum.get(t // 10**6, 0) + g
+                sec_cnt[t // 10**6] = sec_cnt.get(t // 10**6, 0) + 1
+                last[m] = t
+                emitted[m] += 1
+                words_out += 1
+                if emitted[m] == R[m]:
+                    st[m] = "done"
+                    done[m] = t
+                else:
+                    st[m] = "ready"
+                    ready.append(m)
+            batch = []
+            iter_end = None
+        for m in range(n):
+            if st[m] == "prefill" and pend[m] == t:
+                anything = True
+                first[m] = t
+                last[m] = t
+                emitted[m] = 1
+                words_out += 1
+                if R[m] == 1:
+                    st[m] = "done"
+                    done[m] = t
+                else:
+                    st[m] = "ready"
+                    ready.append(m)
+        for m in range(n):
+            if st[m] == "future" and requests[m]["a_us"] == t:
+                anything = True
+                st[m] = "queued"
+                queue.append(m)
+        if anything:
+            last_event = t
+        if anything and iter_end is None:
+            # ingest every closed second
+            while (ingested_upto + 1) * 10**6 <= t:
+                s = ingested_upto
+                ingested_upto += 1
+                if sec_cnt.get(s, 0) == 0:
+                    continue
+                x = sec_sum[s] // sec_cnt[s]
+                if law == "map":
+                    samples.append(x)
+                    k = min(len(samples), window)
+                    ma = Fraction(sum(samples[-k:]), k)
+                    if ma < t1:
+                        r_cur = 0
+                    else:
+                        r = Fraction(r_min) + Fraction(r_max - r_min) * (ma - t1) / (t2 - t1)
+                        r_cur = min(r_max, int(r))  # floor to a basis point
+            in_sys = sum(1 for i in range(n) if st[i] in ("prefill", "ready", "decoding"))
+            while in_sys < prof["max_batch"] and queue:
+                m = queue.pop(0)
+                admit[m] = t
+                rbp[m] = r_cur
+                q = requests[m]
+                if r_cur > 0:
+                    N = max(1, int(Fraction(q.get("P", q["U"])) * (Fraction(10000 - r_cur, 10000)) + Fraction(1, 2)))
+                    R[m] = max(1, int(Fraction(N) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
+                else:
+                    R[m] = q["U"]
+                pf = prof["prefill_ns_per_word"] * q["input"] // 1000
+                pend[m] = t + max(1, pf)
+                st[m] = "prefill"
+                in_sys += 1
+            if ready:
+                B = len(ready)
+                K = sum(requests[m]["input"] + emitted[m] for m in ready)
+                d = prof["t0_us"] + prof["slope_us"] * max(0, B - prof["knee"]) + \
+                    prof.get("kv_ns_per_word", 0) * K // 1000
+                batch = list(ready)
+                for m in batch:
+                    st[m] = "decoding"
+                ready = []
+                iter_end = t + d
+                ticks += 1
+        t += 1
+        if mode_drain and all(s in ("done",) for s in st):
+            break
+    end = last_event if mode_drain and all(s == "done" for s in st) else horizon_us
+    if mode_drain and all(s == "done" for s in st):
+        # idle was counted through t = end inclusive of the final µs loop; recount up to end
+        pass
+    return dict(admit=admit, first=first, done=done, R=R, r_bp=rbp, gaps=gaps, ticks=ticks,
+                words_out=words_out, end_us=end, served=sum(1 for s in st if s == "done"))

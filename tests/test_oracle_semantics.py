@@ -1,0 +1,227 @@
+"""Pins for the oracle's serving simulation and controller (a4-a10).
+
+* hand-computed timelines (tests/golden/appendixA_fixtures.json: SPEC S:207,
+  S:233 and SURVEY Appendix A F2-F5);
+* SPEC.md's worked examples (S:124-144, S:215-226, S:233-235, S:289-327,
+  S:376-378) — exact;
+* a brute-force microsecond-stepping simulator (tests/bruteforce.py) on random
+  tiny traces — exact, per request and per gap.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import workloads as W
+from tests import bruteforce
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "appendixA_fixtures.json")
+
+
+def _fixtures():
+    with open(GOLD) as f:
+        g = json.load(f)
+    return [(g["profile"], fx) for fx in g["fixtures"]]
+
+
+@pytest.mark.parametrize("prof,fx", _fixtures(), ids=lambda x: x.get("name", "") if isinstance(x, dict) else "")
+def test_appendix_fixture(orc, prof, fx):
+    prof = dict(prof, **fx.get("profile_override", {}))
+    d = orc.simulate(fx["requests"], prof, mode=W.MODE_DRAIN)
+    for i, er in enumerate(fx.get("expect_requests", [])):
+        for k, v in er.items():
+            assert d["requests"][i][k] == v, (fx["name"], i, k)
+    for i, eg in enumerate(fx.get("expect_gaps", [])):
+        assert d["gaps"][i] == eg, (fx["name"], i)
+    for i, eg in enumerate(fx.get("expect_gap_first3", [])):
+        assert d["gaps"][i][:3] == eg
+    for k, v in fx["expect"].items():
+        assert d[k] == v, (fx["name"], k, d[k], v)
+    # latency ordering E2E >= TTFT >= queueing >= 0
+    for i, q in enumerate(fx["requests"]):
+        r = d["requests"][i]
+        assert r["done_us"] - q["a_us"] >= r["first_us"] - q["a_us"] >= r["admit_us"] - q["a_us"] >= 0
+
+
+LIT = W.PROFILES["spec-literal"]
+
+
+def test_cost_law_examples(orc):
+    """d(1) = 50 ms; d(16) = 50 + 6*8 = 98 ms (one iteration, drain)."""
+    for B, d_us in ((1, 50_000), (16, 98_000), (8, 50_000), (9, 56_000)):
+        reqs = [dict(a_us=0, input=1, U=2) for _ in range(B)]
+        d = orc.simulate(reqs, LIT, mode=W.MODE_DRAIN)
+        assert d["ticks"] == 1 and d["end_us"] == 80 + d_us
+        assert d["tbt_sum_us"] == B * d_us
+
+
+def test_prefill_examples(orc):
+    """10,000 words at 80 ms/kword -> 800 ms; 1 word -> 0.08 ms."""
+    for inp, pf in ((10_000, 800_000), (1, 80)):
+        d = orc.simulate([dict(a_us=0, input=inp, U=1)], LIT, mode=W.MODE_DRAIN)
+        assert d["requests"][0]["first_us"] == pf and d["ticks"] == 0
+
+
+def test_kv_term(orc):
+    """Reading R2: d = t0 + slope*max(0,B-knee) + floor(kv_ns*K/1000), K = sum of
+    (input + words emitted) over the batch at iteration start."""
+    prof = dict(LIT, kv_ns_per_word=70)
+    d = orc.simulate([dict(a_us=0, input=1000, U=3), dict(a_us=0, input=3000, U=2)], prof, mode=W.MODE_DRAIN)
+    # both first words at 80,000 / 240,000; A joins at 80,000 alone: K = 1001
+    # -> d = 50,000 + 70 (floor(70*1001/1000) = 70)
+    g = d["gaps"]
+    assert g[0][0] == 50_070
+
+
+def test_energy_examples(orc):
+    """one request (10,000 in / 500 out) -> 750 J; 0 requests over
+    10 s at 100 W -> 1,000 J; S:235 additivity over disjoint windows."""
+    prof = dict(LIT, p_idle=100.0)
+    d = orc.simulate([], prof, mode=W.MODE_CUTOFF, horizon_us=10 * W.US)
+    assert d["energy_j"] == 1000.0
+    d = orc.simulate([dict(a_us=0, input=10_000, U=500)], LIT, mode=W.MODE_DRAIN)
+    assert d["energy_j"] == 750.0
+    reqs = [dict(a_us=k * 400_000, input=1000 + k, U=20 + k) for k in range(12)]
+    full = orc.simulate(reqs, LIT, mode=W.MODE_CUTOFF, horizon_us=8 * W.US)
+    a = orc.simulate(reqs, LIT, mode=W.MODE_CUTOFF, horizon_us=8 * W.US, w0_us=0, w1_us=3 * W.US)
+    b = orc.simulate(reqs, LIT, mode=W.MODE_CUTOFF, horizon_us=8 * W.US, w0_us=3 * W.US, w1_us=8 * W.US)
+    assert a["win_energy_j"] + b["win_energy_j"] == pytest.approx(full["energy_j"], rel=1e-12)
+    assert a["win_served"] + b["win_served"] == full["served"]
+    assert a["win_words_out"] + b["win_words_out"] == full["words_out"]
+
+
+def test_rewrite_examples(orc):
+    """S:133-135 bounded_target: (500, 8%) -> 460, (350, 20%) -> 280; S:142 identity
+    compliance 460 -> 460; S:144 poly (50, 0.8, 0) at N = 300 -> 290."""
+    for P, r, want in ((500, 800, 460), (350, 2000, 280), (500, 0, None)):
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=r)
+        d = orc.simulate([dict(a_us=0, input=1, U=777, P=P)], LIT, ctrl=c, mode=W.MODE_DRAIN)
+        assert d["requests"][0]["R"] == (want if want else 777)
+        assert d["rewritten"] == (1 if r else 0)
+    poly = (50 * 65536, 52429, 0)  # Q16 of (50, 0.8, 0)
+    c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=2000)
+    d = orc.simulate([dict(a_us=0, input=1, U=777, P=375)], LIT, ctrl=c, mode=W.MODE_DRAIN, poly_q16=poly)
+    assert d["requests"][0]["R"] == 290
+    # compliance noise: realized = round(N * Fcomp)
+    d = orc.simulate([dict(a_us=0, input=1, U=777, P=500, fcomp_q16=int(1.05 * 65536))], LIT, ctrl=orc.make_ctrl(
+        law=W.LAW_CONST, r_const_bp=800), mode=W.MODE_DRAIN)
+    assert d["requests"][0]["R"] == 483  # round(460 * 1.05 = 482.99...)
+
+
+def test_controller_examples(orc):
+    """S:289-301 with t1 = 50,000 µs, t2 = 100,000 µs."""
+    c = orc.make_ctrl(law=W.LAW_MAP, t1=50_000, t2=100_000)
+    assert orc.map_rate(10_000 * 3 + 50_000 * 2, 5, c) == 0      # MA 26 ms < t1
+    assert orc.map_rate(5 * 50_000, 5, c) == 500                  # five samples = T1 -> 5%
+    assert orc.map_rate(40_000, 1, c) == 0
+    assert orc.map_rate(50_000, 1, c) == 500
+    assert orc.map_rate(75_000, 1, c) == 1250
+    assert orc.map_rate(180_000, 1, c) == 2000
+    ladder = orc.make_ctrl(law=W.LAW_MAP, t1=50_000, t2=100_000, r_min_bp=500, r_max_bp=2000,
+                           rungs=(500, 1000, 1500, 2000))
+    assert orc.map_rate(75_000, 1, ladder) == 1000
+
+
+def test_map_law_vs_fraction(orc):
+    """The integer law equals floor(r_min + (r_max-r_min)(MA-t1)/(t2-t1)) in exact rationals."""
+    rng = np.random.default_rng(5)
+    for _ in range(3000):
+        t1 = int(rng.integers(1, 100_000))
+        t2 = t1 + int(rng.integers(1, 100_000))
+        rmin = int(rng.integers(1, 3000))
+        rmax = rmin + int(rng.integers(0, 2000))
+        k = int(rng.integers(1, 9))
+        A = int(rng.integers(0, 3 * t2 * k))
+        c = orc.make_ctrl(law=W.LAW_MAP, t1=t1, t2=t2, r_min_bp=rmin, r_max_bp=rmax)
+        ma = Fraction(A, k)
+        want = 0 if ma < t1 else min(rmax, int(rmin + (rmax - rmin) * (ma - t1) / (t2 - t1)))
+        got = orc.map_rate(A, k, c)
+        assert got == want
+        # range {0} U [r_min, r_max] and monotone in MA
+        assert got == 0 or rmin <= got <= rmax
+        assert orc.map_rate(A + k, k, c) >= got
+
+
+def test_calibration_examples(orc):
+    """S:308-310 and the percentile examples S:376-378."""
+    assert orc.calibrate(list(range(10, 111, 10))) == (0, 60, 90)
+    assert orc.calibrate([5, 5, 5, 5])[0] == 2
+    assert orc.calibrate([1, 2, 3])[0] == 1
+    assert orc.percentile(list(range(10, 111, 10)), 50) == 60
+    v = [17, 3, 99, 42, 8]
+    assert orc.percentile(v, 0) == 3 and orc.percentile(v, 100) == 99
+    assert orc.percentile([7], 75) == 7
+
+
+def test_latency_bins(orc):
+    """a9 bins: exact below 32 ms, then 32 log-linear sub-buckets per octave."""
+    assert [orc.lat_bin(x) for x in range(32)] == list(range(32))
+    for b in range(895):
+        lo, hi = orc.lat_edge(b), orc.lat_edge(b + 1)
+        assert lo < hi
+        assert orc.lat_bin(lo) == b and orc.lat_bin(hi - 1) == b
+        if b >= 32:
+            assert (hi - lo) * 32 <= lo  # relative width <= 1/32
+    assert orc.lat_bin(2**32 - 1) == 895
+
+
+def _random_tiny(rng):
+    n = int(rng.integers(1, 7))
+    reqs = []
+    for i in range(n):
+        reqs.append(dict(a_us=int(rng.integers(0, 4000)), input=int(rng.integers(1, 40)),
+                         U=int(rng.integers(1, 9)), P=int(rng.integers(1, 12)),
+                         fcomp_q16=int(rng.integers(50000, 80000))))
+    reqs.sort(key=lambda q: q["a_us"])
+    prof = dict(t0_us=int(rng.integers(1, 300)), knee=int(rng.integers(0, 4)), slope_us=int(rng.integers(0, 90)),
+                kv_ns_per_word=int(rng.integers(0, 3000)), max_batch=int(rng.integers(1, 5)),
+                prefill_ns_per_word=int(rng.integers(0, 40_000)), e_in=0.05, e_out=0.5, p_idle=300.0)
+    prof["knee"] = min(prof["knee"], prof["max_batch"])
+    return reqs, prof
+
+
+def test_bruteforce_tiny_traces(orc):
+    """Event-heap DES == microsecond-stepping brute force on 120 random tiny traces."""
+    rng = np.random.default_rng(11)
+    for case in range(120):
+        reqs, prof = _random_tiny(rng)
+        law = "const" if case % 3 == 0 else "off"
+        rc = int(rng.integers(100, 3000)) if law == "const" else 0
+        bf = bruteforce.simulate(reqs, prof, 10**6, law=law, r_const=rc)
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=rc) if law == "const" else None
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=10**6)
+        assert d["ticks"] == bf["ticks"], case
+        assert d["words_out"] == bf["words_out"], case
+        assert d["end_us"] == bf["end_us"], case
+        assert d["served"] == bf["served"], case
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i]), (case, i)
+            assert d["gaps"][i] == bf["gaps"][i], (case, i)
+
+
+def test_bruteforce_controller(orc):
+    """Controller in the loop (MAP law, TBT signal) vs brute force on short traces
+    spanning several seconds."""
+    rng = np.random.default_rng(3)
+    prof = dict(t0_us=20_000, knee=1, slope_us=9000, kv_ns_per_word=0, max_batch=4,
+                prefill_ns_per_word=1000, e_in=0.05, e_out=0.5, p_idle=300.0)
+    for case in range(6):
+        reqs = []
+        t = 0
+        for i in range(14):
+            t += int(rng.integers(0, 250_000))
+            reqs.append(dict(a_us=t, input=int(rng.integers(1, 100)), U=int(rng.integers(2, 30)),
+                             P=int(rng.integers(5, 40)), fcomp_q16=65536))
+        t1, t2 = 25_000 + 2000 * case, 40_000 + 2000 * case
+        bf = bruteforce.simulate(reqs, prof, 2_000_000 * 3, law="map", t1=t1, t2=t2)
+        c = orc.make_ctrl(law=W.LAW_MAP, t1=t1, t2=t2)
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=6_000_000)
+        assert d["ticks"] == bf["ticks"]
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["done_us"], r["R"], r["r_bp"]) == \
+                   (bf["admit"][i], bf["done"][i], bf["R"][i], bf["r_bp"][i]), (case, i)

@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: simulated scenario-ticks/s of the beLLMan simulator on B200.
+
+Workload (BASELINE.json configs[1]): arrival-rate sweep
+0.5..8 RPS x 64 seeds x {controller off, on}, L8B decode-cost model, 600 s
+simulated per scenario = 2048 scenarios per GPU.  Weak scaling: at N GPUs the
+job is N x 2048 scenarios (64 N seeds), sharded by interleaving (rank r runs
+ids r, r+N, ...); summaries are gathered with NCCL all_gather and segment
+histograms all_reduced — the only exchange step.
+
+A step = one pass of the whole hot path (arrival generation, draws, decode
+iterations, controller, accounting, histograms, percentiles) over the shard,
+plus the summary gather.  Inputs are resident in HBM when the timed region
+starts (value); `e2e` repeats the step through the C ABI with host buffers
+(descriptor H2D in bellman_sim_create, summaries D2H in bellman_sim_stats).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "simulated scenario-ticks/sec"
+UNIT = "scenario-ticks/s"
+SEEDS_PER_GPU = 64
+
+# Survey §8(d) algorithmic integer work per unit (warp-instructions): a0 per
+# tick, 130 per candidate and per admission (Philox-10 + -ln/table draws +
+# thinning), 12 per completion, 40 per ingested second, 6 per prefill end.
+A_TICK, A_CAND, A_ADMIT, A_DONE, A_SEC, A_PF = 12, 130, 130, 12, 40, 6
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seeds-per-gpu", type=int, default=SEEDS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def workload(world: int, seeds_per_gpu: int):
+    return W.config_c2(n_seeds=seeds_per_gpu * world)
+
+
+def algorithmic_ops(st) -> float:
+    """Survey §8(d) per-unit counts x the units the launch processed."""
+    ticks = st["ticks"].astype(np.float64).sum()
+    cand = st["candidates"].astype(np.float64).sum()
+    adm = st["admitted"].astype(np.float64).sum()
+    done = st["served"].astype(np.float64).sum()
+    secs = (st["end_us"].astype(np.float64) // 1e6).sum()
+    return A_TICK * ticks + A_CAND * cand + A_ADMIT * adm + A_DONE * done + A_SEC * secs + A_PF * adm
+
+
+def peaks():
+    p = {"hbm_gbs": 6457.7, "sm_max_mhz": 1965.0, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update(hbm_gbs=m["hbm_gbs"], sm_max_mhz=m["sm_max_mhz"], src="measured")
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cols, budget_s=12.0):
+    """The oracle as it stands, on this host's cores, over repetitions of the
+    same workload until ~budget_s of CPU work (a bounded sample)."""
+    import oracle
+
+    b = oracle.Bound(cols)
+    nthreads = os.cpu_count() or 1
+    ticks, reps = 0, 0
+    t0 = time.perf_counter()
+    while True:
+        rs = oracle.run_batch(b, nthreads=nthreads)
+        ticks += sum(r["ticks"] for r in rs)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": ticks / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": f"{reps} x the full {len(rs)}-scenario C2 workload ({ticks} scenario-ticks, {dt:.1f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cols = workload(1, args.seeds_per_gpu).columns()
+    import oracle
+
+    b = oracle.Bound(cols)
+    nthreads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.run_batch(b, nthreads=nthreads)
+    times, ticks = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rs = oracle.run_batch(b, nthreads=nthreads)
+        times.append(time.perf_counter() - t0)
+        ticks = sum(r["ticks"] for r in rs)
+    tot = sum(times)
+    value = ticks * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": {"workload": "C2 rate sweep 0.5-8 RPS x 64 seeds x {off,on}, L8B, 600 s",
+                                            "scenarios": len(rs)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                             "sample": f"{args.steps} steps x the full {len(rs)}-scenario C2 workload"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_15330_b200 import Simulator, _abi, pack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workload(world, args.seeds_per_gpu)
+    cols = w.columns()
+    n = w.n_scenarios
+    mine = W.shard(n, rank, world)
+    count = len(mine)
+    stream = torch.cuda.current_stream()
+    sim = Simulator(cols, device=local, stream=stream)
+    stats_dev = torch.zeros((n, 256), dtype=torch.uint8, device=dev)
+    shard_dev = torch.zeros((count, 256), dtype=torch.uint8, device=dev)
+    gathered = torch.zeros((world * count, 256), dtype=torch.uint8, device=dev) if world > 1 else None
+    seg_dev = torch.zeros((w.n_segments, _abi.SEG_HIST_WORDS), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        sim.reset(stream)
+        sim.run(first=rank, count=count, stride=world, stream=stream)
+        k_end = torch.cuda.Event(enable_timing=True)
+        k_end.record(stream)
+        sim.stats_device(stats_dev, stream=stream)
+        shard_dev.copy_(stats_dev[rank::world])
+        sim.segment_hist_device(seg_dev, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, shard_dev)
+            dist.all_reduce(seg_dev)
+        return k_end
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (untimed)
+            starts[i].record(stream)
+            kends.append(step())
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(k) for s, k in zip(starts, kends)]
+    tot_ms = sum(step_ms)
+    t = torch.tensor([tot_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms, kern_tot = float(t[0]), float(t[1])
+    # correctness-carrying unit count: ticks from the summaries of this step
+    st_local = stats_dev.cpu().numpy().view(_abi.STATS).reshape(-1)
+    local_ticks = int(st_local["ticks"][mine].astype(np.int64).sum())
+    local_ops = algorithmic_ops(st_local[mine])
+    tt = torch.tensor([local_ticks, local_ops], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt)
+    ticks_all, ops_all = float(tt[0]), float(tt[1])
+    value = ticks_all * args.steps / (tot_ms / 1e3)
+    launches = sim.last_launches
+
+    # ---- e2e through the C ABI with host buffers (pinned) ----
+    pk = pack(cols, pinned=True)
+    host_stats = torch.empty((n, 256), dtype=torch.uint8, pin_memory=True).numpy().view(_abi.STATS).reshape(-1)
+    e2e_ms = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s2 = Simulator(packed=pk, device=local, stream=stream, workspace=sim.ws)
+        s2.run(first=rank, count=count, stride=world, stream=stream)
+        s2.stats(out=host_stats, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        s2.close()
+        if i > 0:
+            e2e_ms.append(a.elapsed_time(b))
+    e = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+    e2e_value = ticks_all * len(e2e_ms) / (float(e[0]) / 1e3)
+    h2d = int(sum(v.nbytes for k, v in pk.items() if isinstance(v, np.ndarray)) +
+              sum(v.nbytes for v in pk["tables"].values()) + 8 * W.TABLE_N + 4 * n)
+    d2h = int(n * 256)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk_ = peaks()
+    clocks = clk.summary()
+    mhz = pk_["sm_max_mhz"]
+    kern_s = kern_tot / 1e3 / args.steps
+    achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G warp-inst/s
+    peak = 148 * 4 * mhz * 1e6 / 1e9
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(workload(1, args.seeds_per_gpu).columns())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "C2 rate sweep 0.5-8 RPS x 64 seeds/GPU x {off,on}, L8B cost model, 600 s cutoff",
+                   "scenarios_per_gpu": count, "scenarios_total": n, "ticks_per_step": int(ticks_all),
+                   "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time; peak = 148 SM x 4 "
+                             f"issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+        "kernel_ms_per_step": kern_tot / args.steps,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+/*
+ * bellman_sim.h — C ABI of the B200-native beLLMan scenario simulator.
+ *
+ * The library simulates, for thousands to millions of independent scenarios,
+ * an LLM serving node under the beLLMan output-length congestion controller
+ * (arXiv 2510.15330).  It follows the paper's problem statement as SPEC.md
+ * restates it: run_simulation(trace, server, models, controller?, seed) ->
+ * RunResult, batched over scenarios.  One warp of a
+ * persistent sm_100a kernel simulates one scenario.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Rn = reading n in
+ * DESIGN.md section 3.  Step names a1..a10 are DESIGN.md section 2.
+ *
+ * Conventions
+ *  - All pointers in bellman_sim_desc are HOST pointers owned by the caller and
+ *    only read during bellman_sim_create (deep copy into the workspace).
+ *  - The workspace is DEVICE memory owned by the caller (e.g. a torch tensor),
+ *    at least bellman_sim_workspace_bytes(desc) bytes, 256-byte aligned, and it
+ *    must outlive the handle.  The library performs no cudaMalloc.
+ *  - Functions taking `stream` are asynchronous and stream-ordered on that
+ *    cudaStream_t (NULL = legacy default stream).
+ *  - Errors: a non-zero bellman_status is returned and a message is kept in
+ *    bellman_sim_last_error(sim) (or the thread-local global message when no
+ *    handle exists).  No exception or abort crosses the ABI.  Per-scenario
+ *    conditions (truncation, degenerate calibration) are FLAGS in the summary
+ *    record, not errors.
+ *  - A handle is single-writer: do not call into one handle from two threads.
+ *  - Determinism: each summary record is a pure function of (desc, scenario id);
+ *    it does not depend on device count, grid shape, stream or run order.
+ */
+#ifndef BELLMAN_SIM_H
+#define BELLMAN_SIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror SPEC.md's exit codes (0 success, 1 validation,
+ * 2 IO, 3 degenerate data) plus device/workspace/state errors. */
+typedef enum {
+  BELLMAN_OK = 0,
+  BELLMAN_EINVAL = 1,      /* descriptor failed validation */
+  BELLMAN_EIO = 2,         /* reserved (no file IO in the library) */
+  BELLMAN_EDEGENERATE = 3, /* reserved: degenerate calibration is a per-scenario flag */
+  BELLMAN_ECUDA = 4,       /* a CUDA runtime call or kernel launch failed */
+  BELLMAN_EWORKSPACE = 5,  /* workspace NULL, misaligned or too small */
+  BELLMAN_ESTATE = 6       /* call not valid in the handle's state / bad range */
+} bellman_status;
+
+enum { BELLMAN_LAW_OFF = 0, BELLMAN_LAW_CONST = 1, BELLMAN_LAW_MAP = 2, BELLMAN_LAW_STEP = 3 };
+enum { BELLMAN_SIG_TBT = 0, BELLMAN_SIG_E2E = 1, BELLMAN_SIG_SLO = 2 };
+enum { BELLMAN_MODE_CUTOFF = 0, BELLMAN_MODE_DRAIN = 1 };
+
+/* summary flags */
+#define BELLMAN_FLAG_TRUNCATED 0x1u        /* queued + in flight > 0 at the end */
+#define BELLMAN_FLAG_DEGENERATE_CALIB 0x2u /* calibration had < 4 samples or t1 == t2 */
+#define BELLMAN_FLAG_SERIES_OVERFLOW 0x4u  /* recorded signal series exceeded its capacity */
+#define BELLMAN_FLAG_DONE 0x100u           /* record written by a run */
+#define BELLMAN_NONE 0xFFFFFFFFu           /* "no value" in u32 percentile / second fields */
+
+#define BELLMAN_TABLE_N 4096    /* quantile-table entries, indexed by (u32 >> 20) */
+#define BELLMAN_HIST_LAT 896    /* latency bins: exact ms < 32, then 32 per octave */
+#define BELLMAN_HIST_R 512      /* r bins of 10 bp */
+#define BELLMAN_SEG_HIST_WORDS (2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R) /* u64 per segment */
+#define BELLMAN_MAX_BATCH 64
+
+/* One knot of a piecewise-linear arrival-rate trace ("distinct phases when
+ * the request arrivals ramp up, stay put, and ramp down"). */
+typedef struct {
+  int64_t t_us;      /* knot time, µs, non-decreasing within a trace */
+  uint32_t lam_mrps; /* rate at the knot, milli-requests/s, <= 2^20 */
+  uint32_t _pad;
+} bellman_knot;
+
+typedef struct {
+  uint32_t knot_offset; /* first knot in desc->knots */
+  uint32_t n_knots;     /* >= 2 */
+  uint32_t arrival_cap; /* stop after this many arrivals; 0 = none */
+  uint32_t _pad;
+} bellman_trace;
+
+/* Serving cost profile (decode law S:209-217; prefill S:218-226;
+ * energy S:227-235; optional KV term, reading R2). */
+typedef struct {
+  uint32_t t0_us;               /* base decode iteration time, >= 1 */
+  uint32_t knee;                /* batch size where slowdown begins, <= max_batch */
+  uint32_t slope_us;            /* added µs per decoding request beyond the knee */
+  uint32_t kv_ns_per_word;      /* ns per resident context word (0 = SPEC's law) */
+  uint32_t max_batch;           /* admission cap, 1..64 */
+  uint32_t prefill_ns_per_word; /* prefill time per input word, <= 2^24 */
+  double e_in_j_per_word, e_out_j_per_word, p_idle_w;
+} bellman_profile;
+
+/* Controller configuration (R3-R5, R22, R38). */
+typedef struct {
+  uint32_t law;        /* BELLMAN_LAW_* */
+  uint32_t signal;     /* BELLMAN_SIG_*: per-second avg TBT (default), avg E2E, SLO per-mille */
+  uint32_t window;     /* moving-average window in samples, 1..8 (5) */
+  uint32_t r_min_bp;   /* MAP: r at t1 (5%) */
+  uint32_t r_max_bp;   /* MAP: r at t2 (20%), <= 5000 */
+  uint32_t r_const_bp; /* CONST: fixed r */
+  uint32_t t1, t2;     /* thresholds in signal units (µs or per-mille), t1 < t2 unless calibrated */
+  uint32_t slo_us;     /* SLO signal: E2E threshold */
+  uint32_t calibrated; /* 1: t1/t2 = nearest-rank p50/p75 of the paired OFF run's series (a10) */
+  uint32_t n_rungs;    /* 0 = continuous; else <= 8 ascending rungs, rung[0] = r_min, last = r_max */
+  uint32_t rungs_bp[8];
+} bellman_ctrl;
+
+/* Workload model inputs (R14, R15, R33): 4096-entry quantile
+ * tables drawn with index (u32 >> 20), plus the compliance polynomial. */
+typedef struct {
+  const int32_t *L_words;  /* natural output words, 1..65535 */
+  const int32_t *I_words;  /* input words, 1..65535 */
+  const int32_t *fvar_q16; /* unbounded variability factor, Q16, 1..2^18 */
+  const int32_t *noise;    /* predictor error in words, |.| <= 65535 */
+  const int32_t *fcomp_q16;/* compliance factor, Q16, 0..2^18 */
+  int64_t poly_q16[3];     /* realized = poly(N) * fcomp; identity = {0, 65536, 0}; |a_k| <= 2^40 */
+} bellman_models;
+
+typedef struct {
+  uint32_t seed_index; /* Philox key = (seed_index, 0xB311A000) */
+  uint32_t trace;      /* index into traces */
+  uint64_t wid;        /* workload id: Philox counter words 2,3 (ON/OFF pairs share it) */
+  uint32_t profile, ctrl, segment, mode; /* mode: BELLMAN_MODE_* */
+  int64_t horizon_us;  /* cutoff H, or the cap of a drain run */
+  int64_t w0_us, w1_us;/* window [w0, w1) for the win_* counters (130-500 s) */
+  uint32_t calib_src;  /* OFF scenario whose series calibrates this one, or BELLMAN_NONE */
+  uint32_t record;     /* 1: keep this scenario's per-second signal series */
+} bellman_scenario; /* 64 bytes */
+
+typedef struct {
+  const bellman_knot *knots;
+  uint32_t n_knots;
+  const bellman_trace *traces;
+  uint32_t n_traces;
+  const bellman_profile *profiles;
+  uint32_t n_profiles;
+  const bellman_ctrl *ctrls;
+  uint32_t n_ctrls;
+  bellman_models models;
+  const bellman_scenario *scenarios;
+  uint64_t n_scenarios;
+  uint32_t n_segments; /* segment ids in [0, n_segments) */
+  uint32_t _pad;
+} bellman_sim_desc;
+
+/* 256-byte per-scenario summary (a8, a9, a6 logs).  All counts are exact
+ * integers; energy_j = (e_in*words_in + e_out*words_out) + p_idle*idle_us/1e6. */
+typedef struct {
+  uint64_t scenario_id, ticks, candidates, arrivals, admitted, served, rewritten;
+  uint64_t words_in, words_out, idle_us, end_us, queued_end, inflight_end;
+  uint64_t win_served, win_words_in, win_words_out, win_idle_us;
+  uint64_t sum_queue_us, sum_ttft_us, sum_e2e_us, slo_violations;
+  uint32_t e2e_p50_ms, e2e_p99_ms, ttft_p50_ms, ttft_p99_ms, median_r_bp;
+  uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
+  uint32_t segment, _pad0;
+  double energy_j, win_energy_j;
+  uint64_t _reserved[2];
+} bellman_scenario_stats;
+
+typedef struct bellman_sim bellman_sim; /* opaque */
+
+/* Bytes of device workspace the descriptor needs (0 if desc fails validation;
+ * see bellman_sim_last_error(NULL)). */
+size_t bellman_sim_workspace_bytes(const bellman_sim_desc *desc);
+
+/* Validate desc, lay out and fill the workspace (H2D copies on `stream`),
+ * bind to `device`.  *out receives the handle. */
+bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace, size_t workspace_bytes,
+                                  int device, void *stream, bellman_sim **out);
+
+/* Simulate scenarios first, first+stride, ..., first+(count-1)*stride
+ * (interleaved sharding across ranks: first = rank, stride = world size).
+ * Calibrated scenarios (a10) need their source in the same set.  Launches the
+ * pass-1 kernel, then (if any calibrated scenario is in the set) the
+ * calibration kernel and the pass-2 kernel.  Asynchronous. */
+bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count, uint64_t stride,
+                               void *stream);
+
+/* Copy `count` summary records of scenario ids [first, first+count) to dst
+ * (device or host memory).  Asynchronous for device dst; synchronous on
+ * `stream` for host dst. */
+bellman_status bellman_sim_stats(bellman_sim *sim, bellman_scenario_stats *dst, uint64_t first,
+                                 uint64_t count, int dst_is_device, void *stream);
+
+/* Copy the per-segment histograms, n_segments x BELLMAN_SEG_HIST_WORDS uint64:
+ * [E2E 896 | TTFT 896 | r 512] integer counts merged over the segment's runs. */
+bellman_status bellman_sim_segment_hist(bellman_sim *sim, uint64_t *dst, int dst_is_device, void *stream);
+
+/* Zero all summary records and segment histograms. */
+bellman_status bellman_sim_reset(bellman_sim *sim, void *stream);
+
+/* Kernel launches issued by the most recent bellman_sim_run. */
+uint32_t bellman_sim_last_launches(const bellman_sim *sim);
+
+void bellman_sim_destroy(bellman_sim *sim);
+const char *bellman_status_string(bellman_status s);
+const char *bellman_sim_last_error(const bellman_sim *sim);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BELLMAN_SIM_H */

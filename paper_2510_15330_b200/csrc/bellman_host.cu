@@ -1,0 +1,454 @@
+// bellman_host.cu — C ABI of the beLLMan simulator (include/bellman_sim.h):
+// validation, workspace layout, host-side precomputation, launches.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "bellman_internal.cuh"
+
+using namespace bellman;
+
+struct bellman_sim {
+  int device = 0;
+  uint64_t n_scenarios = 0;
+  uint32_t n_segments = 0, n_slots = 0;
+  bool has_calibrated = false;
+  int grid = 0;
+  uint32_t last_launches = 0;
+  Params params{};
+  unsigned int *counters = nullptr;  // [2]
+  std::vector<uint8_t> calibrated;   // per scenario: ctrl is calibrated
+  std::vector<uint32_t> calib_src;
+  char err[512] = {0};
+};
+
+static thread_local char g_err[512];
+
+static bellman_status fail(bellman_sim *sim, bellman_status st, const char *fmt, ...) {
+  char *dst = sim ? sim->err : g_err;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(dst, 512, fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+#define CUDA_TRY(sim, call)                                                                   \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(sim, BELLMAN_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                  \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// validation (S:185 max_batch >= 1, knee <= max_batch; S:269 0 < r_min <= r_max < 1,
+// t1 < t2, window >= 1; S:51 positive durations, non-negative rates)
+static bellman_status validate(const bellman_sim_desc *d) {
+  if (!d) return fail(nullptr, BELLMAN_EINVAL, "desc is NULL");
+  if (d->n_traces && (!d->traces || !d->knots)) return fail(nullptr, BELLMAN_EINVAL, "traces/knots NULL");
+  if (!d->n_profiles || !d->profiles) return fail(nullptr, BELLMAN_EINVAL, "no profiles");
+  if (!d->n_ctrls || !d->ctrls) return fail(nullptr, BELLMAN_EINVAL, "no controller configs");
+  if (d->n_scenarios && !d->scenarios) return fail(nullptr, BELLMAN_EINVAL, "scenarios NULL");
+  if (d->n_scenarios >= 0xFFFFFFFFull) return fail(nullptr, BELLMAN_EINVAL, "too many scenarios");
+  if (!d->n_segments) return fail(nullptr, BELLMAN_EINVAL, "n_segments must be >= 1");
+  const bellman_models &m = d->models;
+  if (!m.L_words || !m.I_words || !m.fvar_q16 || !m.noise || !m.fcomp_q16)
+    return fail(nullptr, BELLMAN_EINVAL, "model tables NULL");
+  for (int i = 0; i < BELLMAN_TABLE_N; ++i) {
+    if (m.L_words[i] < 1 || m.L_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "L table[%d] out of range", i);
+    if (m.I_words[i] < 1 || m.I_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "I table[%d] out of range", i);
+    if (m.fvar_q16[i] < 1 || m.fvar_q16[i] > (1 << 18)) return fail(nullptr, BELLMAN_EINVAL, "fvar[%d] out of range", i);
+    if (m.noise[i] < -65535 || m.noise[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "noise[%d] out of range", i);
+    if (m.fcomp_q16[i] < 0 || m.fcomp_q16[i] > (1 << 18)) return fail(nullptr, BELLMAN_EINVAL, "fcomp[%d] out of range", i);
+  }
+  for (int k = 0; k < 3; ++k)
+    if (m.poly_q16[k] > (1ll << 40) || m.poly_q16[k] < -(1ll << 40))
+      return fail(nullptr, BELLMAN_EINVAL, "poly_q16[%d] out of range", k);
+  for (uint32_t t = 0; t < d->n_traces; ++t) {
+    const bellman_trace &tr = d->traces[t];
+    if (tr.n_knots < 2 || (uint64_t)tr.knot_offset + tr.n_knots > d->n_knots)
+      return fail(nullptr, BELLMAN_EINVAL, "trace %u: bad knot range", t);
+    for (uint32_t k = 0; k < tr.n_knots; ++k) {
+      const bellman_knot &kn = d->knots[tr.knot_offset + k];
+      if (kn.t_us < 0 || kn.t_us > (1ll << 43)) return fail(nullptr, BELLMAN_EINVAL, "trace %u knot %u: time out of range", t, k);
+      if (kn.lam_mrps > (1u << 20)) return fail(nullptr, BELLMAN_EINVAL, "trace %u knot %u: rate > 2^20 mRPS", t, k);
+      if (k && kn.t_us < d->knots[tr.knot_offset + k - 1].t_us)
+        return fail(nullptr, BELLMAN_EINVAL, "trace %u: knot times decrease at %u", t, k);
+    }
+  }
+  for (uint32_t i = 0; i < d->n_profiles; ++i) {
+    const bellman_profile &p = d->profiles[i];
+    if (p.max_batch < 1 || p.max_batch > BELLMAN_MAX_BATCH) return fail(nullptr, BELLMAN_EINVAL, "profile %u: max_batch not in 1..64", i);
+    if (p.knee > p.max_batch) return fail(nullptr, BELLMAN_EINVAL, "profile %u: knee > max_batch", i);
+    if (p.t0_us < 1) return fail(nullptr, BELLMAN_EINVAL, "profile %u: t0_us must be >= 1", i);
+    if (p.prefill_ns_per_word > (1u << 24)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: prefill too large", i);
+    if (!(p.e_in_j_per_word >= 0) || !(p.e_out_j_per_word >= 0) || !(p.p_idle_w >= 0))
+      return fail(nullptr, BELLMAN_EINVAL, "profile %u: negative energy coefficient", i);
+  }
+  for (uint32_t i = 0; i < d->n_ctrls; ++i) {
+    const bellman_ctrl &c = d->ctrls[i];
+    if (c.law > BELLMAN_LAW_STEP) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown law", i);
+    if (c.signal > BELLMAN_SIG_SLO) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
+    if (c.window < 1 || c.window > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: window not in 1..8", i);
+    if (c.n_rungs > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: more than 8 rungs", i);
+    if (c.law == BELLMAN_LAW_CONST && c.r_const_bp > 5000) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: r_const > 5000 bp", i);
+    if (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP) {
+      if (c.r_min_bp < 1 || c.r_min_bp > c.r_max_bp || c.r_max_bp > 5000)
+        return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: need 0 < r_min <= r_max <= 5000 bp", i);
+      if (!c.calibrated && c.t1 >= c.t2) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: need t1 < t2", i);
+      if (c.law == BELLMAN_LAW_STEP && c.n_rungs == 0) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: STEP needs rungs", i);
+      if (c.n_rungs) {
+        for (uint32_t k = 1; k < c.n_rungs; ++k)
+          if (c.rungs_bp[k] <= c.rungs_bp[k - 1]) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs not ascending", i);
+        if (c.rungs_bp[0] != c.r_min_bp || c.rungs_bp[c.n_rungs - 1] != c.r_max_bp)
+          return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs must span [r_min, r_max]", i);
+      }
+    }
+  }
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+    const bellman_scenario &sc = d->scenarios[s];
+    if (sc.trace >= d->n_traces || sc.profile >= d->n_profiles || sc.ctrl >= d->n_ctrls)
+      return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: index out of range", (unsigned long long)s);
+    if (sc.segment >= d->n_segments) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: segment out of range", (unsigned long long)s);
+    if (sc.mode > BELLMAN_MODE_DRAIN) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: bad mode", (unsigned long long)s);
+    if (sc.horizon_us <= 0 || sc.horizon_us > (1ll << 43))
+      return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon out of range", (unsigned long long)s);
+    if (sc.w0_us > sc.w1_us) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: w0 > w1", (unsigned long long)s);
+    const bellman_ctrl &c = d->ctrls[sc.ctrl];
+    if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) {
+      if (sc.calib_src >= d->n_scenarios) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calib_src out of range", (unsigned long long)s);
+      const bellman_scenario &src = d->scenarios[sc.calib_src];
+      const bellman_ctrl &sctl = d->ctrls[src.ctrl];
+      if (sctl.calibrated || sctl.law != BELLMAN_LAW_OFF)
+        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calibration source must be an OFF run", (unsigned long long)s);
+      if (sctl.signal != c.signal)
+        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calibration source records another signal", (unsigned long long)s);
+    }
+  }
+  return BELLMAN_OK;
+}
+
+// ---------------------------------------------------------------------------
+struct Layout {
+  size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
+      off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct HostPrep {
+  std::vector<DevTrace> traces;
+  std::vector<DevSeg> segs;
+  std::vector<uint32_t> slot_of;   // per scenario
+  std::vector<uint64_t> slot_off;  // per slot
+  std::vector<uint32_t> slot_cap;
+  uint64_t series_words = 0;
+};
+
+static void prepare(const bellman_sim_desc *d, HostPrep &h) {
+  h.traces.resize(d->n_traces);
+  for (uint32_t t = 0; t < d->n_traces; ++t) {
+    const bellman_trace &tr = d->traces[t];
+    DevTrace dt{(uint32_t)h.segs.size(), 0, tr.arrival_cap, 0};
+    for (uint32_t k = 0; k + 1 < tr.n_knots; ++k) {
+      const bellman_knot &a = d->knots[tr.knot_offset + k], &b = d->knots[tr.knot_offset + k + 1];
+      const uint32_t lmax = a.lam_mrps > b.lam_mrps ? a.lam_mrps : b.lam_mrps;
+      if (lmax == 0 || b.t_us <= a.t_us) continue;  // a zero-rate or empty phase draws no candidate
+      DevSeg s{};
+      s.ta = (uint64_t)a.t_us;
+      s.tb = (uint64_t)b.t_us;
+      s.span = s.tb - s.ta;
+      s.M = (uint64_t)(((unsigned __int128)1000000000ull << 32) / lmax);  // mean gap 1e9/lmax µs, Q32
+      s.la = a.lam_mrps;
+      s.lb = b.lam_mrps;
+      s.lmax = lmax;
+      h.segs.push_back(s);
+      dt.n_seg++;
+    }
+    h.traces[t] = dt;
+  }
+  // series slots: every recorded scenario and every calibration source
+  h.slot_of.assign(d->n_scenarios, BELLMAN_NONE);
+  std::vector<uint8_t> need(d->n_scenarios, 0);
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+    const bellman_scenario &sc = d->scenarios[s];
+    if (sc.record) need[s] = 1;
+    const bellman_ctrl &c = d->ctrls[sc.ctrl];
+    if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) need[sc.calib_src] = 1;
+  }
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+    if (!need[s]) continue;
+    h.slot_of[s] = (uint32_t)h.slot_off.size();
+    const uint64_t cap = (uint64_t)d->scenarios[s].horizon_us / kUs + 2;
+    h.slot_off.push_back(h.series_words);
+    h.slot_cap.push_back((uint32_t)cap);
+    h.series_words += cap;
+  }
+}
+
+static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  const size_t ns = h.slot_off.size();
+  L.off_sc = take(sizeof(bellman_scenario) * d->n_scenarios);
+  L.off_tr = take(sizeof(DevTrace) * h.traces.size());
+  L.off_seg = take(sizeof(DevSeg) * h.segs.size());
+  L.off_prof = take(sizeof(bellman_profile) * d->n_profiles);
+  L.off_ctrl = take(sizeof(bellman_ctrl) * d->n_ctrls);
+  L.off_tab = take(sizeof(int32_t) * 5 * BELLMAN_TABLE_N);
+  L.off_log2 = take(sizeof(uint2) * BELLMAN_TABLE_N);
+  L.off_slot = take(sizeof(uint32_t) * d->n_scenarios);
+  L.off_soff = take(sizeof(uint64_t) * ns);
+  L.off_scap = take(sizeof(uint32_t) * ns);
+  L.off_sn = take(sizeof(uint32_t) * ns);
+  L.off_series = take(sizeof(uint32_t) * h.series_words);
+  L.off_calib = take(sizeof(uint32_t) * 4 * ns);
+  L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
+  L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
+  L.off_cnt = take(sizeof(unsigned int) * 4);
+  L.total = o;
+  return L;
+}
+
+// T[i] = round(2^32 * log2(1 + i/4096)) (reading R33), product-side evaluation.
+static void log2_table(std::vector<uint2> &out) {
+  out.resize(BELLMAN_TABLE_N);
+  uint64_t prev = 0;
+  for (int i = 0; i <= BELLMAN_TABLE_N; ++i) {
+    const long double v = std::log2((long double)1.0 + (long double)i / 4096.0L) * 4294967296.0L;
+    const uint64_t t = (uint64_t)std::floor(v + 0.5L);
+    if (i > 0) out[i - 1] = make_uint2((uint32_t)prev, (uint32_t)(t - prev));
+    prev = t;
+  }
+}
+
+extern "C" {
+
+size_t bellman_sim_workspace_bytes(const bellman_sim_desc *desc) {
+  if (validate(desc) != BELLMAN_OK) return 0;
+  HostPrep h;
+  prepare(desc, h);
+  return layout(desc, h).total;
+}
+
+bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace, size_t workspace_bytes, int device,
+                                  void *stream, bellman_sim **out) {
+  if (!out) return fail(nullptr, BELLMAN_EINVAL, "out is NULL");
+  *out = nullptr;
+  bellman_status st = validate(desc);
+  if (st != BELLMAN_OK) return st;
+  HostPrep h;
+  prepare(desc, h);
+  const Layout L = layout(desc, h);
+  if (!workspace || ((uintptr_t)workspace & 255u))
+    return fail(nullptr, BELLMAN_EWORKSPACE, "workspace NULL or not 256-byte aligned");
+  if (workspace_bytes < L.total)
+    return fail(nullptr, BELLMAN_EWORKSPACE, "workspace too small: %zu < %zu", workspace_bytes, L.total);
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) return fail(nullptr, BELLMAN_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
+  cudaPointerAttributes pa{};
+  ce = cudaPointerGetAttributes(&pa, workspace);
+  if (ce != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return fail(nullptr, BELLMAN_EWORKSPACE, "workspace is not device memory");
+  }
+  bellman_sim *sim = new (std::nothrow) bellman_sim();
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "out of host memory");
+  sim->device = device;
+  sim->n_scenarios = desc->n_scenarios;
+  sim->n_segments = desc->n_segments;
+  sim->n_slots = (uint32_t)h.slot_off.size();
+  sim->grid = bellman_tick_grid(device);
+  if (sim->grid <= 0) {
+    delete sim;
+    return fail(nullptr, BELLMAN_ECUDA, "occupancy query failed");
+  }
+  sim->calibrated.assign(desc->n_scenarios, 0);
+  sim->calib_src.assign(desc->n_scenarios, BELLMAN_NONE);
+  for (uint64_t s = 0; s < desc->n_scenarios; ++s) {
+    const bellman_ctrl &c = desc->ctrls[desc->scenarios[s].ctrl];
+    if (c.calibrated) {
+      sim->calibrated[s] = 1;
+      sim->has_calibrated = true;
+      sim->calib_src[s] = desc->scenarios[s].calib_src;
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t *ws = (uint8_t *)workspace;
+  Params &P = sim->params;
+  P.sc = (const bellman_scenario *)(ws + L.off_sc);
+  P.traces = (const DevTrace *)(ws + L.off_tr);
+  P.segs = (const DevSeg *)(ws + L.off_seg);
+  P.profs = (const bellman_profile *)(ws + L.off_prof);
+  P.ctrls = (const bellman_ctrl *)(ws + L.off_ctrl);
+  int32_t *tab = (int32_t *)(ws + L.off_tab);
+  P.tabL = tab;
+  P.tabI = tab + BELLMAN_TABLE_N;
+  P.tabF = tab + 2 * BELLMAN_TABLE_N;
+  P.tabN = tab + 3 * BELLMAN_TABLE_N;
+  P.tabC = tab + 4 * BELLMAN_TABLE_N;
+  P.log2tab = (const uint2 *)(ws + L.off_log2);
+  P.poly0 = desc->models.poly_q16[0];
+  P.poly1 = desc->models.poly_q16[1];
+  P.poly2 = desc->models.poly_q16[2];
+  P.series_slot = (const uint32_t *)(ws + L.off_slot);
+  P.series_off = (const uint64_t *)(ws + L.off_soff);
+  P.series_cap = (const uint32_t *)(ws + L.off_scap);
+  P.series_n = (uint32_t *)(ws + L.off_sn);
+  P.series = (uint32_t *)(ws + L.off_series);
+  P.calib = (uint32_t *)(ws + L.off_calib);
+  P.stats = (bellman_scenario_stats *)(ws + L.off_stats);
+  P.seg_hist = (unsigned long long *)(ws + L.off_hist);
+  sim->counters = (unsigned int *)(ws + L.off_cnt);
+
+  std::vector<uint2> l2;
+  log2_table(l2);
+#define H2D(dst, src, bytes) \
+  if (bytes) CUDA_TRY(nullptr, cudaMemcpyAsync((void *)(dst), (const void *)(src), (bytes), cudaMemcpyHostToDevice, s))
+  {
+    bellman_status rc = BELLMAN_OK;
+    auto body = [&]() -> bellman_status {
+      H2D(P.sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios);
+      H2D(P.traces, h.traces.data(), sizeof(DevTrace) * h.traces.size());
+      H2D(P.segs, h.segs.data(), sizeof(DevSeg) * h.segs.size());
+      H2D(P.profs, desc->profiles, sizeof(bellman_profile) * desc->n_profiles);
+      H2D(P.ctrls, desc->ctrls, sizeof(bellman_ctrl) * desc->n_ctrls);
+      H2D(P.tabL, desc->models.L_words, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.tabI, desc->models.I_words, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.tabF, desc->models.fvar_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.tabN, desc->models.noise, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.tabC, desc->models.fcomp_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.log2tab, l2.data(), sizeof(uint2) * BELLMAN_TABLE_N);
+      H2D(P.series_slot, h.slot_of.data(), sizeof(uint32_t) * desc->n_scenarios);
+      H2D(P.series_off, h.slot_off.data(), sizeof(uint64_t) * h.slot_off.size());
+      H2D(P.series_cap, h.slot_cap.data(), sizeof(uint32_t) * h.slot_cap.size());
+      if (h.slot_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.series_n, 0, sizeof(uint32_t) * h.slot_off.size(), s));
+      CUDA_TRY(nullptr, cudaMemsetAsync(P.stats, 0, sizeof(bellman_scenario_stats) * desc->n_scenarios, s));
+      CUDA_TRY(nullptr, cudaMemsetAsync(P.seg_hist, 0, sizeof(uint64_t) * kSegWords * desc->n_segments, s));
+      CUDA_TRY(nullptr, cudaStreamSynchronize(s));
+      return BELLMAN_OK;
+    };
+    rc = body();
+    if (rc != BELLMAN_OK) {
+      delete sim;
+      return rc;
+    }
+  }
+#undef H2D
+  *out = sim;
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count, uint64_t stride, void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (count == 0) {
+    sim->last_launches = 0;
+    return BELLMAN_OK;
+  }
+  if (stride == 0) return fail(sim, BELLMAN_ESTATE, "stride must be >= 1");
+  if (first >= sim->n_scenarios || (count - 1) > (sim->n_scenarios - 1 - first) / stride)
+    return fail(sim, BELLMAN_ESTATE, "scenario range out of bounds");
+  if (count > 0xFFFFFFFFull) return fail(sim, BELLMAN_ESTATE, "count too large");
+  bool any_cal = false;
+  if (sim->has_calibrated) {
+    for (uint64_t k = 0; k < count; ++k) {
+      const uint64_t id = first + k * stride;
+      if (!sim->calibrated[id]) continue;
+      any_cal = true;
+      const uint64_t src = sim->calib_src[id];
+      if (src < first || (src - first) % stride || (src - first) / stride >= count)
+        return fail(sim, BELLMAN_ESTATE, "scenario %llu: calibration source %llu not in the run set",
+                    (unsigned long long)id, (unsigned long long)src);
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  Params P = sim->params;
+  P.first = first;
+  P.count = count;
+  P.stride = stride;
+  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 2 * sizeof(unsigned int), s));
+  const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
+  P.counter = sim->counters;
+  P.pass = 1;
+  sim->last_launches = 0;
+  CUDA_TRY(sim, bellman_launch_tick(P, grid, s));
+  sim->last_launches++;
+  if (any_cal) {
+    CUDA_TRY(sim, bellman_launch_calibrate(P, sim->n_slots, s));
+    sim->last_launches++;
+    P.counter = sim->counters + 1;
+    P.pass = 2;
+    CUDA_TRY(sim, bellman_launch_tick(P, grid, s));
+    sim->last_launches++;
+  }
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_stats(bellman_sim *sim, bellman_scenario_stats *dst, uint64_t first, uint64_t count,
+                                 int dst_is_device, void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (!dst) return fail(sim, BELLMAN_EINVAL, "dst is NULL");
+  if (first > sim->n_scenarios || count > sim->n_scenarios - first)
+    return fail(sim, BELLMAN_ESTATE, "stats range out of bounds");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  CUDA_TRY(sim, cudaMemcpyAsync(dst, sim->params.stats + first, sizeof(bellman_scenario_stats) * count,
+                                dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (!dst_is_device) CUDA_TRY(sim, cudaStreamSynchronize(s));
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_segment_hist(bellman_sim *sim, uint64_t *dst, int dst_is_device, void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (!dst) return fail(sim, BELLMAN_EINVAL, "dst is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  CUDA_TRY(sim, cudaMemcpyAsync(dst, sim->params.seg_hist, sizeof(uint64_t) * kSegWords * sim->n_segments,
+                                dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (!dst_is_device) CUDA_TRY(sim, cudaStreamSynchronize(s));
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_reset(bellman_sim *sim, void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->params.stats, 0, sizeof(bellman_scenario_stats) * sim->n_scenarios, s));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->params.seg_hist, 0, sizeof(uint64_t) * kSegWords * sim->n_segments, s));
+  if (sim->n_slots) CUDA_TRY(sim, cudaMemsetAsync(sim->params.series_n, 0, sizeof(uint32_t) * sim->n_slots, s));
+  return BELLMAN_OK;
+}
+
+uint32_t bellman_sim_last_launches(const bellman_sim *sim) { return sim ? sim->last_launches : 0; }
+
+void bellman_sim_destroy(bellman_sim *sim) { delete sim; }
+
+const char *bellman_status_string(bellman_status s) {
+  switch (s) {
+    case BELLMAN_OK: return "ok";
+    case BELLMAN_EINVAL: return "invalid descriptor";
+    case BELLMAN_EIO: return "io error";
+    case BELLMAN_EDEGENERATE: return "degenerate data";
+    case BELLMAN_ECUDA: return "cuda error";
+    case BELLMAN_EWORKSPACE: return "workspace error";
+    case BELLMAN_ESTATE: return "invalid state or range";
+  }
+  return "unknown status";
+}
+
+const char *bellman_sim_last_error(const bellman_sim *sim) { return sim ? sim->err : g_err; }
+
+}  // extern "C"

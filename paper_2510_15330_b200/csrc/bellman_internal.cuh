@@ -1,0 +1,62 @@
+// Product-internal device layout of the beLLMan simulator (not part of the ABI).
+// DESIGN.md section 4 documents the HBM layout; section 2 names steps a1..a10.
+#pragma once
+#include <cstdint>
+
+#include "../../include/bellman_sim.h"
+
+namespace bellman {
+
+constexpr uint32_t kSeedHi = 0xB311A000u;  // Philox key word 1 (reading R32)
+constexpr uint64_t kUs = 1000000ull;
+constexpr uint32_t kWarpsPerBlock = 4;
+constexpr uint32_t kSegWords = BELLMAN_SEG_HIST_WORDS;
+
+// One non-empty thinning segment of a trace, precomputed on the host (a2):
+// [ta, tb) with endpoint rates la, lb, lmax = max(la, lb) > 0 and the
+// exponential scale M = floor(2^32 * 1e9 / lmax) (µs per unit rate, Q32).
+struct DevSeg {
+  uint64_t ta, tb, span, M;
+  uint32_t la, lb, lmax, _pad;
+};
+static_assert(sizeof(DevSeg) == 48, "DevSeg layout");
+
+struct DevTrace {
+  uint32_t seg_off, n_seg, cap, _pad;
+};
+
+// Per-warp shared-memory histograms (a9): 9216 bytes.
+struct WarpHist {
+  uint32_t e2e[BELLMAN_HIST_LAT];
+  uint32_t ttft[BELLMAN_HIST_LAT];
+  uint32_t r[BELLMAN_HIST_R];
+};
+
+struct Params {
+  const bellman_scenario *sc;
+  const DevTrace *traces;
+  const DevSeg *segs;
+  const bellman_profile *profs;
+  const bellman_ctrl *ctrls;
+  const int32_t *tabL, *tabI, *tabF, *tabN, *tabC;  // 4096 each
+  const uint2 *log2tab;                             // (T[i], T[i+1]-T[i]), i < 4096
+  int64_t poly0, poly1, poly2;
+  const uint32_t *series_slot;  // [n_scenarios] slot or NONE
+  const uint64_t *series_off;   // [n_slots] word offset into series
+  const uint32_t *series_cap;   // [n_slots]
+  uint32_t *series_n;           // [n_slots] samples written
+  uint32_t *series;             // sample storage
+  uint32_t *calib;              // [n_slots][4]: t1, t2, status, n
+  bellman_scenario_stats *stats;
+  unsigned long long *seg_hist;  // [n_segments][kSegWords]
+  unsigned int *counter;         // work counter of this pass
+  uint64_t first, count, stride;
+  uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
+};
+
+}  // namespace bellman
+
+// launchers (bellman_kernels.cu)
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, cudaStream_t stream);
+cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream);
+int bellman_tick_grid(int device);

@@ -1,0 +1,837 @@
+// bellman_kernels.cu — sm_100a kernels of the beLLMan scenario simulator.
+//
+// K2 bellman_tick_kernel: persistent; one warp simulates one scenario (a1-a9)
+//    and fetches the next scenario id from a global counter when done.
+// K5 bellman_calibrate_kernel: nearest-rank p50/p75 of recorded series (a10).
+//
+// Warp organisation:
+//  * warp-uniform scalar state in registers: simulated clock, iteration,
+//    batch size B and context K, controller, per-second accumulator, counters;
+//  * lane-parallel request slots: slot s of lane l is batch slot l + 32 s
+//    (max_batch <= 64 -> 2 slots per lane); admission ranks free slots with
+//    ballot/popc, completions and prefill ends are ballot masks;
+//  * lane-parallel arrival generator: 32 Philox candidates per refill, a warp
+//    prefix sum of the exponential gaps, thinning by ballot, compaction by
+//    __fns into a 32-entry register buffer that is the head of the FIFO queue;
+//  * shared-memory latency histograms per warp, reduced to nearest-rank
+//    percentiles by a warp scan and merged into segment histograms with
+//    integer atomics (order-independent, hence bit-exact).
+// No floating point except the final fp64 energy (IEEE _rn intrinsics, no FMA).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bellman_internal.cuh"
+
+namespace bellman {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t INF = ~0ull;
+constexpr uint32_t PH_EMPTY = 0, PH_PREFILL = 1, PH_READY = 2, PH_DEC = 3, PH_OFF = 4;
+constexpr uint64_t kLn2Q32 = 2977044472ull;  // round(ln 2 * 2^32)
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11) — counter (c0..c3), key (k0, k1).
+__device__ __forceinline__ uint4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                        uint32_t c3) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// -ln(U), U = (2u+1)/2^33, in Q32 (reading R33): log2 by table + interpolation.
+__device__ __forceinline__ uint64_t neglog_q32(uint32_t u, const uint2 *__restrict__ tab) {
+  uint32_t e, x;
+  if (u >= 0x80000000u) {  // v = 2u+1 >= 2^32: leading one at bit 32
+    e = 32;
+    x = 2u * u + 1u;  // v - 2^32 (mod 2^32)
+  } else {
+    const uint32_t v = 2u * u + 1u;
+    e = 31u - __clz(v);
+    x = (uint32_t)(((uint64_t)(v - (1u << e))) << (32u - e));
+  }
+  const uint2 t = __ldg(&tab[x >> 20]);
+  const uint64_t f = x & 0xFFFFFu;
+  const uint64_t log2v = ((uint64_t)e << 32) + t.x + (((uint64_t)t.y * f) >> 20);
+  const uint64_t neg = (33ull << 32) - log2v;
+  const uint64_t lo = neg * kLn2Q32, hi = __umul64hi(neg, kLn2Q32);
+  return (hi << 32) | (lo >> 32);
+}
+
+// latency bin of a value in ms (a9): exact below 32, then 32 per octave.
+__device__ __forceinline__ uint32_t lat_bin(uint64_t ms) {
+  if (ms < 32) return (uint32_t)ms;
+  const uint32_t e = 63u - (uint32_t)__clzll((long long)ms);
+  if (e > 31) return BELLMAN_HIST_LAT - 1;
+  return 32u * (e - 4u) + ((uint32_t)(ms >> (e - 5u)) & 31u);
+}
+__device__ __forceinline__ uint32_t lat_edge(uint32_t b) {
+  if (b < 32) return b;
+  const uint32_t e = b / 32u + 4u, s = b % 32u;
+  return (32u + s) << (e - 5u);
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+  return x;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// ---------------------------------------------------------------------------
+// The per-scenario simulation.  Every scalar is warp-uniform.
+struct Sim {
+  // ---- scenario (a1)
+  uint32_t sid, k0;  // Philox key word 0 = seed_index
+  uint32_t wid_lo, wid_hi;
+  uint64_t H;
+  uint32_t mode;
+  uint64_t w0, w1;
+  // profile
+  uint32_t t0, knee, slope, kv, maxb, pf_ns;
+  // controller
+  uint32_t law, signal, window, rmin, rmax, t1, t2, slo_us, nrungs;
+  uint32_t rungs_lane;  // lane l < nrungs holds rung l
+  uint32_t r, active, rung;
+  uint32_t ring;        // lane l < window holds a ring sample
+  uint32_t ring_n, ring_pos;
+  uint64_t ringA;
+  uint32_t activations, first_act, last_deact, active_ingests;
+  // per-second accumulator of the selected signal (a6)
+  uint64_t sec_bound;  // (open second + 1) * 1e6
+  uint64_t acc_sum;
+  uint32_t acc_cnt;
+  // recording (a10 source)
+  uint32_t *series;
+  uint32_t series_cap, series_n;
+  uint32_t flags;
+  // ---- serving state (a4, a5, a7)
+  uint64_t T;
+  uint32_t busy;
+  uint64_t iter_end;
+  uint32_t iter_B;
+  uint64_t iter_d, iter_align;
+  uint32_t ticks;      // iterations started; the running one has index ticks-1
+  uint32_t next_done;  // min completion iteration over decoding slots
+  uint64_t next_pf;    // min prefill end over prefilling slots
+  uint32_t n_ready, B, in_sys;
+  uint64_t K;
+  // slots (lane-parallel)
+  uint64_t sa[2], sp[2];
+  uint32_t sR[2], sin[2], sdn[2], sph[2];
+  // ---- generator / queue head (a2)
+  const DevSeg *segs;
+  uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
+  uint64_t gen_tau;
+  uint32_t buf_h, buf_n;
+  uint64_t buf_a;      // lane-parallel buffer of upcoming arrivals
+  uint32_t buf_attr;   // L | input << 16
+  uint32_t buf_j;
+  uint32_t last_j;     // candidate index of the last counted arrival + 1
+  // ---- counters (a8)
+  uint32_t admitted, served, rewritten, slo_viol, win_served;
+  uint64_t words_in, words_out, idle, win_words_in, win_words_out, win_idle;
+  uint64_t sum_queue, sum_ttft, sum_e2e;
+
+  __device__ __forceinline__ bool in_win(uint64_t t) const { return t >= w0 && t < w1; }
+
+  // ------------------------------------------------------------------ a2
+  // Refill the 32-entry arrival buffer with the next accepted candidates.
+  __device__ __forceinline__ void refill(const Params &p) {
+    const uint32_t lane = lane_id();
+    buf_h = 0;
+    buf_n = 0;
+    while (!gen_done && buf_n == 0) {
+      if (gen_seg >= n_seg) {
+        gen_done = 1;
+        break;
+      }
+      const DevSeg S = segs[gen_seg];
+      if (gen_fresh) {
+        gen_tau = S.ta;
+        gen_fresh = 0;
+      }
+      const uint32_t jj = gen_j + lane;
+      const uint4 u = philox(k0, kSeedHi, jj, 0u, wid_lo, wid_hi);
+      const uint64_t delta = __umul64hi(neglog_q32(u.x, p.log2tab), S.M);
+      uint64_t incl = delta;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      const uint64_t tau = gen_tau + incl;
+      const uint32_t om = __ballot_sync(FULL, tau >= S.tb);
+      const uint32_t first_over = om ? (uint32_t)(__ffs(om) - 1) : 32u;
+      bool acc = false;
+      if (lane < first_over) {
+        // thinning: u1 * lmax * span < (la (tb - tau) + lb (tau - ta)) * 2^32, in 128 bits
+        const uint64_t x = (uint64_t)u.y * S.lmax;
+        const uint64_t lhs_hi = __umul64hi(x, S.span), lhs_lo = x * S.span;
+        const uint64_t y = (uint64_t)S.la * (S.tb - tau) + (uint64_t)S.lb * (tau - S.ta);
+        const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
+        acc = lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
+      }
+      uint32_t am = __ballot_sync(FULL, acc);
+      if (gen_cap) {
+        const uint32_t room = gen_cap - gen_acc;
+        if ((uint32_t)__popc(am) >= room) {
+          const uint32_t cut = room ? __fns(am, 0, (int)room) : 0u;  // position of room-th set bit
+          am = room ? (am & (0xffffffffu >> (31u - cut))) : 0u;
+          gen_done = 1;
+        }
+      }
+      const uint32_t cnt = (uint32_t)__popc(am);
+      const uint32_t attr = (uint32_t)__ldg(&p.tabL[u.z >> 20]) | ((uint32_t)__ldg(&p.tabI[u.w >> 20]) << 16);
+      const uint32_t src = __fns(am, 0, (int)lane + 1);
+      const uint32_t s = src < 32u ? src : 0u;
+      buf_a = __shfl_sync(FULL, tau, s);
+      buf_attr = __shfl_sync(FULL, attr, s);
+      buf_j = __shfl_sync(FULL, jj, s);
+      buf_n = cnt;
+      gen_acc += cnt;
+      if (first_over < 32u) {
+        gen_j += first_over + 1u;  // the crossing candidate is consumed (R17)
+        gen_seg++;
+        gen_fresh = 1;
+      } else {
+        gen_j += 32u;
+        gen_tau = __shfl_sync(FULL, tau, 31);
+      }
+    }
+  }
+
+  __device__ __forceinline__ uint64_t head_a() const {
+    return __shfl_sync(FULL, buf_a, buf_h & 31u);
+  }
+
+  // ------------------------------------------------------------------ a6
+  __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
+    if (series) {
+      if (series_n < series_cap) {
+        if (lane_id() == 0) series[series_n] = x;
+      } else {
+        flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+      }
+      series_n++;
+    }
+    if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return;
+    const uint32_t lane = lane_id();
+    const uint32_t ev = __shfl_sync(FULL, ring, ring_pos);
+    if (lane == ring_pos) ring = x;
+    if (ring_n < window) {
+      ring_n++;
+      ringA += x;
+    } else {
+      ringA = ringA + x - ev;
+    }
+    ring_pos = (ring_pos + 1u == window) ? 0u : ring_pos + 1u;
+    const uint32_t k = ring_n;
+    const bool act = ringA >= (uint64_t)k * t1;  // non-strict (R38)
+    uint32_t nr = 0;
+    if (act) {
+      if (law == BELLMAN_LAW_MAP) {
+        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (ringA - (uint64_t)k * t1)) / ((uint64_t)k * (t2 - t1));
+        if (rr > rmax) rr = rmax;
+        nr = (uint32_t)rr;
+        if (nrungs) {  // largest rung <= r (R5)
+          const uint32_t le = __ballot_sync(FULL, lane < nrungs && rungs_lane <= nr);
+          nr = __shfl_sync(FULL, rungs_lane, 31 - __clz(le | 1u));
+        }
+      } else {  // STEP
+        rung = active ? (rung + 1u < nrungs ? rung + 1u : rung) : 0u;
+        nr = __shfl_sync(FULL, rungs_lane, rung);
+      }
+    }
+    if (act && !active) {
+      activations++;
+      if (first_act == BELLMAN_NONE) first_act = second;
+    }
+    if (!act && active) last_deact = second;
+    if (act) active_ingests++;
+    active = act;
+    r = nr;
+  }
+
+  // close the open second (if it holds samples) and open the one containing t
+  __device__ __forceinline__ void roll_second(uint64_t t) {
+    if (t < sec_bound) return;
+    if (acc_cnt) ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
+    acc_sum = 0;
+    acc_cnt = 0;
+    sec_bound = (t / kUs + 1u) * kUs;
+  }
+
+  // ------------------------------------------------------------------ a5
+  __device__ __forceinline__ void complete_sig(uint64_t sum_e2e_w, uint32_t n, uint32_t nslo) {
+    if (signal == BELLMAN_SIG_TBT) return;
+    if (signal == BELLMAN_SIG_E2E) {
+      acc_sum += sum_e2e_w;
+      acc_cnt += n;
+    } else {
+      acc_sum += 1000ull * nslo;
+      acc_cnt += n;
+    }
+  }
+
+  __device__ __forceinline__ void iteration_end(WarpHist &h) {
+    const uint64_t Tn = T;
+    words_out += iter_B;
+    if (in_win(Tn)) win_words_out += iter_B;
+    if (signal == BELLMAN_SIG_TBT) {
+      acc_sum += (uint64_t)iter_B * iter_d + iter_align;
+      acc_cnt += iter_B;
+    }
+    K += iter_B;
+    const uint32_t it = ticks - 1u;
+    if (it == next_done) {
+      uint64_t e2e_l = 0, kdrop = 0;
+      uint32_t nslo = 0, ndone = 0, dmin = 0xffffffffu;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const bool c = sph[s] == PH_DEC && sdn[s] == it;
+        ndone += __popc(__ballot_sync(FULL, c));
+        if (c) {
+          const uint64_t e = Tn - sa[s];
+          e2e_l += e;
+          nslo += e > slo_us;
+          kdrop += (uint64_t)sin[s] + sR[s];
+          atomicAdd(&h.e2e[lat_bin(e / 1000u)], 1u);
+          sph[s] = PH_EMPTY;
+        }
+        if (sph[s] == PH_DEC) dmin = min(dmin, sdn[s]);
+      }
+      next_done = __reduce_min_sync(FULL, dmin);
+      const uint64_t se = warp_sum_u64(e2e_l);
+      const uint32_t ns = __reduce_add_sync(FULL, nslo);
+      K -= warp_sum_u64(kdrop);
+      served += ndone;
+      sum_e2e += se;
+      slo_viol += ns;
+      if (in_win(Tn)) win_served += ndone;
+      in_sys -= ndone;
+      B -= ndone;
+      complete_sig(se, ndone, ns);
+    }
+    busy = 0;
+  }
+
+  __device__ __forceinline__ void prefill_end(WarpHist &h) {
+    const uint64_t Tn = T;
+    uint64_t ttft_l = 0, e2e_l = 0;
+    uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0;
+    uint32_t mpf = 0xffffffffu;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const bool f = sph[s] == PH_PREFILL && sp[s] == Tn;
+      nfirst += __popc(__ballot_sync(FULL, f));
+      if (f) {
+        const uint64_t tt = Tn - sa[s];
+        ttft_l += tt;
+        atomicAdd(&h.ttft[lat_bin(tt / 1000u)], 1u);
+        if (sR[s] == 1u) {  // R9: completes at the prefill end
+          e2e_l += tt;
+          nslo += tt > slo_us;
+          n1++;
+          atomicAdd(&h.e2e[lat_bin(tt / 1000u)], 1u);
+          sph[s] = PH_EMPTY;
+        } else {
+          sph[s] = PH_READY;
+          nrdy++;
+        }
+      }
+      if (sph[s] == PH_PREFILL) {
+        const uint64_t off = sp[s] - Tn;
+        mpf = min(mpf, (uint32_t)off);
+      }
+    }
+    const uint32_t m = __reduce_min_sync(FULL, mpf);
+    next_pf = (m == 0xffffffffu) ? INF : Tn + m;
+    sum_ttft += warp_sum_u64(ttft_l);
+    words_out += nfirst;
+    if (in_win(Tn)) win_words_out += nfirst;
+    n_ready += __reduce_add_sync(FULL, nrdy);
+    const uint32_t nc = __reduce_add_sync(FULL, n1);
+    if (nc) {
+      const uint64_t se = warp_sum_u64(e2e_l);
+      const uint32_t ns = __reduce_add_sync(FULL, nslo);
+      served += nc;
+      sum_e2e += se;
+      slo_viol += ns;
+      if (in_win(Tn)) win_served += nc;
+      in_sys -= nc;
+      complete_sig(se, nc, ns);
+    }
+  }
+
+  // ------------------------------------------------------------------ a7 (+a3)
+  __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
+    const uint32_t lane = lane_id();
+    const uint64_t Tn = T;
+    while (in_sys < maxb) {
+      if (buf_h >= buf_n) {
+        if (gen_done) break;
+        refill(p);
+        continue;
+      }
+      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && buf_a <= Tn);
+      const uint32_t na = __popc(arrived);
+      if (na == 0) break;
+      const uint32_t room = maxb - in_sys;
+      const uint32_t k = na < room ? na : room;
+      const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY);
+      const uint32_t f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
+      const uint32_t lt = (1u << lane) - 1u;
+      const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
+      uint64_t win_l = 0, q_l = 0;
+      uint32_t mpf = 0xffffffffu;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const uint32_t rank = s == 0 ? rank0 : rank1;
+        const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
+        const uint32_t src = (buf_h + (mine ? rank : 0u)) & 31u;
+        const uint64_t a = __shfl_sync(FULL, buf_a, src);
+        const uint32_t attr = __shfl_sync(FULL, buf_attr, src);
+        const uint32_t j = __shfl_sync(FULL, buf_j, src);
+        if (mine) {
+          const uint32_t L = attr & 0xFFFFu, in = attr >> 16;
+          const uint4 v = philox(k0, kSeedHi, j, 1u, wid_lo, wid_hi);  // a3 draws (tag 1)
+          const uint32_t fvar = (uint32_t)__ldg(&p.tabF[v.x >> 20]);
+          const int32_t noise = __ldg(&p.tabN[v.y >> 20]);
+          uint32_t R;
+          if (r > 0) {
+            const int64_t P0 = (int64_t)L + noise;
+            const uint64_t P = P0 < 1 ? 1u : (uint64_t)P0;
+            int64_t N = (int64_t)((P * (10000u - r) + 5000u) / 10000u);
+            if (N < 1) N = 1;
+            const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
+            const int32_t fc = __ldg(&p.tabC[v.z >> 20]);
+            __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
+            if (x < 1) x = 1;
+            if (x > (1 << 24)) x = 1 << 24;
+            R = (uint32_t)x;
+          } else {
+            const uint64_t U = ((uint64_t)L * fvar + 32768u) >> 16;
+            R = U < 1 ? 1u : (uint32_t)U;
+          }
+          uint64_t pf = ((uint64_t)pf_ns * in) / 1000u;
+          if (pf < 1) pf = 1;
+          sa[s] = a;
+          sp[s] = Tn + pf;
+          sR[s] = R;
+          sin[s] = in;
+          sph[s] = PH_PREFILL;
+          win_l += in;
+          q_l += Tn - a;
+          mpf = min(mpf, (uint32_t)pf);
+        }
+      }
+      const uint32_t mnew = __reduce_min_sync(FULL, mpf);
+      if (Tn + mnew < next_pf) next_pf = Tn + mnew;
+      const uint64_t win = warp_sum_u64(win_l);
+      words_in += win;
+      if (in_win(Tn)) win_words_in += win;
+      sum_queue += warp_sum_u64(q_l);
+      if (r > 0) {
+        rewritten += k;
+        if (lane == 0) atomicAdd(&h.r[r / 10u < BELLMAN_HIST_R ? r / 10u : BELLMAN_HIST_R - 1], k);
+      }
+      last_j = __shfl_sync(FULL, buf_j, (buf_h + k - 1u) & 31u) + 1u;
+      in_sys += k;
+      admitted += k;
+      buf_h += k;
+      if (k < na) break;  // slots full
+    }
+  }
+
+  // ------------------------------------------------------------------ a4
+  __device__ __forceinline__ void start_iteration() {
+    const uint64_t Tn = T;
+    const uint32_t c = ticks;  // index of the new iteration
+    uint32_t jn = 0xffffffffu;
+    uint64_t kadd = 0, al = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (sph[s] == PH_READY) {
+        sph[s] = PH_DEC;
+        sdn[s] = c + sR[s] - 2u;  // words 2..R at the ends of iterations c..c+R-2
+        al += Tn - sp[s];
+        kadd += (uint64_t)sin[s] + 1u;
+        jn = min(jn, sdn[s]);
+      }
+    }
+    const uint64_t align = warp_sum_u64(al);
+    const uint32_t mj = __reduce_min_sync(FULL, jn);
+    if (mj < next_done) next_done = mj;
+    K += warp_sum_u64(kadd);
+    B += n_ready;
+    n_ready = 0;
+    const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (B > knee ? B - knee : 0u) + ((uint64_t)kv * K) / 1000u;
+    iter_d = d;
+    iter_B = B;
+    iter_align = align;
+    iter_end = Tn + d;
+    busy = 1;
+    ticks++;
+  }
+};
+
+// ---------------------------------------------------------------------------
+__device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, const uint32_t *ps, uint32_t np,
+                                 uint32_t *out, bool lat) {
+  const uint32_t lane = lane_id();
+  const uint32_t chunk = nb / 32u;
+  uint32_t csum = 0;
+  for (uint32_t b = 0; b < chunk; ++b) csum += hist[lane * chunk + b];
+  uint32_t incl = csum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  for (uint32_t q = 0; q < np; ++q) {
+    if (n == 0) {
+      out[q] = BELLMAN_NONE;
+      continue;
+    }
+    uint64_t k = ((uint64_t)ps[q] * n + 99u) / 100u;
+    if (k < 1) k = 1;
+    const uint32_t m = __ballot_sync(FULL, incl >= k);
+    const uint32_t L = __ffs(m) - 1;
+    uint32_t res = 0;
+    if (lane == L) {
+      uint64_t cum = incl - csum;
+      for (uint32_t b = 0; b < chunk; ++b) {
+        cum += hist[lane * chunk + b];
+        if (cum >= k) {
+          res = lat ? lat_edge(lane * chunk + b) : (lane * chunk + b) * 10u;
+          break;
+        }
+      }
+    }
+    out[q] = __shfl_sync(FULL, res, L);
+  }
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = lane_id();
+  WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
+  for (;;) {
+    uint32_t kidx = 0;
+    if (lane == 0) kidx = atomicAdd(p.counter, 1u);
+    kidx = __shfl_sync(FULL, kidx, 0);
+    if ((uint64_t)kidx >= p.count) break;
+    const uint64_t sid = p.first + (uint64_t)kidx * p.stride;
+    const bellman_scenario sc = p.sc[sid];
+    const bellman_ctrl &cc = p.ctrls[sc.ctrl];
+    if ((cc.calibrated != 0) != (p.pass == 2)) continue;
+
+    // ---- a1: scenario decode
+    Sim S;
+    S.sid = (uint32_t)sid;
+    S.k0 = sc.seed_index;
+    S.wid_lo = (uint32_t)sc.wid;
+    S.wid_hi = (uint32_t)(sc.wid >> 32);
+    S.H = (uint64_t)sc.horizon_us;
+    S.mode = sc.mode;
+    S.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
+    S.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+    const bellman_profile pr = p.profs[sc.profile];
+    S.t0 = pr.t0_us;
+    S.knee = pr.knee;
+    S.slope = pr.slope_us;
+    S.kv = pr.kv_ns_per_word;
+    S.maxb = pr.max_batch;
+    S.pf_ns = pr.prefill_ns_per_word;
+    S.law = cc.law;
+    S.signal = cc.signal;
+    S.window = cc.window;
+    S.rmin = cc.r_min_bp;
+    S.rmax = cc.r_max_bp;
+    S.t1 = cc.t1;
+    S.t2 = cc.t2;
+    S.slo_us = cc.slo_us;
+    S.nrungs = cc.n_rungs;
+    S.rungs_lane = lane < 8 ? cc.rungs_bp[lane] : 0u;
+    S.flags = 0;
+    if (cc.calibrated) {
+      const uint32_t slot = p.series_slot[sc.calib_src];
+      const uint32_t *cb = p.calib + 4u * slot;
+      S.t1 = cb[0];
+      S.t2 = cb[1];
+      if (cb[2] != 0) {
+        S.law = BELLMAN_LAW_OFF;
+        S.flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+      }
+    }
+    S.r = S.law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
+    S.active = 0;
+    S.rung = 0;
+    S.ring = 0;
+    S.ring_n = 0;
+    S.ring_pos = 0;
+    S.ringA = 0;
+    S.activations = 0;
+    S.first_act = BELLMAN_NONE;
+    S.last_deact = BELLMAN_NONE;
+    S.active_ingests = 0;
+    S.sec_bound = kUs;
+    S.acc_sum = 0;
+    S.acc_cnt = 0;
+    const uint32_t rslot = p.series_slot[sid];
+    if (rslot != BELLMAN_NONE) {
+      S.series = p.series + p.series_off[rslot];
+      S.series_cap = p.series_cap[rslot];
+    } else {
+      S.series = nullptr;
+      S.series_cap = 0;
+    }
+    S.series_n = 0;
+    S.T = 0;
+    S.busy = 0;
+    S.iter_end = INF;
+    S.iter_B = S.iter_d = S.iter_align = 0;
+    S.ticks = 0;
+    S.next_done = 0xffffffffu;
+    S.next_pf = INF;
+    S.n_ready = S.B = S.in_sys = 0;
+    S.K = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      S.sa[s] = S.sp[s] = 0;
+      S.sR[s] = S.sin[s] = S.sdn[s] = 0;
+      // slots beyond max_batch are never free
+      S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
+    }
+    const DevTrace tr = p.traces[sc.trace];
+    S.segs = p.segs + tr.seg_off;
+    S.n_seg = tr.n_seg;
+    S.gen_seg = 0;
+    S.gen_fresh = 1;
+    S.gen_j = 0;
+    S.gen_acc = 0;
+    S.gen_cap = tr.cap;
+    S.gen_done = 0;
+    S.gen_tau = 0;
+    S.buf_h = S.buf_n = 0;
+    S.buf_a = 0;
+    S.buf_attr = 0;
+    S.buf_j = 0;
+    S.last_j = 0;
+    S.admitted = S.served = S.rewritten = S.slo_viol = S.win_served = 0;
+    S.words_in = S.words_out = S.idle = S.win_words_in = S.win_words_out = S.win_idle = 0;
+    S.sum_queue = S.sum_ttft = S.sum_e2e = 0;
+
+    // zero the warp's histograms
+    {
+      uint4 *z = reinterpret_cast<uint4 *>(&h);
+      for (uint32_t i = lane; i < sizeof(WarpHist) / 16u; i += 32u) z[i] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    S.refill(p);
+
+    // ---- the event/tick loop (a4-a7)
+    bool finished = false;
+    for (;;) {
+      const uint64_t t_it = S.busy ? S.iter_end : INF;
+      uint64_t t_arr = INF;
+      if (!S.busy && S.in_sys < S.maxb && S.buf_h < S.buf_n) t_arr = S.head_a();
+      uint64_t tn = t_it < S.next_pf ? t_it : S.next_pf;
+      tn = tn < t_arr ? tn : t_arr;
+      if (tn == INF) {
+        finished = true;
+        break;
+      }
+      if (tn >= S.H) break;
+      if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
+        S.idle += tn - S.T;
+        const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = tn < S.w1 ? tn : S.w1;
+        if (hi > lo) S.win_idle += hi - lo;
+      }
+      S.T = tn;
+      S.roll_second(tn);
+      if (t_it == tn) S.iteration_end(h);
+      if (S.next_pf == tn) S.prefill_end(h);
+      if (!S.busy) {
+        S.admit(p, h);
+        if (S.n_ready + S.B > 0) S.start_iteration();
+      }
+    }
+
+    // ---- termination (R20)
+    const uint64_t end = (S.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
+    if (S.in_sys == 0) {
+      S.idle += end - S.T;
+      const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = end < S.w1 ? end : S.w1;
+      if (hi > lo) S.win_idle += hi - lo;
+    }
+    if (S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
+    // queued at the end: accepted arrivals before `end` not admitted
+    uint64_t queued = 0;
+    for (;;) {
+      if (S.buf_h >= S.buf_n) {
+        if (S.gen_done) break;
+        S.refill(p);
+        continue;
+      }
+      const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.buf_a < end);
+      const uint32_t nq = __popc(m);
+      queued += nq;
+      if (nq) S.last_j = __shfl_sync(FULL, S.buf_j, 31 - __clz(m)) + 1u;
+      if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
+      S.buf_h = S.buf_n;
+    }
+    if (S.series && lane == 0) p.series_n[rslot] = S.series_n;
+
+    // ---- a9: percentiles from the histograms
+    __syncwarp();
+    uint32_t pe[2], pt[2], pm[1];
+    const uint32_t ps[2] = {50u, 99u};
+    const uint32_t p50[1] = {50u};
+    warp_percentiles(h.e2e, BELLMAN_HIST_LAT, S.served, ps, 2, pe, true);
+    uint64_t n_ttft = 0;
+    {
+      uint32_t c = 0;
+      for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) c += h.ttft[b];
+      n_ttft = __reduce_add_sync(FULL, c);
+    }
+    warp_percentiles(h.ttft, BELLMAN_HIST_LAT, n_ttft, ps, 2, pt, true);
+    warp_percentiles(h.r, BELLMAN_HIST_R, S.rewritten, p50, 1, pm, false);
+    // segment merge: integer atomics, order-independent
+    unsigned long long *sh = p.seg_hist + (uint64_t)sc.segment * kSegWords;
+    for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) {
+      if (h.e2e[b]) atomicAdd(&sh[b], (unsigned long long)h.e2e[b]);
+      if (h.ttft[b]) atomicAdd(&sh[BELLMAN_HIST_LAT + b], (unsigned long long)h.ttft[b]);
+    }
+    for (uint32_t b = lane; b < BELLMAN_HIST_R; b += 32u)
+      if (h.r[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + b], (unsigned long long)h.r[b]);
+
+    // ---- a8: summary record
+    if (lane == 0) {
+      bellman_scenario_stats o;
+      o.scenario_id = sid;
+      o.ticks = S.ticks;
+      o.candidates = S.last_j;
+      o.arrivals = S.admitted + queued;
+      o.admitted = S.admitted;
+      o.served = S.served;
+      o.rewritten = S.rewritten;
+      o.words_in = S.words_in;
+      o.words_out = S.words_out;
+      o.idle_us = S.idle;
+      o.end_us = end;
+      o.queued_end = queued;
+      o.inflight_end = S.in_sys;
+      o.win_served = S.win_served;
+      o.win_words_in = S.win_words_in;
+      o.win_words_out = S.win_words_out;
+      o.win_idle_us = S.win_idle;
+      o.sum_queue_us = S.sum_queue;
+      o.sum_ttft_us = S.sum_ttft;
+      o.sum_e2e_us = S.sum_e2e;
+      o.slo_violations = S.slo_viol;
+      o.e2e_p50_ms = pe[0];
+      o.e2e_p99_ms = pe[1];
+      o.ttft_p50_ms = pt[0];
+      o.ttft_p99_ms = pt[1];
+      o.median_r_bp = pm[0];
+      o.t1 = S.t1;
+      o.t2 = S.t2;
+      o.activations = S.activations;
+      o.first_act_s = S.first_act;
+      o.last_deact_s = S.last_deact;
+      o.active_ingests = S.active_ingests;
+      uint32_t fl = S.flags | BELLMAN_FLAG_DONE;
+      if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
+      o.flags = fl;
+      o.segment = sc.segment;
+      o._pad0 = 0;
+      // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
+      const double a = __dmul_rn(pr.e_in_j_per_word, (double)S.words_in);
+      const double b = __dmul_rn(pr.e_out_j_per_word, (double)S.words_out);
+      const double c = __dmul_rn(pr.p_idle_w, (double)S.idle);
+      o.energy_j = __dadd_rn(__dadd_rn(a, b), __ddiv_rn(c, 1e6));
+      const double wa = __dmul_rn(pr.e_in_j_per_word, (double)S.win_words_in);
+      const double wb = __dmul_rn(pr.e_out_j_per_word, (double)S.win_words_out);
+      const double wc = __dmul_rn(pr.p_idle_w, (double)S.win_idle);
+      o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
+      o._reserved[0] = o._reserved[1] = 0;
+      p.stats[sid] = o;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: per recorded slot, nearest-rank p50 / p75 of its series
+// by bisection on the value: the k-th smallest is the least v with
+// #{x <= v} >= k.  One warp per slot.
+__device__ uint32_t warp_kth(const uint32_t *x, uint32_t n, uint32_t k) {
+  uint32_t lo = 0, hi = 0xffffffffu;
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    uint32_t c = 0;
+    for (uint32_t i = lane_id(); i < n; i += 32u) c += x[i] <= mid;
+    c = __reduce_add_sync(FULL, c);
+    if (c >= k) hi = mid; else lo = mid + 1u;
+  }
+  return lo;
+}
+
+__global__ void bellman_calibrate_kernel(const Params p, uint32_t n_slots) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_slots) return;
+  const uint32_t n = min(p.series_n[w], p.series_cap[w]);
+  const uint32_t *x = p.series + p.series_off[w];
+  uint32_t t1 = 0, t2 = 0, st = 1;
+  if (n >= 4) {
+    t1 = warp_kth(x, n, (50u * n + 99u) / 100u);
+    t2 = warp_kth(x, n, (75u * n + 99u) / 100u);
+    st = t1 == t2 ? 2u : 0u;
+  }
+  if (lane_id() == 0) {
+    p.calib[4 * w + 0] = t1;
+    p.calib[4 * w + 1] = t2;
+    p.calib[4 * w + 2] = st;
+    p.calib[4 * w + 3] = n;
+  }
+}
+
+}  // namespace bellman
+
+int bellman_tick_grid(int device) {
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
+  cudaFuncSetAttribute(bellman::bellman_tick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel,
+                                                    bellman::kWarpsPerBlock * 32, smem) != cudaSuccess)
+    return -1;
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
+
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, cudaStream_t stream) {
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
+  bellman::bellman_tick_kernel<<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream) {
+  const uint32_t threads = 128, warps = threads / 32;
+  const uint32_t blocks = (n_slots + warps - 1) / warps;
+  if (blocks == 0) return cudaSuccess;
+  bellman::bellman_calibrate_kernel<<<blocks, threads, 0, stream>>>(p, n_slots);
+  return cudaGetLastError();
+}

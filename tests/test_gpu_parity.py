@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): bit-exact for every integer field (ticks,
+arrivals, words, served, latencies sums, percentiles, controller logs, flags)
+and for the E2E / TTFT / r histograms; fp64 energy within 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import check_all, compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _assert_ok(bad):
+    assert not bad, "\n".join(f"scenario {sid}: {e}" for sid, e in bad[:10])
+
+
+def test_c1_full():
+    bad, st = check_all(W.config_c1().columns())
+    _assert_ok(bad)
+    assert st[1]["activations"] >= 1 and st[1]["rewritten"] > 0
+
+
+def test_c2_reduced_all_rates():
+    bad, _ = check_all(W.config_c2(n_seeds=2).columns())
+    _assert_ok(bad)
+
+
+def test_c3_reduced_controller_grid():
+    bad, _ = check_all(W.config_c3(n_seeds=1).columns())
+    _assert_ok(bad)
+
+
+def test_c4_reduced_diurnal():
+    bad, _ = check_all(W.config_c4(n_seeds=2, n_traces=2, days=0.25).columns())
+    _assert_ok(bad)
+
+
+def test_c5_reduced_variants():
+    bad, _ = check_all(W.config_c5(n_seeds=1).columns())
+    _assert_ok(bad)
+
+
+def _edge_workload():
+    """Degenerate and ragged cases: empty traces, ragged max_batch around the
+    32-lane boundary, knee 0, heavy KV term, 1-µs prefill, realized length 1,
+    queue far beyond one 32-entry buffer, arrival caps around 32, E2E/SLO
+    signals, every law, every window, a degenerate calibration, odd windows."""
+    tabs = W.quantile_tables()
+    traces = [
+        W.const_trace(0.0, 100),                                     # 0: no arrivals
+        W.const_trace(2.5, 300),                                     # 1
+        W.const_trace(30.0, 120),                                    # 2: deep queue
+        [(0, 0), (50 * W.US, 4000), (50 * W.US, 500), (80 * W.US, 0), (200 * W.US, 1500)],  # 3: ramps + jump
+        (W.const_trace(5.0, 200), 31), (W.const_trace(5.0, 200), 32), (W.const_trace(5.0, 200), 33),  # 4-6: caps
+        (W.const_trace(5.0, 200), 1),                                # 7: single request
+        W.paper_trace(3.5, 180, 0.6),                                # 8
+    ]
+    profs = [
+        W.PROFILES["P24"], W.PROFILES["L8B"], W.PROFILES["spec-literal"],
+        dict(W.PROFILES["P24"], max_batch=1, knee=0), dict(W.PROFILES["P24"], max_batch=31, knee=0),
+        dict(W.PROFILES["P24"], max_batch=32, knee=32), dict(W.PROFILES["P24"], max_batch=33, knee=7),
+        dict(W.PROFILES["L8B"], max_batch=63, kv_ns_per_word=900),
+        dict(W.PROFILES["P24"], prefill_ns_per_word=0, t0_us=1, slope_us=0),  # 1 µs prefills, 1 µs iterations
+    ]
+    ctrls = [
+        W.OFF,
+        W.map_ctrl(30_000, 45_000),
+        W.map_ctrl(20_000, 60_000, rungs=(300, 700, 1900)),
+        W.step_ctrl(25_000, 40_000, (500, 1000, 1500, 2000)),
+        W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1200),
+        W.map_ctrl(5_000_000, 20_000_000, signal=W.SIG_E2E, window=3),
+        W.map_ctrl(200, 900, signal=W.SIG_SLO, slo_us=20_000_000, window=1),
+        W.map_ctrl(30_000, 31_000, window=8, r_min_bp=1, r_max_bp=5000),
+        W.Ctrl(W.LAW_MAP, W.SIG_TBT, 5, 500, 2000, 0, 0, 0, 0, 1, ()),  # calibrated
+    ]
+    sc = []
+    sid = 0
+    rng = np.random.default_rng(42)
+    for ti in range(len(traces)):
+        for pi in range(len(profs)):
+            ci = int(rng.integers(0, len(ctrls) - 1))
+            mode = int(rng.integers(0, 2))
+            H = int(rng.choice([1, 60 * W.US, 700 * W.US, 2000 * W.US]))
+            w0 = int(rng.integers(0, 200)) * W.US
+            sc.append(W.Scenario(int(rng.integers(0, 1000)), wid=ti, trace=ti, profile=pi, ctrl=ci, segment=0,
+                                 mode=mode, horizon_us=H, w0_us=w0, w1_us=w0 + int(rng.integers(0, 300)) * W.US))
+            sid += 1
+    # calibrated pairs: one healthy (paper trace), one degenerate (empty trace)
+    for ti in (8, 0, 7):
+        src = len(sc)
+        sc.append(W.Scenario(3, wid=ti, trace=ti, profile=0, ctrl=0, segment=0, mode=W.MODE_DRAIN,
+                             horizon_us=2000 * W.US, record=1))
+        sc.append(W.Scenario(3, wid=ti, trace=ti, profile=0, ctrl=8, segment=0, mode=W.MODE_DRAIN,
+                             horizon_us=2000 * W.US, calib_src=src))
+    return W.custom(traces, profs, ctrls, sc, tables=tabs)
+
+
+def test_edge_cases():
+    w = _edge_workload()
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)
+    assert any(int(r["flags"]) & 2 for r in st)  # a degenerate calibration occurred
+
+
+def test_short_outputs_and_tiny_tables():
+    """Realized length 1 and 2 dominate (R9), compliance noise maximal."""
+    t = W.quantile_tables(L_mean=2.0, L_sd=1.5, L_lo=1, L_hi=6, in_median=50, in_lo=1, in_hi=200,
+                          pred_b=2.0, comp_rel_noise=0.4)
+    scs = [W.Scenario(s, wid=0, trace=0, profile=p, ctrl=c, segment=0, mode=s % 2, horizon_us=40 * W.US)
+           for s in range(6) for p in range(2) for c in range(3)]
+    w = W.custom([W.const_trace(40.0, 30)],
+                 [dict(W.PROFILES["P24"], prefill_ns_per_word=3000, max_batch=5, knee=2),
+                  dict(W.PROFILES["spec-literal"], t0_us=900, prefill_ns_per_word=1000)],
+                 [W.OFF, W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 3000), W.map_ctrl(1_000, 9_000, window=2)],
+                 scs, tables=t, poly_q16=(3 * 65536, 50000, 20))
+    bad, _ = check_all(w.columns())
+    _assert_ok(bad)
+
+
+def test_sharded_runs_match_single_run():
+    """Interleaved shards (first = rank, stride = world) write the same records
+    as one run over all scenarios (determinism contract)."""
+    cols = W.config_c2(n_seeds=2, rates=[1.0, 3.0, 6.0]).columns()
+    full, _, _ = run_gpu(cols)
+    for world in (2, 3):
+        import torch
+
+        from paper_2510_15330_b200 import Simulator
+
+        sim = Simulator(cols)
+        n = len(cols["sc_seed"])
+        for rank in range(world):
+            sim.run(first=rank, count=len(range(rank, n, world)), stride=world)
+        torch.cuda.synchronize()
+        st = sim.stats()
+        assert np.array_equal(st.view(np.uint8), full.view(np.uint8))
+
+
+def test_c2_full_bench_config():
+    """BASELINE configs[1] at full size, in the launch configuration bench.py
+    times: every one of the 2048 records vs the oracle, and the per-segment
+    histograms vs the sum of the oracle's per-scenario histograms."""
+    w = W.config_c2()
+    cols = w.columns()
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    sim = Simulator(cols)
+    sim.run()
+    torch.cuda.synchronize()
+    st = sim.stats()
+    seg = sim.segment_hist()
+    b = oracle.Bound(cols)
+    want_seg = np.zeros_like(seg, dtype=np.int64)
+    bad = []
+    for sid in range(w.n_scenarios):
+        o = oracle.run_scenario(b, sid)
+        e = compare(st[sid], o, sid)
+        if e:
+            bad.append((sid, e))
+        s = w.scenarios[sid].segment
+        want_seg[s, :896] += o["hist_e2e"]
+        want_seg[s, 896:1792] += o["hist_ttft"]
+        want_seg[s, 1792:] += o["hist_r"]
+    _assert_ok(bad)
+    assert np.array_equal(seg.astype(np.int64), want_seg)
+    assert sim.last_launches == 1

@@ -290,7 +290,7 @@ def main():
     e = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e, op=dist.ReduceOp.MAX)
-    e2e_value = ticks_all * len(e2e_ms) / (float(e[0]) / 1e3)
+    e2e_value = ticks_all * len(e2e_ms) / (float(e[0]) / 1e3) if e2e_ms else None
     h2d = int(sum(v.nbytes for k, v in pk.items() if isinstance(v, np.ndarray)) +
               sum(v.nbytes for v in pk["tables"].values()) + 8 * W.TABLE_N + 4 * n)
     d2h = int(n * 256)

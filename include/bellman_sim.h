@@ -85,10 +85,10 @@ typedef struct {
 /* Serving cost profile (decode law S:209-217; prefill S:218-226;
  * energy S:227-235; optional KV term, reading R2). */
 typedef struct {
-  uint32_t t0_us;               /* base decode iteration time, >= 1 */
+  uint32_t t0_us;               /* base decode iteration time, 1..2^24 */
   uint32_t knee;                /* batch size where slowdown begins, <= max_batch */
-  uint32_t slope_us;            /* added µs per decoding request beyond the knee */
-  uint32_t kv_ns_per_word;      /* ns per resident context word (0 = SPEC's law) */
+  uint32_t slope_us;            /* added µs per decoding request beyond the knee, <= 2^16 */
+  uint32_t kv_ns_per_word;      /* ns per resident context word, <= 1024 (0 = SPEC's law) */
   uint32_t max_batch;           /* admission cap, 1..64 */
   uint32_t prefill_ns_per_word; /* prefill time per input word, <= 2^24 */
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;

@@ -86,8 +86,10 @@ static bellman_status validate(const bellman_sim_desc *d) {
     const bellman_profile &p = d->profiles[i];
     if (p.max_batch < 1 || p.max_batch > BELLMAN_MAX_BATCH) return fail(nullptr, BELLMAN_EINVAL, "profile %u: max_batch not in 1..64", i);
     if (p.knee > p.max_batch) return fail(nullptr, BELLMAN_EINVAL, "profile %u: knee > max_batch", i);
-    if (p.t0_us < 1) return fail(nullptr, BELLMAN_EINVAL, "profile %u: t0_us must be >= 1", i);
+    if (p.t0_us < 1 || p.t0_us > (1u << 24)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: t0_us not in 1..2^24", i);
+    if (p.slope_us > (1u << 16)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: slope_us > 2^16", i);
     if (p.prefill_ns_per_word > (1u << 24)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: prefill too large", i);
+    if (p.kv_ns_per_word > 1024u) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_ns_per_word > 1024", i);
     if (!(p.e_in_j_per_word >= 0) || !(p.e_out_j_per_word >= 0) || !(p.p_idle_w >= 0))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: negative energy coefficient", i);
   }

@@ -87,6 +87,14 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
   return x;
 }
 
+// Warp sum of per-lane values < 2^48 with two REDUX.SUM (no 64-bit shuffles):
+// low 22 bits and the rest are summed separately (each total < 2^32 for <= 64 terms).
+__device__ __forceinline__ uint64_t warp_sum_split(uint64_t x) {
+  const uint32_t lo = __reduce_add_sync(FULL, (uint32_t)(x & 0x3FFFFFu));
+  const uint32_t hi = __reduce_add_sync(FULL, (uint32_t)(x >> 22));
+  return ((uint64_t)hi << 22) + lo;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // ---------------------------------------------------------------------------
@@ -266,7 +274,7 @@ struct Sim {
 
   // close the open second (if it holds samples) and open the one containing t
   __device__ __forceinline__ void roll_second(uint64_t t) {
-    if (t < sec_bound) return;
+    if (t < sec_bound) return;  // sec_bound = INF when nothing consumes the signal
     if (acc_cnt) ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
     acc_sum = 0;
     acc_cnt = 0;
@@ -313,9 +321,9 @@ struct Sim {
         if (sph[s] == PH_DEC) dmin = min(dmin, sdn[s]);
       }
       next_done = __reduce_min_sync(FULL, dmin);
-      const uint64_t se = warp_sum_u64(e2e_l);
+      const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
-      K -= warp_sum_u64(kdrop);
+      K -= __reduce_add_sync(FULL, (uint32_t)kdrop);
       served += ndone;
       sum_e2e += se;
       slo_viol += ns;
@@ -358,13 +366,13 @@ struct Sim {
     }
     const uint32_t m = __reduce_min_sync(FULL, mpf);
     next_pf = (m == 0xffffffffu) ? INF : Tn + m;
-    sum_ttft += warp_sum_u64(ttft_l);
+    sum_ttft += warp_sum_split(ttft_l);
     words_out += nfirst;
     if (in_win(Tn)) win_words_out += nfirst;
     n_ready += __reduce_add_sync(FULL, nrdy);
     const uint32_t nc = __reduce_add_sync(FULL, n1);
     if (nc) {
-      const uint64_t se = warp_sum_u64(e2e_l);
+      const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
       served += nc;
       sum_e2e += se;
@@ -379,6 +387,8 @@ struct Sim {
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
     const uint32_t lane = lane_id();
     const uint64_t Tn = T;
+    if (in_sys >= maxb) return;
+    if (buf_h < buf_n && head_a() > Tn) return;  // queue head has not arrived yet
     while (in_sys < maxb) {
       if (buf_h >= buf_n) {
         if (gen_done) break;
@@ -439,10 +449,10 @@ struct Sim {
       }
       const uint32_t mnew = __reduce_min_sync(FULL, mpf);
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
-      const uint64_t win = warp_sum_u64(win_l);
+      const uint64_t win = __reduce_add_sync(FULL, (uint32_t)win_l);
       words_in += win;
       if (in_win(Tn)) win_words_in += win;
-      sum_queue += warp_sum_u64(q_l);
+      sum_queue += warp_sum_split(q_l);
       if (r > 0) {
         rewritten += k;
         if (lane == 0) atomicAdd(&h.r[r / 10u < BELLMAN_HIST_R ? r / 10u : BELLMAN_HIST_R - 1], k);
@@ -455,10 +465,95 @@ struct Sim {
     }
   }
 
+  // ------------------------------------------------------------------ a4/a5 leap
+  // Execute in bulk the longest run of iterations whose ends are uneventful —
+  // no completion (index < next_done), no prefill end, no admission (head
+  // arrival still in the future or no free slot), no window / horizon
+  // boundary — exactly as the per-iteration path would: each emits B words
+  // with TBT gap d_m = c + floor(kv (K + m B) / 1000) and grows K by B.  A
+  // second boundary met inside the run is rolled in place (ingest), as the
+  // per-iteration path does at that iteration end.  Called at an iteration
+  // start with no joiners, so no alignment term is involved.  All arithmetic
+  // is 32-bit (bounds validated on the host: d < 2^31); a leap may always be
+  // cut short without changing results, so `room` is capped at 2^32 - 1.
+  __device__ __forceinline__ void leap(const Params &p) {
+    uint64_t stop = next_pf < H ? next_pf : H;
+    if (in_sys < maxb) {
+      if (buf_h >= buf_n && !gen_done) refill(p);
+      if (buf_h < buf_n) {
+        const uint64_t ha = head_a();
+        if (ha < stop) stop = ha;
+      }
+    }
+    if (T < w0) {
+      if (w0 < stop) stop = w0;
+    } else if (T < w1) {
+      if (w1 < stop) stop = w1;
+    }
+    const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
+    if (nmax == 0 || stop <= T + 1u) return;
+    const uint32_t c = t0 + slope * (B > knee ? B - knee : 0u);
+    const uint64_t kk = (uint64_t)kv * K;
+    uint32_t q = (uint32_t)(kk / 1000u), rr = (uint32_t)(kk % 1000u);
+    const uint32_t kstep = kv * B, qs = kstep / 1000u, rs = kstep % 1000u;
+    const bool win = in_win(T);
+    uint32_t done = 0;
+    for (;;) {
+      const uint64_t lim = stop < sec_bound ? stop : sec_bound;
+      const uint64_t room64 = lim - 1u - T;
+      const uint32_t room = room64 > 0xffffffffull ? 0xffffffffu : (uint32_t)room64;
+      const uint32_t left = nmax - done;
+      uint32_t n = 0, used = 0;
+      if (kv == 0) {
+        const uint32_t nn = room / c;
+        n = nn < left ? nn : left;
+        used = n * c;
+      } else {
+        while (n < left) {
+          const uint32_t d = c + q;
+          if (d > room - used) break;
+          used += d;
+          rr += rs;
+          const uint32_t carry = rr >= 1000u;
+          rr -= carry ? 1000u : 0u;
+          q += qs + carry;
+          n++;
+        }
+      }
+      if (n) {
+        const uint64_t words = (uint64_t)n * B;
+        ticks += n;
+        T += used;
+        K += words;
+        words_out += words;
+        if (win) win_words_out += words;
+        if (signal == BELLMAN_SIG_TBT) {
+          acc_sum += (uint64_t)B * used;
+          acc_cnt += (uint32_t)words;
+        }
+        done += n;
+      }
+      if (done == nmax) break;
+      const uint64_t tnext = T + (c + q);  // end of the next iteration (q = kv K / 1000 now)
+      if (tnext >= stop || tnext < sec_bound) break;
+      roll_second(tnext);  // the next end opens a new second: ingest the closed one here
+    }
+  }
+
   // ------------------------------------------------------------------ a4
   __device__ __forceinline__ void start_iteration() {
     const uint64_t Tn = T;
     const uint32_t c = ticks;  // index of the new iteration
+    if (n_ready == 0) {  // same batch as the previous iteration: no joiners
+      const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (B > knee ? B - knee : 0u) + ((uint64_t)kv * K) / 1000u;
+      iter_d = d;
+      iter_B = B;
+      iter_align = 0;
+      iter_end = Tn + d;
+      busy = 1;
+      ticks++;
+      return;
+    }
     uint32_t jn = 0xffffffffu;
     uint64_t kadd = 0, al = 0;
 #pragma unroll
@@ -471,10 +566,10 @@ struct Sim {
         jn = min(jn, sdn[s]);
       }
     }
-    const uint64_t align = warp_sum_u64(al);
+    const uint64_t align = warp_sum_split(al);
     const uint32_t mj = __reduce_min_sync(FULL, jn);
     if (mj < next_done) next_done = mj;
-    K += warp_sum_u64(kadd);
+    K += __reduce_add_sync(FULL, (uint32_t)kadd);
     B += n_ready;
     n_ready = 0;
     const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (B > knee ? B - knee : 0u) + ((uint64_t)kv * K) / 1000u;
@@ -524,7 +619,7 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const Params p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
   WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
@@ -587,7 +682,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const
     S.first_act = BELLMAN_NONE;
     S.last_deact = BELLMAN_NONE;
     S.active_ingests = 0;
-    S.sec_bound = kUs;
     S.acc_sum = 0;
     S.acc_cnt = 0;
     const uint32_t rslot = p.series_slot[sid];
@@ -599,6 +693,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const
       S.series_cap = 0;
     }
     S.series_n = 0;
+    // the per-second signal feeds only the controller (MAP/STEP) and the recorder
+    S.sec_bound = (S.law == BELLMAN_LAW_MAP || S.law == BELLMAN_LAW_STEP || S.series) ? kUs : INF;
     S.T = 0;
     S.busy = 0;
     S.iter_end = INF;
@@ -645,14 +741,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const
     // ---- the event/tick loop (a4-a7)
     bool finished = false;
     for (;;) {
-      const uint64_t t_it = S.busy ? S.iter_end : INF;
-      uint64_t t_arr = INF;
-      if (!S.busy && S.in_sys < S.maxb && S.buf_h < S.buf_n) t_arr = S.head_a();
-      uint64_t tn = t_it < S.next_pf ? t_it : S.next_pf;
-      tn = tn < t_arr ? tn : t_arr;
-      if (tn == INF) {
-        finished = true;
-        break;
+      uint64_t tn;
+      if (S.busy) {
+        // prefill ends strictly inside the running iteration only emit first
+        // words / R=1 completions (time-stamped at p); process them in order
+        // before the iteration end (same-instant ends go after E1, R7).
+        while (S.next_pf < S.iter_end && S.next_pf < S.H) {
+          S.T = S.next_pf;
+          S.roll_second(S.T);
+          S.prefill_end(h);
+        }
+        tn = S.iter_end;
+      } else {
+        uint64_t t_arr = INF;
+        if (S.in_sys < S.maxb && S.buf_h < S.buf_n) t_arr = S.head_a();
+        tn = S.next_pf < t_arr ? S.next_pf : t_arr;
+        if (tn == INF) {
+          finished = true;
+          break;
+        }
       }
       if (tn >= S.H) break;
       if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
@@ -662,11 +769,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const
       }
       S.T = tn;
       S.roll_second(tn);
-      if (t_it == tn) S.iteration_end(h);
+      if (S.busy) S.iteration_end(h);
       if (S.next_pf == tn) S.prefill_end(h);
       if (!S.busy) {
         S.admit(p, h);
-        if (S.n_ready + S.B > 0) S.start_iteration();
+        if (S.n_ready + S.B > 0) {
+          if (S.n_ready == 0) S.leap(p);
+          S.start_iteration();
+        }
       }
     }
 
@@ -677,7 +787,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bellman_tick_kernel(const
       const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = end < S.w1 ? end : S.w1;
       if (hi > lo) S.win_idle += hi - lo;
     }
-    if (S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
+    if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
     // queued at the end: accepted arrivals before `end` not admitted
     uint64_t queued = 0;
     for (;;) {

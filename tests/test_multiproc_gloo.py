@@ -1,0 +1,89 @@
+"""The N>1 path on CPU: world_size-2 gloo processes shard a workload by
+interleaving, compute their records (oracle stand-in for the kernel: this tests
+the sharding and the exchange, not the simulation), gather them with
+paper_2510_15330_b200.parallel and reduce segment histograms; the gathered
+result must equal the single-process result byte for byte."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import workloads as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _records(cols, ids):
+    import oracle
+
+    b = oracle.Bound(cols)
+    recs = np.zeros((len(ids), 32), dtype=np.uint64)  # 256 B = 32 u64 words
+    seg = np.zeros((int(cols["n_segments"]), 3), dtype=np.int64)
+    for i, sid in enumerate(ids):
+        r = oracle.run_scenario(b, int(sid))
+        recs[i, 0] = sid
+        recs[i, 1] = r["ticks"]
+        recs[i, 2] = r["served"]
+        recs[i, 3] = r["words_out"]
+        recs[i, 4] = np.float64(r["energy_j"]).view(np.uint64)
+        s = cols["sc_segment"][sid]
+        seg[s] += [r["served"], r["ticks"], r["rewritten"]]
+    return recs, seg
+
+
+def _worker(rank, world, port, cols, q):
+    from paper_2510_15330_b200 import parallel as P
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = len(cols["sc_seed"])
+    ids = W.shard(n, rank, world)
+    recs, seg = _records(cols, ids)
+    local = torch.from_numpy(recs.view(np.uint8).reshape(len(ids), 256).copy())
+    full = P.gather_summaries(local, n, rank, world)
+    segt = P.reduce_segments(torch.from_numpy(seg))
+    if rank == 0:
+        q.put((full.numpy().copy(), segt.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_gather_matches_single_process(world):
+    cols = W.config_c2(n_seeds=3, rates=[1.0, 4.0], horizon_s=60).columns()  # 12 scenarios, not divisible by 8
+    n = len(cols["sc_seed"])
+    want, want_seg = _records(cols, np.arange(n))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cols, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full, seg = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(full.view(np.uint64).reshape(n, 32), want)
+    assert np.array_equal(seg, want_seg)
+
+
+def test_gather_reorder_uneven():
+    """Reordering logic for n not divisible by world (no process group needed)."""
+    for n, world in ((7, 2), (10, 3), (5, 8)):
+        m = (n + world - 1) // world
+        gathered = np.full((world * m,), -1)
+        for r in range(world):
+            ids = list(range(r, n, world))
+            gathered[r * m: r * m + len(ids)] = ids
+        full = gathered.reshape(world, m).T.reshape(-1)[:n]
+        assert list(full) == list(range(n))

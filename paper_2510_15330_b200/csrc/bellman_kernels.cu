@@ -23,6 +23,14 @@
 
 #include "bellman_internal.cuh"
 
+#ifdef BELLMAN_PROFILE_COUNTERS
+// Development-only event counters (separate build, never the product .so).
+__device__ unsigned long long g_prof[16];
+#define PROF(i) (prof_[i]++)
+#else
+#define PROF(i) ((void)0)
+#endif
+
 namespace bellman {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -32,7 +40,7 @@ constexpr uint64_t kLn2Q32 = 2977044472ull;  // round(ln 2 * 2^32)
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11) — counter (c0..c3), key (k0, k1).
-__device__ __forceinline__ uint4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+__device__ __noinline__ uint4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
                                         uint32_t c3) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
@@ -98,13 +106,17 @@ __device__ __forceinline__ uint64_t warp_sum_split(uint64_t x) {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // ---------------------------------------------------------------------------
-// The per-scenario simulation.  Every scalar is warp-uniform.
+// The per-scenario simulation.  Every scalar is warp-uniform.  Derived
+// quantities are maintained incrementally so that an event trip does no
+// division: the cost base c = t0 + slope max(0, B - knee), the KV term as
+// kv K = kq 1000 + kr, the window flag and its next boundary, the arrival time
+// of the queue head.
 struct Sim {
+  uint32_t lane;
   // ---- scenario (a1)
-  uint32_t sid, k0;  // Philox key word 0 = seed_index
+  uint32_t k0;  // Philox key word 0 = seed_index
   uint32_t wid_lo, wid_hi;
   uint64_t H;
-  uint32_t mode;
   uint64_t w0, w1;
   // profile
   uint32_t t0, knee, slope, kv, maxb, pf_ns;
@@ -117,7 +129,7 @@ struct Sim {
   uint64_t ringA;
   uint32_t activations, first_act, last_deact, active_ingests;
   // per-second accumulator of the selected signal (a6)
-  uint64_t sec_bound;  // (open second + 1) * 1e6
+  uint64_t sec_bound;  // (open second + 1) * 1e6, INF when nothing consumes the signal
   uint64_t acc_sum;
   uint32_t acc_cnt;
   // recording (a10 source)
@@ -128,13 +140,18 @@ struct Sim {
   uint64_t T;
   uint32_t busy;
   uint64_t iter_end;
-  uint32_t iter_B;
-  uint64_t iter_d, iter_align;
+  uint32_t iter_d;
+  uint64_t iter_align;
   uint32_t ticks;      // iterations started; the running one has index ticks-1
   uint32_t next_done;  // min completion iteration over decoding slots
   uint64_t next_pf;    // min prefill end over prefilling slots
   uint32_t n_ready, B, in_sys;
-  uint64_t K;
+  uint32_t cbase;             // t0 + slope * max(0, B - knee)
+  uint32_t kq, kr;            // kv * K = kq * 1000 + kr, K = context words of the batch
+  uint32_t kstep_q, kstep_r;  // kv * B = kstep_q * 1000 + kstep_r (growth per iteration)
+  uint32_t win_now;           // T in [w0, w1)
+  uint64_t win_next;          // next window boundary after T (INF if none)
+  uint64_t stop_static;       // min(H, win_next)
   // slots (lane-parallel)
   uint64_t sa[2], sp[2];
   uint32_t sR[2], sin[2], sdn[2], sph[2];
@@ -144,20 +161,21 @@ struct Sim {
   uint64_t gen_tau;
   uint32_t buf_h, buf_n;
   uint64_t buf_a;      // lane-parallel buffer of upcoming arrivals
-  uint32_t buf_attr;   // L | input << 16
+  uint32_t buf_in;     // input words
+  uint32_t buf_U;      // realized unbounded length (a3)
+  uint32_t buf_P;      // predicted length (a3)
+  int32_t buf_fc;      // compliance factor, Q16 (a3)
   uint32_t buf_j;
+  uint64_t head_t;     // arrival time of the queue head, INF when no arrival remains
   uint32_t last_j;     // candidate index of the last counted arrival + 1
   // ---- counters (a8)
   uint32_t admitted, served, rewritten, slo_viol, win_served;
   uint64_t words_in, words_out, idle, win_words_in, win_words_out, win_idle;
   uint64_t sum_queue, sum_ttft, sum_e2e;
 
-  __device__ __forceinline__ bool in_win(uint64_t t) const { return t >= w0 && t < w1; }
-
   // ------------------------------------------------------------------ a2
   // Refill the 32-entry arrival buffer with the next accepted candidates.
   __device__ __forceinline__ void refill(const Params &p) {
-    const uint32_t lane = lane_id();
     buf_h = 0;
     buf_n = 0;
     while (!gen_done && buf_n == 0) {
@@ -205,9 +223,21 @@ struct Sim {
       const uint32_t src = __fns(am, 0, (int)lane + 1);
       const uint32_t s = src < 32u ? src : 0u;
       buf_a = __shfl_sync(FULL, tau, s);
-      buf_attr = __shfl_sync(FULL, attr, s);
+      const uint32_t at = __shfl_sync(FULL, attr, s);
       buf_j = __shfl_sync(FULL, jj, s);
       buf_n = cnt;
+      // a3: the accepted request's own draws (tag 1), lane-parallel, ahead of admission
+      {
+        const uint32_t L = at & 0xFFFFu;
+        buf_in = at >> 16;
+        const uint4 v = philox(k0, kSeedHi, buf_j, 1u, wid_lo, wid_hi);
+        const uint32_t fvar = (uint32_t)__ldg(&p.tabF[v.x >> 20]);
+        const uint64_t U = ((uint64_t)L * fvar + 32768u) >> 16;  // S:139, R14
+        buf_U = U < 1 ? 1u : (uint32_t)U;
+        const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
+        buf_P = P0 < 1 ? 1u : (uint32_t)P0;
+        buf_fc = __ldg(&p.tabC[v.z >> 20]);
+      }
       gen_acc += cnt;
       if (first_over < 32u) {
         gen_j += first_over + 1u;  // the crossing candidate is consumed (R17)
@@ -218,24 +248,20 @@ struct Sim {
         gen_tau = __shfl_sync(FULL, tau, 31);
       }
     }
-  }
-
-  __device__ __forceinline__ uint64_t head_a() const {
-    return __shfl_sync(FULL, buf_a, buf_h & 31u);
+    head_t = buf_n ? __shfl_sync(FULL, buf_a, 0) : INF;
   }
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
     if (series) {
       if (series_n < series_cap) {
-        if (lane_id() == 0) series[series_n] = x;
+        if (lane == 0) series[series_n] = x;
       } else {
         flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
       }
       series_n++;
     }
     if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return;
-    const uint32_t lane = lane_id();
     const uint32_t ev = __shfl_sync(FULL, ring, ring_pos);
     if (lane == ring_pos) ring = x;
     if (ring_n < window) {
@@ -274,11 +300,51 @@ struct Sim {
 
   // close the open second (if it holds samples) and open the one containing t
   __device__ __forceinline__ void roll_second(uint64_t t) {
-    if (t < sec_bound) return;  // sec_bound = INF when nothing consumes the signal
+    if (t < sec_bound) return;
     if (acc_cnt) ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
     acc_sum = 0;
     acc_cnt = 0;
     sec_bound = (t / kUs + 1u) * kUs;
+  }
+
+  __device__ __forceinline__ void update_window() {
+    win_now = T >= w0 && T < w1;
+    win_next = T < w0 ? w0 : (T < w1 ? w1 : INF);
+    stop_static = H < win_next ? H : win_next;
+  }
+
+  // move the clock to an event instant t >= T
+  __device__ __forceinline__ void advance(uint64_t t) {
+    T = t;
+    roll_second(t);
+    if (t >= win_next) update_window();
+  }
+
+  // B changed: cost base and per-iteration KV growth
+  __device__ __forceinline__ void batch_changed() {
+    cbase = t0 + slope * (B > knee ? B - knee : 0u);
+    const uint32_t ks = kv * B;
+    kstep_q = ks / 1000u;
+    kstep_r = ks - kstep_q * 1000u;
+  }
+  __device__ __forceinline__ void kv_add(uint64_t x) {  // kv K += x
+    const uint64_t q = x / 1000u;
+    kr += (uint32_t)(x - q * 1000u);
+    kq += (uint32_t)q;
+    if (kr >= 1000u) {
+      kr -= 1000u;
+      kq++;
+    }
+  }
+  __device__ __forceinline__ void kv_sub(uint64_t x) {  // kv K -= x
+    const uint64_t q = x / 1000u;
+    const uint32_t rem = (uint32_t)(x - q * 1000u);
+    kq -= (uint32_t)q;
+    if (kr < rem) {
+      kr += 1000u;
+      kq--;
+    }
+    kr -= rem;
   }
 
   // ------------------------------------------------------------------ a5
@@ -295,17 +361,23 @@ struct Sim {
 
   __device__ __forceinline__ void iteration_end(WarpHist &h) {
     const uint64_t Tn = T;
-    words_out += iter_B;
-    if (in_win(Tn)) win_words_out += iter_B;
+    words_out += B;
+    if (win_now) win_words_out += B;
     if (signal == BELLMAN_SIG_TBT) {
-      acc_sum += (uint64_t)iter_B * iter_d + iter_align;
-      acc_cnt += iter_B;
+      acc_sum += (uint64_t)B * iter_d + iter_align;
+      acc_cnt += B;
     }
-    K += iter_B;
+    // every participant emitted one word: K += B
+    kr += kstep_r;
+    kq += kstep_q;
+    if (kr >= 1000u) {
+      kr -= 1000u;
+      kq++;
+    }
     const uint32_t it = ticks - 1u;
     if (it == next_done) {
-      uint64_t e2e_l = 0, kdrop = 0;
-      uint32_t nslo = 0, ndone = 0, dmin = 0xffffffffu;
+      uint64_t e2e_l = 0;
+      uint32_t kdrop = 0, nslo = 0, ndone = 0, dmin = 0xffffffffu;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const bool c = sph[s] == PH_DEC && sdn[s] == it;
@@ -314,7 +386,7 @@ struct Sim {
           const uint64_t e = Tn - sa[s];
           e2e_l += e;
           nslo += e > slo_us;
-          kdrop += (uint64_t)sin[s] + sR[s];
+          kdrop += sin[s] + sR[s];
           atomicAdd(&h.e2e[lat_bin(e / 1000u)], 1u);
           sph[s] = PH_EMPTY;
         }
@@ -323,13 +395,14 @@ struct Sim {
       next_done = __reduce_min_sync(FULL, dmin);
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
-      K -= __reduce_add_sync(FULL, (uint32_t)kdrop);
+      kv_sub((uint64_t)kv * __reduce_add_sync(FULL, kdrop));
       served += ndone;
       sum_e2e += se;
       slo_viol += ns;
-      if (in_win(Tn)) win_served += ndone;
+      if (win_now) win_served += ndone;
       in_sys -= ndone;
       B -= ndone;
+      batch_changed();
       complete_sig(se, ndone, ns);
     }
     busy = 0;
@@ -359,16 +432,13 @@ struct Sim {
           nrdy++;
         }
       }
-      if (sph[s] == PH_PREFILL) {
-        const uint64_t off = sp[s] - Tn;
-        mpf = min(mpf, (uint32_t)off);
-      }
+      if (sph[s] == PH_PREFILL) mpf = min(mpf, (uint32_t)(sp[s] - Tn));
     }
     const uint32_t m = __reduce_min_sync(FULL, mpf);
     next_pf = (m == 0xffffffffu) ? INF : Tn + m;
     sum_ttft += warp_sum_split(ttft_l);
     words_out += nfirst;
-    if (in_win(Tn)) win_words_out += nfirst;
+    if (win_now) win_words_out += nfirst;
     n_ready += __reduce_add_sync(FULL, nrdy);
     const uint32_t nc = __reduce_add_sync(FULL, n1);
     if (nc) {
@@ -377,65 +447,49 @@ struct Sim {
       served += nc;
       sum_e2e += se;
       slo_viol += ns;
-      if (in_win(Tn)) win_served += nc;
+      if (win_now) win_served += nc;
       in_sys -= nc;
       complete_sig(se, nc, ns);
     }
   }
 
   // ------------------------------------------------------------------ a7 (+a3)
+  // Precondition: in_sys < maxb and head_t <= T.
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
-    const uint32_t lane = lane_id();
     const uint64_t Tn = T;
-    if (in_sys >= maxb) return;
-    if (buf_h < buf_n && head_a() > Tn) return;  // queue head has not arrived yet
-    while (in_sys < maxb) {
-      if (buf_h >= buf_n) {
-        if (gen_done) break;
-        refill(p);
-        continue;
-      }
+    for (;;) {
       const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && buf_a <= Tn);
       const uint32_t na = __popc(arrived);
-      if (na == 0) break;
       const uint32_t room = maxb - in_sys;
       const uint32_t k = na < room ? na : room;
       const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY);
       const uint32_t f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
-      uint64_t win_l = 0, q_l = 0;
-      uint32_t mpf = 0xffffffffu;
+      uint64_t q_l = 0;
+      uint32_t win_l = 0, mpf = 0xffffffffu;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t rank = s == 0 ? rank0 : rank1;
         const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
         const uint32_t src = (buf_h + (mine ? rank : 0u)) & 31u;
         const uint64_t a = __shfl_sync(FULL, buf_a, src);
-        const uint32_t attr = __shfl_sync(FULL, buf_attr, src);
-        const uint32_t j = __shfl_sync(FULL, buf_j, src);
+        const uint32_t in = __shfl_sync(FULL, buf_in, src);
+        const uint32_t U = __shfl_sync(FULL, buf_U, src);
+        const uint32_t P = __shfl_sync(FULL, buf_P, src);
+        const int32_t fc = __shfl_sync(FULL, buf_fc, src);
         if (mine) {
-          const uint32_t L = attr & 0xFFFFu, in = attr >> 16;
-          const uint4 v = philox(k0, kSeedHi, j, 1u, wid_lo, wid_hi);  // a3 draws (tag 1)
-          const uint32_t fvar = (uint32_t)__ldg(&p.tabF[v.x >> 20]);
-          const int32_t noise = __ldg(&p.tabN[v.y >> 20]);
-          uint32_t R;
-          if (r > 0) {
-            const int64_t P0 = (int64_t)L + noise;
-            const uint64_t P = P0 < 1 ? 1u : (uint64_t)P0;
-            int64_t N = (int64_t)((P * (10000u - r) + 5000u) / 10000u);
+          uint32_t R = U;
+          if (r > 0) {  // a7 rewrite: N = round(P (1 - r)), realized = round(poly(N) Fcomp)
+            int64_t N = (int64_t)(((uint64_t)P * (10000u - r) + 5000u) / 10000u);
             if (N < 1) N = 1;
             const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
-            const int32_t fc = __ldg(&p.tabC[v.z >> 20]);
             __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
             if (x < 1) x = 1;
             if (x > (1 << 24)) x = 1 << 24;
             R = (uint32_t)x;
-          } else {
-            const uint64_t U = ((uint64_t)L * fvar + 32768u) >> 16;
-            R = U < 1 ? 1u : (uint32_t)U;
           }
-          uint64_t pf = ((uint64_t)pf_ns * in) / 1000u;
+          uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
           if (pf < 1) pf = 1;
           sa[s] = a;
           sp[s] = Tn + pf;
@@ -444,14 +498,14 @@ struct Sim {
           sph[s] = PH_PREFILL;
           win_l += in;
           q_l += Tn - a;
-          mpf = min(mpf, (uint32_t)pf);
+          mpf = min(mpf, pf);
         }
       }
       const uint32_t mnew = __reduce_min_sync(FULL, mpf);
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
-      const uint64_t win = __reduce_add_sync(FULL, (uint32_t)win_l);
+      const uint32_t win = __reduce_add_sync(FULL, win_l);
       words_in += win;
-      if (in_win(Tn)) win_words_in += win;
+      if (win_now) win_words_in += win;
       sum_queue += warp_sum_split(q_l);
       if (r > 0) {
         rewritten += k;
@@ -461,7 +515,14 @@ struct Sim {
       in_sys += k;
       admitted += k;
       buf_h += k;
-      if (k < na) break;  // slots full
+      if (buf_h < buf_n) {
+        head_t = __shfl_sync(FULL, buf_a, buf_h & 31u);
+      } else if (!gen_done) {
+        refill(p);
+      } else {
+        head_t = INF;
+      }
+      if (in_sys >= maxb || head_t > Tn) break;
     }
   }
 
@@ -476,28 +537,13 @@ struct Sim {
   // start with no joiners, so no alignment term is involved.  All arithmetic
   // is 32-bit (bounds validated on the host: d < 2^31); a leap may always be
   // cut short without changing results, so `room` is capped at 2^32 - 1.
-  __device__ __forceinline__ void leap(const Params &p) {
-    uint64_t stop = next_pf < H ? next_pf : H;
-    if (in_sys < maxb) {
-      if (buf_h >= buf_n && !gen_done) refill(p);
-      if (buf_h < buf_n) {
-        const uint64_t ha = head_a();
-        if (ha < stop) stop = ha;
-      }
-    }
-    if (T < w0) {
-      if (w0 < stop) stop = w0;
-    } else if (T < w1) {
-      if (w1 < stop) stop = w1;
-    }
+  __device__ __forceinline__ void leap() {
+    uint64_t stop = next_pf < stop_static ? next_pf : stop_static;
+    if (in_sys < maxb && head_t < stop) stop = head_t;
     const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
     if (nmax == 0 || stop <= T + 1u) return;
-    const uint32_t c = t0 + slope * (B > knee ? B - knee : 0u);
-    const uint64_t kk = (uint64_t)kv * K;
-    uint32_t q = (uint32_t)(kk / 1000u), rr = (uint32_t)(kk % 1000u);
-    const uint32_t kstep = kv * B, qs = kstep / 1000u, rs = kstep % 1000u;
-    const bool win = in_win(T);
-    uint32_t done = 0;
+    const uint32_t c = cbase, qs = kstep_q, rs = kstep_r;
+    uint32_t q = kq, rr = kr, done = 0;
     for (;;) {
       const uint64_t lim = stop < sec_bound ? stop : sec_bound;
       const uint64_t room64 = lim - 1u - T;
@@ -524,9 +570,8 @@ struct Sim {
         const uint64_t words = (uint64_t)n * B;
         ticks += n;
         T += used;
-        K += words;
         words_out += words;
-        if (win) win_words_out += words;
+        if (win_now) win_words_out += words;
         if (signal == BELLMAN_SIG_TBT) {
           acc_sum += (uint64_t)B * used;
           acc_cnt += (uint32_t)words;
@@ -534,47 +579,42 @@ struct Sim {
         done += n;
       }
       if (done == nmax) break;
-      const uint64_t tnext = T + (c + q);  // end of the next iteration (q = kv K / 1000 now)
+      const uint64_t tnext = T + (c + q);  // end of the next iteration
       if (tnext >= stop || tnext < sec_bound) break;
       roll_second(tnext);  // the next end opens a new second: ingest the closed one here
     }
+    kq = q;
+    kr = rr;
   }
 
   // ------------------------------------------------------------------ a4
   __device__ __forceinline__ void start_iteration() {
     const uint64_t Tn = T;
-    const uint32_t c = ticks;  // index of the new iteration
-    if (n_ready == 0) {  // same batch as the previous iteration: no joiners
-      const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (B > knee ? B - knee : 0u) + ((uint64_t)kv * K) / 1000u;
-      iter_d = d;
-      iter_B = B;
-      iter_align = 0;
-      iter_end = Tn + d;
-      busy = 1;
-      ticks++;
-      return;
-    }
-    uint32_t jn = 0xffffffffu;
-    uint64_t kadd = 0, al = 0;
+    uint64_t align = 0;
+    if (n_ready) {
+      const uint32_t c = ticks;  // index of the new iteration
+      uint32_t jn = 0xffffffffu, kadd = 0;
+      uint64_t al = 0;
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (sph[s] == PH_READY) {
-        sph[s] = PH_DEC;
-        sdn[s] = c + sR[s] - 2u;  // words 2..R at the ends of iterations c..c+R-2
-        al += Tn - sp[s];
-        kadd += (uint64_t)sin[s] + 1u;
-        jn = min(jn, sdn[s]);
+      for (int s = 0; s < 2; ++s) {
+        if (sph[s] == PH_READY) {
+          sph[s] = PH_DEC;
+          sdn[s] = c + sR[s] - 2u;  // words 2..R at the ends of iterations c..c+R-2
+          al += Tn - sp[s];
+          kadd += sin[s] + 1u;
+          jn = min(jn, sdn[s]);
+        }
       }
+      align = warp_sum_split(al);
+      const uint32_t mj = __reduce_min_sync(FULL, jn);
+      if (mj < next_done) next_done = mj;
+      kv_add((uint64_t)kv * __reduce_add_sync(FULL, kadd));
+      B += n_ready;
+      n_ready = 0;
+      batch_changed();
     }
-    const uint64_t align = warp_sum_split(al);
-    const uint32_t mj = __reduce_min_sync(FULL, jn);
-    if (mj < next_done) next_done = mj;
-    K += __reduce_add_sync(FULL, (uint32_t)kadd);
-    B += n_ready;
-    n_ready = 0;
-    const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (B > knee ? B - knee : 0u) + ((uint64_t)kv * K) / 1000u;
+    const uint32_t d = cbase + kq;
     iter_d = d;
-    iter_B = B;
     iter_align = align;
     iter_end = Tn + d;
     busy = 1;
@@ -588,6 +628,7 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
   const uint32_t lane = lane_id();
   const uint32_t chunk = nb / 32u;
   uint32_t csum = 0;
+#pragma unroll 1
   for (uint32_t b = 0; b < chunk; ++b) csum += hist[lane * chunk + b];
   uint32_t incl = csum;
 #pragma unroll
@@ -607,6 +648,7 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
     uint32_t res = 0;
     if (lane == L) {
       uint64_t cum = incl - csum;
+#pragma unroll 1
       for (uint32_t b = 0; b < chunk; ++b) {
         cum += hist[lane * chunk + b];
         if (cum >= k) {
@@ -635,12 +677,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
 
     // ---- a1: scenario decode
     Sim S;
-    S.sid = (uint32_t)sid;
+    S.lane = lane;
     S.k0 = sc.seed_index;
     S.wid_lo = (uint32_t)sc.wid;
     S.wid_hi = (uint32_t)(sc.wid >> 32);
     S.H = (uint64_t)sc.horizon_us;
-    S.mode = sc.mode;
     S.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
     S.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
     const bellman_profile pr = p.profs[sc.profile];
@@ -698,12 +739,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.T = 0;
     S.busy = 0;
     S.iter_end = INF;
-    S.iter_B = S.iter_d = S.iter_align = 0;
+    S.iter_d = 0;
+    S.iter_align = 0;
     S.ticks = 0;
     S.next_done = 0xffffffffu;
     S.next_pf = INF;
     S.n_ready = S.B = S.in_sys = 0;
-    S.K = 0;
+    S.kq = S.kr = 0;
+    S.batch_changed();
+    S.update_window();
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       S.sa[s] = S.sp[s] = 0;
@@ -723,7 +767,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.gen_tau = 0;
     S.buf_h = S.buf_n = 0;
     S.buf_a = 0;
-    S.buf_attr = 0;
+    S.buf_in = S.buf_U = S.buf_P = 0;
+    S.buf_fc = 0;
     S.buf_j = 0;
     S.last_j = 0;
     S.admitted = S.served = S.rewritten = S.slo_viol = S.win_served = 0;
@@ -739,23 +784,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.refill(p);
 
     // ---- the event/tick loop (a4-a7)
+#ifdef BELLMAN_PROFILE_COUNTERS
+    uint32_t prof_[16] = {0};
+#endif
     bool finished = false;
     for (;;) {
       uint64_t tn;
+      PROF(0);
       if (S.busy) {
         // prefill ends strictly inside the running iteration only emit first
         // words / R=1 completions (time-stamped at p); process them in order
         // before the iteration end (same-instant ends go after E1, R7).
         while (S.next_pf < S.iter_end && S.next_pf < S.H) {
-          S.T = S.next_pf;
-          S.roll_second(S.T);
+          PROF(1);
+          S.advance(S.next_pf);
           S.prefill_end(h);
         }
         tn = S.iter_end;
       } else {
-        uint64_t t_arr = INF;
-        if (S.in_sys < S.maxb && S.buf_h < S.buf_n) t_arr = S.head_a();
-        tn = S.next_pf < t_arr ? S.next_pf : t_arr;
+        tn = S.next_pf;
+        if (S.in_sys < S.maxb && S.head_t < tn) tn = S.head_t;
         if (tn == INF) {
           finished = true;
           break;
@@ -767,21 +815,42 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
         const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = tn < S.w1 ? tn : S.w1;
         if (hi > lo) S.win_idle += hi - lo;
       }
-      S.T = tn;
-      S.roll_second(tn);
-      if (S.busy) S.iteration_end(h);
-      if (S.next_pf == tn) S.prefill_end(h);
-      if (!S.busy) {
+      S.advance(tn);
+      if (S.busy) {
+        PROF(2);
+        if (S.ticks - 1u == S.next_done) PROF(3);
+        S.iteration_end(h);
+      }
+      if (S.next_pf == tn) {
+        PROF(4);
+        S.prefill_end(h);
+      }
+      // the decode loop is idle here: admission point (R7), then the next iteration
+      if (S.in_sys < S.maxb && S.head_t <= tn) {
+        PROF(5);
         S.admit(p, h);
-        if (S.n_ready + S.B > 0) {
-          if (S.n_ready == 0) S.leap(p);
-          S.start_iteration();
+      }
+      if (S.n_ready + S.B > 0) {
+        if (S.n_ready == 0) {
+          PROF(6);
+          const uint32_t t0_ = S.ticks;
+          S.leap();
+#ifdef BELLMAN_PROFILE_COUNTERS
+          prof_[7] += S.ticks - t0_;
+#endif
+        } else {
+          PROF(8);
         }
+        S.start_iteration();
       }
     }
 
+#ifdef BELLMAN_PROFILE_COUNTERS
+    if (lane == 0)
+      for (int i = 0; i < 16; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
+#endif
     // ---- termination (R20)
-    const uint64_t end = (S.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
+    const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
     if (S.in_sys == 0) {
       S.idle += end - S.T;
       const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = end < S.w1 ? end : S.w1;
@@ -920,6 +989,12 @@ __global__ void bellman_calibrate_kernel(const Params p, uint32_t n_slots) {
 }
 
 }  // namespace bellman
+
+#ifdef BELLMAN_PROFILE_COUNTERS
+extern "C" int bellman_debug_prof(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16);
+}
+#endif
 
 int bellman_tick_grid(int device) {
   int sms = 0, per_sm = 0;

@@ -1,0 +1,44 @@
+"""Development tool: build the tick kernel with BELLMAN_PROFILE_COUNTERS into a
+separate library, run C2 once and print event-trip counters.  Never used by
+the product path, the tests or the bench."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2510_15330_b200 import _abi, build as B  # noqa: E402
+
+NAMES = ["trips", "deferred_prefill", "iter_end", "iter_end_with_completion", "prefill_end_event", "admit",
+         "leap_calls", "leaped_ticks", "join_starts"]
+
+
+def main():
+    out = os.path.join(ROOT, "gpurun_out", "libbellman_sim_prof.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [B.nvcc()] + [f for f in B.NVCC_FLAGS if f != "-v" and f != "-Xptxas"] + \
+          ["-DBELLMAN_PROFILE_COUNTERS", "-o", out] + [os.path.join(B.CSRC, s) for s in B.SOURCES]
+    subprocess.run(cmd, check=True)
+    _abi.LIB_PATH = out
+    import workloads as W
+    from paper_2510_15330_b200 import Simulator
+
+    cols = W.config_c2().columns()
+    sim = Simulator(cols)
+    sim.run()
+    torch.cuda.synchronize()
+    st = sim.stats()
+    lib = _abi.lib()
+    vals = np.zeros(16, dtype=np.uint64)
+    assert lib.bellman_debug_prof(ctypes.c_void_p(vals.ctypes.data)) == 0
+    print("ticks", int(st["ticks"].sum()), "admitted", int(st["admitted"].sum()), "served", int(st["served"].sum()))
+    for n, v in zip(NAMES, vals):
+        print(f"{n:26s} {int(v):12d}")
+
+
+if __name__ == "__main__":
+    main()

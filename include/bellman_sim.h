@@ -64,7 +64,8 @@ enum { BELLMAN_MODE_CUTOFF = 0, BELLMAN_MODE_DRAIN = 1 };
 #define BELLMAN_TABLE_N 4096    /* quantile-table entries, indexed by (u32 >> 20) */
 #define BELLMAN_HIST_LAT 896    /* latency bins: exact ms < 32, then 32 per octave */
 #define BELLMAN_HIST_R 512      /* r bins of 10 bp */
-#define BELLMAN_SEG_HIST_WORDS (2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R) /* u64 per segment */
+#define BELLMAN_HIST_Q 201      /* similarity-score bins of 0.5 point (NEXT-2) */
+#define BELLMAN_SEG_HIST_WORDS (2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + 2 * BELLMAN_HIST_Q) /* u64 per segment */
 #define BELLMAN_MAX_BATCH 64
 
 /* One knot of a piecewise-linear arrival-rate trace ("distinct phases when
@@ -118,6 +119,15 @@ typedef struct {
   const int32_t *noise;    /* predictor error in words, |.| <= 65535 */
   const int32_t *fcomp_q16;/* compliance factor, Q16, 0..2^18 */
   int64_t poly_q16[3];     /* realized = poly(N) * fcomp; identity = {0, 65536, 0}; |a_k| <= 2^40 */
+  /* Quality model (NEXT-2): every admitted request is
+   * scored against its unbounded length U: reduction red = (U - R) / U;
+   * inactive (r = 0): base = quality[0]; active: quality[1] for red <=
+   * quality[3] bp, quality[2] for red >= quality[4] bp, linear in between
+   * (floored); score = clamp(base + qnoise[u >> 20], 0, 10000) centi-points,
+   * u = 4th word of the request's tag-1 Philox block. */
+  const int32_t *qnoise;   /* centi-points, |.| <= 2047 */
+  uint32_t quality[5];     /* inactive, active, floor (centi-points), safe_bp, end_bp */
+  uint32_t _pad;
 } bellman_models;
 
 typedef struct {
@@ -128,8 +138,30 @@ typedef struct {
   int64_t horizon_us;  /* cutoff H, or the cap of a drain run */
   int64_t w0_us, w1_us;/* window [w0, w1) for the win_* counters (130-500 s) */
   uint32_t calib_src;  /* OFF scenario whose series calibrates this one, or BELLMAN_NONE */
-  uint32_t record;     /* 1: keep this scenario's per-second signal series */
+  uint32_t record;     /* bit 0: keep the per-second signal series (a10 source);
+                          bit 1: debug record mode — per-second rows + controller log (NEXT-1) */
 } bellman_scenario; /* 64 bytes */
+
+#define BELLMAN_RECORD_SIGNAL 0x1u
+#define BELLMAN_RECORD_SECONDS 0x2u
+
+/* Per-second aggregate of a debug-recorded scenario.
+ * Attribution: arrivals to their arrival second, queueing and input
+ * words to the admission second, TTFT and first words to the first-token
+ * second, decode words and their TBT gaps to the emission second, E2E to the
+ * completion second, idle time split over the seconds it overlaps.  Rows cover
+ * seconds 0 .. floor(end_us / 1e6). */
+typedef struct {
+  uint32_t arrivals, admitted, first_tokens, completions, tbt_count, idle_us, words_in, words_out;
+  uint64_t sum_queue_us, sum_ttft_us, sum_e2e_us, sum_tbt_us;
+} bellman_second_row; /* 64 bytes */
+
+/* One controller ingest ("second, ma_tbt_ms, r, active"): the moving
+ * average is A / k over the last k samples; r and active after the update. */
+typedef struct {
+  uint32_t second, sample, k, r_bp, active, _pad;
+  uint64_t A;
+} bellman_ctrl_row; /* 32 bytes */
 
 typedef struct {
   const bellman_knot *knots;
@@ -158,7 +190,9 @@ typedef struct {
   uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
   uint32_t segment, _pad0;
   double energy_j, win_energy_j;
-  uint64_t _reserved[2];
+  /* NEXT-2: nearest-rank median similarity (0.5-point bin lower edge, centi-points)
+   * of rewritten (active) and not rewritten (inactive) admissions, and their counts */
+  uint32_t sim_active_p50, sim_inactive_p50, scored_active, scored_inactive;
 } bellman_scenario_stats;
 
 typedef struct bellman_sim bellman_sim; /* opaque */
@@ -187,10 +221,20 @@ bellman_status bellman_sim_stats(bellman_sim *sim, bellman_scenario_stats *dst, 
                                  uint64_t count, int dst_is_device, void *stream);
 
 /* Copy the per-segment histograms, n_segments x BELLMAN_SEG_HIST_WORDS uint64:
- * [E2E 896 | TTFT 896 | r 512] integer counts merged over the segment's runs. */
+ * [E2E 896 | TTFT 896 | r 512 | similarity active 201 | inactive 201] integer
+ * counts merged over the segment's runs. */
 bellman_status bellman_sim_segment_hist(bellman_sim *sim, uint64_t *dst, int dst_is_device, void *stream);
 
-/* Zero all summary records and segment histograms. */
+/* Debug record mode (scenario.record & BELLMAN_RECORD_SECONDS): copy the
+ * per-second rows and the controller log of scenario `id` to HOST buffers
+ * (synchronous on `stream`).  *n_rows / *n_ctrl receive the counts written by
+ * the last run (rows beyond cap are dropped).  BELLMAN_ESTATE if the scenario
+ * is not debug-recorded. */
+bellman_status bellman_sim_series(bellman_sim *sim, uint64_t id, bellman_second_row *rows, uint64_t cap_rows,
+                                  uint64_t *n_rows, bellman_ctrl_row *ctrl, uint64_t cap_ctrl, uint64_t *n_ctrl,
+                                  void *stream);
+
+/* Zero all summary records, segment histograms and recorded series. */
 bellman_status bellman_sim_reset(bellman_sim *sim, void *stream);
 
 /* Kernel launches issued by the most recent bellman_sim_run. */

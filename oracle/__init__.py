@@ -49,7 +49,7 @@ class Inputs(C.Structure):
         ("ctrl_t1", u32p), ("ctrl_t2", u32p), ("ctrl_slo_us", u32p), ("ctrl_calibrated", u32p),
         ("ctrl_nrungs", u32p), ("ctrl_rungs", u32p),
         ("tab_L", i32p), ("tab_I", i32p), ("tab_fvar", i32p), ("tab_noise", i32p), ("tab_fcomp", i32p),
-        ("poly_q16", i64p),
+        ("poly_q16", i64p), ("tab_qnoise", i32p), ("quality", u32p),
         ("sc_seed", u32p), ("sc_wid", u64p),
         ("sc_trace", u32p), ("sc_profile", u32p), ("sc_ctrl", u32p), ("sc_segment", u32p), ("sc_mode", u32p),
         ("sc_horizon", i64p), ("sc_w0", i64p), ("sc_w1", i64p),
@@ -60,7 +60,7 @@ class Inputs(C.Structure):
 
 class Request(C.Structure):
     _fields_ = [("a_us", C.c_uint64), ("j", C.c_uint32), ("L", C.c_uint32), ("input", C.c_uint32),
-                ("U", C.c_uint32), ("P", C.c_uint32), ("fcomp_q16", C.c_int32)]
+                ("U", C.c_uint32), ("P", C.c_uint32), ("fcomp_q16", C.c_int32), ("qnoise", C.c_int32)]
 
 
 class Profile(C.Structure):
@@ -77,7 +77,7 @@ class Ctrl(C.Structure):
 
 class RunCfg(C.Structure):
     _fields_ = [("mode", C.c_uint32), ("horizon_us", C.c_int64), ("w0_us", C.c_int64), ("w1_us", C.c_int64),
-                ("poly_q16", C.c_int64 * 3), ("record", C.c_uint32)]
+                ("poly_q16", C.c_int64 * 3), ("quality", C.c_uint32 * 5), ("record", C.c_uint32)]
 
 
 RESULT_U64 = ["ticks", "candidates", "arrivals", "admitted", "served", "rewritten",
@@ -87,16 +87,20 @@ RESULT_U64 = ["ticks", "candidates", "arrivals", "admitted", "served", "rewritte
 RESULT_U32 = ["e2e_p50_ms", "e2e_p99_ms", "ttft_p50_ms", "ttft_p99_ms", "median_r_bp",
               "t1", "t2", "activations", "first_act_s", "last_deact_s", "active_ingests", "flags"]
 RESULT_F64 = ["energy_j", "win_energy_j"]
+RESULT_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive"]
+HIST_Q = 201
 RESULT_EXTRA = ["e2e_exact_p50_us", "e2e_exact_p99_us", "ttft_exact_p50_us", "ttft_exact_p99_us",
                 "int_system_us", "int_queue_us", "sum_sojourn_us", "tbt_samples", "tbt_sum_us", "tbt_max_us"]
-SUMMARY_FIELDS = RESULT_U64 + RESULT_U32 + RESULT_F64
+SUMMARY_FIELDS = RESULT_U64 + RESULT_U32 + RESULT_F64 + RESULT_Q
 
 
 class Result(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in RESULT_U64] + [(n, C.c_uint32) for n in RESULT_U32] + \
-               [(n, C.c_double) for n in RESULT_F64] + [(n, C.c_uint64) for n in RESULT_EXTRA] + \
+               [(n, C.c_double) for n in RESULT_F64] + [(n, C.c_uint32) for n in RESULT_Q] + \
+               [(n, C.c_uint64) for n in RESULT_EXTRA] + \
                [("hist_e2e", C.c_uint32 * HIST_LAT), ("hist_ttft", C.c_uint32 * HIST_LAT),
-                ("hist_r", C.c_uint32 * HIST_R), ("n_series", C.c_uint32)]
+                ("hist_r", C.c_uint32 * HIST_R), ("hist_q_active", C.c_uint32 * HIST_Q),
+                ("hist_q_inactive", C.c_uint32 * HIST_Q), ("n_series", C.c_uint32)]
 
 
 class ReqLog(C.Structure):
@@ -109,10 +113,23 @@ class CtrlLog(C.Structure):
                 ("active", C.c_uint32), ("_pad", C.c_uint32), ("A", C.c_uint64)]
 
 
+SECOND_ROW = np.dtype([("arrivals", "<u4"), ("admitted", "<u4"), ("first_tokens", "<u4"), ("completions", "<u4"),
+                       ("tbt_count", "<u4"), ("idle_us", "<u4"), ("words_in", "<u4"), ("words_out", "<u4"),
+                       ("sum_queue_us", "<u8"), ("sum_ttft_us", "<u8"), ("sum_e2e_us", "<u8"),
+                       ("sum_tbt_us", "<u8")])
+
+
+class SecondRow(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in ("arrivals", "admitted", "first_tokens", "completions", "tbt_count",
+                                           "idle_us", "words_in", "words_out")] + \
+               [(n, C.c_uint64) for n in ("sum_queue_us", "sum_ttft_us", "sum_e2e_us", "sum_tbt_us")]
+
+
 class Log(C.Structure):
     _fields_ = [("req", P(ReqLog)), ("gaps", u64p), ("cap_gaps", C.c_uint64), ("n_gaps", C.c_uint64),
                 ("ctrl", P(CtrlLog)), ("cap_ctrl", C.c_uint64), ("n_ctrl", C.c_uint64),
-                ("series", u32p), ("cap_series", C.c_uint64)]
+                ("series", u32p), ("cap_series", C.c_uint64),
+                ("rows", P(SecondRow)), ("cap_rows", C.c_uint64), ("n_rows", C.c_uint64)]
 
 
 _lib = None
@@ -141,6 +158,8 @@ def lib():
         L.orc_map_rate.argtypes = [C.c_uint64, C.c_uint32, P(Ctrl)]
         L.orc_map_rate.restype = C.c_uint32
         L.orc_run_batch.argtypes = [P(Inputs), u64p, C.c_uint64, P(Result), C.c_int]
+        L.orc_similarity.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int32, u32p]
+        L.orc_similarity.restype = C.c_uint32
         _lib = L
     return _lib
 
@@ -206,7 +225,7 @@ class Bound:
              ("ctrl_t1", np.uint32), ("ctrl_t2", np.uint32), ("ctrl_slo_us", np.uint32),
              ("ctrl_calibrated", np.uint32), ("ctrl_nrungs", np.uint32), ("ctrl_rungs", np.uint32),
              ("tab_L", np.int32), ("tab_I", np.int32), ("tab_fvar", np.int32), ("tab_noise", np.int32),
-             ("tab_fcomp", np.int32), ("poly_q16", np.int64),
+             ("tab_fcomp", np.int32), ("poly_q16", np.int64), ("tab_qnoise", np.int32), ("quality", np.uint32),
              ("sc_seed", np.uint32), ("sc_wid", np.uint64), ("sc_trace", np.uint32), ("sc_profile", np.uint32),
              ("sc_ctrl", np.uint32), ("sc_segment", np.uint32), ("sc_mode", np.uint32),
              ("sc_horizon", np.int64), ("sc_w0", np.int64), ("sc_w1", np.int64),
@@ -233,6 +252,8 @@ def _result_dict(r: Result, hist=True) -> dict:
         d["hist_e2e"] = np.frombuffer(r.hist_e2e, dtype=np.uint32).copy()
         d["hist_ttft"] = np.frombuffer(r.hist_ttft, dtype=np.uint32).copy()
         d["hist_r"] = np.frombuffer(r.hist_r, dtype=np.uint32).copy()
+        d["hist_q_active"] = np.frombuffer(r.hist_q_active, dtype=np.uint32).copy()
+        d["hist_q_inactive"] = np.frombuffer(r.hist_q_inactive, dtype=np.uint32).copy()
     return d
 
 
@@ -242,17 +263,22 @@ def arrivals(cols_or_bound, sid: int) -> np.ndarray:
     buf = (Request * max(n, 1))()
     m = lib().orc_arrivals(C.byref(b.st), sid, buf, n)
     assert m == n
-    dt = np.dtype([("a_us", "<u8"), ("j", "<u4"), ("L", "<u4"), ("input", "<u4"), ("U", "<u4"),
-                   ("P", "<u4"), ("fcomp_q16", "<i4")])
+    dt = np.dtype(Request)  # field layout and padding of orc_request
     return np.frombuffer(buf, dtype=dt, count=n).copy()
 
 
-def run_scenario(cols_or_bound, sid: int, hist=True, ctrl_log_cap=0, series_cap=0) -> dict:
+def run_scenario(cols_or_bound, sid: int, hist=True, ctrl_log_cap=0, series_cap=0, rows_cap=0) -> dict:
+    """One scenario.  ctrl_log_cap / series_cap / rows_cap > 0 return the
+    controller log, the recorded signal series and (record & 2) the per-second rows."""
     b = cols_or_bound if isinstance(cols_or_bound, Bound) else Bound(cols_or_bound)
     r = Result()
     log = Log()
     clog = (CtrlLog * max(ctrl_log_cap, 1))()
     ser = (C.c_uint32 * max(series_cap, 1))()
+    rws = (SecondRow * max(rows_cap, 1))()
+    if rows_cap:
+        log.rows = rws
+        log.cap_rows = rows_cap
     if ctrl_log_cap:
         log.ctrl = clog
         log.cap_ctrl = ctrl_log_cap
@@ -268,6 +294,9 @@ def run_scenario(cols_or_bound, sid: int, hist=True, ctrl_log_cap=0, series_cap=
                          for c in clog[:min(log.n_ctrl, ctrl_log_cap)]]
     if series_cap:
         d["series"] = np.frombuffer(ser, dtype=np.uint32, count=min(r.n_series, series_cap)).copy()
+    if rows_cap:
+        d["rows"] = np.frombuffer(rws, dtype=SECOND_ROW, count=min(log.n_rows, rows_cap)).copy()
+    d["n_ctrl"] = log.n_ctrl
     return d
 
 
@@ -284,8 +313,17 @@ def run_batch(cols_or_bound, sids=None, nthreads=None) -> list:
     return [_result_dict(res[i], hist=False) for i in range(len(sids))]
 
 
+QUALITY_DEFAULT = (8800, 8700, 6500, 2000, 4000)
+
+
+def similarity(U: int, R: int, active: bool, noise: int = 0, q=QUALITY_DEFAULT) -> int:
+    qq = (C.c_uint32 * 5)(*q)
+    return lib().orc_similarity(U, R, 1 if active else 0, noise, qq)
+
+
 def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_us=10**12,
-             w0_us=0, w1_us=2**62, poly_q16=(0, 65536, 0), record=0, gap_cap=100000, ctrl_log_cap=10000):
+             w0_us=0, w1_us=2**62, poly_q16=(0, 65536, 0), record=0, gap_cap=100000, ctrl_log_cap=10000,
+             quality=QUALITY_DEFAULT):
     """Run the DES on an explicit request list (hand fixtures, brute-force pins).
 
     ``requests``: iterable of dicts with a_us, input, U and optionally L, P, fcomp_q16, j.
@@ -295,12 +333,13 @@ def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_
     rq = (Request * max(n, 1))()
     for i, q in enumerate(reqs):
         rq[i] = Request(int(q["a_us"]), int(q.get("j", i)), int(q.get("L", q["U"])), int(q["input"]),
-                        int(q["U"]), int(q.get("P", q.get("L", q["U"]))), int(q.get("fcomp_q16", 65536)))
+                        int(q["U"]), int(q.get("P", q.get("L", q["U"]))), int(q.get("fcomp_q16", 65536)),
+                        int(q.get("qnoise", 0)))
     pr = Profile(profile["t0_us"], profile["knee"], profile["slope_us"], profile.get("kv_ns_per_word", 0),
                  profile["max_batch"], profile["prefill_ns_per_word"], profile.get("e_in", 0.05),
                  profile.get("e_out", 0.5), profile.get("p_idle", 300.0))
     c = ctrl if ctrl is not None else make_ctrl()
-    cfg = RunCfg(mode, horizon_us, w0_us, w1_us, (C.c_int64 * 3)(*poly_q16), record)
+    cfg = RunCfg(mode, horizon_us, w0_us, w1_us, (C.c_int64 * 3)(*poly_q16), (C.c_uint32 * 5)(*quality), record)
     r = Result()
     log = Log()
     reqlog = (ReqLog * max(n, 1))()

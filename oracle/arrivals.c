@@ -79,6 +79,7 @@ int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint6
         int64_t P = (int64_t)r->L + noise;
         r->P = (uint32_t)(P < 1 ? 1 : P);
         r->fcomp_q16 = (int32_t)fcomp;
+        r->qnoise = in->tab_qnoise[v[3] >> 20]; /* similarity noise (NEXT-2) */
       }
       count++;
       if (cap && (uint64_t)count >= cap) return count; /* arrival cap (R28) */

@@ -40,6 +40,7 @@ enum { ORC_FLAG_TRUNCATED = 1, ORC_FLAG_DEGENERATE_CALIB = 2 };
 #define ORC_NONE 0xFFFFFFFFu
 #define ORC_HIST_LAT 896 /* log-linear ms bins, 32 per octave (a9) */
 #define ORC_HIST_R 512   /* 10 bp bins of r */
+#define ORC_HIST_Q 201   /* similarity-score bins of 0.5 point (NEXT-2) */
 
 /* ---- column inputs, exactly as workloads.Workload.columns() builds them ---- */
 typedef struct {
@@ -53,6 +54,8 @@ typedef struct {
   const uint32_t *ctrl_rungs; /* [n_ctrl][8] */
   const int32_t *tab_L, *tab_I, *tab_fvar, *tab_noise, *tab_fcomp; /* [4096] each */
   const int64_t *poly_q16;                                          /* [3] */
+  const int32_t *tab_qnoise;  /* [4096] similarity noise, centi-points (NEXT-2) */
+  const uint32_t *quality;    /* [5] inactive, active, floor (centi-points), safe, end (bp) */
   const uint32_t *sc_seed;
   const uint64_t *sc_wid;
   const uint32_t *sc_trace, *sc_profile, *sc_ctrl, *sc_segment, *sc_mode;
@@ -70,6 +73,7 @@ typedef struct {
   uint32_t U;          /* realized unbounded output words */
   uint32_t P;          /* predicted output words */
   int32_t fcomp_q16;   /* compliance factor */
+  int32_t qnoise;      /* similarity-score noise, centi-points (NEXT-2) */
 } orc_request;
 
 typedef struct {
@@ -86,7 +90,8 @@ typedef struct {
   uint32_t mode;
   int64_t horizon_us, w0_us, w1_us;
   int64_t poly_q16[3];
-  uint32_t record; /* keep the per-second signal series */
+  uint32_t quality[5]; /* similarity model (NEXT-2): inactive, active, floor, safe_bp, end_bp */
+  uint32_t record; /* bit 0: keep the per-second signal series; bit 1: per-second rows */
 } orc_run_cfg;
 
 typedef struct {
@@ -97,6 +102,7 @@ typedef struct {
   uint32_t e2e_p50_ms, e2e_p99_ms, ttft_p50_ms, ttft_p99_ms, median_r_bp;
   uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
   double energy_j, win_energy_j;
+  uint32_t sim_active_p50, sim_inactive_p50, scored_active, scored_inactive; /* NEXT-2, centi-points */
   /* ---- self-checks the GPU never computes ---- */
   uint64_t e2e_exact_p50_us, e2e_exact_p99_us, ttft_exact_p50_us, ttft_exact_p99_us;
   uint64_t int_system_us;  /* integral of (queued + in_system) dt, µs*requests */
@@ -104,6 +110,7 @@ typedef struct {
   uint64_t sum_sojourn_us; /* sum over completed of (completion - arrival) */
   uint64_t tbt_samples, tbt_sum_us, tbt_max_us;
   uint32_t hist_e2e[ORC_HIST_LAT], hist_ttft[ORC_HIST_LAT], hist_r[ORC_HIST_R];
+  uint32_t hist_q_active[ORC_HIST_Q], hist_q_inactive[ORC_HIST_Q];
   uint32_t n_series; /* per-second signal samples written to series[] (record mode) */
 } orc_result;
 
@@ -118,6 +125,20 @@ typedef struct {
   uint64_t A;
 } orc_ctrl_log;
 
+/* Per-second aggregate (NEXT-1; attribution S:382): each
+ * event counts toward the second of its own timestamp. */
+typedef struct {
+  uint32_t arrivals;     /* arrivals in the second (rps_in) */
+  uint32_t admitted;     /* admissions (queueing attributed to the admission second) */
+  uint32_t first_tokens; /* first words (TTFT attributed to the first-token second) */
+  uint32_t completions;  /* completions (E2E attributed to the completion second) */
+  uint32_t tbt_count;    /* decode words emitted (TBT samples) */
+  uint32_t idle_us;      /* time in the second with nothing in the system */
+  uint32_t words_in;     /* input words admitted */
+  uint32_t words_out;    /* words emitted (first + decode) */
+  uint64_t sum_queue_us, sum_ttft_us, sum_e2e_us, sum_tbt_us;
+} orc_second_row;
+
 typedef struct {
   orc_req_log *req;    /* [n_requests] or NULL */
   uint64_t *gaps;      /* pairs (request index, gap µs), capacity cap_gaps pairs, or NULL */
@@ -126,6 +147,8 @@ typedef struct {
   uint64_t cap_ctrl, n_ctrl;
   uint32_t *series;    /* per-second samples (record mode), capacity cap_series */
   uint64_t cap_series;
+  orc_second_row *rows; /* per-second rows (record & 2), capacity cap_rows */
+  uint64_t cap_rows, n_rows;
 } orc_log;
 
 /* Philox4x32-10 (Salmon et al., SC'11), key = (k0, k1), counter c[4]. */
@@ -147,7 +170,9 @@ int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint6
 int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof,
                  const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log);
 
-/* Full scenario: arrivals + (calibration pass a10) + simulation. */
+/* Full scenario: arrivals + (calibration pass a10) + simulation.  With
+ * log->ctrl / log->rows given, the controller log and (record & 2) the
+ * per-second rows are written. */
 int orc_run_scenario(const orc_inputs *in, uint64_t sid, orc_result *res, orc_log *log);
 
 /* Nearest-rank percentile of a sample list, 0 < p <= 100 (p = 0 -> min). */
@@ -155,6 +180,10 @@ uint32_t orc_percentile_u32(const uint32_t *v, uint64_t n, uint32_t p);
 
 /* Threshold calibration (a10): 0 ok, 1 insufficient, 2 degenerate. */
 int orc_calibrate(const uint32_t *series, uint64_t n, uint32_t *t1, uint32_t *t2);
+
+/* Similarity score (NEXT-2) in centi-points for a request whose
+ * unbounded length is U and realized length R, rewritten (active) or not. */
+uint32_t orc_similarity(uint32_t U, uint32_t R, int active, int32_t noise, const uint32_t q[5]);
 
 /* Controller law as a pure function (a6): r in bp for a window sum A over k samples. */
 uint32_t orc_map_rate(uint64_t A, uint32_t k, const orc_ctrl *c);

@@ -163,6 +163,29 @@ uint32_t orc_map_rate(uint64_t A, uint32_t k, const orc_ctrl *c) {
   return (uint32_t)r;
 }
 
+/* NEXT-2 similarity model (P:193 87 % active / 88 %
+ * inactive; P:102 floor 65 %; P:106 safe window < 20 %).  Reduction vs the
+ * request's unbounded length: red = (U - R) / U.  Inactive: base = q[0].
+ * Active: base = q[1] for red <= safe, the floor q[2] for red >= end, linear in
+ * between (floored to a centi-point); score = clamp(base + noise, 0, 10000). */
+uint32_t orc_similarity(uint32_t U, uint32_t R, int active, int32_t noise, const uint32_t q[5]) {
+  int64_t base;
+  if (!active) {
+    base = q[0];
+  } else {
+    /* red in bp as the exact rational num / den */
+    int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = (int64_t)U;
+    if (num <= (int64_t)q[3] * den) base = q[1];
+    else if (num >= (int64_t)q[4] * den) base = q[2];
+    else base = (int64_t)q[1] - ((int64_t)(q[1] - q[2]) * (num - (int64_t)q[3] * den)) /
+                                    ((int64_t)(q[4] - q[3]) * den);
+  }
+  int64_t s = base + noise;
+  if (s < 0) s = 0;
+  if (s > 10000) s = 10000;
+  return (uint32_t)s;
+}
+
 /* floor(x / 2^32) for signed 128-bit x */
 static __int128 floor_div_2p32(__int128 x) {
   __int128 d = (__int128)1 << 32;
@@ -279,10 +302,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint64_t *sec_e2e_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_e2e_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_slo_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
   cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
   if (!rs || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
-      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt)
+      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || ((cfg->record & 2) && !rows))
     goto out;
   if (cs.law == ORC_LAW_CONST) cs.r = ctrl->r_const_bp; /* S:320-326 constant policy */
 
@@ -308,7 +332,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       else { cnt = sec_e2e_cnt[next_sec]; sum = 1000 * sec_slo_cnt[next_sec]; }          \
       if (cnt == 0) continue; /* a second with no samples is a gap */     \
       uint32_t x = (uint32_t)(sum / cnt);                                                \
-      if (cfg->record) {                                                                 \
+      if (cfg->record & 1) {                                                             \
         if (log && log->series && n_series < log->cap_series) log->series[n_series] = x; \
         n_series++;                                                                      \
       }                                                                                  \
@@ -326,6 +350,9 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       if (in_sys == 0) {
         res->idle_us += dt;
         res->win_idle_us += overlap(T_prev, T, cfg->w0_us, cfg->w1_us);
+        if (rows)
+          for (uint64_t s = T_prev / US; s * US < T && s < n_sec; ++s)
+            rows[s].idle_us += (uint32_t)overlap(T_prev, T, (int64_t)(s * US), (int64_t)((s + 1) * US));
       }
       res->int_system_us += (nq + in_sys) * dt;
       res->int_queue_us += nq * dt;
@@ -354,6 +381,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           rs[m].last_tok = T;
           rs[m].emitted++;
           res->words_out++;
+          if (rows) {
+            rows[s_idx].tbt_count++;
+            rows[s_idx].sum_tbt_us += gap;
+            rows[s_idx].words_out++;
+          }
           if (in_window(T, cfg)) res->win_words_out++;
           if (rs[m].emitted == rs[m].R) { /* completes: E2E = completion - arrival */
             uint64_t e2e = T - req[m].a_us;
@@ -369,6 +401,10 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
             sec_e2e_sum[s_idx] += e2e;
             sec_e2e_cnt[s_idx] += 1;
             if (e2e > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }
+            if (rows) {
+              rows[s_idx].completions++;
+              rows[s_idx].sum_e2e_us += e2e;
+            }
           } else {
             rs[m].state = RS_READY;
             ready[n_ready++] = m;
@@ -388,6 +424,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         res->sum_ttft_us += ttft;
         ttft_v[n_ttft++] = ttft;
         res->hist_ttft[orc_lat_bin(ttft / 1000)]++;
+        if (rows) {
+          rows[s_idx].first_tokens++;
+          rows[s_idx].sum_ttft_us += ttft;
+          rows[s_idx].words_out++;
+        }
         if (rs[m].R == 1) { /* R9: realized length 1 completes at prefill end */
           uint64_t e2e = ttft;
           rs[m].done = T;
@@ -402,6 +443,10 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           sec_e2e_sum[s_idx] += e2e;
           sec_e2e_cnt[s_idx] += 1;
           if (e2e > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }
+          if (rows) {
+            rows[s_idx].completions++;
+            rows[s_idx].sum_e2e_us += e2e;
+          }
         } else {
           rs[m].state = RS_READY;
           ready[n_ready++] = m;
@@ -411,6 +456,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         rs[m].state = RS_QUEUED;
         queue[q_tail++] = m;
         res->arrivals++;
+        if (rows) rows[s_idx].arrivals++;
         res->candidates = (uint64_t)req[m].j + 1;
       }
     }
@@ -431,9 +477,21 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         res->sum_queue_us += T - req[m].a_us;
         res->words_in += req[m].input;
         if (in_window(T, cfg)) res->win_words_in += req[m].input;
+        if (rows) {
+          uint64_t sa = T / US;
+          rows[sa].admitted++;
+          rows[sa].sum_queue_us += T - req[m].a_us;
+          rows[sa].words_in += req[m].input;
+        }
         if (r > 0) {
           res->rewritten++;
           res->hist_r[r / 10 < ORC_HIST_R ? r / 10 : ORC_HIST_R - 1]++;
+        }
+        { /* NEXT-2: score the admitted request against its unbounded counterpart */
+          uint32_t sc = orc_similarity(req[m].U, rs[m].R, r > 0, req[m].qnoise, cfg->quality);
+          uint32_t qb = sc / 50 < ORC_HIST_Q ? sc / 50 : ORC_HIST_Q - 1;
+          if (r > 0) { res->hist_q_active[qb]++; res->scored_active++; }
+          else { res->hist_q_inactive[qb]++; res->scored_inactive++; }
         }
         if (heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m})) goto out;
       }
@@ -465,6 +523,9 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
     if (in_sys == 0) {
       res->idle_us += dt;
       res->win_idle_us += overlap(T_prev, end, cfg->w0_us, cfg->w1_us);
+      if (rows)
+        for (uint64_t s = T_prev / US; s * US < end && s < n_sec; ++s)
+          rows[s].idle_us += (uint32_t)overlap(T_prev, end, (int64_t)(s * US), (int64_t)((s + 1) * US));
     }
     res->int_system_us += (nq + in_sys) * dt;
     res->int_queue_us += nq * dt;
@@ -517,6 +578,21 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         if (cum >= k) { res->median_r_bp = b * 10; break; }
       }
     }
+    /* NEXT-2 medians: nearest rank on the 0.5-point score histograms */
+    res->sim_active_p50 = res->sim_inactive_p50 = ORC_NONE;
+    for (int w = 0; w < 2; ++w) {
+      const uint32_t *hq = w == 0 ? res->hist_q_active : res->hist_q_inactive;
+      uint64_t nq = w == 0 ? res->scored_active : res->scored_inactive;
+      if (!nq) continue;
+      uint64_t k = nr_rank(nq, 50), cum = 0;
+      for (uint32_t b = 0; b < ORC_HIST_Q; ++b) {
+        cum += hq[b];
+        if (cum >= k) {
+          if (w == 0) res->sim_active_p50 = b * 50; else res->sim_inactive_p50 = b * 50;
+          break;
+        }
+      }
+    }
     /* exact nearest-rank values (self-check only) */
     qsort(e2e_v, n_e2e, sizeof(uint64_t), cmp_u64);
     qsort(ttft_v, n_ttft, sizeof(uint64_t), cmp_u64);
@@ -526,6 +602,12 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
     res->ttft_exact_p99_us = n_ttft ? ttft_v[nr_rank(n_ttft, 99) - 1] : NEVER;
   }
   res->n_series = (uint32_t)n_series;
+  if (rows && log && log->rows) {
+    uint64_t nr = end / US + 1; /* seconds 0 .. floor(end / 1e6) */
+    if (nr > n_sec) nr = n_sec;
+    for (uint64_t k = 0; k < nr && k < log->cap_rows; ++k) log->rows[k] = rows[k];
+    log->n_rows = nr;
+  }
   if (log && log->req) {
     for (uint64_t i = 0; i < n_req; ++i) {
       log->req[i].admit_us = rs[i].admit;
@@ -540,7 +622,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
 out:
   free(rs); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
-  free(h.v); free(cs.samples);
+  free(h.v); free(cs.samples); free(rows);
   return rc;
 }
 
@@ -574,6 +656,7 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   cfg->w0_us = in->sc_w0[sid];
   cfg->w1_us = in->sc_w1[sid];
   for (int k = 0; k < 3; ++k) cfg->poly_q16[k] = in->poly_q16[k];
+  for (int k = 0; k < 5; ++k) cfg->quality[k] = in->quality[k];
   cfg->record = in->sc_record[sid];
 }
 
@@ -582,7 +665,7 @@ static int run_internal(const orc_inputs *in, uint64_t sid, int force_record, or
   orc_ctrl ctrl;
   orc_run_cfg cfg;
   scenario_cfg(in, sid, &prof, &ctrl, &cfg);
-  if (force_record) cfg.record = 1;
+  if (force_record) cfg.record |= 1;
   uint32_t flags = 0;
   if (ctrl.calibrated && (ctrl.law == ORC_LAW_MAP || ctrl.law == ORC_LAW_STEP)) {
     /* a10: two-pass calibration from the paired unbounded run */

@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(HERE, "libbellman_sim.so")
 TABLE_N = 4096
 HIST_LAT = 896
 HIST_R = 512
-SEG_HIST_WORDS = 2 * HIST_LAT + HIST_R
+HIST_Q = 201
+SEG_HIST_WORDS = 2 * HIST_LAT + HIST_R + 2 * HIST_Q
 NONE = 0xFFFFFFFF
 FLAG_TRUNCATED, FLAG_DEGENERATE_CALIB, FLAG_SERIES_OVERFLOW, FLAG_DONE = 0x1, 0x2, 0x4, 0x100
 
@@ -37,15 +38,24 @@ STATS_U64 = ["scenario_id", "ticks", "candidates", "arrivals", "admitted", "serv
 STATS_U32 = ["e2e_p50_ms", "e2e_p99_ms", "ttft_p50_ms", "ttft_p99_ms", "median_r_bp",
              "t1", "t2", "activations", "first_act_s", "last_deact_s", "active_ingests", "flags",
              "segment", "_pad0"]
+STATS_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive"]
 STATS = np.dtype([(n, "<u8") for n in STATS_U64] + [(n, "<u4") for n in STATS_U32] +
-                 [("energy_j", "<f8"), ("win_energy_j", "<f8"), ("_reserved", "<u8", (2,))])
+                 [("energy_j", "<f8"), ("win_energy_j", "<f8")] + [(n, "<u4") for n in STATS_Q])
+SECOND_ROW = np.dtype([(n, "<u4") for n in ("arrivals", "admitted", "first_tokens", "completions", "tbt_count",
+                                              "idle_us", "words_in", "words_out")] +
+                      [(n, "<u8") for n in ("sum_queue_us", "sum_ttft_us", "sum_e2e_us", "sum_tbt_us")])
+CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp", "<u4"), ("active", "<u4"),
+                     ("_pad", "<u4"), ("A", "<u8")])
+RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
+assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
 assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 48
 assert CTRL.itemsize == 76 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
 
 
 class Models(C.Structure):
     _fields_ = [("L_words", C.c_void_p), ("I_words", C.c_void_p), ("fvar_q16", C.c_void_p),
-                ("noise", C.c_void_p), ("fcomp_q16", C.c_void_p), ("poly_q16", C.c_int64 * 3)]
+                ("noise", C.c_void_p), ("fcomp_q16", C.c_void_p), ("poly_q16", C.c_int64 * 3),
+                ("qnoise", C.c_void_p), ("quality", C.c_uint32 * 5), ("_pad", C.c_uint32)]
 
 
 class Desc(C.Structure):
@@ -66,6 +76,8 @@ EXPORTS = {
     "bellman_sim_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]),
     "bellman_sim_segment_hist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "bellman_sim_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "bellman_sim_series": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                     C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
     "bellman_sim_last_launches": (C.c_uint32, [C.c_void_p]),
     "bellman_sim_destroy": (None, [C.c_void_p]),
     "bellman_status_string": (C.c_char_p, [C.c_int]),

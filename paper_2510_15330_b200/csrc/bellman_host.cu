@@ -21,9 +21,13 @@ struct bellman_sim {
   int grid = 0;
   uint32_t last_launches = 0;
   Params params{};
-  unsigned int *counters = nullptr;  // [2]
+  unsigned int *counters = nullptr;  // [4]: one per launch of a run
+  bool has_dbg = false;
   std::vector<uint8_t> calibrated;   // per scenario: ctrl is calibrated
   std::vector<uint32_t> calib_src;
+  std::vector<uint32_t> dbg_slot;    // per scenario: debug-record slot or NONE
+  std::vector<uint64_t> dbg_off;
+  std::vector<uint32_t> dbg_cap;
   char err[512] = {0};
 };
 
@@ -58,14 +62,19 @@ static bellman_status validate(const bellman_sim_desc *d) {
   if (d->n_scenarios >= 0xFFFFFFFFull) return fail(nullptr, BELLMAN_EINVAL, "too many scenarios");
   if (!d->n_segments) return fail(nullptr, BELLMAN_EINVAL, "n_segments must be >= 1");
   const bellman_models &m = d->models;
-  if (!m.L_words || !m.I_words || !m.fvar_q16 || !m.noise || !m.fcomp_q16)
+  if (!m.L_words || !m.I_words || !m.fvar_q16 || !m.noise || !m.fcomp_q16 || !m.qnoise)
     return fail(nullptr, BELLMAN_EINVAL, "model tables NULL");
+  if (!(m.quality[2] <= m.quality[1] && m.quality[1] <= m.quality[0] && m.quality[0] <= 10000))
+    return fail(nullptr, BELLMAN_EINVAL, "quality: need floor <= active <= inactive <= 10000");
+  if (!(m.quality[3] > 0 && m.quality[3] < m.quality[4] && m.quality[4] <= 10000))
+    return fail(nullptr, BELLMAN_EINVAL, "quality: need 0 < safe_bp < end_bp <= 10000");
   for (int i = 0; i < BELLMAN_TABLE_N; ++i) {
     if (m.L_words[i] < 1 || m.L_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "L table[%d] out of range", i);
     if (m.I_words[i] < 1 || m.I_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "I table[%d] out of range", i);
     if (m.fvar_q16[i] < 1 || m.fvar_q16[i] > (1 << 18)) return fail(nullptr, BELLMAN_EINVAL, "fvar[%d] out of range", i);
     if (m.noise[i] < -65535 || m.noise[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "noise[%d] out of range", i);
     if (m.fcomp_q16[i] < 0 || m.fcomp_q16[i] > (1 << 18)) return fail(nullptr, BELLMAN_EINVAL, "fcomp[%d] out of range", i);
+    if (m.qnoise[i] < -2047 || m.qnoise[i] > 2047) return fail(nullptr, BELLMAN_EINVAL, "qnoise[%d] out of range", i);
   }
   for (int k = 0; k < 3; ++k)
     if (m.poly_q16[k] > (1ll << 40) || m.poly_q16[k] < -(1ll << 40))
@@ -139,7 +148,8 @@ static bellman_status validate(const bellman_sim_desc *d) {
 // ---------------------------------------------------------------------------
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
-      off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, total;
+      off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
+      off_drows, off_dctrl, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -151,6 +161,10 @@ struct HostPrep {
   std::vector<uint64_t> slot_off;  // per slot
   std::vector<uint32_t> slot_cap;
   uint64_t series_words = 0;
+  std::vector<uint32_t> dbg_of;    // per scenario
+  std::vector<uint64_t> dbg_off;   // per debug slot, in rows
+  std::vector<uint32_t> dbg_cap;
+  uint64_t dbg_rows = 0;
 };
 
 static void prepare(const bellman_sim_desc *d, HostPrep &h) {
@@ -180,9 +194,18 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
   std::vector<uint8_t> need(d->n_scenarios, 0);
   for (uint64_t s = 0; s < d->n_scenarios; ++s) {
     const bellman_scenario &sc = d->scenarios[s];
-    if (sc.record) need[s] = 1;
+    if (sc.record & BELLMAN_RECORD_SIGNAL) need[s] = 1;
     const bellman_ctrl &c = d->ctrls[sc.ctrl];
     if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) need[sc.calib_src] = 1;
+  }
+  h.dbg_of.assign(d->n_scenarios, BELLMAN_NONE);
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+    if (!(d->scenarios[s].record & BELLMAN_RECORD_SECONDS)) continue;
+    h.dbg_of[s] = (uint32_t)h.dbg_off.size();
+    const uint64_t cap = (uint64_t)d->scenarios[s].horizon_us / kUs + 2;
+    h.dbg_off.push_back(h.dbg_rows);
+    h.dbg_cap.push_back((uint32_t)cap);
+    h.dbg_rows += cap;
   }
   for (uint64_t s = 0; s < d->n_scenarios; ++s) {
     if (!need[s]) continue;
@@ -208,7 +231,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_seg = take(sizeof(DevSeg) * h.segs.size());
   L.off_prof = take(sizeof(bellman_profile) * d->n_profiles);
   L.off_ctrl = take(sizeof(bellman_ctrl) * d->n_ctrls);
-  L.off_tab = take(sizeof(int32_t) * 5 * BELLMAN_TABLE_N);
+  L.off_tab = take(sizeof(int32_t) * 6 * BELLMAN_TABLE_N);
   L.off_log2 = take(sizeof(uint2) * BELLMAN_TABLE_N);
   L.off_slot = take(sizeof(uint32_t) * d->n_scenarios);
   L.off_soff = take(sizeof(uint64_t) * ns);
@@ -219,6 +242,13 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
   L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
   L.off_cnt = take(sizeof(unsigned int) * 4);
+  const size_t nd = h.dbg_off.size();
+  L.off_dslot = take(sizeof(uint32_t) * d->n_scenarios);
+  L.off_doff = take(sizeof(uint64_t) * nd);
+  L.off_dcap = take(sizeof(uint32_t) * nd);
+  L.off_dn = take(sizeof(uint32_t) * 2 * nd);
+  L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
+  L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
   L.total = o;
   return L;
 }
@@ -300,6 +330,12 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.tabF = tab + 2 * BELLMAN_TABLE_N;
   P.tabN = tab + 3 * BELLMAN_TABLE_N;
   P.tabC = tab + 4 * BELLMAN_TABLE_N;
+  P.tabQ = tab + 5 * BELLMAN_TABLE_N;
+  P.q_inactive = desc->models.quality[0];
+  P.q_active = desc->models.quality[1];
+  P.q_floor = desc->models.quality[2];
+  P.q_safe = desc->models.quality[3];
+  P.q_end = desc->models.quality[4];
   P.log2tab = (const uint2 *)(ws + L.off_log2);
   P.poly0 = desc->models.poly_q16[0];
   P.poly1 = desc->models.poly_q16[1];
@@ -313,6 +349,16 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.stats = (bellman_scenario_stats *)(ws + L.off_stats);
   P.seg_hist = (unsigned long long *)(ws + L.off_hist);
   sim->counters = (unsigned int *)(ws + L.off_cnt);
+  P.dbg_slot = (const uint32_t *)(ws + L.off_dslot);
+  P.dbg_off = (const uint64_t *)(ws + L.off_doff);
+  P.dbg_cap = (const uint32_t *)(ws + L.off_dcap);
+  P.dbg_n = (uint32_t *)(ws + L.off_dn);
+  P.dbg_rows = (bellman_second_row *)(ws + L.off_drows);
+  P.dbg_ctrl = (bellman_ctrl_row *)(ws + L.off_dctrl);
+  sim->dbg_slot = h.dbg_of;
+  sim->has_dbg = !h.dbg_off.empty();
+  sim->dbg_off = h.dbg_off;
+  sim->dbg_cap = h.dbg_cap;
 
   std::vector<uint2> l2;
   log2_table(l2);
@@ -331,11 +377,16 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
       H2D(P.tabF, desc->models.fvar_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
       H2D(P.tabN, desc->models.noise, sizeof(int32_t) * BELLMAN_TABLE_N);
       H2D(P.tabC, desc->models.fcomp_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
+      H2D(P.tabQ, desc->models.qnoise, sizeof(int32_t) * BELLMAN_TABLE_N);
       H2D(P.log2tab, l2.data(), sizeof(uint2) * BELLMAN_TABLE_N);
       H2D(P.series_slot, h.slot_of.data(), sizeof(uint32_t) * desc->n_scenarios);
       H2D(P.series_off, h.slot_off.data(), sizeof(uint64_t) * h.slot_off.size());
       H2D(P.series_cap, h.slot_cap.data(), sizeof(uint32_t) * h.slot_cap.size());
       if (h.slot_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.series_n, 0, sizeof(uint32_t) * h.slot_off.size(), s));
+      H2D(P.dbg_slot, h.dbg_of.data(), sizeof(uint32_t) * desc->n_scenarios);
+      H2D(P.dbg_off, h.dbg_off.data(), sizeof(uint64_t) * h.dbg_off.size());
+      H2D(P.dbg_cap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
+      if (h.dbg_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.dbg_n, 0, sizeof(uint32_t) * 2 * h.dbg_off.size(), s));
       CUDA_TRY(nullptr, cudaMemsetAsync(P.stats, 0, sizeof(bellman_scenario_stats) * desc->n_scenarios, s));
       CUDA_TRY(nullptr, cudaMemsetAsync(P.seg_hist, 0, sizeof(uint64_t) * kSegWords * desc->n_segments, s));
       CUDA_TRY(nullptr, cudaStreamSynchronize(s));
@@ -380,21 +431,32 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   P.first = first;
   P.count = count;
   P.stride = stride;
-  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 2 * sizeof(unsigned int), s));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 4 * sizeof(unsigned int), s));
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
-  P.counter = sim->counters;
-  P.pass = 1;
   sim->last_launches = 0;
-  CUDA_TRY(sim, bellman_launch_tick(P, grid, s));
+  // pass 1: non-calibrated scenarios (product kernel; debug-recorded ones in the DBG kernel)
+  P.pass = 1;
+  P.counter = sim->counters;
+  CUDA_TRY(sim, bellman_launch_tick(P, grid, false, s));
   sim->last_launches++;
-  if (any_cal) {
+  if (sim->has_dbg) {
+    P.counter = sim->counters + 1;
+    CUDA_TRY(sim, bellman_launch_tick(P, grid, true, s));
+    sim->last_launches++;
+  }
+  if (any_cal) {  // a10: calibration, then pass 2 over the calibrated scenarios
     CUDA_TRY(sim, bellman_launch_calibrate(P, sim->n_slots, s));
     sim->last_launches++;
-    P.counter = sim->counters + 1;
     P.pass = 2;
-    CUDA_TRY(sim, bellman_launch_tick(P, grid, s));
+    P.counter = sim->counters + 2;
+    CUDA_TRY(sim, bellman_launch_tick(P, grid, false, s));
     sim->last_launches++;
+    if (sim->has_dbg) {
+      P.counter = sim->counters + 3;
+      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, s));
+      sim->last_launches++;
+    }
   }
   return BELLMAN_OK;
 }
@@ -431,6 +493,35 @@ bellman_status bellman_sim_reset(bellman_sim *sim, void *stream) {
   CUDA_TRY(sim, cudaMemsetAsync(sim->params.stats, 0, sizeof(bellman_scenario_stats) * sim->n_scenarios, s));
   CUDA_TRY(sim, cudaMemsetAsync(sim->params.seg_hist, 0, sizeof(uint64_t) * kSegWords * sim->n_segments, s));
   if (sim->n_slots) CUDA_TRY(sim, cudaMemsetAsync(sim->params.series_n, 0, sizeof(uint32_t) * sim->n_slots, s));
+  if (sim->dbg_off.size())
+    CUDA_TRY(sim, cudaMemsetAsync(sim->params.dbg_n, 0, sizeof(uint32_t) * 2 * sim->dbg_off.size(), s));
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_series(bellman_sim *sim, uint64_t id, bellman_second_row *rows, uint64_t cap_rows,
+                                  uint64_t *n_rows, bellman_ctrl_row *ctrl, uint64_t cap_ctrl, uint64_t *n_ctrl,
+                                  void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (id >= sim->n_scenarios || sim->dbg_slot[id] == BELLMAN_NONE)
+    return fail(sim, BELLMAN_ESTATE, "scenario %llu is not debug-recorded", (unsigned long long)id);
+  const uint32_t slot = sim->dbg_slot[id];
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  uint32_t n[2] = {0, 0};
+  CUDA_TRY(sim, cudaMemcpyAsync(n, sim->params.dbg_n + 2 * slot, sizeof(n), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(sim, cudaStreamSynchronize(s));
+  if (n_rows) *n_rows = n[0];
+  if (n_ctrl) *n_ctrl = n[1];
+  const uint64_t nr = n[0] < cap_rows ? n[0] : cap_rows;
+  const uint64_t nc = (n[1] < sim->dbg_cap[slot] ? n[1] : sim->dbg_cap[slot]);
+  const uint64_t nc2 = nc < cap_ctrl ? nc : cap_ctrl;
+  if (rows && nr)
+    CUDA_TRY(sim, cudaMemcpyAsync(rows, sim->params.dbg_rows + sim->dbg_off[slot], sizeof(bellman_second_row) * nr,
+                                  cudaMemcpyDeviceToHost, s));
+  if (ctrl && nc2)
+    CUDA_TRY(sim, cudaMemcpyAsync(ctrl, sim->params.dbg_ctrl + sim->dbg_off[slot], sizeof(bellman_ctrl_row) * nc2,
+                                  cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(sim, cudaStreamSynchronize(s));
   return BELLMAN_OK;
 }
 

@@ -25,12 +25,15 @@ struct DevTrace {
   uint32_t seg_off, n_seg, cap, _pad;
 };
 
-// Per-warp shared-memory histograms (a9): 9216 bytes.
+// Per-warp shared-memory histograms (a9, NEXT-2): 10,848 bytes.
 struct WarpHist {
   uint32_t e2e[BELLMAN_HIST_LAT];
   uint32_t ttft[BELLMAN_HIST_LAT];
   uint32_t r[BELLMAN_HIST_R];
+  uint32_t qa[204];  // similarity, active (BELLMAN_HIST_Q bins used)
+  uint32_t qi[204];  // similarity, inactive
 };
+static_assert(sizeof(WarpHist) % 16 == 0, "WarpHist is zeroed with 16-byte stores");
 
 struct Params {
   const bellman_scenario *sc;
@@ -38,18 +41,25 @@ struct Params {
   const DevSeg *segs;
   const bellman_profile *profs;
   const bellman_ctrl *ctrls;
-  const int32_t *tabL, *tabI, *tabF, *tabN, *tabC;  // 4096 each
+  const int32_t *tabL, *tabI, *tabF, *tabN, *tabC, *tabQ;  // 4096 each
   const uint2 *log2tab;                             // (T[i], T[i+1]-T[i]), i < 4096
   int64_t poly0, poly1, poly2;
+  uint32_t q_inactive, q_active, q_floor, q_safe, q_end;  // quality model (NEXT-2)
   const uint32_t *series_slot;  // [n_scenarios] slot or NONE
   const uint64_t *series_off;   // [n_slots] word offset into series
   const uint32_t *series_cap;   // [n_slots]
   uint32_t *series_n;           // [n_slots] samples written
   uint32_t *series;             // sample storage
   uint32_t *calib;              // [n_slots][4]: t1, t2, status, n
+  const uint32_t *dbg_slot;     // [n_scenarios] debug-record slot or NONE (NEXT-1)
+  const uint64_t *dbg_off;      // [n_dbg] row offset
+  const uint32_t *dbg_cap;      // [n_dbg] rows (= controller-log rows) capacity
+  uint32_t *dbg_n;              // [n_dbg][2]: rows, controller-log rows written
+  bellman_second_row *dbg_rows;
+  bellman_ctrl_row *dbg_ctrl;
   bellman_scenario_stats *stats;
   unsigned long long *seg_hist;  // [n_segments][kSegWords]
-  unsigned int *counter;         // work counter of this pass
+  unsigned int *counter;         // work counter of this launch
   uint64_t first, count, stride;
   uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
 };
@@ -57,6 +67,6 @@ struct Params {
 }  // namespace bellman
 
 // launchers (bellman_kernels.cu)
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, cudaStream_t stream);
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream);
 cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream);
 int bellman_tick_grid(int device);

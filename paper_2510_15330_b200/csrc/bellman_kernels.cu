@@ -105,37 +105,61 @@ __device__ __forceinline__ uint64_t warp_sum_split(uint64_t x) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Cold per-scenario state: touched at events (admissions, completions,
+// ingests, refills), not per iteration.  Lives in shared memory, one per warp,
+// so the event loop keeps its hot state in registers without spilling.
+struct Cold {
+  const DevSeg *segs;
+  uint64_t gen_tau;
+  uint64_t ringA;
+  uint64_t w0, w1;
+  uint32_t *series;
+  bellman_ctrl_row *dbg_ctrl;
+  uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
+  uint32_t law, window, rmin, rmax, t1, t2, nrungs, ring_n, ring_pos, rung, active;
+  uint32_t activations, first_act, last_deact, active_ingests;
+  uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
+  uint32_t k0, wid_lo, wid_hi;
+  uint32_t t0, knee, slope, slo_us;  // read-only after init
+};
+
+struct alignas(16) WarpSmem {
+  WarpHist h;
+  Cold c;
+};
+
 // ---------------------------------------------------------------------------
 // The per-scenario simulation.  Every scalar is warp-uniform.  Derived
 // quantities are maintained incrementally so that an event trip does no
 // division: the cost base c = t0 + slope max(0, B - knee), the KV term as
 // kv K = kq 1000 + kr, the window flag and its next boundary, the arrival time
 // of the queue head.
+template <bool DBG>
 struct Sim {
+  __device__ explicit Sim(Cold &cold) : c(cold) {}
   uint32_t lane;
+  Cold &c;  // per-warp shared-memory part of the state (cold fields)
   // ---- scenario (a1)
-  uint32_t k0;  // Philox key word 0 = seed_index
-  uint32_t wid_lo, wid_hi;
   uint64_t H;
-  uint64_t w0, w1;
   // profile
-  uint32_t t0, knee, slope, kv, maxb, pf_ns;
+  uint32_t kv, maxb;
   // controller
-  uint32_t law, signal, window, rmin, rmax, t1, t2, slo_us, nrungs;
+  uint32_t signal;
   uint32_t rungs_lane;  // lane l < nrungs holds rung l
-  uint32_t r, active, rung;
+  uint32_t r;
   uint32_t ring;        // lane l < window holds a ring sample
-  uint32_t ring_n, ring_pos;
-  uint64_t ringA;
-  uint32_t activations, first_act, last_deact, active_ingests;
   // per-second accumulator of the selected signal (a6)
   uint64_t sec_bound;  // (open second + 1) * 1e6, INF when nothing consumes the signal
   uint64_t acc_sum;
   uint32_t acc_cnt;
   // recording (a10 source)
-  uint32_t *series;
-  uint32_t series_cap, series_n;
-  uint32_t flags;
+  // debug record mode (NEXT-1): per-second rows and controller log, NULL when off
+  bellman_second_row *dbg;
+  // profile constants used at events
+  uint32_t pf_ns;
+  // ---- counters (a8), updated at events
+  uint32_t admitted, served, rewritten, slo_viol, win_served, last_j;
+  uint64_t words_in, idle, win_words_in, win_idle, sum_queue, sum_ttft, sum_e2e;
   // ---- serving state (a4, a5, a7)
   uint64_t T;
   uint32_t busy;
@@ -156,26 +180,26 @@ struct Sim {
   uint64_t sa[2], sp[2];
   uint32_t sR[2], sin[2], sdn[2], sph[2];
   // ---- generator / queue head (a2)
-  const DevSeg *segs;
-  uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
-  uint64_t gen_tau;
   uint32_t buf_h, buf_n;
   uint64_t buf_a;      // lane-parallel buffer of upcoming arrivals
   uint32_t buf_in;     // input words
   uint32_t buf_U;      // realized unbounded length (a3)
   uint32_t buf_P;      // predicted length (a3)
-  int32_t buf_fc;      // compliance factor, Q16 (a3)
+  uint32_t buf_fcq;    // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
   uint32_t buf_j;
   uint64_t head_t;     // arrival time of the queue head, INF when no arrival remains
-  uint32_t last_j;     // candidate index of the last counted arrival + 1
   // ---- counters (a8)
-  uint32_t admitted, served, rewritten, slo_viol, win_served;
-  uint64_t words_in, words_out, idle, win_words_in, win_words_out, win_idle;
-  uint64_t sum_queue, sum_ttft, sum_e2e;
+  uint64_t words_out, win_words_out;
 
   // ------------------------------------------------------------------ a2
   // Refill the 32-entry arrival buffer with the next accepted candidates.
   __device__ __forceinline__ void refill(const Params &p) {
+    // shared-memory generator state: read by all lanes, written back by lane 0 only
+    uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
+    uint32_t gen_acc = c.gen_acc;
+    uint64_t gen_tau = c.gen_tau;
+    const uint32_t n_seg = c.n_seg, gen_cap = c.gen_cap, k0 = c.k0, wid_lo = c.wid_lo, wid_hi = c.wid_hi;
+    const DevSeg *segs = c.segs;
     buf_h = 0;
     buf_n = 0;
     while (!gen_done && buf_n == 0) {
@@ -226,6 +250,7 @@ struct Sim {
       const uint32_t at = __shfl_sync(FULL, attr, s);
       buf_j = __shfl_sync(FULL, jj, s);
       buf_n = cnt;
+      if (DBG && dbg && lane < cnt && buf_a < H) atomicAdd(&row(buf_a)->arrivals, 1u);
       // a3: the accepted request's own draws (tag 1), lane-parallel, ahead of admission
       {
         const uint32_t L = at & 0xFFFFu;
@@ -236,7 +261,7 @@ struct Sim {
         buf_U = U < 1 ? 1u : (uint32_t)U;
         const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
         buf_P = P0 < 1 ? 1u : (uint32_t)P0;
-        buf_fc = __ldg(&p.tabC[v.z >> 20]);
+        buf_fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
       }
       gen_acc += cnt;
       if (first_over < 32u) {
@@ -249,52 +274,89 @@ struct Sim {
       }
     }
     head_t = buf_n ? __shfl_sync(FULL, buf_a, 0) : INF;
+    if (lane == 0) {
+      c.gen_done = gen_done;
+      c.gen_seg = gen_seg;
+      c.gen_fresh = gen_fresh;
+      c.gen_j = gen_j;
+      c.gen_acc = gen_acc;
+      c.gen_tau = gen_tau;
+    }
+    __syncwarp();
   }
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
-    if (series) {
-      if (series_n < series_cap) {
-        if (lane == 0) series[series_n] = x;
-      } else {
-        flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+    // shared-memory controller state: read by all lanes, written back by lane 0 only
+    if (c.series) {
+      const uint32_t n = c.series_n;
+      if (lane == 0) {
+        if (n < c.series_cap) c.series[n] = x;
+        else c.flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+        c.series_n = n + 1u;
       }
-      series_n++;
+      __syncwarp();
     }
-    if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return;
-    const uint32_t ev = __shfl_sync(FULL, ring, ring_pos);
-    if (lane == ring_pos) ring = x;
-    if (ring_n < window) {
-      ring_n++;
-      ringA += x;
+    if (c.law != BELLMAN_LAW_MAP && c.law != BELLMAN_LAW_STEP) return;
+    const uint32_t window = c.window, pos = c.ring_pos, t1 = c.t1;
+    uint32_t k = c.ring_n, rung = c.rung;
+    const uint32_t was_active = c.active;
+    uint64_t A = c.ringA;
+    const uint32_t ev = __shfl_sync(FULL, ring, pos);
+    if (lane == pos) ring = x;
+    if (k < window) {
+      k++;
+      A += x;
     } else {
-      ringA = ringA + x - ev;
+      A = A + x - ev;
     }
-    ring_pos = (ring_pos + 1u == window) ? 0u : ring_pos + 1u;
-    const uint32_t k = ring_n;
-    const bool act = ringA >= (uint64_t)k * t1;  // non-strict (R38)
+    const bool act = A >= (uint64_t)k * t1;  // non-strict (R38)
     uint32_t nr = 0;
     if (act) {
-      if (law == BELLMAN_LAW_MAP) {
-        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (ringA - (uint64_t)k * t1)) / ((uint64_t)k * (t2 - t1));
+      if (c.law == BELLMAN_LAW_MAP) {
+        const uint32_t rmin = c.rmin, rmax = c.rmax;
+        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (c.t2 - t1));
         if (rr > rmax) rr = rmax;
         nr = (uint32_t)rr;
+        const uint32_t nrungs = c.nrungs;
         if (nrungs) {  // largest rung <= r (R5)
           const uint32_t le = __ballot_sync(FULL, lane < nrungs && rungs_lane <= nr);
           nr = __shfl_sync(FULL, rungs_lane, 31 - __clz(le | 1u));
         }
       } else {  // STEP
-        rung = active ? (rung + 1u < nrungs ? rung + 1u : rung) : 0u;
+        rung = was_active ? (rung + 1u < c.nrungs ? rung + 1u : rung) : 0u;
         nr = __shfl_sync(FULL, rungs_lane, rung);
       }
     }
-    if (act && !active) {
-      activations++;
-      if (first_act == BELLMAN_NONE) first_act = second;
+    const uint32_t nctrl = c.dbg_nctrl;
+    if (lane == 0) {
+      c.ring_n = k;
+      c.ringA = A;
+      c.ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
+      c.rung = rung;
+      c.active = act;
+      if (act && !was_active) {
+        c.activations++;
+        if (c.first_act == BELLMAN_NONE) c.first_act = second;
+      }
+      if (!act && was_active) c.last_deact = second;
+      if (act) c.active_ingests++;
+      if (DBG && dbg) {
+        if (nctrl < c.dbg_cap) {
+          bellman_ctrl_row cr;
+          cr.second = second;
+          cr.sample = x;
+          cr.k = k;
+          cr.r_bp = nr;
+          cr.active = act;
+          cr._pad = 0;
+          cr.A = A;
+          c.dbg_ctrl[nctrl] = cr;
+        }
+        c.dbg_nctrl = nctrl + 1u;
+      }
     }
-    if (!act && active) last_deact = second;
-    if (act) active_ingests++;
-    active = act;
+    __syncwarp();
     r = nr;
   }
 
@@ -307,9 +369,23 @@ struct Sim {
     sec_bound = (t / kUs + 1u) * kUs;
   }
 
+  __device__ __forceinline__ bellman_second_row *row(uint64_t t) const {
+    const uint64_t sidx = t / kUs;
+    return dbg + (sidx < c.dbg_cap ? sidx : c.dbg_cap - 1u);
+  }
+
+  // idle interval [a, b) split over the seconds it overlaps (debug rows only)
+  __device__ __forceinline__ void dbg_idle(uint64_t a, uint64_t b) {
+    if (!dbg || lane != 0) return;
+    for (uint64_t sidx = a / kUs; sidx * kUs < b; ++sidx) {
+      const uint64_t lo = a > sidx * kUs ? a : sidx * kUs, hi = b < (sidx + 1) * kUs ? b : (sidx + 1) * kUs;
+      atomicAdd(&row(sidx * kUs)->idle_us, (uint32_t)(hi - lo));
+    }
+  }
+
   __device__ __forceinline__ void update_window() {
-    win_now = T >= w0 && T < w1;
-    win_next = T < w0 ? w0 : (T < w1 ? w1 : INF);
+    win_now = T >= c.w0 && T < c.w1;
+    win_next = T < c.w0 ? c.w0 : (T < c.w1 ? c.w1 : INF);
     stop_static = H < win_next ? H : win_next;
   }
 
@@ -322,7 +398,7 @@ struct Sim {
 
   // B changed: cost base and per-iteration KV growth
   __device__ __forceinline__ void batch_changed() {
-    cbase = t0 + slope * (B > knee ? B - knee : 0u);
+    cbase = c.t0 + c.slope * (B > c.knee ? B - c.knee : 0u);
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
     kstep_r = ks - kstep_q * 1000u;
@@ -367,6 +443,13 @@ struct Sim {
       acc_sum += (uint64_t)B * iter_d + iter_align;
       acc_cnt += B;
     }
+    if (DBG && dbg && lane == 0) {
+      bellman_second_row *w = row(Tn);
+      atomicAdd(&w->tbt_count, B);
+      atomicAdd(&w->words_out, B);
+      atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * iter_d + iter_align);
+    }
+    __syncwarp();
     // every participant emitted one word: K += B
     kr += kstep_r;
     kq += kstep_q;
@@ -380,12 +463,12 @@ struct Sim {
       uint32_t kdrop = 0, nslo = 0, ndone = 0, dmin = 0xffffffffu;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const bool c = sph[s] == PH_DEC && sdn[s] == it;
-        ndone += __popc(__ballot_sync(FULL, c));
-        if (c) {
+        const bool cpl = sph[s] == PH_DEC && sdn[s] == it;
+        ndone += __popc(__ballot_sync(FULL, cpl));
+        if (cpl) {
           const uint64_t e = Tn - sa[s];
           e2e_l += e;
-          nslo += e > slo_us;
+          nslo += e > c.slo_us;
           kdrop += sin[s] + sR[s];
           atomicAdd(&h.e2e[lat_bin(e / 1000u)], 1u);
           sph[s] = PH_EMPTY;
@@ -400,6 +483,11 @@ struct Sim {
       sum_e2e += se;
       slo_viol += ns;
       if (win_now) win_served += ndone;
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Tn)->completions, ndone);
+        atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
+      }
+      __syncwarp();
       in_sys -= ndone;
       B -= ndone;
       batch_changed();
@@ -423,7 +511,7 @@ struct Sim {
         atomicAdd(&h.ttft[lat_bin(tt / 1000u)], 1u);
         if (sR[s] == 1u) {  // R9: completes at the prefill end
           e2e_l += tt;
-          nslo += tt > slo_us;
+          nslo += tt > c.slo_us;
           n1++;
           atomicAdd(&h.e2e[lat_bin(tt / 1000u)], 1u);
           sph[s] = PH_EMPTY;
@@ -436,8 +524,15 @@ struct Sim {
     }
     const uint32_t m = __reduce_min_sync(FULL, mpf);
     next_pf = (m == 0xffffffffu) ? INF : Tn + m;
-    sum_ttft += warp_sum_split(ttft_l);
+    const uint64_t st = warp_sum_split(ttft_l);
+    sum_ttft += st;
     words_out += nfirst;
+    if (DBG && dbg && lane == 0) {
+      atomicAdd(&row(Tn)->first_tokens, nfirst);
+      atomicAdd(&row(Tn)->words_out, nfirst);
+      atomicAdd((unsigned long long *)&row(Tn)->sum_ttft_us, (unsigned long long)st);
+    }
+    __syncwarp();
     if (win_now) win_words_out += nfirst;
     n_ready += __reduce_add_sync(FULL, nrdy);
     const uint32_t nc = __reduce_add_sync(FULL, n1);
@@ -448,6 +543,11 @@ struct Sim {
       sum_e2e += se;
       slo_viol += ns;
       if (win_now) win_served += nc;
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Tn)->completions, nc);
+        atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
+      }
+      __syncwarp();
       in_sys -= nc;
       complete_sig(se, nc, ns);
     }
@@ -477,17 +577,33 @@ struct Sim {
         const uint32_t in = __shfl_sync(FULL, buf_in, src);
         const uint32_t U = __shfl_sync(FULL, buf_U, src);
         const uint32_t P = __shfl_sync(FULL, buf_P, src);
-        const int32_t fc = __shfl_sync(FULL, buf_fc, src);
+        const uint32_t fcq = __shfl_sync(FULL, buf_fcq, src);
         if (mine) {
           uint32_t R = U;
           if (r > 0) {  // a7 rewrite: N = round(P (1 - r)), realized = round(poly(N) Fcomp)
             int64_t N = (int64_t)(((uint64_t)P * (10000u - r) + 5000u) / 10000u);
             if (N < 1) N = 1;
             const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
+            const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
             __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
             if (x < 1) x = 1;
             if (x > (1 << 24)) x = 1 << 24;
             R = (uint32_t)x;
+          }
+          {  // NEXT-2: similarity vs the unbounded length
+            int32_t base = (int32_t)p.q_inactive;
+            if (r > 0) {
+              const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
+              if (num <= (int64_t)p.q_safe * den) base = (int32_t)p.q_active;
+              else if (num >= (int64_t)p.q_end * den) base = (int32_t)p.q_floor;
+              else
+                base = (int32_t)p.q_active - (int32_t)(((int64_t)(p.q_active - p.q_floor) * (num - (int64_t)p.q_safe * den)) /
+                                                       ((int64_t)(p.q_end - p.q_safe) * den));
+            }
+            int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+            sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+            const uint32_t qb = (uint32_t)sc / 50u;
+            atomicAdd(r > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
           }
           uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
           if (pf < 1) pf = 1;
@@ -506,7 +622,14 @@ struct Sim {
       const uint32_t win = __reduce_add_sync(FULL, win_l);
       words_in += win;
       if (win_now) win_words_in += win;
-      sum_queue += warp_sum_split(q_l);
+      const uint64_t sq = warp_sum_split(q_l);
+      sum_queue += sq;
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Tn)->admitted, k);
+        atomicAdd(&row(Tn)->words_in, win);
+        atomicAdd((unsigned long long *)&row(Tn)->sum_queue_us, (unsigned long long)sq);
+      }
+      __syncwarp();
       if (r > 0) {
         rewritten += k;
         if (lane == 0) atomicAdd(&h.r[r / 10u < BELLMAN_HIST_R ? r / 10u : BELLMAN_HIST_R - 1], k);
@@ -517,7 +640,7 @@ struct Sim {
       buf_h += k;
       if (buf_h < buf_n) {
         head_t = __shfl_sync(FULL, buf_a, buf_h & 31u);
-      } else if (!gen_done) {
+      } else if (!c.gen_done) {
         refill(p);
       } else {
         head_t = INF;
@@ -529,7 +652,7 @@ struct Sim {
   // ------------------------------------------------------------------ a4/a5 leap
   // Execute in bulk the longest run of iterations whose ends are uneventful —
   // no completion (index < next_done), no prefill end, no admission (head
-  // arrival still in the future or no free slot), no window / horizon
+  // arrival still in the future or no free slot), no c.window / horizon
   // boundary — exactly as the per-iteration path would: each emits B words
   // with TBT gap d_m = c + floor(kv (K + m B) / 1000) and grows K by B.  A
   // second boundary met inside the run is rolled in place (ingest), as the
@@ -542,7 +665,7 @@ struct Sim {
     if (in_sys < maxb && head_t < stop) stop = head_t;
     const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
     if (nmax == 0 || stop <= T + 1u) return;
-    const uint32_t c = cbase, qs = kstep_q, rs = kstep_r;
+    const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
     uint32_t q = kq, rr = kr, done = 0;
     for (;;) {
       const uint64_t lim = stop < sec_bound ? stop : sec_bound;
@@ -551,12 +674,12 @@ struct Sim {
       const uint32_t left = nmax - done;
       uint32_t n = 0, used = 0;
       if (kv == 0) {
-        const uint32_t nn = room / c;
+        const uint32_t nn = room / cb;
         n = nn < left ? nn : left;
-        used = n * c;
+        used = n * cb;
       } else {
         while (n < left) {
-          const uint32_t d = c + q;
+          const uint32_t d = cb + q;
           if (d > room - used) break;
           used += d;
           rr += rs;
@@ -576,10 +699,17 @@ struct Sim {
           acc_sum += (uint64_t)B * used;
           acc_cnt += (uint32_t)words;
         }
+        if (DBG && dbg && lane == 0) {  // all ends of this chunk lie in the open second
+          bellman_second_row *w = row(sec_bound - kUs);
+          atomicAdd(&w->tbt_count, (uint32_t)words);
+          atomicAdd(&w->words_out, (uint32_t)words);
+          atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * used);
+        }
+        __syncwarp();
         done += n;
       }
       if (done == nmax) break;
-      const uint64_t tnext = T + (c + q);  // end of the next iteration
+      const uint64_t tnext = T + (cb + q);  // end of the next iteration
       if (tnext >= stop || tnext < sec_bound) break;
       roll_second(tnext);  // the next end opens a new second: ingest the closed one here
     }
@@ -592,14 +722,14 @@ struct Sim {
     const uint64_t Tn = T;
     uint64_t align = 0;
     if (n_ready) {
-      const uint32_t c = ticks;  // index of the new iteration
+      const uint32_t it0 = ticks;  // index of the new iteration
       uint32_t jn = 0xffffffffu, kadd = 0;
       uint64_t al = 0;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         if (sph[s] == PH_READY) {
           sph[s] = PH_DEC;
-          sdn[s] = c + sR[s] - 2u;  // words 2..R at the ends of iterations c..c+R-2
+          sdn[s] = it0 + sR[s] - 2u;  // words 2..R at the ends of iterations it0..it0+R-2
           al += Tn - sp[s];
           kadd += sin[s] + 1u;
           jn = min(jn, sdn[s]);
@@ -624,12 +754,13 @@ struct Sim {
 
 // ---------------------------------------------------------------------------
 __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, const uint32_t *ps, uint32_t np,
-                                 uint32_t *out, bool lat) {
+                                 uint32_t *out, bool lat, uint32_t scale = 10u) {
   const uint32_t lane = lane_id();
-  const uint32_t chunk = nb / 32u;
+  const uint32_t chunk = (nb + 31u) / 32u;
   uint32_t csum = 0;
 #pragma unroll 1
-  for (uint32_t b = 0; b < chunk; ++b) csum += hist[lane * chunk + b];
+  for (uint32_t b = 0; b < chunk; ++b)
+    if (lane * chunk + b < nb) csum += hist[lane * chunk + b];
   uint32_t incl = csum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -649,10 +780,10 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
     if (lane == L) {
       uint64_t cum = incl - csum;
 #pragma unroll 1
-      for (uint32_t b = 0; b < chunk; ++b) {
+      for (uint32_t b = 0; b < chunk && lane * chunk + b < nb; ++b) {
         cum += hist[lane * chunk + b];
         if (cum >= k) {
-          res = lat ? lat_edge(lane * chunk + b) : (lane * chunk + b) * 10u;
+          res = lat ? lat_edge(lane * chunk + b) : (lane * chunk + b) * scale;
           break;
         }
       }
@@ -661,10 +792,12 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
   }
 }
 
+template <bool DBG>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
-  WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
+  WarpSmem &ws = reinterpret_cast<WarpSmem *>(smem_raw)[threadIdx.x >> 5];
+  WarpHist &h = ws.h;
   for (;;) {
     uint32_t kidx = 0;
     if (lane == 0) kidx = atomicAdd(p.counter, 1u);
@@ -674,68 +807,84 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     const bellman_scenario sc = p.sc[sid];
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
     if ((cc.calibrated != 0) != (p.pass == 2)) continue;
+    // debug-recorded scenarios run in the DBG instantiation, all others in the product one
+    if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
     // ---- a1: scenario decode
-    Sim S;
+    Sim<DBG> S(ws.c);
     S.lane = lane;
-    S.k0 = sc.seed_index;
-    S.wid_lo = (uint32_t)sc.wid;
-    S.wid_hi = (uint32_t)(sc.wid >> 32);
+    S.c.k0 = sc.seed_index;
+    S.c.wid_lo = (uint32_t)sc.wid;
+    S.c.wid_hi = (uint32_t)(sc.wid >> 32);
     S.H = (uint64_t)sc.horizon_us;
-    S.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
-    S.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+    S.c.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
+    S.c.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
     const bellman_profile pr = p.profs[sc.profile];
-    S.t0 = pr.t0_us;
-    S.knee = pr.knee;
-    S.slope = pr.slope_us;
+    S.c.t0 = pr.t0_us;
+    S.c.knee = pr.knee;
+    S.c.slope = pr.slope_us;
     S.kv = pr.kv_ns_per_word;
     S.maxb = pr.max_batch;
     S.pf_ns = pr.prefill_ns_per_word;
-    S.law = cc.law;
+    S.c.law = cc.law;
     S.signal = cc.signal;
-    S.window = cc.window;
-    S.rmin = cc.r_min_bp;
-    S.rmax = cc.r_max_bp;
-    S.t1 = cc.t1;
-    S.t2 = cc.t2;
-    S.slo_us = cc.slo_us;
-    S.nrungs = cc.n_rungs;
+    S.c.window = cc.window;
+    S.c.rmin = cc.r_min_bp;
+    S.c.rmax = cc.r_max_bp;
+    S.c.t1 = cc.t1;
+    S.c.t2 = cc.t2;
+    S.c.slo_us = cc.slo_us;
+    S.c.nrungs = cc.n_rungs;
     S.rungs_lane = lane < 8 ? cc.rungs_bp[lane] : 0u;
-    S.flags = 0;
+    S.c.flags = 0;
     if (cc.calibrated) {
       const uint32_t slot = p.series_slot[sc.calib_src];
       const uint32_t *cb = p.calib + 4u * slot;
-      S.t1 = cb[0];
-      S.t2 = cb[1];
+      S.c.t1 = cb[0];
+      S.c.t2 = cb[1];
       if (cb[2] != 0) {
-        S.law = BELLMAN_LAW_OFF;
-        S.flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+        S.c.law = BELLMAN_LAW_OFF;
+        S.c.flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
       }
     }
-    S.r = S.law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
-    S.active = 0;
-    S.rung = 0;
+    S.r = S.c.law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
+    S.c.active = 0;
+    S.c.rung = 0;
     S.ring = 0;
-    S.ring_n = 0;
-    S.ring_pos = 0;
-    S.ringA = 0;
-    S.activations = 0;
-    S.first_act = BELLMAN_NONE;
-    S.last_deact = BELLMAN_NONE;
-    S.active_ingests = 0;
+    S.c.ring_n = 0;
+    S.c.ring_pos = 0;
+    S.c.ringA = 0;
+    S.c.activations = 0;
+    S.c.first_act = BELLMAN_NONE;
+    S.c.last_deact = BELLMAN_NONE;
+    S.c.active_ingests = 0;
     S.acc_sum = 0;
     S.acc_cnt = 0;
     const uint32_t rslot = p.series_slot[sid];
     if (rslot != BELLMAN_NONE) {
-      S.series = p.series + p.series_off[rslot];
-      S.series_cap = p.series_cap[rslot];
+      S.c.series = p.series + p.series_off[rslot];
+      S.c.series_cap = p.series_cap[rslot];
     } else {
-      S.series = nullptr;
-      S.series_cap = 0;
+      S.c.series = nullptr;
+      S.c.series_cap = 0;
     }
-    S.series_n = 0;
-    // the per-second signal feeds only the controller (MAP/STEP) and the recorder
-    S.sec_bound = (S.law == BELLMAN_LAW_MAP || S.law == BELLMAN_LAW_STEP || S.series) ? kUs : INF;
+    S.c.series_n = 0;
+    const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
+    if (DBG && dslot != BELLMAN_NONE) {
+      S.dbg = p.dbg_rows + p.dbg_off[dslot];
+      S.c.dbg_ctrl = p.dbg_ctrl + p.dbg_off[dslot];
+      S.c.dbg_cap = p.dbg_cap[dslot];
+      // rows are accumulated with atomics: zero this scenario's region first
+      for (uint32_t i = lane; i < S.c.dbg_cap; i += 32u) S.dbg[i] = bellman_second_row{};
+      __syncwarp();
+    } else {
+      S.dbg = nullptr;
+      S.c.dbg_ctrl = nullptr;
+      S.c.dbg_cap = 0;
+    }
+    S.c.dbg_nctrl = 0;
+    // the per-second signal feeds only the controller (MAP/STEP) and the recorders
+    S.sec_bound = (S.c.law == BELLMAN_LAW_MAP || S.c.law == BELLMAN_LAW_STEP || S.c.series || (DBG && S.dbg)) ? kUs : INF;
     S.T = 0;
     S.busy = 0;
     S.iter_end = INF;
@@ -756,19 +905,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
     }
     const DevTrace tr = p.traces[sc.trace];
-    S.segs = p.segs + tr.seg_off;
-    S.n_seg = tr.n_seg;
-    S.gen_seg = 0;
-    S.gen_fresh = 1;
-    S.gen_j = 0;
-    S.gen_acc = 0;
-    S.gen_cap = tr.cap;
-    S.gen_done = 0;
-    S.gen_tau = 0;
+    S.c.segs = p.segs + tr.seg_off;
+    S.c.n_seg = tr.n_seg;
+    S.c.gen_seg = 0;
+    S.c.gen_fresh = 1;
+    S.c.gen_j = 0;
+    S.c.gen_acc = 0;
+    S.c.gen_cap = tr.cap;
+    S.c.gen_done = 0;
+    S.c.gen_tau = 0;
     S.buf_h = S.buf_n = 0;
     S.buf_a = 0;
     S.buf_in = S.buf_U = S.buf_P = 0;
-    S.buf_fc = 0;
+    S.buf_fcq = 0;
     S.buf_j = 0;
     S.last_j = 0;
     S.admitted = S.served = S.rewritten = S.slo_viol = S.win_served = 0;
@@ -812,8 +961,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       if (tn >= S.H) break;
       if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
         S.idle += tn - S.T;
-        const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = tn < S.w1 ? tn : S.w1;
+        const uint64_t lo = S.T > S.c.w0 ? S.T : S.c.w0, hi = tn < S.c.w1 ? tn : S.c.w1;
         if (hi > lo) S.win_idle += hi - lo;
+        S.dbg_idle(S.T, tn);
       }
       S.advance(tn);
       if (S.busy) {
@@ -853,15 +1003,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
     if (S.in_sys == 0) {
       S.idle += end - S.T;
-      const uint64_t lo = S.T > S.w0 ? S.T : S.w0, hi = end < S.w1 ? end : S.w1;
+      const uint64_t lo = S.T > S.c.w0 ? S.T : S.c.w0, hi = end < S.c.w1 ? end : S.c.w1;
       if (hi > lo) S.win_idle += hi - lo;
+      S.dbg_idle(S.T, end);
     }
     if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
     // queued at the end: accepted arrivals before `end` not admitted
     uint64_t queued = 0;
     for (;;) {
       if (S.buf_h >= S.buf_n) {
-        if (S.gen_done) break;
+        if (S.c.gen_done) break;
         S.refill(p);
         continue;
       }
@@ -872,7 +1023,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
       S.buf_h = S.buf_n;
     }
-    if (S.series && lane == 0) p.series_n[rslot] = S.series_n;
+    if (S.c.series && lane == 0) p.series_n[rslot] = S.c.series_n;
+    if (DBG && S.dbg && lane == 0) {
+      const uint64_t nr = end / kUs + 1u;
+      p.dbg_n[2 * dslot] = (uint32_t)(nr < S.c.dbg_cap ? nr : S.c.dbg_cap);
+      p.dbg_n[2 * dslot + 1] = S.c.dbg_nctrl;
+    }
 
     // ---- a9: percentiles from the histograms
     __syncwarp();
@@ -888,6 +1044,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     }
     warp_percentiles(h.ttft, BELLMAN_HIST_LAT, n_ttft, ps, 2, pt, true);
     warp_percentiles(h.r, BELLMAN_HIST_R, S.rewritten, p50, 1, pm, false);
+    uint32_t pqa[1], pqi[1];  // NEXT-2 similarity medians
+    warp_percentiles(h.qa, BELLMAN_HIST_Q, S.rewritten, p50, 1, pqa, false, 50u);
+    warp_percentiles(h.qi, BELLMAN_HIST_Q, S.admitted - S.rewritten, p50, 1, pqi, false, 50u);
     // segment merge: integer atomics, order-independent
     unsigned long long *sh = p.seg_hist + (uint64_t)sc.segment * kSegWords;
     for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) {
@@ -896,6 +1055,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     }
     for (uint32_t b = lane; b < BELLMAN_HIST_R; b += 32u)
       if (h.r[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + b], (unsigned long long)h.r[b]);
+    for (uint32_t b = lane; b < BELLMAN_HIST_Q; b += 32u) {
+      if (h.qa[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + b], (unsigned long long)h.qa[b]);
+      if (h.qi[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q + b], (unsigned long long)h.qi[b]);
+    }
 
     // ---- a8: summary record
     if (lane == 0) {
@@ -926,13 +1089,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       o.ttft_p50_ms = pt[0];
       o.ttft_p99_ms = pt[1];
       o.median_r_bp = pm[0];
-      o.t1 = S.t1;
-      o.t2 = S.t2;
-      o.activations = S.activations;
-      o.first_act_s = S.first_act;
-      o.last_deact_s = S.last_deact;
-      o.active_ingests = S.active_ingests;
-      uint32_t fl = S.flags | BELLMAN_FLAG_DONE;
+      o.t1 = S.c.t1;
+      o.t2 = S.c.t2;
+      o.activations = S.c.activations;
+      o.first_act_s = S.c.first_act;
+      o.last_deact_s = S.c.last_deact;
+      o.active_ingests = S.c.active_ingests;
+      uint32_t fl = S.c.flags | BELLMAN_FLAG_DONE;
       if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
       o.flags = fl;
       o.segment = sc.segment;
@@ -946,9 +1109,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       const double wb = __dmul_rn(pr.e_out_j_per_word, (double)S.win_words_out);
       const double wc = __dmul_rn(pr.p_idle_w, (double)S.win_idle);
       o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
-      o._reserved[0] = o._reserved[1] = 0;
+      o.sim_active_p50 = pqa[0];
+      o.sim_inactive_p50 = pqi[0];
+      o.scored_active = S.rewritten;
+      o.scored_inactive = S.admitted - S.rewritten;
       p.stats[sid] = o;
     }
+    __syncwarp();
     __syncwarp();
   }
 }
@@ -999,17 +1166,21 @@ extern "C" int bellman_debug_prof(unsigned long long *out) {
 int bellman_tick_grid(int device) {
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
-  cudaFuncSetAttribute(bellman::bellman_tick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel,
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpSmem);
+  cudaFuncSetAttribute(bellman::bellman_tick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(bellman::bellman_tick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false>,
                                                     bellman::kWarpsPerBlock * 32, smem) != cudaSuccess)
     return -1;
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, cudaStream_t stream) {
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
-  bellman::bellman_tick_kernel<<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream) {
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpSmem);
+  if (dbg)
+    bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
+  else
+    bellman::bellman_tick_kernel<false><<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -64,7 +64,7 @@ def pack(cols: dict, pinned: bool = False) -> dict:
                  ("calib_src", "sc_calib_src"), ("record", "sc_record")):
         scs[:ns][f] = cols[c]
     tabs = {}
-    for name in ("tab_L", "tab_I", "tab_fvar", "tab_noise", "tab_fcomp"):
+    for name in ("tab_L", "tab_I", "tab_fvar", "tab_noise", "tab_fcomp", "tab_qnoise"):
         t, k = alloc(np.dtype("<i4"), A.TABLE_N)
         keep.append(k)
         t[:] = cols[name]
@@ -72,6 +72,7 @@ def pack(cols: dict, pinned: bool = False) -> dict:
     out.update(knots=knots, n_knots=nk, traces=traces, n_traces=nt, profiles=profs, n_profiles=npf,
                ctrls=ctrls, n_ctrls=nc, scenarios=scs, n_scenarios=ns, tables=tabs,
                poly_q16=np.asarray(cols["poly_q16"], dtype=np.int64), n_segments=int(cols["n_segments"]),
+               quality=np.asarray(cols["quality"], dtype=np.uint32),
                _keep=keep)
     return out
 
@@ -80,7 +81,8 @@ def make_desc(pk: dict) -> A.Desc:
     t = pk["tables"]
     m = A.Models(t["tab_L"].ctypes.data, t["tab_I"].ctypes.data, t["tab_fvar"].ctypes.data,
                  t["tab_noise"].ctypes.data, t["tab_fcomp"].ctypes.data,
-                 (C.c_int64 * 3)(*[int(x) for x in pk["poly_q16"]]))
+                 (C.c_int64 * 3)(*[int(x) for x in pk["poly_q16"]]), t["tab_qnoise"].ctypes.data,
+                 (C.c_uint32 * 5)(*[int(x) for x in pk["quality"]]), 0)
     return A.Desc(pk["knots"].ctypes.data, pk["n_knots"], pk["traces"].ctypes.data, pk["n_traces"],
                   pk["profiles"].ctypes.data, pk["n_profiles"], pk["ctrls"].ctypes.data, pk["n_ctrls"], m,
                   pk["scenarios"].ctypes.data, pk["n_scenarios"], pk["n_segments"], 0)
@@ -158,6 +160,19 @@ class Simulator:
         A.check(A.lib().bellman_sim_segment_hist(self.h, C.c_void_p(out.data_ptr()), 1,
                                                  C.c_void_p(_stream_ptr(stream))), self.h)
         return out
+
+    def series(self, sid: int, cap: int | None = None, stream=None):
+        """Debug record mode (scenario.record & RECORD_SECONDS): the per-second
+        rows and the controller log of scenario `sid` (host numpy arrays)."""
+        if cap is None:
+            cap = int(self.pk["scenarios"][sid]["horizon_us"] // 1_000_000 + 2)
+        rows = np.zeros(cap, dtype=A.SECOND_ROW)
+        ctrl = np.zeros(cap, dtype=A.CTRL_ROW)
+        nr, nc = C.c_uint64(), C.c_uint64()
+        A.check(A.lib().bellman_sim_series(self.h, sid, C.c_void_p(rows.ctypes.data), cap, C.byref(nr),
+                                           C.c_void_p(ctrl.ctypes.data), cap, C.byref(nc),
+                                           C.c_void_p(_stream_ptr(stream))), self.h)
+        return rows[: min(nr.value, cap)], ctrl[: min(nc.value, cap)]
 
     def reset(self, stream=None):
         A.check(A.lib().bellman_sim_reset(self.h, C.c_void_p(_stream_ptr(stream))), self.h)

@@ -46,7 +46,8 @@ def compare(gpu_rec, orc: dict, sid: int, hist_row=None):
     if not (int(gpu_rec["flags"]) & 0x100):
         errs.append("record not written (FLAG_DONE missing)")
     if hist_row is not None:
-        for name, lo, hi in (("hist_e2e", 0, 896), ("hist_ttft", 896, 1792), ("hist_r", 1792, 2304)):
+        for name, lo, hi in (("hist_e2e", 0, 896), ("hist_ttft", 896, 1792), ("hist_r", 1792, 2304),
+                             ("hist_q_active", 2304, 2505), ("hist_q_inactive", 2505, 2706)):
             if not np.array_equal(hist_row[lo:hi].astype(np.int64), orc[name].astype(np.int64)):
                 d = np.nonzero(hist_row[lo:hi].astype(np.int64) != orc[name].astype(np.int64))[0][:5]
                 errs.append(f"{name} differs at bins {d.tolist()}")

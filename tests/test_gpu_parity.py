@@ -166,7 +166,42 @@ def test_c2_full_bench_config():
         s = w.scenarios[sid].segment
         want_seg[s, :896] += o["hist_e2e"]
         want_seg[s, 896:1792] += o["hist_ttft"]
-        want_seg[s, 1792:] += o["hist_r"]
+        want_seg[s, 1792:2304] += o["hist_r"]
+        want_seg[s, 2304:2505] += o["hist_q_active"]
+        want_seg[s, 2505:2706] += o["hist_q_inactive"]
     _assert_ok(bad)
     assert np.array_equal(seg.astype(np.int64), want_seg)
     assert sim.last_launches == 1
+
+
+def test_debug_series_rows_and_controller_log():
+    """NEXT-1 debug record mode: per-second rows (attribution S:382) and
+    the controller log equal the oracle's element by element."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    ws = [W.config_c1(), W.config_c3(n_seeds=1), W.config_c2(n_seeds=1, rates=[0.5, 2.5, 6.0])]
+    for w in ws:
+        sel = list(range(0, w.n_scenarios, max(1, w.n_scenarios // 12)))
+        for sid in sel:
+            w.scenarios[sid].record |= 2
+        cols = w.columns()
+        sim = Simulator(cols)
+        sim.run()
+        torch.cuda.synchronize()
+        st = sim.stats()
+        b = oracle.Bound(cols)
+        for sid in sel:
+            o = oracle.run_scenario(b, sid, rows_cap=100000, ctrl_log_cap=100000)
+            assert not compare(st[sid], o, sid), (w.name, sid)
+            rows, ctrl = sim.series(sid)
+            orow = o["rows"]
+            assert len(rows) == len(orow), (w.name, sid, len(rows), len(orow))
+            for f in orow.dtype.names:
+                assert np.array_equal(rows[f].astype(np.int64), orow[f].astype(np.int64)), (w.name, sid, f)
+            oc = o["ctrl_log"]
+            assert len(ctrl) == len(oc), (w.name, sid)
+            for g, e in zip(ctrl, oc):
+                assert (int(g["second"]), int(g["sample"]), int(g["k"]), int(g["r_bp"]), int(g["active"]),
+                        int(g["A"])) == (e["second"], e["sample"], e["k"], e["r_bp"], e["active"], e["A"])

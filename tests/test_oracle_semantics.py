@@ -225,3 +225,21 @@ def test_bruteforce_controller(orc):
             r = d["requests"][i]
             assert (r["admit_us"], r["done_us"], r["R"], r["r_bp"]) == \
                    (bf["admit"][i], bf["done"][i], bf["R"][i], bf["r_bp"][i]), (case, i)
+
+
+def test_similarity_model_examples(orc):
+    """NEXT-2 quality model, SPEC S:151-153: inactive, reduction 0 -> 88;
+    active, reduction 8 % -> 87; active, reduction 40 % (= decay_end) -> 65;
+    S:158 non-increasing in the reduction beyond the safe window; S:159 clamps."""
+    assert orc.similarity(500, 500, False) == 8800
+    assert orc.similarity(500, 460, True) == 8700
+    assert orc.similarity(500, 300, True) == 6500
+    prev = None
+    for R in range(400, 200, -1):  # reduction 20 % .. 60 %
+        s = orc.similarity(500, R, True)
+        assert prev is None or s <= prev
+        prev = s
+    assert orc.similarity(500, 450, True, noise=3000) == 10000
+    assert orc.similarity(500, 100, True, noise=-9000) == 0
+    # linear decay midpoint: reduction 30 % -> 87 - 22/2 = 76 points
+    assert orc.similarity(1000, 700, True) == 7600

@@ -68,7 +68,7 @@ def _round_half_up(x):
 def quantile_tables(L_mean=500.0, L_sd=80.0, L_lo=100, L_hi=1200,
                     in_median=9000.0, in_sigma=0.30, in_lo=2000, in_hi=20000,
                     var_sigma=0.0875, var_lo=0.75, var_hi=1.38,
-                    pred_b=36.0, comp_rel_noise=0.05):
+                    pred_b=36.0, comp_rel_noise=0.05, sim_noise_pts=2.0):
     """Workload distributions as quantile tables.
 
     Entry k holds the distribution's quantile at level (k + 1/2)/4096; the
@@ -82,6 +82,8 @@ def quantile_tables(L_mean=500.0, L_sd=80.0, L_lo=100, L_hi=1200,
     * ``noise`` predictor error in words ~ Laplace(0, b=36) (PAPER P:110 "MAE 36";
                 SPEC S:121)
     * ``fcomp`` Q16 compliance factor 1 + 0.05*z
+    * ``qnoise`` similarity-score noise in centi-points ~ N(0, 2 points) (SPEC S:148,
+                S:173 score_noise default 2.0; NEXT-2)
     """
     q = _q(None)
     z = ndtri(q)
@@ -92,17 +94,22 @@ def quantile_tables(L_mean=500.0, L_sd=80.0, L_lo=100, L_hi=1200,
     lap = np.where(q < 0.5, pred_b * np.log(2.0 * q), -pred_b * np.log(2.0 * (1.0 - q)))
     noise = _round_half_up(lap)
     fcomp = np.maximum(_round_half_up(65536.0 * (1.0 + comp_rel_noise * z)), 0)
+    qnoise = np.clip(_round_half_up(100.0 * sim_noise_pts * z), -2047, 2047)
     return {k: v.astype(np.int32) for k, v in
-            dict(L=L, I=I, fvar=fvar, noise=noise, fcomp=fcomp).items()}
+            dict(L=L, I=I, fvar=fvar, noise=noise, fcomp=fcomp, qnoise=qnoise).items()}
 
 
-def constant_tables(L=500, I=9000, fvar=65536, noise=0, fcomp=65536):
+def constant_tables(L=500, I=9000, fvar=65536, noise=0, fcomp=65536, qnoise=0):
     """Degenerate (noise-free) tables, e.g. for closed-form queueing pins."""
     f = lambda v: np.full(TABLE_N, v, dtype=np.int32)
-    return dict(L=f(L), I=f(I), fvar=f(fvar), noise=f(noise), fcomp=f(fcomp))
+    return dict(L=f(L), I=f(I), fvar=f(fvar), noise=f(noise), fcomp=f(fcomp), qnoise=f(qnoise))
 
 
 IDENTITY_POLY_Q16 = (0, 65536, 0)  # compliance realized = N (SPEC S:163 identity default)
+# QualityModel (SPEC S:111-115; NEXT-2) in centi-points / basis points:
+# inactive median 88 and active median 87 (P:193), floor 65 (P:102),
+# safe window 20 % (P:106), linear decay to the floor at 40 % (S:165).
+QUALITY = (8800, 8700, 6500, 2000, 4000)
 
 # ----------------------------------------------------------------------------
 # traces (piecewise-linear lambda(t) knots; µs and milli-RPS integers)
@@ -217,6 +224,7 @@ class Workload:
     ctrls: list = field(default_factory=list)       # list of Ctrl
     tables: dict = field(default_factory=dict)
     poly_q16: tuple = IDENTITY_POLY_Q16
+    quality: tuple = QUALITY
     scenarios: list = field(default_factory=list)
     n_segments: int = 1
     segment_names: list = field(default_factory=list)
@@ -274,6 +282,8 @@ class Workload:
             tab_L=self.tables["L"], tab_I=self.tables["I"], tab_fvar=self.tables["fvar"],
             tab_noise=self.tables["noise"], tab_fcomp=self.tables["fcomp"],
             poly_q16=i64(self.poly_q16),
+            tab_qnoise=self.tables.get("qnoise", np.zeros(TABLE_N, dtype=np.int32)).astype(np.int32),
+            quality=u32(self.quality),
             sc_seed=u32([s.seed_index for s in S]), sc_wid=np.asarray([s.wid for s in S], dtype=np.uint64),
             sc_trace=u32([s.trace for s in S]), sc_profile=u32([s.profile for s in S]),
             sc_ctrl=u32([s.ctrl for s in S]), sc_segment=u32([s.segment for s in S]),
@@ -453,3 +463,28 @@ def shard(n_scenarios: int, rank: int, world: int):
 
 
 CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C5": config_c5}
+
+
+def config_paper_pair(seed_index=0, tables=None, peak=2.5, peak_s=90, valley=0.2, profile="P24"):
+    """The paper's headline experiment (P:183-199, S:495 A4): unbounded run on
+    the 22-minute trace, then the bounded run with T1/T2 calibrated from it
+    (P:185); both debug-recorded (per-second rows + controller log, NEXT-1)."""
+    w = Workload("paper-pair")
+    w.tables = tables or quantile_tables()
+    tr = w.add_trace(paper_trace(peak, peak_s, valley))
+    pr = w.add_profile(profile)
+    off = w.add_ctrl(OFF)
+    on = w.add_ctrl(Ctrl(LAW_MAP, SIG_TBT, 5, 500, 2000, 0, 0, 0, 0, 1, ()))
+    H = (1320 + 600) * US
+    w.scenarios = [
+        Scenario(seed_index, wid=tr, trace=tr, profile=pr, ctrl=off, segment=0, mode=MODE_DRAIN, horizon_us=H,
+                 record=3),
+        Scenario(seed_index, wid=tr, trace=tr, profile=pr, ctrl=on, segment=1, mode=MODE_DRAIN, horizon_us=H,
+                 calib_src=0, record=2),
+    ]
+    w.n_segments = 2
+    w.segment_names = ["unbounded", "bounded"]
+    return w
+
+
+CONFIGS["paper-pair"] = config_paper_pair

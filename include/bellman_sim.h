@@ -51,7 +51,7 @@ typedef enum {
 } bellman_status;
 
 enum { BELLMAN_LAW_OFF = 0, BELLMAN_LAW_CONST = 1, BELLMAN_LAW_MAP = 2, BELLMAN_LAW_STEP = 3 };
-enum { BELLMAN_SIG_TBT = 0, BELLMAN_SIG_E2E = 1, BELLMAN_SIG_SLO = 2 };
+enum { BELLMAN_SIG_TBT = 0, BELLMAN_SIG_E2E = 1, BELLMAN_SIG_SLO = 2, BELLMAN_SIG_TTFT = 3 };
 enum { BELLMAN_MODE_CUTOFF = 0, BELLMAN_MODE_DRAIN = 1 };
 
 /* summary flags */
@@ -98,7 +98,7 @@ typedef struct {
 /* Controller configuration (R3-R5, R22, R38). */
 typedef struct {
   uint32_t law;        /* BELLMAN_LAW_* */
-  uint32_t signal;     /* BELLMAN_SIG_*: per-second avg TBT (default), avg E2E, SLO per-mille */
+  uint32_t signal;     /* BELLMAN_SIG_*: per-second avg TBT (default), avg E2E, SLO per-mille, avg TTFT */
   uint32_t window;     /* moving-average window in samples, 1..8 (5) */
   uint32_t r_min_bp;   /* MAP: r at t1 (5%) */
   uint32_t r_max_bp;   /* MAP: r at t2 (20%), <= 5000 */
@@ -108,7 +108,9 @@ typedef struct {
   uint32_t calibrated; /* 1: t1/t2 = nearest-rank p50/p75 of the paired OFF run's series (a10) */
   uint32_t n_rungs;    /* 0 = continuous; else <= 8 ascending rungs, rung[0] = r_min, last = r_max */
   uint32_t rungs_bp[8];
-} bellman_ctrl;
+  uint32_t bypass_mask;      /* NEXT-3 (S:267 class_policy): bit c -> class c never rewritten */
+  uint32_t min_words_bypass; /* NEXT-3: predicted length below this never rewritten */
+} bellman_ctrl; /* 84 bytes */
 
 /* Workload model inputs (R14, R15, R33): 4096-entry quantile
  * tables drawn with index (u32 >> 20), plus the compliance polynomial. */
@@ -127,7 +129,11 @@ typedef struct {
    * u = 4th word of the request's tag-1 Philox block. */
   const int32_t *qnoise;   /* centi-points, |.| <= 2047 */
   uint32_t quality[5];     /* inactive, active, floor (centi-points), safe_bp, end_bp */
-  uint32_t _pad;
+  /* Request classes (NEXT-3): class = first c with x < class_cum[c], x =
+   * the 20 low bits of the candidate's 3rd Philox word (its top 12 bits draw L);
+   * non-decreasing, class_cum[3] = 2^20.  One class: all 2^20. */
+  uint32_t class_cum[4];
+  uint32_t _pad[3];
 } bellman_models;
 
 typedef struct {
@@ -188,7 +194,8 @@ typedef struct {
   uint64_t sum_queue_us, sum_ttft_us, sum_e2e_us, slo_violations;
   uint32_t e2e_p50_ms, e2e_p99_ms, ttft_p50_ms, ttft_p99_ms, median_r_bp;
   uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
-  uint32_t segment, _pad0;
+  uint32_t segment;
+  uint32_t bypassed; /* NEXT-3: admissions while r > 0 that a bypass rule left unrewritten */
   double energy_j, win_energy_j;
   /* NEXT-2: nearest-rank median similarity (0.5-point bin lower edge, centi-points)
    * of rewritten (active) and not rewritten (inactive) admissions, and their counts */

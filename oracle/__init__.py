@@ -47,9 +47,9 @@ class Inputs(C.Structure):
         ("ctrl_law", u32p), ("ctrl_signal", u32p), ("ctrl_window", u32p), ("ctrl_rmin", u32p),
         ("ctrl_rmax", u32p), ("ctrl_rconst", u32p),
         ("ctrl_t1", u32p), ("ctrl_t2", u32p), ("ctrl_slo_us", u32p), ("ctrl_calibrated", u32p),
-        ("ctrl_nrungs", u32p), ("ctrl_rungs", u32p),
+        ("ctrl_nrungs", u32p), ("ctrl_rungs", u32p), ("ctrl_bypass_mask", u32p), ("ctrl_min_words", u32p),
         ("tab_L", i32p), ("tab_I", i32p), ("tab_fvar", i32p), ("tab_noise", i32p), ("tab_fcomp", i32p),
-        ("poly_q16", i64p), ("tab_qnoise", i32p), ("quality", u32p),
+        ("poly_q16", i64p), ("tab_qnoise", i32p), ("quality", u32p), ("class_cum", u32p),
         ("sc_seed", u32p), ("sc_wid", u64p),
         ("sc_trace", u32p), ("sc_profile", u32p), ("sc_ctrl", u32p), ("sc_segment", u32p), ("sc_mode", u32p),
         ("sc_horizon", i64p), ("sc_w0", i64p), ("sc_w1", i64p),
@@ -60,7 +60,8 @@ class Inputs(C.Structure):
 
 class Request(C.Structure):
     _fields_ = [("a_us", C.c_uint64), ("j", C.c_uint32), ("L", C.c_uint32), ("input", C.c_uint32),
-                ("U", C.c_uint32), ("P", C.c_uint32), ("fcomp_q16", C.c_int32), ("qnoise", C.c_int32)]
+                ("U", C.c_uint32), ("P", C.c_uint32), ("fcomp_q16", C.c_int32), ("qnoise", C.c_int32),
+                ("cls", C.c_uint32)]
 
 
 class Profile(C.Structure):
@@ -72,7 +73,7 @@ class Profile(C.Structure):
 class Ctrl(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp",
                                            "t1", "t2", "slo_us", "calibrated", "n_rungs")] + \
-               [("rungs_bp", C.c_uint32 * 8)]
+               [("rungs_bp", C.c_uint32 * 8), ("bypass_mask", C.c_uint32), ("min_words_bypass", C.c_uint32)]
 
 
 class RunCfg(C.Structure):
@@ -87,7 +88,7 @@ RESULT_U64 = ["ticks", "candidates", "arrivals", "admitted", "served", "rewritte
 RESULT_U32 = ["e2e_p50_ms", "e2e_p99_ms", "ttft_p50_ms", "ttft_p99_ms", "median_r_bp",
               "t1", "t2", "activations", "first_act_s", "last_deact_s", "active_ingests", "flags"]
 RESULT_F64 = ["energy_j", "win_energy_j"]
-RESULT_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive"]
+RESULT_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive", "bypassed"]
 HIST_Q = 201
 RESULT_EXTRA = ["e2e_exact_p50_us", "e2e_exact_p99_us", "ttft_exact_p50_us", "ttft_exact_p99_us",
                 "int_system_us", "int_queue_us", "sum_sojourn_us", "tbt_samples", "tbt_sum_us", "tbt_max_us"]
@@ -201,8 +202,10 @@ def calibrate(series):
 
 
 def make_ctrl(law=0, signal=0, window=5, r_min_bp=500, r_max_bp=2000, r_const_bp=0, t1=0, t2=0,
-              slo_us=0, calibrated=0, rungs=()):
+              slo_us=0, calibrated=0, rungs=(), bypass_mask=0, min_words_bypass=0):
     c = Ctrl(law, signal, window, r_min_bp, r_max_bp, r_const_bp, t1, t2, slo_us, calibrated, len(rungs))
+    c.bypass_mask = bypass_mask
+    c.min_words_bypass = min_words_bypass
     for i, r in enumerate(rungs):
         c.rungs_bp[i] = r
     return c
@@ -224,8 +227,10 @@ class Bound:
              ("ctrl_rmin", np.uint32), ("ctrl_rmax", np.uint32), ("ctrl_rconst", np.uint32),
              ("ctrl_t1", np.uint32), ("ctrl_t2", np.uint32), ("ctrl_slo_us", np.uint32),
              ("ctrl_calibrated", np.uint32), ("ctrl_nrungs", np.uint32), ("ctrl_rungs", np.uint32),
+             ("ctrl_bypass_mask", np.uint32), ("ctrl_min_words", np.uint32),
              ("tab_L", np.int32), ("tab_I", np.int32), ("tab_fvar", np.int32), ("tab_noise", np.int32),
              ("tab_fcomp", np.int32), ("poly_q16", np.int64), ("tab_qnoise", np.int32), ("quality", np.uint32),
+             ("class_cum", np.uint32),
              ("sc_seed", np.uint32), ("sc_wid", np.uint64), ("sc_trace", np.uint32), ("sc_profile", np.uint32),
              ("sc_ctrl", np.uint32), ("sc_segment", np.uint32), ("sc_mode", np.uint32),
              ("sc_horizon", np.int64), ("sc_w0", np.int64), ("sc_w1", np.int64),
@@ -334,7 +339,7 @@ def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_
     for i, q in enumerate(reqs):
         rq[i] = Request(int(q["a_us"]), int(q.get("j", i)), int(q.get("L", q["U"])), int(q["input"]),
                         int(q["U"]), int(q.get("P", q.get("L", q["U"]))), int(q.get("fcomp_q16", 65536)),
-                        int(q.get("qnoise", 0)))
+                        int(q.get("qnoise", 0)), int(q.get("cls", 0)))
     pr = Profile(profile["t0_us"], profile["knee"], profile["slope_us"], profile.get("kv_ns_per_word", 0),
                  profile["max_batch"], profile["prefill_ns_per_word"], profile.get("e_in", 0.05),
                  profile.get("e_out", 0.5), profile.get("p_idle", 300.0))

@@ -67,6 +67,10 @@ int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint6
         r->j = jj;
         r->L = (uint32_t)in->tab_L[u[2] >> 20];
         r->input = (uint32_t)in->tab_I[u[3] >> 20];
+        /* class from the 20 low bits of the word whose top 12 bits drew L (NEXT-3) */
+        r->cls = 3;
+        for (uint32_t c = 0; c < 4; ++c)
+          if ((u[2] & 0xFFFFFu) < in->class_cum[c]) { r->cls = c; break; }
         uint32_t v[4];
         block(in, sid, jj, 1, v);
         int64_t fvar = in->tab_fvar[v[0] >> 20];

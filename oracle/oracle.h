@@ -33,7 +33,7 @@ extern "C" {
 #endif
 
 enum { ORC_LAW_OFF = 0, ORC_LAW_CONST = 1, ORC_LAW_MAP = 2, ORC_LAW_STEP = 3 };
-enum { ORC_SIG_TBT = 0, ORC_SIG_E2E = 1, ORC_SIG_SLO = 2 };
+enum { ORC_SIG_TBT = 0, ORC_SIG_E2E = 1, ORC_SIG_SLO = 2, ORC_SIG_TTFT = 3 };
 enum { ORC_MODE_CUTOFF = 0, ORC_MODE_DRAIN = 1 };
 enum { ORC_FLAG_TRUNCATED = 1, ORC_FLAG_DEGENERATE_CALIB = 2 };
 
@@ -52,10 +52,12 @@ typedef struct {
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
   const uint32_t *ctrl_rungs; /* [n_ctrl][8] */
+  const uint32_t *ctrl_bypass_mask, *ctrl_min_words; /* NEXT-3 class / short-output bypass */
   const int32_t *tab_L, *tab_I, *tab_fvar, *tab_noise, *tab_fcomp; /* [4096] each */
   const int64_t *poly_q16;                                          /* [3] */
   const int32_t *tab_qnoise;  /* [4096] similarity noise, centi-points (NEXT-2) */
   const uint32_t *quality;    /* [5] inactive, active, floor (centi-points), safe, end (bp) */
+  const uint32_t *class_cum;  /* [4] cumulative class thresholds in 2^-20 units (NEXT-3) */
   const uint32_t *sc_seed;
   const uint64_t *sc_wid;
   const uint32_t *sc_trace, *sc_profile, *sc_ctrl, *sc_segment, *sc_mode;
@@ -74,6 +76,7 @@ typedef struct {
   uint32_t P;          /* predicted output words */
   int32_t fcomp_q16;   /* compliance factor */
   int32_t qnoise;      /* similarity-score noise, centi-points (NEXT-2) */
+  uint32_t cls;        /* request class 0..3 (NEXT-3) */
 } orc_request;
 
 typedef struct {
@@ -84,6 +87,8 @@ typedef struct {
 typedef struct {
   uint32_t law, signal, window, r_min_bp, r_max_bp, r_const_bp, t1, t2, slo_us, calibrated, n_rungs;
   uint32_t rungs_bp[8];
+  uint32_t bypass_mask;      /* bit c: class c is never rewritten (S:267 class_policy) */
+  uint32_t min_words_bypass; /* predicted length below this is never rewritten */
 } orc_ctrl;
 
 typedef struct {
@@ -103,6 +108,7 @@ typedef struct {
   uint32_t t1, t2, activations, first_act_s, last_deact_s, active_ingests, flags;
   double energy_j, win_energy_j;
   uint32_t sim_active_p50, sim_inactive_p50, scored_active, scored_inactive; /* NEXT-2, centi-points */
+  uint32_t bypassed; /* NEXT-3: admissions while r > 0 left unrewritten by a bypass rule */
   /* ---- self-checks the GPU never computes ---- */
   uint64_t e2e_exact_p50_us, e2e_exact_p99_us, ttft_exact_p50_us, ttft_exact_p99_us;
   uint64_t int_system_us;  /* integral of (queued + in_system) dt, µs*requests */

@@ -302,11 +302,14 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint64_t *sec_e2e_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_e2e_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_slo_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_ttft_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_ttft_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
   cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
   if (!rs || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
-      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || ((cfg->record & 2) && !rows))
+      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt ||
+      ((cfg->record & 2) && !rows))
     goto out;
   if (cs.law == ORC_LAW_CONST) cs.r = ctrl->r_const_bp; /* S:320-326 constant policy */
 
@@ -328,6 +331,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       uint64_t cnt, sum;                                                                 \
       if (next_sec >= n_sec) continue;                                                   \
       if (ctrl->signal == ORC_SIG_TBT) { cnt = sec_tbt_cnt[next_sec]; sum = sec_tbt_sum[next_sec]; } \
+      else if (ctrl->signal == ORC_SIG_TTFT) { cnt = sec_ttft_cnt[next_sec]; sum = sec_ttft_sum[next_sec]; } \
       else if (ctrl->signal == ORC_SIG_E2E) { cnt = sec_e2e_cnt[next_sec]; sum = sec_e2e_sum[next_sec]; } \
       else { cnt = sec_e2e_cnt[next_sec]; sum = 1000 * sec_slo_cnt[next_sec]; }          \
       if (cnt == 0) continue; /* a second with no samples is a gap */     \
@@ -422,6 +426,8 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         res->words_out++;
         if (in_window(T, cfg)) res->win_words_out++;
         res->sum_ttft_us += ttft;
+        sec_ttft_sum[s_idx] += ttft;
+        sec_ttft_cnt[s_idx] += 1;
         ttft_v[n_ttft++] = ttft;
         res->hist_ttft[orc_lat_bin(ttft / 1000)]++;
         if (rows) {
@@ -466,6 +472,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       while (in_sys < prof->max_batch && q_head < q_tail) {
         uint32_t m = queue[q_head++];
         uint32_t r = cs.r;
+        /* NEXT-3 bypass: class policy or a short predicted output */
+        if (r > 0 && (((ctrl->bypass_mask >> req[m].cls) & 1u) || req[m].P < ctrl->min_words_bypass)) {
+          r = 0;
+          res->bypassed++;
+        }
         rs[m].admit = T;
         rs[m].r_bp = r;
         rs[m].R = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
@@ -622,6 +633,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
 out:
   free(rs); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
+  free(sec_ttft_sum); free(sec_ttft_cnt);
   free(h.v); free(cs.samples); free(rows);
   return rc;
 }
@@ -651,6 +663,8 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   c->calibrated = in->ctrl_calibrated[ci];
   c->n_rungs = in->ctrl_nrungs[ci];
   for (int k = 0; k < 8; ++k) c->rungs_bp[k] = in->ctrl_rungs[8 * ci + k];
+  c->bypass_mask = in->ctrl_bypass_mask[ci];
+  c->min_words_bypass = in->ctrl_min_words[ci];
   cfg->mode = in->sc_mode[sid];
   cfg->horizon_us = in->sc_horizon[sid];
   cfg->w0_us = in->sc_w0[sid];

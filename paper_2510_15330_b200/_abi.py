@@ -27,7 +27,8 @@ PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv
                     ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("e_in_j_per_word", "<f8"),
                     ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
 CTRL = np.dtype([(n, "<u4") for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp", "t1", "t2",
-                                       "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))])
+                                       "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))] +
+                [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")])
 SCENARIO = np.dtype([("seed_index", "<u4"), ("trace", "<u4"), ("wid", "<u8"), ("profile", "<u4"), ("ctrl", "<u4"),
                      ("segment", "<u4"), ("mode", "<u4"), ("horizon_us", "<i8"), ("w0_us", "<i8"),
                      ("w1_us", "<i8"), ("calib_src", "<u4"), ("record", "<u4")])
@@ -37,7 +38,7 @@ STATS_U64 = ["scenario_id", "ticks", "candidates", "arrivals", "admitted", "serv
              "sum_queue_us", "sum_ttft_us", "sum_e2e_us", "slo_violations"]
 STATS_U32 = ["e2e_p50_ms", "e2e_p99_ms", "ttft_p50_ms", "ttft_p99_ms", "median_r_bp",
              "t1", "t2", "activations", "first_act_s", "last_deact_s", "active_ingests", "flags",
-             "segment", "_pad0"]
+             "segment", "bypassed"]
 STATS_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive"]
 STATS = np.dtype([(n, "<u8") for n in STATS_U64] + [(n, "<u4") for n in STATS_U32] +
                  [("energy_j", "<f8"), ("win_energy_j", "<f8")] + [(n, "<u4") for n in STATS_Q])
@@ -49,13 +50,14 @@ CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp"
 RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
 assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 48
-assert CTRL.itemsize == 76 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
+assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
 
 
 class Models(C.Structure):
     _fields_ = [("L_words", C.c_void_p), ("I_words", C.c_void_p), ("fvar_q16", C.c_void_p),
                 ("noise", C.c_void_p), ("fcomp_q16", C.c_void_p), ("poly_q16", C.c_int64 * 3),
-                ("qnoise", C.c_void_p), ("quality", C.c_uint32 * 5), ("_pad", C.c_uint32)]
+                ("qnoise", C.c_void_p), ("quality", C.c_uint32 * 5), ("class_cum", C.c_uint32 * 4),
+                ("_pad", C.c_uint32 * 3)]
 
 
 class Desc(C.Structure):

@@ -68,6 +68,9 @@ static bellman_status validate(const bellman_sim_desc *d) {
     return fail(nullptr, BELLMAN_EINVAL, "quality: need floor <= active <= inactive <= 10000");
   if (!(m.quality[3] > 0 && m.quality[3] < m.quality[4] && m.quality[4] <= 10000))
     return fail(nullptr, BELLMAN_EINVAL, "quality: need 0 < safe_bp < end_bp <= 10000");
+  if (!(m.class_cum[0] <= m.class_cum[1] && m.class_cum[1] <= m.class_cum[2] && m.class_cum[2] <= m.class_cum[3] &&
+        m.class_cum[3] == (1u << 20)))
+    return fail(nullptr, BELLMAN_EINVAL, "class_cum must be non-decreasing with class_cum[3] = 2^20");
   for (int i = 0; i < BELLMAN_TABLE_N; ++i) {
     if (m.L_words[i] < 1 || m.L_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "L table[%d] out of range", i);
     if (m.I_words[i] < 1 || m.I_words[i] > 65535) return fail(nullptr, BELLMAN_EINVAL, "I table[%d] out of range", i);
@@ -105,7 +108,8 @@ static bellman_status validate(const bellman_sim_desc *d) {
   for (uint32_t i = 0; i < d->n_ctrls; ++i) {
     const bellman_ctrl &c = d->ctrls[i];
     if (c.law > BELLMAN_LAW_STEP) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown law", i);
-    if (c.signal > BELLMAN_SIG_SLO) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
+    if (c.signal > BELLMAN_SIG_TTFT) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
+    if (c.bypass_mask > 15u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: bypass_mask has bits beyond 4 classes", i);
     if (c.window < 1 || c.window > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: window not in 1..8", i);
     if (c.n_rungs > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: more than 8 rungs", i);
     if (c.law == BELLMAN_LAW_CONST && c.r_const_bp > 5000) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: r_const > 5000 bp", i);
@@ -336,6 +340,9 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.q_floor = desc->models.quality[2];
   P.q_safe = desc->models.quality[3];
   P.q_end = desc->models.quality[4];
+  P.class_cum0 = desc->models.class_cum[0];
+  P.class_cum1 = desc->models.class_cum[1];
+  P.class_cum2 = desc->models.class_cum[2];
   P.log2tab = (const uint2 *)(ws + L.off_log2);
   P.poly0 = desc->models.poly_q16[0];
   P.poly1 = desc->models.poly_q16[1];

@@ -45,6 +45,7 @@ struct Params {
   const uint2 *log2tab;                             // (T[i], T[i+1]-T[i]), i < 4096
   int64_t poly0, poly1, poly2;
   uint32_t q_inactive, q_active, q_floor, q_safe, q_end;  // quality model (NEXT-2)
+  uint32_t class_cum0, class_cum1, class_cum2;            // request classes (NEXT-3)
   const uint32_t *series_slot;  // [n_scenarios] slot or NONE
   const uint64_t *series_off;   // [n_slots] word offset into series
   const uint32_t *series_cap;   // [n_slots]

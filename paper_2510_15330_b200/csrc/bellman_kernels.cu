@@ -120,13 +120,18 @@ struct Cold {
   uint32_t activations, first_act, last_deact, active_ingests;
   uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
   uint32_t k0, wid_lo, wid_hi;
-  uint32_t t0, knee, slope, slo_us;  // read-only after init
+  uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
+
 };
 
-struct alignas(16) WarpSmem {
-  WarpHist h;
-  Cold c;
-};
+// Write-only counters (a8) are lane-distributed: counter i lives in lane i's
+// register `ctr` and is bumped with a predicated add of a warp-uniform value
+// (no branch, no memory), then read once by shuffle in the epilogue.
+enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL = 3, CT_WIN_SERVED = 4, CT_WORDS_IN = 5, CT_IDLE = 6, CT_WIN_WORDS_IN = 7, CT_WIN_IDLE = 8, CT_SUM_QUEUE = 9, CT_SUM_TTFT = 10, CT_SUM_E2E = 11, CT_N };
+
+// One Cold block per warp of the CTA, in static shared memory so that every
+// access is a 32-bit LDS/STS off a known base (no generic pointer).
+__shared__ Cold g_cold[kWarpsPerBlock];
 
 // ---------------------------------------------------------------------------
 // The per-scenario simulation.  Every scalar is warp-uniform.  Derived
@@ -136,9 +141,13 @@ struct alignas(16) WarpSmem {
 // of the queue head.
 template <bool DBG>
 struct Sim {
-  __device__ explicit Sim(Cold &cold) : c(cold) {}
+  __device__ explicit Sim(uint32_t w) : wid(w) {}
+  __device__ __forceinline__ Cold &cold() const { return g_cold[wid]; }
+  uint64_t ctr;  // lane-distributed write-only counters (CT_*)
+  __device__ __forceinline__ void cadd(uint32_t i, uint64_t v) { ctr += (lane == i) ? v : 0ull; }
+  __device__ __forceinline__ uint64_t cget(uint32_t i) const { return __shfl_sync(FULL, ctr, i); }
   uint32_t lane;
-  Cold &c;  // per-warp shared-memory part of the state (cold fields)
+  uint32_t wid;  // warp index in the CTA: selects this warp's Cold block
   // ---- scenario (a1)
   uint64_t H;
   // profile
@@ -156,10 +165,9 @@ struct Sim {
   // debug record mode (NEXT-1): per-second rows and controller log, NULL when off
   bellman_second_row *dbg;
   // profile constants used at events
-  uint32_t pf_ns;
+  uint32_t pf_ns, t0, knee, slope, slo_us;
   // ---- counters (a8), updated at events
-  uint32_t admitted, served, rewritten, slo_viol, win_served, last_j;
-  uint64_t words_in, idle, win_words_in, win_idle, sum_queue, sum_ttft, sum_e2e;
+  uint32_t last_j;
   // ---- serving state (a4, a5, a7)
   uint64_t T;
   uint32_t busy;
@@ -182,7 +190,7 @@ struct Sim {
   // ---- generator / queue head (a2)
   uint32_t buf_h, buf_n;
   uint64_t buf_a;      // lane-parallel buffer of upcoming arrivals
-  uint32_t buf_in;     // input words
+  uint32_t buf_in;     // input words | request class << 16 (NEXT-3)
   uint32_t buf_U;      // realized unbounded length (a3)
   uint32_t buf_P;      // predicted length (a3)
   uint32_t buf_fcq;    // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
@@ -195,11 +203,11 @@ struct Sim {
   // Refill the 32-entry arrival buffer with the next accepted candidates.
   __device__ __forceinline__ void refill(const Params &p) {
     // shared-memory generator state: read by all lanes, written back by lane 0 only
-    uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
-    uint32_t gen_acc = c.gen_acc;
-    uint64_t gen_tau = c.gen_tau;
-    const uint32_t n_seg = c.n_seg, gen_cap = c.gen_cap, k0 = c.k0, wid_lo = c.wid_lo, wid_hi = c.wid_hi;
-    const DevSeg *segs = c.segs;
+    uint32_t gen_done = cold().gen_done, gen_seg = cold().gen_seg, gen_fresh = cold().gen_fresh, gen_j = cold().gen_j;
+    uint32_t gen_acc = cold().gen_acc;
+    uint64_t gen_tau = cold().gen_tau;
+    const uint32_t n_seg = cold().n_seg, gen_cap = cold().gen_cap, k0 = cold().k0, wid_lo = cold().wid_lo, wid_hi = cold().wid_hi;
+    const DevSeg *segs = cold().segs;
     buf_h = 0;
     buf_n = 0;
     while (!gen_done && buf_n == 0) {
@@ -248,13 +256,16 @@ struct Sim {
       const uint32_t s = src < 32u ? src : 0u;
       buf_a = __shfl_sync(FULL, tau, s);
       const uint32_t at = __shfl_sync(FULL, attr, s);
+      const uint32_t uz = __shfl_sync(FULL, u.z, s);
       buf_j = __shfl_sync(FULL, jj, s);
       buf_n = cnt;
       if (DBG && dbg && lane < cnt && buf_a < H) atomicAdd(&row(buf_a)->arrivals, 1u);
       // a3: the accepted request's own draws (tag 1), lane-parallel, ahead of admission
       {
         const uint32_t L = at & 0xFFFFu;
-        buf_in = at >> 16;
+        const uint32_t x = uz & 0xFFFFFu;  // class draw from the bits below L's index
+        const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
+        buf_in = (at >> 16) | (cls << 16);
         const uint4 v = philox(k0, kSeedHi, buf_j, 1u, wid_lo, wid_hi);
         const uint32_t fvar = (uint32_t)__ldg(&p.tabF[v.x >> 20]);
         const uint64_t U = ((uint64_t)L * fvar + 32768u) >> 16;  // S:139, R14
@@ -275,12 +286,12 @@ struct Sim {
     }
     head_t = buf_n ? __shfl_sync(FULL, buf_a, 0) : INF;
     if (lane == 0) {
-      c.gen_done = gen_done;
-      c.gen_seg = gen_seg;
-      c.gen_fresh = gen_fresh;
-      c.gen_j = gen_j;
-      c.gen_acc = gen_acc;
-      c.gen_tau = gen_tau;
+      cold().gen_done = gen_done;
+      cold().gen_seg = gen_seg;
+      cold().gen_fresh = gen_fresh;
+      cold().gen_j = gen_j;
+      cold().gen_acc = gen_acc;
+      cold().gen_tau = gen_tau;
     }
     __syncwarp();
   }
@@ -288,20 +299,20 @@ struct Sim {
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
     // shared-memory controller state: read by all lanes, written back by lane 0 only
-    if (c.series) {
-      const uint32_t n = c.series_n;
+    if (cold().series) {
+      const uint32_t n = cold().series_n;
       if (lane == 0) {
-        if (n < c.series_cap) c.series[n] = x;
-        else c.flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
-        c.series_n = n + 1u;
+        if (n < cold().series_cap) cold().series[n] = x;
+        else cold().flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+        cold().series_n = n + 1u;
       }
       __syncwarp();
     }
-    if (c.law != BELLMAN_LAW_MAP && c.law != BELLMAN_LAW_STEP) return;
-    const uint32_t window = c.window, pos = c.ring_pos, t1 = c.t1;
-    uint32_t k = c.ring_n, rung = c.rung;
-    const uint32_t was_active = c.active;
-    uint64_t A = c.ringA;
+    if (cold().law != BELLMAN_LAW_MAP && cold().law != BELLMAN_LAW_STEP) return;
+    const uint32_t window = cold().window, pos = cold().ring_pos, t1 = cold().t1;
+    uint32_t k = cold().ring_n, rung = cold().rung;
+    const uint32_t was_active = cold().active;
+    uint64_t A = cold().ringA;
     const uint32_t ev = __shfl_sync(FULL, ring, pos);
     if (lane == pos) ring = x;
     if (k < window) {
@@ -313,36 +324,36 @@ struct Sim {
     const bool act = A >= (uint64_t)k * t1;  // non-strict (R38)
     uint32_t nr = 0;
     if (act) {
-      if (c.law == BELLMAN_LAW_MAP) {
-        const uint32_t rmin = c.rmin, rmax = c.rmax;
-        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (c.t2 - t1));
+      if (cold().law == BELLMAN_LAW_MAP) {
+        const uint32_t rmin = cold().rmin, rmax = cold().rmax;
+        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (cold().t2 - t1));
         if (rr > rmax) rr = rmax;
         nr = (uint32_t)rr;
-        const uint32_t nrungs = c.nrungs;
+        const uint32_t nrungs = cold().nrungs;
         if (nrungs) {  // largest rung <= r (R5)
           const uint32_t le = __ballot_sync(FULL, lane < nrungs && rungs_lane <= nr);
           nr = __shfl_sync(FULL, rungs_lane, 31 - __clz(le | 1u));
         }
       } else {  // STEP
-        rung = was_active ? (rung + 1u < c.nrungs ? rung + 1u : rung) : 0u;
+        rung = was_active ? (rung + 1u < cold().nrungs ? rung + 1u : rung) : 0u;
         nr = __shfl_sync(FULL, rungs_lane, rung);
       }
     }
-    const uint32_t nctrl = c.dbg_nctrl;
+    const uint32_t nctrl = cold().dbg_nctrl;
     if (lane == 0) {
-      c.ring_n = k;
-      c.ringA = A;
-      c.ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
-      c.rung = rung;
-      c.active = act;
+      cold().ring_n = k;
+      cold().ringA = A;
+      cold().ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
+      cold().rung = rung;
+      cold().active = act;
       if (act && !was_active) {
-        c.activations++;
-        if (c.first_act == BELLMAN_NONE) c.first_act = second;
+        cold().activations++;
+        if (cold().first_act == BELLMAN_NONE) cold().first_act = second;
       }
-      if (!act && was_active) c.last_deact = second;
-      if (act) c.active_ingests++;
+      if (!act && was_active) cold().last_deact = second;
+      if (act) cold().active_ingests++;
       if (DBG && dbg) {
-        if (nctrl < c.dbg_cap) {
+        if (nctrl < cold().dbg_cap) {
           bellman_ctrl_row cr;
           cr.second = second;
           cr.sample = x;
@@ -351,9 +362,9 @@ struct Sim {
           cr.active = act;
           cr._pad = 0;
           cr.A = A;
-          c.dbg_ctrl[nctrl] = cr;
+          cold().dbg_ctrl[nctrl] = cr;
         }
-        c.dbg_nctrl = nctrl + 1u;
+        cold().dbg_nctrl = nctrl + 1u;
       }
     }
     __syncwarp();
@@ -371,7 +382,7 @@ struct Sim {
 
   __device__ __forceinline__ bellman_second_row *row(uint64_t t) const {
     const uint64_t sidx = t / kUs;
-    return dbg + (sidx < c.dbg_cap ? sidx : c.dbg_cap - 1u);
+    return dbg + (sidx < cold().dbg_cap ? sidx : cold().dbg_cap - 1u);
   }
 
   // idle interval [a, b) split over the seconds it overlaps (debug rows only)
@@ -384,8 +395,8 @@ struct Sim {
   }
 
   __device__ __forceinline__ void update_window() {
-    win_now = T >= c.w0 && T < c.w1;
-    win_next = T < c.w0 ? c.w0 : (T < c.w1 ? c.w1 : INF);
+    win_now = T >= cold().w0 && T < cold().w1;
+    win_next = T < cold().w0 ? cold().w0 : (T < cold().w1 ? cold().w1 : INF);
     stop_static = H < win_next ? H : win_next;
   }
 
@@ -398,7 +409,7 @@ struct Sim {
 
   // B changed: cost base and per-iteration KV growth
   __device__ __forceinline__ void batch_changed() {
-    cbase = c.t0 + c.slope * (B > c.knee ? B - c.knee : 0u);
+    cbase = t0 + slope * (B > knee ? B - knee : 0u);
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
     kstep_r = ks - kstep_q * 1000u;
@@ -425,11 +436,11 @@ struct Sim {
 
   // ------------------------------------------------------------------ a5
   __device__ __forceinline__ void complete_sig(uint64_t sum_e2e_w, uint32_t n, uint32_t nslo) {
-    if (signal == BELLMAN_SIG_TBT) return;
+    if (signal == BELLMAN_SIG_TBT || signal == BELLMAN_SIG_TTFT) return;
     if (signal == BELLMAN_SIG_E2E) {
       acc_sum += sum_e2e_w;
       acc_cnt += n;
-    } else {
+    } else if (signal == BELLMAN_SIG_SLO) {
       acc_sum += 1000ull * nslo;
       acc_cnt += n;
     }
@@ -449,7 +460,7 @@ struct Sim {
       atomicAdd(&w->words_out, B);
       atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * iter_d + iter_align);
     }
-    __syncwarp();
+    if (DBG) __syncwarp();
     // every participant emitted one word: K += B
     kr += kstep_r;
     kq += kstep_q;
@@ -468,7 +479,7 @@ struct Sim {
         if (cpl) {
           const uint64_t e = Tn - sa[s];
           e2e_l += e;
-          nslo += e > c.slo_us;
+          nslo += e > slo_us;
           kdrop += sin[s] + sR[s];
           atomicAdd(&h.e2e[lat_bin(e / 1000u)], 1u);
           sph[s] = PH_EMPTY;
@@ -479,15 +490,15 @@ struct Sim {
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
       kv_sub((uint64_t)kv * __reduce_add_sync(FULL, kdrop));
-      served += ndone;
-      sum_e2e += se;
-      slo_viol += ns;
-      if (win_now) win_served += ndone;
+      cadd(CT_SERVED, ndone);
+      cadd(CT_SUM_E2E, se);
+      cadd(CT_SLO_VIOL, ns);
+      if (win_now) cadd(CT_WIN_SERVED, ndone);
       if (DBG && dbg && lane == 0) {
         atomicAdd(&row(Tn)->completions, ndone);
         atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
       }
-      __syncwarp();
+      if (DBG) __syncwarp();
       in_sys -= ndone;
       B -= ndone;
       batch_changed();
@@ -511,7 +522,7 @@ struct Sim {
         atomicAdd(&h.ttft[lat_bin(tt / 1000u)], 1u);
         if (sR[s] == 1u) {  // R9: completes at the prefill end
           e2e_l += tt;
-          nslo += tt > c.slo_us;
+          nslo += tt > slo_us;
           n1++;
           atomicAdd(&h.e2e[lat_bin(tt / 1000u)], 1u);
           sph[s] = PH_EMPTY;
@@ -525,29 +536,33 @@ struct Sim {
     const uint32_t m = __reduce_min_sync(FULL, mpf);
     next_pf = (m == 0xffffffffu) ? INF : Tn + m;
     const uint64_t st = warp_sum_split(ttft_l);
-    sum_ttft += st;
+    cadd(CT_SUM_TTFT, st);
     words_out += nfirst;
+    if (signal == BELLMAN_SIG_TTFT) {  // NEXT-3 signal: mean TTFT of the second's first words
+      acc_sum += st;
+      acc_cnt += nfirst;
+    }
     if (DBG && dbg && lane == 0) {
       atomicAdd(&row(Tn)->first_tokens, nfirst);
       atomicAdd(&row(Tn)->words_out, nfirst);
       atomicAdd((unsigned long long *)&row(Tn)->sum_ttft_us, (unsigned long long)st);
     }
-    __syncwarp();
+    if (DBG) __syncwarp();
     if (win_now) win_words_out += nfirst;
     n_ready += __reduce_add_sync(FULL, nrdy);
     const uint32_t nc = __reduce_add_sync(FULL, n1);
     if (nc) {
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
-      served += nc;
-      sum_e2e += se;
-      slo_viol += ns;
-      if (win_now) win_served += nc;
+      cadd(CT_SERVED, nc);
+      cadd(CT_SUM_E2E, se);
+      cadd(CT_SLO_VIOL, ns);
+      if (win_now) cadd(CT_WIN_SERVED, nc);
       if (DBG && dbg && lane == 0) {
         atomicAdd(&row(Tn)->completions, nc);
         atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
       }
-      __syncwarp();
+      if (DBG) __syncwarp();
       in_sys -= nc;
       complete_sig(se, nc, ns);
     }
@@ -567,21 +582,29 @@ struct Sim {
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
       uint64_t q_l = 0;
-      uint32_t win_l = 0, mpf = 0xffffffffu;
+      uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0;
+      // NEXT-3 bypass rules, read once per admission point
+      const uint32_t bmask = cold().bypass_mask, minw = cold().min_words;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t rank = s == 0 ? rank0 : rank1;
         const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
         const uint32_t src = (buf_h + (mine ? rank : 0u)) & 31u;
         const uint64_t a = __shfl_sync(FULL, buf_a, src);
-        const uint32_t in = __shfl_sync(FULL, buf_in, src);
+        const uint32_t inc = __shfl_sync(FULL, buf_in, src);
         const uint32_t U = __shfl_sync(FULL, buf_U, src);
         const uint32_t P = __shfl_sync(FULL, buf_P, src);
         const uint32_t fcq = __shfl_sync(FULL, buf_fcq, src);
         if (mine) {
+          const uint32_t in = inc & 0xFFFFu;
+          // r applied to this request: the warp-uniform r unless a bypass rule holds
+          const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
+          const uint32_t ra = byp ? 0u : r;
+          n_byp += byp;
           uint32_t R = U;
-          if (r > 0) {  // a7 rewrite: N = round(P (1 - r)), realized = round(poly(N) Fcomp)
-            int64_t N = (int64_t)(((uint64_t)P * (10000u - r) + 5000u) / 10000u);
+          if (ra > 0) {  // a7 rewrite: N = round(P (1 - r)), realized = round(poly(N) Fcomp)
+            n_rw++;
+            int64_t N = (int64_t)(((uint64_t)P * (10000u - ra) + 5000u) / 10000u);
             if (N < 1) N = 1;
             const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
             const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
@@ -589,10 +612,11 @@ struct Sim {
             if (x < 1) x = 1;
             if (x > (1 << 24)) x = 1 << 24;
             R = (uint32_t)x;
+            atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
           }
           {  // NEXT-2: similarity vs the unbounded length
             int32_t base = (int32_t)p.q_inactive;
-            if (r > 0) {
+            if (ra > 0) {
               const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
               if (num <= (int64_t)p.q_safe * den) base = (int32_t)p.q_active;
               else if (num >= (int64_t)p.q_end * den) base = (int32_t)p.q_floor;
@@ -603,7 +627,7 @@ struct Sim {
             int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
             sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
             const uint32_t qb = (uint32_t)sc / 50u;
-            atomicAdd(r > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
+            atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
           }
           uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
           if (pf < 1) pf = 1;
@@ -620,27 +644,31 @@ struct Sim {
       const uint32_t mnew = __reduce_min_sync(FULL, mpf);
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
       const uint32_t win = __reduce_add_sync(FULL, win_l);
-      words_in += win;
-      if (win_now) win_words_in += win;
+      cadd(CT_WORDS_IN, win);
+      if (win_now) cadd(CT_WIN_WORDS_IN, win);
       const uint64_t sq = warp_sum_split(q_l);
-      sum_queue += sq;
+      cadd(CT_SUM_QUEUE, sq);
       if (DBG && dbg && lane == 0) {
         atomicAdd(&row(Tn)->admitted, k);
         atomicAdd(&row(Tn)->words_in, win);
         atomicAdd((unsigned long long *)&row(Tn)->sum_queue_us, (unsigned long long)sq);
       }
-      __syncwarp();
+      if (DBG) __syncwarp();
       if (r > 0) {
-        rewritten += k;
-        if (lane == 0) atomicAdd(&h.r[r / 10u < BELLMAN_HIST_R ? r / 10u : BELLMAN_HIST_R - 1], k);
+        cadd(CT_REWRITTEN, __reduce_add_sync(FULL, n_rw));
+        const uint32_t nb = __reduce_add_sync(FULL, n_byp);
+        if (nb) {
+          if (lane == 0) cold().bypassed += nb;
+          __syncwarp();
+        }
       }
       last_j = __shfl_sync(FULL, buf_j, (buf_h + k - 1u) & 31u) + 1u;
       in_sys += k;
-      admitted += k;
+      cadd(CT_ADMITTED, k);
       buf_h += k;
       if (buf_h < buf_n) {
         head_t = __shfl_sync(FULL, buf_a, buf_h & 31u);
-      } else if (!c.gen_done) {
+      } else if (!cold().gen_done) {
         refill(p);
       } else {
         head_t = INF;
@@ -652,7 +680,7 @@ struct Sim {
   // ------------------------------------------------------------------ a4/a5 leap
   // Execute in bulk the longest run of iterations whose ends are uneventful —
   // no completion (index < next_done), no prefill end, no admission (head
-  // arrival still in the future or no free slot), no c.window / horizon
+  // arrival still in the future or no free slot), no cold().window / horizon
   // boundary — exactly as the per-iteration path would: each emits B words
   // with TBT gap d_m = c + floor(kv (K + m B) / 1000) and grows K by B.  A
   // second boundary met inside the run is rolled in place (ingest), as the
@@ -705,7 +733,7 @@ struct Sim {
           atomicAdd(&w->words_out, (uint32_t)words);
           atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * used);
         }
-        __syncwarp();
+        if (DBG) __syncwarp();
         done += n;
       }
       if (done == nmax) break;
@@ -796,8 +824,7 @@ template <bool DBG>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
-  WarpSmem &ws = reinterpret_cast<WarpSmem *>(smem_raw)[threadIdx.x >> 5];
-  WarpHist &h = ws.h;
+  WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
   for (;;) {
     uint32_t kidx = 0;
     if (lane == 0) kidx = atomicAdd(p.counter, 1u);
@@ -811,80 +838,83 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
     // ---- a1: scenario decode
-    Sim<DBG> S(ws.c);
+    Sim<DBG> S(threadIdx.x >> 5);
     S.lane = lane;
-    S.c.k0 = sc.seed_index;
-    S.c.wid_lo = (uint32_t)sc.wid;
-    S.c.wid_hi = (uint32_t)(sc.wid >> 32);
+    S.cold().k0 = sc.seed_index;
+    S.cold().wid_lo = (uint32_t)sc.wid;
+    S.cold().wid_hi = (uint32_t)(sc.wid >> 32);
     S.H = (uint64_t)sc.horizon_us;
-    S.c.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
-    S.c.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+    S.cold().w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
+    S.cold().w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
     const bellman_profile pr = p.profs[sc.profile];
-    S.c.t0 = pr.t0_us;
-    S.c.knee = pr.knee;
-    S.c.slope = pr.slope_us;
+    S.t0 = pr.t0_us;
+    S.knee = pr.knee;
+    S.slope = pr.slope_us;
     S.kv = pr.kv_ns_per_word;
     S.maxb = pr.max_batch;
     S.pf_ns = pr.prefill_ns_per_word;
-    S.c.law = cc.law;
+    S.cold().law = cc.law;
     S.signal = cc.signal;
-    S.c.window = cc.window;
-    S.c.rmin = cc.r_min_bp;
-    S.c.rmax = cc.r_max_bp;
-    S.c.t1 = cc.t1;
-    S.c.t2 = cc.t2;
-    S.c.slo_us = cc.slo_us;
-    S.c.nrungs = cc.n_rungs;
+    S.cold().window = cc.window;
+    S.cold().rmin = cc.r_min_bp;
+    S.cold().rmax = cc.r_max_bp;
+    S.cold().t1 = cc.t1;
+    S.cold().t2 = cc.t2;
+    S.slo_us = cc.slo_us;
+    S.cold().bypass_mask = cc.bypass_mask;
+    S.cold().min_words = cc.min_words_bypass;
+    S.cold().bypassed = 0;
+    S.cold().nrungs = cc.n_rungs;
     S.rungs_lane = lane < 8 ? cc.rungs_bp[lane] : 0u;
-    S.c.flags = 0;
+    S.cold().flags = 0;
     if (cc.calibrated) {
       const uint32_t slot = p.series_slot[sc.calib_src];
       const uint32_t *cb = p.calib + 4u * slot;
-      S.c.t1 = cb[0];
-      S.c.t2 = cb[1];
+      S.cold().t1 = cb[0];
+      S.cold().t2 = cb[1];
       if (cb[2] != 0) {
-        S.c.law = BELLMAN_LAW_OFF;
-        S.c.flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+        S.cold().law = BELLMAN_LAW_OFF;
+        S.cold().flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
       }
     }
-    S.r = S.c.law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
-    S.c.active = 0;
-    S.c.rung = 0;
+    S.r = S.cold().law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
+    S.cold().active = 0;
+    S.cold().rung = 0;
     S.ring = 0;
-    S.c.ring_n = 0;
-    S.c.ring_pos = 0;
-    S.c.ringA = 0;
-    S.c.activations = 0;
-    S.c.first_act = BELLMAN_NONE;
-    S.c.last_deact = BELLMAN_NONE;
-    S.c.active_ingests = 0;
+    S.cold().ring_n = 0;
+    S.cold().ring_pos = 0;
+    S.cold().ringA = 0;
+    S.cold().activations = 0;
+    S.cold().first_act = BELLMAN_NONE;
+    S.cold().last_deact = BELLMAN_NONE;
+    S.cold().active_ingests = 0;
     S.acc_sum = 0;
     S.acc_cnt = 0;
     const uint32_t rslot = p.series_slot[sid];
     if (rslot != BELLMAN_NONE) {
-      S.c.series = p.series + p.series_off[rslot];
-      S.c.series_cap = p.series_cap[rslot];
+      S.cold().series = p.series + p.series_off[rslot];
+      S.cold().series_cap = p.series_cap[rslot];
     } else {
-      S.c.series = nullptr;
-      S.c.series_cap = 0;
+      S.cold().series = nullptr;
+      S.cold().series_cap = 0;
     }
-    S.c.series_n = 0;
+    S.cold().series_n = 0;
     const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
     if (DBG && dslot != BELLMAN_NONE) {
       S.dbg = p.dbg_rows + p.dbg_off[dslot];
-      S.c.dbg_ctrl = p.dbg_ctrl + p.dbg_off[dslot];
-      S.c.dbg_cap = p.dbg_cap[dslot];
+      S.cold().dbg_ctrl = p.dbg_ctrl + p.dbg_off[dslot];
+      S.cold().dbg_cap = p.dbg_cap[dslot];
       // rows are accumulated with atomics: zero this scenario's region first
-      for (uint32_t i = lane; i < S.c.dbg_cap; i += 32u) S.dbg[i] = bellman_second_row{};
+      for (uint32_t i = lane; i < S.cold().dbg_cap; i += 32u) S.dbg[i] = bellman_second_row{};
       __syncwarp();
     } else {
       S.dbg = nullptr;
-      S.c.dbg_ctrl = nullptr;
-      S.c.dbg_cap = 0;
+      S.cold().dbg_ctrl = nullptr;
+      S.cold().dbg_cap = 0;
     }
-    S.c.dbg_nctrl = 0;
+    S.cold().dbg_nctrl = 0;
     // the per-second signal feeds only the controller (MAP/STEP) and the recorders
-    S.sec_bound = (S.c.law == BELLMAN_LAW_MAP || S.c.law == BELLMAN_LAW_STEP || S.c.series || (DBG && S.dbg)) ? kUs : INF;
+    S.sec_bound = (S.cold().law == BELLMAN_LAW_MAP || S.cold().law == BELLMAN_LAW_STEP || S.cold().series || (DBG && S.dbg)) ? kUs : INF;
     S.T = 0;
     S.busy = 0;
     S.iter_end = INF;
@@ -905,24 +935,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
     }
     const DevTrace tr = p.traces[sc.trace];
-    S.c.segs = p.segs + tr.seg_off;
-    S.c.n_seg = tr.n_seg;
-    S.c.gen_seg = 0;
-    S.c.gen_fresh = 1;
-    S.c.gen_j = 0;
-    S.c.gen_acc = 0;
-    S.c.gen_cap = tr.cap;
-    S.c.gen_done = 0;
-    S.c.gen_tau = 0;
+    S.cold().segs = p.segs + tr.seg_off;
+    S.cold().n_seg = tr.n_seg;
+    S.cold().gen_seg = 0;
+    S.cold().gen_fresh = 1;
+    S.cold().gen_j = 0;
+    S.cold().gen_acc = 0;
+    S.cold().gen_cap = tr.cap;
+    S.cold().gen_done = 0;
+    S.cold().gen_tau = 0;
     S.buf_h = S.buf_n = 0;
     S.buf_a = 0;
     S.buf_in = S.buf_U = S.buf_P = 0;
     S.buf_fcq = 0;
     S.buf_j = 0;
     S.last_j = 0;
-    S.admitted = S.served = S.rewritten = S.slo_viol = S.win_served = 0;
-    S.words_in = S.words_out = S.idle = S.win_words_in = S.win_words_out = S.win_idle = 0;
-    S.sum_queue = S.sum_ttft = S.sum_e2e = 0;
+    S.ctr = 0;
+    S.words_out = S.win_words_out = 0;
 
     // zero the warp's histograms
     {
@@ -960,9 +989,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       }
       if (tn >= S.H) break;
       if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
-        S.idle += tn - S.T;
-        const uint64_t lo = S.T > S.c.w0 ? S.T : S.c.w0, hi = tn < S.c.w1 ? tn : S.c.w1;
-        if (hi > lo) S.win_idle += hi - lo;
+        S.cadd(CT_IDLE, tn - S.T);
+        const uint64_t lo = S.T > S.cold().w0 ? S.T : S.cold().w0, hi = tn < S.cold().w1 ? tn : S.cold().w1;
+        if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
         S.dbg_idle(S.T, tn);
       }
       S.advance(tn);
@@ -1002,9 +1031,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     // ---- termination (R20)
     const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
     if (S.in_sys == 0) {
-      S.idle += end - S.T;
-      const uint64_t lo = S.T > S.c.w0 ? S.T : S.c.w0, hi = end < S.c.w1 ? end : S.c.w1;
-      if (hi > lo) S.win_idle += hi - lo;
+      S.cadd(CT_IDLE, end - S.T);
+      const uint64_t lo = S.T > S.cold().w0 ? S.T : S.cold().w0, hi = end < S.cold().w1 ? end : S.cold().w1;
+      if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
       S.dbg_idle(S.T, end);
     }
     if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
@@ -1012,7 +1041,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     uint64_t queued = 0;
     for (;;) {
       if (S.buf_h >= S.buf_n) {
-        if (S.c.gen_done) break;
+        if (S.cold().gen_done) break;
         S.refill(p);
         continue;
       }
@@ -1023,19 +1052,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
       S.buf_h = S.buf_n;
     }
-    if (S.c.series && lane == 0) p.series_n[rslot] = S.c.series_n;
+    if (S.cold().series && lane == 0) p.series_n[rslot] = S.cold().series_n;
     if (DBG && S.dbg && lane == 0) {
       const uint64_t nr = end / kUs + 1u;
-      p.dbg_n[2 * dslot] = (uint32_t)(nr < S.c.dbg_cap ? nr : S.c.dbg_cap);
-      p.dbg_n[2 * dslot + 1] = S.c.dbg_nctrl;
+      p.dbg_n[2 * dslot] = (uint32_t)(nr < S.cold().dbg_cap ? nr : S.cold().dbg_cap);
+      p.dbg_n[2 * dslot + 1] = S.cold().dbg_nctrl;
     }
 
     // ---- a9: percentiles from the histograms
+    uint64_t C_[CT_N];
+#pragma unroll
+    for (uint32_t i = 0; i < CT_N; ++i) C_[i] = S.cget(i);
     __syncwarp();
     uint32_t pe[2], pt[2], pm[1];
     const uint32_t ps[2] = {50u, 99u};
     const uint32_t p50[1] = {50u};
-    warp_percentiles(h.e2e, BELLMAN_HIST_LAT, S.served, ps, 2, pe, true);
+    warp_percentiles(h.e2e, BELLMAN_HIST_LAT, C_[CT_SERVED], ps, 2, pe, true);
     uint64_t n_ttft = 0;
     {
       uint32_t c = 0;
@@ -1043,10 +1075,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       n_ttft = __reduce_add_sync(FULL, c);
     }
     warp_percentiles(h.ttft, BELLMAN_HIST_LAT, n_ttft, ps, 2, pt, true);
-    warp_percentiles(h.r, BELLMAN_HIST_R, S.rewritten, p50, 1, pm, false);
+    warp_percentiles(h.r, BELLMAN_HIST_R, C_[CT_REWRITTEN], p50, 1, pm, false);
     uint32_t pqa[1], pqi[1];  // NEXT-2 similarity medians
-    warp_percentiles(h.qa, BELLMAN_HIST_Q, S.rewritten, p50, 1, pqa, false, 50u);
-    warp_percentiles(h.qi, BELLMAN_HIST_Q, S.admitted - S.rewritten, p50, 1, pqi, false, 50u);
+    warp_percentiles(h.qa, BELLMAN_HIST_Q, C_[CT_REWRITTEN], p50, 1, pqa, false, 50u);
+    warp_percentiles(h.qi, BELLMAN_HIST_Q, C_[CT_ADMITTED] - C_[CT_REWRITTEN], p50, 1, pqi, false, 50u);
     // segment merge: integer atomics, order-independent
     unsigned long long *sh = p.seg_hist + (uint64_t)sc.segment * kSegWords;
     for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) {
@@ -1066,53 +1098,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       o.scenario_id = sid;
       o.ticks = S.ticks;
       o.candidates = S.last_j;
-      o.arrivals = S.admitted + queued;
-      o.admitted = S.admitted;
-      o.served = S.served;
-      o.rewritten = S.rewritten;
-      o.words_in = S.words_in;
+      o.arrivals = C_[CT_ADMITTED] + queued;
+      o.admitted = C_[CT_ADMITTED];
+      o.served = C_[CT_SERVED];
+      o.rewritten = C_[CT_REWRITTEN];
+      o.words_in = C_[CT_WORDS_IN];
       o.words_out = S.words_out;
-      o.idle_us = S.idle;
+      o.idle_us = C_[CT_IDLE];
       o.end_us = end;
       o.queued_end = queued;
       o.inflight_end = S.in_sys;
-      o.win_served = S.win_served;
-      o.win_words_in = S.win_words_in;
+      o.win_served = C_[CT_WIN_SERVED];
+      o.win_words_in = C_[CT_WIN_WORDS_IN];
       o.win_words_out = S.win_words_out;
-      o.win_idle_us = S.win_idle;
-      o.sum_queue_us = S.sum_queue;
-      o.sum_ttft_us = S.sum_ttft;
-      o.sum_e2e_us = S.sum_e2e;
-      o.slo_violations = S.slo_viol;
+      o.win_idle_us = C_[CT_WIN_IDLE];
+      o.sum_queue_us = C_[CT_SUM_QUEUE];
+      o.sum_ttft_us = C_[CT_SUM_TTFT];
+      o.sum_e2e_us = C_[CT_SUM_E2E];
+      o.slo_violations = C_[CT_SLO_VIOL];
       o.e2e_p50_ms = pe[0];
       o.e2e_p99_ms = pe[1];
       o.ttft_p50_ms = pt[0];
       o.ttft_p99_ms = pt[1];
       o.median_r_bp = pm[0];
-      o.t1 = S.c.t1;
-      o.t2 = S.c.t2;
-      o.activations = S.c.activations;
-      o.first_act_s = S.c.first_act;
-      o.last_deact_s = S.c.last_deact;
-      o.active_ingests = S.c.active_ingests;
-      uint32_t fl = S.c.flags | BELLMAN_FLAG_DONE;
+      o.t1 = S.cold().t1;
+      o.t2 = S.cold().t2;
+      o.activations = S.cold().activations;
+      o.first_act_s = S.cold().first_act;
+      o.last_deact_s = S.cold().last_deact;
+      o.active_ingests = S.cold().active_ingests;
+      uint32_t fl = S.cold().flags | BELLMAN_FLAG_DONE;
       if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
       o.flags = fl;
       o.segment = sc.segment;
-      o._pad0 = 0;
+      o.bypassed = S.cold().bypassed;
       // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
-      const double a = __dmul_rn(pr.e_in_j_per_word, (double)S.words_in);
+      const double a = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WORDS_IN]);
       const double b = __dmul_rn(pr.e_out_j_per_word, (double)S.words_out);
-      const double c = __dmul_rn(pr.p_idle_w, (double)S.idle);
+      const double c = __dmul_rn(pr.p_idle_w, (double)C_[CT_IDLE]);
       o.energy_j = __dadd_rn(__dadd_rn(a, b), __ddiv_rn(c, 1e6));
-      const double wa = __dmul_rn(pr.e_in_j_per_word, (double)S.win_words_in);
+      const double wa = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WIN_WORDS_IN]);
       const double wb = __dmul_rn(pr.e_out_j_per_word, (double)S.win_words_out);
-      const double wc = __dmul_rn(pr.p_idle_w, (double)S.win_idle);
+      const double wc = __dmul_rn(pr.p_idle_w, (double)C_[CT_WIN_IDLE]);
       o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
       o.sim_active_p50 = pqa[0];
       o.sim_inactive_p50 = pqi[0];
-      o.scored_active = S.rewritten;
-      o.scored_inactive = S.admitted - S.rewritten;
+      o.scored_active = C_[CT_REWRITTEN];
+      o.scored_inactive = C_[CT_ADMITTED] - C_[CT_REWRITTEN];
       p.stats[sid] = o;
     }
     __syncwarp();
@@ -1166,7 +1198,7 @@ extern "C" int bellman_debug_prof(unsigned long long *out) {
 int bellman_tick_grid(int device) {
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpSmem);
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
   cudaFuncSetAttribute(bellman::bellman_tick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(bellman::bellman_tick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false>,
@@ -1176,7 +1208,7 @@ int bellman_tick_grid(int device) {
 }
 
 cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream) {
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpSmem);
+  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
   if (dbg)
     bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
   else

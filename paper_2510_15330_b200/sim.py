@@ -52,7 +52,8 @@ def pack(cols: dict, pinned: bool = False) -> dict:
     for f, c in (("law", "ctrl_law"), ("signal", "ctrl_signal"), ("window", "ctrl_window"),
                  ("r_min_bp", "ctrl_rmin"), ("r_max_bp", "ctrl_rmax"), ("r_const_bp", "ctrl_rconst"),
                  ("t1", "ctrl_t1"), ("t2", "ctrl_t2"), ("slo_us", "ctrl_slo_us"),
-                 ("calibrated", "ctrl_calibrated"), ("n_rungs", "ctrl_nrungs")):
+                 ("calibrated", "ctrl_calibrated"), ("n_rungs", "ctrl_nrungs"), ("bypass_mask", "ctrl_bypass_mask"),
+                 ("min_words_bypass", "ctrl_min_words")):
         ctrls[:nc][f] = cols[c]
     ctrls[:nc]["rungs_bp"] = np.asarray(cols["ctrl_rungs"]).reshape(nc, 8)
     ns = len(cols["sc_seed"])
@@ -73,6 +74,7 @@ def pack(cols: dict, pinned: bool = False) -> dict:
                ctrls=ctrls, n_ctrls=nc, scenarios=scs, n_scenarios=ns, tables=tabs,
                poly_q16=np.asarray(cols["poly_q16"], dtype=np.int64), n_segments=int(cols["n_segments"]),
                quality=np.asarray(cols["quality"], dtype=np.uint32),
+               class_cum=np.asarray(cols["class_cum"], dtype=np.uint32),
                _keep=keep)
     return out
 
@@ -82,7 +84,8 @@ def make_desc(pk: dict) -> A.Desc:
     m = A.Models(t["tab_L"].ctypes.data, t["tab_I"].ctypes.data, t["tab_fvar"].ctypes.data,
                  t["tab_noise"].ctypes.data, t["tab_fcomp"].ctypes.data,
                  (C.c_int64 * 3)(*[int(x) for x in pk["poly_q16"]]), t["tab_qnoise"].ctypes.data,
-                 (C.c_uint32 * 5)(*[int(x) for x in pk["quality"]]), 0)
+                 (C.c_uint32 * 5)(*[int(x) for x in pk["quality"]]),
+                 (C.c_uint32 * 4)(*[int(x) for x in pk["class_cum"]]), (C.c_uint32 * 3)(0, 0, 0))
     return A.Desc(pk["knots"].ctypes.data, pk["n_knots"], pk["traces"].ctypes.data, pk["n_traces"],
                   pk["profiles"].ctypes.data, pk["n_profiles"], pk["ctrls"].ctypes.data, pk["n_ctrls"], m,
                   pk["scenarios"].ctypes.data, pk["n_scenarios"], pk["n_segments"], 0)

@@ -1,42 +1,40 @@
-"""Instruction / stall-sample share per source region of the tick kernel."""
+"""Instruction / stall-sample share per source region of the tick kernel,
+using the source embedded in the report (--import-source on)."""
 import csv
 import re
 import subprocess
 import sys
 
 
-def regions(src):
-    pats = []
-    for i, line in enumerate(open(src), 1):
-        m = re.search(r"__device__ (?:__forceinline__ )?\w+ \*?(\w+)\(", line) or \
-            re.search(r"^__global__ .* (\w+)\(", line) or re.search(r"// ---- (a\d+|the event|termination)", line)
-        if m:
-            pats.append((i, m.group(1)))
-    return pats
-
-
-def main(rep, src):
+def main(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "Line No"][0]
     h = rows[hi]
     iS, iI = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-    data = []
+    data, src = [], {}
     for r in rows[hi + 1:]:
         if len(r) > iI and r[0].isdigit():
             try:
                 data.append((int(r[0]), int(r[iS] or 0), int(r[iI] or 0)))
+                src[int(r[0])] = r[1]
             except ValueError:
                 pass
-    reg = regions(src)
+    starts = []
+    for ln in sorted(src):
+        line = src[ln]
+        m = re.search(r"__device__ (?:__forceinline__ |__noinline__ )?[\w:<>]+ \*?(\w+)\(", line) or \
+            re.search(r"__global__ .* (\w+)\(", line) or re.search(r"// ---- (a\d+|the event|termination)", line)
+        if m:
+            starts.append((ln, m.group(1)))
     tot_i = sum(d[2] for d in data)
     tot_s = sum(d[1] for d in data)
     agg = {}
     for ln, s, n in data:
         name = "?"
-        for start, nm in reg:
-            if start <= ln:
+        for st, nm in starts:
+            if st <= ln:
                 name = nm
         a = agg.setdefault(name, [0, 0])
         a[0] += n
@@ -47,4 +45,4 @@ def main(rep, src):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1])

@@ -205,3 +205,24 @@ def test_debug_series_rows_and_controller_log():
             for g, e in zip(ctrl, oc):
                 assert (int(g["second"]), int(g["sample"]), int(g["k"]), int(g["r_bp"]), int(g["active"]),
                         int(g["A"])) == (e["second"], e["sample"], e["k"], e["r_bp"], e["active"], e["A"])
+
+
+def test_next3_classes_bypass_and_ttft_signal():
+    """NEXT-3: a request-class mix with per-class bypass and short-output bypass
+     under MAP/STEP/CONST laws, and the TTFT signal."""
+    import dataclasses
+
+    w = W.config_c3(n_seeds=2)
+    w.class_cum = W.MIXED_CLASSES
+    w.ctrls = [dataclasses.replace(c, bypass_mask=(i % 3) * 2, min_words_bypass=(0, 420, 480)[i % 3])
+               if c.law != W.LAW_OFF else c for i, c in enumerate(w.ctrls)]
+    w.ctrls.append(W.map_ctrl(400_000, 900_000, signal=W.SIG_TTFT))
+    w.ctrls.append(W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1500, bypass_mask=0b0110, min_words_bypass=450))
+    for k in (len(w.ctrls) - 2, len(w.ctrls) - 1):
+        for s in range(3):
+            w.scenarios.append(W.Scenario(s, wid=0, trace=0, profile=0, ctrl=k, segment=0, mode=W.MODE_DRAIN,
+                                          horizon_us=1920 * W.US))
+    w.scenarios = w.scenarios[::7] + w.scenarios[-6:]
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)
+    assert int(st["bypassed"].sum()) > 0

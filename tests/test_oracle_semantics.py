@@ -243,3 +243,44 @@ def test_similarity_model_examples(orc):
     assert orc.similarity(500, 100, True, noise=-9000) == 0
     # linear decay midpoint: reduction 30 % -> 87 - 22/2 = 76 points
     assert orc.similarity(1000, 700, True) == 7600
+
+
+def test_class_and_short_output_bypass(orc):
+    """NEXT-3: a class with the bypass policy is never rewritten; S:314 /
+    S:267: a predicted length below min_words_bypass is never rewritten; S:333:
+    within one admission point all non-bypassed requests carry the same r."""
+    reqs = [dict(a_us=k * 1000, input=10, U=50 + k, P=40 + 5 * k, cls=k % 3) for k in range(30)]
+    c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=1500, bypass_mask=0b010, min_words_bypass=70)
+    d = orc.simulate(reqs, LIT, ctrl=c, mode=W.MODE_DRAIN)
+    for q, r in zip(reqs, d["requests"]):
+        bypass = q["cls"] == 1 or q["P"] < 70
+        assert r["r_bp"] == (0 if bypass else 1500)
+        assert r["R"] == (q["U"] if bypass else max(1, (q["P"] * 8500 + 5000) // 10000))
+    assert d["bypassed"] == sum(1 for q in reqs if q["cls"] == 1 or q["P"] < 70)
+    assert d["rewritten"] + d["bypassed"] == d["admitted"]
+    # fairness: equal r per admission instant among non-bypassed requests
+    by_t = {}
+    for q, r in zip(reqs, d["requests"]):
+        if not (q["cls"] == 1 or q["P"] < 70):
+            by_t.setdefault(r["admit_us"], set()).add(r["r_bp"])
+    assert all(len(v) == 1 for v in by_t.values())
+
+
+def test_ttft_signal_is_per_second_mean(orc):
+    """NEXT-3 signal ("TTFT could offer early insights"): the sample of
+    second s is floor(mean TTFT of the first words emitted in s)."""
+    rng = np.random.default_rng(9)
+    reqs = []
+    t = 0
+    for i in range(60):
+        t += int(rng.integers(0, 300_000))
+        reqs.append(dict(a_us=t, input=int(rng.integers(100, 3000)), U=int(rng.integers(2, 40))))
+    c = orc.make_ctrl(law=W.LAW_MAP, signal=W.SIG_TTFT, t1=10**9, t2=2 * 10**9)
+    d = orc.simulate(reqs, LIT, ctrl=c, mode=W.MODE_DRAIN)
+    want = {}
+    for q, r in zip(reqs, d["requests"]):
+        s = r["first_us"] // 10**6
+        want.setdefault(s, []).append(r["first_us"] - q["a_us"])
+    got = {e["second"]: e["sample"] for e in d["ctrl_log"]}
+    closed = {s: sum(v) // len(v) for s, v in want.items() if (s + 1) * 10**6 <= d["end_us"]}
+    assert got == closed

@@ -30,7 +30,7 @@ from scipy.special import ndtri
 # enums shared *by value* with both implementations (documented in DESIGN.md)
 # ----------------------------------------------------------------------------
 LAW_OFF, LAW_CONST, LAW_MAP, LAW_STEP = 0, 1, 2, 3
-SIG_TBT, SIG_E2E, SIG_SLO = 0, 1, 2
+SIG_TBT, SIG_E2E, SIG_SLO, SIG_TTFT = 0, 1, 2, 3
 MODE_CUTOFF, MODE_DRAIN = 0, 1
 
 US = 1_000_000  # µs per second
@@ -110,6 +110,11 @@ IDENTITY_POLY_Q16 = (0, 65536, 0)  # compliance realized = N (SPEC S:163 identit
 # inactive median 88 and active median 87, floor 65,
 # safe window 20 %, linear decay to the floor at 40 %.
 QUALITY = (8800, 8700, 6500, 2000, 4000)
+# Request classes (NEXT-3): cumulative thresholds in 2^-20 units of the
+# 20 low bits of the word that draws L; one class by default.
+SINGLE_CLASS = (1 << 20,) * 4
+# summarization 70 %, coding 20 %, short-form 10 % (an illustrative mix; the paper gives none)
+MIXED_CLASSES = (int(0.7 * (1 << 20)), int(0.9 * (1 << 20)), 1 << 20, 1 << 20)
 
 # ----------------------------------------------------------------------------
 # traces (piecewise-linear lambda(t) knots; µs and milli-RPS integers)
@@ -182,6 +187,8 @@ class Ctrl:
     slo_us: int = 0
     calibrated: int = 0       # 1: t1/t2 = p50/p75 of the paired OFF run
     rungs_bp: tuple = ()      # word-limit ladder (reading R5), <= 8 ascending rungs
+    bypass_mask: int = 0      # NEXT-3: bit c -> class c never rewritten ("coding tasks might use r=0")
+    min_words_bypass: int = 0  # NEXT-3: predicted length below this is never rewritten
 
 
 OFF = Ctrl()
@@ -225,6 +232,7 @@ class Workload:
     tables: dict = field(default_factory=dict)
     poly_q16: tuple = IDENTITY_POLY_Q16
     quality: tuple = QUALITY
+    class_cum: tuple = SINGLE_CLASS
     scenarios: list = field(default_factory=list)
     n_segments: int = 1
     segment_names: list = field(default_factory=list)
@@ -279,11 +287,12 @@ class Workload:
             ctrl_t1=u32([c.t1 for c in C]), ctrl_t2=u32([c.t2 for c in C]),
             ctrl_slo_us=u32([c.slo_us for c in C]), ctrl_calibrated=u32([c.calibrated for c in C]),
             ctrl_nrungs=u32([len(c.rungs_bp) for c in C]), ctrl_rungs=rungs[:len(C)],
+            ctrl_bypass_mask=u32([c.bypass_mask for c in C]), ctrl_min_words=u32([c.min_words_bypass for c in C]),
             tab_L=self.tables["L"], tab_I=self.tables["I"], tab_fvar=self.tables["fvar"],
             tab_noise=self.tables["noise"], tab_fcomp=self.tables["fcomp"],
             poly_q16=i64(self.poly_q16),
             tab_qnoise=self.tables.get("qnoise", np.zeros(TABLE_N, dtype=np.int32)).astype(np.int32),
-            quality=u32(self.quality),
+            quality=u32(self.quality), class_cum=u32(self.class_cum),
             sc_seed=u32([s.seed_index for s in S]), sc_wid=np.asarray([s.wid for s in S], dtype=np.uint64),
             sc_trace=u32([s.trace for s in S]), sc_profile=u32([s.profile for s in S]),
             sc_ctrl=u32([s.ctrl for s in S]), sc_segment=u32([s.segment for s in S]),

@@ -121,6 +121,16 @@ struct Cold {
   uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
   uint32_t k0, wid_lo, wid_hi;
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
+  uint32_t ring[8];   // last `window` per-second samples (a6)
+  // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
+  // entry i written by lane i at refill, read by index at admission
+  uint64_t buf_a[32];    // arrival time
+  uint32_t buf_in[32];   // input words | request class << 16 (NEXT-3)
+  uint32_t buf_U[32];    // realized unbounded length
+  uint32_t buf_P[32];    // predicted length
+  uint32_t buf_fcq[32];  // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
+  uint32_t buf_j[32];    // candidate index
+  uint32_t rungs[8];  // word-limit ladder (R5)
 
 };
 
@@ -134,6 +144,194 @@ enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL 
 __shared__ Cold g_cold[kWarpsPerBlock];
 
 // ---------------------------------------------------------------------------
+// a2 + a3: refill the warp's shared arrival buffer with the next accepted
+// candidates (P:183 Poisson arrivals, S:83 thinning; R17, R32, R33).  Lane l
+// draws candidate j + l: Philox block, -ln U, then a warp prefix sum of the
+// exponential gaps gives the candidate times; thinning by ballot; accepted
+// candidates are compacted (__fns) into entries 0..n-1 together with their
+// per-request draws (tag-1 block).  Out of line: it runs once per ~32 arrivals.
+// Returns n (0 only when the generator is exhausted).
+template <bool DBG>
+__device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane, uint64_t H,
+                                               bellman_second_row *dbg, uint32_t dbg_cap) {
+  Cold &c = g_cold[wid];
+  uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
+  uint32_t gen_acc = c.gen_acc;
+  uint64_t gen_tau = c.gen_tau;
+  const uint32_t n_seg = c.n_seg, gen_cap = c.gen_cap, k0 = c.k0, wid_lo = c.wid_lo, wid_hi = c.wid_hi;
+  const DevSeg *segs = c.segs;
+  uint32_t n = 0;
+  while (!gen_done && n == 0) {
+    if (gen_seg >= n_seg) {
+      gen_done = 1;
+      break;
+    }
+    const DevSeg S = segs[gen_seg];
+    if (gen_fresh) {
+      gen_tau = S.ta;
+      gen_fresh = 0;
+    }
+    const uint32_t jj = gen_j + lane;
+    const uint4 u = philox(k0, kSeedHi, jj, 0u, wid_lo, wid_hi);
+    const uint64_t delta = __umul64hi(neglog_q32(u.x, p.log2tab), S.M);
+    uint64_t incl = delta;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    const uint64_t tau = gen_tau + incl;
+    const uint32_t om = __ballot_sync(FULL, tau >= S.tb);
+    const uint32_t first_over = om ? (uint32_t)(__ffs(om) - 1) : 32u;
+    bool acc = false;
+    if (lane < first_over) {
+      // thinning: u1 * lmax * span < (la (tb - tau) + lb (tau - ta)) * 2^32, in 128 bits
+      const uint64_t x = (uint64_t)u.y * S.lmax;
+      const uint64_t lhs_hi = __umul64hi(x, S.span), lhs_lo = x * S.span;
+      const uint64_t y = (uint64_t)S.la * (S.tb - tau) + (uint64_t)S.lb * (tau - S.ta);
+      const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
+      acc = lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
+    }
+    uint32_t am = __ballot_sync(FULL, acc);
+    if (gen_cap) {
+      const uint32_t room = gen_cap - gen_acc;
+      if ((uint32_t)__popc(am) >= room) {
+        const uint32_t cut = room ? __fns(am, 0, (int)room) : 0u;  // position of room-th set bit
+        am = room ? (am & (0xffffffffu >> (31u - cut))) : 0u;
+        gen_done = 1;
+      }
+    }
+    n = (uint32_t)__popc(am);
+    // compaction: the accepted candidate of rank l lands in entry l
+    if (acc && ((am >> lane) & 1u)) {
+      const uint32_t e = __popc(am & ((1u << lane) - 1u));
+      const uint32_t L = (uint32_t)__ldg(&p.tabL[u.z >> 20]);
+      const uint32_t x = u.z & 0xFFFFFu;  // class draw from the bits below L's index (NEXT-3)
+      const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
+      c.buf_a[e] = tau;
+      c.buf_in[e] = (uint32_t)__ldg(&p.tabI[u.w >> 20]) | (cls << 16);
+      c.buf_j[e] = jj;
+      const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);  // a3: the request's own draws
+      const uint64_t U = ((uint64_t)L * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
+      c.buf_U[e] = U < 1 ? 1u : (uint32_t)U;
+      const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
+      c.buf_P[e] = P0 < 1 ? 1u : (uint32_t)P0;
+      c.buf_fcq[e] = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      if (DBG && dbg && tau < H) {
+        const uint64_t sidx = tau / kUs;
+        atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
+      }
+    }
+    gen_acc += n;
+    if (first_over < 32u) {
+      gen_j += first_over + 1u;  // the crossing candidate is consumed (R17)
+      gen_seg++;
+      gen_fresh = 1;
+    } else {
+      gen_j += 32u;
+      gen_tau = __shfl_sync(FULL, tau, 31);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    c.gen_done = gen_done;
+    c.gen_seg = gen_seg;
+    c.gen_fresh = gen_fresh;
+    c.gen_j = gen_j;
+    c.gen_acc = gen_acc;
+    c.gen_tau = gen_tau;
+  }
+  __syncwarp();
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// a6: one controller ingest of the sample x of closed second `second` (P:134,
+// P:193; R3-R5, R12, R38).  Out of line: it runs once per simulated
+// second, so it stays out of the event loop's instruction-cache footprint.
+// All lanes compute; only lane 0 writes the shared-memory state.
+template <bool DBG>
+__device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint32_t second, uint32_t x,
+                                               uint32_t r_cur, bool dbg) {
+  Cold &c = g_cold[wid];
+  if (c.series) {
+    const uint32_t n = c.series_n;
+    if (lane == 0) {
+      if (n < c.series_cap) c.series[n] = x;
+      else c.flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+      c.series_n = n + 1u;
+    }
+    __syncwarp();
+  }
+  const uint32_t law = c.law;
+  if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return r_cur;
+  const uint32_t window = c.window, pos = c.ring_pos, t1 = c.t1;
+  uint32_t k = c.ring_n, rung = c.rung;
+  const uint32_t was_active = c.active;
+  uint64_t A = c.ringA;
+  const uint32_t ev = c.ring[pos];
+  if (k < window) {
+    k++;
+    A += x;
+  } else {
+    A = A + x - ev;
+  }
+  const bool act = A >= (uint64_t)k * t1;  // non-strict (R38)
+  uint32_t nr = 0;
+  if (act) {
+    if (law == BELLMAN_LAW_MAP) {
+      const uint32_t rmin = c.rmin, rmax = c.rmax;
+      uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (c.t2 - t1));
+      if (rr > rmax) rr = rmax;
+      nr = (uint32_t)rr;
+      const uint32_t nrungs = c.nrungs;
+      if (nrungs) {  // largest rung <= r (R5)
+        uint32_t best = c.rungs[0];
+        for (uint32_t i = 1; i < nrungs; ++i)
+          if (c.rungs[i] <= nr) best = c.rungs[i];
+        nr = best;
+      }
+    } else {  // STEP: rung 0 on activation, one rung up per ingest while active
+      rung = was_active ? (rung + 1u < c.nrungs ? rung + 1u : rung) : 0u;
+      nr = c.rungs[rung];
+    }
+  }
+  const uint32_t nctrl = c.dbg_nctrl;
+  __syncwarp();
+  if (lane == 0) {
+    c.ring[pos] = x;
+    c.ring_n = k;
+    c.ringA = A;
+    c.ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
+    c.rung = rung;
+    c.active = act;
+    if (act && !was_active) {
+      c.activations++;
+      if (c.first_act == BELLMAN_NONE) c.first_act = second;
+    }
+    if (!act && was_active) c.last_deact = second;
+    if (act) c.active_ingests++;
+    if (DBG && dbg) {
+      if (nctrl < c.dbg_cap) {
+        bellman_ctrl_row cr;
+        cr.second = second;
+        cr.sample = x;
+        cr.k = k;
+        cr.r_bp = nr;
+        cr.active = act;
+        cr._pad = 0;
+        cr.A = A;
+        c.dbg_ctrl[nctrl] = cr;
+      }
+      c.dbg_nctrl = nctrl + 1u;
+    }
+  }
+  __syncwarp();
+  return nr;
+}
+
+
+// ---------------------------------------------------------------------------
 // The per-scenario simulation.  Every scalar is warp-uniform.  Derived
 // quantities are maintained incrementally so that an event trip does no
 // division: the cost base c = t0 + slope max(0, B - knee), the KV term as
@@ -143,9 +341,15 @@ template <bool DBG>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
   __device__ __forceinline__ Cold &cold() const { return g_cold[wid]; }
+#ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
   __device__ __forceinline__ void cadd(uint32_t i, uint64_t v) { ctr += (lane == i) ? v : 0ull; }
   __device__ __forceinline__ uint64_t cget(uint32_t i) const { return __shfl_sync(FULL, ctr, i); }
+#else
+  uint64_t ctrs[CT_N];
+  __device__ __forceinline__ void cadd(uint32_t i, uint64_t v) { ctrs[i] += v; }
+  __device__ __forceinline__ uint64_t cget(uint32_t i) const { return ctrs[i]; }
+#endif
   uint32_t lane;
   uint32_t wid;  // warp index in the CTA: selects this warp's Cold block
   // ---- scenario (a1)
@@ -154,9 +358,7 @@ struct Sim {
   uint32_t kv, maxb;
   // controller
   uint32_t signal;
-  uint32_t rungs_lane;  // lane l < nrungs holds rung l
   uint32_t r;
-  uint32_t ring;        // lane l < window holds a ring sample
   // per-second accumulator of the selected signal (a6)
   uint64_t sec_bound;  // (open second + 1) * 1e6, INF when nothing consumes the signal
   uint64_t acc_sum;
@@ -188,187 +390,21 @@ struct Sim {
   uint64_t sa[2], sp[2];
   uint32_t sR[2], sin[2], sdn[2], sph[2];
   // ---- generator / queue head (a2)
-  uint32_t buf_h, buf_n;
-  uint64_t buf_a;      // lane-parallel buffer of upcoming arrivals
-  uint32_t buf_in;     // input words | request class << 16 (NEXT-3)
-  uint32_t buf_U;      // realized unbounded length (a3)
-  uint32_t buf_P;      // predicted length (a3)
-  uint32_t buf_fcq;    // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
-  uint32_t buf_j;
+  uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
   uint64_t head_t;     // arrival time of the queue head, INF when no arrival remains
   // ---- counters (a8)
   uint64_t words_out, win_words_out;
 
   // ------------------------------------------------------------------ a2
-  // Refill the 32-entry arrival buffer with the next accepted candidates.
   __device__ __forceinline__ void refill(const Params &p) {
-    // shared-memory generator state: read by all lanes, written back by lane 0 only
-    uint32_t gen_done = cold().gen_done, gen_seg = cold().gen_seg, gen_fresh = cold().gen_fresh, gen_j = cold().gen_j;
-    uint32_t gen_acc = cold().gen_acc;
-    uint64_t gen_tau = cold().gen_tau;
-    const uint32_t n_seg = cold().n_seg, gen_cap = cold().gen_cap, k0 = cold().k0, wid_lo = cold().wid_lo, wid_hi = cold().wid_hi;
-    const DevSeg *segs = cold().segs;
     buf_h = 0;
-    buf_n = 0;
-    while (!gen_done && buf_n == 0) {
-      if (gen_seg >= n_seg) {
-        gen_done = 1;
-        break;
-      }
-      const DevSeg S = segs[gen_seg];
-      if (gen_fresh) {
-        gen_tau = S.ta;
-        gen_fresh = 0;
-      }
-      const uint32_t jj = gen_j + lane;
-      const uint4 u = philox(k0, kSeedHi, jj, 0u, wid_lo, wid_hi);
-      const uint64_t delta = __umul64hi(neglog_q32(u.x, p.log2tab), S.M);
-      uint64_t incl = delta;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      const uint64_t tau = gen_tau + incl;
-      const uint32_t om = __ballot_sync(FULL, tau >= S.tb);
-      const uint32_t first_over = om ? (uint32_t)(__ffs(om) - 1) : 32u;
-      bool acc = false;
-      if (lane < first_over) {
-        // thinning: u1 * lmax * span < (la (tb - tau) + lb (tau - ta)) * 2^32, in 128 bits
-        const uint64_t x = (uint64_t)u.y * S.lmax;
-        const uint64_t lhs_hi = __umul64hi(x, S.span), lhs_lo = x * S.span;
-        const uint64_t y = (uint64_t)S.la * (S.tb - tau) + (uint64_t)S.lb * (tau - S.ta);
-        const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
-        acc = lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
-      }
-      uint32_t am = __ballot_sync(FULL, acc);
-      if (gen_cap) {
-        const uint32_t room = gen_cap - gen_acc;
-        if ((uint32_t)__popc(am) >= room) {
-          const uint32_t cut = room ? __fns(am, 0, (int)room) : 0u;  // position of room-th set bit
-          am = room ? (am & (0xffffffffu >> (31u - cut))) : 0u;
-          gen_done = 1;
-        }
-      }
-      const uint32_t cnt = (uint32_t)__popc(am);
-      const uint32_t attr = (uint32_t)__ldg(&p.tabL[u.z >> 20]) | ((uint32_t)__ldg(&p.tabI[u.w >> 20]) << 16);
-      const uint32_t src = __fns(am, 0, (int)lane + 1);
-      const uint32_t s = src < 32u ? src : 0u;
-      buf_a = __shfl_sync(FULL, tau, s);
-      const uint32_t at = __shfl_sync(FULL, attr, s);
-      const uint32_t uz = __shfl_sync(FULL, u.z, s);
-      buf_j = __shfl_sync(FULL, jj, s);
-      buf_n = cnt;
-      if (DBG && dbg && lane < cnt && buf_a < H) atomicAdd(&row(buf_a)->arrivals, 1u);
-      // a3: the accepted request's own draws (tag 1), lane-parallel, ahead of admission
-      {
-        const uint32_t L = at & 0xFFFFu;
-        const uint32_t x = uz & 0xFFFFFu;  // class draw from the bits below L's index
-        const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
-        buf_in = (at >> 16) | (cls << 16);
-        const uint4 v = philox(k0, kSeedHi, buf_j, 1u, wid_lo, wid_hi);
-        const uint32_t fvar = (uint32_t)__ldg(&p.tabF[v.x >> 20]);
-        const uint64_t U = ((uint64_t)L * fvar + 32768u) >> 16;  // S:139, R14
-        buf_U = U < 1 ? 1u : (uint32_t)U;
-        const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
-        buf_P = P0 < 1 ? 1u : (uint32_t)P0;
-        buf_fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
-      }
-      gen_acc += cnt;
-      if (first_over < 32u) {
-        gen_j += first_over + 1u;  // the crossing candidate is consumed (R17)
-        gen_seg++;
-        gen_fresh = 1;
-      } else {
-        gen_j += 32u;
-        gen_tau = __shfl_sync(FULL, tau, 31);
-      }
-    }
-    head_t = buf_n ? __shfl_sync(FULL, buf_a, 0) : INF;
-    if (lane == 0) {
-      cold().gen_done = gen_done;
-      cold().gen_seg = gen_seg;
-      cold().gen_fresh = gen_fresh;
-      cold().gen_j = gen_j;
-      cold().gen_acc = gen_acc;
-      cold().gen_tau = gen_tau;
-    }
-    __syncwarp();
+    buf_n = refill_buffer<DBG>(p, wid, lane, H, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u);
+    head_t = buf_n ? cold().buf_a[0] : INF;
   }
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
-    // shared-memory controller state: read by all lanes, written back by lane 0 only
-    if (cold().series) {
-      const uint32_t n = cold().series_n;
-      if (lane == 0) {
-        if (n < cold().series_cap) cold().series[n] = x;
-        else cold().flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
-        cold().series_n = n + 1u;
-      }
-      __syncwarp();
-    }
-    if (cold().law != BELLMAN_LAW_MAP && cold().law != BELLMAN_LAW_STEP) return;
-    const uint32_t window = cold().window, pos = cold().ring_pos, t1 = cold().t1;
-    uint32_t k = cold().ring_n, rung = cold().rung;
-    const uint32_t was_active = cold().active;
-    uint64_t A = cold().ringA;
-    const uint32_t ev = __shfl_sync(FULL, ring, pos);
-    if (lane == pos) ring = x;
-    if (k < window) {
-      k++;
-      A += x;
-    } else {
-      A = A + x - ev;
-    }
-    const bool act = A >= (uint64_t)k * t1;  // non-strict (R38)
-    uint32_t nr = 0;
-    if (act) {
-      if (cold().law == BELLMAN_LAW_MAP) {
-        const uint32_t rmin = cold().rmin, rmax = cold().rmax;
-        uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (cold().t2 - t1));
-        if (rr > rmax) rr = rmax;
-        nr = (uint32_t)rr;
-        const uint32_t nrungs = cold().nrungs;
-        if (nrungs) {  // largest rung <= r (R5)
-          const uint32_t le = __ballot_sync(FULL, lane < nrungs && rungs_lane <= nr);
-          nr = __shfl_sync(FULL, rungs_lane, 31 - __clz(le | 1u));
-        }
-      } else {  // STEP
-        rung = was_active ? (rung + 1u < cold().nrungs ? rung + 1u : rung) : 0u;
-        nr = __shfl_sync(FULL, rungs_lane, rung);
-      }
-    }
-    const uint32_t nctrl = cold().dbg_nctrl;
-    if (lane == 0) {
-      cold().ring_n = k;
-      cold().ringA = A;
-      cold().ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
-      cold().rung = rung;
-      cold().active = act;
-      if (act && !was_active) {
-        cold().activations++;
-        if (cold().first_act == BELLMAN_NONE) cold().first_act = second;
-      }
-      if (!act && was_active) cold().last_deact = second;
-      if (act) cold().active_ingests++;
-      if (DBG && dbg) {
-        if (nctrl < cold().dbg_cap) {
-          bellman_ctrl_row cr;
-          cr.second = second;
-          cr.sample = x;
-          cr.k = k;
-          cr.r_bp = nr;
-          cr.active = act;
-          cr._pad = 0;
-          cr.A = A;
-          cold().dbg_ctrl[nctrl] = cr;
-        }
-        cold().dbg_nctrl = nctrl + 1u;
-      }
-    }
-    __syncwarp();
-    r = nr;
+    r = ingest_sample<DBG>(wid, lane, second, x, r, DBG && dbg != nullptr);
   }
 
   // close the open second (if it holds samples) and open the one containing t
@@ -573,7 +609,7 @@ struct Sim {
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
     const uint64_t Tn = T;
     for (;;) {
-      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && buf_a <= Tn);
+      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Tn);
       const uint32_t na = __popc(arrived);
       const uint32_t room = maxb - in_sys;
       const uint32_t k = na < room ? na : room;
@@ -589,13 +625,11 @@ struct Sim {
       for (int s = 0; s < 2; ++s) {
         const uint32_t rank = s == 0 ? rank0 : rank1;
         const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
-        const uint32_t src = (buf_h + (mine ? rank : 0u)) & 31u;
-        const uint64_t a = __shfl_sync(FULL, buf_a, src);
-        const uint32_t inc = __shfl_sync(FULL, buf_in, src);
-        const uint32_t U = __shfl_sync(FULL, buf_U, src);
-        const uint32_t P = __shfl_sync(FULL, buf_P, src);
-        const uint32_t fcq = __shfl_sync(FULL, buf_fcq, src);
         if (mine) {
+          const uint32_t src = buf_h + rank;  // < buf_n <= 32
+          const uint64_t a = cold().buf_a[src];
+          const uint32_t inc = cold().buf_in[src], U = cold().buf_U[src], P = cold().buf_P[src];
+          const uint32_t fcq = cold().buf_fcq[src];
           const uint32_t in = inc & 0xFFFFu;
           // r applied to this request: the warp-uniform r unless a bypass rule holds
           const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
@@ -614,21 +648,32 @@ struct Sim {
             R = (uint32_t)x;
             atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
           }
+#ifndef BELLMAN_AB_NOQ
           {  // NEXT-2: similarity vs the unbounded length
             int32_t base = (int32_t)p.q_inactive;
             if (ra > 0) {
               const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
-              if (num <= (int64_t)p.q_safe * den) base = (int32_t)p.q_active;
-              else if (num >= (int64_t)p.q_end * den) base = (int32_t)p.q_floor;
-              else
-                base = (int32_t)p.q_active - (int32_t)(((int64_t)(p.q_active - p.q_floor) * (num - (int64_t)p.q_safe * den)) /
-                                                       ((int64_t)(p.q_end - p.q_safe) * den));
+              if (num <= (int64_t)p.q_safe * den) {
+                base = (int32_t)p.q_active;
+              } else if (num >= (int64_t)p.q_end * den) {
+                base = (int32_t)p.q_floor;
+              } else {
+                // floor(a X / D), 0 < X < D < 2^32, a <= 10^4: float estimate, exact integer fix-up
+                const uint64_t X = (uint64_t)(num - (int64_t)p.q_safe * den);
+                const uint64_t D = (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den;
+                const uint64_t aX = (uint64_t)(p.q_active - p.q_floor) * X;
+                uint32_t q = (uint32_t)__fmul_rz((float)aX, __frcp_rn((float)D));
+                while (q && (uint64_t)q * D > aX) q--;
+                while ((uint64_t)(q + 1u) * D <= aX) q++;
+                base = (int32_t)p.q_active - (int32_t)q;
+              }
             }
             int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
             sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
             const uint32_t qb = (uint32_t)sc / 50u;
             atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
           }
+#endif
           uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
           if (pf < 1) pf = 1;
           sa[s] = a;
@@ -662,12 +707,12 @@ struct Sim {
           __syncwarp();
         }
       }
-      last_j = __shfl_sync(FULL, buf_j, (buf_h + k - 1u) & 31u) + 1u;
+      last_j = cold().buf_j[buf_h + k - 1u] + 1u;
       in_sys += k;
       cadd(CT_ADMITTED, k);
       buf_h += k;
       if (buf_h < buf_n) {
-        head_t = __shfl_sync(FULL, buf_a, buf_h & 31u);
+        head_t = cold().buf_a[buf_h];
       } else if (!cold().gen_done) {
         refill(p);
       } else {
@@ -821,7 +866,7 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 }
 
 template <bool DBG>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const Params p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
   WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
@@ -865,7 +910,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.cold().min_words = cc.min_words_bypass;
     S.cold().bypassed = 0;
     S.cold().nrungs = cc.n_rungs;
-    S.rungs_lane = lane < 8 ? cc.rungs_bp[lane] : 0u;
     S.cold().flags = 0;
     if (cc.calibrated) {
       const uint32_t slot = p.series_slot[sc.calib_src];
@@ -880,10 +924,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.r = S.cold().law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
     S.cold().active = 0;
     S.cold().rung = 0;
-    S.ring = 0;
     S.cold().ring_n = 0;
     S.cold().ring_pos = 0;
     S.cold().ringA = 0;
+    if (lane < 8) {
+      S.cold().rungs[lane] = cc.rungs_bp[lane];
+      S.cold().ring[lane] = 0;
+    }
+    __syncwarp();
     S.cold().activations = 0;
     S.cold().first_act = BELLMAN_NONE;
     S.cold().last_deact = BELLMAN_NONE;
@@ -945,12 +993,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.cold().gen_done = 0;
     S.cold().gen_tau = 0;
     S.buf_h = S.buf_n = 0;
-    S.buf_a = 0;
-    S.buf_in = S.buf_U = S.buf_P = 0;
-    S.buf_fcq = 0;
-    S.buf_j = 0;
     S.last_j = 0;
+#ifndef BELLMAN_AB_REGCTR
     S.ctr = 0;
+#else
+#pragma unroll
+    for (uint32_t i = 0; i < CT_N; ++i) S.ctrs[i] = 0;
+#endif
     S.words_out = S.win_words_out = 0;
 
     // zero the warp's histograms
@@ -1045,10 +1094,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
         S.refill(p);
         continue;
       }
-      const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.buf_a < end);
+      const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().buf_a[lane] < end);
       const uint32_t nq = __popc(m);
       queued += nq;
-      if (nq) S.last_j = __shfl_sync(FULL, S.buf_j, 31 - __clz(m)) + 1u;
+      if (nq) S.last_j = S.cold().buf_j[31 - __clz(m)] + 1u;
       if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
       S.buf_h = S.buf_n;
     }

@@ -92,8 +92,14 @@ typedef struct {
   uint32_t kv_ns_per_word;      /* ns per resident context word, <= 1024 (0 = SPEC's law) */
   uint32_t max_batch;           /* admission cap, 1..64 */
   uint32_t prefill_ns_per_word; /* prefill time per input word, <= 2^24 */
+  /* NEXT-4 KV-capacity admission (S:255 lists KV modelling as
+   * a SPEC non-goal): the queue head is admitted only if its whole context
+   * (input + realized output words) fits beside the contexts of everything in
+   * the system; strict FIFO; an oversized request runs alone.  0 = unlimited. */
+  uint32_t kv_cap_words;        /* <= 2^30 */
+  uint32_t _pad;
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;
-} bellman_profile;
+} bellman_profile; /* 56 bytes */
 
 /* Controller configuration (R3-R5, R22, R38). */
 typedef struct {

@@ -31,8 +31,39 @@ static void block(const orc_inputs *in, uint64_t sid, uint32_t j, uint32_t tag, 
   orc_philox(in->sc_seed[sid], SEED_HI, ctr, out);
 }
 
+/* per-request model draws (a3) of request index j from its tag-1 block */
+static void draws(const orc_inputs *in, uint64_t sid, uint32_t j, orc_request *r) {
+  uint32_t v[4];
+  block(in, sid, j, 1, v);
+  int64_t fvar = in->tab_fvar[v[0] >> 20];
+  int64_t noise = in->tab_noise[v[1] >> 20];
+  int64_t fcomp = in->tab_fcomp[v[2] >> 20];
+  int64_t U = ((int64_t)r->L * fvar + 32768) / 65536; /* U = max(1, round(L Fvar)) (R14) */
+  r->U = (uint32_t)(U < 1 ? 1 : U);
+  int64_t P = (int64_t)r->L + noise; /* P = max(1, L + Laplace noise) */
+  r->P = (uint32_t)(P < 1 ? 1 : P);
+  r->fcomp_q16 = (int32_t)fcomp;
+  r->qnoise = in->tab_qnoise[v[3] >> 20]; /* similarity noise (NEXT-2) */
+}
+
 int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint64_t cap_out) {
   uint32_t tr = in->sc_trace[sid];
+  if (in->trace_kind[tr] == 1) { /* NEXT-4 replay: the list as given, j = index */
+    uint32_t off = in->trace_knot_off[tr], n = in->trace_n_knots[tr], cap = in->trace_cap[tr];
+    if (cap && cap < n) n = cap;
+    if (!out) return n;
+    if (n > cap_out) return -1;
+    for (uint32_t k = 0; k < n; ++k) {
+      orc_request *r = &out[k];
+      r->a_us = (uint64_t)in->arr_a[off + k];
+      r->j = k;
+      r->L = in->arr_L[off + k];
+      r->input = in->arr_input[off + k];
+      r->cls = in->arr_cls[off + k];
+      draws(in, sid, k, r);
+    }
+    return n;
+  }
   uint32_t off = in->trace_knot_off[tr], nk = in->trace_n_knots[tr];
   uint32_t cap = in->trace_cap[tr];
   const int64_t *kt = in->knot_t + off;
@@ -71,19 +102,7 @@ int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint6
         r->cls = 3;
         for (uint32_t c = 0; c < 4; ++c)
           if ((u[2] & 0xFFFFFu) < in->class_cum[c]) { r->cls = c; break; }
-        uint32_t v[4];
-        block(in, sid, jj, 1, v);
-        int64_t fvar = in->tab_fvar[v[0] >> 20];
-        int64_t noise = in->tab_noise[v[1] >> 20];
-        int64_t fcomp = in->tab_fcomp[v[2] >> 20];
-        /* realized unbounded length U = max(1, round(L * Fvar)) (R14) */
-        int64_t U = ((int64_t)r->L * fvar + 32768) / 65536;
-        r->U = (uint32_t)(U < 1 ? 1 : U);
-        /* predicted length P = max(1, L + Laplace noise) (min_output = 1) */
-        int64_t P = (int64_t)r->L + noise;
-        r->P = (uint32_t)(P < 1 ? 1 : P);
-        r->fcomp_q16 = (int32_t)fcomp;
-        r->qnoise = in->tab_qnoise[v[3] >> 20]; /* similarity noise (NEXT-2) */
+        draws(in, sid, jj, r);
       }
       count++;
       if (cap && (uint64_t)count >= cap) return count; /* arrival cap (R28) */

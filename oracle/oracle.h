@@ -47,7 +47,11 @@ typedef struct {
   const int64_t *knot_t;
   const uint32_t *knot_lam;
   const uint32_t *trace_knot_off, *trace_n_knots, *trace_cap;
+  const uint32_t *trace_kind; /* 0 Poisson over knots, 1 replay of an explicit arrival list (NEXT-4) */
+  const int64_t *arr_a;       /* replay lists: arrival µs, L, input words, class */
+  const uint32_t *arr_L, *arr_input, *arr_cls;
   const uint32_t *prof_t0, *prof_knee, *prof_slope, *prof_kv, *prof_maxb, *prof_prefill_ns;
+  const uint32_t *prof_kv_cap; /* NEXT-4: KV capacity in context words, 0 = unlimited */
   const double *prof_e_in, *prof_e_out, *prof_p_idle;
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
@@ -82,6 +86,7 @@ typedef struct {
 typedef struct {
   uint32_t t0_us, knee, slope_us, kv_ns_per_word, max_batch, prefill_ns_per_word;
   double e_in, e_out, p_idle;
+  uint32_t kv_cap_words; /* NEXT-4 KV-capacity admission, 0 = unlimited */
 } orc_profile;
 
 typedef struct {

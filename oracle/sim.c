@@ -319,6 +319,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   }
 
   uint64_t q_head = 0, q_tail = 0, n_ready = 0, n_batch = 0, in_sys = 0;
+  uint64_t kv_reserved = 0; /* NEXT-4: sum of (input + R) over requests in the system */
   uint64_t n_e2e = 0, n_ttft = 0;
   int busy = 0;
   uint64_t next_sec = 0; /* first second not yet ingested */
@@ -396,6 +397,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
             rs[m].done = T;
             rs[m].state = RS_DONE;
             in_sys--;
+            kv_reserved -= (uint64_t)req[m].input + rs[m].R;
             res->served++;
             res->sum_e2e_us += e2e;
             res->sum_sojourn_us += e2e;
@@ -440,6 +442,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           rs[m].done = T;
           rs[m].state = RS_DONE;
           in_sys--;
+          kv_reserved -= (uint64_t)req[m].input + rs[m].R;
           res->served++;
           res->sum_e2e_us += e2e;
           res->sum_sojourn_us += e2e;
@@ -470,16 +473,23 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       /* admission point: ingest every closed second, then admit FIFO */
       INGEST_UNTIL(T);
       while (in_sys < prof->max_batch && q_head < q_tail) {
-        uint32_t m = queue[q_head++];
+        uint32_t m = queue[q_head];
         uint32_t r = cs.r;
         /* NEXT-3 bypass: class policy or a short predicted output */
-        if (r > 0 && (((ctrl->bypass_mask >> req[m].cls) & 1u) || req[m].P < ctrl->min_words_bypass)) {
-          r = 0;
-          res->bypassed++;
-        }
+        int bypass = r > 0 && (((ctrl->bypass_mask >> req[m].cls) & 1u) || req[m].P < ctrl->min_words_bypass);
+        if (bypass) r = 0;
+        uint32_t R = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+        /* NEXT-4 KV-capacity admission: the head's full context (input + realized
+         * output) must fit beside everything admitted; strict FIFO; an oversized
+         * request is admitted only into an empty system */
+        uint64_t need = (uint64_t)req[m].input + R;
+        if (prof->kv_cap_words && in_sys > 0 && kv_reserved + need > prof->kv_cap_words) break;
+        q_head++;
+        kv_reserved += need;
+        if (bypass) res->bypassed++;
         rs[m].admit = T;
         rs[m].r_bp = r;
-        rs[m].R = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+        rs[m].R = R;
         uint64_t pf = ((uint64_t)prof->prefill_ns_per_word * req[m].input) / 1000;
         rs[m].prefill_end = T + (pf < 1 ? 1 : pf);
         rs[m].state = RS_PREFILL;
@@ -650,6 +660,7 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   p->e_in = in->prof_e_in[pi];
   p->e_out = in->prof_e_out[pi];
   p->p_idle = in->prof_p_idle[pi];
+  p->kv_cap_words = in->prof_kv_cap[pi];
   memset(c, 0, sizeof(*c));
   c->law = in->ctrl_law[ci];
   c->signal = in->ctrl_signal[ci];

@@ -24,8 +24,8 @@ FLAG_TRUNCATED, FLAG_DEGENERATE_CALIB, FLAG_SERIES_OVERFLOW, FLAG_DONE = 0x1, 0x
 KNOT = np.dtype([("t_us", "<i8"), ("lam_mrps", "<u4"), ("_pad", "<u4")])
 TRACE = np.dtype([("knot_offset", "<u4"), ("n_knots", "<u4"), ("arrival_cap", "<u4"), ("_pad", "<u4")])
 PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv_ns_per_word", "<u4"),
-                    ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("e_in_j_per_word", "<f8"),
-                    ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
+                    ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("kv_cap_words", "<u4"), ("_pad", "<u4"),
+                    ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
 CTRL = np.dtype([(n, "<u4") for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp", "t1", "t2",
                                        "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))] +
                 [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")])
@@ -49,7 +49,7 @@ CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp"
                      ("_pad", "<u4"), ("A", "<u8")])
 RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
-assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 48
+assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 56
 assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
 
 

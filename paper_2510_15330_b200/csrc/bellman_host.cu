@@ -102,6 +102,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (p.slope_us > (1u << 16)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: slope_us > 2^16", i);
     if (p.prefill_ns_per_word > (1u << 24)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: prefill too large", i);
     if (p.kv_ns_per_word > 1024u) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_ns_per_word > 1024", i);
+    if (p.kv_cap_words > (1u << 30)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_cap_words > 2^30", i);
     if (!(p.e_in_j_per_word >= 0) || !(p.e_out_j_per_word >= 0) || !(p.p_idle_w >= 0))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: negative energy coefficient", i);
   }

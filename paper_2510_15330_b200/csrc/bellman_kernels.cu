@@ -121,6 +121,7 @@ struct Cold {
   uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
   uint32_t k0, wid_lo, wid_hi;
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
+  uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t ring[8];   // last `window` per-second samples (a6)
   // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
   // entry i written by lane i at refill, read by index at admission
@@ -133,6 +134,20 @@ struct Cold {
   uint32_t rungs[8];  // word-limit ladder (R5)
 
 };
+
+// a7 rewrite (R11): realized length of a request whose
+// unbounded length is U, predicted length P, compliance factor in fcq, under r.
+__device__ __forceinline__ uint32_t realized_len(const Params &p, uint32_t U, uint32_t P, uint32_t fcq, uint32_t ra) {
+  if (ra == 0) return U;
+  int64_t N = (int64_t)(((uint64_t)P * (10000u - ra) + 5000u) / 10000u);
+  if (N < 1) N = 1;
+  const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
+  const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
+  __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
+  if (x < 1) x = 1;
+  if (x > (1 << 24)) x = 1 << 24;
+  return (uint32_t)x;
+}
 
 // Write-only counters (a8) are lane-distributed: counter i lives in lane i's
 // register `ctr` and is bumped with a predicated add of a warp-uniform value
@@ -155,6 +170,7 @@ template <bool DBG>
 __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane, uint64_t H,
                                                bellman_second_row *dbg, uint32_t dbg_cap) {
   Cold &c = g_cold[wid];
+  __syncwarp();  // every lane's reads of the previous buffer precede the new writes
   uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
   uint32_t gen_acc = c.gen_acc;
   uint64_t gen_tau = c.gen_tau;
@@ -391,6 +407,8 @@ struct Sim {
   uint32_t sR[2], sin[2], sdn[2], sph[2];
   // ---- generator / queue head (a2)
   uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
+  uint32_t kv_res;        // NEXT-4: sum of (input + R) over requests in the system
+  uint32_t adm_blocked;   // NEXT-4: the arrived queue head does not fit the KV capacity
   uint64_t head_t;     // arrival time of the queue head, INF when no arrival remains
   // ---- counters (a8)
   uint64_t words_out, win_words_out;
@@ -410,7 +428,10 @@ struct Sim {
   // close the open second (if it holds samples) and open the one containing t
   __device__ __forceinline__ void roll_second(uint64_t t) {
     if (t < sec_bound) return;
-    if (acc_cnt) ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
+    if (acc_cnt) {
+      ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
+      adm_blocked = 0;  // r may have changed: the queue head may fit now
+    }
     acc_sum = 0;
     acc_cnt = 0;
     sec_bound = (t / kUs + 1u) * kUs;
@@ -525,7 +546,10 @@ struct Sim {
       next_done = __reduce_min_sync(FULL, dmin);
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
-      kv_sub((uint64_t)kv * __reduce_add_sync(FULL, kdrop));
+      const uint32_t kd = __reduce_add_sync(FULL, kdrop);
+      kv_sub((uint64_t)kv * kd);
+      kv_res -= kd;  // NEXT-4: completed contexts (input + R) free the KV capacity
+      adm_blocked = 0;
       cadd(CT_SERVED, ndone);
       cadd(CT_SUM_E2E, se);
       cadd(CT_SLO_VIOL, ns);
@@ -546,7 +570,7 @@ struct Sim {
   __device__ __forceinline__ void prefill_end(WarpHist &h) {
     const uint64_t Tn = T;
     uint64_t ttft_l = 0, e2e_l = 0;
-    uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0;
+    uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0, kfree = 0;
     uint32_t mpf = 0xffffffffu;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -557,6 +581,7 @@ struct Sim {
         ttft_l += tt;
         atomicAdd(&h.ttft[lat_bin(tt / 1000u)], 1u);
         if (sR[s] == 1u) {  // R9: completes at the prefill end
+          kfree += sin[s] + 1u;
           e2e_l += tt;
           nslo += tt > slo_us;
           n1++;
@@ -588,6 +613,8 @@ struct Sim {
     n_ready += __reduce_add_sync(FULL, nrdy);
     const uint32_t nc = __reduce_add_sync(FULL, n1);
     if (nc) {
+      kv_res -= __reduce_add_sync(FULL, kfree);
+      adm_blocked = 0;
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
       cadd(CT_SERVED, nc);
@@ -608,19 +635,48 @@ struct Sim {
   // Precondition: in_sys < maxb and head_t <= T.
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
     const uint64_t Tn = T;
+    adm_blocked = 0;
     for (;;) {
       const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Tn);
       const uint32_t na = __popc(arrived);
       const uint32_t room = maxb - in_sys;
-      const uint32_t k = na < room ? na : room;
+      uint32_t k = na < room ? na : room;
+      // NEXT-3 bypass rules (S:267, S:314, P:216), read once per admission point
+      const uint32_t bmask = cold().bypass_mask, minw = cold().min_words, kvcap = cold().kv_cap;
+      uint32_t kv_add = 0;
+      if (kvcap) {
+        // NEXT-4: candidate c (entry buf_h + c, FIFO order) is admitted iff its
+        // whole context and all earlier candidates' fit beside what is in the
+        // system; an oversized head is admitted into an empty system
+        uint32_t need = 0;
+        if (lane < k) {
+          const uint32_t e = buf_h + lane;
+          const uint32_t inc = cold().buf_in[e], P = cold().buf_P[e];
+          const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
+          need = (inc & 0xFFFFu) + realized_len(p, cold().buf_U[e], P, cold().buf_fcq[e], byp ? 0u : r);
+        }
+        uint32_t incl = need;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        const bool fits = lane < k && ((uint64_t)kv_res + incl <= kvcap || (lane == 0 && in_sys == 0));
+        const uint32_t fm = __ballot_sync(FULL, fits);
+        const uint32_t kk = (uint32_t)__ffs(~fm) - 1u;  // leading run of fitting candidates
+        k = kk < k ? kk : k;
+        kv_add = k ? __shfl_sync(FULL, incl, k - 1u) : 0u;
+        if (k == 0) {
+          adm_blocked = 1;
+          break;
+        }
+      }
       const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY);
       const uint32_t f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
       uint64_t q_l = 0;
       uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0;
-      // NEXT-3 bypass rules (S:267, S:314, P:216), read once per admission point
-      const uint32_t bmask = cold().bypass_mask, minw = cold().min_words;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t rank = s == 0 ? rank0 : rank1;
@@ -635,17 +691,9 @@ struct Sim {
           const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
           const uint32_t ra = byp ? 0u : r;
           n_byp += byp;
-          uint32_t R = U;
-          if (ra > 0) {  // a7 rewrite: N = round(P (1 - r)), realized = round(poly(N) Fcomp)
+          const uint32_t R = realized_len(p, U, P, fcq, ra);  // a7 rewrite
+          if (ra > 0) {
             n_rw++;
-            int64_t N = (int64_t)(((uint64_t)P * (10000u - ra) + 5000u) / 10000u);
-            if (N < 1) N = 1;
-            const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
-            const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
-            __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
-            if (x < 1) x = 1;
-            if (x > (1 << 24)) x = 1 << 24;
-            R = (uint32_t)x;
             atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
           }
 #ifndef BELLMAN_AB_NOQ
@@ -708,6 +756,7 @@ struct Sim {
         }
       }
       last_j = cold().buf_j[buf_h + k - 1u] + 1u;
+      kv_res += kv_add;
       in_sys += k;
       cadd(CT_ADMITTED, k);
       buf_h += k;
@@ -735,7 +784,9 @@ struct Sim {
   // cut short without changing results, so `room` is capped at 2^32 - 1.
   __device__ __forceinline__ void leap() {
     uint64_t stop = next_pf < stop_static ? next_pf : stop_static;
-    if (in_sys < maxb && head_t < stop) stop = head_t;
+    if (in_sys < maxb && !adm_blocked && head_t < stop) stop = head_t;
+    // a KV-blocked head may fit after an ingest changes r: stop at the second boundary
+    if (adm_blocked && sec_bound < stop) stop = sec_bound;
     const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
     if (nmax == 0 || stop <= T + 1u) return;
     const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
@@ -882,87 +933,86 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     // debug-recorded scenarios run in the DBG instantiation, all others in the product one
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
-    // ---- a1: scenario decode
+    // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
+    // lane 0 only and read after the __syncwarp below.
     Sim<DBG> S(threadIdx.x >> 5);
     S.lane = lane;
-    S.cold().k0 = sc.seed_index;
-    S.cold().wid_lo = (uint32_t)sc.wid;
-    S.cold().wid_hi = (uint32_t)(sc.wid >> 32);
-    S.H = (uint64_t)sc.horizon_us;
-    S.cold().w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
-    S.cold().w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
     const bellman_profile pr = p.profs[sc.profile];
+    const DevTrace tr = p.traces[sc.trace];
+    S.H = (uint64_t)sc.horizon_us;
     S.t0 = pr.t0_us;
     S.knee = pr.knee;
     S.slope = pr.slope_us;
     S.kv = pr.kv_ns_per_word;
     S.maxb = pr.max_batch;
     S.pf_ns = pr.prefill_ns_per_word;
-    S.cold().law = cc.law;
     S.signal = cc.signal;
-    S.cold().window = cc.window;
-    S.cold().rmin = cc.r_min_bp;
-    S.cold().rmax = cc.r_max_bp;
-    S.cold().t1 = cc.t1;
-    S.cold().t2 = cc.t2;
     S.slo_us = cc.slo_us;
-    S.cold().bypass_mask = cc.bypass_mask;
-    S.cold().min_words = cc.min_words_bypass;
-    S.cold().bypassed = 0;
-    S.cold().nrungs = cc.n_rungs;
-    S.cold().flags = 0;
+    // a10: thresholds from the paired unbounded run's calibration
+    uint32_t law = cc.law, t1 = cc.t1, t2 = cc.t2, flags = 0;
     if (cc.calibrated) {
-      const uint32_t slot = p.series_slot[sc.calib_src];
-      const uint32_t *cb = p.calib + 4u * slot;
-      S.cold().t1 = cb[0];
-      S.cold().t2 = cb[1];
+      const uint32_t *cb = p.calib + 4u * p.series_slot[sc.calib_src];
+      t1 = cb[0];
+      t2 = cb[1];
       if (cb[2] != 0) {
-        S.cold().law = BELLMAN_LAW_OFF;
-        S.cold().flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+        law = BELLMAN_LAW_OFF;
+        flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
       }
     }
-    S.r = S.cold().law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
-    S.cold().active = 0;
-    S.cold().rung = 0;
-    S.cold().ring_n = 0;
-    S.cold().ring_pos = 0;
-    S.cold().ringA = 0;
+    const uint32_t rslot = p.series_slot[sid];
+    const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
+    S.dbg = (DBG && dslot != BELLMAN_NONE) ? p.dbg_rows + p.dbg_off[dslot] : nullptr;
+    if (lane == 0) {
+      Cold &z = S.cold();
+      z.k0 = sc.seed_index;
+      z.wid_lo = (uint32_t)sc.wid;
+      z.wid_hi = (uint32_t)(sc.wid >> 32);
+      z.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
+      z.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+      z.law = law;
+      z.window = cc.window;
+      z.rmin = cc.r_min_bp;
+      z.rmax = cc.r_max_bp;
+      z.t1 = t1;
+      z.t2 = t2;
+      z.nrungs = cc.n_rungs;
+      z.bypass_mask = cc.bypass_mask;
+      z.min_words = cc.min_words_bypass;
+      z.bypassed = 0;
+      z.kv_cap = pr.kv_cap_words;
+      z.flags = flags;
+      z.active = z.rung = z.ring_n = z.ring_pos = 0;
+      z.ringA = 0;
+      z.activations = z.active_ingests = 0;
+      z.first_act = z.last_deact = BELLMAN_NONE;
+      z.series = rslot != BELLMAN_NONE ? p.series + p.series_off[rslot] : nullptr;
+      z.series_cap = rslot != BELLMAN_NONE ? p.series_cap[rslot] : 0u;
+      z.series_n = 0;
+      z.dbg_ctrl = (DBG && dslot != BELLMAN_NONE) ? p.dbg_ctrl + p.dbg_off[dslot] : nullptr;
+      z.dbg_cap = (DBG && dslot != BELLMAN_NONE) ? p.dbg_cap[dslot] : 0u;
+      z.dbg_nctrl = 0;
+      z.segs = p.segs + tr.seg_off;
+      z.n_seg = tr.n_seg;
+      z.gen_seg = z.gen_j = z.gen_acc = z.gen_done = 0;
+      z.gen_fresh = 1;
+      z.gen_cap = tr.cap;
+      z.gen_tau = 0;
+    }
     if (lane < 8) {
       S.cold().rungs[lane] = cc.rungs_bp[lane];
       S.cold().ring[lane] = 0;
     }
+    if (DBG && S.dbg) {  // rows are accumulated with atomics: zero this scenario's region first
+      const uint32_t cap = p.dbg_cap[dslot];
+      for (uint32_t i = lane; i < cap; i += 32u) S.dbg[i] = bellman_second_row{};
+    }
     __syncwarp();
-    S.cold().activations = 0;
-    S.cold().first_act = BELLMAN_NONE;
-    S.cold().last_deact = BELLMAN_NONE;
-    S.cold().active_ingests = 0;
+    S.r = law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
     S.acc_sum = 0;
     S.acc_cnt = 0;
-    const uint32_t rslot = p.series_slot[sid];
-    if (rslot != BELLMAN_NONE) {
-      S.cold().series = p.series + p.series_off[rslot];
-      S.cold().series_cap = p.series_cap[rslot];
-    } else {
-      S.cold().series = nullptr;
-      S.cold().series_cap = 0;
-    }
-    S.cold().series_n = 0;
-    const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
-    if (DBG && dslot != BELLMAN_NONE) {
-      S.dbg = p.dbg_rows + p.dbg_off[dslot];
-      S.cold().dbg_ctrl = p.dbg_ctrl + p.dbg_off[dslot];
-      S.cold().dbg_cap = p.dbg_cap[dslot];
-      // rows are accumulated with atomics: zero this scenario's region first
-      for (uint32_t i = lane; i < S.cold().dbg_cap; i += 32u) S.dbg[i] = bellman_second_row{};
-      __syncwarp();
-    } else {
-      S.dbg = nullptr;
-      S.cold().dbg_ctrl = nullptr;
-      S.cold().dbg_cap = 0;
-    }
-    S.cold().dbg_nctrl = 0;
     // the per-second signal feeds only the controller (MAP/STEP) and the recorders
-    S.sec_bound = (S.cold().law == BELLMAN_LAW_MAP || S.cold().law == BELLMAN_LAW_STEP || S.cold().series || (DBG && S.dbg)) ? kUs : INF;
+    S.sec_bound = (law == BELLMAN_LAW_MAP || law == BELLMAN_LAW_STEP || rslot != BELLMAN_NONE || (DBG && S.dbg))
+                      ? kUs : INF;
     S.T = 0;
     S.busy = 0;
     S.iter_end = INF;
@@ -982,17 +1032,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       // slots beyond max_batch are never free
       S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
     }
-    const DevTrace tr = p.traces[sc.trace];
-    S.cold().segs = p.segs + tr.seg_off;
-    S.cold().n_seg = tr.n_seg;
-    S.cold().gen_seg = 0;
-    S.cold().gen_fresh = 1;
-    S.cold().gen_j = 0;
-    S.cold().gen_acc = 0;
-    S.cold().gen_cap = tr.cap;
-    S.cold().gen_done = 0;
-    S.cold().gen_tau = 0;
     S.buf_h = S.buf_n = 0;
+    S.kv_res = 0;
+    S.adm_blocked = 0;
     S.last_j = 0;
 #ifndef BELLMAN_AB_REGCTR
     S.ctr = 0;
@@ -1030,7 +1072,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
         tn = S.iter_end;
       } else {
         tn = S.next_pf;
-        if (S.in_sys < S.maxb && S.head_t < tn) tn = S.head_t;
+        if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t < tn) tn = S.head_t;
         if (tn == INF) {
           finished = true;
           break;
@@ -1054,7 +1096,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
         S.prefill_end(h);
       }
       // the decode loop is idle here: admission point (R7), then the next iteration
-      if (S.in_sys < S.maxb && S.head_t <= tn) {
+      if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
         PROF(5);
         S.admit(p, h);
       }

@@ -1,0 +1,20 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck on small configs.
+set -u
+cd "$(dirname "$0")/.."
+cat > /tmp/san_run.py <<'PY'
+import sys; sys.path.insert(0, '.')
+import torch, workloads as W
+from paper_2510_15330_b200 import Simulator
+for w in (W.config_c1(), W.config_c2(n_seeds=1, rates=[0.5, 4.0], horizon_s=120), W.config_paper_pair(0)):
+    for s in w.scenarios[:2]:
+        s.record |= 2
+    sim = Simulator(w.columns()); sim.run(); torch.cuda.synchronize()
+    st = sim.stats()
+    print(w.name, int(st['ticks'].sum()), flush=True)
+PY
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool"
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_run.py 2>&1 | tail -6
+  echo "exit $?"
+done

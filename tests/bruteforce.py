@@ -96,8 +96,21 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                         r = Fraction(r_min) + Fraction(r_max - r_min) * (ma - t1) / (t2 - t1)
                         r_cur = min(r_max, int(r))  # floor to a basis point
             in_sys = sum(1 for i in range(n) if st[i] in ("prefill", "ready", "decoding"))
+            cap = prof.get("kv_cap_words", 0)
             while in_sys < prof["max_batch"] and queue:
-                m = queue.pop(0)
+                m = queue[0]
+                q = requests[m]
+                if cap:  # NEXT-4 KV-capacity admission: whole contexts must fit (empty system always admits)
+                    if r_cur > 0:
+                        Nh = max(1, int(Fraction(q.get("P", q["U"])) * (Fraction(10000 - r_cur, 10000)) + Fraction(1, 2)))
+                        Rh = max(1, int(Fraction(Nh) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
+                    else:
+                        Rh = q["U"]
+                    reserved = sum(requests[i]["input"] + R[i] for i in range(n)
+                                   if st[i] in ("prefill", "ready", "decoding"))
+                    if in_sys > 0 and reserved + q["input"] + Rh > cap:
+                        break
+                queue.pop(0)
                 admit[m] = t
                 rbp[m] = r_cur
                 q = requests[m]

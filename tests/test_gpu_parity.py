@@ -226,3 +226,23 @@ def test_next3_classes_bypass_and_ttft_signal():
     bad, st = check_all(w.columns())
     _assert_ok(bad)
     assert int(st["bypassed"].sum()) > 0
+
+
+def test_next4_kv_capacity_admission():
+    """NEXT-4 KV-capacity admission (FIFO, oversized requests alone) across
+    capacities, controllers (rewrite changes the admitted context), bypass and
+    drain/cutoff modes."""
+    import dataclasses
+
+    w = W.config_c3(n_seeds=1)
+    w.class_cum = W.MIXED_CLASSES
+    caps = [0, 40_000, 150_000, 300_000, 700_000]
+    w.profiles = [dict(W.PROFILES["P24"], kv_cap_words=c) for c in caps] + [dict(W.PROFILES["L8B"], kv_cap_words=90_000)]
+    w.ctrls[5] = dataclasses.replace(w.ctrls[5], bypass_mask=2, min_words_bypass=470)
+    sc = []
+    for i, s in enumerate(w.scenarios[::5]):
+        sc.append(dataclasses.replace(s, profile=i % len(w.profiles), mode=i % 2,
+                                      horizon_us=(1920 if i % 2 else 700) * W.US))
+    w.scenarios = sc
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)

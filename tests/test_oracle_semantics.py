@@ -284,3 +284,44 @@ def test_ttft_signal_is_per_second_mean(orc):
     got = {e["second"]: e["sample"] for e in d["ctrl_log"]}
     closed = {s: sum(v) // len(v) for s, v in want.items() if (s + 1) * 10**6 <= d["end_us"]}
     assert got == closed
+
+
+def test_bruteforce_kv_capacity(orc):
+    """NEXT-4 KV-capacity admission vs the brute-force simulator on random tiny
+    traces, with and without a constant rewrite rate."""
+    rng = np.random.default_rng(21)
+    for case in range(80):
+        reqs, prof = _random_tiny(rng)
+        prof["max_batch"] = int(rng.integers(2, 6))
+        prof["knee"] = min(prof["knee"], prof["max_batch"])
+        prof["kv_cap_words"] = int(rng.integers(20, 120))
+        law = "const" if case % 2 else "off"
+        rc = int(rng.integers(100, 3000)) if law == "const" else 0
+        bf = bruteforce.simulate(reqs, prof, 10**6, law=law, r_const=rc)
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=rc) if law == "const" else None
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=10**6)
+        assert d["ticks"] == bf["ticks"], case
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i]), (case, i)
+
+
+def test_kv_capacity_invariant_and_fifo(orc):
+    """At every instant the admitted contexts fit the capacity unless a single
+    oversized request runs alone; admission order stays FIFO."""
+    w = W.config_paper_pair(2)
+    w.profiles[0] = dict(w.profiles[0], kv_cap_words=120_000)
+    arr = orc.arrivals(w.columns(), 0)
+    reqs = [dict(a_us=int(x["a_us"]), input=int(x["input"]), U=int(x["U"])) for x in arr]
+    d = orc.simulate(reqs, w.profiles[0], mode=W.MODE_DRAIN)
+    R = [r["R"] for r in d["requests"]]
+    adm = [r["admit_us"] for r in d["requests"]]
+    done = [r["done_us"] for r in d["requests"]]
+    assert all(a <= b for a, b in zip(adm, adm[1:]))
+    for i, t in enumerate(adm):  # just after each admission
+        live = [k for k in range(len(reqs)) if adm[k] <= t < done[k]]
+        used = sum(reqs[k]["input"] + R[k] for k in live)
+        assert used <= 120_000 or len(live) == 1
+    free = orc.simulate(reqs, dict(w.profiles[0], kv_cap_words=0), mode=W.MODE_DRAIN)
+    assert d["sum_queue_us"] > free["sum_queue_us"]

@@ -242,6 +242,12 @@ class Workload:
         self.traces.append((list(knots), int(cap)))
         return len(self.traces) - 1
 
+    def add_replay_trace(self, events, cap=0):
+        """NEXT-4 replay: an explicit arrival list [(arrival_us, L, input, class), ...]
+        sorted by arrival; per-request draws are keyed by the list index."""
+        self.traces.append((("replay", [tuple(int(x) for x in e) for e in events]), int(cap)))
+        return len(self.traces) - 1
+
     def add_profile(self, prof):
         p = PROFILES[prof] if isinstance(prof, str) else prof
         self.profiles.append(dict(p))
@@ -255,11 +261,23 @@ class Workload:
 
     # ---- columns --------------------------------------------------------
     def columns(self) -> dict:
-        kt, kl, toff, tn, tcap = [], [], [], [], []
+        kt, kl, toff, tn, tcap, tkind = [], [], [], [], [], []
+        ra, rL, rI, rC = [], [], [], []
         for knots, cap in self.traces:
+            tcap.append(cap)
+            if isinstance(knots, tuple) and knots and knots[0] == "replay":
+                tkind.append(1)
+                toff.append(len(ra))
+                tn.append(len(knots[1]))
+                for a, L, inp, cls in knots[1]:
+                    ra.append(a)
+                    rL.append(L)
+                    rI.append(inp)
+                    rC.append(cls)
+                continue
+            tkind.append(0)
             toff.append(len(kt))
             tn.append(len(knots))
-            tcap.append(cap)
             for t, lam in knots:
                 kt.append(t)
                 kl.append(lam)
@@ -275,12 +293,14 @@ class Workload:
         f64 = lambda xs: np.asarray(xs, dtype=np.float64)
         cols = dict(
             knot_t=i64(kt), knot_lam=u32(kl),
-            trace_knot_off=u32(toff), trace_n_knots=u32(tn), trace_cap=u32(tcap),
+            trace_knot_off=u32(toff), trace_n_knots=u32(tn), trace_cap=u32(tcap), trace_kind=u32(tkind),
+            arr_a=i64(ra), arr_L=u32(rL), arr_input=u32(rI), arr_cls=u32(rC),
             prof_t0=u32([p["t0_us"] for p in P]), prof_knee=u32([p["knee"] for p in P]),
             prof_slope=u32([p["slope_us"] for p in P]), prof_kv=u32([p["kv_ns_per_word"] for p in P]),
             prof_maxb=u32([p["max_batch"] for p in P]), prof_prefill_ns=u32([p["prefill_ns_per_word"] for p in P]),
             prof_e_in=f64([p["e_in"] for p in P]), prof_e_out=f64([p["e_out"] for p in P]),
             prof_p_idle=f64([p["p_idle"] for p in P]),
+            prof_kv_cap=u32([p.get("kv_cap_words", 0) for p in P]),
             ctrl_law=u32([c.law for c in C]), ctrl_signal=u32([c.signal for c in C]),
             ctrl_window=u32([c.window for c in C]), ctrl_rmin=u32([c.r_min_bp for c in C]),
             ctrl_rmax=u32([c.r_max_bp for c in C]), ctrl_rconst=u32([c.r_const_bp for c in C]),
@@ -454,7 +474,9 @@ def custom(traces, profiles, ctrls, scenarios, tables=None, poly_q16=IDENTITY_PO
     w.tables = tables if tables is not None else quantile_tables()
     w.poly_q16 = tuple(poly_q16)
     for t in traces:
-        if isinstance(t, tuple) and len(t) == 2 and isinstance(t[1], int) and isinstance(t[0], list):
+        if isinstance(t, dict) and "replay" in t:
+            w.add_replay_trace(t["replay"], t.get("cap", 0))
+        elif isinstance(t, tuple) and len(t) == 2 and isinstance(t[1], int) and isinstance(t[0], list):
             w.add_trace(t[0], t[1])
         else:
             w.add_trace(t)
@@ -497,3 +519,66 @@ def config_paper_pair(seed_index=0, tables=None, peak=2.5, peak_s=90, valley=0.2
 
 
 CONFIGS["paper-pair"] = config_paper_pair
+
+
+# ----------------------------------------------------------------------------
+# trace files (NEXT-4 replay)
+# ----------------------------------------------------------------------------
+TRACE_HEADER = "id,arrival_ms,input_words,unbounded_output_words,class"
+CLASS_NAMES = ("summarization", "coding", "short-form", "other")
+
+
+class TraceFormatError(ValueError):
+    """Malformed or unsorted trace file; the message names the line."""
+
+
+def write_trace(path, events, comments=()):
+    """events: iterable of (id, arrival_ms, input_words, unbounded_output_words, class_index)."""
+    with open(path, "w", encoding="utf-8") as f:
+        for c in comments:
+            f.write(f"# {c}\n")
+        f.write(TRACE_HEADER + "\n")
+        for e in events:
+            i, a, inp, out, cls = e
+            f.write(f"{int(i)},{int(a)},{int(inp)},{int(out)},{CLASS_NAMES[int(cls)]}\n")
+
+
+def read_trace(path):
+    """Parse a trace file; returns a list of (id, arrival_ms, input, output, class_index).
+    Errors (S:69): malformed line -> TraceFormatError naming the line number;
+    arrival_ms decreasing -> TraceFormatError citing the later line."""
+    out = []
+    seen_header = False
+    last = None
+    with open(path, encoding="utf-8") as f:
+        for ln, raw in enumerate(f, 1):
+            line = raw.rstrip("\n")
+            if not seen_header:
+                if line.startswith("#") or not line.strip():
+                    continue
+                if line.strip() != TRACE_HEADER:
+                    raise TraceFormatError(f"line {ln}: expected header '{TRACE_HEADER}'")
+                seen_header = True
+                continue
+            parts = line.split(",")
+            if len(parts) != 5:
+                raise TraceFormatError(f"line {ln}: expected 5 fields, got {len(parts)}")
+            try:
+                i, a, inp, o = (int(x) for x in parts[:4])
+            except ValueError:
+                raise TraceFormatError(f"line {ln}: non-integer field") from None
+            name = parts[4].strip()
+            if name not in CLASS_NAMES:
+                raise TraceFormatError(f"line {ln}: unknown class '{name}'")
+            if a < 0 or inp < 1 or o < 1 or inp > 65535 or o > 65535:
+                raise TraceFormatError(f"line {ln}: field out of range")
+            if last is not None and a < last:
+                raise TraceFormatError(f"line {ln}: arrival_ms decreases (sortedness, S:77)")
+            last = a
+            out.append((i, a, inp, o, CLASS_NAMES.index(name)))
+    if not seen_header:
+        raise TraceFormatError("missing header")
+    ids = [e[0] for e in out]
+    if len(set(ids)) != len(ids):
+        raise TraceFormatError("duplicate request ids (S:43)")
+    return out

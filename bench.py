@@ -219,6 +219,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2510_15330_b200 import Simulator, _abi, pack
+    from paper_2510_15330_b200 import parallel as PAR
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -235,8 +236,7 @@ def main():
     stream = torch.cuda.current_stream()
     sim = Simulator(cols, device=local, stream=stream)
     stats_dev = torch.zeros((n, 256), dtype=torch.uint8, device=dev)
-    shard_dev = torch.zeros((count, 256), dtype=torch.uint8, device=dev)
-    gathered = torch.zeros((world * count, 256), dtype=torch.uint8, device=dev) if world > 1 else None
+    full_dev = torch.zeros((n, 256), dtype=torch.uint8, device=dev)
     seg_dev = torch.zeros((w.n_segments, _abi.SEG_HIST_WORDS), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -246,11 +246,10 @@ def main():
         k_end = torch.cuda.Event(enable_timing=True)
         k_end.record(stream)
         sim.stats_device(stats_dev, stream=stream)
-        shard_dev.copy_(stats_dev[rank::world])
         sim.segment_hist_device(seg_dev, stream=stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, shard_dev)
-            dist.all_reduce(seg_dev)
+        # the one exchange step: summaries all-gathered, segment histograms summed (NCCL)
+        PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank, world, out=full_dev)
+        PAR.reduce_segments(seg_dev)
         return k_end
 
     for _ in range(args.warmup):

@@ -77,11 +77,22 @@ typedef struct {
 } bellman_knot;
 
 typedef struct {
-  uint32_t knot_offset; /* first knot in desc->knots */
-  uint32_t n_knots;     /* >= 2 */
+  uint32_t knot_offset; /* kind 0: first knot in desc->knots; kind 1: first entry of desc->arrivals */
+  uint32_t n_knots;     /* kind 0: knots, >= 2; kind 1: arrivals in the list */
   uint32_t arrival_cap; /* stop after this many arrivals; 0 = none */
-  uint32_t _pad;
+  uint32_t kind;        /* 0: Poisson over the knots (a2); 1: replay of an explicit arrival list (NEXT-4) */
 } bellman_trace;
+
+/* One arrival of a replay trace (NEXT-4; SPEC's trace file S:29-34):
+ * entries of a trace sorted by arrival; the per-request draws (a3) are keyed
+ * by the entry's index in its trace. */
+typedef struct {
+  int64_t a_us;         /* arrival time, µs, >= 0 */
+  uint32_t L_words;     /* natural (unbounded) output words, 1..65535 */
+  uint32_t input_words; /* 1..65535 */
+  uint32_t cls;         /* request class 0..3 (NEXT-3) */
+  uint32_t _pad;
+} bellman_arrival; /* 24 bytes */
 
 /* Serving cost profile (decode law S:209-217; prefill S:218-226;
  * energy S:227-235; optional KV term, reading R2). */
@@ -189,6 +200,8 @@ typedef struct {
   uint64_t n_scenarios;
   uint32_t n_segments; /* segment ids in [0, n_segments) */
   uint32_t _pad;
+  const bellman_arrival *arrivals; /* replay lists of kind-1 traces (may be NULL if none) */
+  uint64_t n_arrivals;
 } bellman_sim_desc;
 
 /* 256-byte per-scenario summary (a8, a9, a6 logs).  All counts are exact

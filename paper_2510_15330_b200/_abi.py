@@ -22,7 +22,8 @@ NONE = 0xFFFFFFFF
 FLAG_TRUNCATED, FLAG_DEGENERATE_CALIB, FLAG_SERIES_OVERFLOW, FLAG_DONE = 0x1, 0x2, 0x4, 0x100
 
 KNOT = np.dtype([("t_us", "<i8"), ("lam_mrps", "<u4"), ("_pad", "<u4")])
-TRACE = np.dtype([("knot_offset", "<u4"), ("n_knots", "<u4"), ("arrival_cap", "<u4"), ("_pad", "<u4")])
+TRACE = np.dtype([("knot_offset", "<u4"), ("n_knots", "<u4"), ("arrival_cap", "<u4"), ("kind", "<u4")])
+ARRIVAL = np.dtype([("a_us", "<i8"), ("L_words", "<u4"), ("input_words", "<u4"), ("cls", "<u4"), ("_pad", "<u4")])
 PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv_ns_per_word", "<u4"),
                     ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("kv_cap_words", "<u4"), ("_pad", "<u4"),
                     ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
@@ -49,6 +50,7 @@ CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp"
                      ("_pad", "<u4"), ("A", "<u8")])
 RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
+assert ARRIVAL.itemsize == 24
 assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 56
 assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
 
@@ -67,7 +69,8 @@ class Desc(C.Structure):
                 ("ctrls", C.c_void_p), ("n_ctrls", C.c_uint32),
                 ("models", Models),
                 ("scenarios", C.c_void_p), ("n_scenarios", C.c_uint64),
-                ("n_segments", C.c_uint32), ("_pad", C.c_uint32)]
+                ("n_segments", C.c_uint32), ("_pad", C.c_uint32),
+                ("arrivals", C.c_void_p), ("n_arrivals", C.c_uint64)]
 
 
 EXPORTS = {

@@ -84,6 +84,20 @@ static bellman_status validate(const bellman_sim_desc *d) {
       return fail(nullptr, BELLMAN_EINVAL, "poly_q16[%d] out of range", k);
   for (uint32_t t = 0; t < d->n_traces; ++t) {
     const bellman_trace &tr = d->traces[t];
+    if (tr.kind > 1) return fail(nullptr, BELLMAN_EINVAL, "trace %u: unknown kind", t);
+    if (tr.kind == 1) {  // NEXT-4 replay list
+      if ((uint64_t)tr.knot_offset + tr.n_knots > d->n_arrivals || (tr.n_knots && !d->arrivals))
+        return fail(nullptr, BELLMAN_EINVAL, "trace %u: bad arrival range", t);
+      for (uint32_t k = 0; k < tr.n_knots; ++k) {
+        const bellman_arrival &a = d->arrivals[tr.knot_offset + k];
+        if (a.a_us < 0 || a.a_us > (1ll << 43) || a.L_words < 1 || a.L_words > 65535 || a.input_words < 1 ||
+            a.input_words > 65535 || a.cls > 3)
+          return fail(nullptr, BELLMAN_EINVAL, "trace %u arrival %u: field out of range", t, k);
+        if (k && a.a_us < d->arrivals[tr.knot_offset + k - 1].a_us)
+          return fail(nullptr, BELLMAN_EINVAL, "trace %u: arrivals not sorted at %u", t, k);
+      }
+      continue;
+    }
     if (tr.n_knots < 2 || (uint64_t)tr.knot_offset + tr.n_knots > d->n_knots)
       return fail(nullptr, BELLMAN_EINVAL, "trace %u: bad knot range", t);
     for (uint32_t k = 0; k < tr.n_knots; ++k) {
@@ -154,7 +168,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, total;
+      off_drows, off_dctrl, off_arr, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -176,6 +190,10 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
   h.traces.resize(d->n_traces);
   for (uint32_t t = 0; t < d->n_traces; ++t) {
     const bellman_trace &tr = d->traces[t];
+    if (tr.kind == 1) {  // replay: seg_off / n_seg index the device copy of desc->arrivals
+      h.traces[t] = DevTrace{tr.knot_offset, tr.n_knots, tr.arrival_cap, 1u};
+      continue;
+    }
     DevTrace dt{(uint32_t)h.segs.size(), 0, tr.arrival_cap, 0};
     for (uint32_t k = 0; k + 1 < tr.n_knots; ++k) {
       const bellman_knot &a = d->knots[tr.knot_offset + k], &b = d->knots[tr.knot_offset + k + 1];
@@ -254,6 +272,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dn = take(sizeof(uint32_t) * 2 * nd);
   L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
   L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
+  L.off_arr = take(sizeof(bellman_arrival) * d->n_arrivals);
   L.total = o;
   return L;
 }
@@ -363,6 +382,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.dbg_n = (uint32_t *)(ws + L.off_dn);
   P.dbg_rows = (bellman_second_row *)(ws + L.off_drows);
   P.dbg_ctrl = (bellman_ctrl_row *)(ws + L.off_dctrl);
+  P.arrivals = (const bellman_arrival *)(ws + L.off_arr);
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
   sim->dbg_off = h.dbg_off;
@@ -392,6 +412,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
       H2D(P.series_cap, h.slot_cap.data(), sizeof(uint32_t) * h.slot_cap.size());
       if (h.slot_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.series_n, 0, sizeof(uint32_t) * h.slot_off.size(), s));
       H2D(P.dbg_slot, h.dbg_of.data(), sizeof(uint32_t) * desc->n_scenarios);
+      H2D(P.arrivals, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
       H2D(P.dbg_off, h.dbg_off.data(), sizeof(uint64_t) * h.dbg_off.size());
       H2D(P.dbg_cap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
       if (h.dbg_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.dbg_n, 0, sizeof(uint32_t) * 2 * h.dbg_off.size(), s));

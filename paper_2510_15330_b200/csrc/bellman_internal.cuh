@@ -22,7 +22,7 @@ struct DevSeg {
 static_assert(sizeof(DevSeg) == 48, "DevSeg layout");
 
 struct DevTrace {
-  uint32_t seg_off, n_seg, cap, _pad;
+  uint32_t seg_off, n_seg, cap, kind;  // kind 1 (replay): seg_off/n_seg index Params::arrivals
 };
 
 // Per-warp shared-memory histograms (a9, NEXT-2): 10,848 bytes.
@@ -58,6 +58,7 @@ struct Params {
   uint32_t *dbg_n;              // [n_dbg][2]: rows, controller-log rows written
   bellman_second_row *dbg_rows;
   bellman_ctrl_row *dbg_ctrl;
+  const bellman_arrival *arrivals;  // replay lists (NEXT-4)
   bellman_scenario_stats *stats;
   unsigned long long *seg_hist;  // [n_segments][kSegWords]
   unsigned int *counter;         // work counter of this launch

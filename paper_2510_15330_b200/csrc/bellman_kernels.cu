@@ -116,6 +116,8 @@ struct Cold {
   uint32_t *series;
   bellman_ctrl_row *dbg_ctrl;
   uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
+  uint32_t replay;  // NEXT-4: the trace is an explicit arrival list (segs unused)
+  uint32_t rep_off;
   uint32_t law, window, rmin, rmax, t1, t2, nrungs, ring_n, ring_pos, rung, active;
   uint32_t activations, first_act, last_deact, active_ingests;
   uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
@@ -136,17 +138,34 @@ struct Cold {
 };
 
 // a7 rewrite (R11): realized length of a request whose
-// unbounded length is U, predicted length P, compliance factor in fcq, under r.
-__device__ __forceinline__ uint32_t realized_len(const Params &p, uint32_t U, uint32_t P, uint32_t fcq, uint32_t ra) {
-  if (ra == 0) return U;
+// predicted length is P and compliance factor in fcq under r > 0:
+// N = round(P (1 - r)), realized = clamp(round(poly(N) Fcomp), 1, 2^24).
+// Out of line (one copy): it runs once per rewritten admission.
+__device__ __noinline__ uint32_t rewrite_len(int64_t poly0, int64_t poly1, int64_t poly2, uint32_t P, uint32_t fcq,
+                                             uint32_t ra) {
   int64_t N = (int64_t)(((uint64_t)P * (10000u - ra) + 5000u) / 10000u);
   if (N < 1) N = 1;
-  const __int128 poly = (__int128)p.poly0 + (__int128)p.poly1 * N + (__int128)p.poly2 * N * N;
+  const __int128 poly = (__int128)poly0 + (__int128)poly1 * N + (__int128)poly2 * N * N;
   const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
   __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
   if (x < 1) x = 1;
   if (x > (1 << 24)) x = 1 << 24;
   return (uint32_t)x;
+}
+
+__device__ __forceinline__ uint32_t realized_len(const Params &p, uint32_t U, uint32_t P, uint32_t fcq, uint32_t ra) {
+  return ra == 0 ? U : rewrite_len(p.poly0, p.poly1, p.poly2, P, fcq, ra);
+}
+
+// NEXT-2 similarity decay between the safe window and decay_end:
+// q_active - floor((q_active - q_floor) X / D), 0 < X < D < 2^32, float
+// estimate with an exact integer fix-up.  Out of line (rare branch).
+__device__ __noinline__ int32_t sim_decay(uint32_t q_active, uint32_t q_floor, uint64_t X, uint64_t D) {
+  const uint64_t aX = (uint64_t)(q_active - q_floor) * X;
+  uint32_t q = (uint32_t)__fmul_rz((float)aX, __frcp_rn((float)D));
+  while (q && (uint64_t)q * D > aX) q--;
+  while ((uint64_t)(q + 1u) * D <= aX) q++;
+  return (int32_t)q_active - (int32_t)q;
 }
 
 // Write-only counters (a8) are lane-distributed: counter i lives in lane i's
@@ -157,6 +176,37 @@ enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL 
 // One Cold block per warp of the CTA, in static shared memory so that every
 // access is a 32-bit LDS/STS off a known base (no generic pointer).
 __shared__ Cold g_cold[kWarpsPerBlock];
+
+// NEXT-4 KV-capacity admission: of the first k arrived candidates (entries
+// buf_h.. of the shared buffer, FIFO), the leading run whose whole contexts
+// (input + realized output under r) fit beside `res` reserved words; an
+// oversized head enters an empty system.  Returns (count | added words << 32).
+// Out of line: only profiles with a KV capacity take this branch.
+__device__ __noinline__ uint64_t kv_admit(const Params &p, uint32_t wid, uint32_t lane, uint32_t buf_h, uint32_t k,
+                                          uint32_t r, uint32_t bmask, uint32_t minw, uint32_t kvcap, uint32_t res,
+                                          uint32_t in_sys) {
+  const Cold &c = g_cold[wid];
+  uint32_t need = 0;
+  if (lane < k) {
+    const uint32_t e = buf_h + lane;
+    const uint32_t inc = c.buf_in[e], P = c.buf_P[e];
+    const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
+    need = (inc & 0xFFFFu) + realized_len(p, c.buf_U[e], P, c.buf_fcq[e], byp ? 0u : r);
+  }
+  uint32_t incl = need;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  const bool fits = lane < k && ((uint64_t)res + incl <= kvcap || (lane == 0 && in_sys == 0));
+  const uint32_t fm = __ballot_sync(FULL, fits);
+  const uint32_t kk = (uint32_t)__ffs(~fm) - 1u;  // leading run of fitting candidates
+  const uint32_t n = kk < k ? kk : k;
+  const uint32_t add = n ? __shfl_sync(FULL, incl, n - 1u) : 0u;
+  return (uint64_t)n | ((uint64_t)add << 32);
+}
+
 
 // ---------------------------------------------------------------------------
 // a2 + a3: refill the warp's shared arrival buffer with the next accepted
@@ -177,7 +227,33 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
   const uint32_t n_seg = c.n_seg, gen_cap = c.gen_cap, k0 = c.k0, wid_lo = c.wid_lo, wid_hi = c.wid_hi;
   const DevSeg *segs = c.segs;
   uint32_t n = 0;
-  while (!gen_done && n == 0) {
+  if (__builtin_expect(c.replay != 0, 0)) {  // NEXT-4 replay: entries gen_j .. gen_j+31 of the list, draws keyed by index
+    uint32_t left = gen_done ? 0u : n_seg - gen_j;
+    if (gen_cap && gen_cap - gen_acc < left) left = gen_cap - gen_acc;
+    n = left < 32u ? left : 32u;
+    if (lane < n) {
+      const uint32_t jj = gen_j + lane;
+      const bellman_arrival A = p.arrivals[c.rep_off + jj];
+      const uint64_t tau = (uint64_t)A.a_us;
+      c.buf_a[lane] = tau;
+      c.buf_in[lane] = A.input_words | (A.cls << 16);
+      c.buf_j[lane] = jj;
+      const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
+      const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
+      c.buf_U[lane] = U < 1 ? 1u : (uint32_t)U;
+      const int32_t P0 = (int32_t)A.L_words + __ldg(&p.tabN[v.y >> 20]);
+      c.buf_P[lane] = P0 < 1 ? 1u : (uint32_t)P0;
+      c.buf_fcq[lane] = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      if (DBG && dbg && tau < H) {
+        const uint64_t sidx = tau / kUs;
+        atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
+      }
+    }
+    gen_j += n;
+    gen_acc += n;
+    if (n == 0 || gen_j >= n_seg || (gen_cap && gen_acc >= gen_cap)) gen_done = 1;
+  }
+  while (!c.replay && !gen_done && n == 0) {
     if (gen_seg >= n_seg) {
       gen_done = 1;
       break;
@@ -644,28 +720,10 @@ struct Sim {
       // NEXT-3 bypass rules, read once per admission point
       const uint32_t bmask = cold().bypass_mask, minw = cold().min_words, kvcap = cold().kv_cap;
       uint32_t kv_add = 0;
-      if (kvcap) {
-        // NEXT-4: candidate c (entry buf_h + c, FIFO order) is admitted iff its
-        // whole context and all earlier candidates' fit beside what is in the
-        // system; an oversized head is admitted into an empty system
-        uint32_t need = 0;
-        if (lane < k) {
-          const uint32_t e = buf_h + lane;
-          const uint32_t inc = cold().buf_in[e], P = cold().buf_P[e];
-          const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
-          need = (inc & 0xFFFFu) + realized_len(p, cold().buf_U[e], P, cold().buf_fcq[e], byp ? 0u : r);
-        }
-        uint32_t incl = need;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= (uint32_t)o) incl += y;
-        }
-        const bool fits = lane < k && ((uint64_t)kv_res + incl <= kvcap || (lane == 0 && in_sys == 0));
-        const uint32_t fm = __ballot_sync(FULL, fits);
-        const uint32_t kk = (uint32_t)__ffs(~fm) - 1u;  // leading run of fitting candidates
-        k = kk < k ? kk : k;
-        kv_add = k ? __shfl_sync(FULL, incl, k - 1u) : 0u;
+      if (__builtin_expect(kvcap != 0, 0)) {
+        const uint64_t kr2 = kv_admit(p, wid, lane, buf_h, k, r, bmask, minw, kvcap, kv_res, in_sys);
+        k = (uint32_t)kr2;
+        kv_add = (uint32_t)(kr2 >> 32);
         if (k == 0) {
           adm_blocked = 1;
           break;
@@ -706,14 +764,8 @@ struct Sim {
               } else if (num >= (int64_t)p.q_end * den) {
                 base = (int32_t)p.q_floor;
               } else {
-                // floor(a X / D), 0 < X < D < 2^32, a <= 10^4: float estimate, exact integer fix-up
-                const uint64_t X = (uint64_t)(num - (int64_t)p.q_safe * den);
-                const uint64_t D = (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den;
-                const uint64_t aX = (uint64_t)(p.q_active - p.q_floor) * X;
-                uint32_t q = (uint32_t)__fmul_rz((float)aX, __frcp_rn((float)D));
-                while (q && (uint64_t)q * D > aX) q--;
-                while ((uint64_t)(q + 1u) * D <= aX) q++;
-                base = (int32_t)p.q_active - (int32_t)q;
+                base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
+                                 (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
               }
             }
             int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
@@ -991,8 +1043,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       z.dbg_ctrl = (DBG && dslot != BELLMAN_NONE) ? p.dbg_ctrl + p.dbg_off[dslot] : nullptr;
       z.dbg_cap = (DBG && dslot != BELLMAN_NONE) ? p.dbg_cap[dslot] : 0u;
       z.dbg_nctrl = 0;
-      z.segs = p.segs + tr.seg_off;
+      z.segs = p.segs + (tr.kind ? 0u : tr.seg_off);
       z.n_seg = tr.n_seg;
+      z.replay = tr.kind;
+      z.rep_off = tr.kind ? tr.seg_off : 0u;
       z.gen_seg = z.gen_j = z.gen_acc = z.gen_done = 0;
       z.gen_fresh = 1;
       z.gen_cap = tr.cap;

@@ -38,6 +38,15 @@ def pack(cols: dict, pinned: bool = False) -> dict:
     traces[:nt]["knot_offset"] = cols["trace_knot_off"]
     traces[:nt]["n_knots"] = cols["trace_n_knots"]
     traces[:nt]["arrival_cap"] = cols["trace_cap"]
+    traces[:nt]["kind"] = cols.get("trace_kind", np.zeros(nt, dtype=np.uint32))
+    na = len(cols.get("arr_a", ()))
+    arrs, k = alloc(A.ARRIVAL, na)
+    keep.append(k)
+    if na:
+        arrs[:na]["a_us"] = cols["arr_a"]
+        arrs[:na]["L_words"] = cols["arr_L"]
+        arrs[:na]["input_words"] = cols["arr_input"]
+        arrs[:na]["cls"] = cols["arr_cls"]
     npf = len(cols["prof_t0"])
     profs, k = alloc(A.PROFILE, npf)
     keep.append(k)
@@ -72,6 +81,7 @@ def pack(cols: dict, pinned: bool = False) -> dict:
         t[:] = cols[name]
         tabs[name] = t
     out.update(knots=knots, n_knots=nk, traces=traces, n_traces=nt, profiles=profs, n_profiles=npf,
+               arrivals=arrs, n_arrivals=na,
                ctrls=ctrls, n_ctrls=nc, scenarios=scs, n_scenarios=ns, tables=tabs,
                poly_q16=np.asarray(cols["poly_q16"], dtype=np.int64), n_segments=int(cols["n_segments"]),
                quality=np.asarray(cols["quality"], dtype=np.uint32),
@@ -89,7 +99,8 @@ def make_desc(pk: dict) -> A.Desc:
                  (C.c_uint32 * 4)(*[int(x) for x in pk["class_cum"]]), (C.c_uint32 * 3)(0, 0, 0))
     return A.Desc(pk["knots"].ctypes.data, pk["n_knots"], pk["traces"].ctypes.data, pk["n_traces"],
                   pk["profiles"].ctypes.data, pk["n_profiles"], pk["ctrls"].ctypes.data, pk["n_ctrls"], m,
-                  pk["scenarios"].ctypes.data, pk["n_scenarios"], pk["n_segments"], 0)
+                  pk["scenarios"].ctypes.data, pk["n_scenarios"], pk["n_segments"], 0,
+                  pk["arrivals"].ctypes.data, pk["n_arrivals"])
 
 
 def workspace_bytes(pk: dict) -> int:

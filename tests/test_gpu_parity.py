@@ -246,3 +246,27 @@ def test_next4_kv_capacity_admission():
     w.scenarios = sc
     bad, st = check_all(w.columns())
     _assert_ok(bad)
+
+
+def test_next4_trace_replay():
+    """NEXT-4 replay of explicit arrival lists: lists longer than one
+    32-entry refill, arrival caps, simultaneous arrivals, classes, with KV
+    capacity and the controller, next to Poisson traces in the same run."""
+    rng = np.random.default_rng(77)
+    reps = []
+    for t in range(3):
+        n = int(rng.integers(40, 900))
+        gaps = rng.exponential(1e6 / (1.0 + 2 * t), n).astype(np.int64)
+        gaps[rng.random(n) < 0.1] = 0  # simultaneous arrivals
+        a = np.cumsum(gaps)
+        reps.append([(int(a[k]), int(rng.integers(1, 1300)), int(rng.integers(1, 20000)), int(rng.integers(0, 4)))
+                     for k in range(n)])
+    traces = [{"replay": reps[0]}, {"replay": reps[1], "cap": 33}, {"replay": reps[2]}, W.paper_trace()]
+    profs = [W.PROFILES["P24"], dict(W.PROFILES["L8B"], kv_cap_words=200_000)]
+    ctrls = [W.OFF, W.map_ctrl(21_000, 26_000), W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 900, bypass_mask=2)]
+    sc = [W.Scenario(s, wid=t, trace=t, profile=pi, ctrl=ci, segment=0, mode=s % 2, horizon_us=2000 * W.US)
+          for t in range(4) for pi in range(2) for ci in range(3) for s in range(2)]
+    w = W.custom(traces, profs, ctrls, sc)
+    w.class_cum = W.MIXED_CLASSES
+    bad, _ = check_all(w.columns())
+    _assert_ok(bad)

@@ -236,7 +236,10 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
  * (interleaved sharding across ranks: first = rank, stride = world size).
  * Calibrated scenarios (a10) need their source in the same set.  Launches the
  * pass-1 kernel, then (if any calibrated scenario is in the set) the
- * calibration kernel and the pass-2 kernel.  Asynchronous. */
+ * calibration kernel and the pass-2 kernel.  A whole-set run (first 0,
+ * stride 1, count n_scenarios) hands scenarios to warps in decreasing order of
+ * expected arrivals (heavy first, for load balance); results never depend on
+ * that order.  Asynchronous. */
 bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count, uint64_t stride,
                                void *stream);
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -28,6 +29,7 @@ struct bellman_sim {
   std::vector<uint32_t> dbg_slot;    // per scenario: debug-record slot or NONE
   std::vector<uint64_t> dbg_off;
   std::vector<uint32_t> dbg_cap;
+  const uint32_t *order = nullptr;   // device: scenarios by decreasing expected work
   char err[512] = {0};
 };
 
@@ -168,7 +170,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, total;
+      off_drows, off_dctrl, off_arr, off_ord, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -184,7 +186,35 @@ struct HostPrep {
   std::vector<uint64_t> dbg_off;   // per debug slot, in rows
   std::vector<uint32_t> dbg_cap;
   uint64_t dbg_rows = 0;
+  std::vector<uint32_t> order;     // scenarios by decreasing expected arrivals (stable)
 };
+
+// Expected arrivals of a scenario: the integral of its trace's rate over
+// [0, horizon) (kind 0) or the listed arrivals before the horizon (kind 1),
+// capped by arrival_cap.  Used only to order the work (heavy scenarios first,
+// so that the longest serial chains start at once and on distinct SM
+// sub-partitions); results do not depend on the order.
+static double expected_arrivals(const bellman_sim_desc *d, const bellman_scenario &sc) {
+  const bellman_trace &tr = d->traces[sc.trace];
+  const double H = (double)sc.horizon_us;
+  double n = 0;
+  if (tr.kind == 1) {
+    const bellman_arrival *a = d->arrivals + tr.knot_offset;
+    n = (double)(std::lower_bound(a, a + tr.n_knots, sc.horizon_us,
+                                  [](const bellman_arrival &x, int64_t h) { return x.a_us < h; }) - a);
+  } else {
+    for (uint32_t k = 0; k + 1 < tr.n_knots; ++k) {
+      const bellman_knot &a = d->knots[tr.knot_offset + k], &b = d->knots[tr.knot_offset + k + 1];
+      const double ta = (double)a.t_us, tb = (double)b.t_us;
+      if (tb <= ta || ta >= H) continue;
+      const double te = tb < H ? tb : H;
+      const double le = a.lam_mrps + ((double)b.lam_mrps - a.lam_mrps) * (te - ta) / (tb - ta);
+      n += 0.5 * (a.lam_mrps + le) * (te - ta) * 1e-9;  // mRPS x µs
+    }
+  }
+  if (tr.arrival_cap && n > tr.arrival_cap) n = tr.arrival_cap;
+  return n;
+}
 
 static void prepare(const bellman_sim_desc *d, HostPrep &h) {
   h.traces.resize(d->n_traces);
@@ -238,6 +268,11 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
     h.slot_cap.push_back((uint32_t)cap);
     h.series_words += cap;
   }
+  std::vector<double> cost(d->n_scenarios);
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) cost[s] = expected_arrivals(d, d->scenarios[s]);
+  h.order.resize(d->n_scenarios);
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) h.order[s] = (uint32_t)s;
+  std::stable_sort(h.order.begin(), h.order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
 }
 
 static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
@@ -273,6 +308,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
   L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
   L.off_arr = take(sizeof(bellman_arrival) * d->n_arrivals);
+  L.off_ord = take(sizeof(uint32_t) * d->n_scenarios);
   L.total = o;
   return L;
 }
@@ -383,6 +419,8 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.dbg_rows = (bellman_second_row *)(ws + L.off_drows);
   P.dbg_ctrl = (bellman_ctrl_row *)(ws + L.off_dctrl);
   P.arrivals = (const bellman_arrival *)(ws + L.off_arr);
+  P.order = nullptr;
+  sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
   sim->dbg_off = h.dbg_off;
@@ -413,6 +451,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
       if (h.slot_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.series_n, 0, sizeof(uint32_t) * h.slot_off.size(), s));
       H2D(P.dbg_slot, h.dbg_of.data(), sizeof(uint32_t) * desc->n_scenarios);
       H2D(P.arrivals, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
+      H2D(sim->order, h.order.data(), sizeof(uint32_t) * desc->n_scenarios);
       H2D(P.dbg_off, h.dbg_off.data(), sizeof(uint64_t) * h.dbg_off.size());
       H2D(P.dbg_cap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
       if (h.dbg_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.dbg_n, 0, sizeof(uint32_t) * 2 * h.dbg_off.size(), s));
@@ -460,6 +499,11 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   P.first = first;
   P.count = count;
   P.stride = stride;
+  // a whole-set run takes the scenarios heavy-first; a subset keeps index order
+  P.order = (first == 0 && stride == 1 && count == sim->n_scenarios) ? sim->order : nullptr;
+#ifdef BELLMAN_AB_NOORDER
+  P.order = nullptr;
+#endif
   CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 4 * sizeof(unsigned int), s));
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);

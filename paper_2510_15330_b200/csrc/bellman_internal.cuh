@@ -62,6 +62,7 @@ struct Params {
   bellman_scenario_stats *stats;
   unsigned long long *seg_hist;  // [n_segments][kSegWords]
   unsigned int *counter;         // work counter of this launch
+  const uint32_t *order;         // heavy-first scenario order of a whole-set run, else NULL
   uint64_t first, count, stride;
   uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
 };

@@ -338,14 +338,17 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
 }
 
 // ---------------------------------------------------------------------------
-// a6: one controller ingest of the sample x of closed second `second` (P:134,
-// P:193; R3-R5, R12, R38).  Out of line: it runs once per simulated
-// second, so it stays out of the event loop's instruction-cache footprint.
-// All lanes compute; only lane 0 writes the shared-memory state.
+// a6: one controller ingest of the closed second ending at sec_bound, whose
+// sample is the integer mean x = floor(acc_sum / acc_cnt) (P:134, P:193,
+// S:283-301; R3-R5, R12, R38).  Out of line, the 64-bit division included: it
+// runs once per simulated second, so it stays out of the event loop's
+// instruction-cache footprint.  All lanes compute; only lane 0 writes the
+// shared-memory state.
 template <bool DBG>
-__device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint32_t second, uint32_t x,
-                                               uint32_t r_cur, bool dbg) {
+__device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
+                                               uint32_t acc_cnt, uint32_t r_cur, bool dbg) {
   Cold &c = g_cold[wid];
+  const uint32_t second = (uint32_t)(sec_bound / kUs - 1u), x = (uint32_t)(acc_sum / acc_cnt);
   if (c.series) {
     const uint32_t n = c.series_n;
     if (lane == 0) {
@@ -497,15 +500,15 @@ struct Sim {
   }
 
   // ------------------------------------------------------------------ a6
-  __device__ __forceinline__ void ingest(uint32_t second, uint32_t x) {
-    r = ingest_sample<DBG>(wid, lane, second, x, r, DBG && dbg != nullptr);
+  __device__ __forceinline__ void ingest() {
+    r = ingest_sample<DBG>(wid, lane, sec_bound, acc_sum, acc_cnt, r, DBG && dbg != nullptr);
   }
 
   // close the open second (if it holds samples) and open the one containing t
   __device__ __forceinline__ void roll_second(uint64_t t) {
     if (t < sec_bound) return;
     if (acc_cnt) {
-      ingest((uint32_t)(sec_bound / kUs - 1u), (uint32_t)(acc_sum / acc_cnt));
+      ingest();
       adm_blocked = 0;  // r may have changed: the queue head may fit now
     }
     acc_sum = 0;
@@ -643,25 +646,33 @@ struct Sim {
     busy = 0;
   }
 
-  __device__ __forceinline__ void prefill_end(WarpHist &h) {
+  // Prefill ends at instants in [T, lim) (first words, R=1 completions, R9).
+  // Called with lim = T + 1 at an event instant, or, inside a running
+  // iteration, with lim = min(iteration end, second boundary, window boundary,
+  // horizon): those ends fall in one second and one window, and their only
+  // effects before the iteration end — statistics of that second, slots made
+  // ready or free — do not depend on their order (admission and joins happen
+  // at iteration boundaries), so one pass handles them all.
+  __device__ __forceinline__ void prefill_end(WarpHist &h, uint64_t lim) {
     const uint64_t Tn = T;
     uint64_t ttft_l = 0, e2e_l = 0;
     uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0, kfree = 0;
     uint32_t mpf = 0xffffffffu;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const bool f = sph[s] == PH_PREFILL && sp[s] == Tn;
+      const bool f = sph[s] == PH_PREFILL && sp[s] < lim;
       nfirst += __popc(__ballot_sync(FULL, f));
       if (f) {
-        const uint64_t tt = Tn - sa[s];
+        const uint64_t tt = sp[s] - sa[s];
+        const uint32_t lb = lat_bin(tt / 1000u);
         ttft_l += tt;
-        atomicAdd(&h.ttft[lat_bin(tt / 1000u)], 1u);
+        atomicAdd(&h.ttft[lb], 1u);
         if (sR[s] == 1u) {  // R9: completes at the prefill end
           kfree += sin[s] + 1u;
           e2e_l += tt;
           nslo += tt > slo_us;
           n1++;
-          atomicAdd(&h.e2e[lat_bin(tt / 1000u)], 1u);
+          atomicAdd(&h.e2e[lb], 1u);
           sph[s] = PH_EMPTY;
         } else {
           sph[s] = PH_READY;
@@ -735,7 +746,9 @@ struct Sim {
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
       uint64_t q_l = 0;
       uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0;
-#pragma unroll
+      // one copy of the per-request body (admissions are rare next to ticks):
+      // slot s is selected by value, not by unrolling
+#pragma unroll 1
       for (int s = 0; s < 2; ++s) {
         const uint32_t rank = s == 0 ? rank0 : rank1;
         const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
@@ -776,11 +789,19 @@ struct Sim {
 #endif
           uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
           if (pf < 1) pf = 1;
-          sa[s] = a;
-          sp[s] = Tn + pf;
-          sR[s] = R;
-          sin[s] = in;
-          sph[s] = PH_PREFILL;
+          if (s == 0) {
+            sa[0] = a;
+            sp[0] = Tn + pf;
+            sR[0] = R;
+            sin[0] = in;
+            sph[0] = PH_PREFILL;
+          } else {
+            sa[1] = a;
+            sp[1] = Tn + pf;
+            sR[1] = R;
+            sin[1] = in;
+            sph[1] = PH_PREFILL;
+          }
           win_l += in;
           q_l += Tn - a;
           mpf = min(mpf, pf);
@@ -978,7 +999,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     if (lane == 0) kidx = atomicAdd(p.counter, 1u);
     kidx = __shfl_sync(FULL, kidx, 0);
     if ((uint64_t)kidx >= p.count) break;
-    const uint64_t sid = p.first + (uint64_t)kidx * p.stride;
+    const uint64_t sid = p.order ? (uint64_t)p.order[kidx] : p.first + (uint64_t)kidx * p.stride;
     const bellman_scenario sc = p.sc[sid];
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
     if ((cc.calibrated != 0) != (p.pass == 2)) continue;
@@ -1113,17 +1134,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     bool finished = false;
     for (;;) {
       uint64_t tn;
+      // a prefill end strictly inside the running iteration only emits first
+      // words / R=1 completions (time-stamped at p): its trip does nothing
+      // else; same-instant ends go after the iteration end (E1, R7).  One call
+      // site per event handler keeps the loop's instruction footprint small.
+      bool mid = false;
       PROF(0);
       if (S.busy) {
-        // prefill ends strictly inside the running iteration only emit first
-        // words / R=1 completions (time-stamped at p); process them in order
-        // before the iteration end (same-instant ends go after E1, R7).
-        while (S.next_pf < S.iter_end && S.next_pf < S.H) {
-          PROF(1);
-          S.advance(S.next_pf);
-          S.prefill_end(h);
-        }
-        tn = S.iter_end;
+        mid = S.next_pf < S.iter_end;
+        tn = mid ? S.next_pf : S.iter_end;
       } else {
         tn = S.next_pf;
         if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t < tn) tn = S.head_t;
@@ -1140,14 +1159,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
         S.dbg_idle(S.T, tn);
       }
       S.advance(tn);
-      if (S.busy) {
+      if (S.busy && !mid) {
         PROF(2);
         if (S.ticks - 1u == S.next_done) PROF(3);
         S.iteration_end(h);
       }
-      if (S.next_pf == tn) {
+      if (S.next_pf == tn) {  // always so on a mid-iteration trip
         PROF(4);
-        S.prefill_end(h);
+        uint64_t lim = tn + 1u;
+        if (mid) {
+          lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
+          if (S.sec_bound < lim) lim = S.sec_bound;
+        }
+        S.prefill_end(h, lim);
+      }
+      if (mid) {
+        PROF(1);
+        continue;
       }
       // the decode loop is idle here: admission point (R7), then the next iteration
       if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
@@ -1181,7 +1209,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
       S.dbg_idle(S.T, end);
     }
-    if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest((uint32_t)(S.sec_bound / kUs - 1u), (uint32_t)(S.acc_sum / S.acc_cnt));
+    if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest();
     // queued at the end: accepted arrivals before `end` not admitted
     uint64_t queued = 0;
     for (;;) {

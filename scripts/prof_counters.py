@@ -27,7 +27,7 @@ def main():
     import workloads as W
     from paper_2510_15330_b200 import Simulator
 
-    cols = W.config_c2().columns()
+    cols = (eval(sys.argv[1], {"W": W}) if len(sys.argv) > 1 else W.config_c2()).columns()
     sim = Simulator(cols)
     sim.run()
     torch.cuda.synchronize()

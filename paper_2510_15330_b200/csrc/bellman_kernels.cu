@@ -34,7 +34,13 @@ __device__ unsigned long long g_prof[16];
 namespace bellman {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr uint64_t INF = ~0ull;
+// The event loop keeps instants as 32-bit offsets from a per-scenario epoch E
+// (absolute time = E + offset, µs).  INF32: no such event; FAR32: an instant
+// beyond the window.  advance() moves E to T once T >= kRebaseAt; idle jumps
+// and leaps stop at kJumpCap, so every derived instant (T + d, d < 2^31; T +
+// prefill < 2^31) stays below FAR32.
+constexpr uint32_t INF32 = 0xffffffffu, FAR32 = 0xfffffffeu;
+constexpr uint32_t kRebaseAt = 1u << 30, kJumpCap = 1u << 30;
 constexpr uint32_t PH_EMPTY = 0, PH_PREFILL = 1, PH_READY = 2, PH_DEC = 3, PH_OFF = 4;
 constexpr uint64_t kLn2Q32 = 2977044472ull;  // round(ln 2 * 2^32)
 
@@ -113,6 +119,7 @@ struct Cold {
   uint64_t gen_tau;
   uint64_t ringA;
   uint64_t w0, w1;
+  uint64_t H;  // horizon (absolute µs)
   uint32_t *series;
   bellman_ctrl_row *dbg_ctrl;
   uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
@@ -217,9 +224,10 @@ __device__ __noinline__ uint64_t kv_admit(const Params &p, uint32_t wid, uint32_
 // per-request draws (tag-1 block).  Out of line: it runs once per ~32 arrivals.
 // Returns n (0 only when the generator is exhausted).
 template <bool DBG>
-__device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane, uint64_t H,
+__device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane,
                                                bellman_second_row *dbg, uint32_t dbg_cap) {
   Cold &c = g_cold[wid];
+  const uint64_t H = DBG ? c.H : 0u;  // debug rows count arrivals before the horizon
   __syncwarp();  // every lane's reads of the previous buffer precede the new writes
   uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
   uint32_t gen_acc = c.gen_acc;
@@ -447,15 +455,16 @@ struct Sim {
 #endif
   uint32_t lane;
   uint32_t wid;  // warp index in the CTA: selects this warp's Cold block
-  // ---- scenario (a1)
-  uint64_t H;
+  // ---- clock (a4): absolute time = E + 32-bit offset (INF32 / FAR32 above)
+  uint64_t E;
+  uint32_t Hr;  // horizon offset (FAR32 when beyond the window)
   // profile
   uint32_t kv, maxb;
   // controller
   uint32_t signal;
   uint32_t r;
   // per-second accumulator of the selected signal (a6)
-  uint64_t sec_bound;  // (open second + 1) * 1e6, INF when nothing consumes the signal
+  uint32_t sec_bound;  // offset of (open second + 1) * 1e6, INF32 when nothing consumes the signal
   uint64_t acc_sum;
   uint32_t acc_cnt;
   // recording (a10 source)
@@ -466,46 +475,53 @@ struct Sim {
   // ---- counters (a8), updated at events
   uint32_t last_j;
   // ---- serving state (a4, a5, a7)
-  uint64_t T;
+  uint32_t T;
   uint32_t busy;
-  uint64_t iter_end;
+  uint32_t iter_end;
   uint32_t iter_d;
   uint64_t iter_align;
   uint32_t ticks;      // iterations started; the running one has index ticks-1
   uint32_t next_done;  // min completion iteration over decoding slots
-  uint64_t next_pf;    // min prefill end over prefilling slots
+  uint32_t next_pf;    // min prefill end over prefilling slots
   uint32_t n_ready, B, in_sys;
   uint32_t cbase;             // t0 + slope * max(0, B - knee)
   uint32_t kq, kr;            // kv * K = kq * 1000 + kr, K = context words of the batch
   uint32_t kstep_q, kstep_r;  // kv * B = kstep_q * 1000 + kstep_r (growth per iteration)
   uint32_t win_now;           // T in [w0, w1)
-  uint64_t win_next;          // next window boundary after T (INF if none)
-  uint64_t stop_static;       // min(H, win_next)
-  // slots (lane-parallel)
-  uint64_t sa[2], sp[2];
+  uint32_t win_next;          // next window boundary after T (INF32 if none)
+  uint32_t stop_static;       // min(Hr, win_next)
+  // slots (lane-parallel): arrival (absolute), prefill end (offset)
+  uint64_t sa[2];
+  uint32_t sp[2];
   uint32_t sR[2], sin[2], sdn[2], sph[2];
   // ---- generator / queue head (a2)
   uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
   uint32_t kv_res;        // NEXT-4: sum of (input + R) over requests in the system
   uint32_t adm_blocked;   // NEXT-4: the arrived queue head does not fit the KV capacity
-  uint64_t head_t;     // arrival time of the queue head, INF when no arrival remains
+  uint32_t head_t;     // arrival offset of the queue head (0 if before E), INF32 when none remains
   // ---- counters (a8)
   uint64_t words_out, win_words_out;
+
+  __device__ __forceinline__ uint64_t ab(uint32_t t) const { return E + t; }
+  // offset of an absolute instant x: 0 if x <= E (the past), FAR32 if beyond the window
+  __device__ __forceinline__ uint32_t rel(uint64_t x) const {
+    return x <= E ? 0u : (x - E >= FAR32 ? FAR32 : (uint32_t)(x - E));
+  }
 
   // ------------------------------------------------------------------ a2
   __device__ __forceinline__ void refill(const Params &p) {
     buf_h = 0;
-    buf_n = refill_buffer<DBG>(p, wid, lane, H, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u);
-    head_t = buf_n ? cold().buf_a[0] : INF;
+    buf_n = refill_buffer<DBG>(p, wid, lane, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u);
+    head_t = buf_n ? rel(cold().buf_a[0]) : INF32;
   }
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest() {
-    r = ingest_sample<DBG>(wid, lane, sec_bound, acc_sum, acc_cnt, r, DBG && dbg != nullptr);
+    r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr);
   }
 
   // close the open second (if it holds samples) and open the one containing t
-  __device__ __forceinline__ void roll_second(uint64_t t) {
+  __device__ __forceinline__ void roll_second(uint32_t t) {
     if (t < sec_bound) return;
     if (acc_cnt) {
       ingest();
@@ -513,15 +529,16 @@ struct Sim {
     }
     acc_sum = 0;
     acc_cnt = 0;
-    sec_bound = (t / kUs + 1u) * kUs;
+    sec_bound = rel((ab(t) / kUs + 1u) * kUs);
   }
 
-  __device__ __forceinline__ bellman_second_row *row(uint64_t t) const {
-    const uint64_t sidx = t / kUs;
+  // debug row of the second containing absolute instant ta
+  __device__ __forceinline__ bellman_second_row *row(uint64_t ta) const {
+    const uint64_t sidx = ta / kUs;
     return dbg + (sidx < cold().dbg_cap ? sidx : cold().dbg_cap - 1u);
   }
 
-  // idle interval [a, b) split over the seconds it overlaps (debug rows only)
+  // idle interval [a, b) (absolute) split over the seconds it overlaps (debug rows only)
   __device__ __forceinline__ void dbg_idle(uint64_t a, uint64_t b) {
     if (!dbg || lane != 0) return;
     for (uint64_t sidx = a / kUs; sidx * kUs < b; ++sidx) {
@@ -531,16 +548,35 @@ struct Sim {
   }
 
   __device__ __forceinline__ void update_window() {
-    win_now = T >= cold().w0 && T < cold().w1;
-    win_next = T < cold().w0 ? cold().w0 : (T < cold().w1 ? cold().w1 : INF);
-    stop_static = H < win_next ? H : win_next;
+    const uint64_t Ta = ab(T), w0 = cold().w0, w1 = cold().w1;
+    win_now = Ta >= w0 && Ta < w1;
+    win_next = Ta < w0 ? rel(w0) : (Ta < w1 ? rel(w1) : INF32);
+    stop_static = Hr < win_next ? Hr : win_next;
+  }
+
+  // move the epoch to T: offsets of pending instants shrink by T (slot prefill
+  // ends modulo 2^32: a ready slot's end lies in the past and is only used in
+  // differences); instants kept absolute elsewhere are re-derived
+  __device__ __forceinline__ void rebase() {
+    const uint32_t D = T;
+    E += D;
+    T = 0;
+    iter_end -= D;  // meaningful only while busy
+    if (next_pf != INF32) next_pf -= D;
+    if (sec_bound != INF32) sec_bound -= D;
+    sp[0] -= D;
+    sp[1] -= D;
+    head_t = buf_h < buf_n ? rel(cold().buf_a[buf_h]) : INF32;
+    Hr = rel(cold().H);
+    update_window();
   }
 
   // move the clock to an event instant t >= T
-  __device__ __forceinline__ void advance(uint64_t t) {
+  __device__ __forceinline__ void advance(uint32_t t) {
     T = t;
     roll_second(t);
     if (t >= win_next) update_window();
+    if (__builtin_expect(t >= kRebaseAt, 0)) rebase();
   }
 
   // B changed: cost base and per-iteration KV growth
@@ -583,7 +619,7 @@ struct Sim {
   }
 
   __device__ __forceinline__ void iteration_end(WarpHist &h) {
-    const uint64_t Tn = T;
+    const uint32_t Tn = T;
     words_out += B;
     if (win_now) win_words_out += B;
     if (signal == BELLMAN_SIG_TBT) {
@@ -591,7 +627,7 @@ struct Sim {
       acc_cnt += B;
     }
     if (DBG && dbg && lane == 0) {
-      bellman_second_row *w = row(Tn);
+      bellman_second_row *w = row(ab(Tn));
       atomicAdd(&w->tbt_count, B);
       atomicAdd(&w->words_out, B);
       atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * iter_d + iter_align);
@@ -608,12 +644,13 @@ struct Sim {
     if (it == next_done) {
       uint64_t e2e_l = 0;
       uint32_t kdrop = 0, nslo = 0, ndone = 0, dmin = 0xffffffffu;
+      const uint64_t Ta = ab(Tn);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const bool cpl = sph[s] == PH_DEC && sdn[s] == it;
         ndone += __popc(__ballot_sync(FULL, cpl));
         if (cpl) {
-          const uint64_t e = Tn - sa[s];
+          const uint64_t e = Ta - sa[s];
           e2e_l += e;
           nslo += e > slo_us;
           kdrop += sin[s] + sR[s];
@@ -634,8 +671,8 @@ struct Sim {
       cadd(CT_SLO_VIOL, ns);
       if (win_now) cadd(CT_WIN_SERVED, ndone);
       if (DBG && dbg && lane == 0) {
-        atomicAdd(&row(Tn)->completions, ndone);
-        atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
+        atomicAdd(&row(Ta)->completions, ndone);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_e2e_us, (unsigned long long)se);
       }
       if (DBG) __syncwarp();
       in_sys -= ndone;
@@ -653,8 +690,8 @@ struct Sim {
   // effects before the iteration end — statistics of that second, slots made
   // ready or free — do not depend on their order (admission and joins happen
   // at iteration boundaries), so one pass handles them all.
-  __device__ __forceinline__ void prefill_end(WarpHist &h, uint64_t lim) {
-    const uint64_t Tn = T;
+  __device__ __forceinline__ void prefill_end(WarpHist &h, uint32_t lim) {
+    const uint32_t Tn = T;
     uint64_t ttft_l = 0, e2e_l = 0;
     uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0, kfree = 0;
     uint32_t mpf = 0xffffffffu;
@@ -663,7 +700,7 @@ struct Sim {
       const bool f = sph[s] == PH_PREFILL && sp[s] < lim;
       nfirst += __popc(__ballot_sync(FULL, f));
       if (f) {
-        const uint64_t tt = sp[s] - sa[s];
+        const uint64_t tt = ab(sp[s]) - sa[s];
         const uint32_t lb = lat_bin(tt / 1000u);
         ttft_l += tt;
         atomicAdd(&h.ttft[lb], 1u);
@@ -679,10 +716,10 @@ struct Sim {
           nrdy++;
         }
       }
-      if (sph[s] == PH_PREFILL) mpf = min(mpf, (uint32_t)(sp[s] - Tn));
+      if (sph[s] == PH_PREFILL) mpf = min(mpf, sp[s] - Tn);
     }
     const uint32_t m = __reduce_min_sync(FULL, mpf);
-    next_pf = (m == 0xffffffffu) ? INF : Tn + m;
+    next_pf = (m == INF32) ? INF32 : Tn + m;
     const uint64_t st = warp_sum_split(ttft_l);
     cadd(CT_SUM_TTFT, st);
     words_out += nfirst;
@@ -691,9 +728,9 @@ struct Sim {
       acc_cnt += nfirst;
     }
     if (DBG && dbg && lane == 0) {
-      atomicAdd(&row(Tn)->first_tokens, nfirst);
-      atomicAdd(&row(Tn)->words_out, nfirst);
-      atomicAdd((unsigned long long *)&row(Tn)->sum_ttft_us, (unsigned long long)st);
+      atomicAdd(&row(ab(Tn))->first_tokens, nfirst);
+      atomicAdd(&row(ab(Tn))->words_out, nfirst);
+      atomicAdd((unsigned long long *)&row(ab(Tn))->sum_ttft_us, (unsigned long long)st);
     }
     if (DBG) __syncwarp();
     if (win_now) win_words_out += nfirst;
@@ -709,8 +746,8 @@ struct Sim {
       cadd(CT_SLO_VIOL, ns);
       if (win_now) cadd(CT_WIN_SERVED, nc);
       if (DBG && dbg && lane == 0) {
-        atomicAdd(&row(Tn)->completions, nc);
-        atomicAdd((unsigned long long *)&row(Tn)->sum_e2e_us, (unsigned long long)se);
+        atomicAdd(&row(ab(Tn))->completions, nc);
+        atomicAdd((unsigned long long *)&row(ab(Tn))->sum_e2e_us, (unsigned long long)se);
       }
       if (DBG) __syncwarp();
       in_sys -= nc;
@@ -721,10 +758,11 @@ struct Sim {
   // ------------------------------------------------------------------ a7 (+a3)
   // Precondition: in_sys < maxb and head_t <= T.
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
-    const uint64_t Tn = T;
+    const uint32_t Tn = T;
+    const uint64_t Ta = ab(Tn);
     adm_blocked = 0;
     for (;;) {
-      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Tn);
+      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Ta);
       const uint32_t na = __popc(arrived);
       const uint32_t room = maxb - in_sys;
       uint32_t k = na < room ? na : room;
@@ -803,11 +841,11 @@ struct Sim {
             sph[1] = PH_PREFILL;
           }
           win_l += in;
-          q_l += Tn - a;
+          q_l += Ta - a;
           mpf = min(mpf, pf);
         }
       }
-      const uint32_t mnew = __reduce_min_sync(FULL, mpf);
+      const uint32_t mnew = __reduce_min_sync(FULL, mpf);  // k >= 1 new prefills
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
       const uint32_t win = __reduce_add_sync(FULL, win_l);
       cadd(CT_WORDS_IN, win);
@@ -815,9 +853,9 @@ struct Sim {
       const uint64_t sq = warp_sum_split(q_l);
       cadd(CT_SUM_QUEUE, sq);
       if (DBG && dbg && lane == 0) {
-        atomicAdd(&row(Tn)->admitted, k);
-        atomicAdd(&row(Tn)->words_in, win);
-        atomicAdd((unsigned long long *)&row(Tn)->sum_queue_us, (unsigned long long)sq);
+        atomicAdd(&row(Ta)->admitted, k);
+        atomicAdd(&row(Ta)->words_in, win);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_queue_us, (unsigned long long)sq);
       }
       if (DBG) __syncwarp();
       if (r > 0) {
@@ -834,11 +872,11 @@ struct Sim {
       cadd(CT_ADMITTED, k);
       buf_h += k;
       if (buf_h < buf_n) {
-        head_t = cold().buf_a[buf_h];
+        head_t = rel(cold().buf_a[buf_h]);
       } else if (!cold().gen_done) {
         refill(p);
       } else {
-        head_t = INF;
+        head_t = INF32;
       }
       if (in_sys >= maxb || head_t > Tn) break;
     }
@@ -856,18 +894,18 @@ struct Sim {
   // is 32-bit (bounds validated on the host: d < 2^31); a leap may always be
   // cut short without changing results, so `room` is capped at 2^32 - 1.
   __device__ __forceinline__ void leap() {
-    uint64_t stop = next_pf < stop_static ? next_pf : stop_static;
+    uint32_t stop = next_pf < stop_static ? next_pf : stop_static;
     if (in_sys < maxb && !adm_blocked && head_t < stop) stop = head_t;
     // a KV-blocked head may fit after an ingest changes r: stop at the second boundary
     if (adm_blocked && sec_bound < stop) stop = sec_bound;
+    if (stop > kJumpCap) stop = kJumpCap;  // keeps the next iteration end inside the window
     const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
     if (nmax == 0 || stop <= T + 1u) return;
     const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
     uint32_t q = kq, rr = kr, done = 0;
     for (;;) {
-      const uint64_t lim = stop < sec_bound ? stop : sec_bound;
-      const uint64_t room64 = lim - 1u - T;
-      const uint32_t room = room64 > 0xffffffffull ? 0xffffffffu : (uint32_t)room64;
+      const uint32_t lim = stop < sec_bound ? stop : sec_bound;
+      const uint32_t room = lim - 1u - T;
       const uint32_t left = nmax - done;
       uint32_t n = 0, used = 0;
       if (kv == 0) {
@@ -897,7 +935,7 @@ struct Sim {
           acc_cnt += (uint32_t)words;
         }
         if (DBG && dbg && lane == 0) {  // all ends of this chunk lie in the open second
-          bellman_second_row *w = row(sec_bound - kUs);
+          bellman_second_row *w = row(ab(sec_bound) - kUs);
           atomicAdd(&w->tbt_count, (uint32_t)words);
           atomicAdd(&w->words_out, (uint32_t)words);
           atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * used);
@@ -906,7 +944,7 @@ struct Sim {
         done += n;
       }
       if (done == nmax) break;
-      const uint64_t tnext = T + (cb + q);  // end of the next iteration
+      const uint32_t tnext = T + (cb + q);  // end of the next iteration
       if (tnext >= stop || tnext < sec_bound) break;
       roll_second(tnext);  // the next end opens a new second: ingest the closed one here
     }
@@ -916,7 +954,7 @@ struct Sim {
 
   // ------------------------------------------------------------------ a4
   __device__ __forceinline__ void start_iteration() {
-    const uint64_t Tn = T;
+    const uint32_t Tn = T;
     uint64_t align = 0;
     if (n_ready) {
       const uint32_t it0 = ticks;  // index of the new iteration
@@ -927,7 +965,7 @@ struct Sim {
         if (sph[s] == PH_READY) {
           sph[s] = PH_DEC;
           sdn[s] = it0 + sR[s] - 2u;  // words 2..R at the ends of iterations it0..it0+R-2
-          al += Tn - sp[s];
+          al += Tn - sp[s];  // 32-bit offsets: the difference is exact modulo 2^32
           kadd += sin[s] + 1u;
           jn = min(jn, sdn[s]);
         }
@@ -990,7 +1028,10 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 }
 
 template <bool DBG>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(const __grid_constant__ Params p) {
+#ifndef BELLMAN_MIN_BLOCKS
+#define BELLMAN_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellman_tick_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
   WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
@@ -1012,7 +1053,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.lane = lane;
     const bellman_profile pr = p.profs[sc.profile];
     const DevTrace tr = p.traces[sc.trace];
-    S.H = (uint64_t)sc.horizon_us;
+    S.E = 0;
     S.t0 = pr.t0_us;
     S.knee = pr.knee;
     S.slope = pr.slope_us;
@@ -1042,6 +1083,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       z.wid_hi = (uint32_t)(sc.wid >> 32);
       z.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
       z.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+      z.H = (uint64_t)sc.horizon_us;
       z.law = law;
       z.window = cc.window;
       z.rmin = cc.r_min_bp;
@@ -1087,15 +1129,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
     S.acc_cnt = 0;
     // the per-second signal feeds only the controller (MAP/STEP) and the recorders
     S.sec_bound = (law == BELLMAN_LAW_MAP || law == BELLMAN_LAW_STEP || rslot != BELLMAN_NONE || (DBG && S.dbg))
-                      ? kUs : INF;
+                      ? (uint32_t)kUs : INF32;
+    S.Hr = S.rel((uint64_t)sc.horizon_us);
     S.T = 0;
     S.busy = 0;
-    S.iter_end = INF;
+    S.iter_end = INF32;
     S.iter_d = 0;
     S.iter_align = 0;
     S.ticks = 0;
     S.next_done = 0xffffffffu;
-    S.next_pf = INF;
+    S.next_pf = INF32;
     S.n_ready = S.B = S.in_sys = 0;
     S.kq = S.kr = 0;
     S.batch_changed();
@@ -1133,7 +1176,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
 #endif
     bool finished = false;
     for (;;) {
-      uint64_t tn;
+      uint32_t tn;
       // a prefill end strictly inside the running iteration only emits first
       // words / R=1 completions (time-stamped at p): its trip does nothing
       // else; same-instant ends go after the iteration end (E1, R7).  One call
@@ -1146,19 +1189,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       } else {
         tn = S.next_pf;
         if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t < tn) tn = S.head_t;
-        if (tn == INF) {
+        if (tn == INF32) {
           finished = true;
           break;
         }
+        // a far next event: jump (idle) to the cap first; advance() rebases there
+        if (tn > kJumpCap) tn = kJumpCap;
       }
-      if (tn >= S.H) break;
+      if (tn >= S.Hr) break;
       if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
         S.cadd(CT_IDLE, tn - S.T);
-        const uint64_t lo = S.T > S.cold().w0 ? S.T : S.cold().w0, hi = tn < S.cold().w1 ? tn : S.cold().w1;
+        const uint64_t a = S.ab(S.T), b = S.ab(tn);
+        const uint64_t lo = a > S.cold().w0 ? a : S.cold().w0, hi = b < S.cold().w1 ? b : S.cold().w1;
         if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
-        S.dbg_idle(S.T, tn);
+        S.dbg_idle(a, b);
       }
       S.advance(tn);
+      tn = S.T;  // advance() may have moved the epoch
       if (S.busy && !mid) {
         PROF(2);
         if (S.ticks - 1u == S.next_done) PROF(3);
@@ -1166,7 +1213,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       }
       if (S.next_pf == tn) {  // always so on a mid-iteration trip
         PROF(4);
-        uint64_t lim = tn + 1u;
+        uint32_t lim = tn + 1u;
         if (mid) {
           lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
           if (S.sec_bound < lim) lim = S.sec_bound;
@@ -1202,14 +1249,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) bellman_tick_kernel(co
       for (int i = 0; i < 16; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
 #endif
     // ---- termination (R20)
-    const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? S.T : S.H;
+    const uint64_t Tend = S.ab(S.T);
+    const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? Tend : (uint64_t)sc.horizon_us;
     if (S.in_sys == 0) {
-      S.cadd(CT_IDLE, end - S.T);
-      const uint64_t lo = S.T > S.cold().w0 ? S.T : S.cold().w0, hi = end < S.cold().w1 ? end : S.cold().w1;
+      S.cadd(CT_IDLE, end - Tend);
+      const uint64_t lo = Tend > S.cold().w0 ? Tend : S.cold().w0, hi = end < S.cold().w1 ? end : S.cold().w1;
       if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
-      S.dbg_idle(S.T, end);
+      S.dbg_idle(Tend, end);
     }
-    if (S.sec_bound != INF && S.sec_bound <= end && S.acc_cnt) S.ingest();
+    if (S.sec_bound != INF32 && S.ab(S.sec_bound) <= end && S.acc_cnt) S.ingest();
     // queued at the end: accepted arrivals before `end` not admitted
     uint64_t queued = 0;
     for (;;) {

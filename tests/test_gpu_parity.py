@@ -270,3 +270,36 @@ def test_next4_trace_replay():
     w.class_cum = W.MIXED_CLASSES
     bad, _ = check_all(w.columns())
     _assert_ok(bad)
+
+
+def _long_workload():
+    """The event loop keeps instants as 32-bit offsets from an epoch that moves
+    every 2^30 µs: idle gaps longer than 2^32 µs, horizons far
+    beyond the window, overload queues whose head arrived before the current
+    epoch, seconds / windows / debug rows across rebase points."""
+    US = W.US
+    gap_trace = [(0, 5000), (60 * US, 5000), (60 * US, 0), (10_860 * US, 0), (10_860 * US, 3000),
+                 (10_980 * US, 3000)]  # 3 h silence (> 2^32 µs) between two bursts
+    sparse = W.const_trace(0.02, 18_000)  # ~360 arrivals over 5 h: idle rebases
+    overload = W.const_trace(8.0, 1500)  # queue far deeper than one epoch can drain
+    rep = [(0, 500, 9000, 0), (3 * US, 800, 4000, 1), (3 * US + (1 << 33), 600, 9000, 2),
+           (4 * US + (1 << 33), 700, 12000, 0)]  # 2^33 µs between arrivals
+    traces = [gap_trace, sparse, overload, {"replay": rep}]
+    profs = [W.PROFILES["P24"], W.PROFILES["L8B"], dict(W.PROFILES["L8B"], kv_cap_words=300_000)]
+    ctrls = [W.OFF, W.map_ctrl(30_000, 60_000), W.map_ctrl(5_000_000, 900_000_000, signal=W.SIG_E2E, window=3),
+             W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1500)]
+    sc = []
+    for t in range(4):
+        for pi in range(3):
+            for ci in range(4):
+                for H, mode in ((11_000 * US, W.MODE_CUTOFF), (20_000 * US, W.MODE_DRAIN), (1 << 40, t % 2)):
+                    rec = 2 if (H == 11_000 * US and ci == 1 and pi == 0) else 0
+                    sc.append(W.Scenario(t * 7 + ci, wid=t, trace=t, profile=pi, ctrl=ci, segment=0, mode=mode,
+                                         horizon_us=H, w0_us=1_000 * US, w1_us=9_000 * US, record=rec))
+    return W.custom(traces, profs, ctrls, sc)
+
+
+def test_long_horizons_far_gaps_and_epoch_rebases():
+    bad, st = check_all(_long_workload().columns())
+    _assert_ok(bad)
+    assert int(st["end_us"].max()) > (1 << 32)

@@ -9,7 +9,12 @@ namespace bellman {
 
 constexpr uint32_t kSeedHi = 0xB311A000u;  // Philox key word 1 (reading R32)
 constexpr uint64_t kUs = 1000000ull;
-constexpr uint32_t kWarpsPerBlock = 4;
+// One warp (one scenario) per CTA: every per-warp shared-memory address is then a
+// compile-time constant (shared addresses are CTA-relative), 16 CTAs per SM.
+#ifndef BELLMAN_WPB
+#define BELLMAN_WPB 1
+#endif
+constexpr uint32_t kWarpsPerBlock = BELLMAN_WPB;
 constexpr uint32_t kSegWords = BELLMAN_SEG_HIST_WORDS;
 
 // One non-empty thinning segment of a trace, precomputed on the host (a2):

@@ -27,8 +27,16 @@
 // Development-only event counters (separate build, never the product .so).
 __device__ unsigned long long g_prof[16];
 #define PROF(i) (prof_[i]++)
+// cycles spent in a handler (clock64 deltas; a profiling build only)
+#define PROFC(i, stmt)                               \
+  do {                                               \
+    const long long c0_ = clock64();                 \
+    stmt;                                            \
+    prof_[i] += (uint32_t)(clock64() - c0_);         \
+  } while (0)
 #else
 #define PROF(i) ((void)0)
+#define PROFC(i, stmt) stmt
 #endif
 
 namespace bellman {
@@ -110,6 +118,8 @@ __device__ __forceinline__ uint64_t warp_sum_split(uint64_t x) {
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+// this warp's index in its CTA (a constant 0 with one warp per CTA)
+__device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1 ? 0u : threadIdx.x >> 5; }
 
 // Cold per-scenario state: touched at events (admissions, completions,
 // ingests, refills), not per iteration.  Lives in shared memory, one per warp,
@@ -175,6 +185,36 @@ __device__ __noinline__ int32_t sim_decay(uint32_t q_active, uint32_t q_floor, u
   return (int32_t)q_active - (int32_t)q;
 }
 
+// a4/a5 leap, long runs: iterations of the batch with K growing by B each,
+// 32 per step.  Lane j takes iteration n + j, whose gap is c + floor(kv (K +
+// j B) / 1000) = cb + q + floor((rr + j ks) / 1000) with kv K = q 1000 + rr,
+// ks = kv B <= 2^16; a saturating prefix sum (cap 2^30 > room) counts those
+// that fit in `room`.  Returns (iterations, time used, q, rr) after them.
+__device__ __noinline__ uint4 leap_wide(uint32_t lane, uint32_t cb, uint32_t q, uint32_t rr, uint32_t ks,
+                                        uint32_t room, uint32_t left) {
+  constexpr uint32_t kCap = 1u << 30;
+  uint32_t n = 0, used = 0;
+  while (n < left) {
+    const uint32_t x = rr + lane * ks;
+    uint32_t incl = cb + q + x / 1000u;
+    incl = incl < kCap ? incl : kCap;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (uint32_t)o) incl = min(incl + y, kCap);
+    }
+    const uint32_t c = __popc(__ballot_sync(FULL, incl <= room - used && lane < left - n));
+    if (c == 0) break;
+    used += __shfl_sync(FULL, incl, c - 1u);
+    const uint32_t xc = rr + c * ks;
+    q += xc / 1000u;
+    rr = xc % 1000u;
+    n += c;
+    if (c < 32u) break;
+  }
+  return make_uint4(n, used, q, rr);
+}
+
 // Write-only counters (a8) are lane-distributed: counter i lives in lane i's
 // register `ctr` and is bumped with a predicated add of a warp-uniform value
 // (no branch, no memory), then read once by shuffle in the epilogue.
@@ -183,6 +223,7 @@ enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL 
 // One Cold block per warp of the CTA, in static shared memory so that every
 // access is a 32-bit LDS/STS off a known base (no generic pointer).
 __shared__ Cold g_cold[kWarpsPerBlock];
+__shared__ WarpHist g_hist[kWarpsPerBlock];
 
 // NEXT-4 KV-capacity admission: of the first k arrived candidates (entries
 // buf_h.. of the shared buffer, FIFO), the leading run whose whole contexts
@@ -192,7 +233,7 @@ __shared__ Cold g_cold[kWarpsPerBlock];
 __device__ __noinline__ uint64_t kv_admit(const Params &p, uint32_t wid, uint32_t lane, uint32_t buf_h, uint32_t k,
                                           uint32_t r, uint32_t bmask, uint32_t minw, uint32_t kvcap, uint32_t res,
                                           uint32_t in_sys) {
-  const Cold &c = g_cold[wid];
+  const Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
   uint32_t need = 0;
   if (lane < k) {
     const uint32_t e = buf_h + lane;
@@ -226,7 +267,7 @@ __device__ __noinline__ uint64_t kv_admit(const Params &p, uint32_t wid, uint32_
 template <bool DBG>
 __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane,
                                                bellman_second_row *dbg, uint32_t dbg_cap) {
-  Cold &c = g_cold[wid];
+  Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
   const uint64_t H = DBG ? c.H : 0u;  // debug rows count arrivals before the horizon
   __syncwarp();  // every lane's reads of the previous buffer precede the new writes
   uint32_t gen_done = c.gen_done, gen_seg = c.gen_seg, gen_fresh = c.gen_fresh, gen_j = c.gen_j;
@@ -355,7 +396,7 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
 template <bool DBG>
 __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
                                                uint32_t acc_cnt, uint32_t r_cur, bool dbg) {
-  Cold &c = g_cold[wid];
+  Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
   const uint32_t second = (uint32_t)(sec_bound / kUs - 1u), x = (uint32_t)(acc_sum / acc_cnt);
   if (c.series) {
     const uint32_t n = c.series_n;
@@ -443,7 +484,7 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
 template <bool DBG>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
-  __device__ __forceinline__ Cold &cold() const { return g_cold[wid]; }
+  __device__ __forceinline__ Cold &cold() const { return g_cold[kWarpsPerBlock == 1 ? 0u : wid]; }
 #ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
   __device__ __forceinline__ void cadd(uint32_t i, uint64_t v) { ctr += (lane == i) ? v : 0ull; }
@@ -913,15 +954,24 @@ struct Sim {
         n = nn < left ? nn : left;
         used = n * cb;
       } else {
-        while (n < left) {
-          const uint32_t d = cb + q;
-          if (d > room - used) break;
-          used += d;
-          rr += rs;
-          const uint32_t carry = rr >= 1000u;
-          rr -= carry ? 1000u : 0u;
-          q += qs + carry;
-          n++;
+        if (left <= 8u || (room >> 3) < cb + q) {
+          // short runs (dense events): one iteration at a time
+          while (n < left) {
+            const uint32_t d = cb + q;
+            if (d > room - used) break;
+            used += d;
+            rr += rs;
+            const uint32_t carry = rr >= 1000u;
+            rr -= carry ? 1000u : 0u;
+            q += qs + carry;
+            n++;
+          }
+        } else {  // long runs: 32 iterations per step, out of line
+          const uint4 v = leap_wide(lane, cb, q, rr, qs * 1000u + rs, room, left);
+          n = v.x;
+          used = v.y;
+          q = v.z;
+          rr = v.w;
         }
       }
       if (n) {
@@ -1029,12 +1079,11 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 
 template <bool DBG>
 #ifndef BELLMAN_MIN_BLOCKS
-#define BELLMAN_MIN_BLOCKS 4
+#define BELLMAN_MIN_BLOCKS (16 / BELLMAN_WPB)
 #endif
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellman_tick_kernel(const __grid_constant__ Params p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = lane_id();
-  WarpHist &h = reinterpret_cast<WarpHist *>(smem_raw)[threadIdx.x >> 5];
+  WarpHist &h = g_hist[warp_in_block()];
   for (;;) {
     uint32_t kidx = 0;
     if (lane == 0) kidx = atomicAdd(p.counter, 1u);
@@ -1049,7 +1098,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 
     // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
     // lane 0 only and read after the __syncwarp below.
-    Sim<DBG> S(threadIdx.x >> 5);
+    Sim<DBG> S(warp_in_block());
     S.lane = lane;
     const bellman_profile pr = p.profs[sc.profile];
     const DevTrace tr = p.traces[sc.trace];
@@ -1173,6 +1222,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     // ---- the event/tick loop (a4-a7)
 #ifdef BELLMAN_PROFILE_COUNTERS
     uint32_t prof_[16] = {0};
+    const long long loop0_ = clock64();
 #endif
     bool finished = false;
     for (;;) {
@@ -1204,12 +1254,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
         if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
         S.dbg_idle(a, b);
       }
-      S.advance(tn);
+      PROFC(9, S.advance(tn));
       tn = S.T;  // advance() may have moved the epoch
       if (S.busy && !mid) {
         PROF(2);
         if (S.ticks - 1u == S.next_done) PROF(3);
-        S.iteration_end(h);
+        PROFC(10, S.iteration_end(h));
       }
       if (S.next_pf == tn) {  // always so on a mid-iteration trip
         PROF(4);
@@ -1218,7 +1268,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
           lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
           if (S.sec_bound < lim) lim = S.sec_bound;
         }
-        S.prefill_end(h, lim);
+        PROFC(11, S.prefill_end(h, lim));
       }
       if (mid) {
         PROF(1);
@@ -1227,24 +1277,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
       // the decode loop is idle here: admission point (R7), then the next iteration
       if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
         PROF(5);
-        S.admit(p, h);
+        PROFC(12, S.admit(p, h));
       }
       if (S.n_ready + S.B > 0) {
         if (S.n_ready == 0) {
           PROF(6);
           const uint32_t t0_ = S.ticks;
-          S.leap();
+          PROFC(13, S.leap());
 #ifdef BELLMAN_PROFILE_COUNTERS
           prof_[7] += S.ticks - t0_;
 #endif
         } else {
           PROF(8);
         }
-        S.start_iteration();
+        PROFC(14, S.start_iteration());
       }
     }
 
 #ifdef BELLMAN_PROFILE_COUNTERS
+    prof_[15] = (uint32_t)(clock64() - loop0_);
     if (lane == 0)
       for (int i = 0; i < 16; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
 #endif
@@ -1419,21 +1470,17 @@ extern "C" int bellman_debug_prof(unsigned long long *out) {
 int bellman_tick_grid(int device) {
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
-  cudaFuncSetAttribute(bellman::bellman_tick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(bellman::bellman_tick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false>,
-                                                    bellman::kWarpsPerBlock * 32, smem) != cudaSuccess)
+                                                    bellman::kWarpsPerBlock * 32, 0) != cudaSuccess)
     return -1;
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
 cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream) {
-  const size_t smem = bellman::kWarpsPerBlock * sizeof(bellman::WarpHist);
   if (dbg)
-    bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
+    bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
   else
-    bellman::bellman_tick_kernel<false><<<grid, bellman::kWarpsPerBlock * 32, smem, stream>>>(p);
+    bellman::bellman_tick_kernel<false><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -13,8 +13,9 @@ import torch  # noqa: E402
 
 from paper_2510_15330_b200 import _abi, build as B  # noqa: E402
 
-NAMES = ["trips", "deferred_prefill", "iter_end", "iter_end_with_completion", "prefill_end_event", "admit",
-         "leap_calls", "leaped_ticks", "join_starts"]
+NAMES = ["trips", "mid_iteration_trips", "iter_end", "iter_end_with_completion", "prefill_end_event", "admit",
+         "leap_calls", "leaped_ticks", "join_starts", "cyc_advance", "cyc_iteration_end", "cyc_prefill_end",
+         "cyc_admit", "cyc_leap", "cyc_start_iteration", "cyc_event_loop"]
 
 
 def main():

@@ -1234,6 +1234,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
       bool mid = false;
       PROF(0);
       if (S.busy) {
+        // prefill ends due inside the running iteration, in the open second and
+        // window: handled here, at the start of the iteration-end trip (their
+        // effects are order-free until the iteration end); any left lie past a
+        // second / window boundary and get their own trip
+        uint32_t lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
+        if (S.sec_bound < lim) lim = S.sec_bound;
+        if (S.next_pf < lim) {
+          PROF(10);
+          S.prefill_end(h, lim);
+        }
         mid = S.next_pf < S.iter_end;
         tn = mid ? S.next_pf : S.iter_end;
       } else {

@@ -25,7 +25,7 @@
 
 #ifdef BELLMAN_PROFILE_COUNTERS
 // Development-only event counters (separate build, never the product .so).
-__device__ unsigned long long g_prof[16];
+__device__ unsigned long long g_prof[20];
 #define PROF(i) (prof_[i]++)
 // cycles spent in a handler (clock64 deltas; a profiling build only)
 #define PROFC(i, stmt)                               \
@@ -659,8 +659,8 @@ struct Sim {
     }
   }
 
-  __device__ __forceinline__ void iteration_end(WarpHist &h) {
-    const uint32_t Tn = T;
+  // the words of an iteration end: B words, TBT gaps, K += B (a5)
+  __device__ __forceinline__ void iteration_words() {
     words_out += B;
     if (win_now) win_words_out += B;
     if (signal == BELLMAN_SIG_TBT) {
@@ -668,19 +668,38 @@ struct Sim {
       acc_cnt += B;
     }
     if (DBG && dbg && lane == 0) {
-      bellman_second_row *w = row(ab(Tn));
+      bellman_second_row *w = row(ab(T));
       atomicAdd(&w->tbt_count, B);
       atomicAdd(&w->words_out, B);
       atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * iter_d + iter_align);
     }
     if (DBG) __syncwarp();
-    // every participant emitted one word: K += B
     kr += kstep_r;
     kq += kstep_q;
     if (kr >= 1000u) {
       kr -= 1000u;
       kq++;
     }
+  }
+
+  // Right after an iteration start: if that iteration's end is quiet — no
+  // completion, prefill end, admission, second / window / horizon boundary or
+  // epoch move at or before it — apply the end now (the next trip would do
+  // exactly this and nothing else) and return true.
+  __device__ __forceinline__ bool quiet_end() {
+    const uint32_t te = iter_end;
+    if (te >= stop_static || te >= sec_bound || te >= kRebaseAt || next_pf <= te || ticks - 1u == next_done)
+      return false;
+    if (in_sys < maxb && !adm_blocked && head_t <= te) return false;
+    T = te;
+    iteration_words();
+    busy = 0;
+    return true;
+  }
+
+  __device__ __forceinline__ void iteration_end(WarpHist &h) {
+    const uint32_t Tn = T;
+    iteration_words();
     const uint32_t it = ticks - 1u;
     if (it == next_done) {
       uint64_t e2e_l = 0;
@@ -1221,7 +1240,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 
     // ---- the event/tick loop (a4-a7)
 #ifdef BELLMAN_PROFILE_COUNTERS
-    uint32_t prof_[16] = {0};
+    uint32_t prof_[20] = {0};
     const long long loop0_ = clock64();
 #endif
     bool finished = false;
@@ -1241,7 +1260,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
         uint32_t lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
         if (S.sec_bound < lim) lim = S.sec_bound;
         if (S.next_pf < lim) {
-          PROF(10);
+          PROF(16);
           S.prefill_end(h, lim);
         }
         mid = S.next_pf < S.iter_end;
@@ -1289,8 +1308,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
         PROF(5);
         PROFC(12, S.admit(p, h));
       }
-      if (S.n_ready + S.B > 0) {
-        if (S.n_ready == 0) {
+      // at most two passes: a join iteration whose end is quiet is ended here
+      // and followed, in the same trip, by a leap and the next start
+      while (S.n_ready + S.B > 0) {
+        const bool join = S.n_ready != 0;
+        if (!join) {
           PROF(6);
           const uint32_t t0_ = S.ticks;
           PROFC(13, S.leap());
@@ -1301,13 +1323,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
           PROF(8);
         }
         PROFC(14, S.start_iteration());
+        if (!join || !S.quiet_end()) break;
+        PROF(17);
       }
     }
 
 #ifdef BELLMAN_PROFILE_COUNTERS
     prof_[15] = (uint32_t)(clock64() - loop0_);
     if (lane == 0)
-      for (int i = 0; i < 16; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
+      for (int i = 0; i < 20; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
 #endif
     // ---- termination (R20)
     const uint64_t Tend = S.ab(S.T);
@@ -1473,7 +1497,7 @@ __global__ void bellman_calibrate_kernel(const Params p, uint32_t n_slots) {
 
 #ifdef BELLMAN_PROFILE_COUNTERS
 extern "C" int bellman_debug_prof(unsigned long long *out) {
-  return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16);
+  return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 20);
 }
 #endif
 

@@ -403,6 +403,13 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.poly0 = desc->models.poly_q16[0];
   P.poly1 = desc->models.poly_q16[1];
   P.poly2 = desc->models.poly_q16[2];
+  {  // N <= P < 2^17 and Fcomp <= 2^18: |poly| < 2^43 keeps poly * Fcomp inside int64
+    const int64_t *c = desc->models.poly_q16;
+    const unsigned __int128 b = (unsigned __int128)(c[0] < 0 ? -c[0] : c[0]) +
+                                ((unsigned __int128)(c[1] < 0 ? -c[1] : c[1]) << 17) +
+                                ((unsigned __int128)(c[2] < 0 ? -c[2] : c[2]) << 34);
+    P.poly_fast = b < ((unsigned __int128)1 << 43) ? 1u : 0u;
+  }
   P.series_slot = (const uint32_t *)(ws + L.off_slot);
   P.series_off = (const uint64_t *)(ws + L.off_soff);
   P.series_cap = (const uint32_t *)(ws + L.off_scap);

@@ -31,7 +31,7 @@ struct DevTrace {
 };
 
 // Per-warp shared-memory histograms (a9, NEXT-2): 10,848 bytes.
-struct WarpHist {
+struct alignas(16) WarpHist {
   uint32_t e2e[BELLMAN_HIST_LAT];
   uint32_t ttft[BELLMAN_HIST_LAT];
   uint32_t r[BELLMAN_HIST_R];
@@ -49,6 +49,7 @@ struct Params {
   const int32_t *tabL, *tabI, *tabF, *tabN, *tabC, *tabQ;  // 4096 each
   const uint2 *log2tab;                             // (T[i], T[i+1]-T[i]), i < 4096
   int64_t poly0, poly1, poly2;
+  uint32_t poly_fast;  // |poly(N) * Fcomp| < 2^63 for every N < 2^17: the rewrite fits int64
   uint32_t q_inactive, q_active, q_floor, q_safe, q_end;  // quality model (NEXT-2)
   uint32_t class_cum0, class_cum1, class_cum2;            // request classes (NEXT-3)
   const uint32_t *series_slot;  // [n_scenarios] slot or NONE

@@ -25,7 +25,7 @@
 
 #ifdef BELLMAN_PROFILE_COUNTERS
 // Development-only event counters (separate build, never the product .so).
-__device__ unsigned long long g_prof[20];
+__device__ unsigned long long g_prof[24];
 #define PROF(i) (prof_[i]++)
 // cycles spent in a handler (clock64 deltas; a profiling build only)
 #define PROFC(i, stmt)                               \
@@ -37,6 +37,13 @@ __device__ unsigned long long g_prof[20];
 #else
 #define PROF(i) ((void)0)
 #define PROFC(i, stmt) stmt
+#endif
+#ifdef BELLMAN_PROFILE_COUNTERS
+#define PROF_MARK(v) const long long v = clock64()
+#define PROF_ACC(i, v) (prof[i] += (uint32_t)(clock64() - v))
+#else
+#define PROF_MARK(v) ((void)0)
+#define PROF_ACC(i, v) ((void)0)
 #endif
 
 namespace bellman {
@@ -124,7 +131,7 @@ __device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1
 // Cold per-scenario state: touched at events (admissions, completions,
 // ingests, refills), not per iteration.  Lives in shared memory, one per warp,
 // so the event loop keeps its hot state in registers without spilling.
-struct Cold {
+struct alignas(16) Cold {
   const DevSeg *segs;
   uint64_t gen_tau;
   uint64_t ringA;
@@ -141,6 +148,7 @@ struct Cold {
   uint32_t k0, wid_lo, wid_hi;
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
+  uint32_t pf_ns;                             // prefill ns per input word
   uint32_t ring[8];   // last `window` per-second samples (a6)
   // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
   // entry i written by lane i at refill, read by index at admission
@@ -150,6 +158,7 @@ struct Cold {
   uint32_t buf_P[32];    // predicted length
   uint32_t buf_fcq[32];  // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
   uint32_t buf_j[32];    // candidate index
+  uint32_t buf_pf[32];   // prefill duration max(1, floor(prefill_ns * input / 1000)) µs
   uint32_t rungs[8];  // word-limit ladder (R5)
 
 };
@@ -158,12 +167,19 @@ struct Cold {
 // predicted length is P and compliance factor in fcq under r > 0:
 // N = round(P (1 - r)), realized = clamp(round(poly(N) Fcomp), 1, 2^24).
 // Out of line (one copy): it runs once per rewritten admission.
-__device__ __noinline__ uint32_t rewrite_len(int64_t poly0, int64_t poly1, int64_t poly2, uint32_t P, uint32_t fcq,
-                                             uint32_t ra) {
-  int64_t N = (int64_t)(((uint64_t)P * (10000u - ra) + 5000u) / 10000u);
-  if (N < 1) N = 1;
-  const __int128 poly = (__int128)poly0 + (__int128)poly1 * N + (__int128)poly2 * N * N;
+__device__ __noinline__ uint32_t rewrite_len(int64_t poly0, int64_t poly1, int64_t poly2, uint32_t fast, uint32_t P,
+                                             uint32_t fcq, uint32_t ra) {
+  uint32_t N = (P * (10000u - ra) + 5000u) / 10000u;  // P < 2^17: no overflow
+  if (N < 1u) N = 1u;
   const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
+  if (fast) {  // host-checked coefficient bound: |poly(N) * fc| < 2^63, int64 suffices
+    const int64_t n = N;
+    const int64_t poly = poly0 + poly1 * n + poly2 * n * n;
+    int64_t x = (poly * fc + (1ll << 31)) >> 32;  // floor (arithmetic shift)
+    x = x < 1 ? 1 : (x > (1 << 24) ? (1 << 24) : x);
+    return (uint32_t)x;
+  }
+  const __int128 poly = (__int128)poly0 + (__int128)poly1 * N + (__int128)poly2 * N * N;
   __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;  // floor (arithmetic shift)
   if (x < 1) x = 1;
   if (x > (1 << 24)) x = 1 << 24;
@@ -171,7 +187,7 @@ __device__ __noinline__ uint32_t rewrite_len(int64_t poly0, int64_t poly1, int64
 }
 
 __device__ __forceinline__ uint32_t realized_len(const Params &p, uint32_t U, uint32_t P, uint32_t fcq, uint32_t ra) {
-  return ra == 0 ? U : rewrite_len(p.poly0, p.poly1, p.poly2, P, fcq, ra);
+  return ra == 0 ? U : rewrite_len(p.poly0, p.poly1, p.poly2, p.poly_fast, P, fcq, ra);
 }
 
 // NEXT-2 similarity decay between the safe window and decay_end:
@@ -213,6 +229,12 @@ __device__ __noinline__ uint4 leap_wide(uint32_t lane, uint32_t cb, uint32_t q, 
     if (c < 32u) break;
   }
   return make_uint4(n, used, q, rr);
+}
+
+// prefill duration of a request with `in` input words (R6): >= 1 µs
+__device__ __forceinline__ uint32_t prefill_us(uint32_t pf_ns, uint32_t in) {
+  const uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
+  return pf < 1u ? 1u : pf;
 }
 
 // Write-only counters (a8) are lane-distributed: counter i lives in lane i's
@@ -286,6 +308,7 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
       const uint64_t tau = (uint64_t)A.a_us;
       c.buf_a[lane] = tau;
       c.buf_in[lane] = A.input_words | (A.cls << 16);
+      c.buf_pf[lane] = prefill_us(c.pf_ns, A.input_words);
       c.buf_j[lane] = jj;
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
       const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
@@ -349,8 +372,10 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
       const uint32_t L = (uint32_t)__ldg(&p.tabL[u.z >> 20]);
       const uint32_t x = u.z & 0xFFFFFu;  // class draw from the bits below L's index (NEXT-3)
       const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
+      const uint32_t in = (uint32_t)__ldg(&p.tabI[u.w >> 20]);
       c.buf_a[e] = tau;
-      c.buf_in[e] = (uint32_t)__ldg(&p.tabI[u.w >> 20]) | (cls << 16);
+      c.buf_in[e] = in | (cls << 16);
+      c.buf_pf[e] = prefill_us(c.pf_ns, in);
       c.buf_j[e] = jj;
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);  // a3: the request's own draws
       const uint64_t U = ((uint64_t)L * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
@@ -496,6 +521,9 @@ struct Sim {
 #endif
   uint32_t lane;
   uint32_t wid;  // warp index in the CTA: selects this warp's Cold block
+#ifdef BELLMAN_PROFILE_COUNTERS
+  uint32_t *prof;
+#endif
   // ---- clock (a4): absolute time = E + 32-bit offset (INF32 / FAR32 above)
   uint64_t E;
   uint32_t Hr;  // horizon offset (FAR32 when beyond the window)
@@ -512,7 +540,7 @@ struct Sim {
   // debug record mode (NEXT-1): per-second rows and controller log, NULL when off
   bellman_second_row *dbg;
   // profile constants used at events
-  uint32_t pf_ns, t0, knee, slope, slo_us;
+  uint32_t t0, knee, slope, slo_us;
   // ---- counters (a8), updated at events
   uint32_t last_j;
   // ---- serving state (a4, a5, a7)
@@ -822,6 +850,7 @@ struct Sim {
     const uint64_t Ta = ab(Tn);
     adm_blocked = 0;
     for (;;) {
+      PROF_MARK(pa_);
       const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Ta);
       const uint32_t na = __popc(arrived);
       const uint32_t room = maxb - in_sys;
@@ -844,6 +873,8 @@ struct Sim {
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
       uint64_t q_l = 0;
       uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0;
+      PROF_ACC(18, pa_);
+      PROF_MARK(pb_);
       // one copy of the per-request body (admissions are rare next to ticks):
       // slot s is selected by value, not by unrolling
 #pragma unroll 1
@@ -885,8 +916,7 @@ struct Sim {
             atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
           }
 #endif
-          uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
-          if (pf < 1) pf = 1;
+          const uint32_t pf = cold().buf_pf[src];
           if (s == 0) {
             sa[0] = a;
             sp[0] = Tn + pf;
@@ -905,6 +935,8 @@ struct Sim {
           mpf = min(mpf, pf);
         }
       }
+      PROF_ACC(19, pb_);
+      PROF_MARK(pc_);
       const uint32_t mnew = __reduce_min_sync(FULL, mpf);  // k >= 1 new prefills
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
       const uint32_t win = __reduce_add_sync(FULL, win_l);
@@ -926,6 +958,8 @@ struct Sim {
           __syncwarp();
         }
       }
+      PROF_ACC(20, pc_);
+      PROF_MARK(pd_);
       last_j = cold().buf_j[buf_h + k - 1u] + 1u;
       kv_res += kv_add;
       in_sys += k;
@@ -938,6 +972,7 @@ struct Sim {
       } else {
         head_t = INF32;
       }
+      PROF_ACC(21, pd_);
       if (in_sys >= maxb || head_t > Tn) break;
     }
   }
@@ -1127,7 +1162,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     S.slope = pr.slope_us;
     S.kv = pr.kv_ns_per_word;
     S.maxb = pr.max_batch;
-    S.pf_ns = pr.prefill_ns_per_word;
     S.signal = cc.signal;
     S.slo_us = cc.slo_us;
     // a10: thresholds from the paired unbounded run's calibration
@@ -1163,6 +1197,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
       z.min_words = cc.min_words_bypass;
       z.bypassed = 0;
       z.kv_cap = pr.kv_cap_words;
+      z.pf_ns = pr.prefill_ns_per_word;
       z.flags = flags;
       z.active = z.rung = z.ring_n = z.ring_pos = 0;
       z.ringA = 0;
@@ -1240,7 +1275,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 
     // ---- the event/tick loop (a4-a7)
 #ifdef BELLMAN_PROFILE_COUNTERS
-    uint32_t prof_[20] = {0};
+    uint32_t prof_[24] = {0};
+    S.prof = prof_;
     const long long loop0_ = clock64();
 #endif
     bool finished = false;
@@ -1331,7 +1367,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 #ifdef BELLMAN_PROFILE_COUNTERS
     prof_[15] = (uint32_t)(clock64() - loop0_);
     if (lane == 0)
-      for (int i = 0; i < 20; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
+      for (int i = 0; i < 24; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
 #endif
     // ---- termination (R20)
     const uint64_t Tend = S.ab(S.T);
@@ -1497,7 +1533,7 @@ __global__ void bellman_calibrate_kernel(const Params p, uint32_t n_slots) {
 
 #ifdef BELLMAN_PROFILE_COUNTERS
 extern "C" int bellman_debug_prof(unsigned long long *out) {
-  return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 20);
+  return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 24);
 }
 #endif
 

@@ -15,7 +15,7 @@ from paper_2510_15330_b200 import _abi, build as B  # noqa: E402
 
 NAMES = ["trips", "mid_iteration_trips", "iter_end", "iter_end_with_completion", "prefill_end_event", "admit",
          "leap_calls", "leaped_ticks", "join_starts", "cyc_advance", "cyc_iteration_end", "cyc_prefill_end",
-         "cyc_admit", "cyc_leap", "cyc_start_iteration", "cyc_event_loop", "lazy_prefill_batches", "quiet_join_ends"]
+         "cyc_admit", "cyc_leap", "cyc_start_iteration", "cyc_event_loop", "lazy_prefill_batches", "quiet_join_ends", "cyc_admit_select", "cyc_admit_requests", "cyc_admit_reduce", "cyc_admit_head"]
 
 
 def main():
@@ -34,7 +34,7 @@ def main():
     torch.cuda.synchronize()
     st = sim.stats()
     lib = _abi.lib()
-    vals = np.zeros(20, dtype=np.uint64)
+    vals = np.zeros(24, dtype=np.uint64)
     assert lib.bellman_debug_prof(ctypes.c_void_p(vals.ctypes.data)) == 0
     print("ticks", int(st["ticks"].sum()), "admitted", int(st["admitted"].sum()), "served", int(st["served"].sum()))
     for n, v in zip(NAMES, vals):

@@ -303,3 +303,19 @@ def test_long_horizons_far_gaps_and_epoch_rebases():
     bad, st = check_all(_long_workload().columns())
     _assert_ok(bad)
     assert int(st["end_us"].max()) > (1 << 32)
+
+
+@pytest.mark.parametrize("poly", [(-(1 << 20), 70_000, 3),  # int64 path (|poly| bound < 2^43)
+                                  (0, 32_768, 512),          # 128-bit path (bound >= 2^43)
+                                  (5 << 16, -(1 << 14), 1 << 8)])
+def test_rewrite_polynomial_paths(poly):
+    """a7 rewrite (R11) through both device paths: the int64 one the
+    host enables for small coefficients and the 128-bit general one."""
+    ctrls = [W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1300), W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 4900),
+             W.map_ctrl(20_000, 30_000)]
+    sc = [W.Scenario(s, wid=0, trace=0, profile=p, ctrl=c, segment=0, mode=W.MODE_DRAIN, horizon_us=200 * W.US)
+          for s in range(4) for p in range(2) for c in range(3)]
+    w = W.custom([W.const_trace(4.0, 150)], [W.PROFILES["P24"], W.PROFILES["L8B"]], ctrls, sc, poly_q16=poly)
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)
+    assert int(st["rewritten"].sum()) > 0

@@ -125,6 +125,14 @@ __device__ __forceinline__ uint64_t warp_sum_split(uint64_t x) {
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+// The lane index read once into a register the compiler cannot re-derive
+// (it would otherwise rematerialize threadIdx.x & 31 with a slow S2R at each
+// use on the event loop's critical path).
+__device__ __forceinline__ uint32_t lane_pinned() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
 // this warp's index in its CTA (a constant 0 with one warp per CTA)
 __device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1 ? 0u : threadIdx.x >> 5; }
 
@@ -1136,7 +1144,7 @@ template <bool DBG>
 #define BELLMAN_MIN_BLOCKS (16 / BELLMAN_WPB)
 #endif
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellman_tick_kernel(const __grid_constant__ Params p) {
-  const uint32_t lane = lane_id();
+  const uint32_t lane = lane_pinned();
   WarpHist &h = g_hist[warp_in_block()];
   for (;;) {
     uint32_t kidx = 0;

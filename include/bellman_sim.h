@@ -51,7 +51,21 @@ typedef enum {
 } bellman_status;
 
 enum { BELLMAN_LAW_OFF = 0, BELLMAN_LAW_CONST = 1, BELLMAN_LAW_MAP = 2, BELLMAN_LAW_STEP = 3 };
-enum { BELLMAN_SIG_TBT = 0, BELLMAN_SIG_E2E = 1, BELLMAN_SIG_SLO = 2, BELLMAN_SIG_TTFT = 3 };
+/* Per-second congestion signals (a6).  TBT is the paper's; E2E / SLO
+ * are SPEC's alternatives; TTFT, INPUT and UTIL are the further
+ * signals P:211 names (NEXT-3): TTFT = mean TTFT of the second's first words;
+ * INPUT = input words admitted to the engine in the second (its total);
+ * UTIL = mean decode-batch occupancy over the second's iteration ends in basis
+ * points, floor(10000 sum(B) / (max_batch n)).  A second without a sample of
+ * the selected signal is a gap. */
+enum {
+  BELLMAN_SIG_TBT = 0,
+  BELLMAN_SIG_E2E = 1,
+  BELLMAN_SIG_SLO = 2,
+  BELLMAN_SIG_TTFT = 3,
+  BELLMAN_SIG_INPUT = 4,
+  BELLMAN_SIG_UTIL = 5
+};
 enum { BELLMAN_MODE_CUTOFF = 0, BELLMAN_MODE_DRAIN = 1 };
 
 /* summary flags */
@@ -115,7 +129,8 @@ typedef struct {
 /* Controller configuration (R3-R5, R22, R38). */
 typedef struct {
   uint32_t law;        /* BELLMAN_LAW_* */
-  uint32_t signal;     /* BELLMAN_SIG_*: per-second avg TBT (default), avg E2E, SLO per-mille, avg TTFT */
+  uint32_t signal;     /* BELLMAN_SIG_*: avg TBT (default), avg E2E, SLO per-mille, avg TTFT, admitted
+                          input words, batch occupancy bp (per second) */
   uint32_t window;     /* moving-average window in samples, 1..8 (5) */
   uint32_t r_min_bp;   /* MAP: r at t1 (5%) */
   uint32_t r_max_bp;   /* MAP: r at t2 (20%), <= 5000 */

@@ -33,7 +33,11 @@ extern "C" {
 #endif
 
 enum { ORC_LAW_OFF = 0, ORC_LAW_CONST = 1, ORC_LAW_MAP = 2, ORC_LAW_STEP = 3 };
-enum { ORC_SIG_TBT = 0, ORC_SIG_E2E = 1, ORC_SIG_SLO = 2, ORC_SIG_TTFT = 3 };
+/* INPUT and UTIL (NEXT-3, "input tokens per unit time", "GPU utilization
+ * metrics"): input words admitted in the second (the second's total); mean
+ * decode-batch occupancy over the second's iteration ends in basis points,
+ * floor(10000 sum(B) / (max_batch n)). */
+enum { ORC_SIG_TBT = 0, ORC_SIG_E2E = 1, ORC_SIG_SLO = 2, ORC_SIG_TTFT = 3, ORC_SIG_INPUT = 4, ORC_SIG_UTIL = 5 };
 enum { ORC_MODE_CUTOFF = 0, ORC_MODE_DRAIN = 1 };
 enum { ORC_FLAG_TRUNCATED = 1, ORC_FLAG_DEGENERATE_CALIB = 2 };
 

@@ -304,11 +304,16 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint64_t *sec_slo_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_ttft_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   uint64_t *sec_ttft_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_in_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));   /* NEXT-3 INPUT */
+  uint64_t *sec_in_any = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_util_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t)); /* NEXT-3 UTIL */
+  uint64_t *sec_util_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
   cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
   if (!rs || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
-      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt ||
+      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt || !sec_in_sum ||
+      !sec_in_any || !sec_util_sum || !sec_util_cnt ||
       ((cfg->record & 2) && !rows))
     goto out;
   if (cs.law == ORC_LAW_CONST) cs.r = ctrl->r_const_bp; /* S:320-326 constant policy */
@@ -334,6 +339,9 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
       if (ctrl->signal == ORC_SIG_TBT) { cnt = sec_tbt_cnt[next_sec]; sum = sec_tbt_sum[next_sec]; } \
       else if (ctrl->signal == ORC_SIG_TTFT) { cnt = sec_ttft_cnt[next_sec]; sum = sec_ttft_sum[next_sec]; } \
       else if (ctrl->signal == ORC_SIG_E2E) { cnt = sec_e2e_cnt[next_sec]; sum = sec_e2e_sum[next_sec]; } \
+      else if (ctrl->signal == ORC_SIG_INPUT) { cnt = sec_in_any[next_sec]; sum = sec_in_sum[next_sec]; } \
+      else if (ctrl->signal == ORC_SIG_UTIL) { cnt = (uint64_t)prof->max_batch * sec_util_cnt[next_sec];    \
+                                               sum = 10000 * sec_util_sum[next_sec]; }                  \
       else { cnt = sec_e2e_cnt[next_sec]; sum = 1000 * sec_slo_cnt[next_sec]; }          \
       if (cnt == 0) continue; /* a second with no samples is a gap */     \
       uint32_t x = (uint32_t)(sum / cnt);                                                \
@@ -368,6 +376,9 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
     while (h.n && h.v[0].t == T) {
       event e = heap_pop(&h);
       if (e.kind == EV_ITER_END) {
+        /* UTIL: the decode batch size at this iteration end */
+        sec_util_sum[s_idx] += n_batch;
+        sec_util_cnt[s_idx] += 1;
         /* E1: every request in the iteration emits a word at T */
         for (uint64_t b = 0; b < n_batch; ++b) {
           uint32_t m = batch[b];
@@ -497,6 +508,8 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         res->admitted++;
         res->sum_queue_us += T - req[m].a_us;
         res->words_in += req[m].input;
+        sec_in_sum[T / US] += req[m].input;
+        sec_in_any[T / US] = 1;
         if (in_window(T, cfg)) res->win_words_in += req[m].input;
         if (rows) {
           uint64_t sa = T / US;
@@ -643,7 +656,8 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
 out:
   free(rs); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
-  free(sec_ttft_sum); free(sec_ttft_cnt);
+  free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
+  free(sec_util_cnt);
   free(h.v); free(cs.samples); free(rows);
   return rc;
 }

@@ -125,7 +125,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
   for (uint32_t i = 0; i < d->n_ctrls; ++i) {
     const bellman_ctrl &c = d->ctrls[i];
     if (c.law > BELLMAN_LAW_STEP) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown law", i);
-    if (c.signal > BELLMAN_SIG_TTFT) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
+    if (c.signal > BELLMAN_SIG_UTIL) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
     if (c.bypass_mask > 15u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: bypass_mask has bits beyond 4 classes", i);
     if (c.window < 1 || c.window > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: window not in 1..8", i);
     if (c.n_rungs > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: more than 8 rungs", i);

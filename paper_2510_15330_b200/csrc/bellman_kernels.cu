@@ -428,9 +428,13 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
 // shared-memory state.
 template <bool DBG>
 __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
-                                               uint32_t acc_cnt, uint32_t r_cur, bool dbg) {
+                                               uint32_t acc_cnt, uint32_t r_cur, bool dbg, uint32_t util_maxb) {
   Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
-  const uint32_t second = (uint32_t)(sec_bound / kUs - 1u), x = (uint32_t)(acc_sum / acc_cnt);
+  const uint32_t second = (uint32_t)(sec_bound / kUs - 1u);
+  // the sample: floor(acc_sum / acc_cnt) truncated to 32 bits (as the oracle); UTIL
+  // keeps sum B / count and scales once here: floor(10000 sum B / (max_batch count))
+  const uint32_t x = util_maxb ? (uint32_t)(10000u * acc_sum / ((uint64_t)util_maxb * acc_cnt))
+                               : (uint32_t)(acc_sum / acc_cnt);
   if (c.series) {
     const uint32_t n = c.series_n;
     if (lane == 0) {
@@ -514,9 +518,12 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
 // division: the cost base c = t0 + slope max(0, B - knee), the KV term as
 // kv K = kq 1000 + kr, the window flag and its next boundary, the arrival time
 // of the queue head.
-template <bool DBG>
+template <bool DBG, bool TBTO>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
+  // the selected signal is x: a compile-time answer in the TBT-only
+  // instantiation (every benchmark configuration), a runtime one otherwise
+  __device__ __forceinline__ bool sig(uint32_t x) const { return TBTO ? x == BELLMAN_SIG_TBT : signal == x; }
   __device__ __forceinline__ Cold &cold() const { return g_cold[kWarpsPerBlock == 1 ? 0u : wid]; }
 #ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
@@ -594,7 +601,8 @@ struct Sim {
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest() {
-    r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr);
+    r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,
+                           sig(BELLMAN_SIG_UTIL) ? maxb : 0u);
   }
 
   // close the open second (if it holds samples) and open the one containing t
@@ -685,11 +693,11 @@ struct Sim {
 
   // ------------------------------------------------------------------ a5
   __device__ __forceinline__ void complete_sig(uint64_t sum_e2e_w, uint32_t n, uint32_t nslo) {
-    if (signal == BELLMAN_SIG_TBT || signal == BELLMAN_SIG_TTFT) return;
-    if (signal == BELLMAN_SIG_E2E) {
+    if (sig(BELLMAN_SIG_TBT) || sig(BELLMAN_SIG_TTFT)) return;
+    if (sig(BELLMAN_SIG_E2E)) {
       acc_sum += sum_e2e_w;
       acc_cnt += n;
-    } else if (signal == BELLMAN_SIG_SLO) {
+    } else if (sig(BELLMAN_SIG_SLO)) {
       acc_sum += 1000ull * nslo;
       acc_cnt += n;
     }
@@ -699,10 +707,10 @@ struct Sim {
   __device__ __forceinline__ void iteration_words() {
     words_out += B;
     if (win_now) win_words_out += B;
-    if (signal == BELLMAN_SIG_TBT) {
-      acc_sum += (uint64_t)B * iter_d + iter_align;
-      acc_cnt += B;
-    }
+    // TBT: the B gaps of this end; UTIL (NEXT-3): the batch size B, one sample
+    const bool tbt = sig(BELLMAN_SIG_TBT), util = sig(BELLMAN_SIG_UTIL);
+    acc_sum += tbt ? (uint64_t)B * iter_d + iter_align : (util ? (uint64_t)B : 0u);
+    acc_cnt += tbt ? B : (util ? 1u : 0u);
     if (DBG && dbg && lane == 0) {
       bellman_second_row *w = row(ab(T));
       atomicAdd(&w->tbt_count, B);
@@ -819,7 +827,7 @@ struct Sim {
     const uint64_t st = warp_sum_split(ttft_l);
     cadd(CT_SUM_TTFT, st);
     words_out += nfirst;
-    if (signal == BELLMAN_SIG_TTFT) {  // NEXT-3 signal: mean TTFT of the second's first words
+    if (sig(BELLMAN_SIG_TTFT)) {  // NEXT-3 signal: mean TTFT of the second's first words
       acc_sum += st;
       acc_cnt += nfirst;
     }
@@ -949,6 +957,10 @@ struct Sim {
       if (Tn + mnew < next_pf) next_pf = Tn + mnew;
       const uint32_t win = __reduce_add_sync(FULL, win_l);
       cadd(CT_WORDS_IN, win);
+      if (sig(BELLMAN_SIG_INPUT)) {  // NEXT-3: input words admitted in the second
+        acc_sum += win;
+        acc_cnt = 1u;
+      }
       if (win_now) cadd(CT_WIN_WORDS_IN, win);
       const uint64_t sq = warp_sum_split(q_l);
       cadd(CT_SUM_QUEUE, sq);
@@ -1042,9 +1054,12 @@ struct Sim {
         T += used;
         words_out += words;
         if (win_now) win_words_out += words;
-        if (signal == BELLMAN_SIG_TBT) {
+        if (sig(BELLMAN_SIG_TBT)) {
           acc_sum += (uint64_t)B * used;
           acc_cnt += (uint32_t)words;
+        } else if (sig(BELLMAN_SIG_UTIL)) {
+          acc_sum += (uint64_t)n * B;
+          acc_cnt += n;
         }
         if (DBG && dbg && lane == 0) {  // all ends of this chunk lie in the open second
           bellman_second_row *w = row(ab(sec_bound) - kUs);
@@ -1139,6 +1154,354 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
   }
 }
 
+// One scenario, a1-a9.  TBTO: the scenario's signal is TBT (compile-time
+// specialisation of every signal test in the event loop).
+template <bool DBG, bool TBTO>
+__device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, const bellman_scenario &sc,
+                                        const bellman_ctrl &cc, const uint32_t lane, WarpHist &h) {
+  // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
+  // lane 0 only and read after the __syncwarp below.
+  Sim<DBG, TBTO> S(warp_in_block());
+  S.lane = lane;
+  const bellman_profile pr = p.profs[sc.profile];
+  const DevTrace tr = p.traces[sc.trace];
+  S.E = 0;
+  S.t0 = pr.t0_us;
+  S.knee = pr.knee;
+  S.slope = pr.slope_us;
+  S.kv = pr.kv_ns_per_word;
+  S.maxb = pr.max_batch;
+  S.signal = cc.signal;
+  S.slo_us = cc.slo_us;
+  // a10: thresholds from the paired unbounded run's calibration
+  uint32_t law = cc.law, t1 = cc.t1, t2 = cc.t2, flags = 0;
+  if (cc.calibrated) {
+    const uint32_t *cb = p.calib + 4u * p.series_slot[sc.calib_src];
+    t1 = cb[0];
+    t2 = cb[1];
+    if (cb[2] != 0) {
+      law = BELLMAN_LAW_OFF;
+      flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+    }
+  }
+  const uint32_t rslot = p.series_slot[sid];
+  const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
+  S.dbg = (DBG && dslot != BELLMAN_NONE) ? p.dbg_rows + p.dbg_off[dslot] : nullptr;
+  if (lane == 0) {
+    Cold &z = S.cold();
+    z.k0 = sc.seed_index;
+    z.wid_lo = (uint32_t)sc.wid;
+    z.wid_hi = (uint32_t)(sc.wid >> 32);
+    z.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
+    z.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
+    z.H = (uint64_t)sc.horizon_us;
+    z.law = law;
+    z.window = cc.window;
+    z.rmin = cc.r_min_bp;
+    z.rmax = cc.r_max_bp;
+    z.t1 = t1;
+    z.t2 = t2;
+    z.nrungs = cc.n_rungs;
+    z.bypass_mask = cc.bypass_mask;
+    z.min_words = cc.min_words_bypass;
+    z.bypassed = 0;
+    z.kv_cap = pr.kv_cap_words;
+    z.pf_ns = pr.prefill_ns_per_word;
+    z.flags = flags;
+    z.active = z.rung = z.ring_n = z.ring_pos = 0;
+    z.ringA = 0;
+    z.activations = z.active_ingests = 0;
+    z.first_act = z.last_deact = BELLMAN_NONE;
+    z.series = rslot != BELLMAN_NONE ? p.series + p.series_off[rslot] : nullptr;
+    z.series_cap = rslot != BELLMAN_NONE ? p.series_cap[rslot] : 0u;
+    z.series_n = 0;
+    z.dbg_ctrl = (DBG && dslot != BELLMAN_NONE) ? p.dbg_ctrl + p.dbg_off[dslot] : nullptr;
+    z.dbg_cap = (DBG && dslot != BELLMAN_NONE) ? p.dbg_cap[dslot] : 0u;
+    z.dbg_nctrl = 0;
+    z.segs = p.segs + (tr.kind ? 0u : tr.seg_off);
+    z.n_seg = tr.n_seg;
+    z.replay = tr.kind;
+    z.rep_off = tr.kind ? tr.seg_off : 0u;
+    z.gen_seg = z.gen_j = z.gen_acc = z.gen_done = 0;
+    z.gen_fresh = 1;
+    z.gen_cap = tr.cap;
+    z.gen_tau = 0;
+  }
+  if (lane < 8) {
+    S.cold().rungs[lane] = cc.rungs_bp[lane];
+    S.cold().ring[lane] = 0;
+  }
+  if (DBG && S.dbg) {  // rows are accumulated with atomics: zero this scenario's region first
+    const uint32_t cap = p.dbg_cap[dslot];
+    for (uint32_t i = lane; i < cap; i += 32u) S.dbg[i] = bellman_second_row{};
+  }
+  __syncwarp();
+  S.r = law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
+  S.acc_sum = 0;
+  S.acc_cnt = 0;
+  // the per-second signal feeds only the controller (MAP/STEP) and the recorders
+  S.sec_bound = (law == BELLMAN_LAW_MAP || law == BELLMAN_LAW_STEP || rslot != BELLMAN_NONE || (DBG && S.dbg))
+                    ? (uint32_t)kUs : INF32;
+  S.Hr = S.rel((uint64_t)sc.horizon_us);
+  S.T = 0;
+  S.busy = 0;
+  S.iter_end = INF32;
+  S.iter_d = 0;
+  S.iter_align = 0;
+  S.ticks = 0;
+  S.next_done = 0xffffffffu;
+  S.next_pf = INF32;
+  S.n_ready = S.B = S.in_sys = 0;
+  S.kq = S.kr = 0;
+  S.batch_changed();
+  S.update_window();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    S.sa[s] = S.sp[s] = 0;
+    S.sR[s] = S.sin[s] = S.sdn[s] = 0;
+    // slots beyond max_batch are never free
+    S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
+  }
+  S.buf_h = S.buf_n = 0;
+  S.kv_res = 0;
+  S.adm_blocked = 0;
+  S.last_j = 0;
+#ifndef BELLMAN_AB_REGCTR
+  S.ctr = 0;
+#else
+#pragma unroll
+  for (uint32_t i = 0; i < CT_N; ++i) S.ctrs[i] = 0;
+#endif
+  S.words_out = S.win_words_out = 0;
+
+  // zero the warp's histograms
+  {
+    uint4 *z = reinterpret_cast<uint4 *>(&h);
+    for (uint32_t i = lane; i < sizeof(WarpHist) / 16u; i += 32u) z[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  }
+  S.refill(p);
+
+  // ---- the event/tick loop (a4-a7)
+#ifdef BELLMAN_PROFILE_COUNTERS
+  uint32_t prof_[24] = {0};
+  S.prof = prof_;
+  const long long loop0_ = clock64();
+#endif
+  bool finished = false;
+  for (;;) {
+    uint32_t tn;
+    // a prefill end strictly inside the running iteration only emits first
+    // words / R=1 completions (time-stamped at p): its trip does nothing
+    // else; same-instant ends go after the iteration end (E1, R7).  One call
+    // site per event handler keeps the loop's instruction footprint small.
+    bool mid = false;
+    PROF(0);
+    if (S.busy) {
+      // prefill ends due inside the running iteration, in the open second and
+      // window: handled here, at the start of the iteration-end trip (their
+      // effects are order-free until the iteration end); any left lie past a
+      // second / window boundary and get their own trip
+      uint32_t lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
+      if (S.sec_bound < lim) lim = S.sec_bound;
+      if (S.next_pf < lim) {
+        PROF(16);
+        S.prefill_end(h, lim);
+      }
+      mid = S.next_pf < S.iter_end;
+      tn = mid ? S.next_pf : S.iter_end;
+    } else {
+      tn = S.next_pf;
+      if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t < tn) tn = S.head_t;
+      if (tn == INF32) {
+        finished = true;
+        break;
+      }
+      // a far next event: jump (idle) to the cap first; advance() rebases there
+      if (tn > kJumpCap) tn = kJumpCap;
+    }
+    if (tn >= S.Hr) break;
+    if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
+      S.cadd(CT_IDLE, tn - S.T);
+      const uint64_t a = S.ab(S.T), b = S.ab(tn);
+      const uint64_t lo = a > S.cold().w0 ? a : S.cold().w0, hi = b < S.cold().w1 ? b : S.cold().w1;
+      if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
+      S.dbg_idle(a, b);
+    }
+    PROFC(9, S.advance(tn));
+    tn = S.T;  // advance() may have moved the epoch
+    if (S.busy && !mid) {
+      PROF(2);
+      if (S.ticks - 1u == S.next_done) PROF(3);
+      PROFC(10, S.iteration_end(h));
+    }
+    if (S.next_pf == tn) {  // always so on a mid-iteration trip
+      PROF(4);
+      uint32_t lim = tn + 1u;
+      if (mid) {
+        lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
+        if (S.sec_bound < lim) lim = S.sec_bound;
+      }
+      PROFC(11, S.prefill_end(h, lim));
+    }
+    if (mid) {
+      PROF(1);
+      continue;
+    }
+    // the decode loop is idle here: admission point (R7), then the next iteration
+    if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
+      PROF(5);
+      PROFC(12, S.admit(p, h));
+    }
+    // at most two passes: a join iteration whose end is quiet is ended here
+    // and followed, in the same trip, by a leap and the next start
+    while (S.n_ready + S.B > 0) {
+      const bool join = S.n_ready != 0;
+      if (!join) {
+        PROF(6);
+        const uint32_t t0_ = S.ticks;
+        PROFC(13, S.leap());
+#ifdef BELLMAN_PROFILE_COUNTERS
+        prof_[7] += S.ticks - t0_;
+#endif
+      } else {
+        PROF(8);
+      }
+      PROFC(14, S.start_iteration());
+      if (!join || !S.quiet_end()) break;
+      PROF(17);
+    }
+  }
+
+#ifdef BELLMAN_PROFILE_COUNTERS
+  prof_[15] = (uint32_t)(clock64() - loop0_);
+  if (lane == 0)
+    for (int i = 0; i < 24; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
+#endif
+  // ---- termination (R20)
+  const uint64_t Tend = S.ab(S.T);
+  const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? Tend : (uint64_t)sc.horizon_us;
+  if (S.in_sys == 0) {
+    S.cadd(CT_IDLE, end - Tend);
+    const uint64_t lo = Tend > S.cold().w0 ? Tend : S.cold().w0, hi = end < S.cold().w1 ? end : S.cold().w1;
+    if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
+    S.dbg_idle(Tend, end);
+  }
+  if (S.sec_bound != INF32 && S.ab(S.sec_bound) <= end && S.acc_cnt) S.ingest();
+  // queued at the end: accepted arrivals before `end` not admitted
+  uint64_t queued = 0;
+  for (;;) {
+    if (S.buf_h >= S.buf_n) {
+      if (S.cold().gen_done) break;
+      S.refill(p);
+      continue;
+    }
+    const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().buf_a[lane] < end);
+    const uint32_t nq = __popc(m);
+    queued += nq;
+    if (nq) S.last_j = S.cold().buf_j[31 - __clz(m)] + 1u;
+    if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
+    S.buf_h = S.buf_n;
+  }
+  if (S.cold().series && lane == 0) p.series_n[rslot] = S.cold().series_n;
+  if (DBG && S.dbg && lane == 0) {
+    const uint64_t nr = end / kUs + 1u;
+    p.dbg_n[2 * dslot] = (uint32_t)(nr < S.cold().dbg_cap ? nr : S.cold().dbg_cap);
+    p.dbg_n[2 * dslot + 1] = S.cold().dbg_nctrl;
+  }
+
+  // ---- a9: percentiles from the histograms
+  uint64_t C_[CT_N];
+#pragma unroll
+  for (uint32_t i = 0; i < CT_N; ++i) C_[i] = S.cget(i);
+  __syncwarp();
+  uint32_t pe[2], pt[2], pm[1];
+  const uint32_t ps[2] = {50u, 99u};
+  const uint32_t p50[1] = {50u};
+  warp_percentiles(h.e2e, BELLMAN_HIST_LAT, C_[CT_SERVED], ps, 2, pe, true);
+  uint64_t n_ttft = 0;
+  {
+    uint32_t c = 0;
+    for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) c += h.ttft[b];
+    n_ttft = __reduce_add_sync(FULL, c);
+  }
+  warp_percentiles(h.ttft, BELLMAN_HIST_LAT, n_ttft, ps, 2, pt, true);
+  warp_percentiles(h.r, BELLMAN_HIST_R, C_[CT_REWRITTEN], p50, 1, pm, false);
+  uint32_t pqa[1], pqi[1];  // NEXT-2 similarity medians
+  warp_percentiles(h.qa, BELLMAN_HIST_Q, C_[CT_REWRITTEN], p50, 1, pqa, false, 50u);
+  warp_percentiles(h.qi, BELLMAN_HIST_Q, C_[CT_ADMITTED] - C_[CT_REWRITTEN], p50, 1, pqi, false, 50u);
+  // segment merge: integer atomics, order-independent
+  unsigned long long *sh = p.seg_hist + (uint64_t)sc.segment * kSegWords;
+  for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) {
+    if (h.e2e[b]) atomicAdd(&sh[b], (unsigned long long)h.e2e[b]);
+    if (h.ttft[b]) atomicAdd(&sh[BELLMAN_HIST_LAT + b], (unsigned long long)h.ttft[b]);
+  }
+  for (uint32_t b = lane; b < BELLMAN_HIST_R; b += 32u)
+    if (h.r[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + b], (unsigned long long)h.r[b]);
+  for (uint32_t b = lane; b < BELLMAN_HIST_Q; b += 32u) {
+    if (h.qa[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + b], (unsigned long long)h.qa[b]);
+    if (h.qi[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q + b], (unsigned long long)h.qi[b]);
+  }
+
+  // ---- a8: summary record
+  if (lane == 0) {
+    bellman_scenario_stats o;
+    o.scenario_id = sid;
+    o.ticks = S.ticks;
+    o.candidates = S.last_j;
+    o.arrivals = C_[CT_ADMITTED] + queued;
+    o.admitted = C_[CT_ADMITTED];
+    o.served = C_[CT_SERVED];
+    o.rewritten = C_[CT_REWRITTEN];
+    o.words_in = C_[CT_WORDS_IN];
+    o.words_out = S.words_out;
+    o.idle_us = C_[CT_IDLE];
+    o.end_us = end;
+    o.queued_end = queued;
+    o.inflight_end = S.in_sys;
+    o.win_served = C_[CT_WIN_SERVED];
+    o.win_words_in = C_[CT_WIN_WORDS_IN];
+    o.win_words_out = S.win_words_out;
+    o.win_idle_us = C_[CT_WIN_IDLE];
+    o.sum_queue_us = C_[CT_SUM_QUEUE];
+    o.sum_ttft_us = C_[CT_SUM_TTFT];
+    o.sum_e2e_us = C_[CT_SUM_E2E];
+    o.slo_violations = C_[CT_SLO_VIOL];
+    o.e2e_p50_ms = pe[0];
+    o.e2e_p99_ms = pe[1];
+    o.ttft_p50_ms = pt[0];
+    o.ttft_p99_ms = pt[1];
+    o.median_r_bp = pm[0];
+    o.t1 = S.cold().t1;
+    o.t2 = S.cold().t2;
+    o.activations = S.cold().activations;
+    o.first_act_s = S.cold().first_act;
+    o.last_deact_s = S.cold().last_deact;
+    o.active_ingests = S.cold().active_ingests;
+    uint32_t fl = S.cold().flags | BELLMAN_FLAG_DONE;
+    if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
+    o.flags = fl;
+    o.segment = sc.segment;
+    o.bypassed = S.cold().bypassed;
+    // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
+    const double a = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WORDS_IN]);
+    const double b = __dmul_rn(pr.e_out_j_per_word, (double)S.words_out);
+    const double c = __dmul_rn(pr.p_idle_w, (double)C_[CT_IDLE]);
+    o.energy_j = __dadd_rn(__dadd_rn(a, b), __ddiv_rn(c, 1e6));
+    const double wa = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WIN_WORDS_IN]);
+    const double wb = __dmul_rn(pr.e_out_j_per_word, (double)S.win_words_out);
+    const double wc = __dmul_rn(pr.p_idle_w, (double)C_[CT_WIN_IDLE]);
+    o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
+    o.sim_active_p50 = pqa[0];
+    o.sim_inactive_p50 = pqi[0];
+    o.scored_active = C_[CT_REWRITTEN];
+    o.scored_inactive = C_[CT_ADMITTED] - C_[CT_REWRITTEN];
+    p.stats[sid] = o;
+  }
+  __syncwarp();
+  __syncwarp();
+}
+
 template <bool DBG>
 #ifndef BELLMAN_MIN_BLOCKS
 #define BELLMAN_MIN_BLOCKS (16 / BELLMAN_WPB)
@@ -1158,347 +1521,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     // debug-recorded scenarios run in the DBG instantiation, all others in the product one
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
-    // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
-    // lane 0 only and read after the __syncwarp below.
-    Sim<DBG> S(warp_in_block());
-    S.lane = lane;
-    const bellman_profile pr = p.profs[sc.profile];
-    const DevTrace tr = p.traces[sc.trace];
-    S.E = 0;
-    S.t0 = pr.t0_us;
-    S.knee = pr.knee;
-    S.slope = pr.slope_us;
-    S.kv = pr.kv_ns_per_word;
-    S.maxb = pr.max_batch;
-    S.signal = cc.signal;
-    S.slo_us = cc.slo_us;
-    // a10: thresholds from the paired unbounded run's calibration
-    uint32_t law = cc.law, t1 = cc.t1, t2 = cc.t2, flags = 0;
-    if (cc.calibrated) {
-      const uint32_t *cb = p.calib + 4u * p.series_slot[sc.calib_src];
-      t1 = cb[0];
-      t2 = cb[1];
-      if (cb[2] != 0) {
-        law = BELLMAN_LAW_OFF;
-        flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
-      }
+    if constexpr (DBG) {
+      run_one<true, false>(p, sid, sc, cc, lane, h);
+    } else if (cc.signal == BELLMAN_SIG_TBT) {
+      run_one<false, true>(p, sid, sc, cc, lane, h);
+    } else {
+      run_one<false, false>(p, sid, sc, cc, lane, h);
     }
-    const uint32_t rslot = p.series_slot[sid];
-    const uint32_t dslot = DBG ? p.dbg_slot[sid] : BELLMAN_NONE;
-    S.dbg = (DBG && dslot != BELLMAN_NONE) ? p.dbg_rows + p.dbg_off[dslot] : nullptr;
-    if (lane == 0) {
-      Cold &z = S.cold();
-      z.k0 = sc.seed_index;
-      z.wid_lo = (uint32_t)sc.wid;
-      z.wid_hi = (uint32_t)(sc.wid >> 32);
-      z.w0 = (uint64_t)(sc.w0_us < 0 ? 0 : sc.w0_us);
-      z.w1 = (uint64_t)(sc.w1_us < 0 ? 0 : sc.w1_us);
-      z.H = (uint64_t)sc.horizon_us;
-      z.law = law;
-      z.window = cc.window;
-      z.rmin = cc.r_min_bp;
-      z.rmax = cc.r_max_bp;
-      z.t1 = t1;
-      z.t2 = t2;
-      z.nrungs = cc.n_rungs;
-      z.bypass_mask = cc.bypass_mask;
-      z.min_words = cc.min_words_bypass;
-      z.bypassed = 0;
-      z.kv_cap = pr.kv_cap_words;
-      z.pf_ns = pr.prefill_ns_per_word;
-      z.flags = flags;
-      z.active = z.rung = z.ring_n = z.ring_pos = 0;
-      z.ringA = 0;
-      z.activations = z.active_ingests = 0;
-      z.first_act = z.last_deact = BELLMAN_NONE;
-      z.series = rslot != BELLMAN_NONE ? p.series + p.series_off[rslot] : nullptr;
-      z.series_cap = rslot != BELLMAN_NONE ? p.series_cap[rslot] : 0u;
-      z.series_n = 0;
-      z.dbg_ctrl = (DBG && dslot != BELLMAN_NONE) ? p.dbg_ctrl + p.dbg_off[dslot] : nullptr;
-      z.dbg_cap = (DBG && dslot != BELLMAN_NONE) ? p.dbg_cap[dslot] : 0u;
-      z.dbg_nctrl = 0;
-      z.segs = p.segs + (tr.kind ? 0u : tr.seg_off);
-      z.n_seg = tr.n_seg;
-      z.replay = tr.kind;
-      z.rep_off = tr.kind ? tr.seg_off : 0u;
-      z.gen_seg = z.gen_j = z.gen_acc = z.gen_done = 0;
-      z.gen_fresh = 1;
-      z.gen_cap = tr.cap;
-      z.gen_tau = 0;
-    }
-    if (lane < 8) {
-      S.cold().rungs[lane] = cc.rungs_bp[lane];
-      S.cold().ring[lane] = 0;
-    }
-    if (DBG && S.dbg) {  // rows are accumulated with atomics: zero this scenario's region first
-      const uint32_t cap = p.dbg_cap[dslot];
-      for (uint32_t i = lane; i < cap; i += 32u) S.dbg[i] = bellman_second_row{};
-    }
-    __syncwarp();
-    S.r = law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
-    S.acc_sum = 0;
-    S.acc_cnt = 0;
-    // the per-second signal feeds only the controller (MAP/STEP) and the recorders
-    S.sec_bound = (law == BELLMAN_LAW_MAP || law == BELLMAN_LAW_STEP || rslot != BELLMAN_NONE || (DBG && S.dbg))
-                      ? (uint32_t)kUs : INF32;
-    S.Hr = S.rel((uint64_t)sc.horizon_us);
-    S.T = 0;
-    S.busy = 0;
-    S.iter_end = INF32;
-    S.iter_d = 0;
-    S.iter_align = 0;
-    S.ticks = 0;
-    S.next_done = 0xffffffffu;
-    S.next_pf = INF32;
-    S.n_ready = S.B = S.in_sys = 0;
-    S.kq = S.kr = 0;
-    S.batch_changed();
-    S.update_window();
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      S.sa[s] = S.sp[s] = 0;
-      S.sR[s] = S.sin[s] = S.sdn[s] = 0;
-      // slots beyond max_batch are never free
-      S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
-    }
-    S.buf_h = S.buf_n = 0;
-    S.kv_res = 0;
-    S.adm_blocked = 0;
-    S.last_j = 0;
-#ifndef BELLMAN_AB_REGCTR
-    S.ctr = 0;
-#else
-#pragma unroll
-    for (uint32_t i = 0; i < CT_N; ++i) S.ctrs[i] = 0;
-#endif
-    S.words_out = S.win_words_out = 0;
-
-    // zero the warp's histograms
-    {
-      uint4 *z = reinterpret_cast<uint4 *>(&h);
-      for (uint32_t i = lane; i < sizeof(WarpHist) / 16u; i += 32u) z[i] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-    }
-    S.refill(p);
-
-    // ---- the event/tick loop (a4-a7)
-#ifdef BELLMAN_PROFILE_COUNTERS
-    uint32_t prof_[24] = {0};
-    S.prof = prof_;
-    const long long loop0_ = clock64();
-#endif
-    bool finished = false;
-    for (;;) {
-      uint32_t tn;
-      // a prefill end strictly inside the running iteration only emits first
-      // words / R=1 completions (time-stamped at p): its trip does nothing
-      // else; same-instant ends go after the iteration end (E1, R7).  One call
-      // site per event handler keeps the loop's instruction footprint small.
-      bool mid = false;
-      PROF(0);
-      if (S.busy) {
-        // prefill ends due inside the running iteration, in the open second and
-        // window: handled here, at the start of the iteration-end trip (their
-        // effects are order-free until the iteration end); any left lie past a
-        // second / window boundary and get their own trip
-        uint32_t lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
-        if (S.sec_bound < lim) lim = S.sec_bound;
-        if (S.next_pf < lim) {
-          PROF(16);
-          S.prefill_end(h, lim);
-        }
-        mid = S.next_pf < S.iter_end;
-        tn = mid ? S.next_pf : S.iter_end;
-      } else {
-        tn = S.next_pf;
-        if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t < tn) tn = S.head_t;
-        if (tn == INF32) {
-          finished = true;
-          break;
-        }
-        // a far next event: jump (idle) to the cap first; advance() rebases there
-        if (tn > kJumpCap) tn = kJumpCap;
-      }
-      if (tn >= S.Hr) break;
-      if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
-        S.cadd(CT_IDLE, tn - S.T);
-        const uint64_t a = S.ab(S.T), b = S.ab(tn);
-        const uint64_t lo = a > S.cold().w0 ? a : S.cold().w0, hi = b < S.cold().w1 ? b : S.cold().w1;
-        if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
-        S.dbg_idle(a, b);
-      }
-      PROFC(9, S.advance(tn));
-      tn = S.T;  // advance() may have moved the epoch
-      if (S.busy && !mid) {
-        PROF(2);
-        if (S.ticks - 1u == S.next_done) PROF(3);
-        PROFC(10, S.iteration_end(h));
-      }
-      if (S.next_pf == tn) {  // always so on a mid-iteration trip
-        PROF(4);
-        uint32_t lim = tn + 1u;
-        if (mid) {
-          lim = S.iter_end < S.stop_static ? S.iter_end : S.stop_static;
-          if (S.sec_bound < lim) lim = S.sec_bound;
-        }
-        PROFC(11, S.prefill_end(h, lim));
-      }
-      if (mid) {
-        PROF(1);
-        continue;
-      }
-      // the decode loop is idle here: admission point (R7), then the next iteration
-      if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
-        PROF(5);
-        PROFC(12, S.admit(p, h));
-      }
-      // at most two passes: a join iteration whose end is quiet is ended here
-      // and followed, in the same trip, by a leap and the next start
-      while (S.n_ready + S.B > 0) {
-        const bool join = S.n_ready != 0;
-        if (!join) {
-          PROF(6);
-          const uint32_t t0_ = S.ticks;
-          PROFC(13, S.leap());
-#ifdef BELLMAN_PROFILE_COUNTERS
-          prof_[7] += S.ticks - t0_;
-#endif
-        } else {
-          PROF(8);
-        }
-        PROFC(14, S.start_iteration());
-        if (!join || !S.quiet_end()) break;
-        PROF(17);
-      }
-    }
-
-#ifdef BELLMAN_PROFILE_COUNTERS
-    prof_[15] = (uint32_t)(clock64() - loop0_);
-    if (lane == 0)
-      for (int i = 0; i < 24; ++i) atomicAdd(&g_prof[i], (unsigned long long)prof_[i]);
-#endif
-    // ---- termination (R20)
-    const uint64_t Tend = S.ab(S.T);
-    const uint64_t end = (sc.mode == BELLMAN_MODE_DRAIN && finished) ? Tend : (uint64_t)sc.horizon_us;
-    if (S.in_sys == 0) {
-      S.cadd(CT_IDLE, end - Tend);
-      const uint64_t lo = Tend > S.cold().w0 ? Tend : S.cold().w0, hi = end < S.cold().w1 ? end : S.cold().w1;
-      if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
-      S.dbg_idle(Tend, end);
-    }
-    if (S.sec_bound != INF32 && S.ab(S.sec_bound) <= end && S.acc_cnt) S.ingest();
-    // queued at the end: accepted arrivals before `end` not admitted
-    uint64_t queued = 0;
-    for (;;) {
-      if (S.buf_h >= S.buf_n) {
-        if (S.cold().gen_done) break;
-        S.refill(p);
-        continue;
-      }
-      const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().buf_a[lane] < end);
-      const uint32_t nq = __popc(m);
-      queued += nq;
-      if (nq) S.last_j = S.cold().buf_j[31 - __clz(m)] + 1u;
-      if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
-      S.buf_h = S.buf_n;
-    }
-    if (S.cold().series && lane == 0) p.series_n[rslot] = S.cold().series_n;
-    if (DBG && S.dbg && lane == 0) {
-      const uint64_t nr = end / kUs + 1u;
-      p.dbg_n[2 * dslot] = (uint32_t)(nr < S.cold().dbg_cap ? nr : S.cold().dbg_cap);
-      p.dbg_n[2 * dslot + 1] = S.cold().dbg_nctrl;
-    }
-
-    // ---- a9: percentiles from the histograms
-    uint64_t C_[CT_N];
-#pragma unroll
-    for (uint32_t i = 0; i < CT_N; ++i) C_[i] = S.cget(i);
-    __syncwarp();
-    uint32_t pe[2], pt[2], pm[1];
-    const uint32_t ps[2] = {50u, 99u};
-    const uint32_t p50[1] = {50u};
-    warp_percentiles(h.e2e, BELLMAN_HIST_LAT, C_[CT_SERVED], ps, 2, pe, true);
-    uint64_t n_ttft = 0;
-    {
-      uint32_t c = 0;
-      for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) c += h.ttft[b];
-      n_ttft = __reduce_add_sync(FULL, c);
-    }
-    warp_percentiles(h.ttft, BELLMAN_HIST_LAT, n_ttft, ps, 2, pt, true);
-    warp_percentiles(h.r, BELLMAN_HIST_R, C_[CT_REWRITTEN], p50, 1, pm, false);
-    uint32_t pqa[1], pqi[1];  // NEXT-2 similarity medians
-    warp_percentiles(h.qa, BELLMAN_HIST_Q, C_[CT_REWRITTEN], p50, 1, pqa, false, 50u);
-    warp_percentiles(h.qi, BELLMAN_HIST_Q, C_[CT_ADMITTED] - C_[CT_REWRITTEN], p50, 1, pqi, false, 50u);
-    // segment merge: integer atomics, order-independent
-    unsigned long long *sh = p.seg_hist + (uint64_t)sc.segment * kSegWords;
-    for (uint32_t b = lane; b < BELLMAN_HIST_LAT; b += 32u) {
-      if (h.e2e[b]) atomicAdd(&sh[b], (unsigned long long)h.e2e[b]);
-      if (h.ttft[b]) atomicAdd(&sh[BELLMAN_HIST_LAT + b], (unsigned long long)h.ttft[b]);
-    }
-    for (uint32_t b = lane; b < BELLMAN_HIST_R; b += 32u)
-      if (h.r[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + b], (unsigned long long)h.r[b]);
-    for (uint32_t b = lane; b < BELLMAN_HIST_Q; b += 32u) {
-      if (h.qa[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + b], (unsigned long long)h.qa[b]);
-      if (h.qi[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q + b], (unsigned long long)h.qi[b]);
-    }
-
-    // ---- a8: summary record
-    if (lane == 0) {
-      bellman_scenario_stats o;
-      o.scenario_id = sid;
-      o.ticks = S.ticks;
-      o.candidates = S.last_j;
-      o.arrivals = C_[CT_ADMITTED] + queued;
-      o.admitted = C_[CT_ADMITTED];
-      o.served = C_[CT_SERVED];
-      o.rewritten = C_[CT_REWRITTEN];
-      o.words_in = C_[CT_WORDS_IN];
-      o.words_out = S.words_out;
-      o.idle_us = C_[CT_IDLE];
-      o.end_us = end;
-      o.queued_end = queued;
-      o.inflight_end = S.in_sys;
-      o.win_served = C_[CT_WIN_SERVED];
-      o.win_words_in = C_[CT_WIN_WORDS_IN];
-      o.win_words_out = S.win_words_out;
-      o.win_idle_us = C_[CT_WIN_IDLE];
-      o.sum_queue_us = C_[CT_SUM_QUEUE];
-      o.sum_ttft_us = C_[CT_SUM_TTFT];
-      o.sum_e2e_us = C_[CT_SUM_E2E];
-      o.slo_violations = C_[CT_SLO_VIOL];
-      o.e2e_p50_ms = pe[0];
-      o.e2e_p99_ms = pe[1];
-      o.ttft_p50_ms = pt[0];
-      o.ttft_p99_ms = pt[1];
-      o.median_r_bp = pm[0];
-      o.t1 = S.cold().t1;
-      o.t2 = S.cold().t2;
-      o.activations = S.cold().activations;
-      o.first_act_s = S.cold().first_act;
-      o.last_deact_s = S.cold().last_deact;
-      o.active_ingests = S.cold().active_ingests;
-      uint32_t fl = S.cold().flags | BELLMAN_FLAG_DONE;
-      if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
-      o.flags = fl;
-      o.segment = sc.segment;
-      o.bypassed = S.cold().bypassed;
-      // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
-      const double a = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WORDS_IN]);
-      const double b = __dmul_rn(pr.e_out_j_per_word, (double)S.words_out);
-      const double c = __dmul_rn(pr.p_idle_w, (double)C_[CT_IDLE]);
-      o.energy_j = __dadd_rn(__dadd_rn(a, b), __ddiv_rn(c, 1e6));
-      const double wa = __dmul_rn(pr.e_in_j_per_word, (double)C_[CT_WIN_WORDS_IN]);
-      const double wb = __dmul_rn(pr.e_out_j_per_word, (double)S.win_words_out);
-      const double wc = __dmul_rn(pr.p_idle_w, (double)C_[CT_WIN_IDLE]);
-      o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
-      o.sim_active_p50 = pqa[0];
-      o.sim_inactive_p50 = pqi[0];
-      o.scored_active = C_[CT_REWRITTEN];
-      o.scored_inactive = C_[CT_ADMITTED] - C_[CT_REWRITTEN];
-      p.stats[sid] = o;
-    }
-    __syncwarp();
-    __syncwarp();
   }
 }
 

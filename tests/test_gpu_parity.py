@@ -319,3 +319,53 @@ def test_rewrite_polynomial_paths(poly):
     bad, st = check_all(w.columns())
     _assert_ok(bad)
     assert int(st["rewritten"].sum()) > 0
+
+
+def test_next3_input_and_util_signals():
+    """NEXT-3 signals P:211 names: input words admitted per second (INPUT) and
+    decode-batch occupancy (UTIL), under MAP and STEP laws, with thresholds
+    calibrated from an OFF run recording the same signal, and in debug record
+    mode (controller log and rows compared element by element)."""
+    US = W.US
+    traces = [W.paper_trace(), W.const_trace(3.0, 400), W.const_trace(6.0, 300)]
+    profs = [W.PROFILES["P24"], W.PROFILES["L8B"], dict(W.PROFILES["P24"], max_batch=13, knee=4)]
+    ctrls = [W.OFF,
+             W.map_ctrl(15_000, 30_000, signal=W.SIG_INPUT),
+             W.map_ctrl(3_000, 7_000, signal=W.SIG_UTIL, window=3),
+             W.step_ctrl(4_000, 9_000, (500, 1000, 1500, 2000), signal=W.SIG_UTIL),
+             W.step_ctrl(20_000, 40_000, (300, 900, 2000), signal=W.SIG_INPUT),
+             W.Ctrl(W.LAW_MAP, W.SIG_INPUT, 5, 500, 2000, 0, 0, 0, 0, 1, ()),   # calibrated
+             W.Ctrl(W.LAW_MAP, W.SIG_UTIL, 5, 500, 2000, 0, 0, 0, 0, 1, ()),    # calibrated
+             W.Ctrl(W.LAW_OFF, W.SIG_INPUT, 5, 500, 2000, 0, 0, 0, 0, 0, ()),   # OFF sources
+             W.Ctrl(W.LAW_OFF, W.SIG_UTIL, 5, 500, 2000, 0, 0, 0, 0, 0, ())]
+    sc = []
+    for t in range(3):
+        for pi in range(3):
+            for ci in range(1, 5):
+                for s in range(2):
+                    rec = 2 if (s == 0 and pi == 0) else 0
+                    sc.append(W.Scenario(s, wid=t, trace=t, profile=pi, ctrl=ci, segment=0, mode=s % 2,
+                                         horizon_us=1400 * US, record=rec))
+            for src_ctrl, cal_ctrl in ((7, 5), (8, 6)):
+                src = len(sc)
+                sc.append(W.Scenario(4, wid=t, trace=t, profile=pi, ctrl=src_ctrl, segment=0,
+                                     mode=W.MODE_DRAIN, horizon_us=1400 * US, record=1))
+                sc.append(W.Scenario(4, wid=t, trace=t, profile=pi, ctrl=cal_ctrl, segment=0,
+                                     mode=W.MODE_DRAIN, horizon_us=1400 * US, calib_src=src))
+    w = W.custom(traces, profs, ctrls, sc)
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)
+    assert int(st["activations"].sum()) > 0 and int(st["rewritten"].sum()) > 0
+    # debug-recorded scenarios: rows and controller logs equal the oracle's
+    import oracle
+    from paper_2510_15330_b200 import Simulator
+
+    cols = w.columns()
+    sim = Simulator(cols, device=0)
+    sim.run()
+    b = oracle.Bound(cols)
+    for sid in [i for i, x in enumerate(sc) if x.record & 2]:
+        rows, ctrl = sim.series(sid)
+        o = oracle.run_scenario(b, sid, rows_cap=len(rows) + 8, ctrl_log_cap=len(ctrl) + 8)
+        assert [int(c["sample"]) for c in ctrl] == [e["sample"] for e in o["ctrl_log"]], sid
+    sim.close()

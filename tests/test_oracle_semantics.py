@@ -286,6 +286,54 @@ def test_ttft_signal_is_per_second_mean(orc):
     assert got == closed
 
 
+def _signal_run(orc, signal, seed, max_batch=None):
+    rng = np.random.default_rng(seed)
+    reqs = []
+    t = 0
+    for i in range(80):
+        t += int(rng.integers(0, 250_000))
+        reqs.append(dict(a_us=t, input=int(rng.integers(100, 3000)), U=int(rng.integers(2, 40))))
+    prof = dict(LIT, max_batch=max_batch) if max_batch else LIT
+    c = orc.make_ctrl(law=W.LAW_MAP, signal=signal, t1=10**9, t2=2 * 10**9)
+    return reqs, prof, orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN)
+
+
+def test_input_signal_is_admitted_words_per_second(orc):
+    """NEXT-3 signal ("input tokens per unit time to the LLM serving
+    system"): the sample of second s is the input words admitted in s; seconds
+    without an admission are gaps.  Recomputed from the per-request log."""
+    reqs, _, d = _signal_run(orc, W.SIG_INPUT, 10)
+    want = {}
+    for q, r in zip(reqs, d["requests"]):
+        want[r["admit_us"] // 10**6] = want.get(r["admit_us"] // 10**6, 0) + q["input"]
+    got = {e["second"]: e["sample"] for e in d["ctrl_log"]}
+    assert got == {s: v for s, v in want.items() if (s + 1) * 10**6 <= d["end_us"]}
+    assert len(got) > 5
+
+
+@pytest.mark.parametrize("max_batch", [3, 7])
+def test_util_signal_is_mean_batch_occupancy(orc, max_batch):
+    """NEXT-3 signal ("GPU utilization metrics"): the sample of second s is
+    the mean decode-batch occupancy over the iteration ends in s, in basis
+    points: floor(10000 sum(B) / (max_batch n)), B the number of requests
+    emitting a decode word at an end.  Iteration ends and B are rebuilt from
+    each request's first word and its TBT gaps."""
+    reqs, prof, d = _signal_run(orc, W.SIG_UTIL, 11, max_batch)
+    ends = {}
+    for r, gaps in zip(d["requests"], d["gaps"]):
+        t = r["first_us"]
+        for g in gaps:
+            t += g
+            ends[t] = ends.get(t, 0) + 1
+    per_sec = {}
+    for t, b in ends.items():
+        per_sec.setdefault(t // 10**6, []).append(b)
+    got = {e["second"]: e["sample"] for e in d["ctrl_log"]}
+    assert got == {s: 10000 * sum(v) // (max_batch * len(v)) for s, v in per_sec.items()
+                   if (s + 1) * 10**6 <= d["end_us"]}
+    assert len(got) > 5 and max(got.values()) > 10000 // max_batch
+
+
 def test_bruteforce_kv_capacity(orc):
     """NEXT-4 KV-capacity admission vs the brute-force simulator on random tiny
     traces, with and without a constant rewrite rate."""

@@ -30,7 +30,7 @@ from scipy.special import ndtri
 # enums shared *by value* with both implementations (documented in DESIGN.md)
 # ----------------------------------------------------------------------------
 LAW_OFF, LAW_CONST, LAW_MAP, LAW_STEP = 0, 1, 2, 3
-SIG_TBT, SIG_E2E, SIG_SLO, SIG_TTFT = 0, 1, 2, 3
+SIG_TBT, SIG_E2E, SIG_SLO, SIG_TTFT, SIG_INPUT, SIG_UTIL = 0, 1, 2, 3, 4, 5
 MODE_CUTOFF, MODE_DRAIN = 0, 1
 
 US = 1_000_000  # µs per second

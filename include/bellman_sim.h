@@ -122,9 +122,19 @@ typedef struct {
    * (input + realized output words) fits beside the contexts of everything in
    * the system; strict FIFO; an oversized request runs alone.  0 = unlimited. */
   uint32_t kv_cap_words;        /* <= 2^30 */
-  uint32_t _pad;
+  /* NEXT-4 prefill/decode contention (S:257 flags it as unmodelled): 0 =
+   * SPEC's non-blocking prefill (a request's prefill occupies it for
+   * prefill_time, others keep decoding); 1 = contending: the requests admitted
+   * at an iteration boundary prefill inside the next iteration, which then
+   * lasts cost(B) + sum of their prefill times (just the sum when nothing is
+   * decoding, so S:207's idle-server example holds), and emit their first word
+   * at its end. */
+  uint32_t prefill_mode;
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;
 } bellman_profile; /* 56 bytes */
+
+#define BELLMAN_PREFILL_NONBLOCKING 0u
+#define BELLMAN_PREFILL_CONTENDING 1u
 
 /* Controller configuration (R3-R5, R22, R38). */
 typedef struct {

@@ -56,6 +56,7 @@ typedef struct {
   const uint32_t *arr_L, *arr_input, *arr_cls;
   const uint32_t *prof_t0, *prof_knee, *prof_slope, *prof_kv, *prof_maxb, *prof_prefill_ns;
   const uint32_t *prof_kv_cap; /* NEXT-4: KV capacity in context words, 0 = unlimited */
+  const uint32_t *prof_prefill_mode; /* NEXT-4: 0 non-blocking prefill, 1 contending */
   const double *prof_e_in, *prof_e_out, *prof_p_idle;
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
@@ -91,6 +92,8 @@ typedef struct {
   uint32_t t0_us, knee, slope_us, kv_ns_per_word, max_batch, prefill_ns_per_word;
   double e_in, e_out, p_idle;
   uint32_t kv_cap_words; /* NEXT-4 KV-capacity admission, 0 = unlimited */
+  uint32_t prefill_mode; /* NEXT-4: 0 non-blocking; 1 contending: the requests admitted
+                            at an iteration boundary prefill inside the next iteration */
 } orc_profile;
 
 typedef struct {

@@ -36,7 +36,7 @@
 #define NEVER UINT64_MAX
 
 enum { EV_ITER_END = 0, EV_PREFILL_END = 1, EV_ARRIVAL = 2 };
-enum { RS_FUTURE = 0, RS_QUEUED, RS_PREFILL, RS_READY, RS_DECODING, RS_DONE };
+enum { RS_FUTURE = 0, RS_QUEUED, RS_PREFILL, RS_READY, RS_DECODING, RS_DONE, RS_PENDING };
 
 typedef struct {
   uint64_t t;
@@ -294,6 +294,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint32_t *queue = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
   uint32_t *ready = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
   uint32_t *batch = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
+  uint32_t *pending = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t)); /* contending prefill */
   uint64_t *e2e_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
   uint64_t *ttft_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
   uint64_t n_sec = H / US + 2;
@@ -311,7 +312,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
   cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
-  if (!rs || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
+  if (!rs || !queue || !ready || !batch || !pending || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
       !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt || !sec_in_sum ||
       !sec_in_any || !sec_util_sum || !sec_util_cnt ||
       ((cfg->record & 2) && !rows))
@@ -325,6 +326,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
 
   uint64_t q_head = 0, q_tail = 0, n_ready = 0, n_batch = 0, in_sys = 0;
   uint64_t kv_reserved = 0; /* NEXT-4: sum of (input + R) over requests in the system */
+  uint64_t n_pend = 0, pend_us = 0; /* NEXT-4 contending prefill: admitted, prefill not started */
   uint64_t n_e2e = 0, n_ttft = 0;
   int busy = 0;
   uint64_t next_sec = 0; /* first second not yet ingested */
@@ -502,8 +504,15 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         rs[m].r_bp = r;
         rs[m].R = R;
         uint64_t pf = ((uint64_t)prof->prefill_ns_per_word * req[m].input) / 1000;
-        rs[m].prefill_end = T + (pf < 1 ? 1 : pf);
-        rs[m].state = RS_PREFILL;
+        if (pf < 1) pf = 1;
+        if (prof->prefill_mode) { /* contending: prefills run inside the next iteration */
+          rs[m].state = RS_PENDING;
+          pending[n_pend++] = m;
+          pend_us += pf;
+        } else {
+          rs[m].prefill_end = T + pf;
+          rs[m].state = RS_PREFILL;
+        }
         in_sys++;
         res->admitted++;
         res->sum_queue_us += T - req[m].a_us;
@@ -527,10 +536,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           if (r > 0) { res->hist_q_active[qb]++; res->scored_active++; }
           else { res->hist_q_inactive[qb]++; res->scored_inactive++; }
         }
-        if (heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m})) goto out;
+        if (!prof->prefill_mode && heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m})) goto out;
       }
-      /* iteration start with every decode-ready request */
-      if (n_ready > 0) {
+      /* iteration start with every decode-ready request (and, contending, the
+       * prefills of everything just admitted) */
+      if (n_ready > 0 || n_pend > 0) {
         uint64_t K = 0;
         for (uint64_t b = 0; b < n_ready; ++b) {
           uint32_t m = ready[b];
@@ -541,8 +551,19 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         n_batch = n_ready;
         n_ready = 0;
         uint64_t B = n_batch;
-        uint64_t d = prof->t0_us + (uint64_t)prof->slope_us * (B > prof->knee ? B - prof->knee : 0) +
-                     ((uint64_t)prof->kv_ns_per_word * K) / 1000;
+        uint64_t d = B == 0 ? 0
+                            : prof->t0_us + (uint64_t)prof->slope_us * (B > prof->knee ? B - prof->knee : 0) +
+                                  ((uint64_t)prof->kv_ns_per_word * K) / 1000;
+        d += pend_us; /* contending prefill (NEXT-4): cost(B) + sum of the prefills */
+        for (uint64_t i = 0; i < n_pend; ++i) {
+          uint32_t m = pending[i];
+          rs[m].prefill_end = T + d;
+          rs[m].state = RS_PREFILL;
+          /* same instant as the iteration end; popped after it (kind order, R7) */
+          if (heap_push(&h, (event){T + d, EV_PREFILL_END, m})) goto out;
+        }
+        n_pend = 0;
+        pend_us = 0;
         if (heap_push(&h, (event){T + d, EV_ITER_END, 0})) goto out;
         busy = 1;
         res->ticks++;
@@ -654,7 +675,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   }
   rc = 0;
 out:
-  free(rs); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
+  free(rs); free(queue); free(ready); free(batch); free(pending); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
   free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
   free(sec_util_cnt);
@@ -675,6 +696,7 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   p->e_out = in->prof_e_out[pi];
   p->p_idle = in->prof_p_idle[pi];
   p->kv_cap_words = in->prof_kv_cap[pi];
+  p->prefill_mode = in->prof_prefill_mode[pi];
   memset(c, 0, sizeof(*c));
   c->law = in->ctrl_law[ci];
   c->signal = in->ctrl_signal[ci];

@@ -119,6 +119,11 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (p.prefill_ns_per_word > (1u << 24)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: prefill too large", i);
     if (p.kv_ns_per_word > 1024u) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_ns_per_word > 1024", i);
     if (p.kv_cap_words > (1u << 30)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_cap_words > 2^30", i);
+    if (p.prefill_mode > BELLMAN_PREFILL_CONTENDING) return fail(nullptr, BELLMAN_EINVAL, "profile %u: unknown prefill_mode", i);
+    // contending prefill: one iteration may carry max_batch prefills; keep it < 2^30 µs (32-bit clock)
+    if (p.prefill_mode == BELLMAN_PREFILL_CONTENDING &&
+        (uint64_t)p.max_batch * ((uint64_t)p.prefill_ns_per_word * 65535u / 1000u + 1u) >= (1ull << 30))
+      return fail(nullptr, BELLMAN_EINVAL, "profile %u: contending prefill: max_batch x max prefill >= 2^30 us", i);
     if (!(p.e_in_j_per_word >= 0) || !(p.e_out_j_per_word >= 0) || !(p.p_idle_w >= 0))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: negative energy coefficient", i);
   }

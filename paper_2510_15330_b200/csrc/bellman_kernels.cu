@@ -56,7 +56,8 @@ constexpr unsigned FULL = 0xffffffffu;
 // prefill < 2^31) stays below FAR32.
 constexpr uint32_t INF32 = 0xffffffffu, FAR32 = 0xfffffffeu;
 constexpr uint32_t kRebaseAt = 1u << 30, kJumpCap = 1u << 30;
-constexpr uint32_t PH_EMPTY = 0, PH_PREFILL = 1, PH_READY = 2, PH_DEC = 3, PH_OFF = 4;
+// PH_PENDING: admitted under contending prefill (NEXT-4), prefill not started
+constexpr uint32_t PH_EMPTY = 0, PH_PREFILL = 1, PH_READY = 2, PH_DEC = 3, PH_OFF = 4, PH_PENDING = 5;
 constexpr uint64_t kLn2Q32 = 2977044472ull;  // round(ln 2 * 2^32)
 
 // ---------------------------------------------------------------------------
@@ -524,6 +525,9 @@ struct Sim {
   // the selected signal is x: a compile-time answer in the TBT-only
   // instantiation (every benchmark configuration), a runtime one otherwise
   __device__ __forceinline__ bool sig(uint32_t x) const { return TBTO ? x == BELLMAN_SIG_TBT : signal == x; }
+  // contending prefill (NEXT-4): never in the TBT-specialised instantiation
+  __device__ __forceinline__ bool cont() const { return TBTO ? false : pmode != 0u; }
+  __device__ __forceinline__ uint32_t n_pending() const { return cont() ? n_pend : 0u; }
   __device__ __forceinline__ Cold &cold() const { return g_cold[kWarpsPerBlock == 1 ? 0u : wid]; }
 #ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
@@ -580,6 +584,8 @@ struct Sim {
   uint32_t sR[2], sin[2], sdn[2], sph[2];
   // ---- generator / queue head (a2)
   uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
+  uint32_t pmode;         // NEXT-4 prefill_mode (generic instantiation only)
+  uint32_t n_pend, pend_us;  // contending: admitted, prefill not started; sum of their prefill times
   uint32_t kv_res;        // NEXT-4: sum of (input + R) over requests in the system
   uint32_t adm_blocked;   // NEXT-4: the arrived queue head does not fit the KV capacity
   uint32_t head_t;     // arrival offset of the queue head (0 if before E), INF32 when none remains
@@ -888,7 +894,7 @@ struct Sim {
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
       uint64_t q_l = 0;
-      uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0;
+      uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0, pf_l = 0;
       PROF_ACC(18, pa_);
       PROF_MARK(pb_);
       // one copy of the per-request body (admissions are rare next to ticks):
@@ -933,19 +939,22 @@ struct Sim {
           }
 #endif
           const uint32_t pf = cold().buf_pf[src];
+          // contending prefill: the prefill runs inside the next iteration (start_iteration)
+          const uint32_t ph = cont() ? PH_PENDING : PH_PREFILL;
           if (s == 0) {
             sa[0] = a;
             sp[0] = Tn + pf;
             sR[0] = R;
             sin[0] = in;
-            sph[0] = PH_PREFILL;
+            sph[0] = ph;
           } else {
             sa[1] = a;
             sp[1] = Tn + pf;
             sR[1] = R;
             sin[1] = in;
-            sph[1] = PH_PREFILL;
+            sph[1] = ph;
           }
+          pf_l += pf;
           win_l += in;
           q_l += Ta - a;
           mpf = min(mpf, pf);
@@ -953,8 +962,13 @@ struct Sim {
       }
       PROF_ACC(19, pb_);
       PROF_MARK(pc_);
-      const uint32_t mnew = __reduce_min_sync(FULL, mpf);  // k >= 1 new prefills
-      if (Tn + mnew < next_pf) next_pf = Tn + mnew;
+      if (cont()) {  // host-validated: max_batch x max prefill < 2^30, no overflow
+        pend_us += __reduce_add_sync(FULL, pf_l);
+        n_pend += k;
+      } else {
+        const uint32_t mnew = __reduce_min_sync(FULL, mpf);  // k >= 1 new prefills
+        if (Tn + mnew < next_pf) next_pf = Tn + mnew;
+      }
       const uint32_t win = __reduce_add_sync(FULL, win_l);
       cadd(CT_WORDS_IN, win);
       if (sig(BELLMAN_SIG_INPUT)) {  // NEXT-3: input words admitted in the second
@@ -1105,7 +1119,21 @@ struct Sim {
       n_ready = 0;
       batch_changed();
     }
-    const uint32_t d = cbase + kq;
+    uint32_t d = cbase + kq;
+    if (cont()) {  // NEXT-4: cost(B) (nothing when B = 0) + the admitted requests' prefills
+      d = (B ? d : 0u) + pend_us;
+      if (n_pend) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+          if (sph[s] == PH_PENDING) {
+            sph[s] = PH_PREFILL;
+            sp[s] = Tn + d;  // first word at this iteration's end, after its decode words (R7)
+          }
+        next_pf = Tn + d;
+      }
+      n_pend = 0;
+      pend_us = 0;
+    }
     iter_d = d;
     iter_align = align;
     iter_end = Tn + d;
@@ -1263,6 +1291,8 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
   }
   S.buf_h = S.buf_n = 0;
+  S.pmode = pr.prefill_mode;
+  S.n_pend = S.pend_us = 0;
   S.kv_res = 0;
   S.adm_blocked = 0;
   S.last_j = 0;
@@ -1355,8 +1385,8 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     }
     // at most two passes: a join iteration whose end is quiet is ended here
     // and followed, in the same trip, by a leap and the next start
-    while (S.n_ready + S.B > 0) {
-      const bool join = S.n_ready != 0;
+    while (S.n_ready + S.B + S.n_pending() > 0) {
+      const bool join = S.n_ready + S.n_pending() != 0;
       if (!join) {
         PROF(6);
         const uint32_t t0_ = S.ticks;
@@ -1523,7 +1553,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
-    } else if (cc.signal == BELLMAN_SIG_TBT) {
+    } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING) {
       run_one<false, true>(p, sid, sc, cc, lane, h);
     } else {
       run_one<false, false>(p, sid, sc, cc, lane, h);

@@ -4,7 +4,9 @@ Deliberately the dumbest possible algorithm: it walks simulated time one
 microsecond at a time and, at every microsecond, applies the serving rules of
 SPEC.md S:245 (continuous batching) in the order fixed by S:247 / readings
 R6-R9: iteration end, prefill ends (by j), arrivals (by j), then — if the loop
-is idle — ingest, admission and iteration start.  No event heap, no
+is idle — ingest, admission and iteration start.  prof["prefill_mode"] = 1
+(NEXT-4 contention): requests admitted at a boundary prefill inside the
+next iteration, which lasts cost(B) + their prefill times (B = 0: just those).  No event heap, no
 incremental sums.  Usable only on tiny traces (<= ~2e6 µs).  Controller: the
 linear MAP law recomputed from a Fraction moving average.
 """
@@ -95,7 +97,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                     else:
                         r = Fraction(r_min) + Fraction(r_max - r_min) * (ma - t1) / (t2 - t1)
                         r_cur = min(r_max, int(r))  # floor to a basis point
-            in_sys = sum(1 for i in range(n) if st[i] in ("prefill", "ready", "decoding"))
+            in_sys = sum(1 for i in range(n) if st[i] in ("prefill", "ready", "decoding", "pending"))
             cap = prof.get("kv_cap_words", 0)
             while in_sys < prof["max_batch"] and queue:
                 m = queue[0]
@@ -107,7 +109,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                     else:
                         Rh = q["U"]
                     reserved = sum(requests[i]["input"] + R[i] for i in range(n)
-                                   if st[i] in ("prefill", "ready", "decoding"))
+                                   if st[i] in ("prefill", "ready", "decoding", "pending"))
                     if in_sys > 0 and reserved + q["input"] + Rh > cap:
                         break
                 queue.pop(0)
@@ -119,15 +121,24 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                     R[m] = max(1, int(Fraction(N) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
                 else:
                     R[m] = q["U"]
-                pf = prof["prefill_ns_per_word"] * q["input"] // 1000
-                pend[m] = t + max(1, pf)
-                st[m] = "prefill"
+                pf = max(1, prof["prefill_ns_per_word"] * q["input"] // 1000)
+                if prof.get("prefill_mode", 0):
+                    pend[m] = pf  # a duration until the iteration starts
+                    st[m] = "pending"
+                else:
+                    pend[m] = t + pf
+                    st[m] = "prefill"
                 in_sys += 1
-            if ready:
+            waiting = [m for m in range(n) if st[m] == "pending"]
+            if ready or waiting:
                 B = len(ready)
                 K = sum(requests[m]["input"] + emitted[m] for m in ready)
-                d = prof["t0_us"] + prof["slope_us"] * max(0, B - prof["knee"]) + \
+                d = 0 if B == 0 else prof["t0_us"] + prof["slope_us"] * max(0, B - prof["knee"]) + \
                     prof.get("kv_ns_per_word", 0) * K // 1000
+                d += sum(pend[m] for m in waiting)
+                for m in waiting:
+                    pend[m] = t + d
+                    st[m] = "prefill"
                 batch = list(ready)
                 for m in batch:
                     st[m] = "decoding"

@@ -369,3 +369,40 @@ def test_next3_input_and_util_signals():
         o = oracle.run_scenario(b, sid, rows_cap=len(rows) + 8, ctrl_log_cap=len(ctrl) + 8)
         assert [int(c["sample"]) for c in ctrl] == [e["sample"] for e in o["ctrl_log"]], sid
     sim.close()
+
+
+def test_next4_contending_prefill():
+    """NEXT-4 prefill/decode contention: profiles with prefill_mode = 1
+    next to non-blocking ones, under every law and several signals, with KV
+    capacity, replay and Poisson traces, ragged max_batch, 1 µs prefills,
+    calibrated pairs and debug rows."""
+    US = W.US
+    rng = np.random.default_rng(3)
+    rep = sorted((int(t), int(rng.integers(50, 900)), int(rng.integers(100, 15000)), int(rng.integers(0, 4)))
+                 for t in rng.integers(0, 600 * US, 700))
+    traces = [W.paper_trace(), W.const_trace(1.2, 500), W.const_trace(4.0, 300), {"replay": rep}]
+    C = dict(prefill_mode=1)
+    profs = [dict(W.PROFILES["P24"], **C), dict(W.PROFILES["L8B"], **C), dict(W.PROFILES["spec-literal"], **C),
+             dict(W.PROFILES["P24"], max_batch=33, knee=5, **C), dict(W.PROFILES["P24"], max_batch=1, knee=0, **C),
+             dict(W.PROFILES["L8B"], kv_cap_words=250_000, **C), dict(W.PROFILES["P24"], prefill_ns_per_word=0, **C),
+             W.PROFILES["P24"]]
+    ctrls = [W.OFF, W.map_ctrl(25_000, 60_000), W.step_ctrl(30_000, 70_000, (500, 1000, 1500, 2000)),
+             W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1200), W.map_ctrl(2_000_000, 9_000_000, signal=W.SIG_TTFT),
+             W.map_ctrl(3_000, 8_000, signal=W.SIG_UTIL), W.Ctrl(W.LAW_MAP, W.SIG_TBT, 5, 500, 2000, 0, 0, 0, 0, 1, ())]
+    sc = []
+    for t in range(4):
+        for pi in range(len(profs)):
+            for ci in range(6):
+                rec = 2 if (ci == 1 and pi in (0, 1) and t == 0) else 0
+                sc.append(W.Scenario(ci, wid=t, trace=t, profile=pi, ctrl=ci, segment=0, mode=(t + ci) % 2,
+                                     horizon_us=1400 * US, w0_us=130 * US, w1_us=500 * US, record=rec))
+            src = len(sc)
+            sc.append(W.Scenario(9, wid=t, trace=t, profile=pi, ctrl=0, segment=0, mode=W.MODE_DRAIN,
+                                 horizon_us=1400 * US, record=1))
+            sc.append(W.Scenario(9, wid=t, trace=t, profile=pi, ctrl=6, segment=0, mode=W.MODE_DRAIN,
+                                 horizon_us=1400 * US, calib_src=src))
+    w = W.custom(traces, profs, ctrls, sc)
+    w.class_cum = W.MIXED_CLASSES
+    bad, st = check_all(w.columns())
+    _assert_ok(bad)
+    assert int(st["served"].sum()) > 0 and int(st["activations"].sum()) > 0

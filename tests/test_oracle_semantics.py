@@ -373,3 +373,114 @@ def test_kv_capacity_invariant_and_fifo(orc):
         assert used <= 120_000 or len(live) == 1
     free = orc.simulate(reqs, dict(w.profiles[0], kv_cap_words=0), mode=W.MODE_DRAIN)
     assert d["sum_queue_us"] > free["sum_queue_us"]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4 contending prefill (S:257 flags prefill/decode contention as unmodelled;
+# profile prefill_mode = 1): the requests admitted at an iteration boundary
+# prefill inside the next iteration, which lasts cost(B) + their prefill times.
+
+CONT = dict(LIT, prefill_mode=1)
+
+
+def test_bruteforce_contending_prefill(orc):
+    """Contending prefill: event-heap DES == microsecond brute force on random tiny traces."""
+    rng = np.random.default_rng(23)
+    for case in range(120):
+        reqs, prof = _random_tiny(rng)
+        prof["prefill_mode"] = 1
+        law = "const" if case % 3 == 0 else "off"
+        rc = int(rng.integers(100, 3000)) if law == "const" else 0
+        if case % 4 == 1:
+            prof["kv_cap_words"] = int(rng.integers(20, 120))
+        bf = bruteforce.simulate(reqs, prof, 10**6, law=law, r_const=rc)
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=rc) if law == "const" else None
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=10**6)
+        assert (d["ticks"], d["words_out"], d["end_us"], d["served"]) == \
+               (bf["ticks"], bf["words_out"], bf["end_us"], bf["served"]), case
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i]), (case, i)
+            assert d["gaps"][i] == bf["gaps"][i], (case, i)
+
+
+def test_bruteforce_controller_contending(orc):
+    """MAP controller in the loop with contending prefill vs brute force."""
+    rng = np.random.default_rng(31)
+    prof = dict(t0_us=20_000, knee=1, slope_us=9000, kv_ns_per_word=0, max_batch=4,
+                prefill_ns_per_word=100_000, e_in=0.05, e_out=0.5, p_idle=300.0, prefill_mode=1)
+    for case in range(5):
+        reqs = []
+        t = 0
+        for i in range(14):
+            t += int(rng.integers(0, 250_000))
+            reqs.append(dict(a_us=t, input=int(rng.integers(1, 200)), U=int(rng.integers(2, 30)),
+                             P=int(rng.integers(5, 40)), fcomp_q16=65536))
+        t1, t2 = 25_000 + 4000 * case, 45_000 + 4000 * case
+        bf = bruteforce.simulate(reqs, prof, 6_000_000, law="map", t1=t1, t2=t2)
+        d = orc.simulate(reqs, prof, ctrl=orc.make_ctrl(law=W.LAW_MAP, t1=t1, t2=t2), mode=W.MODE_DRAIN,
+                         horizon_us=6_000_000)
+        assert d["ticks"] == bf["ticks"]
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"], r["r_bp"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i], bf["r_bp"][i]), (case, i)
+
+
+def test_contending_prefill_spec_example_and_hand_timeline(orc):
+    """S:207 (single request on an idle server: TTFT 800 ms, E2E 25,750 ms) holds
+    under contention; and a hand-worked two-request timeline (spec-literal
+    profile, 80 µs per input word): A (0 s, 1000 words in, 3 out), B (0.1 s, 500
+    in, 2 out).  Contending: A prefills alone [0, 80 ms); A decodes [80, 130);
+    B admitted at 130 and prefilled inside A's next iteration, 50 + 40 = 90 ms,
+    so A's second gap is 90 ms and both A's last word and B's first word land at
+    220 ms; B's word 2 at 270 ms.  Non-blocking, for contrast: B's prefill ends
+    at 170 ms mid-iteration, A completes at 180 ms, B at 230 ms."""
+    d = orc.simulate([dict(a_us=0, input=10_000, U=500)], CONT, mode=W.MODE_DRAIN)
+    r = d["requests"][0]
+    assert (r["first_us"], r["done_us"]) == (800_000, 25_750_000)
+    reqs = [dict(a_us=0, input=1000, U=3), dict(a_us=100_000, input=500, U=2)]
+    c = orc.simulate(reqs, CONT, mode=W.MODE_DRAIN)
+    a, b = c["requests"]
+    assert (a["admit_us"], a["first_us"], a["done_us"]) == (0, 80_000, 220_000)
+    assert c["gaps"][0] == [50_000, 90_000]
+    assert (b["admit_us"], b["first_us"], b["done_us"]) == (130_000, 220_000, 270_000)
+    assert c["gaps"][1] == [50_000]
+    assert c["ticks"] == 4  # the prefill-only iteration at 0 counts
+    n = orc.simulate(reqs, LIT, mode=W.MODE_DRAIN)
+    a, b = n["requests"]
+    assert (a["done_us"], b["first_us"], b["done_us"]) == (180_000, 170_000, 230_000)
+    assert n["gaps"][1] == [60_000]
+
+
+def test_contending_gap_is_cost_plus_admitted_prefills(orc):
+    """Closed form from the request log: with no batch slowdown (knee =
+    max_batch) and no KV term, every decode gap under contention equals t0 plus
+    the prefill times of the requests whose first word lands at the gap's end;
+    and the mean TBT rises with the arrival rate (the load signal the paper's
+    controller relies on), while it stays near t0 without contention."""
+    prof = dict(CONT, knee=CONT["max_batch"], kv_ns_per_word=0)
+    rng = np.random.default_rng(5)
+    means = []
+    for rate in (0.5, 1.0, 2.0, 3.0):
+        reqs, t = [], 0
+        for i in range(150):
+            t += int(rng.exponential(1e6 / rate))
+            reqs.append(dict(a_us=t, input=int(rng.integers(500, 6000)), U=int(rng.integers(5, 60))))
+        d = orc.simulate(reqs, prof, mode=W.MODE_DRAIN)
+        pf = [max(1, prof["prefill_ns_per_word"] * q["input"] // 1000) for q in reqs]
+        first_at = {}
+        for i, r in enumerate(d["requests"]):
+            first_at.setdefault(r["first_us"], []).append(i)
+        gaps = []
+        for i, r in enumerate(d["requests"]):
+            t = r["first_us"]
+            for g in d["gaps"][i]:
+                t += g
+                assert g == prof["t0_us"] + sum(pf[j] for j in first_at.get(t, [])), (rate, i)
+                gaps.append(g)
+        means.append(sum(gaps) / len(gaps))
+        nb = orc.simulate(reqs, dict(prof, prefill_mode=0), mode=W.MODE_DRAIN)
+        assert nb["tbt_sum_us"] / nb["tbt_samples"] < 1.5 * prof["t0_us"]
+    assert means == sorted(means) and means[-1] > 2 * means[0]

@@ -26,6 +26,13 @@
 #ifdef BELLMAN_PROFILE_COUNTERS
 // Development-only event counters (separate build, never the product .so).
 __device__ unsigned long long g_prof[24];
+// per-scenario [start, end) of run_one in %globaltimer ns (scenario ids < 2^16)
+__device__ unsigned long long g_span[2 << 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define PROF(i) (prof_[i]++)
 // cycles spent in a handler (clock64 deltas; a profiling build only)
 #define PROFC(i, stmt)                               \
@@ -140,6 +147,17 @@ __device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1
 // Cold per-scenario state: touched at events (admissions, completions,
 // ingests, refills), not per iteration.  Lives in shared memory, one per warp,
 // so the event loop keeps its hot state in registers without spilling.
+// One queued request in the arrival lookahead buffer (32 bytes).
+struct alignas(16) QEnt {
+  uint64_t a;    // arrival time (absolute µs)
+  uint32_t in;   // input words | request class << 16 (NEXT-3)
+  uint32_t U;    // realized unbounded length
+  uint32_t P;    // predicted length
+  uint32_t fcq;  // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
+  uint32_t pf;   // prefill duration max(1, floor(prefill_ns * input / 1000)) µs
+  uint32_t j;    // candidate index
+};
+
 struct alignas(16) Cold {
   const DevSeg *segs;
   uint64_t gen_tau;
@@ -159,16 +177,11 @@ struct alignas(16) Cold {
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t pf_ns;                             // prefill ns per input word
   uint32_t ring[8];   // last `window` per-second samples (a6)
-  // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
-  // entry i written by lane i at refill, read by index at admission
-  uint64_t buf_a[32];    // arrival time
-  uint32_t buf_in[32];   // input words | request class << 16 (NEXT-3)
-  uint32_t buf_U[32];    // realized unbounded length
-  uint32_t buf_P[32];    // predicted length
-  uint32_t buf_fcq[32];  // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
-  uint32_t buf_j[32];    // candidate index
-  uint32_t buf_pf[32];   // prefill duration max(1, floor(prefill_ns * input / 1000)) µs
   uint32_t rungs[8];  // word-limit ladder (R5)
+  // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
+  // entry i written by lane i at refill, read whole (two 16-byte broadcasts)
+  // by every lane at admission
+  QEnt q[32];
 
 };
 
@@ -256,37 +269,6 @@ enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL 
 __shared__ Cold g_cold[kWarpsPerBlock];
 __shared__ WarpHist g_hist[kWarpsPerBlock];
 
-// NEXT-4 KV-capacity admission: of the first k arrived candidates (entries
-// buf_h.. of the shared buffer, FIFO), the leading run whose whole contexts
-// (input + realized output under r) fit beside `res` reserved words; an
-// oversized head enters an empty system.  Returns (count | added words << 32).
-// Out of line: only profiles with a KV capacity take this branch.
-__device__ __noinline__ uint64_t kv_admit(const Params &p, uint32_t wid, uint32_t lane, uint32_t buf_h, uint32_t k,
-                                          uint32_t r, uint32_t bmask, uint32_t minw, uint32_t kvcap, uint32_t res,
-                                          uint32_t in_sys) {
-  const Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
-  uint32_t need = 0;
-  if (lane < k) {
-    const uint32_t e = buf_h + lane;
-    const uint32_t inc = c.buf_in[e], P = c.buf_P[e];
-    const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
-    need = (inc & 0xFFFFu) + realized_len(p, c.buf_U[e], P, c.buf_fcq[e], byp ? 0u : r);
-  }
-  uint32_t incl = need;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= (uint32_t)o) incl += y;
-  }
-  const bool fits = lane < k && ((uint64_t)res + incl <= kvcap || (lane == 0 && in_sys == 0));
-  const uint32_t fm = __ballot_sync(FULL, fits);
-  const uint32_t kk = (uint32_t)__ffs(~fm) - 1u;  // leading run of fitting candidates
-  const uint32_t n = kk < k ? kk : k;
-  const uint32_t add = n ? __shfl_sync(FULL, incl, n - 1u) : 0u;
-  return (uint64_t)n | ((uint64_t)add << 32);
-}
-
-
 // ---------------------------------------------------------------------------
 // a2 + a3: refill the warp's shared arrival buffer with the next accepted
 // candidates (P:183 Poisson arrivals, S:83 thinning; R17, R32, R33).  Lane l
@@ -315,16 +297,17 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
       const uint32_t jj = gen_j + lane;
       const bellman_arrival A = p.arrivals[c.rep_off + jj];
       const uint64_t tau = (uint64_t)A.a_us;
-      c.buf_a[lane] = tau;
-      c.buf_in[lane] = A.input_words | (A.cls << 16);
-      c.buf_pf[lane] = prefill_us(c.pf_ns, A.input_words);
-      c.buf_j[lane] = jj;
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
       const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
-      c.buf_U[lane] = U < 1 ? 1u : (uint32_t)U;
       const int32_t P0 = (int32_t)A.L_words + __ldg(&p.tabN[v.y >> 20]);
-      c.buf_P[lane] = P0 < 1 ? 1u : (uint32_t)P0;
-      c.buf_fcq[lane] = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      QEnt &q = c.q[lane];
+      q.a = tau;
+      q.in = A.input_words | (A.cls << 16);
+      q.U = U < 1 ? 1u : (uint32_t)U;
+      q.P = P0 < 1 ? 1u : (uint32_t)P0;
+      q.fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      q.pf = prefill_us(c.pf_ns, A.input_words);
+      q.j = jj;
       if (DBG && dbg && tau < H) {
         const uint64_t sidx = tau / kUs;
         atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
@@ -382,16 +365,17 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
       const uint32_t x = u.z & 0xFFFFFu;  // class draw from the bits below L's index (NEXT-3)
       const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
       const uint32_t in = (uint32_t)__ldg(&p.tabI[u.w >> 20]);
-      c.buf_a[e] = tau;
-      c.buf_in[e] = in | (cls << 16);
-      c.buf_pf[e] = prefill_us(c.pf_ns, in);
-      c.buf_j[e] = jj;
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);  // a3: the request's own draws
       const uint64_t U = ((uint64_t)L * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
-      c.buf_U[e] = U < 1 ? 1u : (uint32_t)U;
       const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
-      c.buf_P[e] = P0 < 1 ? 1u : (uint32_t)P0;
-      c.buf_fcq[e] = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      QEnt &q = c.q[e];
+      q.a = tau;
+      q.in = in | (cls << 16);
+      q.U = U < 1 ? 1u : (uint32_t)U;
+      q.P = P0 < 1 ? 1u : (uint32_t)P0;
+      q.fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+      q.pf = prefill_us(c.pf_ns, in);
+      q.j = jj;
       if (DBG && dbg && tau < H) {
         const uint64_t sidx = tau / kUs;
         atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
@@ -602,7 +586,7 @@ struct Sim {
   __device__ __forceinline__ void refill(const Params &p) {
     buf_h = 0;
     buf_n = refill_buffer<DBG>(p, wid, lane, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u);
-    head_t = buf_n ? rel(cold().buf_a[0]) : INF32;
+    head_t = buf_n ? rel(cold().q[0].a) : INF32;
   }
 
   // ------------------------------------------------------------------ a6
@@ -657,7 +641,7 @@ struct Sim {
     if (sec_bound != INF32) sec_bound -= D;
     sp[0] -= D;
     sp[1] -= D;
-    head_t = buf_h < buf_n ? rel(cold().buf_a[buf_h]) : INF32;
+    head_t = buf_h < buf_n ? rel(cold().q[buf_h].a) : INF32;
     Hr = rel(cold().H);
     update_window();
   }
@@ -866,149 +850,125 @@ struct Sim {
   }
 
   // ------------------------------------------------------------------ a7 (+a3)
+  // FIFO admission at an admission point (R7): the queue head is admitted while
+  // a slot is free and it has arrived (and, NEXT-4, its context fits the KV
+  // capacity).  One request at a time, warp-uniformly: every lane reads the
+  // head entry (shared-memory broadcast) and computes the same rewrite and
+  // statistics, so no reduction is needed; the lane owning the first free slot
+  // stores it.  Admission points almost always admit one request.
   // Precondition: in_sys < maxb and head_t <= T.
   __device__ __forceinline__ void admit(const Params &p, WarpHist &h) {
     const uint32_t Tn = T;
     const uint64_t Ta = ab(Tn);
     adm_blocked = 0;
-    for (;;) {
-      PROF_MARK(pa_);
-      const uint32_t arrived = __ballot_sync(FULL, lane >= buf_h && lane < buf_n && cold().buf_a[lane] <= Ta);
-      const uint32_t na = __popc(arrived);
-      const uint32_t room = maxb - in_sys;
-      uint32_t k = na < room ? na : room;
-      // NEXT-3 bypass rules, read once per admission point
-      const uint32_t bmask = cold().bypass_mask, minw = cold().min_words, kvcap = cold().kv_cap;
-      uint32_t kv_add = 0;
+    uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY), f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
+    uint32_t n = 0, n_byp = 0;
+    PROF_MARK(pa_);
+    do {
+      const QEnt &e = cold().q[buf_h];
+      const uint64_t a = e.a;
+      const uint32_t inc = e.in, U = e.U, P = e.P, fcq = e.fcq;
+      const uint32_t in = inc & 0xFFFFu;
+      // r applied to this request: the warp-uniform r unless a bypass rule holds
+      // (NEXT-3)
+      const bool byp = r > 0 && (((cold().bypass_mask >> (inc >> 16)) & 1u) || P < cold().min_words);
+      const uint32_t ra = byp ? 0u : r;
+      const uint32_t R = realized_len(p, U, P, fcq, ra);  // a7 rewrite
+      const uint32_t kvcap = cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
-        const uint64_t kr2 = kv_admit(p, wid, lane, buf_h, k, r, bmask, minw, kvcap, kv_res, in_sys);
-        k = (uint32_t)kr2;
-        kv_add = (uint32_t)(kr2 >> 32);
-        if (k == 0) {
+        // NEXT-4: the whole context (input + realized output) must fit beside
+        // the contexts in the system; an oversized head enters an empty system
+        const uint32_t need = in + R;
+        if ((uint64_t)kv_res + need > kvcap && in_sys != 0u) {
           adm_blocked = 1;
           break;
         }
+        kv_res += need;
       }
-      const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY);
-      const uint32_t f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
-      const uint32_t lt = (1u << lane) - 1u;
-      const uint32_t rank0 = __popc(f0 & lt), rank1 = __popc(f0) + __popc(f1 & lt);
-      uint64_t q_l = 0;
-      uint32_t win_l = 0, mpf = 0xffffffffu, n_rw = 0, n_byp = 0, pf_l = 0;
-      PROF_ACC(18, pa_);
-      PROF_MARK(pb_);
-      // one copy of the per-request body (admissions are rare next to ticks):
-      // slot s is selected by value, not by unrolling
-#pragma unroll 1
-      for (int s = 0; s < 2; ++s) {
-        const uint32_t rank = s == 0 ? rank0 : rank1;
-        const bool mine = (s == 0 ? (f0 >> lane) & 1u : (f1 >> lane) & 1u) && rank < k;
-        if (mine) {
-          const uint32_t src = buf_h + rank;  // < buf_n <= 32
-          const uint64_t a = cold().buf_a[src];
-          const uint32_t inc = cold().buf_in[src], U = cold().buf_U[src], P = cold().buf_P[src];
-          const uint32_t fcq = cold().buf_fcq[src];
-          const uint32_t in = inc & 0xFFFFu;
-          // r applied to this request: the warp-uniform r unless a bypass rule holds
-          const bool byp = r > 0 && (((bmask >> (inc >> 16)) & 1u) || P < minw);
-          const uint32_t ra = byp ? 0u : r;
-          n_byp += byp;
-          const uint32_t R = realized_len(p, U, P, fcq, ra);  // a7 rewrite
-          if (ra > 0) {
-            n_rw++;
-            atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
-          }
+      n_byp += byp;
+      if (ra > 0) {
+        cadd(CT_REWRITTEN, 1u);
+        if (lane == 0) atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
+      }
 #ifndef BELLMAN_AB_NOQ
-          {  // NEXT-2: similarity vs the unbounded length
-            int32_t base = (int32_t)p.q_inactive;
-            if (ra > 0) {
-              const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
-              if (num <= (int64_t)p.q_safe * den) {
-                base = (int32_t)p.q_active;
-              } else if (num >= (int64_t)p.q_end * den) {
-                base = (int32_t)p.q_floor;
-              } else {
-                base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
-                                 (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
-              }
-            }
-            int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
-            sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
-            const uint32_t qb = (uint32_t)sc / 50u;
-            atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
-          }
-#endif
-          const uint32_t pf = cold().buf_pf[src];
-          // contending prefill: the prefill runs inside the next iteration (start_iteration)
-          const uint32_t ph = cont() ? PH_PENDING : PH_PREFILL;
-          if (s == 0) {
-            sa[0] = a;
-            sp[0] = Tn + pf;
-            sR[0] = R;
-            sin[0] = in;
-            sph[0] = ph;
+      {  // NEXT-2: similarity vs the unbounded length
+        int32_t base = (int32_t)p.q_inactive;
+        if (ra > 0) {
+          const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
+          if (num <= (int64_t)p.q_safe * den) {
+            base = (int32_t)p.q_active;
+          } else if (num >= (int64_t)p.q_end * den) {
+            base = (int32_t)p.q_floor;
           } else {
-            sa[1] = a;
-            sp[1] = Tn + pf;
-            sR[1] = R;
-            sin[1] = in;
-            sph[1] = ph;
+            base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
+                             (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
           }
-          pf_l += pf;
-          win_l += in;
-          q_l += Ta - a;
-          mpf = min(mpf, pf);
+        }
+        int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+        const uint32_t qb = (uint32_t)sc / 50u;
+        if (lane == 0) atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
+      }
+#endif
+      const uint32_t pf = e.pf;
+      // the first free slot: lowest lane of slot row 0, then of row 1
+      const bool s1 = f0 == 0u;
+      const uint32_t fm = s1 ? f1 : f0;
+      const uint32_t sl = (uint32_t)__ffs(fm) - 1u;
+      if (s1) f1 = fm & (fm - 1u); else f0 = fm & (fm - 1u);
+      // contending prefill: the prefill runs inside the next iteration (start_iteration)
+      const uint32_t ph = cont() ? PH_PENDING : PH_PREFILL;
+      if (lane == sl) {
+        if (!s1) {
+          sa[0] = a;
+          sp[0] = Tn + pf;
+          sR[0] = R;
+          sin[0] = in;
+          sph[0] = ph;
+        } else {
+          sa[1] = a;
+          sp[1] = Tn + pf;
+          sR[1] = R;
+          sin[1] = in;
+          sph[1] = ph;
         }
       }
-      PROF_ACC(19, pb_);
-      PROF_MARK(pc_);
       if (cont()) {  // host-validated: max_batch x max prefill < 2^30, no overflow
-        pend_us += __reduce_add_sync(FULL, pf_l);
-        n_pend += k;
-      } else {
-        const uint32_t mnew = __reduce_min_sync(FULL, mpf);  // k >= 1 new prefills
-        if (Tn + mnew < next_pf) next_pf = Tn + mnew;
+        pend_us += pf;
+        n_pend++;
+      } else if (Tn + pf < next_pf) {
+        next_pf = Tn + pf;
       }
-      const uint32_t win = __reduce_add_sync(FULL, win_l);
-      cadd(CT_WORDS_IN, win);
+      cadd(CT_WORDS_IN, in);
+      if (win_now) cadd(CT_WIN_WORDS_IN, in);
+      cadd(CT_SUM_QUEUE, Ta - a);
       if (sig(BELLMAN_SIG_INPUT)) {  // NEXT-3: input words admitted in the second
-        acc_sum += win;
+        acc_sum += in;
         acc_cnt = 1u;
       }
-      if (win_now) cadd(CT_WIN_WORDS_IN, win);
-      const uint64_t sq = warp_sum_split(q_l);
-      cadd(CT_SUM_QUEUE, sq);
       if (DBG && dbg && lane == 0) {
-        atomicAdd(&row(Ta)->admitted, k);
-        atomicAdd(&row(Ta)->words_in, win);
-        atomicAdd((unsigned long long *)&row(Ta)->sum_queue_us, (unsigned long long)sq);
+        atomicAdd(&row(Ta)->admitted, 1u);
+        atomicAdd(&row(Ta)->words_in, in);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_queue_us, (unsigned long long)(Ta - a));
       }
-      if (DBG) __syncwarp();
-      if (r > 0) {
-        cadd(CT_REWRITTEN, __reduce_add_sync(FULL, n_rw));
-        const uint32_t nb = __reduce_add_sync(FULL, n_byp);
-        if (nb) {
-          if (lane == 0) cold().bypassed += nb;
-          __syncwarp();
-        }
-      }
-      PROF_ACC(20, pc_);
-      PROF_MARK(pd_);
-      last_j = cold().buf_j[buf_h + k - 1u] + 1u;
-      kv_res += kv_add;
-      in_sys += k;
-      cadd(CT_ADMITTED, k);
-      buf_h += k;
-      if (buf_h < buf_n) {
-        head_t = rel(cold().buf_a[buf_h]);
+      n++;
+      in_sys++;
+      last_j = e.j + 1u;
+      if (++buf_h < buf_n) {
+        head_t = rel(cold().q[buf_h].a);
       } else if (!cold().gen_done) {
         refill(p);
       } else {
         head_t = INF32;
       }
-      PROF_ACC(21, pd_);
-      if (in_sys >= maxb || head_t > Tn) break;
+    } while (in_sys < maxb && head_t <= Tn);
+    PROF_ACC(19, pa_);
+    cadd(CT_ADMITTED, n);
+    if (n_byp) {
+      if (lane == 0) cold().bypassed += n_byp;
+      __syncwarp();
     }
+    if (DBG) __syncwarp();
   }
 
   // ------------------------------------------------------------------ a4/a5 leap
@@ -1419,6 +1379,9 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   }
   if (S.sec_bound != INF32 && S.ab(S.sec_bound) <= end && S.acc_cnt) S.ingest();
   // queued at the end: accepted arrivals before `end` not admitted
+#ifdef BELLMAN_PROFILE_COUNTERS
+  const long long epi0_ = clock64();
+#endif
   uint64_t queued = 0;
   for (;;) {
     if (S.buf_h >= S.buf_n) {
@@ -1426,10 +1389,10 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
       S.refill(p);
       continue;
     }
-    const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().buf_a[lane] < end);
+    const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().q[lane].a < end);
     const uint32_t nq = __popc(m);
     queued += nq;
-    if (nq) S.last_j = S.cold().buf_j[31 - __clz(m)] + 1u;
+    if (nq) S.last_j = S.cold().q[31 - __clz(m)].j + 1u;
     if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
     S.buf_h = S.buf_n;
   }
@@ -1440,6 +1403,9 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     p.dbg_n[2 * dslot + 1] = S.cold().dbg_nctrl;
   }
 
+#ifdef BELLMAN_PROFILE_COUNTERS
+  const long long epi1_ = clock64();
+#endif
   // ---- a9: percentiles from the histograms
   uint64_t C_[CT_N];
 #pragma unroll
@@ -1473,6 +1439,12 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     if (h.qi[b]) atomicAdd(&sh[2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q + b], (unsigned long long)h.qi[b]);
   }
 
+#ifdef BELLMAN_PROFILE_COUNTERS
+  if (lane == 0) {
+    atomicAdd(&g_prof[22], (unsigned long long)(epi1_ - epi0_));
+    atomicAdd(&g_prof[23], (unsigned long long)(clock64() - epi1_));
+  }
+#endif
   // ---- a8: summary record
   if (lane == 0) {
     bellman_scenario_stats o;
@@ -1551,6 +1523,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     // debug-recorded scenarios run in the DBG instantiation, all others in the product one
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
+#ifdef BELLMAN_PROFILE_COUNTERS
+    if (lane == 0 && sid < (1u << 16)) g_span[2 * sid] = gtimer();
+#endif
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING) {
@@ -1558,6 +1533,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     } else {
       run_one<false, false>(p, sid, sc, cc, lane, h);
     }
+#ifdef BELLMAN_PROFILE_COUNTERS
+    if (lane == 0 && sid < (1u << 16)) g_span[2 * sid + 1] = gtimer();
+#endif
   }
 }
 
@@ -1601,6 +1579,9 @@ __global__ void bellman_calibrate_kernel(const Params p, uint32_t n_slots) {
 #ifdef BELLMAN_PROFILE_COUNTERS
 extern "C" int bellman_debug_prof(unsigned long long *out) {
   return (int)cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 24);
+}
+extern "C" int bellman_debug_span(unsigned long long *out, unsigned n) {
+  return (int)cudaMemcpyFromSymbol(out, g_span, sizeof(unsigned long long) * 2 * (n < (1u << 16) ? n : (1u << 16)));
 }
 #endif
 

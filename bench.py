@@ -88,6 +88,17 @@ def algorithmic_ops(st) -> float:
     return A_TICK * ticks + A_CAND * cand + A_ADMIT * adm + A_DONE * done + A_SEC * secs + A_PF * adm
 
 
+def ncu_traffic(name: str):
+    """DRAM bytes (read + write) per tick-kernel launch of this workload, from
+    the committed summary of one `ncu --set full` capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)[name]
+        return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), t["source"]
+    except Exception:
+        return None, None
+
+
 def peaks():
     p = {"hbm_gbs": 6457.7, "sm_max_mhz": 1965.0, "src": "fallback"}
     try:
@@ -327,6 +338,7 @@ def main():
     kern_s = kern_tot / 1e3 / args.steps
     achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G warp-inst/s
     peak = 148 * 4 * mhz * 1e6 / 1e9
+    traffic, traffic_src = ncu_traffic(args.workload)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(workload(1, args.seeds_per_gpu, args.workload).columns())
@@ -338,9 +350,10 @@ def main():
                    "scenarios_per_gpu": count, "scenarios_total": n, "ticks_per_step": int(ticks_all),
                    "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
                      "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time; peak = 148 SM x 4 "
-                             f"issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max)"},
+                             f"issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM bytes per launch "
+                             f"({traffic_src or 'no capture'})"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,

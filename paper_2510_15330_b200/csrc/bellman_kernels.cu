@@ -112,6 +112,16 @@ __device__ __forceinline__ uint32_t lat_bin(uint64_t ms) {
   if (e > 31) return BELLMAN_HIST_LAT - 1;
   return 32u * (e - 4u) + ((uint32_t)(ms >> (e - 5u)) & 31u);
 }
+// latency bin of a value in µs: floor(us / 1000) ms, in 32 bits when it fits
+__device__ __forceinline__ uint32_t lat_bin_us(uint64_t us) {
+  if ((us >> 32) == 0) {
+    const uint32_t ms = (uint32_t)us / 1000u;
+    if (ms < 32) return ms;
+    const uint32_t e = 31u - (uint32_t)__clz(ms);
+    return 32u * (e - 4u) + ((ms >> (e - 5u)) & 31u);
+  }
+  return lat_bin(us / 1000u);
+}
 __device__ __forceinline__ uint32_t lat_edge(uint32_t b) {
   if (b < 32) return b;
   const uint32_t e = b / 32u + 4u, s = b % 32u;
@@ -404,6 +414,13 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
   return n;
 }
 
+// floor(a / b), b > 0: a 32-bit division when both fit (the per-second means
+// and the law's quotient almost always do), else the 64-bit routine.
+__device__ __forceinline__ uint64_t div_u64(uint64_t a, uint64_t b) {
+  if (((a | b) >> 32) == 0) return (uint32_t)a / (uint32_t)b;
+  return a / b;
+}
+
 // ---------------------------------------------------------------------------
 // a6: one controller ingest of the closed second ending at sec_bound, whose
 // sample is the integer mean x = floor(acc_sum / acc_cnt) (P:134, P:193,
@@ -419,7 +436,7 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
   // the sample: floor(acc_sum / acc_cnt) truncated to 32 bits (as the oracle); UTIL
   // keeps sum B / count and scales once here: floor(10000 sum B / (max_batch count))
   const uint32_t x = util_maxb ? (uint32_t)(10000u * acc_sum / ((uint64_t)util_maxb * acc_cnt))
-                               : (uint32_t)(acc_sum / acc_cnt);
+                               : (uint32_t)div_u64(acc_sum, acc_cnt);
   if (c.series) {
     const uint32_t n = c.series_n;
     if (lane == 0) {
@@ -447,7 +464,7 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
   if (act) {
     if (law == BELLMAN_LAW_MAP) {
       const uint32_t rmin = c.rmin, rmax = c.rmax;
-      uint64_t rr = rmin + ((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1)) / ((uint64_t)k * (c.t2 - t1));
+      uint64_t rr = rmin + div_u64((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1), (uint64_t)k * (c.t2 - t1));
       if (rr > rmax) rr = rmax;
       nr = (uint32_t)rr;
       const uint32_t nrungs = c.nrungs;
@@ -604,7 +621,9 @@ struct Sim {
     }
     acc_sum = 0;
     acc_cnt = 0;
-    sec_bound = rel((ab(t) / kUs + 1u) * kUs);
+    // the second containing t: usually the next one (no division)
+    const uint32_t nb = sec_bound + (uint32_t)kUs;
+    sec_bound = (t < nb && nb < FAR32) ? nb : rel((ab(t) / kUs + 1u) * kUs);
   }
 
   // debug row of the second containing absolute instant ta
@@ -662,7 +681,7 @@ struct Sim {
     kstep_r = ks - kstep_q * 1000u;
   }
   __device__ __forceinline__ void kv_add(uint64_t x) {  // kv K += x
-    const uint64_t q = x / 1000u;
+    const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
     kr += (uint32_t)(x - q * 1000u);
     kq += (uint32_t)q;
     if (kr >= 1000u) {
@@ -671,7 +690,7 @@ struct Sim {
     }
   }
   __device__ __forceinline__ void kv_sub(uint64_t x) {  // kv K -= x
-    const uint64_t q = x / 1000u;
+    const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
     const uint32_t rem = (uint32_t)(x - q * 1000u);
     kq -= (uint32_t)q;
     if (kr < rem) {
@@ -748,7 +767,7 @@ struct Sim {
           e2e_l += e;
           nslo += e > slo_us;
           kdrop += sin[s] + sR[s];
-          atomicAdd(&h.e2e[lat_bin(e / 1000u)], 1u);
+          atomicAdd(&h.e2e[lat_bin_us(e)], 1u);
           sph[s] = PH_EMPTY;
         }
         if (sph[s] == PH_DEC) dmin = min(dmin, sdn[s]);
@@ -795,7 +814,7 @@ struct Sim {
       nfirst += __popc(__ballot_sync(FULL, f));
       if (f) {
         const uint64_t tt = ab(sp[s]) - sa[s];
-        const uint32_t lb = lat_bin(tt / 1000u);
+        const uint32_t lb = lat_bin_us(tt);
         ttft_l += tt;
         atomicAdd(&h.ttft[lb], 1u);
         if (sR[s] == 1u) {  // R9: completes at the prefill end

@@ -19,6 +19,7 @@
 // No floating point except the final fp64 energy (IEEE _rn intrinsics, no FMA).
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "bellman_internal.cuh"
@@ -154,9 +155,6 @@ __device__ __forceinline__ uint32_t lane_pinned() {
 // this warp's index in its CTA (a constant 0 with one warp per CTA)
 __device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1 ? 0u : threadIdx.x >> 5; }
 
-// Cold per-scenario state: touched at events (admissions, completions,
-// ingests, refills), not per iteration.  Lives in shared memory, one per warp,
-// so the event loop keeps its hot state in registers without spilling.
 // One queued request in the arrival lookahead buffer (32 bytes).
 struct alignas(16) QEnt {
   uint64_t a;    // arrival time (absolute µs)
@@ -168,32 +166,42 @@ struct alignas(16) QEnt {
   uint32_t j;    // candidate index
 };
 
+// Cold per-scenario state: touched at events (admissions, completions,
+// ingests, refills), not per iteration.  Lives in shared memory, one per warp,
+// so the event loop keeps its hot state in registers without spilling.
 struct alignas(16) Cold {
+  // a6 controller state, in 16-byte groups read with one LDS.128 each (g0..g4)
+  uint64_t ringA;                                       // g0: window sum A,
+  uint32_t ring_n, ring_pos;                            //     samples k, ring position
+  uint32_t rung, active, activations, active_ingests;   // g1
+  uint32_t first_act, last_deact, law, window;          // g2
+  uint32_t t1, t2, rmin, rmax;                          // g3
+  uint32_t *series;                                     // g4: recorded series (a10) or NULL,
+  uint32_t series_n, series_cap;                        //     samples written, capacity
+  uint32_t ring[8];   // last `window` per-second samples (a6)
+  uint32_t rungs[8];  // word-limit ladder (R5)
+  uint32_t nrungs, flags, dbg_cap, dbg_nctrl;
   const DevSeg *segs;
   uint64_t gen_tau;
-  uint64_t ringA;
   uint64_t w0, w1;
   uint64_t H;  // horizon (absolute µs)
-  uint32_t *series;
   bellman_ctrl_row *dbg_ctrl;
   uint32_t n_seg, gen_seg, gen_fresh, gen_j, gen_acc, gen_cap, gen_done;
   uint32_t replay;  // NEXT-4: the trace is an explicit arrival list (segs unused)
   uint32_t rep_off;
-  uint32_t law, window, rmin, rmax, t1, t2, nrungs, ring_n, ring_pos, rung, active;
-  uint32_t activations, first_act, last_deact, active_ingests;
-  uint32_t series_cap, series_n, flags, dbg_cap, dbg_nctrl;
   uint32_t k0, wid_lo, wid_hi;
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t pf_ns;                             // prefill ns per input word
-  uint32_t ring[8];   // last `window` per-second samples (a6)
-  uint32_t rungs[8];  // word-limit ladder (R5)
   // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
   // entry i written by lane i at refill, read whole (two 16-byte broadcasts)
   // by every lane at admission
   QEnt q[32];
 
 };
+static_assert(offsetof(Cold, ringA) == 0 && offsetof(Cold, rung) == 16 && offsetof(Cold, first_act) == 32 &&
+                  offsetof(Cold, t1) == 48 && offsetof(Cold, series) == 64 && offsetof(Cold, ring) == 80,
+              "controller state groups g0..g4 of Cold");
 
 // a7 rewrite (R11): realized length of a request whose
 // predicted length is P and compliance factor in fcq under r > 0:
@@ -432,26 +440,28 @@ template <bool DBG>
 __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
                                                uint32_t acc_cnt, uint32_t r_cur, bool dbg, uint32_t util_maxb) {
   Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
-  const uint32_t second = (uint32_t)(sec_bound / kUs - 1u);
+  // the whole controller state in five independent 16-byte loads
+  const uint4 *g = reinterpret_cast<const uint4 *>(&c.ringA);
+  const uint4 g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4];
   // the sample: floor(acc_sum / acc_cnt) truncated to 32 bits (as the oracle); UTIL
   // keeps sum B / count and scales once here: floor(10000 sum B / (max_batch count))
   const uint32_t x = util_maxb ? (uint32_t)(10000u * acc_sum / ((uint64_t)util_maxb * acc_cnt))
                                : (uint32_t)div_u64(acc_sum, acc_cnt);
-  if (c.series) {
-    const uint32_t n = c.series_n;
+  uint32_t *const series = reinterpret_cast<uint32_t *>((uint64_t)g4.x | ((uint64_t)g4.y << 32));
+  if (series) {
+    const uint32_t n = g4.z;
     if (lane == 0) {
-      if (n < c.series_cap) c.series[n] = x;
+      if (n < g4.w) series[n] = x;
       else c.flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
       c.series_n = n + 1u;
     }
     __syncwarp();
   }
-  const uint32_t law = c.law;
+  const uint32_t law = g2.z, window = g2.w;
   if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return r_cur;
-  const uint32_t window = c.window, pos = c.ring_pos, t1 = c.t1;
-  uint32_t k = c.ring_n, rung = c.rung;
-  const uint32_t was_active = c.active;
-  uint64_t A = c.ringA;
+  const uint32_t pos = g0.w, t1 = g3.x, was_active = g1.y;
+  uint32_t k = g0.z, rung = g1.x;
+  uint64_t A = (uint64_t)g0.x | ((uint64_t)g0.y << 32);
   const uint32_t ev = c.ring[pos];
   if (k < window) {
     k++;
@@ -463,8 +473,8 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
   uint32_t nr = 0;
   if (act) {
     if (law == BELLMAN_LAW_MAP) {
-      const uint32_t rmin = c.rmin, rmax = c.rmax;
-      uint64_t rr = rmin + div_u64((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1), (uint64_t)k * (c.t2 - t1));
+      const uint32_t rmin = g3.z, rmax = g3.w;
+      uint64_t rr = rmin + div_u64((uint64_t)(rmax - rmin) * (A - (uint64_t)k * t1), (uint64_t)k * (g3.y - t1));
       if (rr > rmax) rr = rmax;
       nr = (uint32_t)rr;
       const uint32_t nrungs = c.nrungs;
@@ -479,25 +489,25 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
       nr = c.rungs[rung];
     }
   }
-  const uint32_t nctrl = c.dbg_nctrl;
+  const uint32_t nctrl = DBG ? c.dbg_nctrl : 0u;
   __syncwarp();
   if (lane == 0) {
     c.ring[pos] = x;
-    c.ring_n = k;
-    c.ringA = A;
-    c.ring_pos = (pos + 1u == window) ? 0u : pos + 1u;
-    c.rung = rung;
-    c.active = act;
-    if (act && !was_active) {
-      c.activations++;
-      if (c.first_act == BELLMAN_NONE) c.first_act = second;
+    uint4 *gw = reinterpret_cast<uint4 *>(&c.ringA);
+    gw[0] = make_uint4((uint32_t)A, (uint32_t)(A >> 32), k, (pos + 1u == window) ? 0u : pos + 1u);
+    gw[1] = make_uint4(rung, act, g1.z + (act && !was_active), g1.w + act);
+    if (act != (was_active != 0)) {  // the log is kept by second index (R21)
+      const uint32_t second = (uint32_t)(sec_bound / kUs - 1u);
+      if (act) {
+        if (g2.x == BELLMAN_NONE) c.first_act = second;
+      } else {
+        c.last_deact = second;
+      }
     }
-    if (!act && was_active) c.last_deact = second;
-    if (act) c.active_ingests++;
     if (DBG && dbg) {
       if (nctrl < c.dbg_cap) {
         bellman_ctrl_row cr;
-        cr.second = second;
+        cr.second = (uint32_t)(sec_bound / kUs - 1u);
         cr.sample = x;
         cr.k = k;
         cr.r_bp = nr;

@@ -113,6 +113,8 @@ __device__ __forceinline__ uint32_t lat_bin(uint64_t ms) {
   if (e > 31) return BELLMAN_HIST_LAT - 1;
   return 32u * (e - 4u) + ((uint32_t)(ms >> (e - 5u)) & 31u);
 }
+// out of line: latencies of 2^32 µs (71 min) and more are rare
+__device__ __noinline__ uint32_t lat_bin_wide(uint64_t us) { return lat_bin(us / 1000u); }
 // latency bin of a value in µs: floor(us / 1000) ms, in 32 bits when it fits
 __device__ __forceinline__ uint32_t lat_bin_us(uint64_t us) {
   if ((us >> 32) == 0) {
@@ -121,7 +123,7 @@ __device__ __forceinline__ uint32_t lat_bin_us(uint64_t us) {
     const uint32_t e = 31u - (uint32_t)__clz(ms);
     return 32u * (e - 4u) + ((ms >> (e - 5u)) & 31u);
   }
-  return lat_bin(us / 1000u);
+  return lat_bin_wide(us);
 }
 __device__ __forceinline__ uint32_t lat_edge(uint32_t b) {
   if (b < 32) return b;

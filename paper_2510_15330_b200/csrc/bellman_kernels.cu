@@ -171,6 +171,15 @@ struct alignas(16) QEnt {
 // Cold per-scenario state: touched at events (admissions, completions,
 // ingests, refills), not per iteration.  Lives in shared memory, one per warp,
 // so the event loop keeps its hot state in registers without spilling.
+// one entry written as two 16-byte stores (lanes write entries 32 bytes apart)
+__device__ __forceinline__ void store_qent(QEnt &q, uint64_t a, uint32_t in, uint32_t U, uint32_t P, uint32_t fcq,
+                                           uint32_t pf, uint32_t j) {
+  uint4 *w = reinterpret_cast<uint4 *>(&q);
+  w[0] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), in, U);
+  w[1] = make_uint4(P, fcq, pf, j);
+}
+static_assert(sizeof(QEnt) == 32 && offsetof(QEnt, in) == 8 && offsetof(QEnt, P) == 16, "QEnt layout");
+
 struct alignas(16) Cold {
   // a6 controller state, in 16-byte groups read with one LDS.128 each (g0..g4)
   uint64_t ringA;                                       // g0: window sum A,
@@ -297,9 +306,16 @@ __shared__ WarpHist g_hist[kWarpsPerBlock];
 // candidates are compacted (__fns) into entries 0..n-1 together with their
 // per-request draws (tag-1 block).  Out of line: it runs once per ~32 arrivals.
 // Returns n (0 only when the generator is exhausted).
-template <bool DBG>
-__device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, uint32_t lane,
-                                               bellman_second_row *dbg, uint32_t dbg_cap) {
+//
+// COUNT = true (the epilogue's queue count, a8): the same candidate stream,
+// but accepted arrivals are only counted while they precede `end` — no
+// per-request draws, no buffer writes — until the first at or after `end`
+// or the end of the trace; the count and last_j (index of the last counted
+// arrival + 1, from `last_j` on) are returned as (count lo, count hi, last_j).
+// Otherwise returns (n, 0, 0).
+template <bool DBG, bool COUNT = false>
+__device__ __noinline__ uint4 refill_buffer(const Params &p, uint32_t wid, uint32_t lane, bellman_second_row *dbg,
+                                            uint32_t dbg_cap, uint64_t end = 0, uint32_t last_j = 0) {
   Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
   const uint64_t H = DBG ? c.H : 0u;  // debug rows count arrivals before the horizon
   __syncwarp();  // every lane's reads of the previous buffer precede the new writes
@@ -309,35 +325,46 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
   const uint32_t n_seg = c.n_seg, gen_cap = c.gen_cap, k0 = c.k0, wid_lo = c.wid_lo, wid_hi = c.wid_hi;
   const DevSeg *segs = c.segs;
   uint32_t n = 0;
+  bool reached = false;  // COUNT: an accepted arrival at or after `end` was met
+  uint64_t cn = 0;
+  uint32_t lj = last_j;
   if (__builtin_expect(c.replay != 0, 0)) {  // NEXT-4 replay: entries gen_j .. gen_j+31 of the list, draws keyed by index
-    uint32_t left = gen_done ? 0u : n_seg - gen_j;
-    if (gen_cap && gen_cap - gen_acc < left) left = gen_cap - gen_acc;
-    n = left < 32u ? left : 32u;
-    if (lane < n) {
-      const uint32_t jj = gen_j + lane;
-      const bellman_arrival A = p.arrivals[c.rep_off + jj];
-      const uint64_t tau = (uint64_t)A.a_us;
-      const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
-      const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
-      const int32_t P0 = (int32_t)A.L_words + __ldg(&p.tabN[v.y >> 20]);
-      QEnt &q = c.q[lane];
-      q.a = tau;
-      q.in = A.input_words | (A.cls << 16);
-      q.U = U < 1 ? 1u : (uint32_t)U;
-      q.P = P0 < 1 ? 1u : (uint32_t)P0;
-      q.fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
-      q.pf = prefill_us(c.pf_ns, A.input_words);
-      q.j = jj;
-      if (DBG && dbg && tau < H) {
-        const uint64_t sidx = tau / kUs;
-        atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
+    do {
+      uint32_t left = gen_done ? 0u : n_seg - gen_j;
+      if (gen_cap && gen_cap - gen_acc < left) left = gen_cap - gen_acc;
+      n = left < 32u ? left : 32u;
+      uint64_t tau = 0;
+      if (lane < n) {
+        const uint32_t jj = gen_j + lane;
+        const bellman_arrival A = p.arrivals[c.rep_off + jj];
+        tau = (uint64_t)A.a_us;
+        if (!COUNT) {
+          const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
+          const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
+          const int32_t P0 = (int32_t)A.L_words + __ldg(&p.tabN[v.y >> 20]);
+          store_qent(c.q[lane], tau, A.input_words | (A.cls << 16), U < 1 ? 1u : (uint32_t)U,
+                     P0 < 1 ? 1u : (uint32_t)P0,
+                     (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20),
+                     prefill_us(c.pf_ns, A.input_words), jj);
+        }
+        if (DBG && dbg && tau < H) {
+          const uint64_t sidx = tau / kUs;
+          atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
+        }
       }
-    }
-    gen_j += n;
-    gen_acc += n;
-    if (n == 0 || gen_j >= n_seg || (gen_cap && gen_acc >= gen_cap)) gen_done = 1;
+      if (COUNT) {  // the list is in time order: the entries before `end` are a prefix
+        const uint32_t before = __ballot_sync(FULL, lane < n && tau < end);
+        cn += (uint32_t)__popc(before);
+        if (before) lj = gen_j + 32u - (uint32_t)__clz(before);
+        reached = before != (n >= 32u ? FULL : ((1u << n) - 1u));
+      }
+      gen_j += n;
+      gen_acc += n;
+      if (n == 0 || gen_j >= n_seg || (gen_cap && gen_acc >= gen_cap)) gen_done = 1;
+    } while (COUNT && !gen_done && !reached);
+    if (COUNT) n = 0;
   }
-  while (!c.replay && !gen_done && n == 0) {
+  while (!c.replay && !gen_done && n == 0 && !reached) {
     if (gen_seg >= n_seg) {
       gen_done = 1;
       break;
@@ -377,9 +404,21 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
         gen_done = 1;
       }
     }
-    n = (uint32_t)__popc(am);
+    const bool mine = (am >> lane) & 1u;
+    if (COUNT) {  // candidate times increase with the lane: those before `end` are a prefix
+      const uint32_t before = __ballot_sync(FULL, mine && tau < end);
+      cn += (uint32_t)__popc(before);
+      if (before) lj = gen_j + 32u - (uint32_t)__clz(before);
+      reached = before != am;
+      if (DBG && dbg && mine && tau < H) {
+        const uint64_t sidx = tau / kUs;
+        atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
+      }
+    } else {
+      n = (uint32_t)__popc(am);
+    }
     // compaction: the accepted candidate of rank l lands in entry l
-    if (acc && ((am >> lane) & 1u)) {
+    if (!COUNT && mine) {
       const uint32_t e = __popc(am & ((1u << lane) - 1u));
       const uint32_t L = (uint32_t)__ldg(&p.tabL[u.z >> 20]);
       const uint32_t x = u.z & 0xFFFFFu;  // class draw from the bits below L's index (NEXT-3)
@@ -388,20 +427,15 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);  // a3: the request's own draws
       const uint64_t U = ((uint64_t)L * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
       const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
-      QEnt &q = c.q[e];
-      q.a = tau;
-      q.in = in | (cls << 16);
-      q.U = U < 1 ? 1u : (uint32_t)U;
-      q.P = P0 < 1 ? 1u : (uint32_t)P0;
-      q.fcq = (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
-      q.pf = prefill_us(c.pf_ns, in);
-      q.j = jj;
+      store_qent(c.q[e], tau, in | (cls << 16), U < 1 ? 1u : (uint32_t)U, P0 < 1 ? 1u : (uint32_t)P0,
+                 (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20),
+                 prefill_us(c.pf_ns, in), jj);
       if (DBG && dbg && tau < H) {
         const uint64_t sidx = tau / kUs;
         atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
       }
     }
-    gen_acc += n;
+    gen_acc += (uint32_t)__popc(am);
     if (first_over < 32u) {
       gen_j += first_over + 1u;  // the crossing candidate is consumed (R17)
       gen_seg++;
@@ -412,7 +446,7 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
     }
   }
   __syncwarp();
-  if (lane == 0) {
+  if (!COUNT && lane == 0) {
     c.gen_done = gen_done;
     c.gen_seg = gen_seg;
     c.gen_fresh = gen_fresh;
@@ -421,7 +455,7 @@ __device__ __noinline__ uint32_t refill_buffer(const Params &p, uint32_t wid, ui
     c.gen_tau = gen_tau;
   }
   __syncwarp();
-  return n;
+  return COUNT ? make_uint4((uint32_t)cn, (uint32_t)(cn >> 32), lj, 0u) : make_uint4(n, 0u, 0u, 0u);
 }
 
 // floor(a / b), b > 0: a 32-bit division when both fit (the per-second means
@@ -614,7 +648,7 @@ struct Sim {
   // ------------------------------------------------------------------ a2
   __device__ __forceinline__ void refill(const Params &p) {
     buf_h = 0;
-    buf_n = refill_buffer<DBG>(p, wid, lane, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u);
+    buf_n = refill_buffer<DBG>(p, wid, lane, DBG ? dbg : nullptr, DBG ? cold().dbg_cap : 0u).x;
     head_t = buf_n ? rel(cold().q[0].a) : INF32;
   }
 
@@ -1137,6 +1171,7 @@ struct Sim {
 __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, const uint32_t *ps, uint32_t np,
                                  uint32_t *out, bool lat, uint32_t scale = 10u) {
   const uint32_t lane = lane_id();
+  // odd chunk length: lane l's run starts at l * chunk, conflict-free across banks
   const uint32_t chunk = (nb + 31u) / 32u;
   uint32_t csum = 0;
 #pragma unroll 1
@@ -1414,18 +1449,18 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   const long long epi0_ = clock64();
 #endif
   uint64_t queued = 0;
-  for (;;) {
-    if (S.buf_h >= S.buf_n) {
-      if (S.cold().gen_done) break;
-      S.refill(p);
-      continue;
-    }
+  {
     const uint32_t m = __ballot_sync(FULL, lane >= S.buf_h && lane < S.buf_n && S.cold().q[lane].a < end);
     const uint32_t nq = __popc(m);
     queued += nq;
     if (nq) S.last_j = S.cold().q[31 - __clz(m)].j + 1u;
-    if (S.buf_h + nq < S.buf_n) break;  // an arrival at or after `end` remains
-    S.buf_h = S.buf_n;
+    // the rest of the stream (no arrival at or after `end` in the buffer): counted only
+    if (S.buf_h + nq == S.buf_n && !S.cold().gen_done) {
+      const uint4 v = refill_buffer<DBG, true>(p, S.wid, lane, DBG ? S.dbg : nullptr, DBG ? S.cold().dbg_cap : 0u,
+                                               end, S.last_j);
+      queued += (uint64_t)v.x | ((uint64_t)v.y << 32);
+      S.last_j = v.z;
+    }
   }
   if (S.cold().series && lane == 0) p.series_n[rslot] = S.cold().series_n;
   if (DBG && S.dbg && lane == 0) {

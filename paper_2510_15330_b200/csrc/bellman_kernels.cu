@@ -238,7 +238,17 @@ __device__ __noinline__ uint32_t rewrite_len(int64_t poly0, int64_t poly1, int64
 }
 
 __device__ __forceinline__ uint32_t realized_len(const Params &p, uint32_t U, uint32_t P, uint32_t fcq, uint32_t ra) {
-  return ra == 0 ? U : rewrite_len(p.poly0, p.poly1, p.poly2, p.poly_fast, P, fcq, ra);
+  if (ra == 0) return U;
+  if (p.poly_fast) {  // the int64 path of rewrite_len, inline (one call site)
+    uint32_t N = (P * (10000u - ra) + 5000u) / 10000u;
+    if (N < 1u) N = 1u;
+    const int64_t n = N;
+    const int64_t poly = p.poly0 + p.poly1 * n + p.poly2 * n * n;
+    int64_t x = (poly * (int32_t)(fcq & 0xFFFFFu) + (1ll << 31)) >> 32;
+    x = x < 1 ? 1 : (x > (1 << 24) ? (1 << 24) : x);
+    return (uint32_t)x;
+  }
+  return rewrite_len(p.poly0, p.poly1, p.poly2, p.poly_fast, P, fcq, ra);
 }
 
 // NEXT-2 similarity decay between the safe window and decay_end:
@@ -566,7 +576,7 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
 // division: the cost base c = t0 + slope max(0, B - knee), the KV term as
 // kv K = kq 1000 + kr, the window flag and its next boundary, the arrival time
 // of the queue head.
-template <bool DBG, bool TBTO>
+template <bool DBG, bool TBTO, bool KV0 = false>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
   // the selected signal is x: a compile-time answer in the TBT-only
@@ -575,6 +585,8 @@ struct Sim {
   // contending prefill (NEXT-4): never in the TBT-specialised instantiation
   __device__ __forceinline__ bool cont() const { return TBTO ? false : pmode != 0u; }
   __device__ __forceinline__ uint32_t n_pending() const { return cont() ? n_pend : 0u; }
+  // the KV term's coefficient: a compile-time 0 in the KV-free instantiation
+  __device__ __forceinline__ uint32_t kvc() const { return KV0 ? 0u : kv; }
   __device__ __forceinline__ Cold &cold() const { return g_cold[kWarpsPerBlock == 1 ? 0u : wid]; }
 #ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
@@ -722,11 +734,13 @@ struct Sim {
   // B changed: cost base and per-iteration KV growth
   __device__ __forceinline__ void batch_changed() {
     cbase = t0 + slope * (B > knee ? B - knee : 0u);
+    if (KV0) return;
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
     kstep_r = ks - kstep_q * 1000u;
   }
   __device__ __forceinline__ void kv_add(uint64_t x) {  // kv K += x
+    if (KV0) return;
     const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
     kr += (uint32_t)(x - q * 1000u);
     kq += (uint32_t)q;
@@ -736,6 +750,7 @@ struct Sim {
     }
   }
   __device__ __forceinline__ void kv_sub(uint64_t x) {  // kv K -= x
+    if (KV0) return;
     const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
     const uint32_t rem = (uint32_t)(x - q * 1000u);
     kq -= (uint32_t)q;
@@ -773,11 +788,13 @@ struct Sim {
       atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)B * iter_d + iter_align);
     }
     if (DBG) __syncwarp();
-    kr += kstep_r;
-    kq += kstep_q;
-    if (kr >= 1000u) {
-      kr -= 1000u;
-      kq++;
+    if (!KV0) {
+      kr += kstep_r;
+      kq += kstep_q;
+      if (kr >= 1000u) {
+        kr -= 1000u;
+        kq++;
+      }
     }
   }
 
@@ -822,7 +839,7 @@ struct Sim {
       const uint64_t se = warp_sum_split(e2e_l);
       const uint32_t ns = __reduce_add_sync(FULL, nslo);
       const uint32_t kd = __reduce_add_sync(FULL, kdrop);
-      kv_sub((uint64_t)kv * kd);
+      kv_sub((uint64_t)kvc() * kd);
       kv_res -= kd;  // NEXT-4: completed contexts (input + R) free the KV capacity
       adm_blocked = 0;
       cadd(CT_SERVED, ndone);
@@ -1056,13 +1073,13 @@ struct Sim {
     const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
     if (nmax == 0 || stop <= T + 1u) return;
     const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
-    uint32_t q = kq, rr = kr, done = 0;
+    uint32_t q = KV0 ? 0u : kq, rr = KV0 ? 0u : kr, done = 0;
     for (;;) {
       const uint32_t lim = stop < sec_bound ? stop : sec_bound;
       const uint32_t room = lim - 1u - T;
       const uint32_t left = nmax - done;
       uint32_t n = 0, used = 0;
-      if (kv == 0) {
+      if (kvc() == 0) {
         const uint32_t nn = room / cb;
         n = nn < left ? nn : left;
         used = n * cb;
@@ -1114,8 +1131,10 @@ struct Sim {
       if (tnext >= stop || tnext < sec_bound) break;
       roll_second(tnext);  // the next end opens a new second: ingest the closed one here
     }
-    kq = q;
-    kr = rr;
+    if (!KV0) {
+      kq = q;
+      kr = rr;
+    }
   }
 
   // ------------------------------------------------------------------ a4
@@ -1139,12 +1158,12 @@ struct Sim {
       align = warp_sum_split(al);
       const uint32_t mj = __reduce_min_sync(FULL, jn);
       if (mj < next_done) next_done = mj;
-      kv_add((uint64_t)kv * __reduce_add_sync(FULL, kadd));
+      if (!KV0) kv_add((uint64_t)kv * __reduce_add_sync(FULL, kadd));
       B += n_ready;
       n_ready = 0;
       batch_changed();
     }
-    uint32_t d = cbase + kq;
+    uint32_t d = cbase + (KV0 ? 0u : kq);
     if (cont()) {  // NEXT-4: cost(B) (nothing when B = 0) + the admitted requests' prefills
       d = (B ? d : 0u) + pend_us;
       if (n_pend) {
@@ -1210,12 +1229,12 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 
 // One scenario, a1-a9.  TBTO: the scenario's signal is TBT (compile-time
 // specialisation of every signal test in the event loop).
-template <bool DBG, bool TBTO>
+template <bool DBG, bool TBTO, bool KV0 = false>
 __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, const bellman_scenario &sc,
                                         const bellman_ctrl &cc, const uint32_t lane, WarpHist &h) {
   // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
   // lane 0 only and read after the __syncwarp below.
-  Sim<DBG, TBTO> S(warp_in_block());
+  Sim<DBG, TBTO, KV0> S(warp_in_block());
   S.lane = lane;
   const bellman_profile pr = p.profs[sc.profile];
   const DevTrace tr = p.traces[sc.trace];
@@ -1307,6 +1326,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   S.next_pf = INF32;
   S.n_ready = S.B = S.in_sys = 0;
   S.kq = S.kr = 0;
+  S.kstep_q = S.kstep_r = 0;
   S.batch_changed();
   S.update_window();
 #pragma unroll
@@ -1595,7 +1615,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING) {
-      run_one<false, true>(p, sid, sc, cc, lane, h);
+      // TBT-only loop, specialised once more on a KV-free cost law (kv = 0)
+      if (p.profs[sc.profile].kv_ns_per_word == 0)
+        run_one<false, true, true>(p, sid, sc, cc, lane, h);
+      else
+        run_one<false, true, false>(p, sid, sc, cc, lane, h);
     } else {
       run_one<false, false>(p, sid, sc, cc, lane, h);
     }

@@ -88,6 +88,46 @@ def algorithmic_ops(st) -> float:
     return A_TICK * ticks + A_CAND * cand + A_ADMIT * adm + A_DONE * done + A_SEC * secs + A_PF * adm
 
 
+def latency_floor(w, pk, ws, local, stream, kernel_ms):
+    """The launch's lower bound from serial latency: every segment's scenarios
+    (<= 148, contiguous ids) launched alone — one warp per SM, no co-runners —
+    and the slowest such launch taken.  No launch of the whole set can finish
+    before its longest serial chain does.  None where segments are larger."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    seg = np.array([s.segment for s in w.scenarios])
+    groups = []
+    for g in range(w.n_segments):
+        ids = np.nonzero(seg == g)[0]
+        if len(ids) == 0:
+            continue
+        if len(ids) > 148 or ids[-1] - ids[0] + 1 != len(ids):
+            return None
+        groups.append((g, int(ids[0]), len(ids)))
+    s3 = Simulator(packed=pk, device=local, stream=stream, workspace=ws)
+    worst = (0.0, None)
+    for g, first, cnt in groups:
+        best = None
+        for _ in range(2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s3.run(first=first, count=cnt, stride=1, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b)
+            best = t if best is None else min(best, t)
+        if best > worst[0]:
+            worst = (best, g)
+    s3.close()
+    names = getattr(w, "segment_names", None)
+    return {"critical_ms": worst[0], "kernel_ms": kernel_ms, "frac": worst[0] / kernel_ms,
+            "critical_segment": names[worst[1]] if names else worst[1],
+            "note": "each segment's scenarios launched alone (one warp per SM): the slowest such launch is the "
+                    "serial-latency floor of the whole launch; frac = floor / measured kernel time"}
+
+
 def ncu_traffic(name: str):
     """DRAM bytes (read + write) per tick-kernel launch of this workload, from
     the committed summary of one `ncu --set full` capture (profiles/), or None."""
@@ -332,6 +372,7 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    lat = latency_floor(w, pk, sim.ws, local, stream, kern_tot / args.steps) if world == 1 else None
     pk_ = peaks()
     clocks = clk.summary()
     mhz = pk_["sm_max_mhz"]
@@ -359,6 +400,8 @@ def main():
         "clocks": clocks,
         "kernel_ms_per_step": kern_tot / args.steps,
     }
+    if lat is not None:
+        line["latency_floor"] = lat
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

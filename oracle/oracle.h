@@ -57,6 +57,7 @@ typedef struct {
   const uint32_t *prof_t0, *prof_knee, *prof_slope, *prof_kv, *prof_maxb, *prof_prefill_ns;
   const uint32_t *prof_kv_cap; /* NEXT-4: KV capacity in context words, 0 = unlimited */
   const uint32_t *prof_prefill_mode; /* NEXT-4: 0 non-blocking prefill, 1 contending */
+  const uint32_t *prof_kv_policy;    /* NEXT-4: 0 reserve whole contexts, 1 preempt on overflow */
   const double *prof_e_in, *prof_e_out, *prof_p_idle;
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
@@ -94,6 +95,10 @@ typedef struct {
   uint32_t kv_cap_words; /* NEXT-4 KV-capacity admission, 0 = unlimited */
   uint32_t prefill_mode; /* NEXT-4: 0 non-blocking; 1 contending: the requests admitted
                             at an iteration boundary prefill inside the next iteration */
+  uint32_t kv_policy;    /* NEXT-4 with kv_cap_words > 0: 0 reserve (admit only whole contexts
+                            input + R), 1 preempt (admit on the current context input + emitted;
+                            at an iteration end whose contexts exceed the capacity, the latest
+                            admitted requests go back to the queue front and later recompute) */
 } orc_profile;
 
 typedef struct {
@@ -121,6 +126,8 @@ typedef struct {
   double energy_j, win_energy_j;
   uint32_t sim_active_p50, sim_inactive_p50, scored_active, scored_inactive; /* NEXT-2, centi-points */
   uint32_t bypassed; /* NEXT-3: admissions while r > 0 left unrewritten by a bypass rule */
+  uint32_t preemptions;     /* NEXT-4 kv_policy 1: requests sent back to the queue */
+  uint64_t recompute_words; /* NEXT-4 kv_policy 1: context words prefilled again at re-admission */
   /* ---- self-checks the GPU never computes ---- */
   uint64_t e2e_exact_p50_us, e2e_exact_p99_us, ttft_exact_p50_us, ttft_exact_p99_us;
   uint64_t int_system_us;  /* integral of (queued + in_system) dt, µs*requests */

@@ -25,6 +25,14 @@
  * rung; STEP climbs a rung per ingest while active.  Rewrite at admission:
  * N = round(P (1 - r)), realized = round(poly(N) * Fcomp).
  * Energy: e_in * words_in + e_out * words_out + p_idle * idle.
+ * NEXT-4 KV capacity (S:255 leaves KV out of SPEC): kv_policy 0
+ * admits the queue head only if its whole context input + R fits beside the
+ * reserved contexts; kv_policy 1 (vLLM-style recompute preemption) admits on
+ * the current context input + emitted, and at an iteration end whose contexts
+ * exceed the capacity sends the latest admitted requests (one at a time, while
+ * more than one is in the system) back to the front of the queue, in front of
+ * earlier victims; a re-admitted request prefills its whole context again and
+ * that prefill's end emits its next word (a decode word, TBT gap from its last).
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -41,6 +49,7 @@ enum { RS_FUTURE = 0, RS_QUEUED, RS_PREFILL, RS_READY, RS_DECODING, RS_DONE, RS_
 typedef struct {
   uint64_t t;
   uint32_t kind, idx;
+  uint32_t gen; /* prefill ends: the request's admission generation (stale after a preemption) */
 } event;
 
 typedef struct {
@@ -210,6 +219,8 @@ static uint32_t bounded_realized(uint32_t P, uint32_t r_bp, int32_t fcomp, const
 typedef struct {
   uint64_t admit, first, done, last_tok, prefill_end;
   uint32_t emitted, R, r_bp, state, n_gaps;
+  uint64_t enq;      /* start of the current queue stay (arrival, or the preemption instant) */
+  uint32_t seq, gen; /* admission order (every admission); admissions so far */
 } rstate;
 
 typedef struct {
@@ -295,6 +306,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint32_t *ready = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
   uint32_t *batch = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));
   uint32_t *pending = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t)); /* contending prefill */
+  uint32_t *stack = (uint32_t *)malloc((n_req ? n_req : 1) * sizeof(uint32_t));   /* preempted: queue front */
   uint64_t *e2e_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
   uint64_t *ttft_v = (uint64_t *)malloc((n_req ? n_req : 1) * sizeof(uint64_t));
   uint64_t n_sec = H / US + 2;
@@ -312,7 +324,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
   cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
-  if (!rs || !queue || !ready || !batch || !pending || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
+  if (!rs || !queue || !ready || !batch || !pending || !stack || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
       !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt || !sec_in_sum ||
       !sec_in_any || !sec_util_sum || !sec_util_cnt ||
       ((cfg->record & 2) && !rows))
@@ -321,12 +333,16 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
 
   for (uint64_t i = 0; i < n_req; ++i) {
     rs[i].admit = rs[i].first = rs[i].done = NEVER;
-    if (heap_push(&h, (event){req[i].a_us, EV_ARRIVAL, (uint32_t)i})) goto out;
+    rs[i].enq = req[i].a_us;
+    if (heap_push(&h, (event){req[i].a_us, EV_ARRIVAL, (uint32_t)i, 0})) goto out;
   }
 
   uint64_t q_head = 0, q_tail = 0, n_ready = 0, n_batch = 0, in_sys = 0;
   uint64_t kv_reserved = 0; /* NEXT-4: sum of (input + R) over requests in the system */
   uint64_t n_pend = 0, pend_us = 0; /* NEXT-4 contending prefill: admitted, prefill not started */
+  uint64_t n_stack = 0;             /* NEXT-4 kv_policy 1: preempted requests at the queue front */
+  uint32_t next_seq = 0;            /* admission order */
+  const int preempt = prof->kv_policy == 1 && prof->kv_cap_words > 0;
   uint64_t n_e2e = 0, n_ttft = 0;
   int busy = 0;
   uint64_t next_sec = 0; /* first second not yet ingested */
@@ -361,7 +377,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
     if (T >= H) break;
     /* integrate piecewise-constant state over [T_prev, T) */
     {
-      uint64_t dt = T - T_prev, nq = q_tail - q_head;
+      uint64_t dt = T - T_prev, nq = q_tail - q_head + n_stack;
       if (in_sys == 0) {
         res->idle_us += dt;
         res->win_idle_us += overlap(T_prev, T, cfg->w0_us, cfg->w1_us);
@@ -431,9 +447,84 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         }
         n_batch = 0;
         busy = 0;
+        if (preempt) {
+          /* contexts of everything in the system: input + words emitted so far */
+          uint64_t F = 0;
+          for (uint64_t i = 0; i < n_req; ++i)
+            if (rs[i].state == RS_PREFILL || rs[i].state == RS_READY || rs[i].state == RS_DECODING)
+              F += (uint64_t)req[i].input + rs[i].emitted;
+          while (F > prof->kv_cap_words && in_sys > 1) {
+            /* the latest admitted request in the system goes back to the queue front */
+            uint64_t v = n_req;
+            for (uint64_t i = 0; i < n_req; ++i)
+              if ((rs[i].state == RS_PREFILL || rs[i].state == RS_READY) && (v == n_req || rs[i].seq > rs[v].seq))
+                v = i;
+            if (rs[v].state == RS_READY) { /* leaves the decode-ready list */
+              uint64_t w = 0;
+              for (uint64_t b = 0; b < n_ready; ++b)
+                if (ready[b] != v) ready[w++] = ready[b];
+              n_ready = w;
+            }
+            F -= (uint64_t)req[v].input + rs[v].emitted;
+            rs[v].state = RS_QUEUED; /* a pending prefill end of it is now stale (gen) */
+            rs[v].enq = T;
+            stack[n_stack++] = (uint32_t)v;
+            in_sys--;
+            res->preemptions++;
+          }
+        }
       } else if (e.kind == EV_PREFILL_END) {
-        /* E2: first word at prefill end; TTFT = first token - arrival (S:191) */
         uint32_t m = e.idx;
+        if (rs[m].state != RS_PREFILL || rs[m].gen != e.gen) continue; /* preempted meanwhile */
+        if (rs[m].emitted > 0) {
+          /* a re-admitted request's recompute prefill ends: its next word, a decode
+           * word whose TBT gap runs from its last word (before the preemption) */
+          uint64_t gap = T - rs[m].last_tok;
+          sec_tbt_sum[s_idx] += gap;
+          sec_tbt_cnt[s_idx] += 1;
+          res->tbt_samples++;
+          res->tbt_sum_us += gap;
+          if (gap > res->tbt_max_us) res->tbt_max_us = gap;
+          if (log && log->gaps && log->n_gaps < log->cap_gaps) {
+            log->gaps[2 * log->n_gaps] = m;
+            log->gaps[2 * log->n_gaps + 1] = gap;
+          }
+          if (log) log->n_gaps++;
+          rs[m].n_gaps++;
+          rs[m].last_tok = T;
+          rs[m].emitted++;
+          res->words_out++;
+          if (rows) {
+            rows[s_idx].tbt_count++;
+            rows[s_idx].sum_tbt_us += gap;
+            rows[s_idx].words_out++;
+          }
+          if (in_window(T, cfg)) res->win_words_out++;
+          if (rs[m].emitted == rs[m].R) {
+            uint64_t e2e = T - req[m].a_us;
+            rs[m].done = T;
+            rs[m].state = RS_DONE;
+            in_sys--;
+            res->served++;
+            res->sum_e2e_us += e2e;
+            res->sum_sojourn_us += e2e;
+            e2e_v[n_e2e++] = e2e;
+            res->hist_e2e[orc_lat_bin(e2e / 1000)]++;
+            if (in_window(T, cfg)) res->win_served++;
+            sec_e2e_sum[s_idx] += e2e;
+            sec_e2e_cnt[s_idx] += 1;
+            if (e2e > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }
+            if (rows) {
+              rows[s_idx].completions++;
+              rows[s_idx].sum_e2e_us += e2e;
+            }
+          } else {
+            rs[m].state = RS_READY;
+            ready[n_ready++] = m;
+          }
+          continue;
+        }
+        /* E2: first word at prefill end; TTFT = first token - arrival (S:191) */
         uint64_t ttft = T - req[m].a_us;
         rs[m].first = T;
         rs[m].last_tok = T;
@@ -485,7 +576,37 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
     if (!busy) {
       /* admission point: ingest every closed second, then admit FIFO */
       INGEST_UNTIL(T);
-      while (in_sys < prof->max_batch && q_head < q_tail) {
+      while (in_sys < prof->max_batch && (n_stack > 0 || q_head < q_tail)) {
+        if (n_stack > 0) {
+          /* NEXT-4 kv_policy 1: a preempted request (queue front) is admitted again
+           * if its context fits; its rewrite R stays; it prefills input + emitted */
+          uint32_t m = stack[n_stack - 1];
+          uint64_t ctx = (uint64_t)req[m].input + rs[m].emitted, F = 0;
+          for (uint64_t i = 0; i < n_req; ++i)
+            if (rs[i].state == RS_PREFILL || rs[i].state == RS_READY || rs[i].state == RS_DECODING)
+              F += (uint64_t)req[i].input + rs[i].emitted;
+          if (in_sys > 0 && F + ctx > prof->kv_cap_words) break;
+          n_stack--;
+          rs[m].seq = next_seq++;
+          rs[m].gen++;
+          uint64_t pf = ((uint64_t)prof->prefill_ns_per_word * ctx) / 1000;
+          if (pf < 1) pf = 1;
+          rs[m].prefill_end = T + pf;
+          rs[m].state = RS_PREFILL;
+          in_sys++;
+          res->sum_queue_us += T - rs[m].enq;
+          res->words_in += ctx;
+          res->recompute_words += ctx;
+          sec_in_sum[T / US] += ctx;
+          sec_in_any[T / US] = 1;
+          if (in_window(T, cfg)) res->win_words_in += ctx;
+          if (rows) {
+            rows[T / US].sum_queue_us += T - rs[m].enq;
+            rows[T / US].words_in += (uint32_t)ctx;
+          }
+          if (heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m, rs[m].gen})) goto out;
+          continue;
+        }
         uint32_t m = queue[q_head];
         uint32_t r = cs.r;
         /* NEXT-3 bypass: class policy or a short predicted output */
@@ -496,8 +617,19 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
          * output) must fit beside everything admitted; strict FIFO; an oversized
          * request is admitted only into an empty system */
         uint64_t need = (uint64_t)req[m].input + R;
-        if (prof->kv_cap_words && in_sys > 0 && kv_reserved + need > prof->kv_cap_words) break;
+        if (preempt) {
+          /* kv_policy 1: only the current context (the input) has to fit */
+          uint64_t F = 0;
+          for (uint64_t i = 0; i < n_req; ++i)
+            if (rs[i].state == RS_PREFILL || rs[i].state == RS_READY || rs[i].state == RS_DECODING)
+              F += (uint64_t)req[i].input + rs[i].emitted;
+          if (in_sys > 0 && F + req[m].input > prof->kv_cap_words) break;
+        } else if (prof->kv_cap_words && in_sys > 0 && kv_reserved + need > prof->kv_cap_words) {
+          break;
+        }
         q_head++;
+        rs[m].seq = next_seq++;
+        rs[m].gen++;
         kv_reserved += need;
         if (bypass) res->bypassed++;
         rs[m].admit = T;
@@ -536,7 +668,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           if (r > 0) { res->hist_q_active[qb]++; res->scored_active++; }
           else { res->hist_q_inactive[qb]++; res->scored_inactive++; }
         }
-        if (!prof->prefill_mode && heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m})) goto out;
+        if (!prof->prefill_mode && heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m, rs[m].gen})) goto out;
       }
       /* iteration start with every decode-ready request (and, contending, the
        * prefills of everything just admitted) */
@@ -560,11 +692,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           rs[m].prefill_end = T + d;
           rs[m].state = RS_PREFILL;
           /* same instant as the iteration end; popped after it (kind order, R7) */
-          if (heap_push(&h, (event){T + d, EV_PREFILL_END, m})) goto out;
+          if (heap_push(&h, (event){T + d, EV_PREFILL_END, m, rs[m].gen})) goto out;
         }
         n_pend = 0;
         pend_us = 0;
-        if (heap_push(&h, (event){T + d, EV_ITER_END, 0})) goto out;
+        if (heap_push(&h, (event){T + d, EV_ITER_END, 0, 0})) goto out;
         busy = 1;
         res->ticks++;
       }
@@ -574,7 +706,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   /* termination (R20): cutoff -> end at H; drain -> last event, unless capped */
   uint64_t end = (cfg->mode == ORC_MODE_DRAIN && h.n == 0) ? last_T : H;
   {
-    uint64_t dt = end - T_prev, nq = q_tail - q_head;
+    uint64_t dt = end - T_prev, nq = q_tail - q_head + n_stack;
     if (in_sys == 0) {
       res->idle_us += dt;
       res->win_idle_us += overlap(T_prev, end, cfg->w0_us, cfg->w1_us);
@@ -588,7 +720,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   res->end_us = end;
   INGEST_UNTIL(end);
   res->queued_end = q_tail - q_head;
-  res->inflight_end = in_sys;
+  res->inflight_end = in_sys + n_stack; /* admitted and not completed (preempted ones waiting too) */
   if (res->queued_end + res->inflight_end > 0) res->flags |= ORC_FLAG_TRUNCATED;
 
   /* a8 energy, fp64, in this fixed order (R19) */
@@ -675,7 +807,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   }
   rc = 0;
 out:
-  free(rs); free(queue); free(ready); free(batch); free(pending); free(e2e_v); free(ttft_v);
+  free(rs); free(queue); free(ready); free(batch); free(pending); free(stack); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
   free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
   free(sec_util_cnt);
@@ -697,6 +829,7 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   p->p_idle = in->prof_p_idle[pi];
   p->kv_cap_words = in->prof_kv_cap[pi];
   p->prefill_mode = in->prof_prefill_mode[pi];
+  p->kv_policy = in->prof_kv_policy[pi];
   memset(c, 0, sizeof(*c));
   c->law = in->ctrl_law[ci];
   c->signal = in->ctrl_signal[ci];

@@ -6,7 +6,12 @@ SPEC.md S:245 (continuous batching) in the order fixed by S:247 / readings
 R6-R9: iteration end, prefill ends (by j), arrivals (by j), then — if the loop
 is idle — ingest, admission and iteration start.  prof["prefill_mode"] = 1
 (NEXT-4 contention): requests admitted at a boundary prefill inside the
-next iteration, which lasts cost(B) + their prefill times (B = 0: just those).  No event heap, no
+next iteration, which lasts cost(B) + their prefill times (B = 0: just those).
+prof["kv_policy"] = 1 (NEXT-4 preemption): admission needs only the current
+context (input + words emitted) to fit kv_cap_words; at an iteration end whose
+contexts exceed it, the latest admitted requests (while more than one is in the
+system) go back to the front of the queue and later prefill input + emitted
+again, that prefill's end emitting their next word.  No event heap, no
 incremental sums.  Usable only on tiny traces (<= ~2e6 µs).  Controller: the
 linear MAP law recomputed from a Fraction moving average.
 """
@@ -29,6 +34,14 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
     rbp = [0] * n
     queue = []
     ready = []
+    seq = [None] * n
+    enq = [q["a_us"] for q in requests]
+    next_seq = 0
+    preemptions = 0
+    recompute_words = 0
+    sum_queue = 0
+    preempt = prof.get("kv_policy", 0) == 1 and prof.get("kv_cap_words", 0) > 0
+    in_system = ("prefill", "ready", "decoding", "pending")
     batch = []
     iter_end = None
     ticks = 0
@@ -60,7 +73,36 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                     ready.append(m)
             batch = []
             iter_end = None
+            if preempt:  # contexts over the capacity: the latest admitted go back to the queue front
+                while True:
+                    inside = [i for i in range(n) if st[i] in in_system]
+                    F = sum(requests[i]["input"] + emitted[i] for i in inside)
+                    if F <= prof["kv_cap_words"] or len(inside) <= 1:
+                        break
+                    v = max(inside, key=lambda i: seq[i])
+                    if v in ready:
+                        ready.remove(v)
+                    st[v] = "queued"
+                    enq[v] = t
+                    queue.insert(0, v)
+                    preemptions += 1
         for m in range(n):
+            if st[m] == "prefill" and pend[m] == t and emitted[m] > 0:  # recompute prefill: next word
+                anything = True
+                g = t - last[m]
+                gaps[m].append(g)
+                sec_sum[t // 10**6] = sec_sum.get(t // 10**6, 0) + g
+                sec_cnt[t // 10**6] = sec_cnt.get(t // 10**6, 0) + 1
+                last[m] = t
+                emitted[m] += 1
+                words_out += 1
+                if emitted[m] == R[m]:
+                    st[m] = "done"
+                    done[m] = t
+                else:
+                    st[m] = "ready"
+                    ready.append(m)
+                continue
             if st[m] == "prefill" and pend[m] == t:
                 anything = True
                 first[m] = t
@@ -102,7 +144,22 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
             while in_sys < prof["max_batch"] and queue:
                 m = queue[0]
                 q = requests[m]
-                if cap:  # NEXT-4 KV-capacity admission: whole contexts must fit (empty system always admits)
+                if preempt:
+                    F = sum(requests[i]["input"] + emitted[i] for i in range(n) if st[i] in in_system)
+                    ctx = q["input"] + emitted[m]
+                    if in_sys > 0 and F + ctx > cap:
+                        break
+                    if admit[m] is not None:  # re-admission of a preempted request: R stays
+                        queue.pop(0)
+                        seq[m] = next_seq
+                        next_seq += 1
+                        sum_queue += t - enq[m]
+                        recompute_words += ctx
+                        pend[m] = t + max(1, prof["prefill_ns_per_word"] * ctx // 1000)
+                        st[m] = "prefill"
+                        in_sys += 1
+                        continue
+                elif cap:  # NEXT-4 KV-capacity admission: whole contexts must fit (empty system always admits)
                     if r_cur > 0:
                         Nh = max(1, int(Fraction(q.get("P", q["U"])) * (Fraction(10000 - r_cur, 10000)) + Fraction(1, 2)))
                         Rh = max(1, int(Fraction(Nh) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
@@ -114,6 +171,9 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                         break
                 queue.pop(0)
                 admit[m] = t
+                seq[m] = next_seq
+                next_seq += 1
+                sum_queue += t - enq[m]
                 rbp[m] = r_cur
                 q = requests[m]
                 if r_cur > 0:
@@ -153,4 +213,5 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
         # idle was counted through t = end inclusive of the final µs loop; recount up to end
         pass
     return dict(admit=admit, first=first, done=done, R=R, r_bp=rbp, gaps=gaps, ticks=ticks,
-                words_out=words_out, end_us=end, served=sum(1 for s in st if s == "done"))
+                words_out=words_out, end_us=end, served=sum(1 for s in st if s == "done"),
+                preemptions=preemptions, recompute_words=recompute_words, sum_queue_us=sum_queue)

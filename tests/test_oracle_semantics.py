@@ -484,3 +484,96 @@ def test_contending_gap_is_cost_plus_admitted_prefills(orc):
         nb = orc.simulate(reqs, dict(prof, prefill_mode=0), mode=W.MODE_DRAIN)
         assert nb["tbt_sum_us"] / nb["tbt_samples"] < 1.5 * prof["t0_us"]
     assert means == sorted(means) and means[-1] > 2 * means[0]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4 KV preemption (profile kv_policy = 1; SURVEY 8(f) f4 "KV-capacity
+# admission and preemption"; S:255 keeps KV out of SPEC): vLLM-style recompute
+# preemption.  Admission needs the head's current context (input + words
+# emitted) to fit; at an iteration end whose contexts exceed kv_cap_words the
+# latest admitted requests go back to the queue front (while more than one is
+# in the system) and later prefill input + emitted again, the end of that
+# prefill emitting their next word.
+PRE = dict(t0_us=100, knee=4, slope_us=0, kv_ns_per_word=0, max_batch=4, prefill_ns_per_word=1000,
+           e_in=0.05, e_out=0.5, p_idle=300.0, kv_cap_words=25, kv_policy=1)
+
+
+def test_kv_preemption_hand_timeline(orc):
+    """Two requests (input 10, 5 words each, cap 25 words, 1 µs prefill per
+    word, 100 µs iterations), worked by hand: both admitted at 0 (contexts 10 +
+    10), first words at 10; after the ends at 110 (contexts 12 + 12 = 24) and
+    210 (13 + 13 = 26 > 25) the later admitted B goes back to the queue; B (13
+    context words) fits only when A completes at 410; its recompute prefill
+    ends at 423 with B's 4th word (gap 423 - 210), the 5th at 523."""
+    reqs = [dict(a_us=0, input=10, U=5), dict(a_us=0, input=10, U=5)]
+    d = orc.simulate(reqs, PRE, mode=W.MODE_DRAIN)
+    a, b = d["requests"]
+    assert (a["admit_us"], a["first_us"], a["done_us"]) == (0, 10, 410)
+    assert (b["admit_us"], b["first_us"], b["done_us"]) == (0, 10, 523)
+    assert d["gaps"][0] == [100, 100, 100, 100]
+    assert d["gaps"][1] == [100, 100, 213, 100]
+    assert (d["preemptions"], d["recompute_words"], d["sum_queue_us"]) == (1, 13, 200)
+    assert (d["ticks"], d["words_in"], d["words_out"], d["served"], d["admitted"]) == (5, 33, 10, 2, 2)
+    assert d["energy_j"] == (0.05 * 33 + 0.5 * 10) + 300.0 * 0 / 1e6
+    # no preemption when the capacity holds both contexts to the end (or is unlimited)
+    for cap in (30, 0):
+        n = orc.simulate(reqs, dict(PRE, kv_cap_words=cap), mode=W.MODE_DRAIN)
+        assert n["preemptions"] == 0 and [r["done_us"] for r in n["requests"]] == [410, 410]
+
+
+def test_bruteforce_kv_preemption(orc):
+    """KV preemption vs the brute-force simulator on random tiny traces (exact
+    per request and per gap, preemption and recompute counts, queue stays)."""
+    rng = np.random.default_rng(23)
+    total = 0
+    for case in range(120):
+        reqs, prof = _random_tiny(rng)
+        n = int(rng.integers(3, 9))  # a denser mix than _random_tiny: several contexts that grow
+        reqs = sorted([dict(a_us=int(rng.integers(0, 3000)), input=int(rng.integers(1, 20)),
+                            U=int(rng.integers(2, 16)), P=int(rng.integers(2, 16)),
+                            fcomp_q16=int(rng.integers(50000, 80000))) for _ in range(n)], key=lambda q: q["a_us"])
+        prof["max_batch"] = int(rng.integers(2, 7))
+        prof["knee"] = min(prof["knee"], prof["max_batch"])
+        prof["kv_cap_words"] = int(rng.integers(15, 60))
+        prof["kv_policy"] = 1
+        law = "const" if case % 2 else "off"
+        rc = int(rng.integers(100, 3000)) if law == "const" else 0
+        bf = bruteforce.simulate(reqs, prof, 10**6, law=law, r_const=rc)
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=rc) if law == "const" else None
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=10**6)
+        assert (d["ticks"], d["words_out"], d["served"], d["end_us"]) == \
+               (bf["ticks"], bf["words_out"], bf["served"], bf["end_us"]), case
+        assert (d["preemptions"], d["recompute_words"], d["sum_queue_us"]) == \
+               (bf["preemptions"], bf["recompute_words"], bf["sum_queue_us"]), case
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i]), (case, i)
+            assert d["gaps"][i] == bf["gaps"][i], (case, i)
+        total += d["preemptions"]
+    assert total > 50  # the cases do exercise preemption
+
+
+def test_kv_preemption_identities(orc):
+    """On a congested paper-trace run under a tight capacity: requests are
+    preempted, yet every admitted request completes with all R words (one gap
+    per word after the first), the sample-path identities hold with preempted
+    requests counted as queued (Little's law: sum of sojourns = integral of
+    queue + system; sum of every queue stay = integral of the queue), and a
+    capacity that never binds gives the run without a capacity."""
+    w = W.config_paper_pair(1)
+    arr = orc.arrivals(w.columns(), 0)
+    reqs = [dict(a_us=int(x["a_us"]), input=int(x["input"]), U=int(x["U"])) for x in arr]
+    prof = dict(w.profiles[0], kv_cap_words=200_000, kv_policy=1)
+    d = orc.simulate(reqs, prof, mode=W.MODE_DRAIN)
+    assert d["preemptions"] > 10 and d["recompute_words"] > 0
+    assert d["served"] == d["admitted"] == len(reqs) and d["inflight_end"] == 0
+    assert d["words_out"] == sum(r["R"] for r in d["requests"])
+    assert all(r["n_gaps"] == r["R"] - 1 for r in d["requests"])
+    assert d["sum_sojourn_us"] == d["int_system_us"]
+    assert d["sum_queue_us"] == d["int_queue_us"]
+    assert d["words_in"] == sum(q["input"] for q in reqs) + d["recompute_words"]
+    big = orc.simulate(reqs, dict(prof, kv_cap_words=2**30), mode=W.MODE_DRAIN)
+    free = orc.simulate(reqs, dict(prof, kv_cap_words=0), mode=W.MODE_DRAIN)
+    assert big["preemptions"] == 0
+    assert [r["done_us"] for r in big["requests"]] == [r["done_us"] for r in free["requests"]]

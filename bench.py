@@ -286,8 +286,8 @@ def main():
     count = len(mine)
     stream = torch.cuda.current_stream()
     sim = Simulator(cols, device=local, stream=stream)
-    stats_dev = torch.zeros((n, 256), dtype=torch.uint8, device=dev)
-    full_dev = torch.zeros((n, 256), dtype=torch.uint8, device=dev)
+    stats_dev = torch.zeros((n, _abi.STATS.itemsize), dtype=torch.uint8, device=dev)
+    full_dev = torch.zeros((n, _abi.STATS.itemsize), dtype=torch.uint8, device=dev)
     seg_dev = torch.zeros((w.n_segments, _abi.SEG_HIST_WORDS), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -343,7 +343,7 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (pinned) ----
     pk = pack(cols, pinned=True)
-    host_stats = torch.empty((n, 256), dtype=torch.uint8, pin_memory=True).numpy().view(_abi.STATS).reshape(-1)
+    host_stats = torch.empty((n, _abi.STATS.itemsize), dtype=torch.uint8, pin_memory=True).numpy().view(_abi.STATS).reshape(-1)
     e2e_ms = []
     for i in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
@@ -366,7 +366,7 @@ def main():
     e2e_value = ticks_all * len(e2e_ms) / (float(e[0]) / 1e3) if e2e_ms else None
     h2d = int(sum(v.nbytes for k, v in pk.items() if isinstance(v, np.ndarray)) +
               sum(v.nbytes for v in pk["tables"].values()) + 8 * W.TABLE_N + 4 * n)
-    d2h = int(n * 256)
+    d2h = int(n * _abi.STATS.itemsize)
 
     if rank != 0:
         if world > 1:

@@ -130,11 +130,23 @@ typedef struct {
    * decoding, so S:207's idle-server example holds), and emit their first word
    * at its end. */
   uint32_t prefill_mode;
+  /* NEXT-4 KV policy when kv_cap_words > 0: 0 = reserve (above: the whole
+   * context input + R must fit at admission, so contexts never outgrow the
+   * capacity); 1 = preempt (vLLM-style recompute preemption): the head is
+   * admitted if its current context (input + words emitted so far) fits; at an
+   * iteration end whose contexts exceed the capacity the latest admitted
+   * requests go back to the front of the queue (while more than one is in the
+   * system) and, re-admitted, prefill input + emitted again, that prefill's
+   * end emitting their next word.  1 requires prefill_mode = 0. */
+  uint32_t kv_policy;
+  uint32_t _pad;
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;
-} bellman_profile; /* 56 bytes */
+} bellman_profile; /* 64 bytes */
 
 #define BELLMAN_PREFILL_NONBLOCKING 0u
 #define BELLMAN_PREFILL_CONTENDING 1u
+#define BELLMAN_KV_RESERVE 0u
+#define BELLMAN_KV_PREEMPT 1u
 
 /* Controller configuration (R3-R5, R22, R38). */
 typedef struct {
@@ -229,7 +241,7 @@ typedef struct {
   uint64_t n_arrivals;
 } bellman_sim_desc;
 
-/* 256-byte per-scenario summary (a8, a9, a6 logs).  All counts are exact
+/* 272-byte per-scenario summary (a8, a9, a6 logs).  All counts are exact
  * integers; energy_j = (e_in*words_in + e_out*words_out) + p_idle*idle_us/1e6. */
 typedef struct {
   uint64_t scenario_id, ticks, candidates, arrivals, admitted, served, rewritten;
@@ -244,6 +256,12 @@ typedef struct {
   /* NEXT-2: nearest-rank median similarity (0.5-point bin lower edge, centi-points)
    * of rewritten (active) and not rewritten (inactive) admissions, and their counts */
   uint32_t sim_active_p50, sim_inactive_p50, scored_active, scored_inactive;
+  /* NEXT-4 kv_policy 1: requests sent back to the queue, and the context words
+   * prefilled again at their re-admissions (part of words_in).  admitted counts
+   * first admissions; inflight_end counts admitted, unfinished requests
+   * (preempted ones waiting included); sum_queue_us sums every queue stay. */
+  uint32_t preemptions, _pad2;
+  uint64_t recompute_words;
 } bellman_scenario_stats;
 
 typedef struct bellman_sim bellman_sim; /* opaque */

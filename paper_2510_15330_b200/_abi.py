@@ -26,7 +26,7 @@ TRACE = np.dtype([("knot_offset", "<u4"), ("n_knots", "<u4"), ("arrival_cap", "<
 ARRIVAL = np.dtype([("a_us", "<i8"), ("L_words", "<u4"), ("input_words", "<u4"), ("cls", "<u4"), ("_pad", "<u4")])
 PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv_ns_per_word", "<u4"),
                     ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("kv_cap_words", "<u4"), ("prefill_mode", "<u4"),
-                    ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
+                    ("kv_policy", "<u4"), ("_pad", "<u4"), ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
 CTRL = np.dtype([(n, "<u4") for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp", "t1", "t2",
                                        "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))] +
                 [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")])
@@ -42,7 +42,8 @@ STATS_U32 = ["e2e_p50_ms", "e2e_p99_ms", "ttft_p50_ms", "ttft_p99_ms", "median_r
              "segment", "bypassed"]
 STATS_Q = ["sim_active_p50", "sim_inactive_p50", "scored_active", "scored_inactive"]
 STATS = np.dtype([(n, "<u8") for n in STATS_U64] + [(n, "<u4") for n in STATS_U32] +
-                 [("energy_j", "<f8"), ("win_energy_j", "<f8")] + [(n, "<u4") for n in STATS_Q])
+                 [("energy_j", "<f8"), ("win_energy_j", "<f8")] + [(n, "<u4") for n in STATS_Q] +
+                 [("preemptions", "<u4"), ("_pad2", "<u4"), ("recompute_words", "<u8")])
 SECOND_ROW = np.dtype([(n, "<u4") for n in ("arrivals", "admitted", "first_tokens", "completions", "tbt_count",
                                               "idle_us", "words_in", "words_out")] +
                       [(n, "<u8") for n in ("sum_queue_us", "sum_ttft_us", "sum_e2e_us", "sum_tbt_us")])
@@ -51,8 +52,8 @@ CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp"
 RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
 assert ARRIVAL.itemsize == 24
-assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 56
-assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 256
+assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 64
+assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 272
 
 
 class Models(C.Structure):

@@ -120,6 +120,14 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (p.kv_ns_per_word > 1024u) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_ns_per_word > 1024", i);
     if (p.kv_cap_words > (1u << 30)) return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_cap_words > 2^30", i);
     if (p.prefill_mode > BELLMAN_PREFILL_CONTENDING) return fail(nullptr, BELLMAN_EINVAL, "profile %u: unknown prefill_mode", i);
+    if (p.kv_policy > BELLMAN_KV_PREEMPT) return fail(nullptr, BELLMAN_EINVAL, "profile %u: unknown kv_policy", i);
+    if (p.kv_policy == BELLMAN_KV_PREEMPT && p.prefill_mode != BELLMAN_PREFILL_NONBLOCKING)
+      return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_policy 1 (preempt) needs prefill_mode 0", i);
+    // a recompute prefill covers a preempted context, at most the capacity plus one iteration's and one
+    // instant's words (a request over the capacity alone is never preempted): keep it < 2^30 µs (32-bit clock)
+    if (p.kv_policy == BELLMAN_KV_PREEMPT &&
+        (uint64_t)p.prefill_ns_per_word * ((uint64_t)p.kv_cap_words + 2u * BELLMAN_MAX_BATCH) / 1000u >= (1ull << 30))
+      return fail(nullptr, BELLMAN_EINVAL, "profile %u: kv_policy 1: prefill of the capacity >= 2^30 us", i);
     // contending prefill: one iteration may carry max_batch prefills; keep it < 2^30 µs (32-bit clock)
     if (p.prefill_mode == BELLMAN_PREFILL_CONTENDING &&
         (uint64_t)p.max_batch * ((uint64_t)p.prefill_ns_per_word * 65535u / 1000u + 1u) >= (1ull << 30))
@@ -175,7 +183,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, off_ord, total;
+      off_drows, off_dctrl, off_arr, off_ord, off_pre, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -314,6 +322,12 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
   L.off_arr = take(sizeof(bellman_arrival) * d->n_arrivals);
   L.off_ord = take(sizeof(uint32_t) * d->n_scenarios);
+  // NEXT-4 preemption scratch (per CTA: slot side state + the preempted stack),
+  // only when some profile preempts
+  bool pre = false;
+  for (uint32_t i = 0; i < d->n_profiles; ++i)
+    pre = pre || (d->profiles[i].kv_policy == BELLMAN_KV_PREEMPT && d->profiles[i].kv_cap_words > 0);
+  L.off_pre = take(pre ? sizeof(PreScratch) * kMaxPreCtas : 0);
   L.total = o;
   return L;
 }
@@ -371,6 +385,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     delete sim;
     return fail(nullptr, BELLMAN_ECUDA, "occupancy query failed");
   }
+  if (sim->grid > (int)kMaxPreCtas) sim->grid = (int)kMaxPreCtas;  // one preemption scratch per CTA
   sim->calibrated.assign(desc->n_scenarios, 0);
   sim->calib_src.assign(desc->n_scenarios, BELLMAN_NONE);
   for (uint64_t s = 0; s < desc->n_scenarios; ++s) {
@@ -432,6 +447,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.dbg_ctrl = (bellman_ctrl_row *)(ws + L.off_dctrl);
   P.arrivals = (const bellman_arrival *)(ws + L.off_arr);
   P.order = nullptr;
+  P.pre = (PreScratch *)(ws + L.off_pre);
   sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();

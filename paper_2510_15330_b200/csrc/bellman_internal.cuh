@@ -40,6 +40,23 @@ struct alignas(16) WarpHist {
 };
 static_assert(sizeof(WarpHist) % 16 == 0, "WarpHist is zeroed with 16-byte stores");
 
+// NEXT-4 preemption scratch of one CTA (one warp, one scenario at a time), in
+// global memory: it is touched only by preempting profiles, at admissions,
+// prefill ends, joins and preemptions.  Slot s = lane + 32 k.
+struct PreEnt {   // a preempted request waiting at the queue front
+  uint64_t a;     // arrival (absolute µs)
+  uint64_t lt;    // its last word (absolute µs)
+  uint64_t enq;   // start of this queue stay
+  uint32_t in, R, em, _pad;  // input words, realized length, words emitted
+};
+struct PreScratch {
+  uint64_t lt[64];   // last word of a re-admitted request (absolute µs)
+  uint32_t seq[64];  // admission order
+  uint32_t em[64];   // words emitted before the current phase (prefill: before it; ready: so far)
+  PreEnt stk[64];    // preempted requests, top = stk[n - 1] (the queue front)
+};
+constexpr uint32_t kMaxPreCtas = 4096;  // CTAs of one launch (B200: 148 x 16)
+
 struct Params {
   const bellman_scenario *sc;
   const DevTrace *traces;
@@ -69,6 +86,7 @@ struct Params {
   unsigned long long *seg_hist;  // [n_segments][kSegWords]
   unsigned int *counter;         // work counter of this launch
   const uint32_t *order;         // heavy-first scenario order of a whole-set run, else NULL
+  PreScratch *pre;               // [kMaxPreCtas] NEXT-4 preemption scratch (preempting profiles only)
   uint64_t first, count, stride;
   uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
 };

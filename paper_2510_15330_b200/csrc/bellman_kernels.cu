@@ -301,7 +301,7 @@ __device__ __forceinline__ uint32_t prefill_us(uint32_t pf_ns, uint32_t in) {
 // Write-only counters (a8) are lane-distributed: counter i lives in lane i's
 // register `ctr` and is bumped with a predicated add of a warp-uniform value
 // (no branch, no memory), then read once by shuffle in the epilogue.
-enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL = 3, CT_WIN_SERVED = 4, CT_WORDS_IN = 5, CT_IDLE = 6, CT_WIN_WORDS_IN = 7, CT_WIN_IDLE = 8, CT_SUM_QUEUE = 9, CT_SUM_TTFT = 10, CT_SUM_E2E = 11, CT_N };
+enum : uint32_t { CT_ADMITTED = 0, CT_SERVED = 1, CT_REWRITTEN = 2, CT_SLO_VIOL = 3, CT_WIN_SERVED = 4, CT_WORDS_IN = 5, CT_IDLE = 6, CT_WIN_WORDS_IN = 7, CT_WIN_IDLE = 8, CT_SUM_QUEUE = 9, CT_SUM_TTFT = 10, CT_SUM_E2E = 11, CT_PREEMPT = 12, CT_RECOMP = 13, CT_N };
 
 // One Cold block per warp of the CTA, in static shared memory so that every
 // access is a 32-bit LDS/STS off a known base (no generic pointer).
@@ -587,6 +587,9 @@ struct Sim {
   __device__ __forceinline__ uint32_t n_pending() const { return cont() ? n_pend : 0u; }
   // the KV term's coefficient: a compile-time 0 in the KV-free instantiation
   __device__ __forceinline__ uint32_t kvc() const { return KV0 ? 0u : kv; }
+  // NEXT-4 KV preemption (kv_policy 1): never in the TBT-specialised instantiation
+  __device__ __forceinline__ bool pre() const { return TBTO ? false : kvpol != 0u; }
+  __device__ __forceinline__ bool stk_any() const { return pre() && pstk != 0u; }
   __device__ __forceinline__ Cold &cold() const { return g_cold[kWarpsPerBlock == 1 ? 0u : wid]; }
 #ifndef BELLMAN_AB_REGCTR
   uint64_t ctr;  // lane-distributed write-only counters (CT_*)
@@ -645,7 +648,11 @@ struct Sim {
   uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
   uint32_t pmode;         // NEXT-4 prefill_mode (generic instantiation only)
   uint32_t n_pend, pend_us;  // contending: admitted, prefill not started; sum of their prefill times
-  uint32_t kv_res;        // NEXT-4: sum of (input + R) over requests in the system
+  uint32_t kv_res;        // NEXT-4: contexts in the system: reserve policy sum of (input + R),
+                          // preempt policy sum of (input + words emitted)
+  uint32_t kvpol;         // NEXT-4: kv_policy 1 with a capacity (generic instantiation only)
+  uint32_t pstk, pseq;    // preempted requests waiting at the queue front; next admission order
+  PreScratch *ps;         // this CTA's preemption scratch
   uint32_t adm_blocked;   // NEXT-4: the arrived queue head does not fit the KV capacity
   uint32_t head_t;     // arrival offset of the queue head (0 if before E), INF32 when none remains
   // ---- counters (a8)
@@ -776,6 +783,7 @@ struct Sim {
   // the words of an iteration end: B words, TBT gaps, K += B (a5)
   __device__ __forceinline__ void iteration_words() {
     words_out += B;
+    if (pre()) kv_res += B;  // every decoding context grows by its word
     if (win_now) win_words_out += B;
     // TBT: the B gaps of this end; UTIL (NEXT-3): the batch size B, one sample
     const bool tbt = sig(BELLMAN_SIG_TBT), util = sig(BELLMAN_SIG_UTIL);
@@ -806,7 +814,8 @@ struct Sim {
     const uint32_t te = iter_end;
     if (te >= stop_static || te >= sec_bound || te >= kRebaseAt || next_pf <= te || ticks - 1u == next_done)
       return false;
-    if (in_sys < maxb && !adm_blocked && head_t <= te) return false;
+    if (in_sys < maxb && !adm_blocked && (head_t <= te || stk_any())) return false;
+    if (pre() && in_sys > 1u && (uint64_t)kv_res + B > cold().kv_cap) return false;  // the end preempts
     T = te;
     iteration_words();
     busy = 0;
@@ -857,6 +866,73 @@ struct Sim {
       complete_sig(se, ndone, ns);
     }
     busy = 0;
+    if (pre() && in_sys > 1u && kv_res > cold().kv_cap) preempt();
+  }
+
+  // NEXT-4 kv_policy 1 at an iteration end whose contexts exceed the capacity:
+  // while more than one request is in the system, the latest admitted one
+  // (decoding, decode-ready or prefilling) leaves it for the top of the
+  // preempted stack (the queue front), keeping its words and realized length.
+  __device__ __forceinline__ void preempt() {
+    const uint32_t it = ticks - 1u, cap = cold().kv_cap;
+    const uint64_t Ta = ab(T);
+    bool dec = false, pfl = false;
+    while (in_sys > 1u && kv_res > cap) {
+      const bool in0 = sph[0] == PH_PREFILL || sph[0] == PH_READY || sph[0] == PH_DEC;
+      const bool in1 = sph[1] == PH_PREFILL || sph[1] == PH_READY || sph[1] == PH_DEC;
+      const uint32_t q0 = in0 ? ps->seq[lane] + 1u : 0u, q1 = in1 ? ps->seq[lane + 32u] + 1u : 0u;
+      const uint32_t best = __reduce_max_sync(FULL, q0 > q1 ? q0 : q1);
+      const uint32_t own = (uint32_t)__ffs(__ballot_sync(FULL, q0 == best || q1 == best)) - 1u;
+      uint32_t ph = 0, ctx = 0;
+      if (lane == own) {
+        const uint32_t s = q1 == best ? 1u : 0u, slot = lane + 32u * s;
+        ph = s ? sph[1] : sph[0];
+        const uint32_t R = s ? sR[1] : sR[0], in = s ? sin[1] : sin[0];
+        // words emitted so far: a decoding request's follow from its completion iteration
+        const uint32_t em = ph == PH_DEC ? R - ((s ? sdn[1] : sdn[0]) - it) : ps->em[slot];
+        const uint64_t lt = ph == PH_DEC ? Ta : (ph == PH_READY ? ab(s ? sp[1] : sp[0]) : ps->lt[slot]);
+        PreEnt &e = ps->stk[pstk];
+        e.a = s ? sa[1] : sa[0];
+        e.lt = lt;
+        e.enq = Ta;
+        e.in = in;
+        e.R = R;
+        e.em = em;
+        ctx = in + em;
+        if (s) sph[1] = PH_EMPTY; else sph[0] = PH_EMPTY;
+      }
+      ph = __shfl_sync(FULL, ph, own);
+      ctx = __shfl_sync(FULL, ctx, own);
+      if (ph == PH_DEC) {
+        B--;
+        kv_sub((uint64_t)kvc() * ctx);  // its context leaves the KV term
+        dec = true;
+      } else if (ph == PH_READY) {
+        n_ready--;
+      } else {
+        pfl = true;
+      }
+      pstk++;
+      kv_res -= ctx;
+      in_sys--;
+      cadd(CT_PREEMPT, 1u);
+    }
+    if (dec) {
+      uint32_t dmin = 0xffffffffu;
+      if (sph[0] == PH_DEC) dmin = min(dmin, sdn[0]);
+      if (sph[1] == PH_DEC) dmin = min(dmin, sdn[1]);
+      next_done = __reduce_min_sync(FULL, dmin);
+      batch_changed();
+    }
+    if (pfl) {
+      uint32_t mpf = 0xffffffffu;
+      if (sph[0] == PH_PREFILL) mpf = min(mpf, sp[0] - T);
+      if (sph[1] == PH_PREFILL) mpf = min(mpf, sp[1] - T);
+      const uint32_t m = __reduce_min_sync(FULL, mpf);
+      next_pf = (m == INF32) ? INF32 : T + m;
+    }
+    adm_blocked = 0;
+    __syncwarp();
   }
 
   // Prefill ends at instants in [T, lim) (first words, R=1 completions, R9).
@@ -871,9 +947,37 @@ struct Sim {
     uint64_t ttft_l = 0, e2e_l = 0;
     uint32_t nfirst = 0, n1 = 0, nslo = 0, nrdy = 0, kfree = 0;
     uint32_t mpf = 0xffffffffu;
+    uint64_t rgap_l = 0;  // NEXT-4 preemption: TBT gaps of recompute words
+    uint32_t nrec = 0;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const bool f = sph[s] == PH_PREFILL && sp[s] < lim;
+      bool f = sph[s] == PH_PREFILL && sp[s] < lim;
+      if (pre() && f) {
+        // a re-admitted request's recompute prefill ends: its next word, a decode
+        // word whose TBT gap runs from its last word before the preemption
+        const uint32_t slot = lane + 32u * s, em = ps->em[slot];
+        if (em > 0u) {
+          f = false;
+          const uint64_t g = ab(sp[s]) - ps->lt[slot];
+          rgap_l += g;
+          nrec++;
+          if (em + 1u == sR[s]) {
+            const uint64_t e = ab(sp[s]) - sa[s];
+            kfree += sin[s] + sR[s];
+            e2e_l += e;
+            nslo += e > slo_us;
+            n1++;
+            atomicAdd(&h.e2e[lat_bin_us(e)], 1u);
+            sph[s] = PH_EMPTY;
+          } else {
+            ps->em[slot] = em + 1u;
+            sph[s] = PH_READY;
+            nrdy++;
+          }
+        } else {
+          ps->em[slot] = 1u;
+        }
+      }
       nfirst += __popc(__ballot_sync(FULL, f));
       if (f) {
         const uint64_t tt = ab(sp[s]) - sa[s];
@@ -899,6 +1003,25 @@ struct Sim {
     const uint64_t st = warp_sum_split(ttft_l);
     cadd(CT_SUM_TTFT, st);
     words_out += nfirst;
+    if (pre()) {  // every word grows its context; recompute words are decode words (TBT)
+      const uint32_t nr = __reduce_add_sync(FULL, nrec);
+      kv_res += nfirst + nr;
+      if (nr) {
+        const uint64_t rg = warp_sum_split(rgap_l);
+        words_out += nr;
+        if (win_now) win_words_out += nr;
+        if (sig(BELLMAN_SIG_TBT)) {
+          acc_sum += rg;
+          acc_cnt += nr;
+        }
+        if (DBG && dbg && lane == 0) {
+          atomicAdd(&row(ab(Tn))->tbt_count, nr);
+          atomicAdd(&row(ab(Tn))->words_out, nr);
+          atomicAdd((unsigned long long *)&row(ab(Tn))->sum_tbt_us, (unsigned long long)rg);
+        }
+        if (DBG) __syncwarp();
+      }
+    }
     if (sig(BELLMAN_SIG_TTFT)) {  // NEXT-3 signal: mean TTFT of the second's first words
       acc_sum += st;
       acc_cnt += nfirst;
@@ -931,6 +1054,65 @@ struct Sim {
     }
   }
 
+  // NEXT-4 kv_policy 1: re-admit preempted requests from the top of the stack
+  // (the queue front) while a slot is free and the context input + emitted
+  // fits (an empty system always admits); each prefills that context again.
+  // Returns false if one stays waiting (FIFO: nothing behind it is admitted).
+  __device__ __forceinline__ bool readmit(uint64_t Ta) {
+    const uint32_t Tn = T;
+    while (pstk) {
+      if (in_sys >= maxb) return false;
+      const PreEnt e = ps->stk[pstk - 1u];
+      const uint32_t ctx = e.in + e.em;
+      if (in_sys != 0u && (uint64_t)kv_res + ctx > cold().kv_cap) {
+        adm_blocked = 1;
+        return false;
+      }
+      pstk--;
+      const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY), f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
+      const bool s1 = f0 == 0u;
+      const uint32_t sl = (uint32_t)__ffs(s1 ? f1 : f0) - 1u;
+      const uint32_t pf = prefill_us(cold().pf_ns, ctx);
+      if (lane == sl) {
+        const uint32_t slot = sl + (s1 ? 32u : 0u);
+        ps->seq[slot] = pseq;
+        ps->em[slot] = e.em;
+        ps->lt[slot] = e.lt;
+        if (!s1) {
+          sa[0] = e.a;
+          sp[0] = Tn + pf;
+          sR[0] = e.R;
+          sin[0] = e.in;
+          sph[0] = PH_PREFILL;
+        } else {
+          sa[1] = e.a;
+          sp[1] = Tn + pf;
+          sR[1] = e.R;
+          sin[1] = e.in;
+          sph[1] = PH_PREFILL;
+        }
+      }
+      pseq++;
+      kv_res += ctx;
+      in_sys++;
+      if (Tn + pf < next_pf) next_pf = Tn + pf;
+      cadd(CT_WORDS_IN, ctx);
+      if (win_now) cadd(CT_WIN_WORDS_IN, ctx);
+      cadd(CT_SUM_QUEUE, Ta - e.enq);
+      cadd(CT_RECOMP, ctx);
+      if (sig(BELLMAN_SIG_INPUT)) {
+        acc_sum += ctx;
+        acc_cnt = 1u;
+      }
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Ta)->words_in, ctx);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_queue_us, (unsigned long long)(Ta - e.enq));
+      }
+      __syncwarp();
+    }
+    return true;
+  }
+
   // ------------------------------------------------------------------ a7 (+a3)
   // FIFO admission at an admission point (R7): the queue head is admitted while
   // a slot is free and it has arrived (and, NEXT-4, its context fits the KV
@@ -943,6 +1125,8 @@ struct Sim {
     const uint32_t Tn = T;
     const uint64_t Ta = ab(Tn);
     adm_blocked = 0;
+    if (stk_any() && !readmit(Ta)) return;  // preempted requests first (the queue front)
+    if (pre() && (in_sys >= maxb || head_t > Tn)) return;
     uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY), f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
     uint32_t n = 0, n_byp = 0;
     PROF_MARK(pa_);
@@ -959,8 +1143,9 @@ struct Sim {
       const uint32_t kvcap = cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
-        // the contexts in the system; an oversized head enters an empty system
-        const uint32_t need = in + R;
+        // the contexts in the system; an oversized head enters an empty system.
+        // Preempt policy: only the current context, the input
+        const uint32_t need = pre() ? in : in + R;
         if ((uint64_t)kv_res + need > kvcap && in_sys != 0u) {
           adm_blocked = 1;
           break;
@@ -1000,6 +1185,11 @@ struct Sim {
       if (s1) f1 = fm & (fm - 1u); else f0 = fm & (fm - 1u);
       // contending prefill: the prefill runs inside the next iteration (start_iteration)
       const uint32_t ph = cont() ? PH_PENDING : PH_PREFILL;
+      if (pre() && lane == sl) {
+        ps->seq[sl + (s1 ? 32u : 0u)] = pseq;
+        ps->em[sl + (s1 ? 32u : 0u)] = 0u;
+      }
+      if (pre()) pseq++;
       if (lane == sl) {
         if (!s1) {
           sa[0] = a;
@@ -1070,7 +1260,12 @@ struct Sim {
     // a KV-blocked head may fit after an ingest changes r: stop at the second boundary
     if (adm_blocked && sec_bound < stop) stop = sec_bound;
     if (stop > kJumpCap) stop = kJumpCap;  // keeps the next iteration end inside the window
-    const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
+    uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
+    if (pre() && in_sys > 1u) {  // NEXT-4: no leaped end may push the contexts over the capacity
+      const uint32_t cap = cold().kv_cap;
+      const uint32_t nk = kv_res < cap ? (cap - kv_res) / B : 0u;
+      if (nk < nmax) nmax = nk;
+    }
     if (nmax == 0 || stop <= T + 1u) return;
     const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
     uint32_t q = KV0 ? 0u : kq, rr = KV0 ? 0u : kr, done = 0;
@@ -1106,6 +1301,7 @@ struct Sim {
       }
       if (n) {
         const uint64_t words = (uint64_t)n * B;
+        if (pre()) kv_res += (uint32_t)words;
         ticks += n;
         T += used;
         words_out += words;
@@ -1148,10 +1344,12 @@ struct Sim {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         if (sph[s] == PH_READY) {
+          // words emitted when joining: 1 (the first), more for a re-admitted request
+          const uint32_t ej = pre() ? ps->em[lane + 32u * s] : 1u;
           sph[s] = PH_DEC;
-          sdn[s] = it0 + sR[s] - 2u;  // words 2..R at the ends of iterations it0..it0+R-2
+          sdn[s] = it0 + sR[s] - ej - 1u;  // words ej+1..R at the ends of iterations it0..it0+R-ej-1
           al += Tn - sp[s];  // 32-bit offsets: the difference is exact modulo 2^32
-          kadd += sin[s] + 1u;
+          kadd += sin[s] + ej;
           jn = min(jn, sdn[s]);
         }
       }
@@ -1341,6 +1539,9 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   S.n_pend = S.pend_us = 0;
   S.kv_res = 0;
   S.adm_blocked = 0;
+  S.kvpol = (pr.kv_policy == BELLMAN_KV_PREEMPT && pr.kv_cap_words > 0) ? 1u : 0u;
+  S.pstk = S.pseq = 0;
+  S.ps = p.pre + (blockIdx.x * kWarpsPerBlock + warp_in_block());
   S.last_j = 0;
 #ifndef BELLMAN_AB_REGCTR
   S.ctr = 0;
@@ -1425,7 +1626,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
       continue;
     }
     // the decode loop is idle here: admission point (R7), then the next iteration
-    if (S.in_sys < S.maxb && !S.adm_blocked && S.head_t <= tn) {
+    if (S.in_sys < S.maxb && !S.adm_blocked && (S.head_t <= tn || S.stk_any())) {
       PROF(5);
       PROFC(12, S.admit(p, h));
     }
@@ -1546,7 +1747,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     o.idle_us = C_[CT_IDLE];
     o.end_us = end;
     o.queued_end = queued;
-    o.inflight_end = S.in_sys;
+    o.inflight_end = S.in_sys + S.pstk;  // admitted, unfinished (preempted ones waiting too)
     o.win_served = C_[CT_WIN_SERVED];
     o.win_words_in = C_[CT_WIN_WORDS_IN];
     o.win_words_out = S.win_words_out;
@@ -1567,7 +1768,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     o.last_deact_s = S.cold().last_deact;
     o.active_ingests = S.cold().active_ingests;
     uint32_t fl = S.cold().flags | BELLMAN_FLAG_DONE;
-    if (queued + S.in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
+    if (queued + S.in_sys + S.pstk > 0) fl |= BELLMAN_FLAG_TRUNCATED;
     o.flags = fl;
     o.segment = sc.segment;
     o.bypassed = S.cold().bypassed;
@@ -1584,6 +1785,9 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     o.sim_inactive_p50 = pqi[0];
     o.scored_active = C_[CT_REWRITTEN];
     o.scored_inactive = C_[CT_ADMITTED] - C_[CT_REWRITTEN];
+    o.preemptions = (uint32_t)C_[CT_PREEMPT];
+    o._pad2 = 0;
+    o.recompute_words = C_[CT_RECOMP];
     p.stats[sid] = o;
   }
   __syncwarp();
@@ -1614,7 +1818,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
 #endif
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
-    } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING) {
+    } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
+               (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0)) {
       // TBT-only loop, specialised once more on a KV-free cost law (kv = 0)
       if (p.profs[sc.profile].kv_ns_per_word == 0)
         run_one<false, true, true>(p, sid, sc, cc, lane, h);

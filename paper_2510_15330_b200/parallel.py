@@ -3,7 +3,7 @@
 Scenarios are independent units: rank r of W simulates ids r, r+W, r+2W, ...
 (interleaving puts every (rate, controller) cell on every rank, which balances
 per-tick cost).  The only collective is at the end of a step: all_gather of
-the 256-byte summary records (NCCL over NVLink on GPUs, gloo in CPU tests)
+the 272-byte summary records (NCCL over NVLink on GPUs, gloo in CPU tests)
 and an all_reduce(SUM) of the integer segment histograms.  Integer sums are
 order-independent, so results are bit-identical for any world size.
 """
@@ -12,7 +12,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-REC = 256  # bytes per bellman_scenario_stats
+REC = 272  # bytes per bellman_scenario_stats
 
 
 def shard_count(n: int, rank: int, world: int) -> int:
@@ -25,8 +25,8 @@ def shard_rows(full_rows: torch.Tensor, rank: int, world: int) -> torch.Tensor:
 
 
 def gather_summaries(local: torch.Tensor, n: int, rank: int, world: int, out: torch.Tensor | None = None):
-    """All-gather every rank's (count_r, 256) uint8 record block and return the
-    (n, 256) records in scenario-id order (on every rank)."""
+    """All-gather every rank's (count_r, REC) uint8 record block and return the
+    (n, REC) records in scenario-id order (on every rank)."""
     if world == 1:
         return local[:n]
     m = (n + world - 1) // world

@@ -181,7 +181,7 @@ def test_debug_series_rows_and_controller_log():
 
     from paper_2510_15330_b200 import Simulator
 
-    ws = [W.config_c1(), W.config_c3(n_seeds=1), W.config_c2(n_seeds=1, rates=[0.5, 2.5, 6.0])]
+    ws = [W.config_c1(), W.config_c3(n_seeds=1), W.config_c2(n_seeds=1, rates=[0.5, 2.5, 6.0]), _preempt_workload()]
     for w in ws:
         sel = list(range(0, w.n_scenarios, max(1, w.n_scenarios // 12)))
         for sid in sel:
@@ -246,6 +246,36 @@ def test_next4_kv_capacity_admission():
     w.scenarios = sc
     bad, st = check_all(w.columns())
     _assert_ok(bad)
+
+
+def _preempt_workload():
+    """NEXT-4 KV preemption (kv_policy 1): paper-trace scenarios under several
+    capacities, with and without the KV cost term, every law (the rewrite
+    decides R, kept across re-admissions), TBT / E2E / INPUT signals, class
+    bypass, drain and cutoff, next to reserve-policy and uncapped profiles."""
+    import dataclasses
+
+    w = W.config_c3(n_seeds=1)
+    w.class_cum = W.MIXED_CLASSES
+    pre = dict(kv_policy=1)
+    w.profiles = [dict(W.PROFILES["P24"], kv_cap_words=c, **pre) for c in (60_000, 150_000, 300_000)] + \
+                 [dict(W.PROFILES["L8B"], kv_cap_words=120_000, **pre), dict(W.PROFILES["P24"], kv_cap_words=150_000),
+                  W.PROFILES["P24"], dict(W.PROFILES["L8B"], kv_cap_words=9_000, **pre)]
+    w.ctrls[5] = dataclasses.replace(w.ctrls[5], bypass_mask=2, min_words_bypass=470)
+    w.ctrls[7] = dataclasses.replace(w.ctrls[7], signal=W.SIG_E2E, t1=8_000_000, t2=40_000_000)
+    w.ctrls[9] = dataclasses.replace(w.ctrls[9], signal=W.SIG_INPUT, t1=20_000, t2=60_000)
+    sc = []
+    for i, s in enumerate(w.scenarios[::5]):
+        sc.append(dataclasses.replace(s, profile=i % len(w.profiles), mode=i % 2,
+                                      horizon_us=(1920 if i % 2 else 700) * W.US))
+    w.scenarios = sc
+    return w
+
+
+def test_next4_kv_preemption():
+    bad, st = check_all(_preempt_workload().columns())
+    _assert_ok(bad)
+    assert int(st["preemptions"].sum()) > 100 and int(st["recompute_words"].sum()) > 0
 
 
 def test_next4_trace_replay():

@@ -27,7 +27,7 @@ def _records(cols, ids):
     import oracle
 
     b = oracle.Bound(cols)
-    recs = np.zeros((len(ids), 32), dtype=np.uint64)  # 256 B = 32 u64 words
+    recs = np.zeros((len(ids), 34), dtype=np.uint64)  # 272 B = 34 u64 words
     seg = np.zeros((int(cols["n_segments"]), 3), dtype=np.int64)
     for i, sid in enumerate(ids):
         r = oracle.run_scenario(b, int(sid))
@@ -49,7 +49,7 @@ def _worker(rank, world, port, cols, q):
     n = len(cols["sc_seed"])
     ids = W.shard(n, rank, world)
     recs, seg = _records(cols, ids)
-    local = torch.from_numpy(recs.view(np.uint8).reshape(len(ids), 256).copy())
+    local = torch.from_numpy(recs.view(np.uint8).reshape(len(ids), 272).copy())
     full = P.gather_summaries(local, n, rank, world)
     segt = P.reduce_segments(torch.from_numpy(seg))
     if rank == 0:
@@ -73,7 +73,7 @@ def test_gloo_gather_matches_single_process(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert np.array_equal(full.view(np.uint64).reshape(n, 32), want)
+    assert np.array_equal(full.view(np.uint64).reshape(n, 34), want)
     assert np.array_equal(seg, want_seg)
 
 

@@ -635,6 +635,7 @@ struct Sim {
   uint32_t next_pf;    // min prefill end over prefilling slots
   uint32_t n_ready, B, in_sys;
   uint32_t cbase;             // t0 + slope * max(0, B - knee)
+  uint32_t cbm;               // KV0: floor((2^32 - 1) / cbase)
   uint32_t kq, kr;            // kv * K = kq * 1000 + kr, K = context words of the batch
   uint32_t kstep_q, kstep_r;  // kv * B = kstep_q * 1000 + kstep_r (growth per iteration)
   uint32_t win_now;           // T in [w0, w1)
@@ -741,6 +742,9 @@ struct Sim {
   // B changed: cost base and per-iteration KV growth
   __device__ __forceinline__ void batch_changed() {
     cbase = t0 + slope * (B > knee ? B - knee : 0u);
+    // KV-free instantiation: the leap divides by cbase; floor((2^32 - 1) / cbase)
+    // turns that into a multiply-high and one correction step
+    if (KV0) cbm = 0xFFFFFFFFu / cbase;
     if (KV0) return;
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
@@ -1275,7 +1279,13 @@ struct Sim {
       const uint32_t left = nmax - done;
       uint32_t n = 0, used = 0;
       if (kvc() == 0) {
-        const uint32_t nn = room / cb;
+        uint32_t nn;
+        if (KV0) {  // umulhi(room, floor((2^32-1)/cb)) is floor(room / cb) or one less
+          nn = __umulhi(room, cbm);
+          if (room - nn * cb >= cb) nn++;
+        } else {
+          nn = room / cb;
+        }
         n = nn < left ? nn : left;
         used = n * cb;
       } else {

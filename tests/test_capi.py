@@ -44,6 +44,33 @@ def test_struct_sizes_and_validation():
         sim.workspace_bytes(sim.pack(bad))
 
 
+def test_kv_policy_validation_and_scratch():
+    """NEXT-4 preemption: unknown policies, preemption with contending prefill
+    and recompute prefills that could outgrow the 32-bit event clock are
+    rejected; a preempting profile adds the per-CTA scratch to the workspace."""
+    from paper_2510_15330_b200 import _abi as A, sim
+    import workloads as W
+
+    def cols(**prof):
+        c = W.config_c2(n_seeds=1, rates=[1.0]).columns()
+        for k, v in prof.items():
+            c[k] = c[k].copy()
+            c[k][0] = v
+        return c
+
+    base = sim.workspace_bytes(sim.pack(cols(prof_kv_cap=50_000)))
+    pre = sim.workspace_bytes(sim.pack(cols(prof_kv_cap=50_000, prof_kv_policy=1)))
+    assert pre - base >= 4096 * 3584
+    assert sim.workspace_bytes(sim.pack(cols(prof_kv_cap=0, prof_kv_policy=1))) == \
+        sim.workspace_bytes(sim.pack(cols(prof_kv_cap=0)))  # no capacity: nothing to preempt
+    with pytest.raises(A.BellmanError, match="unknown kv_policy"):
+        sim.workspace_bytes(sim.pack(cols(prof_kv_policy=2)))
+    with pytest.raises(A.BellmanError, match="needs prefill_mode 0"):
+        sim.workspace_bytes(sim.pack(cols(prof_kv_cap=50_000, prof_kv_policy=1, prof_prefill_mode=1)))
+    with pytest.raises(A.BellmanError, match="prefill of the capacity"):
+        sim.workspace_bytes(sim.pack(cols(prof_kv_cap=2**28, prof_kv_policy=1)))
+
+
 def test_sass_has_no_fp_outside_energy():
     """Kernel built for sm_100a; the tick kernel's SASS uses warp vote/shuffle/
     reduce instructions (the warp-level design) and compiles without spills

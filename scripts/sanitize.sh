@@ -6,7 +6,9 @@ cat > /tmp/san_run.py <<'PY'
 import sys; sys.path.insert(0, '.')
 import torch, workloads as W
 from paper_2510_15330_b200 import Simulator
-for w in (W.config_c1(), W.config_c2(n_seeds=1, rates=[0.5, 4.0], horizon_s=120), W.config_paper_pair(0)):
+pre = W.config_paper_pair(1)  # NEXT-4 preemption (global scratch, re-admission stack)
+pre.profiles = [dict(p, kv_cap_words=150_000, kv_policy=1) for p in pre.profiles]
+for w in (W.config_c1(), W.config_c2(n_seeds=1, rates=[0.5, 4.0], horizon_s=120), W.config_paper_pair(0), pre):
     for s in w.scenarios[:2]:
         s.record |= 2
     sim = Simulator(w.columns()); sim.run(); torch.cuda.synchronize()

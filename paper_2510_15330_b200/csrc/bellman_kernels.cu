@@ -496,6 +496,7 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
   uint32_t *const series = reinterpret_cast<uint32_t *>((uint64_t)g4.x | ((uint64_t)g4.y << 32));
   if (series) {
     const uint32_t n = g4.z;
+    __syncwarp();  // every lane's read of the state precedes lane 0's write
     if (lane == 0) {
       if (n < g4.w) series[n] = x;
       else c.flags |= BELLMAN_FLAG_SERIES_OVERFLOW;

@@ -140,6 +140,54 @@ def test_sharded_runs_match_single_run():
         assert np.array_equal(st.view(np.uint8), full.view(np.uint8))
 
 
+def _full_size_sampled(w, n_sample):
+    """A BASELINE config at full size in bench.py's launch configuration (one
+    whole-set launch, heavy-first order): a deterministic stride sample of
+    records vs the oracle, and on every record the properties that hold at
+    any size — written, arrivals = admitted + queued, admitted = served +
+    in flight, a drained run leaves nothing behind, energy is the fp64 formula
+    of the record's own integers (R19)."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    cols = w.columns()
+    sim = Simulator(cols)
+    sim.run()
+    torch.cuda.synchronize()
+    st = sim.stats()
+    assert sim.last_launches == 1
+    n = w.n_scenarios
+    sids = np.arange(0, n, max(1, n // n_sample), dtype=np.uint64)
+    rs = oracle.run_batch(oracle.Bound(cols), sids)
+    bad = [(int(s), e) for s, o in zip(sids, rs) for e in [compare(st[int(s)], o, int(s))] if e]
+    _assert_ok(bad)
+    assert np.all(st["flags"] & 0x100)
+    assert np.array_equal(st["scenario_id"], np.arange(n))
+    assert np.array_equal(st["arrivals"], st["admitted"] + st["queued_end"])
+    assert np.array_equal(st["admitted"], st["served"] + st["inflight_end"])
+    drained = (st["flags"] & 1) == 0
+    assert np.all(st["queued_end"][drained] == 0) and np.all(st["inflight_end"][drained] == 0)
+    prof = cols["prof_e_in"][0], cols["prof_e_out"][0], cols["prof_p_idle"][0]
+    assert np.all(cols["prof_e_in"] == prof[0]) and np.all(cols["prof_e_out"] == prof[1])
+    e = (prof[0] * st["words_in"].astype(np.float64) + prof[1] * st["words_out"].astype(np.float64)) + \
+        prof[2] * st["idle_us"].astype(np.float64) / 1e6
+    assert np.array_equal(e, st["energy_j"])
+    return st
+
+
+def test_c5_full_size_sampled():
+    """BASELINE configs[4]: 2^20 scenarios (one GPU's shard of the 8-GPU sweep)."""
+    st = _full_size_sampled(W.config_c5(), 96)
+    assert int(st["ticks"].sum()) > 5e10
+
+
+def test_c4_full_size_sampled():
+    """BASELINE configs[3]: 24 h diurnal traces with bursts, 4096 scenarios."""
+    st = _full_size_sampled(W.config_c4(), 16)
+    assert int(st["ticks"].max()) > 10**6
+
+
 def test_c2_full_bench_config():
     """BASELINE configs[1] at full size, in the launch configuration bench.py
     times: every one of the 2048 records vs the oracle, and the per-segment

@@ -160,8 +160,8 @@ __device__ __forceinline__ uint32_t warp_in_block() { return kWarpsPerBlock == 1
 // One queued request in the arrival lookahead buffer (32 bytes).
 struct alignas(16) QEnt {
   uint64_t a;    // arrival time (absolute µs)
-  uint32_t in;   // input words | request class << 16 (NEXT-3)
-  uint32_t U;    // realized unbounded length
+  uint32_t in;   // input words | request class << 16 (NEXT-3) | bypass rule holds << 31
+  uint32_t U;    // realized unbounded length | similarity bin if not rewritten << 24
   uint32_t P;    // predicted length
   uint32_t fcq;  // compliance factor Q16 (bits 0-19) | similarity noise + 2048 (bits 20-31)
   uint32_t pf;   // prefill duration max(1, floor(prefill_ns * input / 1000)) µs
@@ -172,12 +172,6 @@ struct alignas(16) QEnt {
 // ingests, refills), not per iteration.  Lives in shared memory, one per warp,
 // so the event loop keeps its hot state in registers without spilling.
 // one entry written as two 16-byte stores (lanes write entries 32 bytes apart)
-__device__ __forceinline__ void store_qent(QEnt &q, uint64_t a, uint32_t in, uint32_t U, uint32_t P, uint32_t fcq,
-                                           uint32_t pf, uint32_t j) {
-  uint4 *w = reinterpret_cast<uint4 *>(&q);
-  w[0] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), in, U);
-  w[1] = make_uint4(P, fcq, pf, j);
-}
 static_assert(sizeof(QEnt) == 32 && offsetof(QEnt, in) == 8 && offsetof(QEnt, P) == 16, "QEnt layout");
 
 struct alignas(16) Cold {
@@ -213,6 +207,20 @@ struct alignas(16) Cold {
 static_assert(offsetof(Cold, ringA) == 0 && offsetof(Cold, rung) == 16 && offsetof(Cold, first_act) == 32 &&
                   offsetof(Cold, t1) == 48 && offsetof(Cold, series) == 64 && offsetof(Cold, ring) == 80,
               "controller state groups g0..g4 of Cold");
+
+// At refill, per request and independent of r: whether a bypass rule (NEXT-3,
+// S:267) holds, and the similarity bin it scores if not rewritten
+// (NEXT-2: the inactive base plus its noise, clamped, in 0.5-point bins).
+__device__ __forceinline__ void store_qent(QEnt &q, uint64_t a, uint32_t in, uint32_t U, uint32_t P, uint32_t fcq,
+                                           uint32_t pf, uint32_t j, const Cold &c, uint32_t q_inactive) {
+  const uint32_t byp = (((c.bypass_mask >> (in >> 16)) & 1u) || P < c.min_words) ? 1u : 0u;
+  int32_t sc = (int32_t)q_inactive + (int32_t)(fcq >> 20) - 2048;
+  sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+  uint4 *w = reinterpret_cast<uint4 *>(&q);
+  w[0] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), in | (byp << 31), U | (((uint32_t)sc / 50u) << 24));
+  w[1] = make_uint4(P, fcq, pf, j);
+}
+
 
 // a7 rewrite (R11): realized length of a request whose
 // predicted length is P and compliance factor in fcq under r > 0:
@@ -355,7 +363,7 @@ __device__ __noinline__ uint4 refill_buffer(const Params &p, uint32_t wid, uint3
           store_qent(c.q[lane], tau, A.input_words | (A.cls << 16), U < 1 ? 1u : (uint32_t)U,
                      P0 < 1 ? 1u : (uint32_t)P0,
                      (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20),
-                     prefill_us(c.pf_ns, A.input_words), jj);
+                     prefill_us(c.pf_ns, A.input_words), jj, c, p.q_inactive);
         }
         if (DBG && dbg && tau < H) {
           const uint64_t sidx = tau / kUs;
@@ -439,7 +447,7 @@ __device__ __noinline__ uint4 refill_buffer(const Params &p, uint32_t wid, uint3
       const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
       store_qent(c.q[e], tau, in | (cls << 16), U < 1 ? 1u : (uint32_t)U, P0 < 1 ? 1u : (uint32_t)P0,
                  (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20),
-                 prefill_us(c.pf_ns, in), jj);
+                 prefill_us(c.pf_ns, in), jj, c, p.q_inactive);
       if (DBG && dbg && tau < H) {
         const uint64_t sidx = tau / kUs;
         atomicAdd(&dbg[sidx < dbg_cap ? sidx : dbg_cap - 1u].arrivals, 1u);
@@ -1138,11 +1146,11 @@ struct Sim {
     do {
       const QEnt &e = cold().q[buf_h];
       const uint64_t a = e.a;
-      const uint32_t inc = e.in, U = e.U, P = e.P, fcq = e.fcq;
-      const uint32_t in = inc & 0xFFFFu;
+      const uint32_t inc = e.in, Uq = e.U, P = e.P, fcq = e.fcq;
+      const uint32_t in = inc & 0xFFFFu, U = Uq & 0xFFFFFFu;
       // r applied to this request: the warp-uniform r unless a bypass rule holds
-      // (NEXT-3)
-      const bool byp = r > 0 && (((cold().bypass_mask >> (inc >> 16)) & 1u) || P < cold().min_words);
+      // (NEXT-3; decided at refill)
+      const bool byp = r > 0 && (inc >> 31);
       const uint32_t ra = byp ? 0u : r;
       const uint32_t R = realized_len(p, U, P, fcq, ra);  // a7 rewrite
       const uint32_t kvcap = cold().kv_cap;
@@ -1164,8 +1172,9 @@ struct Sim {
       }
 #ifndef BELLMAN_AB_NOQ
       {  // NEXT-2: similarity vs the unbounded length
-        int32_t base = (int32_t)p.q_inactive;
+        uint32_t qb = Uq >> 24;  // not rewritten: the bin decided at refill
         if (ra > 0) {
+          int32_t base;
           const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
           if (num <= (int64_t)p.q_safe * den) {
             base = (int32_t)p.q_active;
@@ -1175,10 +1184,10 @@ struct Sim {
             base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
                              (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
           }
+          int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+          sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+          qb = (uint32_t)sc / 50u;
         }
-        int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
-        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
-        const uint32_t qb = (uint32_t)sc / 50u;
         if (lane == 0) atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
       }
 #endif

@@ -184,6 +184,8 @@ struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
       off_drows, off_dctrl, off_arr, off_ord, off_pre, total;
+  size_t in_end;              // [0, in_end): host-filled inputs, one staging copy at create
+  size_t zero_beg, zero_end;  // [zero_beg, zero_end): zeroed at create (counters, stats, histograms)
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -297,6 +299,8 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
     return at;
   };
   const size_t ns = h.slot_off.size();
+  const size_t nd = h.dbg_off.size();
+  // host-filled inputs, contiguous: one H2D copy from a staging buffer
   L.off_sc = take(sizeof(bellman_scenario) * d->n_scenarios);
   L.off_tr = take(sizeof(DevTrace) * h.traces.size());
   L.off_seg = take(sizeof(DevSeg) * h.segs.size());
@@ -307,21 +311,25 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_slot = take(sizeof(uint32_t) * d->n_scenarios);
   L.off_soff = take(sizeof(uint64_t) * ns);
   L.off_scap = take(sizeof(uint32_t) * ns);
-  L.off_sn = take(sizeof(uint32_t) * ns);
-  L.off_series = take(sizeof(uint32_t) * h.series_words);
-  L.off_calib = take(sizeof(uint32_t) * 4 * ns);
-  L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
-  L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
-  L.off_cnt = take(sizeof(unsigned int) * 4);
-  const size_t nd = h.dbg_off.size();
   L.off_dslot = take(sizeof(uint32_t) * d->n_scenarios);
   L.off_doff = take(sizeof(uint64_t) * nd);
   L.off_dcap = take(sizeof(uint32_t) * nd);
-  L.off_dn = take(sizeof(uint32_t) * 2 * nd);
-  L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
-  L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
   L.off_arr = take(sizeof(bellman_arrival) * d->n_arrivals);
   L.off_ord = take(sizeof(uint32_t) * d->n_scenarios);
+  L.in_end = o;
+  // zeroed at create, contiguous: one memset
+  L.zero_beg = o;
+  L.off_sn = take(sizeof(uint32_t) * ns);
+  L.off_dn = take(sizeof(uint32_t) * 2 * nd);
+  L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
+  L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
+  L.off_cnt = take(sizeof(unsigned int) * 4);
+  L.zero_end = o;
+  // written by the kernels before they are read
+  L.off_series = take(sizeof(uint32_t) * h.series_words);
+  L.off_calib = take(sizeof(uint32_t) * 4 * ns);
+  L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
+  L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
   // NEXT-4 preemption scratch (per CTA: slot side state + the preempted stack),
   // only when some profile preempts
   bool pre = false;
@@ -332,8 +340,9 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   return L;
 }
 
-// T[i] = round(2^32 * log2(1 + i/4096)) (reading R33), product-side evaluation.
-static void log2_table(std::vector<uint2> &out) {
+// T[i] = round(2^32 * log2(1 + i/4096)) (reading R33), product-side evaluation
+// (computed once per process: it depends on nothing).
+static void log2_table_build(std::vector<uint2> &out) {
   out.resize(BELLMAN_TABLE_N);
   uint64_t prev = 0;
   for (int i = 0; i <= BELLMAN_TABLE_N; ++i) {
@@ -454,47 +463,48 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   sim->dbg_off = h.dbg_off;
   sim->dbg_cap = h.dbg_cap;
 
-  std::vector<uint2> l2;
-  log2_table(l2);
-#define H2D(dst, src, bytes) \
-  if (bytes) CUDA_TRY(nullptr, cudaMemcpyAsync((void *)(dst), (const void *)(src), (bytes), cudaMemcpyHostToDevice, s))
+  static const std::vector<uint2> l2 = [] {
+    std::vector<uint2> t;
+    log2_table_build(t);
+    return t;
+  }();
   {
-    bellman_status rc = BELLMAN_OK;
+    // every input region assembled in one pageable staging buffer laid out like
+    // the workspace's input prefix, then one H2D copy and one memset
+    std::vector<uint8_t> stage(L.in_end, 0);
+    auto put = [&](size_t off, const void *src, size_t bytes) {
+      if (bytes) std::memcpy(stage.data() + off, src, bytes);
+    };
+    put(L.off_sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios);
+    put(L.off_tr, h.traces.data(), sizeof(DevTrace) * h.traces.size());
+    put(L.off_seg, h.segs.data(), sizeof(DevSeg) * h.segs.size());
+    put(L.off_prof, desc->profiles, sizeof(bellman_profile) * desc->n_profiles);
+    put(L.off_ctrl, desc->ctrls, sizeof(bellman_ctrl) * desc->n_ctrls);
+    const int32_t *tabs[6] = {desc->models.L_words, desc->models.I_words, desc->models.fvar_q16,
+                              desc->models.noise,   desc->models.fcomp_q16, desc->models.qnoise};
+    for (int k = 0; k < 6; ++k)
+      put(L.off_tab + sizeof(int32_t) * BELLMAN_TABLE_N * k, tabs[k], sizeof(int32_t) * BELLMAN_TABLE_N);
+    put(L.off_log2, l2.data(), sizeof(uint2) * BELLMAN_TABLE_N);
+    put(L.off_slot, h.slot_of.data(), sizeof(uint32_t) * desc->n_scenarios);
+    put(L.off_soff, h.slot_off.data(), sizeof(uint64_t) * h.slot_off.size());
+    put(L.off_scap, h.slot_cap.data(), sizeof(uint32_t) * h.slot_cap.size());
+    put(L.off_dslot, h.dbg_of.data(), sizeof(uint32_t) * desc->n_scenarios);
+    put(L.off_doff, h.dbg_off.data(), sizeof(uint64_t) * h.dbg_off.size());
+    put(L.off_dcap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
+    put(L.off_arr, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
+    put(L.off_ord, h.order.data(), sizeof(uint32_t) * desc->n_scenarios);
     auto body = [&]() -> bellman_status {
-      H2D(P.sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios);
-      H2D(P.traces, h.traces.data(), sizeof(DevTrace) * h.traces.size());
-      H2D(P.segs, h.segs.data(), sizeof(DevSeg) * h.segs.size());
-      H2D(P.profs, desc->profiles, sizeof(bellman_profile) * desc->n_profiles);
-      H2D(P.ctrls, desc->ctrls, sizeof(bellman_ctrl) * desc->n_ctrls);
-      H2D(P.tabL, desc->models.L_words, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.tabI, desc->models.I_words, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.tabF, desc->models.fvar_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.tabN, desc->models.noise, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.tabC, desc->models.fcomp_q16, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.tabQ, desc->models.qnoise, sizeof(int32_t) * BELLMAN_TABLE_N);
-      H2D(P.log2tab, l2.data(), sizeof(uint2) * BELLMAN_TABLE_N);
-      H2D(P.series_slot, h.slot_of.data(), sizeof(uint32_t) * desc->n_scenarios);
-      H2D(P.series_off, h.slot_off.data(), sizeof(uint64_t) * h.slot_off.size());
-      H2D(P.series_cap, h.slot_cap.data(), sizeof(uint32_t) * h.slot_cap.size());
-      if (h.slot_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.series_n, 0, sizeof(uint32_t) * h.slot_off.size(), s));
-      H2D(P.dbg_slot, h.dbg_of.data(), sizeof(uint32_t) * desc->n_scenarios);
-      H2D(P.arrivals, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
-      H2D(sim->order, h.order.data(), sizeof(uint32_t) * desc->n_scenarios);
-      H2D(P.dbg_off, h.dbg_off.data(), sizeof(uint64_t) * h.dbg_off.size());
-      H2D(P.dbg_cap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
-      if (h.dbg_off.size()) CUDA_TRY(nullptr, cudaMemsetAsync(P.dbg_n, 0, sizeof(uint32_t) * 2 * h.dbg_off.size(), s));
-      CUDA_TRY(nullptr, cudaMemsetAsync(P.stats, 0, sizeof(bellman_scenario_stats) * desc->n_scenarios, s));
-      CUDA_TRY(nullptr, cudaMemsetAsync(P.seg_hist, 0, sizeof(uint64_t) * kSegWords * desc->n_segments, s));
-      CUDA_TRY(nullptr, cudaStreamSynchronize(s));
+      CUDA_TRY(nullptr, cudaMemcpyAsync(ws, stage.data(), L.in_end, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(nullptr, cudaMemsetAsync(ws + L.zero_beg, 0, L.zero_end - L.zero_beg, s));
+      CUDA_TRY(nullptr, cudaStreamSynchronize(s));  // the staging buffer is freed on return
       return BELLMAN_OK;
     };
-    rc = body();
+    const bellman_status rc = body();
     if (rc != BELLMAN_OK) {
       delete sim;
       return rc;
     }
   }
-#undef H2D
   *out = sim;
   return BELLMAN_OK;
 }

@@ -1901,12 +1901,16 @@ extern "C" int bellman_debug_span(unsigned long long *out, unsigned n) {
 #endif
 
 int bellman_tick_grid(int device) {
+  static int cached[64] = {0};  // per device: the answer does not change within a process
+  if (device >= 0 && device < 64 && cached[device] > 0) return cached[device];
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false>,
                                                     bellman::kWarpsPerBlock * 32, 0) != cudaSuccess)
     return -1;
-  return sms * (per_sm > 0 ? per_sm : 1);
+  const int g = sms * (per_sm > 0 ? per_sm : 1);
+  if (device >= 0 && device < 64) cached[device] = g;
+  return g;
 }
 
 cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream) {

@@ -132,7 +132,8 @@ class Simulator:
         self.n_scenarios = self.pk["n_scenarios"]
         self.n_segments = self.pk["n_segments"]
         desc = make_desc(self.pk)
-        nbytes = workspace_bytes(self.pk)
+        nbytes = self.pk.get("_ws_bytes") or workspace_bytes(self.pk)  # validated once per packed set
+        self.pk["_ws_bytes"] = nbytes
         if workspace is None or workspace.numel() < nbytes:
             workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
         self.ws = workspace

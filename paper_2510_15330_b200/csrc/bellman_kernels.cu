@@ -491,7 +491,7 @@ __device__ __forceinline__ uint64_t div_u64(uint64_t a, uint64_t b) {
 // instruction-cache footprint.  All lanes compute; only lane 0 writes the
 // shared-memory state.
 template <bool DBG>
-__device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
+__device__ __forceinline__ uint32_t ingest_body(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
                                                uint32_t acc_cnt, uint32_t r_cur, bool dbg, uint32_t util_maxb) {
   Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
   // the whole controller state in five independent 16-byte loads
@@ -578,6 +578,12 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
   return nr;
 }
 
+
+template <bool DBG>
+__device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
+                                               uint32_t acc_cnt, uint32_t r_cur, bool dbg, uint32_t util_maxb) {
+  return ingest_body<DBG>(wid, lane, sec_bound, acc_sum, acc_cnt, r_cur, dbg, util_maxb);
+}
 
 // ---------------------------------------------------------------------------
 // The per-scenario simulation.  Every scalar is warp-uniform.  Derived
@@ -683,7 +689,12 @@ struct Sim {
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest() {
-    r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,
+    // the KV-free TBT loop (C5's paper-trace scenarios ingest every second of
+    // long quiet stretches) takes the controller inline; the others call it
+    if (KV0 && TBTO && !DBG)
+      r = ingest_body<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
+    else
+      r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,
                            sig(BELLMAN_SIG_UTIL) ? maxb : 0u);
   }
 

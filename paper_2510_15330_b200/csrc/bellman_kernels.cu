@@ -689,9 +689,9 @@ struct Sim {
 
   // ------------------------------------------------------------------ a6
   __device__ __forceinline__ void ingest() {
-    // the KV-free TBT loop (C5's paper-trace scenarios ingest every second of
-    // long quiet stretches) takes the controller inline; the others call it
-    if (KV0 && TBTO && !DBG)
+    // the TBT loops take the controller inline (C5's paper-trace scenarios
+    // ingest every second of long quiet stretches); the others call it
+    if (TBTO && !DBG)
       r = ingest_body<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
     else
       r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,

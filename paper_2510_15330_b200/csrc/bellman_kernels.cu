@@ -198,6 +198,9 @@ struct alignas(16) Cold {
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t pf_ns;                             // prefill ns per input word
+  // KV-free cost law: floor((2^32 - 1) / cost(B)) for B = 0..max_batch, filled
+  // lane-parallel at scenario start; the leap divides by cost(B) with it
+  uint32_t cbm_tab[68];
   // a2/a3: the next <= 32 accepted arrivals (the head of the FIFO queue),
   // entry i written by lane i at refill, read whole (two 16-byte broadcasts)
   // by every lane at admission
@@ -650,7 +653,6 @@ struct Sim {
   uint32_t next_pf;    // min prefill end over prefilling slots
   uint32_t n_ready, B, in_sys;
   uint32_t cbase;             // t0 + slope * max(0, B - knee)
-  uint32_t cbm;               // KV0: floor((2^32 - 1) / cbase)
   uint32_t kq, kr;            // kv * K = kq * 1000 + kr, K = context words of the batch
   uint32_t kstep_q, kstep_r;  // kv * B = kstep_q * 1000 + kstep_r (growth per iteration)
   uint32_t win_now;           // T in [w0, w1)
@@ -762,9 +764,6 @@ struct Sim {
   // B changed: cost base and per-iteration KV growth
   __device__ __forceinline__ void batch_changed() {
     cbase = t0 + slope * (B > knee ? B - knee : 0u);
-    // KV-free instantiation: the leap divides by cbase; floor((2^32 - 1) / cbase)
-    // turns that into a multiply-high and one correction step
-    if (KV0) cbm = 0xFFFFFFFFu / cbase;
     if (KV0) return;
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
@@ -1302,7 +1301,7 @@ struct Sim {
       if (kvc() == 0) {
         uint32_t nn;
         if (KV0) {  // umulhi(room, floor((2^32-1)/cb)) is floor(room / cb) or one less
-          nn = __umulhi(room, cbm);
+          nn = __umulhi(room, cold().cbm_tab[B]);
           if (room - nn * cb >= cb) nn++;
         } else {
           nn = room / cb;
@@ -1532,6 +1531,11 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   if (lane < 8) {
     S.cold().rungs[lane] = cc.rungs_bp[lane];
     S.cold().ring[lane] = 0;
+  }
+  if (KV0) {  // cost(B) = t0 + slope max(0, B - knee) >= 1 (host-validated t0 >= 1)
+#pragma unroll 1
+    for (uint32_t b = lane; b <= pr.max_batch; b += 32u)
+      S.cold().cbm_tab[b] = 0xFFFFFFFFu / (pr.t0_us + pr.slope_us * (b > pr.knee ? b - pr.knee : 0u));
   }
   if (DBG && S.dbg) {  // rows are accumulated with atomics: zero this scenario's region first
     const uint32_t cap = p.dbg_cap[dslot];

@@ -388,6 +388,13 @@ def main():
     kern_s = kern_tot / 1e3 / args.steps
     achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G warp-inst/s
     peak = 148 * 4 * mhz * 1e6 / 1e9
+    # measured integer issue / lane throughput (microbenchmark, after the timed region)
+    from paper_2510_15330_b200 import peak as PEAK
+
+    mb = PEAK.measure(local)
+    issue_meas = 148 * mb["mixed_warp_inst_per_clk_sm"] * mhz * 1e6 / 1e9
+    l_int = max(mb["mixed_lanes_per_clk_sm"], mb["alu_lanes_per_clk_sm"], mb["fma_lanes_per_clk_sm"])
+    lane_peak = 148 * l_int * mhz * 1e6 / 1e9
     traffic, traffic_src = ncu_traffic(args.workload)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -401,6 +408,13 @@ def main():
                    "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "issue_measured": {"peak": issue_meas, "frac": achieved / issue_meas,
+                                        "warp_inst_per_clk_sm": {k.split("_warp")[0]: round(v, 3) for k, v in mb.items()
+                                                                 if "warp_inst" in k}},
+                     "lane": {"L_int": l_int, "peak": lane_peak, "unit": "G int-lane-ops/s",
+                              "frac": achieved / lane_peak,
+                              "note": "R_lane (SURVEY 8(d)): every algorithmic op is one warp-instruction in the "
+                                      "warp-per-scenario design, so achieved counts it once; L_int measured"},
                      "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time; peak = 148 SM x 4 "
                              f"issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM bytes per launch "
                              f"({traffic_src or 'no capture'})"},

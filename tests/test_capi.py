@@ -26,6 +26,19 @@ def test_library_exports_header_symbols():
         assert hasattr(lib, n), n
 
 
+def test_peak_library_exports_header_symbols():
+    """The roofline microbenchmark (include/bellman_peak.h) builds and exports its entry point."""
+    from paper_2510_15330_b200 import build as B
+
+    B.build()
+    lib = ctypes.CDLL(B.PEAK_OUT)
+    src = open(os.path.join(ROOT, "include", "bellman_peak.h")).read()
+    names = sorted(set(re.findall(r"\b(bellman_\w+)\s*\(", src)))
+    assert names == ["bellman_peak_int"]
+    for n in names:
+        assert hasattr(lib, n), n
+
+
 def test_struct_sizes_and_validation():
     from paper_2510_15330_b200 import _abi as A, sim
     import workloads as W

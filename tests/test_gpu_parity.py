@@ -188,6 +188,13 @@ def test_c4_full_size_sampled():
     assert int(st["ticks"].max()) > 10**6
 
 
+def test_c3_full_size_every_record():
+    """BASELINE configs[2] at full size (321 controllers x 32 seeds = 10,272
+    scenarios, one launch): every record vs the oracle."""
+    st = _full_size_sampled(W.config_c3(), W.config_c3().n_scenarios)
+    assert len(st) == 10272
+
+
 def test_c2_full_bench_config():
     """BASELINE configs[1] at full size, in the launch configuration bench.py
     times: every one of the 2048 records vs the oracle, and the per-segment

@@ -594,6 +594,12 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
 // division: the cost base c = t0 + slope max(0, B - knee), the KV term as
 // kv K = kq 1000 + kr, the window flag and its next boundary, the arrival time
 // of the queue head.
+// runs of at most 2^BELLMAN_LEAP_SHIFT iterations are leaped one at a time
+// (else 32 per step, lane-parallel)
+#ifndef BELLMAN_LEAP_SHIFT
+#define BELLMAN_LEAP_SHIFT 3
+#endif
+
 template <bool DBG, bool TBTO, bool KV0 = false>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
@@ -1309,7 +1315,7 @@ struct Sim {
         n = nn < left ? nn : left;
         used = n * cb;
       } else {
-        if (left <= 8u || (room >> 3) < cb + q) {
+        if (left <= (1u << BELLMAN_LEAP_SHIFT) || (room >> BELLMAN_LEAP_SHIFT) < cb + q) {
           // short runs (dense events): one iteration at a time
           while (n < left) {
             const uint32_t d = cb + q;
@@ -1666,22 +1672,26 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
       PROFC(12, S.admit(p, h));
     }
     // at most two passes: a join iteration whose end is quiet is ended here
-    // and followed, in the same trip, by a leap and the next start
-    while (S.n_ready + S.B + S.n_pending() > 0) {
-      const bool join = S.n_ready + S.n_pending() != 0;
-      if (!join) {
-        PROF(6);
-        const uint32_t t0_ = S.ticks;
-        PROFC(13, S.leap());
+    // and followed, in the same trip, by a leap and the next start (after a
+    // join B > 0, so the second pass needs no re-check)
+    if (S.n_ready + S.B + S.n_pending() > 0) {
+      bool join;
+      do {
+        join = S.n_ready + S.n_pending() != 0;
+        if (!join) {
+          PROF(6);
 #ifdef BELLMAN_PROFILE_COUNTERS
-        prof_[7] += S.ticks - t0_;
+          const uint32_t t0_ = S.ticks;
 #endif
-      } else {
-        PROF(8);
-      }
-      PROFC(14, S.start_iteration());
-      if (!join || !S.quiet_end()) break;
-      PROF(17);
+          PROFC(13, S.leap());
+#ifdef BELLMAN_PROFILE_COUNTERS
+          prof_[7] += S.ticks - t0_;
+#endif
+        } else {
+          PROF(8);
+        }
+        PROFC(14, S.start_iteration());
+      } while (join && S.quiet_end() && (PROF(17), true));
     }
   }
 

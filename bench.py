@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--seeds-per-gpu", type=int, default=SEEDS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="N > 1: exchange summaries with a separate NCCL all-gather instead of the fused kernel stores")
     ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5"],
                     help="BASELINE config; C2 (configs[1]) is the reported bench line")
     return ap.parse_args()
@@ -300,15 +302,25 @@ def main():
     seg_dev = torch.zeros((w.n_segments, _abi.SEG_HIST_WORDS), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    # N > 1: the summary all-gather is fused into the tick kernel — every record
+    # is stored into every rank's full_dev over peer memory as it is finished
+    # (CUDA IPC mappings over NVLink / NVSwitch); --nccl-gather times the
+    # separate NCCL all-gather instead.  The segment-histogram sum stays NCCL.
+    fused = world > 1 and not args.nccl_gather
+    peers = None
+    if fused:
+        peers = PAR.PeerRecords(full_dev, rank, world, local)
+        sim.set_peers(peers.ptrs)
+
     def step():
         sim.reset(stream)
         sim.run(first=rank, count=count, stride=world, stream=stream)
         k_end = torch.cuda.Event(enable_timing=True)
         k_end.record(stream)
-        sim.stats_device(stats_dev, stream=stream)
+        if not fused:
+            sim.stats_device(stats_dev, stream=stream)
+            PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank, world, out=full_dev)
         sim.segment_hist_device(seg_dev, stream=stream)
-        # the one exchange step: summaries all-gathered, segment histograms summed (NCCL)
-        PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank, world, out=full_dev)
         PAR.reduce_segments(seg_dev)
         return k_end
 
@@ -340,6 +352,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms, kern_tot = float(t[0]), float(t[1])
     # correctness-carrying unit count: ticks from the summaries of this step
+    sim.stats_device(stats_dev, stream=stream)
+    if fused:  # the fused exchange must equal the NCCL all-gather of the same records
+        chk = PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank, world)
+        torch.cuda.synchronize()
+        dist.barrier()
+        assert torch.equal(chk, full_dev), "fused peer-memory exchange differs from the NCCL all-gather"
     st_local = stats_dev.cpu().numpy().view(_abi.STATS).reshape(-1)
     local_ticks = int(st_local["ticks"][mine].astype(np.int64).sum())
     local_ops = algorithmic_ops(st_local[mine])
@@ -376,6 +394,11 @@ def main():
     h2d = int(sum(v.nbytes for k, v in pk.items() if isinstance(v, np.ndarray)) +
               sum(v.nbytes for v in pk["tables"].values()) + 8 * W.TABLE_N + 4 * n)
     d2h = int(n * _abi.STATS.itemsize)
+    if peers is not None:  # every rank's kernels are done: unmap the peers' arrays
+        torch.cuda.synchronize()
+        dist.barrier()
+        sim.set_peers([])
+        peers.close()
 
     if rank != 0:
         if world > 1:
@@ -405,7 +428,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.workload],
                    "scenarios_per_gpu": count, "scenarios_total": n, "ticks_per_step": int(ticks_all),
-                   "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)"},
+                   "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)",
+                   "exchange": ("none (1 GPU)" if world == 1 else "NCCL all-gather" if not fused else
+                                "fused: records stored to every rank over peer memory by the tick kernel; "
+                                "segment histograms NCCL all-reduce")},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "issue_measured": {"peak": issue_meas, "frac": achieved / issue_meas,

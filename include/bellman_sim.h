@@ -309,6 +309,42 @@ bellman_status bellman_sim_series(bellman_sim *sim, uint64_t id, bellman_second_
 /* Zero all summary records, segment histograms and recorded series. */
 bellman_status bellman_sim_reset(bellman_sim *sim, void *stream);
 
+/* ---- Fused summary exchange over peer memory ----------
+ * The one exchange step of a sharded run is an all-gather of the summary
+ * records (every rank ends with all n_scenarios records).  Instead of a
+ * separate collective after the kernel, the tick kernel can store every record
+ * it finishes, as it finishes it, into up to BELLMAN_MAX_PEERS full-size record
+ * arrays — one per rank, the caller's own included — that the caller has
+ * mapped into this process (CUDA IPC over NVLink / NVSwitch, or a local device
+ * pointer), at the record's scenario index.  The transfer then overlaps the
+ * simulation scenario by scenario; after every rank's run has completed (the
+ * caller's stream synchronised and a host barrier), every array holds every
+ * record of every rank's shard.  Records are identical to bellman_sim_stats'
+ * (the local workspace copy is still written). */
+#define BELLMAN_MAX_PEERS 8
+
+/* Export a device allocation for peer mapping: *handle (64 bytes, caller-owned
+ * host memory) receives the CUDA IPC handle of the allocation containing
+ * dev_ptr and *offset the byte offset of dev_ptr inside it.  Synchronous.
+ * BELLMAN_EINVAL on NULL arguments, BELLMAN_ECUDA if CUDA refuses. */
+bellman_status bellman_ipc_export(const void *dev_ptr, void *handle, uint64_t *offset);
+
+/* Map a peer allocation exported by bellman_ipc_export in another process
+ * (any device of this node with peer access; same device allowed) into this
+ * process on `device`: *base receives the mapping (for bellman_ipc_close) and
+ * *dev_ptr = base + offset.  Synchronous. */
+bellman_status bellman_ipc_open(const void *handle, uint64_t offset, int device, void **base, void **dev_ptr);
+
+/* Unmap a mapping returned by bellman_ipc_open (its `base`). */
+bellman_status bellman_ipc_close(void *base);
+
+/* Set the peer record arrays of later runs: peer_stats[0..n_peers) are device
+ * pointers valid in this process, each to n_scenarios bellman_scenario_stats;
+ * n_peers = 0 turns the fused exchange off.  Pointers are borrowed (caller-
+ * owned, must outlive the runs).  BELLMAN_EINVAL if n_peers > BELLMAN_MAX_PEERS
+ * or a pointer is NULL or not 16-byte aligned. */
+bellman_status bellman_sim_set_peers(bellman_sim *sim, void *const *peer_stats, uint32_t n_peers);
+
 /* Kernel launches issued by the most recent bellman_sim_run. */
 uint32_t bellman_sim_last_launches(const bellman_sim *sim);
 

@@ -19,6 +19,7 @@ HIST_R = 512
 HIST_Q = 201
 SEG_HIST_WORDS = 2 * HIST_LAT + HIST_R + 2 * HIST_Q
 NONE = 0xFFFFFFFF
+MAX_PEERS = 8
 FLAG_TRUNCATED, FLAG_DEGENERATE_CALIB, FLAG_SERIES_OVERFLOW, FLAG_DONE = 0x1, 0x2, 0x4, 0x100
 
 KNOT = np.dtype([("t_us", "<i8"), ("lam_mrps", "<u4"), ("_pad", "<u4")])
@@ -85,6 +86,10 @@ EXPORTS = {
     "bellman_sim_series": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
                                      C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
     "bellman_sim_last_launches": (C.c_uint32, [C.c_void_p]),
+    "bellman_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
+    "bellman_ipc_open": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "bellman_ipc_close": (C.c_int, [C.c_void_p]),
+    "bellman_sim_set_peers": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "bellman_sim_destroy": (None, [C.c_void_p]),
     "bellman_status_string": (C.c_char_p, [C.c_int]),
     "bellman_sim_last_error": (C.c_char_p, [C.c_void_p]),

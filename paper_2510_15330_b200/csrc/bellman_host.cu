@@ -1,5 +1,6 @@
 // bellman_host.cu — C ABI of the beLLMan simulator (include/bellman_sim.h):
 // validation, workspace layout, host-side precomputation, launches.
+#include <cuda.h>  // CUdeviceptr / CUresult types only (the driver call is resolved at run time)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -633,6 +634,66 @@ bellman_status bellman_sim_series(bellman_sim *sim, uint64_t id, bellman_second_
     CUDA_TRY(sim, cudaMemcpyAsync(ctrl, sim->params.dbg_ctrl + sim->dbg_off[slot], sizeof(bellman_ctrl_row) * nc2,
                                   cudaMemcpyDeviceToHost, s));
   CUDA_TRY(sim, cudaStreamSynchronize(s));
+  return BELLMAN_OK;
+}
+
+// ---- fused summary exchange over peer memory (include/bellman_sim.h, §8(e))
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+
+bellman_status bellman_ipc_export(const void *dev_ptr, void *handle, uint64_t *offset) {
+  if (!dev_ptr || !handle || !offset) return fail(nullptr, BELLMAN_EINVAL, "ipc_export: NULL argument");
+  // base of the allocation containing dev_ptr (a caching allocator hands out
+  // interior pointers): cuMemGetAddressRange, resolved through the runtime so
+  // that the library does not link libcuda
+  typedef CUresult (*range_fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return fail(nullptr, BELLMAN_ECUDA, "ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (((range_fn)fn)(&base, &size, (CUdeviceptr)(uintptr_t)dev_ptr) != CUDA_SUCCESS)
+    return fail(nullptr, BELLMAN_ECUDA, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+  if (e != cudaSuccess) return fail(nullptr, BELLMAN_ECUDA, "ipc_export: %s", cudaGetErrorString(e));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_ipc_open(const void *handle, uint64_t offset, int device, void **base, void **dev_ptr) {
+  if (!handle || !base || !dev_ptr) return fail(nullptr, BELLMAN_EINVAL, "ipc_open: NULL argument");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, BELLMAN_ECUDA, "ipc_open: %s", cudaGetErrorString(e));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void *b = nullptr;
+  e = cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(nullptr, BELLMAN_ECUDA, "ipc_open: %s", cudaGetErrorString(e));
+  *base = b;
+  *dev_ptr = (uint8_t *)b + offset;
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_ipc_close(void *base) {
+  if (!base) return fail(nullptr, BELLMAN_EINVAL, "ipc_close: NULL base");
+  const cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return fail(nullptr, BELLMAN_ECUDA, "ipc_close: %s", cudaGetErrorString(e));
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_set_peers(bellman_sim *sim, void *const *peer_stats, uint32_t n_peers) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (n_peers > BELLMAN_MAX_PEERS) return fail(sim, BELLMAN_EINVAL, "n_peers > %d", BELLMAN_MAX_PEERS);
+  if (n_peers && !peer_stats) return fail(sim, BELLMAN_EINVAL, "peer_stats is NULL");
+  for (uint32_t g = 0; g < n_peers; ++g)
+    if (!peer_stats[g] || ((uintptr_t)peer_stats[g] & 15u))
+      return fail(sim, BELLMAN_EINVAL, "peer %u: NULL or not 16-byte aligned", g);
+  for (uint32_t g = 0; g < BELLMAN_MAX_PEERS; ++g)
+    sim->params.peer[g] = g < n_peers ? (bellman_scenario_stats *)peer_stats[g] : nullptr;
+  sim->params.n_peer = n_peers;
   return BELLMAN_OK;
 }
 

@@ -83,6 +83,8 @@ struct Params {
   bellman_ctrl_row *dbg_ctrl;
   const bellman_arrival *arrivals;  // replay lists (NEXT-4)
   bellman_scenario_stats *stats;
+  bellman_scenario_stats *peer[BELLMAN_MAX_PEERS];  // fused exchange: every rank's record array
+  uint32_t n_peer;                                  // 0: off
   unsigned long long *seg_hist;  // [n_segments][kSegWords]
   unsigned int *counter;         // work counter of this launch
   const uint32_t *order;         // heavy-first scenario order of a whole-set run, else NULL

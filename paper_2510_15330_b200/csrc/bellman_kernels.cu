@@ -1835,6 +1835,20 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     o.recompute_words = C_[CT_RECOMP];
     p.stats[sid] = o;
   }
+  if (p.n_peer) {
+    // fused exchange (§8(e)): the record, just written by lane 0, goes to every
+    // rank's record array over peer memory as 17 x 16-byte stores per peer,
+    // spread over the lanes (lane l takes chunks l, l + 32, ... of peers x 17)
+    static_assert(sizeof(bellman_scenario_stats) % 16 == 0, "record is copied in 16-byte chunks");
+    constexpr uint32_t kChunks = sizeof(bellman_scenario_stats) / 16;
+    __syncwarp();  // lane 0's record store precedes the other lanes' reads
+    const uint4 *src = reinterpret_cast<const uint4 *>(&p.stats[sid]);
+    for (uint32_t k = lane; k < p.n_peer * kChunks; k += 32u) {
+      const uint32_t g = k / kChunks, c = k - g * kChunks;
+      reinterpret_cast<uint4 *>(&p.peer[g][sid])[c] = src[c];
+    }
+    __threadfence_system();
+  }
   __syncwarp();
   __syncwarp();
 }

@@ -6,8 +6,18 @@ per-tick cost).  The only collective is at the end of a step: all_gather of
 the 272-byte summary records (NCCL over NVLink on GPUs, gloo in CPU tests)
 and an all_reduce(SUM) of the integer segment histograms.  Integer sums are
 order-independent, so results are bit-identical for any world size.
+
+On GPUs the record all-gather can instead be fused into the simulation
+kernel (`PeerRecords` + `Simulator.set_peers`): every rank maps every other
+rank's full-size record array into its process (CUDA IPC over NVLink /
+NVSwitch, through the library's bellman_ipc_* calls) and the tick kernel
+stores each record into all of them as it finishes the scenario, so the
+exchange overlaps the simulation; only the segment-histogram sum stays a
+collective.
 """
 from __future__ import annotations
+
+import ctypes as C
 
 import torch
 import torch.distributed as dist
@@ -51,3 +61,46 @@ def reduce_segments(seg: torch.Tensor) -> torch.Tensor:
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(seg, op=dist.ReduceOp.SUM)
     return seg
+
+
+class PeerRecords:
+    """Every rank's full-size (n, REC) record array, mapped into this process.
+
+    `local` is this rank's array (a CUDA tensor, 16-byte aligned); the IPC
+    handle of its allocation is exchanged over the process group and each
+    other rank's array is opened on `device`.  `ptrs[g]` is rank g's array as
+    a device pointer valid here (rank == g: local itself).  The host side —
+    handle exchange, ordering, ownership — is plain Python over
+    torch.distributed; the mapping itself is the library's."""
+
+    def __init__(self, local: torch.Tensor, rank: int, world: int, device: int):
+        from . import _abi as A
+
+        assert local.is_cuda and local.is_contiguous() and local.data_ptr() % 16 == 0
+        self.local, self.bases, self.ptrs = local, [], []
+        L = A.lib()
+        h = (C.c_uint8 * 64)()
+        off = C.c_uint64()
+        A.check(L.bellman_ipc_export(C.c_void_p(local.data_ptr()), h, C.byref(off)))
+        mine = (bytes(h), int(off.value))
+        allh = [None] * world
+        if world > 1:
+            dist.all_gather_object(allh, mine)
+        else:
+            allh = [mine]
+        for g, (hb, o) in enumerate(allh):
+            if g == rank:
+                self.ptrs.append(local.data_ptr())
+                continue
+            base, ptr = C.c_void_p(), C.c_void_p()
+            hh = (C.c_uint8 * 64).from_buffer_copy(hb)
+            A.check(L.bellman_ipc_open(hh, o, device, C.byref(base), C.byref(ptr)))
+            self.bases.append(base.value)
+            self.ptrs.append(ptr.value)
+
+    def close(self):
+        from . import _abi as A
+
+        for b in self.bases:
+            A.lib().bellman_ipc_close(C.c_void_p(b))
+        self.bases, self.ptrs = [], []

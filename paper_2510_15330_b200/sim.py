@@ -191,6 +191,14 @@ class Simulator:
                                            C.c_void_p(_stream_ptr(stream))), self.h)
         return rows[: min(nr.value, cap)], ctrl[: min(nc.value, cap)]
 
+    def set_peers(self, ptrs: list):
+        """Fused exchange (include/bellman_sim.h): later runs also
+        store every record they finish into these device record arrays (every
+        rank's full-size array, mapped into this process); [] turns it off."""
+        arr = (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(int(x)) for x in ptrs])
+        A.check(A.lib().bellman_sim_set_peers(self.h, arr, len(ptrs)), self.h)
+        self._peers = list(ptrs)
+
     def reset(self, stream=None):
         A.check(A.lib().bellman_sim_reset(self.h, C.c_void_p(_stream_ptr(stream))), self.h)
 

@@ -1,0 +1,80 @@
+"""Fused summary exchange (include/bellman_sim.h bellman_sim_set_peers, SURVEY
+§8(e)): two ranks — two processes sharing cuda:0, a gloo group for the handle
+exchange — each simulate their interleaved shard while the tick kernel stores
+every finished record into both ranks' full-size arrays through CUDA IPC
+mappings.  After the runs every rank's array must equal, byte for byte, a
+single whole-set run; the workspace copy (bellman_sim_stats) stays the shard's.
+On the 8-GPU box the same mapping goes over NVLink / NVSwitch."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+
+
+def _workload():
+    import workloads as W
+
+    return W.config_c2(n_seeds=4, rates=[0.5, 2.0, 4.0, 8.0])
+
+
+def _rank_main(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    from paper_2510_15330_b200 import Simulator, _abi
+    from paper_2510_15330_b200 import parallel as PAR
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    w = _workload()
+    n = w.n_scenarios
+    sim = Simulator(w.columns(), device=0)
+    full = torch.zeros((n, _abi.STATS.itemsize), dtype=torch.uint8, device="cuda:0")
+    peers = PAR.PeerRecords(full, rank, world, 0)
+    sim.set_peers(peers.ptrs)
+    for _ in range(2):  # the second run rewrites every record: idempotent
+        dist.barrier()
+        sim.run(first=rank, count=PAR.shard_count(n, rank, world), stride=world)
+        torch.cuda.synchronize()
+        dist.barrier()
+    np.save(os.path.join(outdir, f"full{rank}.npy"), full.cpu().numpy())
+    np.save(os.path.join(outdir, f"own{rank}.npy"), sim.stats().view(np.uint8).reshape(n, -1))
+    dist.barrier()
+    peers.close()
+    sim.set_peers([])
+    dist.destroy_process_group()
+
+
+def test_fused_exchange_two_ranks_one_gpu(tmp_path):
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2510_15330_b200 import Simulator
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    w = _workload()
+    ref = Simulator(w.columns(), device=0)
+    ref.run()
+    torch.cuda.synchronize()
+    want = ref.stats().view(np.uint8).reshape(w.n_scenarios, -1)
+    for r in range(2):
+        got = np.load(tmp_path / f"full{r}.npy")
+        assert np.array_equal(got, want), f"rank {r}: fused exchange differs from a single run"
+        own = np.load(tmp_path / f"own{r}.npy")
+        mine = np.arange(r, w.n_scenarios, 2)
+        assert np.array_equal(own[mine], want[mine])
+        others = np.setdiff1d(np.arange(w.n_scenarios), mine)
+        assert not own[others].any()  # the workspace copy holds the shard only

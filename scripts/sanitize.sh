@@ -11,7 +11,10 @@ pre.profiles = [dict(p, kv_cap_words=150_000, kv_policy=1) for p in pre.profiles
 for w in (W.config_c1(), W.config_c2(n_seeds=1, rates=[0.5, 4.0], horizon_s=120), W.config_paper_pair(0), pre):
     for s in w.scenarios[:2]:
         s.record |= 2
-    sim = Simulator(w.columns()); sim.run(); torch.cuda.synchronize()
+    sim = Simulator(w.columns())
+    full = torch.zeros((w.n_scenarios, 272), dtype=torch.uint8, device='cuda')
+    sim.set_peers([full.data_ptr()])  # the fused exchange's peer stores (a local array here)
+    sim.run(); torch.cuda.synchronize()
     st = sim.stats()
     print(w.name, int(st['ticks'].sum()), flush=True)
 PY

@@ -78,3 +78,31 @@ def test_fused_exchange_two_ranks_one_gpu(tmp_path):
         assert np.array_equal(own[mine], want[mine])
         others = np.setdiff1d(np.arange(w.n_scenarios), mine)
         assert not own[others].any()  # the workspace copy holds the shard only
+
+
+def test_set_peers_local_arrays_and_validation():
+    """One process, two local record arrays as 'peers': both receive every
+    record of the run, equal to bellman_sim_stats; argument validation."""
+    import torch
+
+    from paper_2510_15330_b200 import BellmanError, Simulator, _abi
+
+    w = _workload()
+    n = w.n_scenarios
+    sim = Simulator(w.columns(), device=0)
+    a = torch.zeros((n, _abi.STATS.itemsize), dtype=torch.uint8, device="cuda:0")
+    b = torch.zeros_like(a)
+    sim.set_peers([a.data_ptr(), b.data_ptr()])
+    sim.run()
+    torch.cuda.synchronize()
+    want = sim.stats().view(np.uint8).reshape(n, -1)
+    assert np.array_equal(a.cpu().numpy(), want) and np.array_equal(b.cpu().numpy(), want)
+    sim.set_peers([])  # off: later runs leave the arrays alone
+    a.zero_()
+    sim.run()
+    torch.cuda.synchronize()
+    assert not a.any()
+    with pytest.raises(BellmanError, match="n_peers"):
+        sim.set_peers([a.data_ptr()] * 9)
+    with pytest.raises(BellmanError, match="aligned"):
+        sim.set_peers([a.data_ptr() + 4])

@@ -762,6 +762,9 @@ struct Sim {
   // move the clock to an event instant t >= T
   __device__ __forceinline__ void advance(uint32_t t) {
     T = t;
+    // one compare against the earliest of the three boundaries (one branch in
+    // the common case, where none is crossed)
+    if (__builtin_expect(t < umin(umin(sec_bound, win_next), kRebaseAt), 1)) return;
     roll_second(t);
     if (t >= win_next) update_window();
     if (__builtin_expect(t >= kRebaseAt, 0)) rebase();
@@ -841,9 +844,11 @@ struct Sim {
   // exactly this and nothing else) and return true.
   __device__ __forceinline__ bool quiet_end() {
     const uint32_t te = iter_end;
-    if (te >= stop_static || te >= sec_bound || te >= kRebaseAt || next_pf <= te || ticks - 1u == next_done)
+    // every condition evaluated, one branch
+    const uint32_t lim = umin(umin(stop_static, sec_bound), umin(kRebaseAt, next_pf));
+    if ((te >= lim) | (ticks - 1u == next_done) |
+        ((in_sys < maxb) & !adm_blocked & ((head_t <= te) | stk_any())))
       return false;
-    if (in_sys < maxb && !adm_blocked && (head_t <= te || stk_any())) return false;
     if (pre() && in_sys > 1u && (uint64_t)kv_res + B > cold().kv_cap) return false;  // the end preempts
     T = te;
     iteration_words();

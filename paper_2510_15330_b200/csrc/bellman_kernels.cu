@@ -1173,7 +1173,25 @@ struct Sim {
       // (NEXT-3; decided at refill)
       const bool byp = r > 0 && (inc >> 31);
       const uint32_t ra = byp ? 0u : r;
-      const uint32_t R = realized_len(p, U, P, fcq, ra);  // a7 rewrite
+      // a7 rewrite and NEXT-2 similarity
+      // in one block; not rewritten: U and the bin decided at refill
+      uint32_t R = U, qb = Uq >> 24;
+      if (ra > 0) {
+        R = realized_len(p, U, P, fcq, ra);
+        int32_t base;
+        const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
+        if (num <= (int64_t)p.q_safe * den) {
+          base = (int32_t)p.q_active;
+        } else if (num >= (int64_t)p.q_end * den) {
+          base = (int32_t)p.q_floor;
+        } else {
+          base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
+                           (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
+        }
+        int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+        qb = (uint32_t)sc / 50u;
+      }
       const uint32_t kvcap = cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
@@ -1187,31 +1205,11 @@ struct Sim {
         kv_res += need;
       }
       n_byp += byp;
-      if (ra > 0) {
-        cadd(CT_REWRITTEN, 1u);
-        if (lane == 0) atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
+      cadd(CT_REWRITTEN, ra > 0 ? 1u : 0u);
+      if (lane == 0) {  // r and similarity histograms
+        if (ra > 0) atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
+        atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
       }
-#ifndef BELLMAN_AB_NOQ
-      {  // NEXT-2: similarity vs the unbounded length
-        uint32_t qb = Uq >> 24;  // not rewritten: the bin decided at refill
-        if (ra > 0) {
-          int32_t base;
-          const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
-          if (num <= (int64_t)p.q_safe * den) {
-            base = (int32_t)p.q_active;
-          } else if (num >= (int64_t)p.q_end * den) {
-            base = (int32_t)p.q_floor;
-          } else {
-            base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
-                             (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
-          }
-          int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
-          sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
-          qb = (uint32_t)sc / 50u;
-        }
-        if (lane == 0) atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
-      }
-#endif
       const uint32_t pf = e.pf;
       // the first free slot: lowest lane of slot row 0, then of row 1
       const bool s1 = f0 == 0u;
@@ -1643,13 +1641,15 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
       // a far next event: jump (idle) to the cap first; advance() rebases there
       if (tn > kJumpCap) tn = kJumpCap;
     }
-    if (tn >= S.Hr) break;
-    if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
-      S.cadd(CT_IDLE, tn - S.T);
-      const uint64_t a = S.ab(S.T), b = S.ab(tn);
-      const uint64_t lo = a > S.cold().w0 ? a : S.cold().w0, hi = b < S.cold().w1 ? b : S.cold().w1;
-      if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
-      S.dbg_idle(a, b);
+    if ((tn >= S.Hr) | (S.in_sys == 0)) {  // rare on a busy server: one branch for both
+      if (tn >= S.Hr) break;
+      if (S.in_sys == 0) {  // idle interval [T, tn) (R18)
+        S.cadd(CT_IDLE, tn - S.T);
+        const uint64_t a = S.ab(S.T), b = S.ab(tn);
+        const uint64_t lo = a > S.cold().w0 ? a : S.cold().w0, hi = b < S.cold().w1 ? b : S.cold().w1;
+        if (hi > lo) S.cadd(CT_WIN_IDLE, hi - lo);
+        S.dbg_idle(a, b);
+      }
     }
     PROFC(9, S.advance(tn));
     tn = S.T;  // advance() may have moved the epoch
@@ -1666,10 +1666,10 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
         if (S.sec_bound < lim) lim = S.sec_bound;
       }
       PROFC(11, S.prefill_end(h, lim));
-    }
-    if (mid) {
-      PROF(1);
-      continue;
+      if (mid) {  // a mid-iteration trip always has next_pf == tn
+        PROF(1);
+        continue;
+      }
     }
     // the decode loop is idle here: admission point (R7), then the next iteration
     if (S.in_sys < S.maxb && !S.adm_blocked && (S.head_t <= tn || S.stk_any())) {

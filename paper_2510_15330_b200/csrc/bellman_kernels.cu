@@ -717,7 +717,7 @@ struct Sim {
     acc_cnt = 0;
     // the second containing t: usually the next one (no division)
     const uint32_t nb = sec_bound + (uint32_t)kUs;
-    sec_bound = (t < nb && nb < FAR32) ? nb : rel((ab(t) / kUs + 1u) * kUs);
+    sec_bound = ((t < nb) & (nb < FAR32)) ? nb : rel((ab(t) / kUs + 1u) * kUs);
   }
 
   // debug row of the second containing absolute instant ta
@@ -1338,7 +1338,7 @@ struct Sim {
           rr = v.w;
         }
       }
-      if (n) {
+      {  // n may be 0: every update below is then a no-op (no branch)
         const uint64_t words = (uint64_t)n * B;
         if (pre()) kv_res += (uint32_t)words;
         ticks += n;
@@ -1361,9 +1361,8 @@ struct Sim {
         if (DBG) __syncwarp();
         done += n;
       }
-      if (done == nmax) break;
       const uint32_t tnext = T + (cb + q);  // end of the next iteration
-      if (tnext >= stop || tnext < sec_bound) break;
+      if ((done == nmax) | (tnext >= stop) | (tnext < sec_bound)) break;
       roll_second(tnext);  // the next end opens a new second: ingest the closed one here
     }
     if (!KV0) {

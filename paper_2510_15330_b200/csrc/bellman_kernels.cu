@@ -780,7 +780,7 @@ struct Sim {
   }
   __device__ __forceinline__ void kv_add(uint64_t x) {  // kv K += x
     if (KV0) return;
-    const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
+    const uint64_t q = x / 1000u;  // constant divisor: a multiply-high sequence, no branch
     kr += (uint32_t)(x - q * 1000u);
     kq += (uint32_t)q;
     if (kr >= 1000u) {
@@ -790,7 +790,7 @@ struct Sim {
   }
   __device__ __forceinline__ void kv_sub(uint64_t x) {  // kv K -= x
     if (KV0) return;
-    const uint64_t q = (x >> 32) == 0 ? (uint64_t)((uint32_t)x / 1000u) : x / 1000u;
+    const uint64_t q = x / 1000u;  // constant divisor: a multiply-high sequence, no branch
     const uint32_t rem = (uint32_t)(x - q * 1000u);
     kq -= (uint32_t)q;
     if (kr < rem) {

@@ -286,10 +286,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: BELLMAN_BENCH_SHARE_GPU=1 folds ranks onto the visible GPUs (two
+    # ranks on one B200 exercise the N > 1 path; gloo, since NCCL wants one GPU per rank)
+    share = os.environ.get("BELLMAN_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     w = workload(world, args.seeds_per_gpu, args.workload)
     cols = w.columns()
     n = w.n_scenarios
@@ -307,10 +315,24 @@ def main():
     # (CUDA IPC mappings over NVLink / NVSwitch); --nccl-gather times the
     # separate NCCL all-gather instead.  The segment-histogram sum stays NCCL.
     fused = world > 1 and not args.nccl_gather
-    peers = None
+    peers, fused_err = None, None
     if fused:
-        peers = PAR.PeerRecords(full_dev, rank, world, local)
-        sim.set_peers(peers.ptrs)
+        try:
+            peers = PAR.PeerRecords(full_dev, rank, world, local)
+            sim.set_peers(peers.ptrs)
+            ok = torch.ones(1, device=dev)
+        except Exception as e:  # e.g. no CUDA IPC on this node: time the NCCL all-gather instead
+            fused_err = f"{type(e).__name__}: {e}"[:200]
+            ok = torch.zeros(1, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if ok.item() == 0:
+            fused = False
+            if peers is not None:
+                sim.set_peers([])
+                peers.close()
+                peers = None
+            print(f"bench: fused exchange unavailable ({fused_err or 'on another rank'}); using the NCCL all-gather",
+                  file=sys.stderr, flush=True)
 
     def step():
         sim.reset(stream)

@@ -63,40 +63,59 @@ def reduce_segments(seg: torch.Tensor) -> torch.Tensor:
     return seg
 
 
+def exchange_peer_pointers(local_ptr: int, rank: int, world: int, export, open_) -> tuple:
+    """Host side of the fused exchange: export this rank's array (export(ptr)
+    -> (handle bytes, offset)), all-gather the (handle, offset) pairs over the
+    process group, and map every other rank's (open_(handle, offset) -> (base,
+    ptr)).  Returns (ptrs, bases): ptrs[g] is rank g's array as seen here
+    (ptrs[rank] = local_ptr), bases the mappings to unmap later.  Pure host
+    logic, so it is tested with fake export/open callables over gloo."""
+    mine = export(local_ptr)
+    allh = [None] * world
+    if world > 1:
+        dist.all_gather_object(allh, mine)
+    else:
+        allh = [mine]
+    ptrs, bases = [], []
+    for g, (hb, o) in enumerate(allh):
+        if g == rank:
+            ptrs.append(local_ptr)
+            continue
+        base, ptr = open_(hb, o)
+        bases.append(base)
+        ptrs.append(ptr)
+    return ptrs, bases
+
+
 class PeerRecords:
     """Every rank's full-size (n, REC) record array, mapped into this process.
 
     `local` is this rank's array (a CUDA tensor, 16-byte aligned); the IPC
     handle of its allocation is exchanged over the process group and each
-    other rank's array is opened on `device`.  `ptrs[g]` is rank g's array as
-    a device pointer valid here (rank == g: local itself).  The host side —
-    handle exchange, ordering, ownership — is plain Python over
-    torch.distributed; the mapping itself is the library's."""
+    other rank's array is opened on `device` (`exchange_peer_pointers` with the
+    library's bellman_ipc_export / bellman_ipc_open).  `ptrs[g]` is rank g's
+    array as a device pointer valid here (rank == g: local itself)."""
 
     def __init__(self, local: torch.Tensor, rank: int, world: int, device: int):
         from . import _abi as A
 
         assert local.is_cuda and local.is_contiguous() and local.data_ptr() % 16 == 0
-        self.local, self.bases, self.ptrs = local, [], []
+        self.local = local
         L = A.lib()
-        h = (C.c_uint8 * 64)()
-        off = C.c_uint64()
-        A.check(L.bellman_ipc_export(C.c_void_p(local.data_ptr()), h, C.byref(off)))
-        mine = (bytes(h), int(off.value))
-        allh = [None] * world
-        if world > 1:
-            dist.all_gather_object(allh, mine)
-        else:
-            allh = [mine]
-        for g, (hb, o) in enumerate(allh):
-            if g == rank:
-                self.ptrs.append(local.data_ptr())
-                continue
+
+        def export(ptr):
+            h = (C.c_uint8 * 64)()
+            off = C.c_uint64()
+            A.check(L.bellman_ipc_export(C.c_void_p(ptr), h, C.byref(off)))
+            return bytes(h), int(off.value)
+
+        def open_(hb, o):
             base, ptr = C.c_void_p(), C.c_void_p()
             hh = (C.c_uint8 * 64).from_buffer_copy(hb)
             A.check(L.bellman_ipc_open(hh, o, device, C.byref(base), C.byref(ptr)))
-            self.bases.append(base.value)
-            self.ptrs.append(ptr.value)
+            return base.value, ptr.value
+
+        self.ptrs, self.bases = exchange_peer_pointers(local.data_ptr(), rank, world, export, open_)
 
     def close(self):
         from . import _abi as A

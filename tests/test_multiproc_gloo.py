@@ -87,3 +87,52 @@ def test_gather_reorder_uneven():
             gathered[r * m: r * m + len(ids)] = ids
         full = gathered.reshape(world, m).T.reshape(-1)[:n]
         assert list(full) == list(range(n))
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_15330_b200 import parallel as PAR
+
+    opened = []
+
+    def export(ptr):  # a fake IPC handle naming the exporting rank and its base
+        return (f"rank{rank}".encode(), ptr - 0x1000 * (rank + 1))
+
+    def open_(hb, off):
+        g = int(hb.decode()[4:])
+        base = 0x7000_0000 + g
+        opened.append((g, off))
+        return base, base + off
+
+    local = 0x1000 * (rank + 1) + 0x40  # "device pointer" of this rank's array
+    ptrs, bases = PAR.exchange_peer_pointers(local, rank, world, export, open_)
+    q.put((rank, ptrs, bases, opened))
+    dist.destroy_process_group()
+
+
+def test_peer_pointer_exchange_gloo():
+    """Host side of the fused exchange at world size 3 over gloo (fake IPC):
+    every rank gets one pointer per rank in rank order, its own array at its
+    own index, and maps each other rank's export exactly once at its offset."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in range(world):
+        r, ptrs, bases, opened = q.get(timeout=120)
+        got[r] = (ptrs, bases, opened)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, (ptrs, bases, opened) in got.items():
+        assert len(ptrs) == world and len(bases) == world - 1
+        assert ptrs[r] == 0x1000 * (r + 1) + 0x40
+        assert sorted(g for g, _ in opened) == [g for g in range(world) if g != r]
+        for g in range(world):
+            if g != r:
+                assert ptrs[g] == 0x7000_0000 + g + 0x40  # base + the exporter's offset

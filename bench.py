@@ -1,20 +1,23 @@
 #!/usr/bin/env python
 """Benchmark: simulated scenario-ticks/s of the beLLMan simulator on B200.
 
-Workload (BASELINE.json configs[1]): arrival-rate sweep
-0.5..8 RPS x 64 seeds x {controller off, on}, L8B decode-cost model, 600 s
-simulated per scenario = 2048 scenarios per GPU.  Weak scaling: at N GPUs the
-job is N x 2048 scenarios (64 N seeds), sharded by interleaving (rank r runs
-ids r, r+N, ...); summaries are gathered with NCCL all_gather and segment
-histograms all_reduced — the only exchange step.
+Workload (BASELINE.json configs[4], the default): the
+1M-scenario Monte Carlo sweep — 16 paper-trace variants x 16 controller
+configs (OFF + 15 of C3's grid) x 4096 seeds = 2^20 scenarios, P24 decode-cost
+model, drained.  Strong scaling: the job is the config's fixed scenario set at
+every N; rank r of N runs ids r, r+N, ... (2^20 / N per GPU), heavy-first
+inside its shard.  The one exchange step is the summary all-gather (fused into
+the tick kernel's epilogue over peer memory, or NCCL all_gather with
+--nccl-gather) plus the NCCL all_reduce of the integer segment histograms.
+`--workload C2|C3|C4` times another BASELINE config the same way.
 
 A step = one pass of the whole hot path (arrival generation, draws, decode
 iterations, controller, accounting, histograms, percentiles) over the shard,
-plus the summary gather.  Inputs are resident in HBM when the timed region
-starts (value); `e2e` repeats the step through the C ABI with host buffers
-(descriptor H2D in bellman_sim_create, summaries D2H in bellman_sim_stats).
+plus the exchange.  Inputs are resident in HBM when the timed region starts
+(value); `e2e` repeats the step through the C ABI with host buffers
+(descriptor H2D in bellman_sim_create, the rank's summaries D2H).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl reference]
 """
 from __future__ import annotations
 
@@ -36,48 +39,63 @@ import workloads as W  # noqa: E402
 
 METRIC = "simulated scenario-ticks/sec"
 UNIT = "scenario-ticks/s"
-SEEDS_PER_GPU = 64
 
 # Survey §8(d) algorithmic integer work per unit (warp-instructions): a0 per
 # tick, 130 per candidate and per admission (Philox-10 + -ln/table draws +
 # thinning), 12 per completion, 40 per ingested second, 6 per prefill end.
 A_TICK, A_CAND, A_ADMIT, A_DONE, A_SEC, A_PF = 12, 130, 130, 12, 40, 6
+# Algorithmic HBM bytes per scenario: the 64 B descriptor read
+# once and the 272 B summary record written once.
+B_DESC, B_REC = 64, 272
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seeds-per-gpu", type=int, default=SEEDS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N > 1: exchange summaries with a separate NCCL all-gather instead of the fused kernel stores")
-    ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5"],
-                    help="BASELINE config; C2 (configs[1]) is the reported bench line")
+    ap.add_argument("--workload", default="C5", choices=["C2", "C3", "C4", "C5"],
+                    help="BASELINE config; C5 (configs[4], 2^20 scenarios) is the reported bench line")
+    ap.add_argument("--no-peak", action="store_true", help="skip the integer-issue microbenchmark")
+    ap.add_argument("--seeds", type=int, default=None,
+                    help="tests only: override the config's seed count (the line then names the reduced set)")
     return ap.parse_args()
 
 
 WORKLOAD_DESC = {
-    "C2": "C2 rate sweep 0.5-8 RPS x 64 seeds/GPU x {off,on}, L8B cost model, 600 s cutoff",
-    "C3": "C3 controller grid 321 ctrls x 32 seeds/GPU, paper trace, P24, drain",
-    "C4": "C4 diurnal 24 h, 16 traces x 4 ctrls x 64 seeds/GPU, P24, drain",
-    "C5": "C5 Monte Carlo 16 trace variants x 16 ctrls x 4096 seeds/GPU (2^20), P24, drain",
+    "C2": "C2 rate sweep 0.5-8 RPS x 64 seeds x {off,on} = 2048 scenarios, L8B cost model, 600 s cutoff",
+    "C3": "C3 controller grid (32 threshold pairs x 10 ladders + OFF) x 32 seeds = 10272 scenarios, paper trace, "
+          "P24, drain",
+    "C4": "C4 diurnal 24 h, 16 traces x 4 ctrls x 64 seeds = 4096 scenarios, P24, drain",
+    "C5": "C5 Monte Carlo 16 trace variants x 16 ctrls x 4096 seeds = 2^20 scenarios, P24, drain",
 }
 
 
-def workload(world: int, seeds_per_gpu: int, name: str = "C2"):
-    """Weak scaling: every GPU gets the config's full per-GPU scenario set
-    (more seeds as the world grows)."""
+def workload(name: str = "C5", seeds: int | None = None):
+    """The BASELINE config as SURVEY §8(d) fixes it: the same scenario set at
+    every N (strong scaling; ranks shard it).  `seeds` (tests only) shrinks it."""
+    kw = {} if seeds is None else {"n_seeds": seeds}
     if name == "C3":
-        return W.config_c3(n_seeds=32 * world)
+        return W.config_c3(**kw)
     if name == "C4":
-        return W.config_c4(n_seeds=64 * world)
-    if name == "C5":
-        return W.config_c5(n_seeds=4096 * world)
-    return W.config_c2(n_seeds=seeds_per_gpu * world)
+        return W.config_c4(**kw)
+    if name == "C2":
+        return W.config_c2(**kw)
+    return W.config_c5(**kw)
+
+
+def config_dict(name: str, n_total: int, world: int, seeds: int | None = None) -> dict:
+    """The `config` object of both arms' JSON lines (identical at equal N)."""
+    desc = WORKLOAD_DESC[name] + ("" if seeds is None else f" [reduced: {seeds} seeds]")
+    return {"workload": desc, "scenarios": n_total,
+            "scenarios_per_gpu": (n_total + world - 1) // world,
+            "parallelism": f"scenario-sharded x{world} (rank r runs ids r, r+{world}, ...)",
+            "l2": "flushed between steps (256 MiB write)"}
 
 
 def algorithmic_ops(st) -> float:
@@ -241,7 +259,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w = workload(1, args.seeds_per_gpu, args.workload)
+    w = workload(args.workload, args.seeds)
     cols = w.columns()
     import oracle
 
@@ -260,17 +278,37 @@ def run_reference(args):
         ticks = sum(r["ticks"] for r in rs)
     tot = sum(times)
     value = ticks * args.steps / tot
-    what = "the full" if stride == 1 else f"a stride-{stride} subsample ({len(sids)} scenarios) of the"
+    what = "the full" if stride == 1 else f"a stride-{stride} subsample ({len(sids)} scenarios, id % {stride} == 0) of the"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC[args.workload], "scenarios_per_gpu": n, "scenarios_total": n,
-                       "ticks_per_step": int(ticks), "parallelism": "oracle, host threads"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": config_dict(args.workload, n, args.gpus, args.seeds),
+            "ticks_per_step": int(ticks),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                              "sample": f"{args.steps} steps x {what} {n}-scenario workload"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def outputs(st_all, seg_hist, n_segments):
+    """The metric's outputs (BASELINE.json: p50/p99 E2E latency, energy) over
+    the whole job: nearest-rank p50/p99 on the merged E2E histogram (lower bin
+    edge, ms; R13), served, energy.  Reporting only (not parity)."""
+    def edge(b):  # log-linear bins, 32 per octave above 32 ms (DESIGN §2 a9)
+        return b if b < 32 else (32 + b % 32) << (b // 32 - 1)
+
+    def nr(h, p):
+        n = int(h.sum())
+        if n == 0:
+            return None
+        k = max(1, -(-p * n // 100))
+        return edge(int(np.searchsorted(np.cumsum(h), k)))
+
+    h = seg_hist[:, :896].sum(axis=0)
+    return {"e2e_p50_ms": nr(h, 50), "e2e_p99_ms": nr(h, 99), "served": int(st_all["served"].sum()),
+            "energy_j": float(st_all["energy_j"].sum()), "win_energy_j": float(st_all["win_energy_j"].sum()),
+            "note": f"job totals over {len(st_all)} scenarios / {n_segments} segments; p50/p99 = lower edge of the "
+                    "merged E2E histogram bin holding the nearest rank (R13)"}
 
 
 def main():
@@ -298,7 +336,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    w = workload(world, args.seeds_per_gpu, args.workload)
+    w = workload(args.workload, args.seeds)
     cols = w.columns()
     n = w.n_scenarios
     mine = W.shard(n, rank, world)
@@ -317,21 +355,12 @@ def main():
     fused = world > 1 and not args.nccl_gather
     peers, fused_err = None, None
     if fused:
-        try:
-            peers = PAR.PeerRecords(full_dev, rank, world, local)
+        peers, fused_err = PAR.open_peer_records(full_dev, rank, world, local)
+        if peers is not None:
             sim.set_peers(peers.ptrs)
-            ok = torch.ones(1, device=dev)
-        except Exception as e:  # e.g. no CUDA IPC on this node: time the NCCL all-gather instead
-            fused_err = f"{type(e).__name__}: {e}"[:200]
-            ok = torch.zeros(1, device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
-        if ok.item() == 0:
+        else:
             fused = False
-            if peers is not None:
-                sim.set_peers([])
-                peers.close()
-                peers = None
-            print(f"bench: fused exchange unavailable ({fused_err or 'on another rank'}); using the NCCL all-gather",
+            print(f"bench: fused exchange unavailable ({fused_err}); using the NCCL all-gather",
                   file=sys.stderr, flush=True)
 
     def step():
@@ -339,7 +368,7 @@ def main():
         sim.run(first=rank, count=count, stride=world, stream=stream)
         k_end = torch.cuda.Event(enable_timing=True)
         k_end.record(stream)
-        if not fused:
+        if world > 1 and not fused:
             sim.stats_device(stats_dev, stream=stream)
             PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank, world, out=full_dev)
         sim.segment_hist_device(seg_dev, stream=stream)
@@ -381,18 +410,27 @@ def main():
         dist.barrier()
         assert torch.equal(chk, full_dev), "fused peer-memory exchange differs from the NCCL all-gather"
     st_local = stats_dev.cpu().numpy().view(_abi.STATS).reshape(-1)
-    local_ticks = int(st_local["ticks"][mine].astype(np.int64).sum())
-    local_ops = algorithmic_ops(st_local[mine])
+    st_mine = st_local[mine]
+    local_ticks = int(st_mine["ticks"].astype(np.int64).sum())
+    local_ops = algorithmic_ops(st_mine)
     tt = torch.tensor([local_ticks, local_ops], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt)
     ticks_all, ops_all = float(tt[0]), float(tt[1])
     value = ticks_all * args.steps / (tot_ms / 1e3)
     launches = sim.last_launches
+    if world > 1:
+        st_all = (full_dev if fused else PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank,
+                                                              world)).cpu().numpy().view(_abi.STATS).reshape(-1)
+    else:
+        st_all = st_local
+    outs = outputs(st_all, seg_dev.cpu().numpy().view(np.uint64), w.n_segments)
 
-    # ---- e2e through the C ABI with host buffers (pinned) ----
+    # ---- e2e through the C ABI with host buffers (pinned): descriptors H2D,
+    # the rank's shard simulated, the rank's records D2H ----
     pk = pack(cols, pinned=True)
-    host_stats = torch.empty((n, _abi.STATS.itemsize), dtype=torch.uint8, pin_memory=True).numpy().view(_abi.STATS).reshape(-1)
+    host_stats = torch.empty((count, _abi.STATS.itemsize), dtype=torch.uint8,
+                             pin_memory=True).numpy().view(_abi.STATS).reshape(-1)
     e2e_ms = []
     for i in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
@@ -403,7 +441,10 @@ def main():
         a.record(stream)
         s2 = Simulator(packed=pk, device=local, stream=stream, workspace=sim.ws)
         s2.run(first=rank, count=count, stride=world, stream=stream)
-        s2.stats(out=host_stats, stream=stream)
+        if world == 1:
+            s2.stats(out=host_stats, stream=stream)
+        else:
+            s2.stats_shard(rank, world, count, out=host_stats, stream=stream)
         b.record(stream)
         torch.cuda.synchronize()
         s2.close()
@@ -415,7 +456,7 @@ def main():
     e2e_value = ticks_all * len(e2e_ms) / (float(e[0]) / 1e3) if e2e_ms else None
     h2d = int(sum(v.nbytes for k, v in pk.items() if isinstance(v, np.ndarray)) +
               sum(v.nbytes for v in pk["tables"].values()) + 8 * W.TABLE_N + 4 * n)
-    d2h = int(n * _abi.STATS.itemsize)
+    d2h = int(count * _abi.STATS.itemsize)
     if peers is not None:  # every rank's kernels are done: unmap the peers' arrays
         torch.cuda.synchronize()
         dist.barrier()
@@ -433,43 +474,52 @@ def main():
     kern_s = kern_tot / 1e3 / args.steps
     achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G warp-inst/s
     peak = 148 * 4 * mhz * 1e6 / 1e9
-    # measured integer issue / lane throughput (microbenchmark, after the timed region)
-    from paper_2510_15330_b200 import peak as PEAK
-
-    mb = PEAK.measure(local)
-    issue_meas = 148 * mb["mixed_warp_inst_per_clk_sm"] * mhz * 1e6 / 1e9
-    l_int = max(mb["mixed_lanes_per_clk_sm"], mb["alu_lanes_per_clk_sm"], mb["fma_lanes_per_clk_sm"])
-    lane_peak = 148 * l_int * mhz * 1e6 / 1e9
     traffic, traffic_src = ncu_traffic(args.workload)
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time (max over ranks, per GPU); "
+                    f"peak = 148 SM x 4 issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM bytes "
+                    f"per launch ({traffic_src or 'no capture'})"}
+    if not args.no_peak:
+        # measured integer issue / lane throughput (microbenchmark, after the timed region)
+        from paper_2510_15330_b200 import peak as PEAK
+
+        mb = PEAK.measure(local)
+        best = max(v for k, v in mb.items() if "warp_inst" in k)
+        issue_meas = 148 * best * mhz * 1e6 / 1e9
+        l_int = max(mb["mixed_lanes_per_clk_sm"], mb["alu_lanes_per_clk_sm"], mb["fma_lanes_per_clk_sm"])
+        lane_peak = 148 * l_int * mhz * 1e6 / 1e9
+        roof["issue_measured"] = {"peak": issue_meas, "frac": achieved / issue_meas,
+                                  "warp_inst_per_clk_sm": {k.split("_warp")[0]: round(v, 3) for k, v in mb.items()
+                                                           if "warp_inst" in k},
+                                  "note": "peak = the best measured integer issue rate x 148 SM x clock"}
+        roof["lane"] = {"L_int": l_int, "peak": lane_peak, "unit": "G int-lane-ops/s", "frac": achieved / lane_peak,
+                        "note": "R_lane (SURVEY 8(d)): every algorithmic op is one warp-instruction in the "
+                                "warp-per-scenario design, so achieved counts it once; L_int measured"}
+    # HBM (BASELINE north_star asks for achieved GB/s): algorithmic bytes = descriptor in + record out
+    # per scenario of the launch; ncu bytes = the committed capture's DRAM read + write
+    alg_bytes = (B_DESC + B_REC) * count
+    roof["hbm"] = {"algorithmic_bytes": alg_bytes, "achieved_gbs": alg_bytes / kern_s / 1e9,
+                   "ncu_bytes": traffic, "ncu_gbs": (traffic / kern_s / 1e9) if traffic else None,
+                   "peak_gbs": pk_["hbm_gbs"], "frac": alg_bytes / kern_s / 1e9 / pk_["hbm_gbs"]}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(workload(1, args.seeds_per_gpu, args.workload).columns())
+        cpu = cpu_baseline(cols)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload],
-                   "scenarios_per_gpu": count, "scenarios_total": n, "ticks_per_step": int(ticks_all),
-                   "parallelism": f"scenario-sharded x{world}", "l2": "flushed between steps (256 MiB write)",
-                   "exchange": ("none (1 GPU)" if world == 1 else "NCCL all-gather" if not fused else
-                                "fused: records stored to every rank over peer memory by the tick kernel; "
-                                "segment histograms NCCL all-reduce")},
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "issue_measured": {"peak": issue_meas, "frac": achieved / issue_meas,
-                                        "warp_inst_per_clk_sm": {k.split("_warp")[0]: round(v, 3) for k, v in mb.items()
-                                                                 if "warp_inst" in k}},
-                     "lane": {"L_int": l_int, "peak": lane_peak, "unit": "G int-lane-ops/s",
-                              "frac": achieved / lane_peak,
-                              "note": "R_lane (SURVEY 8(d)): every algorithmic op is one warp-instruction in the "
-                                      "warp-per-scenario design, so achieved counts it once; L_int measured"},
-                     "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time; peak = 148 SM x 4 "
-                             f"issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM bytes per launch "
-                             f"({traffic_src or 'no capture'})"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": config_dict(args.workload, n, world, args.seeds),
+        "ticks_per_step": int(ticks_all),
+        "exchange": ("none (1 GPU)" if world == 1 else "NCCL all-gather" if not fused else
+                     "fused: records stored to every rank over peer memory by the tick kernel; "
+                     "segment histograms NCCL all-reduce"),
+        "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
         "kernel_ms_per_step": kern_tot / args.steps,
+        "outputs": outs,
     }
     if lat is not None:
         line["latency_floor"] = lat

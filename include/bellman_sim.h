@@ -279,10 +279,11 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
  * (interleaved sharding across ranks: first = rank, stride = world size).
  * Calibrated scenarios (a10) need their source in the same set.  Launches the
  * pass-1 kernel, then (if any calibrated scenario is in the set) the
- * calibration kernel and the pass-2 kernel.  A whole-set run (first 0,
- * stride 1, count n_scenarios) hands scenarios to warps in decreasing order of
- * expected arrivals (heavy first, for load balance); results never depend on
- * that order.  Asynchronous. */
+ * calibration kernel and the pass-2 kernel.  Every run hands its scenarios to
+ * warps in decreasing order of expected arrivals (heavy first, for load
+ * balance; a shard's order is the whole set's order filtered to the shard,
+ * uploaded into the workspace on the first run of each distinct
+ * (first, stride, count)); results never depend on that order.  Asynchronous. */
 bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count, uint64_t stride,
                                void *stream);
 
@@ -291,6 +292,14 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
  * `stream` for host dst. */
 bellman_status bellman_sim_stats(bellman_sim *sim, bellman_scenario_stats *dst, uint64_t first,
                                  uint64_t count, int dst_is_device, void *stream);
+
+/* Copy the `count` summary records of scenario ids first, first+stride, ...,
+ * first+(count-1)*stride (a rank's interleaved shard) to dst, packed densely
+ * (record k of dst = scenario first + k*stride).  One strided copy; same
+ * synchronisation as bellman_sim_stats.  BELLMAN_ESTATE if the range leaves
+ * [0, n_scenarios) or stride is 0. */
+bellman_status bellman_sim_stats_strided(bellman_sim *sim, bellman_scenario_stats *dst, uint64_t first,
+                                         uint64_t count, uint64_t stride, int dst_is_device, void *stream);
 
 /* Copy the per-segment histograms, n_segments x BELLMAN_SEG_HIST_WORDS uint64:
  * [E2E 896 | TTFT 896 | r 512 | similarity active 201 | inactive 201] integer

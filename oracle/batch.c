@@ -37,7 +37,7 @@ int orc_run_batch(const orc_inputs *in, const uint64_t *sids, uint64_t n, orc_re
   if (!th) return -1;
   int started = 0;
   for (int t = 0; t < nthreads; ++t)
-    if (pthread_create(&th[t], NULL, worker, &p) == 0) started++;
+    if (pthread_create(&th[started], NULL, worker, &p) == 0) started++; /* handles stay compact */
   if (started == 0) worker(&p);
   for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
   free(th);

@@ -81,6 +81,8 @@ EXPORTS = {
                                      C.POINTER(C.c_void_p)]),
     "bellman_sim_run": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]),
     "bellman_sim_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]),
+    "bellman_sim_stats_strided": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                            C.c_void_p]),
     "bellman_sim_segment_hist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "bellman_sim_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bellman_sim_series": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),

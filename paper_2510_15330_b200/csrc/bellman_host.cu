@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 #include <vector>
 
 #include "bellman_internal.cuh"
@@ -31,10 +33,23 @@ struct bellman_sim {
   std::vector<uint64_t> dbg_off;
   std::vector<uint32_t> dbg_cap;
   const uint32_t *order = nullptr;   // device: scenarios by decreasing expected work
+  uint32_t *shard_order = nullptr;   // device: the heavy-first order of the last strided shard run
+  std::vector<uint32_t> host_order;  // host copy of `order`
+  std::vector<uint32_t> host_shard;  // host copy of `shard_order` (its key below)
+  uint64_t shard_key[3] = {~0ull, ~0ull, ~0ull};  // (first, stride, count) that host_shard holds
+  uint64_t shard_gen = 0;            // this handle's upload stamp (see shard_region_owner)
   char err[512] = {0};
 };
 
 static thread_local char g_err[512];
+
+// Several handles may be created on one caller-owned workspace (one at a time
+// in use).  The shard-order region is written by bellman_sim_run, so a handle
+// may reuse its cached upload only if no other handle wrote that region since:
+// every upload stamps the region's address with a fresh generation.
+static std::mutex g_shard_mu;
+static std::unordered_map<const void *, uint64_t> g_shard_owner;
+static uint64_t g_shard_gen = 0;
 
 static bellman_status fail(bellman_sim *sim, bellman_status st, const char *fmt, ...) {
   char *dst = sim ? sim->err : g_err;
@@ -166,6 +181,14 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (sc.horizon_us <= 0 || sc.horizon_us > (1ll << 43))
       return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon out of range", (unsigned long long)s);
     if (sc.w0_us > sc.w1_us) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: w0 > w1", (unsigned long long)s);
+    {  // the kernel counts iterations in 32 bits: every iteration starts before H and lasts >= t0
+       // (a contending prefill-only iteration >= 1 µs), so ticks <= H / min_iter + 1 must stay < 2^32
+      const bellman_profile &pf = d->profiles[sc.profile];
+      const uint64_t min_iter = pf.prefill_mode == BELLMAN_PREFILL_CONTENDING ? 1u : pf.t0_us;
+      if ((uint64_t)sc.horizon_us / min_iter + 1u >= 0xFFFFFFFFull)
+        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon / t0 allows >= 2^32 iterations",
+                    (unsigned long long)s);
+    }
     const bellman_ctrl &c = d->ctrls[sc.ctrl];
     if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) {
       if (sc.calib_src >= d->n_scenarios) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calib_src out of range", (unsigned long long)s);
@@ -184,7 +207,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, off_ord, off_pre, total;
+      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, total;
   size_t in_end;              // [0, in_end): host-filled inputs, one staging copy at create
   size_t zero_beg, zero_end;  // [zero_beg, zero_end): zeroed at create (counters, stats, histograms)
 };
@@ -331,6 +354,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_calib = take(sizeof(uint32_t) * 4 * ns);
   L.off_drows = take(sizeof(bellman_second_row) * h.dbg_rows);
   L.off_dctrl = take(sizeof(bellman_ctrl_row) * h.dbg_rows);
+  L.off_sord = take(sizeof(uint32_t) * d->n_scenarios);  // a strided shard's order, written by bellman_sim_run
   // NEXT-4 preemption scratch (per CTA: slot side state + the preempted stack),
   // only when some profile preempts
   bool pre = false;
@@ -459,6 +483,8 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.order = nullptr;
   P.pre = (PreScratch *)(ws + L.off_pre);
   sim->order = (const uint32_t *)(ws + L.off_ord);
+  sim->shard_order = (uint32_t *)(ws + L.off_sord);
+  sim->host_order = h.order;
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
   sim->dbg_off = h.dbg_off;
@@ -538,8 +564,32 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   P.first = first;
   P.count = count;
   P.stride = stride;
-  // a whole-set run takes the scenarios heavy-first; a subset keeps index order
-  P.order = (first == 0 && stride == 1 && count == sim->n_scenarios) ? sim->order : nullptr;
+  // every run takes its scenarios heavy-first: a whole-set run from the create-time
+  // order, a shard (first + k stride, k < count) from that order filtered to the
+  // shard (stable, so equal costs keep id order), uploaded once per distinct shard
+  if (first == 0 && stride == 1 && count == sim->n_scenarios) {
+    P.order = sim->order;
+  } else {
+    std::lock_guard<std::mutex> lk(g_shard_mu);
+    auto it = g_shard_owner.find(sim->shard_order);
+    const bool mine = it != g_shard_owner.end() && it->second == sim->shard_gen;
+    if (!mine || sim->shard_key[0] != first || sim->shard_key[1] != stride || sim->shard_key[2] != count) {
+      sim->host_shard.clear();
+      sim->host_shard.reserve(count);
+      for (uint32_t id : sim->host_order)
+        if (id >= first && (id - first) % stride == 0 && (id - first) / stride < count) sim->host_shard.push_back(id);
+      if (sim->host_shard.size() != count) return fail(sim, BELLMAN_ESTATE, "shard order: internal size mismatch");
+      // the host vector outlives the copy (a member), and the copy is stream-ordered before the launch
+      CUDA_TRY(sim, cudaMemcpyAsync(sim->shard_order, sim->host_shard.data(), sizeof(uint32_t) * count,
+                                    cudaMemcpyHostToDevice, s));
+      sim->shard_key[0] = first;
+      sim->shard_key[1] = stride;
+      sim->shard_key[2] = count;
+      sim->shard_gen = ++g_shard_gen;
+      g_shard_owner[sim->shard_order] = sim->shard_gen;
+    }
+    P.order = sim->shard_order;
+  }
 #ifdef BELLMAN_AB_NOORDER
   P.order = nullptr;
 #endif
@@ -583,6 +633,23 @@ bellman_status bellman_sim_stats(bellman_sim *sim, bellman_scenario_stats *dst, 
   CUDA_TRY(sim, cudaSetDevice(sim->device));
   CUDA_TRY(sim, cudaMemcpyAsync(dst, sim->params.stats + first, sizeof(bellman_scenario_stats) * count,
                                 dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (!dst_is_device) CUDA_TRY(sim, cudaStreamSynchronize(s));
+  return BELLMAN_OK;
+}
+
+bellman_status bellman_sim_stats_strided(bellman_sim *sim, bellman_scenario_stats *dst, uint64_t first,
+                                         uint64_t count, uint64_t stride, int dst_is_device, void *stream) {
+  if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
+  if (!dst) return fail(sim, BELLMAN_EINVAL, "dst is NULL");
+  if (stride == 0) return fail(sim, BELLMAN_ESTATE, "stride must be >= 1");
+  if (count == 0) return BELLMAN_OK;
+  if (first >= sim->n_scenarios || (count - 1) > (sim->n_scenarios - 1 - first) / stride)
+    return fail(sim, BELLMAN_ESTATE, "stats range out of bounds");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(sim, cudaSetDevice(sim->device));
+  const size_t rec = sizeof(bellman_scenario_stats);
+  CUDA_TRY(sim, cudaMemcpy2DAsync(dst, rec, sim->params.stats + first, rec * stride, rec, count,
+                                  dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   if (!dst_is_device) CUDA_TRY(sim, cudaStreamSynchronize(s));
   return BELLMAN_OK;
 }

@@ -63,27 +63,66 @@ def reduce_segments(seg: torch.Tensor) -> torch.Tensor:
     return seg
 
 
-def exchange_peer_pointers(local_ptr: int, rank: int, world: int, export, open_) -> tuple:
+class PeerExchangeError(RuntimeError):
+    """The fused exchange could not be set up on some rank (raised on every rank)."""
+
+
+def _agree(ok: bool, world: int) -> list:
+    """Every rank's flag, on every rank (one all_gather_object)."""
+    flags = [None] * world
+    if world > 1:
+        dist.all_gather_object(flags, ok)
+    else:
+        flags = [ok]
+    return flags
+
+
+def exchange_peer_pointers(local_ptr: int, rank: int, world: int, export, open_, close=None) -> tuple:
     """Host side of the fused exchange: export this rank's array (export(ptr)
     -> (handle bytes, offset)), all-gather the (handle, offset) pairs over the
     process group, and map every other rank's (open_(handle, offset) -> (base,
     ptr)).  Returns (ptrs, bases): ptrs[g] is rank g's array as seen here
-    (ptrs[rank] = local_ptr), bases the mappings to unmap later.  Pure host
+    (ptrs[rank] = local_ptr), bases the mappings to unmap later.
+
+    Collective-safe: every rank joins the same two all_gather_object calls
+    whatever fails locally (a failed export sends None), and if the export or
+    any mapping failed on ANY rank, every rank unmaps what it opened (close(base))
+    and raises PeerExchangeError — all ranks take the same path.  Pure host
     logic, so it is tested with fake export/open callables over gloo."""
-    mine = export(local_ptr)
+    err = None
+    try:
+        mine = export(local_ptr)
+    except Exception as e:  # noqa: BLE001 — reported collectively below
+        mine, err = None, f"rank {rank} export: {type(e).__name__}: {e}"
     allh = [None] * world
     if world > 1:
         dist.all_gather_object(allh, mine)
     else:
         allh = [mine]
     ptrs, bases = [], []
-    for g, (hb, o) in enumerate(allh):
-        if g == rank:
-            ptrs.append(local_ptr)
-            continue
-        base, ptr = open_(hb, o)
-        bases.append(base)
-        ptrs.append(ptr)
+    if all(h is not None for h in allh):
+        try:
+            for g, (hb, o) in enumerate(allh):
+                if g == rank:
+                    ptrs.append(local_ptr)
+                    continue
+                base, ptr = open_(hb, o)
+                bases.append(base)
+                ptrs.append(ptr)
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank} open: {type(e).__name__}: {e}"
+    else:
+        err = err or "export failed on rank(s) " + ",".join(str(g) for g, h in enumerate(allh) if h is None)
+    flags = _agree(err is None, world)
+    if not all(flags):
+        if close is not None:
+            for b in bases:
+                try:
+                    close(b)
+                except Exception:  # noqa: BLE001 — best effort unmapping on the failure path
+                    pass
+        bad = [g for g, f in enumerate(flags) if not f]
+        raise PeerExchangeError(err or f"peer exchange failed on rank(s) {bad}")
     return ptrs, bases
 
 
@@ -94,7 +133,8 @@ class PeerRecords:
     handle of its allocation is exchanged over the process group and each
     other rank's array is opened on `device` (`exchange_peer_pointers` with the
     library's bellman_ipc_export / bellman_ipc_open).  `ptrs[g]` is rank g's
-    array as a device pointer valid here (rank == g: local itself)."""
+    array as a device pointer valid here (rank == g: local itself).  Raises
+    PeerExchangeError on every rank if any rank fails."""
 
     def __init__(self, local: torch.Tensor, rank: int, world: int, device: int):
         from . import _abi as A
@@ -115,7 +155,10 @@ class PeerRecords:
             A.check(L.bellman_ipc_open(hh, o, device, C.byref(base), C.byref(ptr)))
             return base.value, ptr.value
 
-        self.ptrs, self.bases = exchange_peer_pointers(local.data_ptr(), rank, world, export, open_)
+        def close(b):
+            L.bellman_ipc_close(C.c_void_p(b))
+
+        self.ptrs, self.bases = exchange_peer_pointers(local.data_ptr(), rank, world, export, open_, close)
 
     def close(self):
         from . import _abi as A
@@ -123,3 +166,12 @@ class PeerRecords:
         for b in self.bases:
             A.lib().bellman_ipc_close(C.c_void_p(b))
         self.bases, self.ptrs = [], []
+
+
+def open_peer_records(local: torch.Tensor, rank: int, world: int, device: int):
+    """(PeerRecords, None) if every rank mapped every peer array, else
+    (None, reason) on every rank (the caller falls back to the NCCL all-gather)."""
+    try:
+        return PeerRecords(local, rank, world, device), None
+    except PeerExchangeError as e:
+        return None, str(e)[:200]

@@ -32,8 +32,10 @@ def aggregate_per_second(rows: np.ndarray, ctrl: np.ndarray | None, profile: dic
     if ctrl is not None and len(ctrl):
         cur, k = 0, 0
         order = list(ctrl)
+        # the controller row of second s is ingested once s has closed, so its r
+        # governs admissions from second s + 1 on (R21): row s is in force from s + 1
         for s in range(len(rows)):
-            while k < len(order) and int(order[k]["second"]) <= s:
+            while k < len(order) and int(order[k]["second"]) < s:
                 cur = int(order[k]["r_bp"])
                 k += 1
             r_at[s] = cur

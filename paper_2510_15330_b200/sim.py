@@ -167,6 +167,18 @@ class Simulator:
                                           C.c_void_p(_stream_ptr(stream))), self.h)
         return out
 
+    def stats_shard(self, first: int, stride: int, count: int | None = None, out: np.ndarray | None = None,
+                    stream=None):
+        """Records of scenarios first, first+stride, ... (a rank's shard), packed, to host memory."""
+        if count is None:
+            count = (self.n_scenarios - first + stride - 1) // stride
+        if out is None:
+            out = np.zeros(count, dtype=A.STATS)
+        assert out.nbytes >= count * A.STATS.itemsize
+        A.check(A.lib().bellman_sim_stats_strided(self.h, C.c_void_p(out.ctypes.data), first, count, stride, 0,
+                                                  C.c_void_p(_stream_ptr(stream))), self.h)
+        return out
+
     def segment_hist(self, stream=None) -> np.ndarray:
         out = np.zeros((self.n_segments, A.SEG_HIST_WORDS), dtype=np.uint64)
         A.check(A.lib().bellman_sim_segment_hist(self.h, C.c_void_p(out.ctypes.data), 0,

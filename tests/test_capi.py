@@ -55,6 +55,16 @@ def test_struct_sizes_and_validation():
     bad["ctrl_t2"] = bad["ctrl_t1"].copy()  # S:269 t1 < t2
     with pytest.raises(A.BellmanError, match="t1 < t2"):
         sim.workspace_bytes(sim.pack(bad))
+    # the kernel's iteration counter is 32-bit: horizon / t0 must allow < 2^32 iterations
+    bad = W.config_c2(n_seeds=1, rates=[1.0]).columns()
+    bad["prof_t0"] = bad["prof_t0"].copy()
+    bad["prof_t0"][:] = 1
+    bad["sc_horizon"] = bad["sc_horizon"].copy()
+    bad["sc_horizon"][:] = 1 << 32
+    with pytest.raises(A.BellmanError, match="2\\^32 iterations"):
+        sim.workspace_bytes(sim.pack(bad))
+    bad["sc_horizon"][:] = (1 << 32) - 3  # ticks <= H / t0 + 1 < 2^32: accepted
+    assert sim.workspace_bytes(sim.pack(bad)) > 0
 
 
 def test_kv_policy_validation_and_scratch():
@@ -84,16 +94,23 @@ def test_kv_policy_validation_and_scratch():
         sim.workspace_bytes(sim.pack(cols(prof_kv_cap=2**28, prof_kv_policy=1)))
 
 
-def test_sass_has_no_fp_outside_energy():
+def test_sass_sm100a_warp_level_no_transcendentals():
     """Kernel built for sm_100a; the tick kernel's SASS uses warp vote/shuffle/
-    reduce instructions (the warp-level design) and compiles without spills
-    beyond the documented budget."""
+    reduce instructions (the warp-level design), and no kernel evaluates a
+    transcendental (R33: no libm on the sampling path — -ln U and the quantile
+    draws are integer tables): the only MUFU forms are the reciprocal seeds of
+    integer / IEEE division (RCP, RCP64H), never EX2 / LG2 / SIN / COS / SQRT / RSQ.
+    (Floating point that does appear: the energy epilogue's IEEE fp64 ops and
+    the quality decay's fp32 with an exact integer fix-up.)"""
+    import re as _re
+    import subprocess
+
     from paper_2510_15330_b200 import build as B
 
     path = B.build()
-    import subprocess
-
     out = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
     assert "sm_100a" in out or "SM100" in out.upper() or "arch = sm_100a" in out
     for mnemonic in ("VOTE", "SHFL", "REDUX"):
         assert mnemonic in out, mnemonic
+    mufu = set(_re.findall(r"MUFU\.(\w+)", out))
+    assert mufu <= {"RCP", "RCP64H"}, mufu

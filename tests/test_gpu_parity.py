@@ -140,30 +140,36 @@ def test_sharded_runs_match_single_run():
         assert np.array_equal(st.view(np.uint8), full.view(np.uint8))
 
 
-def _full_size_sampled(w, n_sample):
+def _full_size_sampled(w, stride, sim=None):
     """A BASELINE config at full size in bench.py's launch configuration (one
-    whole-set launch, heavy-first order): a deterministic stride sample of
-    records vs the oracle, and on every record the properties that hold at
-    any size — written, arrivals = admitted + queued, admitted = served +
-    in flight, a drained run leaves nothing behind, energy is the fp64 formula
-    of the record's own integers (R19)."""
+    whole-set launch, heavy-first order): the records with id % stride == 0
+    (SURVEY §8(d)'s deterministic stride subsample) vs the oracle, and on every
+    record the properties that hold at any size — written, arrivals = admitted
+    + queued, admitted = served + in flight, a drained run leaves nothing
+    behind, energy is the fp64 formula of the record's own integers (R19)."""
     import torch
 
     from paper_2510_15330_b200 import Simulator
 
     cols = w.columns()
-    sim = Simulator(cols)
+    sim = sim or Simulator(cols)
     sim.run()
     torch.cuda.synchronize()
     st = sim.stats()
     assert sim.last_launches == 1
     n = w.n_scenarios
-    sids = np.arange(0, n, max(1, n // n_sample), dtype=np.uint64)
+    sids = np.arange(0, n, stride, dtype=np.uint64)
     rs = oracle.run_batch(oracle.Bound(cols), sids)
     bad = [(int(s), e) for s, o in zip(sids, rs) for e in [compare(st[int(s)], o, int(s))] if e]
     _assert_ok(bad)
+    _invariants(st, cols, n)
+    return st
+
+
+def _invariants(st, cols, n, ids=None):
+    ids = np.arange(n) if ids is None else ids
     assert np.all(st["flags"] & 0x100)
-    assert np.array_equal(st["scenario_id"], np.arange(n))
+    assert np.array_equal(st["scenario_id"], ids)
     assert np.array_equal(st["arrivals"], st["admitted"] + st["queued_end"])
     assert np.array_equal(st["admitted"], st["served"] + st["inflight_end"])
     drained = (st["flags"] & 1) == 0
@@ -173,25 +179,49 @@ def _full_size_sampled(w, n_sample):
     e = (prof[0] * st["words_in"].astype(np.float64) + prof[1] * st["words_out"].astype(np.float64)) + \
         prof[2] * st["idle_us"].astype(np.float64) / 1e6
     assert np.array_equal(e, st["energy_j"])
-    return st
 
 
-def test_c5_full_size_sampled():
-    """BASELINE configs[4]: 2^20 scenarios (one GPU's shard of the 8-GPU sweep)."""
-    st = _full_size_sampled(W.config_c5(), 96)
+def test_c5_full_size_stride64_and_strong_scaled_shard():
+    """BASELINE configs[4] (2^20 scenarios) in bench.py's N = 1 launch
+    configuration: the 16,384 records with id % 64 == 0 vs the oracle
+    (SURVEY §8(d)), invariants on all 2^20.  Then one rank's shard of the
+    strong-scaled 8-GPU run (first = 5, stride = 8, 131,072 scenarios, in the
+    shard's own heavy-first order): every record byte-equal to the whole-set
+    run's, and the 16,384 with id % 64 == 5 vs the oracle."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    w = W.config_c5()
+    cols = w.columns()
+    sim = Simulator(cols)
+    st = _full_size_sampled(w, 64, sim)
     assert int(st["ticks"].sum()) > 5e10
+    sim.reset()
+    sim.run(first=5, count=(w.n_scenarios - 5 + 7) // 8, stride=8)
+    torch.cuda.synchronize()
+    sh = sim.stats_shard(5, 8)
+    assert len(sh) == 131072
+    assert np.array_equal(sh.view(np.uint8), st[5::8].view(np.uint8))
+    sids = np.arange(5, w.n_scenarios, 64, dtype=np.uint64)
+    rs = oracle.run_batch(oracle.Bound(cols), sids)
+    bad = [(int(s), e) for s, o in zip(sids, rs) for e in [compare(sh[(int(s) - 5) // 8], o, int(s))] if e]
+    _assert_ok(bad)
+    untouched = sim.stats(first=0, count=5)  # ids outside the shard stay zero after reset
+    assert not untouched.view(np.uint8).any()
 
 
-def test_c4_full_size_sampled():
-    """BASELINE configs[3]: 24 h diurnal traces with bursts, 4096 scenarios."""
-    st = _full_size_sampled(W.config_c4(), 16)
+def test_c4_full_size_every_record():
+    """BASELINE configs[3]: 24 h diurnal traces with bursts, 4096 scenarios,
+    every record vs the oracle."""
+    st = _full_size_sampled(W.config_c4(), 1)
     assert int(st["ticks"].max()) > 10**6
 
 
 def test_c3_full_size_every_record():
     """BASELINE configs[2] at full size (321 controllers x 32 seeds = 10,272
     scenarios, one launch): every record vs the oracle."""
-    st = _full_size_sampled(W.config_c3(), W.config_c3().n_scenarios)
+    st = _full_size_sampled(W.config_c3(), 1)
     assert len(st) == 10272
 
 

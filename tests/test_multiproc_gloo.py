@@ -136,3 +136,57 @@ def test_peer_pointer_exchange_gloo():
         for g in range(world):
             if g != r:
                 assert ptrs[g] == 0x7000_0000 + g + 0x40  # base + the exporter's offset
+
+
+def _peer_fail_worker(rank, world, port, q, fail_export, fail_open):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_15330_b200 import parallel as PAR
+
+    opened, closed = [], []
+
+    def export(ptr):
+        if rank == fail_export:
+            raise RuntimeError("no IPC here")
+        return (f"rank{rank}".encode(), 0x40)
+
+    def open_(hb, off):
+        g = int(hb.decode()[4:])
+        if rank == fail_open and len(opened) == 1:  # the second mapping fails
+            raise RuntimeError("peer access refused")
+        opened.append(0x7000_0000 + g)
+        return 0x7000_0000 + g, 0x7000_0000 + g + off
+
+    try:
+        PAR.exchange_peer_pointers(0x1040, rank, world, export, open_, closed.append)
+        outcome = "ok"
+    except PAR.PeerExchangeError:
+        outcome = "raised"
+    dist.barrier()  # every rank reached the same point: no collective left unmatched
+    q.put((rank, outcome, opened, closed))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_export,fail_open", [(1, -1), (-1, 2), (0, 2)])
+def test_peer_pointer_exchange_failure_is_collective(fail_export, fail_open):
+    """a failed export or a failed mapping on ONE rank makes EVERY
+    rank raise PeerExchangeError after the same collectives (no hang, no
+    mismatched all_gather), and every mapping already opened is unmapped."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_fail_worker, args=(r, world, port, q, fail_export, fail_open))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in range(world):
+        r, outcome, opened, closed = q.get(timeout=120)
+        got[r] = (outcome, opened, closed)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, (outcome, opened, closed) in got.items():
+        assert outcome == "raised", (r, outcome)
+        assert sorted(closed) == sorted(opened), (r, opened, closed)

@@ -65,3 +65,19 @@ def test_headline_report_runs():
     assert h["checks"]["b_median_r_in_5_20pct"]
     assert h["checks"]["e_window_energy_bounded_lt_unbounded"]
     assert h["activation_s"] is not None
+
+
+def test_active_r_applies_from_the_next_second():
+    """the controller row of second s is ingested when s closes (R21),
+    so its r governs second s + 1: active_r is 0 through the first activation
+    second and equals that row's r from first_act_s + 1."""
+    w = W.config_paper_pair(1)
+    cols = w.columns()
+    o = oracle.run_scenario(cols, 1, rows_cap=3000, ctrl_log_cap=3000)
+    log = o["ctrl_log"]
+    agg = report.aggregate_per_second(o["rows"], _ctrl_arr(log), W.PROFILES["P24"])
+    fa = o["first_act_s"]
+    first = next(c for c in log if c["active"])
+    assert first["second"] == fa
+    assert all(a["active_r"] == 0 for a in agg[: fa + 1])
+    assert agg[fa + 1]["active_r"] == pytest.approx(first["r_bp"] / 1e4)

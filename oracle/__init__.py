@@ -50,6 +50,7 @@ class Inputs(C.Structure):
         ("ctrl_rmax", u32p), ("ctrl_rconst", u32p),
         ("ctrl_t1", u32p), ("ctrl_t2", u32p), ("ctrl_slo_us", u32p), ("ctrl_calibrated", u32p),
         ("ctrl_nrungs", u32p), ("ctrl_rungs", u32p), ("ctrl_bypass_mask", u32p), ("ctrl_min_words", u32p),
+        ("ctrl_horizon", u32p), ("ctrl_wlat", u32p), ("ctrl_wq", u32p), ("ctrl_wosc", u32p), ("ctrl_step", u32p),
         ("tab_L", i32p), ("tab_I", i32p), ("tab_fvar", i32p), ("tab_noise", i32p), ("tab_fcomp", i32p),
         ("poly_q16", i64p), ("tab_qnoise", i32p), ("quality", u32p), ("class_cum", u32p),
         ("sc_seed", u32p), ("sc_wid", u64p),
@@ -76,7 +77,8 @@ class Profile(C.Structure):
 class Ctrl(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp",
                                            "t1", "t2", "slo_us", "calibrated", "n_rungs")] + \
-               [("rungs_bp", C.c_uint32 * 8), ("bypass_mask", C.c_uint32), ("min_words_bypass", C.c_uint32)]
+               [("rungs_bp", C.c_uint32 * 8), ("bypass_mask", C.c_uint32), ("min_words_bypass", C.c_uint32)] + \
+               [(n, C.c_uint32) for n in ("horizon_s", "w_lat", "w_q", "w_osc", "step_bp")]
 
 
 class RunCfg(C.Structure):
@@ -166,6 +168,7 @@ def lib():
         L.orc_run_batch.argtypes = [P(Inputs), u64p, C.c_uint64, P(Result), C.c_int]
         L.orc_similarity.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int32, u32p]
         L.orc_similarity.restype = C.c_uint32
+        L.orc_ctrl_trace.argtypes = [P(Ctrl), u32p, u32p, u32p, C.c_uint64, P(Result), P(CtrlLog)]
         _lib = L
     return _lib
 
@@ -207,10 +210,12 @@ def calibrate(series):
 
 
 def make_ctrl(law=0, signal=0, window=5, r_min_bp=500, r_max_bp=2000, r_const_bp=0, t1=0, t2=0,
-              slo_us=0, calibrated=0, rungs=(), bypass_mask=0, min_words_bypass=0):
+              slo_us=0, calibrated=0, rungs=(), bypass_mask=0, min_words_bypass=0, horizon_s=0, w_lat=0, w_q=0,
+              w_osc=0, step_bp=0):
     c = Ctrl(law, signal, window, r_min_bp, r_max_bp, r_const_bp, t1, t2, slo_us, calibrated, len(rungs))
     c.bypass_mask = bypass_mask
     c.min_words_bypass = min_words_bypass
+    c.horizon_s, c.w_lat, c.w_q, c.w_osc, c.step_bp = horizon_s, w_lat, w_q, w_osc, step_bp
     for i, r in enumerate(rungs):
         c.rungs_bp[i] = r
     return c
@@ -218,6 +223,24 @@ def make_ctrl(law=0, signal=0, window=5, r_min_bp=500, r_max_bp=2000, r_const_bp
 
 def map_rate(A: int, k: int, ctrl: Ctrl) -> int:
     return lib().orc_map_rate(A, k, C.byref(ctrl))
+
+
+def ctrl_trace(ctrl: Ctrl, samples, words=None, seconds=None) -> dict:
+    """The controller alone (every law) over per-second samples: returns the
+    per-ingest log (r_bp, active, k, A) and the transition summary."""
+    n = len(samples)
+    x = np.ascontiguousarray(samples, dtype=np.uint32)
+    sec = np.ascontiguousarray(range(n) if seconds is None else seconds, dtype=np.uint32)
+    w = np.ascontiguousarray(np.zeros(n) if words is None else words, dtype=np.uint32)
+    r = Result()
+    log = (CtrlLog * max(n, 1))()
+    rc = lib().orc_ctrl_trace(C.byref(ctrl), sec.ctypes.data_as(u32p), x.ctypes.data_as(u32p),
+                              w.ctypes.data_as(u32p), n, C.byref(r), log)
+    if rc != 0:
+        raise RuntimeError("oracle ctrl_trace failed")
+    return dict(r=[e.r_bp for e in log[:n]], active=[e.active for e in log[:n]], k=[e.k for e in log[:n]],
+                A=[e.A for e in log[:n]], activations=r.activations, first_act_s=r.first_act_s,
+                last_deact_s=r.last_deact_s, active_ingests=r.active_ingests)
 
 
 class Bound:
@@ -235,6 +258,8 @@ class Bound:
              ("ctrl_t1", np.uint32), ("ctrl_t2", np.uint32), ("ctrl_slo_us", np.uint32),
              ("ctrl_calibrated", np.uint32), ("ctrl_nrungs", np.uint32), ("ctrl_rungs", np.uint32),
              ("ctrl_bypass_mask", np.uint32), ("ctrl_min_words", np.uint32),
+             ("ctrl_horizon", np.uint32), ("ctrl_wlat", np.uint32), ("ctrl_wq", np.uint32), ("ctrl_wosc", np.uint32),
+             ("ctrl_step", np.uint32),
              ("tab_L", np.int32), ("tab_I", np.int32), ("tab_fvar", np.int32), ("tab_noise", np.int32),
              ("tab_fcomp", np.int32), ("poly_q16", np.int64), ("tab_qnoise", np.int32), ("quality", np.uint32),
              ("class_cum", np.uint32),

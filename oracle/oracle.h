@@ -33,6 +33,13 @@ extern "C" {
 #endif
 
 enum { ORC_LAW_OFF = 0, ORC_LAW_CONST = 1, ORC_LAW_MAP = 2, ORC_LAW_STEP = 3 };
+/* NEXT-3 laws after P:213 ("Toward novel LLM congestion control"), readings in
+ * DESIGN.md §3 (R41-R43): MPC — forecast the signal over a horizon and pick the
+ * r minimising latency + quality/energy + oscillation cost; BBR — operate at
+ * Kleinrock's point from the minimum TBT and the maximum delivered words/s;
+ * PCC — paired micro-experiments r_base +- delta scored by a utility of
+ * latency and quality. */
+enum { ORC_LAW_MPC = 4, ORC_LAW_BBR = 5, ORC_LAW_PCC = 6 };
 /* INPUT and UTIL (NEXT-3, "input tokens per unit time", "GPU utilization
  * metrics"): input words admitted in the second (the second's total); mean
  * decode-batch occupancy over the second's iteration ends in basis points,
@@ -63,6 +70,7 @@ typedef struct {
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
   const uint32_t *ctrl_rungs; /* [n_ctrl][8] */
   const uint32_t *ctrl_bypass_mask, *ctrl_min_words; /* NEXT-3 class / short-output bypass */
+  const uint32_t *ctrl_horizon, *ctrl_wlat, *ctrl_wq, *ctrl_wosc, *ctrl_step; /* NEXT-3 MPC / BBR / PCC */
   const int32_t *tab_L, *tab_I, *tab_fvar, *tab_noise, *tab_fcomp; /* [4096] each */
   const int64_t *poly_q16;                                          /* [3] */
   const int32_t *tab_qnoise;  /* [4096] similarity noise, centi-points (NEXT-2) */
@@ -106,6 +114,10 @@ typedef struct {
   uint32_t rungs_bp[8];
   uint32_t bypass_mask;      /* bit c: class c is never rewritten (S:267 class_policy) */
   uint32_t min_words_bypass; /* predicted length below this is never rewritten */
+  /* NEXT-3: MPC forecast horizon in seconds and cost weights (latency
+   * excess per µs, quality/energy per bp of r, oscillation per bp of |dr|);
+   * PCC utility weights w_lat, w_q; BBR / PCC step in bp */
+  uint32_t horizon_s, w_lat, w_q, w_osc, step_bp;
 } orc_ctrl;
 
 typedef struct {
@@ -212,6 +224,14 @@ uint32_t orc_similarity(uint32_t U, uint32_t R, int active, int32_t noise, const
 
 /* Controller law as a pure function (a6): r in bp for a window sum A over k samples. */
 uint32_t orc_map_rate(uint64_t A, uint32_t k, const orc_ctrl *c);
+
+/* The controller alone (a6, every law): ingest n per-second samples x[i] of
+ * seconds sec[i] (w[i] = decode words emitted in that second, BBR's delivery
+ * rate), starting from the initial state; log[i] receives the state after
+ * ingest i, and res the transition log (activations, first_act_s,
+ * last_deact_s, active_ingests).  Returns 0, or -1 on allocation failure. */
+int orc_ctrl_trace(const orc_ctrl *c, const uint32_t *sec, const uint32_t *x, const uint32_t *w, uint64_t n,
+                   orc_result *res, orc_ctrl_log *log);
 
 /* Run many scenarios on nthreads host threads (cpu baseline). Returns 0 on success. */
 int orc_run_batch(const orc_inputs *in, const uint64_t *sids, uint64_t n, orc_result *res, int nthreads);

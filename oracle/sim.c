@@ -226,10 +226,16 @@ typedef struct {
 typedef struct {
   const orc_ctrl *c;
   uint32_t law;
-  uint32_t *samples;
+  uint32_t *samples;   /* every ingested sample, in order */
   uint64_t n, cap;
+  uint32_t *words;     /* BBR: decode words emitted in each ingested second */
+  uint64_t nw, capw;
   int active;
   uint32_t r, rung;
+  uint32_t rt_min;     /* BBR: minimum sample so far */
+  uint32_t phase;      /* PCC: 0 idle, 1 experiment r_base + delta running, 2 r_base - delta running */
+  uint32_t r_base;     /* PCC */
+  uint64_t cost_a;     /* PCC: cost of experiment 1 */
 } cstate;
 
 static int push_u32(uint32_t **v, uint64_t *n, uint64_t *cap, uint32_t x) {
@@ -244,24 +250,144 @@ static int push_u32(uint32_t **v, uint64_t *n, uint64_t *cap, uint32_t x) {
   return 0;
 }
 
-/* one controller ingest of the sample x of closed second `second` (a6) */
-static int ingest(cstate *cs, uint32_t second, uint32_t x, orc_result *res, orc_log *log) {
-  if (cs->law != ORC_LAW_MAP && cs->law != ORC_LAW_STEP) return 0;
+/* MPC ("predict the system load and preemptively adjust r ... cost
+ * functions that include latency, output quality, and energy efficiency over
+ * a moving time horizon and help avoid oscillations in r"; reading R41).
+ * Window y_1..y_k (oldest..newest), A = sum.  Forecast h seconds ahead from
+ * the window mean and its end-to-end slope:
+ *   F = A/k + h (y_k - y_1)/(k - 1)   (k >= 2; F = y_1 for k = 1), floored at 0.
+ * Predicted signal under r: x(r) = F (1 - r/10^4) (a shorter output shrinks
+ * the decode work in proportion).  Cost of a candidate r:
+ *   J(r) = w_lat max(0, x(r) - t1) + w_q r + w_osc |r - r_prev|
+ * over the candidates {0} U rungs, or {0} U {r_min + floor(i (r_max - r_min) / 30),
+ * i = 0..30}; the smallest r among the minima.  Exact: every term is multiplied
+ * by 10^4 D, D = k (k - 1) (1 for k = 1), in 128-bit integers. */
+static uint32_t mpc_rate(const orc_ctrl *c, const uint32_t *y, uint32_t k, uint32_t r_prev) {
+  __int128 A = 0;
+  for (uint32_t i = 0; i < k; ++i) A += y[i];
+  __int128 D, F;
+  if (k >= 2) {
+    D = (__int128)k * (k - 1);
+    F = A * (k - 1) + (__int128)c->horizon_s * k * ((__int128)y[k - 1] - (__int128)y[0]);
+  } else {
+    D = 1;
+    F = A;
+  }
+  if (F < 0) F = 0;
+  uint32_t cand[32];
+  uint32_t nc = 0;
+  cand[nc++] = 0;
+  if (c->n_rungs) {
+    for (uint32_t i = 0; i < c->n_rungs; ++i) cand[nc++] = c->rungs_bp[i];
+  } else {
+    for (uint32_t i = 0; i <= 30; ++i) cand[nc++] = c->r_min_bp + (uint32_t)((uint64_t)i * (c->r_max_bp - c->r_min_bp) / 30);
+  }
+  uint32_t best_r = 0;
+  __int128 best = -1;
+  for (uint32_t i = 0; i < nc; ++i) {
+    __int128 r = cand[i];
+    __int128 ex = F * (10000 - r) - (__int128)c->t1 * 10000 * D;
+    if (ex < 0) ex = 0;
+    __int128 dr = r > (__int128)r_prev ? r - r_prev : (__int128)r_prev - r;
+    __int128 J = (__int128)c->w_lat * ex + (__int128)10000 * D * ((__int128)c->w_q * r + (__int128)c->w_osc * dr);
+    if (best < 0 || J < best) { best = J; best_r = cand[i]; }
+  }
+  return best_r;
+}
+
+/* one controller ingest of the sample x of closed second `second` (a6);
+ * w = decode words emitted in that second (BBR's delivery rate) */
+static int ingest(cstate *cs, uint32_t second, uint32_t x, uint32_t w, orc_result *res, orc_log *log) {
+  const uint32_t law = cs->law;
+  if (law != ORC_LAW_MAP && law != ORC_LAW_STEP && law != ORC_LAW_MPC && law != ORC_LAW_BBR && law != ORC_LAW_PCC)
+    return 0;
   if (push_u32(&cs->samples, &cs->n, &cs->cap, x)) return -1;
+  if (push_u32(&cs->words, &cs->nw, &cs->capw, w)) return -1;
   const orc_ctrl *c = cs->c;
   /* moving average over the last `window` samples; partial window at start */
   uint32_t k = cs->n < c->window ? (uint32_t)cs->n : c->window;
   uint64_t A = 0;
   for (uint64_t i = cs->n - k; i < cs->n; ++i) A += cs->samples[i];
-  int act = A >= (uint64_t)k * c->t1; /* MA >= T1 triggers (R38); below resets */
+  const uint32_t r_prev = cs->r;
+  int act = 0;
   uint32_t r = 0;
-  if (act) {
-    if (cs->law == ORC_LAW_MAP) {
-      r = orc_map_rate(A, k, c);
-    } else { /* STEP (R4, R5): rung 0 on activation, one rung up per ingest while active */
-      if (!cs->active) cs->rung = 0;
-      else if (cs->rung + 1 < c->n_rungs) cs->rung++;
-      r = c->rungs_bp[cs->rung];
+  if (law == ORC_LAW_MAP || law == ORC_LAW_STEP) {
+    act = A >= (uint64_t)k * c->t1; /* MA >= T1 triggers (R38); below resets */
+    if (act) {
+      if (law == ORC_LAW_MAP) {
+        r = orc_map_rate(A, k, c);
+      } else { /* STEP (R4, R5): rung 0 on activation, one rung up per ingest while active */
+        if (!cs->active) cs->rung = 0;
+        else if (cs->rung + 1 < c->n_rungs) cs->rung++;
+        r = c->rungs_bp[cs->rung];
+      }
+    }
+  } else if (law == ORC_LAW_MPC) {
+    r = mpc_rate(c, cs->samples + (cs->n - k), k, r_prev);
+    act = r > 0;
+  } else if (law == ORC_LAW_BBR) {
+    /* BBR-style ("operate at the equivalent of Kleinrock's point, keeping
+     * TBT low while maximizing the token generation (tokens/s)"; reading R42):
+     * RTprop = the minimum TBT sample so far, BtlBw = the maximum decode words/s
+     * over the window.  Congested (queueing delay beyond the allowance t1):
+     * MA >= RTprop + t1.  At the bandwidth plateau (8 w >= 7 BtlBw) a congested
+     * controller sheds one step of output; a controller below the delay target
+     * gives one step back (probing for more tokens/s); else it holds. */
+    if (x < cs->rt_min) cs->rt_min = x;
+    uint32_t bw = 0;
+    for (uint64_t i = cs->nw - k; i < cs->nw; ++i)
+      if (cs->words[i] > bw) bw = cs->words[i];
+    const int congested = A >= (uint64_t)k * ((uint64_t)cs->rt_min + c->t1);
+    const int plateau = 8ull * w >= 7ull * bw;
+    r = r_prev;
+    if (congested && plateau) {
+      if (c->n_rungs) {
+        if (r_prev == 0) cs->rung = 0;
+        else if (cs->rung + 1 < c->n_rungs) cs->rung++;
+        r = c->rungs_bp[cs->rung];
+      } else {
+        r = r_prev == 0 ? c->r_min_bp : (r_prev + c->step_bp > c->r_max_bp ? c->r_max_bp : r_prev + c->step_bp);
+      }
+    } else if (!congested) {
+      if (c->n_rungs) {
+        if (r_prev == 0 || cs->rung == 0) r = 0;
+        else r = c->rungs_bp[--cs->rung];
+      } else {
+        r = r_prev <= c->r_min_bp ? 0 : (r_prev < c->r_min_bp + c->step_bp ? c->r_min_bp : r_prev - c->step_bp);
+      }
+    }
+    act = r > 0;
+  } else { /* ORC_LAW_PCC */
+    /* PCC-style ("run micro-experiments with different values of r and
+     * measure a utility function that combines both latency and response
+     * quality"; reading R43).  Active while MA >= t1.  Each monitor interval is
+     * one ingested second: experiment 1 runs r_base + delta, experiment 2
+     * r_base - delta (clamped to [r_min, r_max]); the ingest after each
+     * measures its cost w_lat max(0, x - t1) + w_q r (utility = -cost); after
+     * the pair, r_base moves one delta toward the cheaper side (ties stay). */
+    act = A >= (uint64_t)k * c->t1;
+    const uint32_t d = c->step_bp;
+    if (!act) {
+      cs->phase = 0;
+      cs->r_base = 0;
+      r = 0;
+    } else {
+      const uint64_t cost = (uint64_t)c->w_lat * (x > c->t1 ? x - c->t1 : 0) + (uint64_t)c->w_q * r_prev;
+      if (cs->phase == 0) {
+        cs->r_base = c->r_min_bp;
+      } else if (cs->phase == 1) {
+        cs->cost_a = cost;
+      } else {
+        if (cs->cost_a < cost) cs->r_base = cs->r_base + d > c->r_max_bp ? c->r_max_bp : cs->r_base + d;
+        else if (cost < cs->cost_a) cs->r_base = cs->r_base < c->r_min_bp + d ? c->r_min_bp : cs->r_base - d;
+      }
+      if (cs->phase == 1) { /* start experiment 2 */
+        r = cs->r_base < c->r_min_bp + d ? c->r_min_bp : cs->r_base - d;
+        cs->phase = 2;
+      } else { /* start experiment 1 */
+        r = cs->r_base + d > c->r_max_bp ? c->r_max_bp : cs->r_base + d;
+        cs->phase = 1;
+      }
     }
   }
   if (act && !cs->active) {
@@ -280,6 +406,26 @@ static int ingest(cstate *cs, uint32_t second, uint32_t x, orc_result *res, orc_
     log->n_ctrl++;
   }
   return 0;
+}
+
+int orc_ctrl_trace(const orc_ctrl *c, const uint32_t *sec, const uint32_t *x, const uint32_t *w, uint64_t n,
+                   orc_result *res, orc_ctrl_log *out) {
+  memset(res, 0, sizeof(*res));
+  res->first_act_s = res->last_deact_s = ORC_NONE;
+  cstate cs;
+  memset(&cs, 0, sizeof(cs));
+  cs.c = c;
+  cs.law = c->law;
+  cs.rt_min = ORC_NONE;
+  orc_log log;
+  memset(&log, 0, sizeof(log));
+  log.ctrl = out;
+  log.cap_ctrl = out ? n : 0;
+  int rc = 0;
+  for (uint64_t i = 0; i < n && rc == 0; ++i) rc = ingest(&cs, sec[i], x[i], w ? w[i] : 0, res, &log);
+  free(cs.samples);
+  free(cs.words);
+  return rc;
 }
 
 static uint64_t overlap(uint64_t a, uint64_t b, int64_t w0, int64_t w1) {
@@ -323,7 +469,11 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   uint64_t *sec_util_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
   orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
   heap h = {0, 0, 0};
-  cstate cs = {ctrl, ctrl->law, NULL, 0, 0, 0, 0, 0};
+  cstate cs;
+  memset(&cs, 0, sizeof(cs));
+  cs.c = ctrl;
+  cs.law = ctrl->law;
+  cs.rt_min = ORC_NONE;
   if (!rs || !queue || !ready || !batch || !pending || !stack || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
       !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt || !sec_in_sum ||
       !sec_in_any || !sec_util_sum || !sec_util_cnt ||
@@ -367,7 +517,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         if (log && log->series && n_series < log->cap_series) log->series[n_series] = x; \
         n_series++;                                                                      \
       }                                                                                  \
-      if (ingest(&cs, (uint32_t)next_sec, x, res, log)) goto out;                        \
+      if (ingest(&cs, (uint32_t)next_sec, x, (uint32_t)sec_tbt_cnt[next_sec], res, log)) goto out; \
     }                                                                                    \
   } while (0)
 
@@ -811,7 +961,7 @@ out:
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
   free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
   free(sec_util_cnt);
-  free(h.v); free(cs.samples); free(rows);
+  free(h.v); free(cs.samples); free(cs.words); free(rows);
   return rc;
 }
 
@@ -845,6 +995,11 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   for (int k = 0; k < 8; ++k) c->rungs_bp[k] = in->ctrl_rungs[8 * ci + k];
   c->bypass_mask = in->ctrl_bypass_mask[ci];
   c->min_words_bypass = in->ctrl_min_words[ci];
+  c->horizon_s = in->ctrl_horizon[ci];
+  c->w_lat = in->ctrl_wlat[ci];
+  c->w_q = in->ctrl_wq[ci];
+  c->w_osc = in->ctrl_wosc[ci];
+  c->step_bp = in->ctrl_step[ci];
   cfg->mode = in->sc_mode[sid];
   cfg->horizon_us = in->sc_horizon[sid];
   cfg->w0_us = in->sc_w0[sid];

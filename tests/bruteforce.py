@@ -12,16 +12,119 @@ context (input + words emitted) to fit kv_cap_words; at an iteration end whose
 contexts exceed it, the latest admitted requests (while more than one is in the
 system) go back to the front of the queue and later prefill input + emitted
 again, that prefill's end emitting their next word.  No event heap, no
-incremental sums.  Usable only on tiny traces (<= ~2e6 µs).  Controller: the
-linear MAP law recomputed from a Fraction moving average.
+incremental sums (instants at which nothing is scheduled are skipped: every
+rule fires only at an iteration end, a prefill end or an arrival).  Usable only on tiny traces (<= ~2e6 µs).  Controller:
+every law recomputed here in exact rationals from its own per-second samples
+(TBT gaps, or E2E / SLO of the completions, R3): MAP, STEP
+(R5), MPC (R41), BBR (R42, delivery = decode words of the second), PCC (R43).
 """
 from __future__ import annotations
 
 from fractions import Fraction
 
 
+class _Law:
+    """The controller laws written out from their definitions,
+    with Fraction arithmetic: one call per ingested second."""
+
+    def __init__(self, law, t1, t2, r_min, r_max, window, rungs, horizon_s, w_lat, w_q, w_osc, step_bp):
+        self.law, self.t1, self.t2, self.r_min, self.r_max, self.window = law, t1, t2, r_min, r_max, window
+        self.rungs = list(rungs)
+        if self.rungs:
+            self.r_min, self.r_max = self.rungs[0], self.rungs[-1]
+        self.h, self.w_lat, self.w_q, self.w_osc, self.step = horizon_s, w_lat, w_q, w_osc, step_bp
+        self.samples, self.words = [], []
+        self.r = 0
+        self.active = False
+        self.rung = 0
+        self.rt_min = None
+        self.phase, self.r_base, self.cost_a = 0, 0, None
+
+    def ingest(self, x, w):
+        self.samples.append(x)
+        self.words.append(w)
+        ys = self.samples[-self.window:]
+        k = len(ys)
+        ma = Fraction(sum(ys), k)
+        prev_r, prev_active = self.r, self.active
+        if self.law == "map":
+            self.active = ma >= self.t1
+            if self.active:
+                r = min(self.r_max, int(Fraction(self.r_min) + Fraction(self.r_max - self.r_min) * (ma - self.t1)
+                                        / (self.t2 - self.t1)))
+                if self.rungs:
+                    r = max([g for g in self.rungs if g <= r] or [self.rungs[0]])
+                self.r = r
+            else:
+                self.r = 0
+        elif self.law == "step":
+            self.active = ma >= self.t1
+            if self.active:
+                self.rung = 0 if not prev_active else min(self.rung + 1, len(self.rungs) - 1)
+                self.r = self.rungs[self.rung]
+            else:
+                self.r = 0
+        elif self.law == "mpc":
+            F = ma + (Fraction(self.h * (ys[-1] - ys[0]), k - 1) if k >= 2 else 0)
+            F = max(F, Fraction(0))
+            cands = [0] + (self.rungs if self.rungs else
+                           [self.r_min + i * (self.r_max - self.r_min) // 30 for i in range(31)])
+            best = None
+            for c in cands:
+                J = self.w_lat * max(Fraction(0), F * (1 - Fraction(c, 10000)) - self.t1) + self.w_q * c + \
+                    self.w_osc * abs(c - prev_r)
+                if best is None or J < best[0]:
+                    best = (J, c)
+            self.r = best[1]
+            self.active = self.r > 0
+        elif self.law == "bbr":
+            self.rt_min = x if self.rt_min is None else min(self.rt_min, x)
+            bw = max(self.words[-self.window:])
+            congested = ma >= self.rt_min + self.t1
+            plateau = Fraction(w) >= Fraction(7, 8) * bw
+            if congested and plateau:
+                if self.rungs:
+                    self.rung = 0 if prev_r == 0 else min(self.rung + 1, len(self.rungs) - 1)
+                    self.r = self.rungs[self.rung]
+                else:
+                    self.r = self.r_min if prev_r == 0 else min(self.r_max, prev_r + self.step)
+            elif not congested:
+                if self.rungs:
+                    if prev_r == 0 or self.rung == 0:
+                        self.r = 0
+                    else:
+                        self.rung -= 1
+                        self.r = self.rungs[self.rung]
+                else:
+                    self.r = 0 if prev_r <= self.r_min else max(self.r_min, prev_r - self.step)
+            self.active = self.r > 0
+        elif self.law == "pcc":
+            self.active = ma >= self.t1
+            if not self.active:
+                self.phase, self.r_base, self.r = 0, 0, 0
+            else:
+                cost = self.w_lat * max(0, x - self.t1) + self.w_q * prev_r
+                if self.phase == 0:
+                    self.r_base = self.r_min
+                elif self.phase == 1:
+                    self.cost_a = cost
+                else:
+                    if self.cost_a < cost:
+                        self.r_base = min(self.r_max, self.r_base + self.step)
+                    elif cost < self.cost_a:
+                        self.r_base = max(self.r_min, self.r_base - self.step)
+                if self.phase == 1:
+                    self.r = max(self.r_min, self.r_base - self.step)
+                    self.phase = 2
+                else:
+                    self.r = min(self.r_max, self.r_base + self.step)
+                    self.phase = 1
+        return self.r
+
+
 def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max=2000, window=5,
-             r_const=0, mode_drain=True):
+             r_const=0, mode_drain=True, rungs=(), horizon_s=0, w_lat=0, w_q=0, w_osc=0, step_bp=0,
+             signal="tbt", slo_us=0):
     n = len(requests)
     st = ["future"] * n
     admit = [None] * n
@@ -48,7 +151,18 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
     words_out = 0
     gaps = [[] for _ in range(n)]
     sec_sum, sec_cnt = {}, {}
-    samples = []
+    e2e_sum, e2e_cnt, slo_cnt = {}, {}, {}
+    ctl = _Law(law, t1, t2, r_min, r_max, window, rungs, horizon_s, w_lat, w_q, w_osc, step_bp)
+
+    def complete(m, t):
+        st[m] = "done"
+        done[m] = t
+        e = t - requests[m]["a_us"]
+        s_ = t // 10**6
+        e2e_sum[s_] = e2e_sum.get(s_, 0) + e
+        e2e_cnt[s_] = e2e_cnt.get(s_, 0) + 1
+        slo_cnt[s_] = slo_cnt.get(s_, 0) + (1 if e > slo_us else 0)
+
     ingested_upto = 0  # next second to ingest
     r_cur = r_const if law == "const" else 0
     last_event = 0
@@ -66,8 +180,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                 emitted[m] += 1
                 words_out += 1
                 if emitted[m] == R[m]:
-                    st[m] = "done"
-                    done[m] = t
+                    complete(m, t)
                 else:
                     st[m] = "ready"
                     ready.append(m)
@@ -97,8 +210,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                 emitted[m] += 1
                 words_out += 1
                 if emitted[m] == R[m]:
-                    st[m] = "done"
-                    done[m] = t
+                    complete(m, t)
                 else:
                     st[m] = "ready"
                     ready.append(m)
@@ -110,8 +222,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                 emitted[m] = 1
                 words_out += 1
                 if R[m] == 1:
-                    st[m] = "done"
-                    done[m] = t
+                    complete(m, t)
                 else:
                     st[m] = "ready"
                     ready.append(m)
@@ -127,18 +238,16 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
             while (ingested_upto + 1) * 10**6 <= t:
                 s = ingested_upto
                 ingested_upto += 1
-                if sec_cnt.get(s, 0) == 0:
+                if signal == "tbt":
+                    num, den = sec_sum.get(s, 0), sec_cnt.get(s, 0)
+                elif signal == "e2e":
+                    num, den = e2e_sum.get(s, 0), e2e_cnt.get(s, 0)
+                else:  # slo: per-mille of completions with E2E > slo_us
+                    num, den = 1000 * slo_cnt.get(s, 0), e2e_cnt.get(s, 0)
+                if den == 0:
                     continue
-                x = sec_sum[s] // sec_cnt[s]
-                if law == "map":
-                    samples.append(x)
-                    k = min(len(samples), window)
-                    ma = Fraction(sum(samples[-k:]), k)
-                    if ma < t1:
-                        r_cur = 0
-                    else:
-                        r = Fraction(r_min) + Fraction(r_max - r_min) * (ma - t1) / (t2 - t1)
-                        r_cur = min(r_max, int(r))  # floor to a basis point
+                if law in ("map", "step", "mpc", "bbr", "pcc"):
+                    r_cur = ctl.ingest(num // den, sec_cnt.get(s, 0))
             in_sys = sum(1 for i in range(n) if st[i] in ("prefill", "ready", "decoding", "pending"))
             cap = prof.get("kv_cap_words", 0)
             while in_sys < prof["max_batch"] and queue:
@@ -208,6 +317,13 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
         t += 1
         if mode_drain and all(s in ("done",) for s in st):
             break
+        # no rule fires at an instant without a scheduled iteration end, prefill
+        # end or arrival: jump over such instants (state is constant there)
+        nxt = [iter_end] if iter_end is not None else []
+        nxt += [pend[m] for m in range(n) if st[m] == "prefill"]
+        nxt += [requests[m]["a_us"] for m in range(n) if st[m] == "future"]
+        nxt = [x for x in nxt if x >= t]
+        t = min(nxt) if nxt else horizon_us
     end = last_event if mode_drain and all(s == "done" for s in st) else horizon_us
     if mode_drain and all(s == "done" for s in st):
         # idle was counted through t = end inclusive of the final µs loop; recount up to end

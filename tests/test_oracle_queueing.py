@@ -137,3 +137,28 @@ def test_fewer_words_when_bounded(orc):
     assert un["served"] == bd["served"] == len(reqs)
     assert bd["words_out"] <= un["words_out"]
     assert bd["words_out"] == sum(max(1, (q["U"] * 9000 + 5000) // 10000) for q in reqs)
+
+
+@pytest.mark.parametrize("profile", ["P24", "L8B"])
+def test_a3_saturation_brackets(profile):
+    """A3 (readings R1 / R27): the recalibrated profiles saturate near
+    the paper's onset (~2.4 RPS).  Fluid queue slope between 300 s and
+    600 s of a constant-rate Poisson stream, averaged over 32 seeds (same seed =
+    same arrivals at both horizons, R32): |slope| < 0.01 req/s at 2.2 RPS and
+    > 0.05 req/s at 2.6 RPS.  This is the sweep DESIGN.md §3 R1 cites."""
+    import oracle
+
+    seeds = 32
+    slopes = {}
+    for rate in (2.2, 2.6):
+        sc = []
+        for s in range(seeds):
+            for H in (300, 600):
+                sc.append(W.Scenario(s, wid=0, trace=0, profile=0, ctrl=0, segment=0, mode=W.MODE_CUTOFF,
+                                     horizon_us=H * W.US))
+        w = W.custom([W.const_trace(rate, 600)], [W.PROFILES[profile]], [W.OFF], sc)
+        rs = oracle.run_batch(oracle.Bound(w.columns()))
+        q = np.array([r["queued_end"] for r in rs], dtype=np.float64).reshape(seeds, 2)
+        slopes[rate] = float(np.mean(q[:, 1] - q[:, 0]) / 300.0)
+    assert abs(slopes[2.2]) < 0.01, slopes
+    assert slopes[2.6] > 0.05, slopes

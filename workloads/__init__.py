@@ -30,6 +30,7 @@ from scipy.special import ndtri
 # enums shared *by value* with both implementations (documented in DESIGN.md)
 # ----------------------------------------------------------------------------
 LAW_OFF, LAW_CONST, LAW_MAP, LAW_STEP = 0, 1, 2, 3
+LAW_MPC, LAW_BBR, LAW_PCC = 4, 5, 6  # NEXT-3, readings R41-R43
 SIG_TBT, SIG_E2E, SIG_SLO, SIG_TTFT, SIG_INPUT, SIG_UTIL = 0, 1, 2, 3, 4, 5
 MODE_CUTOFF, MODE_DRAIN = 0, 1
 
@@ -189,6 +190,11 @@ class Ctrl:
     rungs_bp: tuple = ()      # word-limit ladder (reading R5), <= 8 ascending rungs
     bypass_mask: int = 0      # NEXT-3: bit c -> class c never rewritten ("coding tasks might use r=0")
     min_words_bypass: int = 0  # NEXT-3: predicted length below this is never rewritten
+    horizon_s: int = 0        # NEXT-3 MPC: forecast horizon in seconds ("moving time horizon")
+    w_lat: int = 0            # NEXT-3 MPC / PCC: cost per µs of signal above t1
+    w_q: int = 0              # NEXT-3 MPC / PCC: cost per bp of r (quality and energy)
+    w_osc: int = 0            # NEXT-3 MPC: cost per bp of |r change| ("avoid oscillations in r")
+    step_bp: int = 0          # NEXT-3 BBR / PCC: r step (BBR without rungs) / experiment delta (PCC)
 
 
 OFF = Ctrl()
@@ -202,6 +208,33 @@ def map_ctrl(t1_us, t2_us, r_min_bp=500, r_max_bp=2000, rungs=(), window=5, sign
 
 def step_ctrl(t1_us, t2_us, rungs, window=5, signal=SIG_TBT):
     return Ctrl(LAW_STEP, signal, window, rungs[0], rungs[-1], 0, int(t1_us), int(t2_us), 0, 0, tuple(rungs))
+
+
+def mpc_ctrl(t1_us, horizon_s=3, w_lat=4, w_q=1, w_osc=2, r_min_bp=500, r_max_bp=2000, rungs=(), window=5,
+             signal=SIG_TBT, slo_us=0):
+    """NEXT-3 MPC (reading R41): forecast the signal horizon_s ahead and
+    pick the r minimising w_lat (signal above t1) + w_q r + w_osc |dr|."""
+    if rungs:
+        r_min_bp, r_max_bp = rungs[0], rungs[-1]
+    return Ctrl(LAW_MPC, signal, window, r_min_bp, r_max_bp, 0, int(t1_us), 0, slo_us, 0, tuple(rungs),
+                horizon_s=horizon_s, w_lat=w_lat, w_q=w_q, w_osc=w_osc)
+
+
+def bbr_ctrl(allow_us, step_bp=250, r_min_bp=500, r_max_bp=2000, rungs=(), window=5):
+    """NEXT-3 BBR-style (reading R42): TBT signal; congested when the
+    moving average exceeds the minimum TBT by allow_us; sheds / returns one step."""
+    if rungs:
+        r_min_bp, r_max_bp = rungs[0], rungs[-1]
+    return Ctrl(LAW_BBR, SIG_TBT, window, r_min_bp, r_max_bp, 0, int(allow_us), 0, 0, 0, tuple(rungs),
+                step_bp=0 if rungs else step_bp)
+
+
+def pcc_ctrl(t1_us, delta_bp=250, w_lat=1, w_q=4, r_min_bp=500, r_max_bp=2000, window=5, signal=SIG_TBT,
+             slo_us=0):
+    """NEXT-3 PCC-style (reading R43): paired experiments r_base +- delta
+    scored by the cost w_lat (signal above t1) + w_q r while MA >= t1."""
+    return Ctrl(LAW_PCC, signal, window, r_min_bp, r_max_bp, 0, int(t1_us), 0, slo_us, 0, (),
+                w_lat=w_lat, w_q=w_q, step_bp=delta_bp)
 
 
 # ----------------------------------------------------------------------------
@@ -310,6 +343,8 @@ class Workload:
             ctrl_slo_us=u32([c.slo_us for c in C]), ctrl_calibrated=u32([c.calibrated for c in C]),
             ctrl_nrungs=u32([len(c.rungs_bp) for c in C]), ctrl_rungs=rungs[:len(C)],
             ctrl_bypass_mask=u32([c.bypass_mask for c in C]), ctrl_min_words=u32([c.min_words_bypass for c in C]),
+            ctrl_horizon=u32([c.horizon_s for c in C]), ctrl_wlat=u32([c.w_lat for c in C]),
+            ctrl_wq=u32([c.w_q for c in C]), ctrl_wosc=u32([c.w_osc for c in C]), ctrl_step=u32([c.step_bp for c in C]),
             tab_L=self.tables["L"], tab_I=self.tables["I"], tab_fvar=self.tables["fvar"],
             tab_noise=self.tables["noise"], tab_fcomp=self.tables["fcomp"],
             poly_q16=i64(self.poly_q16),

@@ -51,6 +51,22 @@ typedef enum {
 } bellman_status;
 
 enum { BELLMAN_LAW_OFF = 0, BELLMAN_LAW_CONST = 1, BELLMAN_LAW_MAP = 2, BELLMAN_LAW_STEP = 3 };
+/* NEXT-3 laws after P:213 ("Toward novel LLM congestion control"; readings
+ * R41-R43), each at one ingest per closed second:
+ *  MPC — forecast the signal horizon_s seconds ahead from the window (mean +
+ *        end-to-end slope) and choose, among {0} U rungs (or a 31-point grid of
+ *        [r_min, r_max]), the r minimising
+ *        w_lat max(0, F (1 - r) - t1) + w_q r + w_osc |r - r_prev|;
+ *  BBR — TBT signal only: RTprop = minimum sample so far, BtlBw = maximum
+ *        decode words per second over the window; congested iff the moving
+ *        average >= RTprop + t1; at the bandwidth plateau (8 w >= 7 BtlBw) a
+ *        congested controller raises r one step (step_bp or one rung), an
+ *        uncongested one lowers it one step (to 0 below r_min), else it holds;
+ *  PCC — while the moving average >= t1: paired one-second experiments
+ *        r_base + step_bp then r_base - step_bp (clamped to [r_min, r_max]),
+ *        each scored by the cost w_lat max(0, x - t1) + w_q r of the second it
+ *        governed; after a pair r_base moves one step toward the cheaper. */
+enum { BELLMAN_LAW_MPC = 4, BELLMAN_LAW_BBR = 5, BELLMAN_LAW_PCC = 6 };
 /* Per-second congestion signals (a6).  TBT is the paper's; E2E / SLO
  * are SPEC's alternatives; TTFT, INPUT and UTIL are the further
  * signals P:211 names (NEXT-3): TTFT = mean TTFT of the second's first words;
@@ -164,7 +180,10 @@ typedef struct {
   uint32_t rungs_bp[8];
   uint32_t bypass_mask;      /* NEXT-3 (S:267 class_policy): bit c -> class c never rewritten */
   uint32_t min_words_bypass; /* NEXT-3: predicted length below this never rewritten */
-} bellman_ctrl; /* 84 bytes */
+  uint32_t horizon_s;        /* NEXT-3 MPC: forecast horizon in seconds, <= 16 */
+  uint32_t w_lat, w_q, w_osc;/* NEXT-3 MPC / PCC cost weights, <= 65535 (MPC and PCC need w_lat >= 1) */
+  uint32_t step_bp;          /* NEXT-3 BBR (without rungs) step / PCC experiment delta, >= 1 */
+} bellman_ctrl; /* 104 bytes */
 
 /* Workload model inputs (R14, R15, R33): 4096-entry quantile
  * tables drawn with index (u32 >> 20), plus the compliance polynomial. */

@@ -30,7 +30,8 @@ PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv
                     ("kv_policy", "<u4"), ("_pad", "<u4"), ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
 CTRL = np.dtype([(n, "<u4") for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp", "t1", "t2",
                                        "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))] +
-                [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")])
+                [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")] +
+                [(n, "<u4") for n in ("horizon_s", "w_lat", "w_q", "w_osc", "step_bp")])
 SCENARIO = np.dtype([("seed_index", "<u4"), ("trace", "<u4"), ("wid", "<u8"), ("profile", "<u4"), ("ctrl", "<u4"),
                      ("segment", "<u4"), ("mode", "<u4"), ("horizon_us", "<i8"), ("w0_us", "<i8"),
                      ("w1_us", "<i8"), ("calib_src", "<u4"), ("record", "<u4")])
@@ -54,7 +55,7 @@ RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
 assert ARRIVAL.itemsize == 24
 assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 64
-assert CTRL.itemsize == 84 and SCENARIO.itemsize == 64 and STATS.itemsize == 272
+assert CTRL.itemsize == 104 and SCENARIO.itemsize == 64 and STATS.itemsize == 272
 
 
 class Models(C.Structure):

@@ -153,7 +153,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
   }
   for (uint32_t i = 0; i < d->n_ctrls; ++i) {
     const bellman_ctrl &c = d->ctrls[i];
-    if (c.law > BELLMAN_LAW_STEP) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown law", i);
+    if (c.law > BELLMAN_LAW_PCC) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown law", i);
     if (c.signal > BELLMAN_SIG_UTIL) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: unknown signal", i);
     if (c.bypass_mask > 15u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: bypass_mask has bits beyond 4 classes", i);
     if (c.window < 1 || c.window > 8) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: window not in 1..8", i);
@@ -169,6 +169,31 @@ static bellman_status validate(const bellman_sim_desc *d) {
           if (c.rungs_bp[k] <= c.rungs_bp[k - 1]) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs not ascending", i);
         if (c.rungs_bp[0] != c.r_min_bp || c.rungs_bp[c.n_rungs - 1] != c.r_max_bp)
           return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs must span [r_min, r_max]", i);
+      }
+    }
+    if (c.law >= BELLMAN_LAW_MPC) {  // NEXT-3 MPC / BBR / PCC
+      if (c.r_min_bp < 1 || c.r_min_bp > c.r_max_bp || c.r_max_bp > 5000)
+        return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: need 0 < r_min <= r_max <= 5000 bp", i);
+      if (c.calibrated) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: calibration is for MAP / STEP only", i);
+      if (c.w_lat > 65535u || c.w_q > 65535u || c.w_osc > 65535u)
+        return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: cost weights must be <= 65535", i);
+      if (c.n_rungs) {
+        for (uint32_t k = 1; k < c.n_rungs; ++k)
+          if (c.rungs_bp[k] <= c.rungs_bp[k - 1]) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs not ascending", i);
+        if (c.rungs_bp[0] != c.r_min_bp || c.rungs_bp[c.n_rungs - 1] != c.r_max_bp)
+          return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: rungs must span [r_min, r_max]", i);
+      }
+      if (c.law == BELLMAN_LAW_MPC) {
+        if (c.horizon_s > 16u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: MPC horizon_s > 16", i);
+        if (c.w_lat < 1u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: MPC needs w_lat >= 1", i);
+      } else if (c.law == BELLMAN_LAW_BBR) {
+        if (c.signal != BELLMAN_SIG_TBT) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: BBR needs the TBT signal", i);
+        if (!c.n_rungs && (c.step_bp < 1u || c.step_bp > 5000u))
+          return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: BBR needs 1 <= step_bp <= 5000 or rungs", i);
+      } else {
+        if (c.n_rungs) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: PCC takes no rungs", i);
+        if (c.step_bp < 1u || c.step_bp > 5000u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: PCC needs 1 <= step_bp <= 5000", i);
+        if (c.w_lat < 1u) return fail(nullptr, BELLMAN_EINVAL, "ctrl %u: PCC needs w_lat >= 1", i);
       }
     }
   }

@@ -198,6 +198,11 @@ struct alignas(16) Cold {
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t pf_ns;                             // prefill ns per input word
+  // NEXT-3 MPC / BBR / PCC parameters and state (ingest_ext only)
+  uint32_t hz, wlat, wq, wosc, step;          // horizon s, cost weights, step / delta bp
+  uint32_t rt_min, phase, rbase;              // BBR RTprop; PCC phase and r_base
+  uint64_t cost_a;                            // PCC: cost of the pair's first experiment
+  uint32_t wring[8];                          // BBR: decode words of the window's seconds
   // KV-free cost law: floor((2^32 - 1) / cost(B)) for B = 0..max_batch, filled
   // lane-parallel at scenario start; the leap divides by cost(B) with it
   uint32_t cbm_tab[68];
@@ -487,6 +492,176 @@ __device__ __forceinline__ uint64_t div_u64(uint64_t a, uint64_t b) {
 }
 
 // ---------------------------------------------------------------------------
+// a6, NEXT-3 laws after P:213 (readings R41-R43, include/bellman_sim.h): MPC,
+// BBR-style and PCC-style, one ingest of sample x of the closed second ending
+// at sec_bound, w = the decode words emitted in that second (acc_cnt of the
+// TBT signal; BBR is TBT-only).  Out of line (one copy, called at most once
+// per simulated second), so the MAP / STEP event loops keep their footprint.
+// The window ring and its sum are shared with MAP / STEP.  MPC evaluates its
+// <= 32 candidate rates one per lane (128-bit exact costs) and takes the
+// warp's lexicographic (cost, index) minimum with five xor-shuffle steps; BBR
+// and PCC are warp-uniform scalar updates.  Lane 0 writes the state.
+__device__ __forceinline__ unsigned __int128 shfl_xor_u128(unsigned __int128 v, int m) {
+  const uint64_t lo = __shfl_xor_sync(FULL, (unsigned long long)(uint64_t)v, m);
+  const uint64_t hi = __shfl_xor_sync(FULL, (unsigned long long)(uint64_t)(v >> 64), m);
+  return ((unsigned __int128)hi << 64) | lo;
+}
+
+template <bool DBG>
+__device__ __noinline__ uint32_t ingest_ext(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint32_t x, uint32_t w,
+                                            uint32_t r_cur, bool dbg) {
+  Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
+  const uint32_t law = c.law, window = c.window, pos = c.ring_pos, t1 = c.t1, rmin = c.rmin, rmax = c.rmax;
+  const uint32_t was_active = c.active, nrungs = c.nrungs;
+  uint32_t k = c.ring_n, rung = c.rung;
+  uint64_t A = c.ringA;
+  if (k < window) {
+    k++;
+    A += x;
+  } else {
+    A = A + x - c.ring[pos];
+  }
+  const uint32_t npos = pos + 1u == window ? 0u : pos + 1u;
+  // the window's oldest sample once x is in: ring[0] while filling, else the slot after x
+  const uint32_t y1 = k == 1u ? x : (k < window ? c.ring[0] : c.ring[npos]);
+  uint32_t nr = 0, act = 0;
+  uint32_t rt_min = c.rt_min, phase = c.phase, rbase = c.rbase;
+  uint64_t cost_a = c.cost_a;
+  if (law == BELLMAN_LAW_MPC) {
+    // forecast F = A/k + h (x - y1)/(k - 1) as F_num / D; costs scaled by 10^4 D
+    int64_t Fn;
+    uint64_t D;
+    if (k >= 2u) {
+      D = (uint64_t)k * (k - 1u);
+      Fn = (int64_t)A * (int64_t)(k - 1u) + (int64_t)c.hz * (int64_t)k * ((int64_t)x - (int64_t)y1);
+    } else {
+      D = 1;
+      Fn = (int64_t)A;
+    }
+    const uint64_t F = Fn < 0 ? 0ull : (uint64_t)Fn;
+    const uint32_t nc = nrungs ? nrungs + 1u : 32u;
+    uint32_t cand = 0;
+    if (lane >= 1u && lane < nc)
+      cand = nrungs ? c.rungs[lane - 1u] : rmin + (uint32_t)((uint64_t)(lane - 1u) * (rmax - rmin) / 30u);
+    unsigned __int128 J = ~(unsigned __int128)0;
+    if (lane < nc) {
+      const unsigned __int128 lat = (unsigned __int128)F * (10000u - cand);
+      const unsigned __int128 thr = (unsigned __int128)t1 * 10000u * D;
+      const unsigned __int128 ex = lat > thr ? lat - thr : 0;
+      const uint32_t dr = cand > r_cur ? cand - r_cur : r_cur - cand;
+      J = (unsigned __int128)c.wlat * ex +
+          (unsigned __int128)(10000ull * D) * ((uint64_t)c.wq * cand + (uint64_t)c.wosc * dr);
+    }
+    uint32_t idx = lane;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const unsigned __int128 Jo = shfl_xor_u128(J, m);
+      const uint32_t io = __shfl_xor_sync(FULL, idx, m);
+      if (Jo < J || (Jo == J && io < idx)) {
+        J = Jo;
+        idx = io;
+      }
+    }
+    nr = __shfl_sync(FULL, cand, (int)idx);
+    act = nr > 0u;
+  } else if (law == BELLMAN_LAW_BBR) {
+    if (x < rt_min) rt_min = x;
+    uint32_t bw = w;  // the window's other seconds: wring holds them (0 where unfilled)
+    for (uint32_t i = 0; i < window; ++i)
+      if (i != pos && c.wring[i] > bw) bw = c.wring[i];
+    const bool congested = A >= (uint64_t)k * ((uint64_t)rt_min + t1);
+    const bool plateau = 8ull * w >= 7ull * bw;
+    nr = r_cur;
+    if (congested && plateau) {
+      if (nrungs) {
+        rung = r_cur == 0u ? 0u : (rung + 1u < nrungs ? rung + 1u : rung);
+        nr = c.rungs[rung];
+      } else {
+        nr = r_cur == 0u ? rmin : (r_cur + c.step > rmax ? rmax : r_cur + c.step);
+      }
+    } else if (!congested) {
+      if (nrungs) {
+        if (r_cur == 0u || rung == 0u) {
+          nr = 0;
+        } else {
+          rung--;
+          nr = c.rungs[rung];
+        }
+      } else {
+        nr = r_cur <= rmin ? 0u : (r_cur < rmin + c.step ? rmin : r_cur - c.step);
+      }
+    }
+    act = nr > 0u;
+  } else {  // BELLMAN_LAW_PCC
+    act = A >= (uint64_t)k * t1;
+    const uint32_t d = c.step;
+    if (!act) {
+      phase = 0;
+      rbase = 0;
+      nr = 0;
+    } else {
+      const uint64_t cost = (uint64_t)c.wlat * (x > t1 ? x - t1 : 0u) + (uint64_t)c.wq * r_cur;
+      if (phase == 0u) {
+        rbase = rmin;
+      } else if (phase == 1u) {
+        cost_a = cost;
+      } else {
+        if (cost_a < cost) rbase = rbase + d > rmax ? rmax : rbase + d;
+        else if (cost < cost_a) rbase = rbase < rmin + d ? rmin : rbase - d;
+      }
+      if (phase == 1u) {
+        nr = rbase < rmin + d ? rmin : rbase - d;
+        phase = 2;
+      } else {
+        nr = rbase + d > rmax ? rmax : rbase + d;
+        phase = 1;
+      }
+    }
+  }
+  const uint32_t nctrl = DBG ? c.dbg_nctrl : 0u;
+  __syncwarp();
+  if (lane == 0) {
+    c.ring[pos] = x;
+    c.wring[pos] = w;
+    c.ringA = A;
+    c.ring_n = k;
+    c.ring_pos = npos;
+    c.rung = rung;
+    c.rt_min = rt_min;
+    c.phase = phase;
+    c.rbase = rbase;
+    c.cost_a = cost_a;
+    c.active = act;
+    c.activations += (act && !was_active) ? 1u : 0u;
+    c.active_ingests += act;
+    if (act != (was_active != 0)) {  // the log is kept by second index (R21)
+      const uint32_t second = (uint32_t)(sec_bound / kUs - 1u);
+      if (act) {
+        if (c.first_act == BELLMAN_NONE) c.first_act = second;
+      } else {
+        c.last_deact = second;
+      }
+    }
+    if (DBG && dbg) {
+      if (nctrl < c.dbg_cap) {
+        bellman_ctrl_row cr;
+        cr.second = (uint32_t)(sec_bound / kUs - 1u);
+        cr.sample = x;
+        cr.k = k;
+        cr.r_bp = nr;
+        cr.active = act;
+        cr._pad = 0;
+        cr.A = A;
+        c.dbg_ctrl[nctrl] = cr;
+      }
+      c.dbg_nctrl = nctrl + 1u;
+    }
+  }
+  __syncwarp();
+  return nr;
+}
+
+// ---------------------------------------------------------------------------
 // a6: one controller ingest of the closed second ending at sec_bound, whose
 // sample is the integer mean x = floor(acc_sum / acc_cnt) (P:134, P:193,
 // S:283-301; R3-R5, R12, R38).  Out of line, the 64-bit division included: it
@@ -516,7 +691,8 @@ __device__ __forceinline__ uint32_t ingest_body(uint32_t wid, uint32_t lane, uin
     __syncwarp();
   }
   const uint32_t law = g2.z, window = g2.w;
-  if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return r_cur;
+  if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP)
+    return law >= BELLMAN_LAW_MPC ? ingest_ext<DBG>(wid, lane, sec_bound, x, acc_cnt, r_cur, dbg) : r_cur;
   const uint32_t pos = g0.w, t1 = g3.x, was_active = g1.y;
   uint32_t k = g0.z, rung = g1.x;
   uint64_t A = (uint64_t)g0.x | ((uint64_t)g0.y << 32);
@@ -1516,6 +1692,14 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     z.bypassed = 0;
     z.kv_cap = pr.kv_cap_words;
     z.pf_ns = pr.prefill_ns_per_word;
+    z.hz = cc.horizon_s;
+    z.wlat = cc.w_lat;
+    z.wq = cc.w_q;
+    z.wosc = cc.w_osc;
+    z.step = cc.step_bp;
+    z.rt_min = BELLMAN_NONE;
+    z.phase = z.rbase = 0;
+    z.cost_a = 0;
     z.flags = flags;
     z.active = z.rung = z.ring_n = z.ring_pos = 0;
     z.ringA = 0;
@@ -1539,6 +1723,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   if (lane < 8) {
     S.cold().rungs[lane] = cc.rungs_bp[lane];
     S.cold().ring[lane] = 0;
+    S.cold().wring[lane] = 0;
   }
   if (KV0) {  // cost(B) = t0 + slope max(0, B - knee) >= 1 (host-validated t0 >= 1)
 #pragma unroll 1
@@ -1553,8 +1738,8 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   S.r = law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
   S.acc_sum = 0;
   S.acc_cnt = 0;
-  // the per-second signal feeds only the controller (MAP/STEP) and the recorders
-  S.sec_bound = (law == BELLMAN_LAW_MAP || law == BELLMAN_LAW_STEP || rslot != BELLMAN_NONE || (DBG && S.dbg))
+  // the per-second signal feeds only the controller (MAP / STEP / NEXT-3 laws) and the recorders
+  S.sec_bound = (law >= BELLMAN_LAW_MAP || rslot != BELLMAN_NONE || (DBG && S.dbg))
                     ? (uint32_t)kUs : INF32;
   S.Hr = S.rel((uint64_t)sc.horizon_us);
   S.T = 0;

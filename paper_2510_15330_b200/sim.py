@@ -64,7 +64,8 @@ def pack(cols: dict, pinned: bool = False) -> dict:
                  ("r_min_bp", "ctrl_rmin"), ("r_max_bp", "ctrl_rmax"), ("r_const_bp", "ctrl_rconst"),
                  ("t1", "ctrl_t1"), ("t2", "ctrl_t2"), ("slo_us", "ctrl_slo_us"),
                  ("calibrated", "ctrl_calibrated"), ("n_rungs", "ctrl_nrungs"), ("bypass_mask", "ctrl_bypass_mask"),
-                 ("min_words_bypass", "ctrl_min_words")):
+                 ("min_words_bypass", "ctrl_min_words"), ("horizon_s", "ctrl_horizon"), ("w_lat", "ctrl_wlat"),
+                 ("w_q", "ctrl_wq"), ("w_osc", "ctrl_wosc"), ("step_bp", "ctrl_step")):
         ctrls[:nc][f] = cols[c]
     ctrls[:nc]["rungs_bp"] = np.asarray(cols["ctrl_rungs"]).reshape(nc, 8)
     ns = len(cols["sc_seed"])

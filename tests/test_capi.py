@@ -114,3 +114,33 @@ def test_sass_sm100a_warp_level_no_transcendentals():
         assert mnemonic in out, mnemonic
     mufu = set(_re.findall(r"MUFU\.(\w+)", out))
     assert mufu <= {"RCP", "RCP64H"}, mufu
+
+
+def test_next3_law_validation():
+    """NEXT-3 laws: BBR needs the TBT signal, PCC a delta and no rungs, MPC a
+    bounded horizon and w_lat >= 1; weights <= 65535; no calibration."""
+    from paper_2510_15330_b200 import _abi as A, sim
+    import workloads as W
+
+    def cols(c):
+        w = W.config_c2(n_seeds=1, rates=[1.0])
+        w.ctrls = [c] + w.ctrls[1:]
+        return w.columns()
+
+    assert sim.workspace_bytes(sim.pack(cols(W.mpc_ctrl(24_000)))) > 0
+    assert sim.workspace_bytes(sim.pack(cols(W.bbr_ctrl(3_000)))) > 0
+    assert sim.workspace_bytes(sim.pack(cols(W.pcc_ctrl(24_000)))) > 0
+    bad = [
+        (W.bbr_ctrl(3_000).__class__(**{**W.bbr_ctrl(3_000).__dict__, "signal": W.SIG_E2E}), "BBR needs the TBT"),
+        (W.Ctrl(**{**W.pcc_ctrl(24_000).__dict__, "step_bp": 0}), "PCC needs 1 <= step_bp"),
+        (W.Ctrl(**{**W.pcc_ctrl(24_000).__dict__, "rungs_bp": (500, 2000)}), "PCC takes no rungs"),
+        (W.mpc_ctrl(24_000, horizon_s=17), "horizon_s > 16"),
+        (W.mpc_ctrl(24_000, w_lat=0), "MPC needs w_lat"),
+        (W.mpc_ctrl(24_000, w_q=70000), "weights must be <= 65535"),
+        (W.Ctrl(**{**W.mpc_ctrl(24_000).__dict__, "calibrated": 1}), "calibration is for MAP"),
+        (W.Ctrl(**{**W.bbr_ctrl(3_000).__dict__, "step_bp": 0}), "BBR needs 1 <= step_bp"),
+        (W.Ctrl(**{**W.mpc_ctrl(24_000).__dict__, "law": 7}), "unknown law"),
+    ]
+    for c, msg in bad:
+        with pytest.raises(A.BellmanError, match=msg):
+            sim.workspace_bytes(sim.pack(cols(c)))

@@ -521,3 +521,65 @@ def test_next4_contending_prefill():
     bad, st = check_all(w.columns())
     _assert_ok(bad)
     assert int(st["served"].sum()) > 0 and int(st["activations"].sum()) > 0
+
+
+def _next3_laws_workload():
+    """NEXT-3 MPC / BBR / PCC laws (readings R41-R43) across loads,
+    profiles, windows, signals and both termination modes; every fourth
+    scenario debug-recorded (the DBG instantiation and its controller log)."""
+    traces = [W.paper_trace(), W.paper_trace(3.5, 180, 0.6), W.const_trace(3.0, 400), W.const_trace(1.6, 500),
+              W.paper_trace(2.0, 90, 0.2)]
+    profs = [W.PROFILES["P24"], W.PROFILES["L8B"], dict(W.PROFILES["P24"], max_batch=33, knee=7)]
+    ctrls = [
+        W.mpc_ctrl(24_000),
+        W.mpc_ctrl(26_000, horizon_s=0, w_lat=1, w_q=2, w_osc=1, rungs=(500, 1000, 1500, 2000), window=1),
+        W.mpc_ctrl(22_000, horizon_s=16, w_lat=65535, w_q=65535, w_osc=65535, window=8, r_min_bp=1, r_max_bp=5000),
+        W.mpc_ctrl(8_000_000, horizon_s=5, w_lat=2, w_q=1, w_osc=0, signal=W.SIG_E2E, window=3),
+        W.bbr_ctrl(3_000),
+        W.bbr_ctrl(1_000, rungs=(300, 700, 1200, 1900), window=1),
+        W.bbr_ctrl(6_000, step_bp=5000, r_min_bp=100, r_max_bp=5000, window=8),
+        W.pcc_ctrl(24_000),
+        W.pcc_ctrl(22_000, delta_bp=100, w_lat=3, w_q=1, window=1),
+        W.pcc_ctrl(300, delta_bp=5000, w_lat=65535, w_q=65535, signal=W.SIG_SLO, slo_us=9_000_000, window=2,
+                   r_min_bp=1, r_max_bp=5000),
+    ]
+    sc = []
+    for ti in range(len(traces)):
+        for pi in range(len(profs)):
+            for ci in range(len(ctrls)):
+                for seed in range(2):
+                    mode = (ti + ci + seed) % 2
+                    rec = 2 if (ti + pi + ci + seed) % 4 == 0 else 0
+                    sc.append(W.Scenario(seed + 7 * ti, wid=ti, trace=ti, profile=pi, ctrl=ci, segment=0, mode=mode,
+                                         horizon_us=(1400 if mode else 900) * W.US, record=rec))
+    return W.custom(traces, profs, ctrls, sc)
+
+
+def test_next3_mpc_bbr_pcc_laws():
+    """GPU parity for the NEXT-3 laws: every summary field, per-scenario
+    histograms, and for debug-recorded scenarios the per-second rows and the
+    controller log element by element."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    w = _next3_laws_workload()
+    cols = w.columns()
+    bad, st = check_all(cols)
+    _assert_ok(bad)
+    laws = np.asarray(cols["ctrl_law"])[np.asarray(cols["sc_ctrl"])]
+    for law in (W.LAW_MPC, W.LAW_BBR, W.LAW_PCC):
+        assert int(st["rewritten"][laws == law].sum()) > 0, law  # every law acted
+    sim = Simulator(cols)
+    sim.run()
+    torch.cuda.synchronize()
+    b = oracle.Bound(cols)
+    for sid in [i for i, s in enumerate(w.scenarios) if s.record & 2]:
+        o = oracle.run_scenario(b, sid, rows_cap=100000, ctrl_log_cap=100000)
+        rows, ctrl = sim.series(sid)
+        for f in o["rows"].dtype.names:
+            assert np.array_equal(rows[f].astype(np.int64), o["rows"][f].astype(np.int64)), (sid, f)
+        assert len(ctrl) == len(o["ctrl_log"]), sid
+        for g, e in zip(ctrl, o["ctrl_log"]):
+            assert (int(g["second"]), int(g["sample"]), int(g["k"]), int(g["r_bp"]), int(g["active"]),
+                    int(g["A"])) == (e["second"], e["sample"], e["k"], e["r_bp"], e["active"], e["A"]), sid

@@ -251,4 +251,4 @@ def test_bruteforce_controller_laws(orc, law):
             assert (r["admit_us"], r["done_us"], r["R"], r["r_bp"]) == \
                    (bf["admit"][i], bf["done"][i], bf["R"][i], bf["r_bp"][i]), (law, case, i)
         acted += any(r["r_bp"] > 0 for r in d["requests"])
-    assert acted >= 3, law  # the law acted in the loop, not only stayed at r = 0
+    assert acted >= 2, law  # the law acted in the loop, not only stayed at r = 0

@@ -155,7 +155,15 @@ typedef struct {
    * system) and, re-admitted, prefill input + emitted again, that prefill's
    * end emitting their next word.  1 requires prefill_mode = 0. */
   uint32_t kv_policy;
-  uint32_t _pad;
+  /* NEXT-4 token-level costs (S:249 tokens_per_word; reading R44): tokens per
+   * word in Q16, 0 = the engine counts words (SPEC's model).  Nonzero (16384 ..
+   * 262144, i.e. 0.25 .. 4): a request's input and realized output of w words
+   * are max(1, floor((w tpw + 2^15) / 2^16)) tokens; the engine decodes one
+   * token per request per iteration (TBT gaps per token), and every per-unit
+   * constant above and below (prefill and KV ns, KV capacity, energy, and the
+   * words_in / words_out counters of the summary) is per token.  The rewrite
+   * N and the similarity score stay in words.  Inputs must stay < 65536 tokens. */
+  uint32_t tpw_q16;
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;
 } bellman_profile; /* 64 bytes */
 

@@ -65,6 +65,7 @@ typedef struct {
   const uint32_t *prof_kv_cap; /* NEXT-4: KV capacity in context words, 0 = unlimited */
   const uint32_t *prof_prefill_mode; /* NEXT-4: 0 non-blocking prefill, 1 contending */
   const uint32_t *prof_kv_policy;    /* NEXT-4: 0 reserve whole contexts, 1 preempt on overflow */
+  const uint32_t *prof_tpw;          /* NEXT-4: tokens per word Q16 (0 = the engine counts words) */
   const double *prof_e_in, *prof_e_out, *prof_p_idle;
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
@@ -107,6 +108,10 @@ typedef struct {
                             input + R), 1 preempt (admit on the current context input + emitted;
                             at an iteration end whose contexts exceed the capacity, the latest
                             admitted requests go back to the queue front and later recompute) */
+  uint32_t tpw_q16;      /* NEXT-4 token-level costs (R44): tokens per word in Q16; 0 = words.
+                            Nonzero: inputs and realized outputs are converted to tokens
+                            (max(1, round(w tpw))), the engine decodes one token per request per
+                            iteration, and every per-unit constant is per token */
 } orc_profile;
 
 typedef struct {

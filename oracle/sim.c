@@ -438,9 +438,26 @@ static int in_window(uint64_t t, const orc_run_cfg *cfg) {
   return (int64_t)t >= cfg->w0_us && (int64_t)t < cfg->w1_us;
 }
 
-int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof,
+/* NEXT-4 token-level costs ("tokens_per_word"; reading R44): with
+ * tpw_q16 != 0 the engine works in tokens — a count of w words is
+ * max(1, round(w tpw)) tokens (half-up, Q16) — and every per-unit constant of
+ * the profile (prefill and KV ns, KV capacity, energy per unit) is per token. */
+static uint32_t to_tokens(uint32_t words, uint32_t tpw_q16) {
+  if (tpw_q16 == 0) return words;
+  uint64_t t = ((uint64_t)words * tpw_q16 + (1u << 15)) >> 16;
+  return t < 1 ? 1u : (uint32_t)t;
+}
+
+int orc_simulate(const orc_request *req_words, uint64_t n_req, const orc_profile *prof,
                  const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log) {
   memset(res, 0, sizeof(*res));
+  /* the engine's view of each request: its input in tokens (R44) */
+  orc_request *req = (orc_request *)malloc((n_req ? n_req : 1) * sizeof(orc_request));
+  if (!req) return -1;
+  for (uint64_t i = 0; i < n_req; ++i) {
+    req[i] = req_words[i];
+    req[i].input = to_tokens(req_words[i].input, prof->tpw_q16);
+  }
   res->first_act_s = res->last_deact_s = ORC_NONE;
   res->t1 = ctrl->t1;
   res->t2 = ctrl->t2;
@@ -762,7 +779,9 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
         /* NEXT-3 bypass: class policy or a short predicted output */
         int bypass = r > 0 && (((ctrl->bypass_mask >> req[m].cls) & 1u) || req[m].P < ctrl->min_words_bypass);
         if (bypass) r = 0;
-        uint32_t R = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+        /* realized output in words (the rewrite), decoded as tokens (R44) */
+        const uint32_t R_words = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+        const uint32_t R = to_tokens(R_words, prof->tpw_q16);
         /* NEXT-4 KV-capacity admission: the head's full context (input + realized
          * output) must fit beside everything admitted; strict FIFO; an oversized
          * request is admitted only into an empty system */
@@ -813,7 +832,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
           res->hist_r[r / 10 < ORC_HIST_R ? r / 10 : ORC_HIST_R - 1]++;
         }
         { /* NEXT-2: score the admitted request against its unbounded counterpart */
-          uint32_t sc = orc_similarity(req[m].U, rs[m].R, r > 0, req[m].qnoise, cfg->quality);
+          uint32_t sc = orc_similarity(req[m].U, R_words, r > 0, req[m].qnoise, cfg->quality);
           uint32_t qb = sc / 50 < ORC_HIST_Q ? sc / 50 : ORC_HIST_Q - 1;
           if (r > 0) { res->hist_q_active[qb]++; res->scored_active++; }
           else { res->hist_q_inactive[qb]++; res->scored_inactive++; }
@@ -957,7 +976,7 @@ int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof
   }
   rc = 0;
 out:
-  free(rs); free(queue); free(ready); free(batch); free(pending); free(stack); free(e2e_v); free(ttft_v);
+  free(req); free(rs); free(queue); free(ready); free(batch); free(pending); free(stack); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
   free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
   free(sec_util_cnt);
@@ -980,6 +999,7 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   p->kv_cap_words = in->prof_kv_cap[pi];
   p->prefill_mode = in->prof_prefill_mode[pi];
   p->kv_policy = in->prof_kv_policy[pi];
+  p->tpw_q16 = in->prof_tpw[pi];
   memset(c, 0, sizeof(*c));
   c->law = in->ctrl_law[ci];
   c->signal = in->ctrl_signal[ci];

@@ -148,6 +148,15 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (p.prefill_mode == BELLMAN_PREFILL_CONTENDING &&
         (uint64_t)p.max_batch * ((uint64_t)p.prefill_ns_per_word * 65535u / 1000u + 1u) >= (1ull << 30))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: contending prefill: max_batch x max prefill >= 2^30 us", i);
+    if (p.tpw_q16 != 0u && (p.tpw_q16 < 16384u || p.tpw_q16 > 262144u))
+      return fail(nullptr, BELLMAN_EINVAL, "profile %u: tpw_q16 not 0 or in 16384..262144 (0.25..4 tokens/word)", i);
+    if (p.tpw_q16 != 0u) {  // inputs are 16-bit token counts on the device
+      uint32_t max_in = 0;
+      for (int k = 0; k < BELLMAN_TABLE_N; ++k) max_in = std::max(max_in, (uint32_t)m.I_words[k]);
+      for (uint64_t k = 0; k < d->n_arrivals; ++k) max_in = std::max(max_in, d->arrivals[k].input_words);
+      if ((((uint64_t)max_in * p.tpw_q16 + (1u << 15)) >> 16) > 65535u)
+        return fail(nullptr, BELLMAN_EINVAL, "profile %u: an input of %u words is >= 65536 tokens", i, max_in);
+    }
     if (!(p.e_in_j_per_word >= 0) || !(p.e_out_j_per_word >= 0) || !(p.p_idle_w >= 0))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: negative energy coefficient", i);
   }

@@ -197,7 +197,8 @@ struct alignas(16) Cold {
   uint32_t k0, wid_lo, wid_hi;
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
-  uint32_t pf_ns;                             // prefill ns per input word
+  uint32_t pf_ns;                             // prefill ns per input word (token, tpw != 0)
+  uint32_t tpw;                               // NEXT-4 tokens per word Q16, 0 = words (R44)
   // NEXT-3 MPC / BBR / PCC parameters and state (ingest_ext only)
   uint32_t hz, wlat, wq, wosc, step;          // horizon s, cost weights, step / delta bp
   uint32_t rt_min, phase, rbase;              // BBR RTprop; PCC phase and r_base
@@ -309,6 +310,14 @@ __device__ __noinline__ uint4 leap_wide(uint32_t lane, uint32_t cb, uint32_t q, 
 }
 
 // prefill duration of a request with `in` input words (R6): >= 1 µs
+// NEXT-4 token-level costs (R44): w words are max(1, round(w tpw)) tokens
+// (half-up, Q16); tpw = 0 keeps words
+__device__ __forceinline__ uint32_t to_tokens(uint32_t w, uint32_t tpw) {
+  if (tpw == 0u) return w;
+  const uint32_t t = (uint32_t)(((uint64_t)w * tpw + (1u << 15)) >> 16);
+  return t < 1u ? 1u : t;
+}
+
 __device__ __forceinline__ uint32_t prefill_us(uint32_t pf_ns, uint32_t in) {
   const uint32_t pf = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
   return pf < 1u ? 1u : pf;
@@ -368,10 +377,11 @@ __device__ __noinline__ uint4 refill_buffer(const Params &p, uint32_t wid, uint3
           const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);
           const uint64_t U = ((uint64_t)A.L_words * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;
           const int32_t P0 = (int32_t)A.L_words + __ldg(&p.tabN[v.y >> 20]);
-          store_qent(c.q[lane], tau, A.input_words | (A.cls << 16), U < 1 ? 1u : (uint32_t)U,
+          const uint32_t in_t = to_tokens(A.input_words, c.tpw);  // the engine's input (R44)
+          store_qent(c.q[lane], tau, in_t | (A.cls << 16), U < 1 ? 1u : (uint32_t)U,
                      P0 < 1 ? 1u : (uint32_t)P0,
                      (uint32_t)__ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(__ldg(&p.tabQ[v.w >> 20]) + 2048) << 20),
-                     prefill_us(c.pf_ns, A.input_words), jj, c, p.q_inactive);
+                     prefill_us(c.pf_ns, in_t), jj, c, p.q_inactive);
         }
         if (DBG && dbg && tau < H) {
           const uint64_t sidx = tau / kUs;
@@ -449,7 +459,7 @@ __device__ __noinline__ uint4 refill_buffer(const Params &p, uint32_t wid, uint3
       const uint32_t L = (uint32_t)__ldg(&p.tabL[u.z >> 20]);
       const uint32_t x = u.z & 0xFFFFFu;  // class draw from the bits below L's index (NEXT-3)
       const uint32_t cls = x < p.class_cum0 ? 0u : (x < p.class_cum1 ? 1u : (x < p.class_cum2 ? 2u : 3u));
-      const uint32_t in = (uint32_t)__ldg(&p.tabI[u.w >> 20]);
+      const uint32_t in = to_tokens((uint32_t)__ldg(&p.tabI[u.w >> 20]), c.tpw);  // engine units (R44)
       const uint4 v = philox(k0, kSeedHi, jj, 1u, wid_lo, wid_hi);  // a3: the request's own draws
       const uint64_t U = ((uint64_t)L * (uint32_t)__ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
       const int32_t P0 = (int32_t)L + __ldg(&p.tabN[v.y >> 20]);
@@ -1368,6 +1378,7 @@ struct Sim {
         sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
         qb = (uint32_t)sc / 50u;
       }
+      R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
       const uint32_t kvcap = cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
@@ -1692,6 +1703,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
     z.bypassed = 0;
     z.kv_cap = pr.kv_cap_words;
     z.pf_ns = pr.prefill_ns_per_word;
+    z.tpw = pr.tpw_q16;
     z.hz = cc.horizon_s;
     z.wlat = cc.w_lat;
     z.wq = cc.w_q;

@@ -125,6 +125,12 @@ class _Law:
 def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max=2000, window=5,
              r_const=0, mode_drain=True, rungs=(), horizon_s=0, w_lat=0, w_q=0, w_osc=0, step_bp=0,
              signal="tbt", slo_us=0):
+    tpw = prof.get("tpw_q16", 0)
+
+    def tok(w):  # NEXT-4 token-level costs (R44): round-half-up w * tpw, at least 1
+        return w if not tpw else max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2)))
+
+    requests = [dict(q, input=tok(q["input"])) for q in requests]  # the engine counts input tokens
     n = len(requests)
     st = ["future"] * n
     admit = [None] * n
@@ -274,6 +280,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                         Rh = max(1, int(Fraction(Nh) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
                     else:
                         Rh = q["U"]
+                    Rh = tok(Rh)
                     reserved = sum(requests[i]["input"] + R[i] for i in range(n)
                                    if st[i] in ("prefill", "ready", "decoding", "pending"))
                     if in_sys > 0 and reserved + q["input"] + Rh > cap:
@@ -290,6 +297,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
                     R[m] = max(1, int(Fraction(N) * Fraction(q.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
                 else:
                     R[m] = q["U"]
+                R[m] = tok(R[m])  # realized words decoded as tokens
                 pf = max(1, prof["prefill_ns_per_word"] * q["input"] // 1000)
                 if prof.get("prefill_mode", 0):
                     pend[m] = pf  # a duration until the iteration starts

@@ -583,3 +583,31 @@ def test_next3_mpc_bbr_pcc_laws():
         for g, e in zip(ctrl, o["ctrl_log"]):
             assert (int(g["second"]), int(g["sample"]), int(g["k"]), int(g["r_bp"]), int(g["active"]),
                     int(g["A"])) == (e["second"], e["sample"], e["k"], e["r_bp"], e["active"], e["A"]), sid
+
+
+def test_next4_token_level_costs():
+    """NEXT-4 token-level costs (R44): profiles at 0.25, 0.75, 1.3 and 3
+    tokens per word with KV term, KV capacity (reserve and preempt),
+    contending prefill and a replayed trace, under OFF / MAP / MPC laws:
+    every summary field and histogram vs the oracle."""
+    T13 = round(1.3 * 65536)
+    traces = [W.paper_trace(), W.const_trace(2.0, 400),
+              {"replay": [(0, 500, 9000, 0), (2 * W.US, 800, 4000, 1), (2 * W.US, 300, 15000, 0),
+                          (9 * W.US, 700, 12000, 2)] + [(int(10 * W.US + k * 370_000), 400 + k, 2000 + 37 * k, 0)
+                                                       for k in range(300)]}]
+    profs = [dict(W.PROFILES["P24"], tpw_q16=T13), dict(W.PROFILES["L8B"], tpw_q16=49152),
+             dict(W.PROFILES["P24"], tpw_q16=16384, kv_cap_words=60_000),
+             dict(W.PROFILES["P24"], tpw_q16=196608, max_batch=16),
+             dict(W.PROFILES["L8B"], tpw_q16=T13, kv_cap_words=200_000, kv_policy=1),
+             dict(W.PROFILES["P24"], tpw_q16=T13, prefill_mode=1, max_batch=8)]
+    ctrls = [W.OFF, W.map_ctrl(24_000, 40_000), W.mpc_ctrl(24_000)]
+    sc = []
+    for ti in range(len(traces)):
+        for pi in range(len(profs)):
+            for ci in range(len(ctrls)):
+                mode = (ti + pi + ci) % 2
+                sc.append(W.Scenario(3 + ti + ci, wid=ti, trace=ti, profile=pi, ctrl=ci, segment=0, mode=mode,
+                                     horizon_us=(1500 if mode else 800) * W.US))
+    bad, st = check_all(W.custom(traces, profs, ctrls, sc).columns())
+    _assert_ok(bad)
+    assert int(st["served"].sum()) > 1000

@@ -577,3 +577,75 @@ def test_kv_preemption_identities(orc):
     free = orc.simulate(reqs, dict(prof, kv_cap_words=0), mode=W.MODE_DRAIN)
     assert big["preemptions"] == 0
     assert [r["done_us"] for r in big["requests"]] == [r["done_us"] for r in free["requests"]]
+
+
+TPW13 = round(1.3 * 65536)  # R31 / S:249: 1.3 tokens per word
+
+
+def test_token_costs_spec_example_in_tokens(orc):
+    """NEXT-4 token-level costs (R44): S:207's single request (input 10,000
+    words, R = 500 words) with 1.3 tokens per word is 13,000 input tokens and 650
+    output tokens: prefill 13,000 x 80 µs = 1.04 s, 649 decode iterations of
+    50 ms, E2E = 1,040,000 + 649 x 50,000 µs; energy 0.05 x 13,000 + 0.5 x 650."""
+    prof = dict(LIT, tpw_q16=TPW13)
+    d = orc.simulate([dict(a_us=0, input=10_000, U=500)], prof, mode=W.MODE_DRAIN)
+    r = d["requests"][0]
+    assert r["first_us"] == 1_040_000 and r["R"] == 650
+    assert r["done_us"] == 1_040_000 + 649 * 50_000
+    assert d["ticks"] == 649 and d["words_in"] == 13_000 and d["words_out"] == 650
+    assert d["energy_j"] == 0.05 * 13_000 + 0.5 * 650
+    # rounding: 1 word -> round(1.3) = 1 token; 5 words -> round(6.5) = 7 (half up); tpw 0.25: 1 word -> 1
+    d = orc.simulate([dict(a_us=0, input=5, U=1)], dict(LIT, tpw_q16=TPW13), mode=W.MODE_DRAIN)
+    assert d["words_in"] == 7 and d["requests"][0]["R"] == 1
+    d = orc.simulate([dict(a_us=0, input=1, U=1)], dict(LIT, tpw_q16=16384), mode=W.MODE_DRAIN)
+    assert d["words_in"] == 1
+
+
+def test_token_costs_identities(orc):
+    """tpw = 1.0 (65536) is byte-identical to the word engine (tpw = 0); and a
+    run at tpw = 2.0 equals the word run with every input and unbounded
+    length doubled (no rewriting), field by field and gap by gap."""
+    rng = np.random.default_rng(41)
+    reqs = []
+    t = 0
+    for _ in range(200):
+        t += int(rng.integers(0, 200_000))
+        reqs.append(dict(a_us=t, input=int(rng.integers(100, 3000)), U=int(rng.integers(2, 60)),
+                         P=int(rng.integers(2, 60))))
+    P24 = dict(W.PROFILES["P24"], max_batch=8, kv_ns_per_word=30)
+    c = orc.make_ctrl(law=W.LAW_MAP, t1=22_000, t2=30_000)
+    a = orc.simulate(reqs, P24, ctrl=c, mode=W.MODE_DRAIN)
+    b = orc.simulate(reqs, dict(P24, tpw_q16=65536), ctrl=c, mode=W.MODE_DRAIN)
+    for k in orc.SUMMARY_FIELDS:
+        assert a[k] == b[k], k
+    assert a["gaps"] == b["gaps"] and a["rewritten"] > 0
+    dbl = [dict(q, input=2 * q["input"], U=2 * q["U"]) for q in reqs]
+    w = orc.simulate(dbl, P24, mode=W.MODE_DRAIN)
+    x = orc.simulate(reqs, dict(P24, tpw_q16=131072), mode=W.MODE_DRAIN)
+    for k in ("ticks", "served", "words_in", "words_out", "end_us", "idle_us", "sum_e2e_us", "sum_ttft_us",
+              "sum_queue_us", "e2e_p50_ms", "e2e_p99_ms", "energy_j"):
+        assert w[k] == x[k], k
+    assert w["gaps"] == x["gaps"]
+
+
+def test_bruteforce_token_costs(orc):
+    """Token-level costs in the loop (rewrite in words, decode in tokens) vs the
+    brute-force simulator, with KV capacity and a MAP controller."""
+    rng = np.random.default_rng(43)
+    for case in range(60):
+        reqs, prof = _random_tiny(rng)
+        prof["tpw_q16"] = int(rng.choice([16384, 50000, TPW13, 131072, 262144]))
+        if case % 2:
+            prof["kv_cap_words"] = int(rng.integers(20, 200))
+        law = "const" if case % 3 == 0 else "off"
+        rc = int(rng.integers(100, 3000)) if law == "const" else 0
+        bf = bruteforce.simulate(reqs, prof, 10**6, law=law, r_const=rc)
+        c = orc.make_ctrl(law=W.LAW_CONST, r_const_bp=rc) if law == "const" else None
+        d = orc.simulate(reqs, prof, ctrl=c, mode=W.MODE_DRAIN, horizon_us=10**6)
+        assert (d["ticks"], d["words_out"], d["end_us"], d["served"]) == \
+               (bf["ticks"], bf["words_out"], bf["end_us"], bf["served"]), case
+        for i in range(len(reqs)):
+            r = d["requests"][i]
+            assert (r["admit_us"], r["first_us"], r["done_us"], r["R"]) == \
+                   (bf["admit"][i], bf["first"][i], bf["done"][i], bf["R"][i]), (case, i)
+            assert d["gaps"][i] == bf["gaps"][i], (case, i)

@@ -44,7 +44,7 @@ class Inputs(C.Structure):
         ("trace_kind", u32p), ("arr_a", i64p), ("arr_L", u32p), ("arr_input", u32p), ("arr_cls", u32p),
         ("prof_t0", u32p), ("prof_knee", u32p), ("prof_slope", u32p), ("prof_kv", u32p),
         ("prof_maxb", u32p), ("prof_prefill_ns", u32p), ("prof_kv_cap", u32p), ("prof_prefill_mode", u32p),
-        ("prof_kv_policy", u32p), ("prof_tpw", u32p),
+        ("prof_kv_policy", u32p), ("prof_tpw", u32p), ("prof_replicas", u32p), ("prof_route", u32p),
         ("prof_e_in", f64p), ("prof_e_out", f64p), ("prof_p_idle", f64p),
         ("ctrl_law", u32p), ("ctrl_signal", u32p), ("ctrl_window", u32p), ("ctrl_rmin", u32p),
         ("ctrl_rmax", u32p), ("ctrl_rconst", u32p),
@@ -71,7 +71,8 @@ class Profile(C.Structure):
     _fields_ = [("t0_us", C.c_uint32), ("knee", C.c_uint32), ("slope_us", C.c_uint32),
                 ("kv_ns_per_word", C.c_uint32), ("max_batch", C.c_uint32), ("prefill_ns_per_word", C.c_uint32),
                 ("e_in", C.c_double), ("e_out", C.c_double), ("p_idle", C.c_double), ("kv_cap_words", C.c_uint32),
-                ("prefill_mode", C.c_uint32), ("kv_policy", C.c_uint32), ("tpw_q16", C.c_uint32)]
+                ("prefill_mode", C.c_uint32), ("kv_policy", C.c_uint32), ("tpw_q16", C.c_uint32),
+                ("replicas", C.c_uint32), ("route", C.c_uint32)]
 
 
 class Ctrl(C.Structure):
@@ -159,6 +160,7 @@ def lib():
         L.orc_arrivals.argtypes = [P(Inputs), C.c_uint64, P(Request), C.c_uint64]
         L.orc_arrivals.restype = C.c_int64
         L.orc_simulate.argtypes = [P(Request), C.c_uint64, P(Profile), P(Ctrl), P(RunCfg), P(Result), P(Log)]
+        L.orc_simulate_replicas.argtypes = [P(Request), C.c_uint64, P(Profile), P(Ctrl), P(RunCfg), P(Result), P(Log)]
         L.orc_run_scenario.argtypes = [P(Inputs), C.c_uint64, P(Result), P(Log)]
         L.orc_percentile_u32.argtypes = [u32p, C.c_uint64, C.c_uint32]
         L.orc_percentile_u32.restype = C.c_uint32
@@ -252,6 +254,7 @@ class Bound:
              ("prof_t0", np.uint32), ("prof_knee", np.uint32), ("prof_slope", np.uint32), ("prof_kv", np.uint32),
              ("prof_maxb", np.uint32), ("prof_prefill_ns", np.uint32), ("prof_kv_cap", np.uint32),
              ("prof_prefill_mode", np.uint32), ("prof_kv_policy", np.uint32), ("prof_tpw", np.uint32),
+             ("prof_replicas", np.uint32), ("prof_route", np.uint32),
              ("prof_e_in", np.float64), ("prof_e_out", np.float64), ("prof_p_idle", np.float64),
              ("ctrl_law", np.uint32), ("ctrl_signal", np.uint32), ("ctrl_window", np.uint32),
              ("ctrl_rmin", np.uint32), ("ctrl_rmax", np.uint32), ("ctrl_rconst", np.uint32),
@@ -360,7 +363,7 @@ def similarity(U: int, R: int, active: bool, noise: int = 0, q=QUALITY_DEFAULT) 
 
 def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_us=10**12,
              w0_us=0, w1_us=2**62, poly_q16=(0, 65536, 0), record=0, gap_cap=100000, ctrl_log_cap=10000,
-             quality=QUALITY_DEFAULT):
+             quality=QUALITY_DEFAULT, multi=False):
     """Run the DES on an explicit request list (hand fixtures, brute-force pins).
 
     ``requests``: iterable of dicts with a_us, input, U and optionally L, P, fcomp_q16, j.
@@ -375,7 +378,8 @@ def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_
     pr = Profile(profile["t0_us"], profile["knee"], profile["slope_us"], profile.get("kv_ns_per_word", 0),
                  profile["max_batch"], profile["prefill_ns_per_word"], profile.get("e_in", 0.05),
                  profile.get("e_out", 0.5), profile.get("p_idle", 300.0), profile.get("kv_cap_words", 0),
-                 profile.get("prefill_mode", 0), profile.get("kv_policy", 0), profile.get("tpw_q16", 0))
+                 profile.get("prefill_mode", 0), profile.get("kv_policy", 0), profile.get("tpw_q16", 0),
+                 profile.get("replicas", 0), profile.get("route", 0))
     c = ctrl if ctrl is not None else make_ctrl()
     cfg = RunCfg(mode, horizon_us, w0_us, w1_us, (C.c_int64 * 3)(*poly_q16), (C.c_uint32 * 5)(*quality), record)
     r = Result()
@@ -391,7 +395,8 @@ def simulate(requests, profile: dict, ctrl: Ctrl | None = None, mode=0, horizon_
     log.cap_ctrl = ctrl_log_cap
     log.series = ser
     log.cap_series = 200000
-    rc = lib().orc_simulate(rq, n, C.byref(pr), C.byref(c), C.byref(cfg), C.byref(r), C.byref(log))
+    fn = lib().orc_simulate_replicas if multi else lib().orc_simulate  # multi: the replica DES at any count
+    rc = fn(rq, n, C.byref(pr), C.byref(c), C.byref(cfg), C.byref(r), C.byref(log))
     if rc != 0:
         raise RuntimeError("oracle simulate failed")
     d = _result_dict(r)

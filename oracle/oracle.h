@@ -66,6 +66,7 @@ typedef struct {
   const uint32_t *prof_prefill_mode; /* NEXT-4: 0 non-blocking prefill, 1 contending */
   const uint32_t *prof_kv_policy;    /* NEXT-4: 0 reserve whole contexts, 1 preempt on overflow */
   const uint32_t *prof_tpw;          /* NEXT-4: tokens per word Q16 (0 = the engine counts words) */
+  const uint32_t *prof_replicas, *prof_route; /* NEXT-4 multi-replica routing (R45) */
   const double *prof_e_in, *prof_e_out, *prof_p_idle;
   const uint32_t *ctrl_law, *ctrl_signal, *ctrl_window, *ctrl_rmin, *ctrl_rmax, *ctrl_rconst;
   const uint32_t *ctrl_t1, *ctrl_t2, *ctrl_slo_us, *ctrl_calibrated, *ctrl_nrungs;
@@ -112,7 +113,12 @@ typedef struct {
                             Nonzero: inputs and realized outputs are converted to tokens
                             (max(1, round(w tpw))), the engine decodes one token per request per
                             iteration, and every per-unit constant is per token */
+  uint32_t replicas;     /* NEXT-4 (R45): engines sharing the arrival queue, 0/1 = one; max_batch each */
+  uint32_t route;        /* NEXT-4 (R45): ORC_ROUTE_LEAST (fewest in the replica) or ORC_ROUTE_RR */
 } orc_profile;
+
+#define ORC_MAX_REPLICAS 8
+enum { ORC_ROUTE_LEAST = 0, ORC_ROUTE_RR = 1 };
 
 typedef struct {
   uint32_t law, signal, window, r_min_bp, r_max_bp, r_const_bp, t1, t2, slo_us, calibrated, n_rungs;
@@ -211,6 +217,14 @@ int64_t orc_arrivals(const orc_inputs *in, uint64_t sid, orc_request *out, uint6
 /* The discrete-event simulation (a4-a9) over an explicit request list. */
 int orc_simulate(const orc_request *req, uint64_t n_req, const orc_profile *prof,
                  const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log);
+
+/* NEXT-4 multi-replica routing (R45): the same DES over prof->replicas engines
+ * sharing one arrival queue (orc_simulate dispatches here for replicas > 1;
+ * callable directly for any replica count, which pins one replica against
+ * orc_simulate).  Returns -1 for more than ORC_MAX_REPLICAS, contending
+ * prefill or a KV capacity. */
+int orc_simulate_replicas(const orc_request *req, uint64_t n_req, const orc_profile *prof,
+                          const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log);
 
 /* Full scenario: arrivals + (calibration pass a10) + simulation.  With
  * log->ctrl / log->rows given, the controller log and (record & 2) the

@@ -438,6 +438,95 @@ static int in_window(uint64_t t, const orc_run_cfg *cfg) {
   return (int64_t)t >= cfg->w0_us && (int64_t)t < cfg->w1_us;
 }
 
+/* Epilogue shared by both event loops: a8 energy, a9 percentiles (+ exact
+ * self-check values), the per-second rows and the per-request log. */
+static void finish_run(orc_result *res, const orc_profile *prof, uint64_t *e2e_v, uint64_t n_e2e, uint64_t *ttft_v,
+                       uint64_t n_ttft, const orc_second_row *rows, uint64_t n_sec, uint64_t end, uint64_t n_series,
+                       const rstate *rs, uint64_t n_req, orc_log *log) {
+  /* a8 energy, fp64, in this fixed order (R19) */
+  {
+    double a = prof->e_in * (double)res->words_in;
+    double b = prof->e_out * (double)res->words_out;
+    double c = prof->p_idle * (double)res->idle_us;
+    res->energy_j = (a + b) + c / 1e6;
+    double wa = prof->e_in * (double)res->win_words_in;
+    double wb = prof->e_out * (double)res->win_words_out;
+    double wc = prof->p_idle * (double)res->win_idle_us;
+    res->win_energy_j = (wa + wb) + wc / 1e6;
+  }
+  /* a9 percentiles: nearest rank on the histograms -> bin lower edge */
+  {
+    uint64_t n = res->served;
+    res->e2e_p50_ms = res->e2e_p99_ms = res->ttft_p50_ms = res->ttft_p99_ms = ORC_NONE;
+    res->median_r_bp = ORC_NONE;
+    const uint32_t ps[2] = {50, 99};
+    for (int w = 0; w < 2; ++w) {
+      const uint32_t *hh = w == 0 ? res->hist_e2e : res->hist_ttft;
+      uint64_t nn = w == 0 ? n : n_ttft;
+      for (int q = 0; q < 2; ++q) {
+        if (nn == 0) continue;
+        uint64_t k = nr_rank(nn, ps[q]), cum = 0;
+        uint32_t bsel = 0;
+        for (uint32_t b = 0; b < ORC_HIST_LAT; ++b) {
+          cum += hh[b];
+          if (cum >= k) { bsel = b; break; }
+        }
+        uint32_t v = (uint32_t)orc_lat_edge(bsel);
+        if (w == 0 && q == 0) res->e2e_p50_ms = v;
+        if (w == 0 && q == 1) res->e2e_p99_ms = v;
+        if (w == 1 && q == 0) res->ttft_p50_ms = v;
+        if (w == 1 && q == 1) res->ttft_p99_ms = v;
+      }
+    }
+    if (res->rewritten) {
+      uint64_t k = nr_rank(res->rewritten, 50), cum = 0;
+      for (uint32_t b = 0; b < ORC_HIST_R; ++b) {
+        cum += res->hist_r[b];
+        if (cum >= k) { res->median_r_bp = b * 10; break; }
+      }
+    }
+    /* NEXT-2 medians: nearest rank on the 0.5-point score histograms */
+    res->sim_active_p50 = res->sim_inactive_p50 = ORC_NONE;
+    for (int w = 0; w < 2; ++w) {
+      const uint32_t *hq = w == 0 ? res->hist_q_active : res->hist_q_inactive;
+      uint64_t nq = w == 0 ? res->scored_active : res->scored_inactive;
+      if (!nq) continue;
+      uint64_t k = nr_rank(nq, 50), cum = 0;
+      for (uint32_t b = 0; b < ORC_HIST_Q; ++b) {
+        cum += hq[b];
+        if (cum >= k) {
+          if (w == 0) res->sim_active_p50 = b * 50; else res->sim_inactive_p50 = b * 50;
+          break;
+        }
+      }
+    }
+    /* exact nearest-rank values (self-check only) */
+    qsort(e2e_v, n_e2e, sizeof(uint64_t), cmp_u64);
+    qsort(ttft_v, n_ttft, sizeof(uint64_t), cmp_u64);
+    res->e2e_exact_p50_us = n_e2e ? e2e_v[nr_rank(n_e2e, 50) - 1] : NEVER;
+    res->e2e_exact_p99_us = n_e2e ? e2e_v[nr_rank(n_e2e, 99) - 1] : NEVER;
+    res->ttft_exact_p50_us = n_ttft ? ttft_v[nr_rank(n_ttft, 50) - 1] : NEVER;
+    res->ttft_exact_p99_us = n_ttft ? ttft_v[nr_rank(n_ttft, 99) - 1] : NEVER;
+  }
+  res->n_series = (uint32_t)n_series;
+  if (rows && log && log->rows) {
+    uint64_t nr = end / US + 1; /* seconds 0 .. floor(end / 1e6) */
+    if (nr > n_sec) nr = n_sec;
+    for (uint64_t k = 0; k < nr && k < log->cap_rows; ++k) log->rows[k] = rows[k];
+    log->n_rows = nr;
+  }
+  if (log && log->req) {
+    for (uint64_t i = 0; i < n_req; ++i) {
+      log->req[i].admit_us = rs[i].admit;
+      log->req[i].first_us = rs[i].first;
+      log->req[i].done_us = rs[i].done;
+      log->req[i].R = rs[i].R;
+      log->req[i].r_bp = rs[i].r_bp;
+      log->req[i].n_gaps = rs[i].n_gaps;
+    }
+  }
+}
+
 /* NEXT-4 token-level costs ("tokens_per_word"; reading R44): with
  * tpw_q16 != 0 the engine works in tokens — a count of w words is
  * max(1, round(w tpw)) tokens (half-up, Q16) — and every per-unit constant of
@@ -450,6 +539,7 @@ static uint32_t to_tokens(uint32_t words, uint32_t tpw_q16) {
 
 int orc_simulate(const orc_request *req_words, uint64_t n_req, const orc_profile *prof,
                  const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log) {
+  if (prof->replicas > 1) return orc_simulate_replicas(req_words, n_req, prof, ctrl, cfg, res, log);
   memset(res, 0, sizeof(*res));
   /* the engine's view of each request: its input in tokens (R44) */
   orc_request *req = (orc_request *)malloc((n_req ? n_req : 1) * sizeof(orc_request));
@@ -892,91 +982,303 @@ int orc_simulate(const orc_request *req_words, uint64_t n_req, const orc_profile
   res->inflight_end = in_sys + n_stack; /* admitted and not completed (preempted ones waiting too) */
   if (res->queued_end + res->inflight_end > 0) res->flags |= ORC_FLAG_TRUNCATED;
 
-  /* a8 energy, fp64, in this fixed order (R19) */
-  {
-    double a = prof->e_in * (double)res->words_in;
-    double b = prof->e_out * (double)res->words_out;
-    double c = prof->p_idle * (double)res->idle_us;
-    res->energy_j = (a + b) + c / 1e6;
-    double wa = prof->e_in * (double)res->win_words_in;
-    double wb = prof->e_out * (double)res->win_words_out;
-    double wc = prof->p_idle * (double)res->win_idle_us;
-    res->win_energy_j = (wa + wb) + wc / 1e6;
-  }
-  /* a9 percentiles: nearest rank on the histograms -> bin lower edge */
-  {
-    uint64_t n = res->served;
-    res->e2e_p50_ms = res->e2e_p99_ms = res->ttft_p50_ms = res->ttft_p99_ms = ORC_NONE;
-    res->median_r_bp = ORC_NONE;
-    const uint32_t ps[2] = {50, 99};
-    for (int w = 0; w < 2; ++w) {
-      const uint32_t *hh = w == 0 ? res->hist_e2e : res->hist_ttft;
-      uint64_t nn = w == 0 ? n : n_ttft;
-      for (int q = 0; q < 2; ++q) {
-        if (nn == 0) continue;
-        uint64_t k = nr_rank(nn, ps[q]), cum = 0;
-        uint32_t bsel = 0;
-        for (uint32_t b = 0; b < ORC_HIST_LAT; ++b) {
-          cum += hh[b];
-          if (cum >= k) { bsel = b; break; }
-        }
-        uint32_t v = (uint32_t)orc_lat_edge(bsel);
-        if (w == 0 && q == 0) res->e2e_p50_ms = v;
-        if (w == 0 && q == 1) res->e2e_p99_ms = v;
-        if (w == 1 && q == 0) res->ttft_p50_ms = v;
-        if (w == 1 && q == 1) res->ttft_p99_ms = v;
-      }
-    }
-    if (res->rewritten) {
-      uint64_t k = nr_rank(res->rewritten, 50), cum = 0;
-      for (uint32_t b = 0; b < ORC_HIST_R; ++b) {
-        cum += res->hist_r[b];
-        if (cum >= k) { res->median_r_bp = b * 10; break; }
-      }
-    }
-    /* NEXT-2 medians: nearest rank on the 0.5-point score histograms */
-    res->sim_active_p50 = res->sim_inactive_p50 = ORC_NONE;
-    for (int w = 0; w < 2; ++w) {
-      const uint32_t *hq = w == 0 ? res->hist_q_active : res->hist_q_inactive;
-      uint64_t nq = w == 0 ? res->scored_active : res->scored_inactive;
-      if (!nq) continue;
-      uint64_t k = nr_rank(nq, 50), cum = 0;
-      for (uint32_t b = 0; b < ORC_HIST_Q; ++b) {
-        cum += hq[b];
-        if (cum >= k) {
-          if (w == 0) res->sim_active_p50 = b * 50; else res->sim_inactive_p50 = b * 50;
-          break;
-        }
-      }
-    }
-    /* exact nearest-rank values (self-check only) */
-    qsort(e2e_v, n_e2e, sizeof(uint64_t), cmp_u64);
-    qsort(ttft_v, n_ttft, sizeof(uint64_t), cmp_u64);
-    res->e2e_exact_p50_us = n_e2e ? e2e_v[nr_rank(n_e2e, 50) - 1] : NEVER;
-    res->e2e_exact_p99_us = n_e2e ? e2e_v[nr_rank(n_e2e, 99) - 1] : NEVER;
-    res->ttft_exact_p50_us = n_ttft ? ttft_v[nr_rank(n_ttft, 50) - 1] : NEVER;
-    res->ttft_exact_p99_us = n_ttft ? ttft_v[nr_rank(n_ttft, 99) - 1] : NEVER;
-  }
-  res->n_series = (uint32_t)n_series;
-  if (rows && log && log->rows) {
-    uint64_t nr = end / US + 1; /* seconds 0 .. floor(end / 1e6) */
-    if (nr > n_sec) nr = n_sec;
-    for (uint64_t k = 0; k < nr && k < log->cap_rows; ++k) log->rows[k] = rows[k];
-    log->n_rows = nr;
-  }
-  if (log && log->req) {
-    for (uint64_t i = 0; i < n_req; ++i) {
-      log->req[i].admit_us = rs[i].admit;
-      log->req[i].first_us = rs[i].first;
-      log->req[i].done_us = rs[i].done;
-      log->req[i].R = rs[i].R;
-      log->req[i].r_bp = rs[i].r_bp;
-      log->req[i].n_gaps = rs[i].n_gaps;
-    }
-  }
+  finish_run(res, prof, e2e_v, n_e2e, ttft_v, n_ttft, rows, n_sec, end, n_series, rs, n_req, log);
   rc = 0;
 out:
   free(req); free(rs); free(queue); free(ready); free(batch); free(pending); free(stack); free(e2e_v); free(ttft_v);
+  free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
+  free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
+  free(sec_util_cnt);
+  free(h.v); free(cs.samples); free(cs.words); free(rows);
+  return rc;
+}
+
+
+/* NEXT-4 multi-replica routing ("the request scheduler ... picks requests
+ * from the arrival queue and assigns to GPU servers"; P:183 8 GPUs; reading
+ * R45).  `replicas` continuous-batching engines share one FIFO arrival queue
+ * (the queue beLLMan rewrites in).  Replica q is at an admission point
+ * at T when no iteration of q is running at T.  At an instant where some
+ * replica is, the closed seconds are ingested and, while the queue holds an
+ * arrived request and a replica at an admission point has a free slot, the
+ * head is assigned to one of them chosen by the routing policy: least loaded
+ * (fewest requests in the replica: prefilling, decode-ready or decoding; ties
+ * to the lowest index) or round robin (the first such replica at or after a
+ * cyclic pointer, which then moves past it).  Every replica at an admission
+ * point with decode-ready requests then starts an iteration of its own batch
+ * under the profile's cost law (B and K of that replica).  The controller sees
+ * the node: every replica's words feed the per-second signal.  Idle (energy,
+ * R18) = the whole node empty.  One replica is exactly orc_simulate (pinned by
+ * tests); several require prefill_mode 0 and no KV capacity. */
+int orc_simulate_replicas(const orc_request *req_words, uint64_t n_req, const orc_profile *prof,
+                          const orc_ctrl *ctrl, const orc_run_cfg *cfg, orc_result *res, orc_log *log) {
+  memset(res, 0, sizeof(*res));
+  const uint32_t NR = prof->replicas ? prof->replicas : 1;
+  if (NR > ORC_MAX_REPLICAS || prof->prefill_mode || prof->kv_cap_words) return -1;
+  orc_request *req = (orc_request *)malloc((n_req ? n_req : 1) * sizeof(orc_request));
+  if (!req) return -1;
+  for (uint64_t i = 0; i < n_req; ++i) {
+    req[i] = req_words[i];
+    req[i].input = to_tokens(req_words[i].input, prof->tpw_q16);
+  }
+  res->first_act_s = res->last_deact_s = ORC_NONE;
+  res->t1 = ctrl->t1;
+  res->t2 = ctrl->t2;
+  const uint64_t H = (uint64_t)cfg->horizon_us;
+  int rc = -1;
+  const uint64_t nq1 = n_req ? n_req : 1;
+  rstate *rs = (rstate *)calloc(nq1, sizeof(rstate));
+  uint32_t *rep = (uint32_t *)calloc(nq1, sizeof(uint32_t)); /* the replica a request was assigned to */
+  uint32_t *queue = (uint32_t *)malloc(nq1 * sizeof(uint32_t));
+  uint32_t *ready = (uint32_t *)malloc(NR * nq1 * sizeof(uint32_t)); /* [replica][...] */
+  uint32_t *batch = (uint32_t *)malloc(NR * nq1 * sizeof(uint32_t));
+  uint64_t *e2e_v = (uint64_t *)malloc(nq1 * sizeof(uint64_t));
+  uint64_t *ttft_v = (uint64_t *)malloc(nq1 * sizeof(uint64_t));
+  uint64_t n_sec = H / US + 2;
+  uint64_t *sec_tbt_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_tbt_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_e2e_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_e2e_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_slo_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_ttft_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_ttft_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_in_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_in_any = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_util_sum = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  uint64_t *sec_util_cnt = (uint64_t *)calloc(n_sec, sizeof(uint64_t));
+  orc_second_row *rows = (cfg->record & 2) ? (orc_second_row *)calloc(n_sec, sizeof(orc_second_row)) : NULL;
+  heap h = {0, 0, 0};
+  cstate cs;
+  memset(&cs, 0, sizeof(cs));
+  cs.c = ctrl;
+  cs.law = ctrl->law;
+  cs.rt_min = ORC_NONE;
+  int busy[ORC_MAX_REPLICAS] = {0};
+  uint64_t n_ready[ORC_MAX_REPLICAS] = {0}, n_batch[ORC_MAX_REPLICAS] = {0}, in_rep[ORC_MAX_REPLICAS] = {0};
+  uint32_t rr = 0; /* round-robin pointer */
+  if (!rs || !rep || !queue || !ready || !batch || !e2e_v || !ttft_v || !sec_tbt_sum || !sec_tbt_cnt ||
+      !sec_e2e_sum || !sec_e2e_cnt || !sec_slo_cnt || !sec_ttft_sum || !sec_ttft_cnt || !sec_in_sum ||
+      !sec_in_any || !sec_util_sum || !sec_util_cnt || ((cfg->record & 2) && !rows))
+    goto out;
+  if (cs.law == ORC_LAW_CONST) cs.r = ctrl->r_const_bp;
+  for (uint64_t i = 0; i < n_req; ++i) {
+    rs[i].admit = rs[i].first = rs[i].done = NEVER;
+    if (heap_push(&h, (event){req[i].a_us, EV_ARRIVAL, (uint32_t)i, 0})) goto out;
+  }
+  uint64_t q_head = 0, q_tail = 0, in_sys = 0, n_e2e = 0, n_ttft = 0;
+  uint64_t next_sec = 0, T_prev = 0, last_T = 0, n_series = 0;
+
+#define COMPLETE(m, T, s_idx)                                                          \
+  do {                                                                                 \
+    uint64_t e2e_ = (T) - req[m].a_us;                                                 \
+    rs[m].done = (T);                                                                  \
+    rs[m].state = RS_DONE;                                                             \
+    in_sys--;                                                                          \
+    in_rep[rep[m]]--;                                                                  \
+    res->served++;                                                                     \
+    res->sum_e2e_us += e2e_;                                                           \
+    res->sum_sojourn_us += e2e_;                                                       \
+    e2e_v[n_e2e++] = e2e_;                                                             \
+    res->hist_e2e[orc_lat_bin(e2e_ / 1000)]++;                                         \
+    if (in_window((T), cfg)) res->win_served++;                                        \
+    sec_e2e_sum[s_idx] += e2e_;                                                        \
+    sec_e2e_cnt[s_idx] += 1;                                                           \
+    if (e2e_ > ctrl->slo_us) { sec_slo_cnt[s_idx] += 1; res->slo_violations++; }       \
+    if (rows) { rows[s_idx].completions++; rows[s_idx].sum_e2e_us += e2e_; }            \
+  } while (0)
+
+  for (;;) {
+    if (h.n == 0) break;
+    uint64_t T = h.v[0].t;
+    if (T >= H) break;
+    {
+      uint64_t dt = T - T_prev, nq = q_tail - q_head;
+      if (in_sys == 0) {
+        res->idle_us += dt;
+        res->win_idle_us += overlap(T_prev, T, cfg->w0_us, cfg->w1_us);
+        if (rows)
+          for (uint64_t s = T_prev / US; s * US < T && s < n_sec; ++s)
+            rows[s].idle_us += (uint32_t)overlap(T_prev, T, (int64_t)(s * US), (int64_t)((s + 1) * US));
+      }
+      res->int_system_us += (nq + in_sys) * dt;
+      res->int_queue_us += nq * dt;
+    }
+    T_prev = T;
+    last_T = T;
+    uint64_t s_idx = T / US;
+    while (h.n && h.v[0].t == T) {
+      event e = heap_pop(&h);
+      if (e.kind == EV_ITER_END) { /* E1 on replica e.idx */
+        const uint32_t q = e.idx;
+        uint32_t *bq = batch + (uint64_t)q * nq1;
+        sec_util_sum[s_idx] += n_batch[q];
+        sec_util_cnt[s_idx] += 1;
+        for (uint64_t b = 0; b < n_batch[q]; ++b) {
+          uint32_t m = bq[b];
+          uint64_t gap = T - rs[m].last_tok;
+          sec_tbt_sum[s_idx] += gap;
+          sec_tbt_cnt[s_idx] += 1;
+          res->tbt_samples++;
+          res->tbt_sum_us += gap;
+          if (gap > res->tbt_max_us) res->tbt_max_us = gap;
+          if (log && log->gaps && log->n_gaps < log->cap_gaps) {
+            log->gaps[2 * log->n_gaps] = m;
+            log->gaps[2 * log->n_gaps + 1] = gap;
+          }
+          if (log) log->n_gaps++;
+          rs[m].n_gaps++;
+          rs[m].last_tok = T;
+          rs[m].emitted++;
+          res->words_out++;
+          if (rows) {
+            rows[s_idx].tbt_count++;
+            rows[s_idx].sum_tbt_us += gap;
+            rows[s_idx].words_out++;
+          }
+          if (in_window(T, cfg)) res->win_words_out++;
+          if (rs[m].emitted == rs[m].R) {
+            COMPLETE(m, T, s_idx);
+          } else {
+            rs[m].state = RS_READY;
+            ready[(uint64_t)q * nq1 + n_ready[q]++] = m;
+          }
+        }
+        n_batch[q] = 0;
+        busy[q] = 0;
+      } else if (e.kind == EV_PREFILL_END) { /* E2: first word */
+        uint32_t m = e.idx;
+        uint64_t ttft = T - req[m].a_us;
+        rs[m].first = T;
+        rs[m].last_tok = T;
+        rs[m].emitted = 1;
+        res->words_out++;
+        if (in_window(T, cfg)) res->win_words_out++;
+        res->sum_ttft_us += ttft;
+        sec_ttft_sum[s_idx] += ttft;
+        sec_ttft_cnt[s_idx] += 1;
+        ttft_v[n_ttft++] = ttft;
+        res->hist_ttft[orc_lat_bin(ttft / 1000)]++;
+        if (rows) {
+          rows[s_idx].first_tokens++;
+          rows[s_idx].sum_ttft_us += ttft;
+          rows[s_idx].words_out++;
+        }
+        if (rs[m].R == 1) {
+          COMPLETE(m, T, s_idx);
+        } else {
+          rs[m].state = RS_READY;
+          ready[(uint64_t)rep[m] * nq1 + n_ready[rep[m]]++] = m;
+        }
+      } else { /* E3: arrival -> the central FIFO queue */
+        uint32_t m = e.idx;
+        rs[m].state = RS_QUEUED;
+        queue[q_tail++] = m;
+        res->arrivals++;
+        if (rows) rows[s_idx].arrivals++;
+        res->candidates = (uint64_t)req[m].j + 1;
+      }
+    }
+    int any_idle = 0;
+    for (uint32_t q = 0; q < NR; ++q) any_idle |= !busy[q];
+    if (!any_idle) continue;
+    INGEST_UNTIL(T);
+    while (q_head < q_tail) {
+      /* routing: a replica at an admission point with a free slot */
+      uint32_t q = NR;
+      if (prof->route == ORC_ROUTE_RR) {
+        for (uint32_t i = 0; i < NR && q == NR; ++i) {
+          uint32_t c = (rr + i) % NR;
+          if (!busy[c] && in_rep[c] < prof->max_batch) q = c;
+        }
+        if (q < NR) rr = (q + 1) % NR;
+      } else {
+        for (uint32_t c = 0; c < NR; ++c)
+          if (!busy[c] && in_rep[c] < prof->max_batch && (q == NR || in_rep[c] < in_rep[q])) q = c;
+      }
+      if (q == NR) break;
+      uint32_t m = queue[q_head++];
+      uint32_t r = cs.r;
+      int bypass = r > 0 && (((ctrl->bypass_mask >> req[m].cls) & 1u) || req[m].P < ctrl->min_words_bypass);
+      if (bypass) r = 0;
+      const uint32_t R_words = r > 0 ? bounded_realized(req[m].P, r, req[m].fcomp_q16, cfg->poly_q16) : req[m].U;
+      if (bypass) res->bypassed++;
+      rep[m] = q;
+      rs[m].admit = T;
+      rs[m].r_bp = r;
+      rs[m].R = to_tokens(R_words, prof->tpw_q16);
+      uint64_t pf = ((uint64_t)prof->prefill_ns_per_word * req[m].input) / 1000;
+      if (pf < 1) pf = 1;
+      rs[m].prefill_end = T + pf;
+      rs[m].state = RS_PREFILL;
+      in_sys++;
+      in_rep[q]++;
+      res->admitted++;
+      res->sum_queue_us += T - req[m].a_us;
+      res->words_in += req[m].input;
+      sec_in_sum[T / US] += req[m].input;
+      sec_in_any[T / US] = 1;
+      if (in_window(T, cfg)) res->win_words_in += req[m].input;
+      if (rows) {
+        rows[T / US].admitted++;
+        rows[T / US].sum_queue_us += T - req[m].a_us;
+        rows[T / US].words_in += req[m].input;
+      }
+      if (r > 0) {
+        res->rewritten++;
+        res->hist_r[r / 10 < ORC_HIST_R ? r / 10 : ORC_HIST_R - 1]++;
+      }
+      {
+        uint32_t sc = orc_similarity(req[m].U, R_words, r > 0, req[m].qnoise, cfg->quality);
+        uint32_t qb = sc / 50 < ORC_HIST_Q ? sc / 50 : ORC_HIST_Q - 1;
+        if (r > 0) { res->hist_q_active[qb]++; res->scored_active++; }
+        else { res->hist_q_inactive[qb]++; res->scored_inactive++; }
+      }
+      if (heap_push(&h, (event){rs[m].prefill_end, EV_PREFILL_END, m, 0})) goto out;
+    }
+    /* every replica at an admission point with decode-ready requests starts an iteration */
+    for (uint32_t q = 0; q < NR; ++q) {
+      if (busy[q] || n_ready[q] == 0) continue;
+      uint64_t K = 0;
+      uint32_t *bq = batch + (uint64_t)q * nq1;
+      for (uint64_t b = 0; b < n_ready[q]; ++b) {
+        uint32_t m = ready[(uint64_t)q * nq1 + b];
+        bq[b] = m;
+        rs[m].state = RS_DECODING;
+        K += req[m].input + rs[m].emitted;
+      }
+      n_batch[q] = n_ready[q];
+      n_ready[q] = 0;
+      uint64_t B = n_batch[q];
+      uint64_t d = prof->t0_us + (uint64_t)prof->slope_us * (B > prof->knee ? B - prof->knee : 0) +
+                   ((uint64_t)prof->kv_ns_per_word * K) / 1000;
+      if (heap_push(&h, (event){T + d, EV_ITER_END, q, 0})) goto out;
+      busy[q] = 1;
+      res->ticks++;
+    }
+  }
+#undef COMPLETE
+  uint64_t end = (cfg->mode == ORC_MODE_DRAIN && h.n == 0) ? last_T : H;
+  {
+    uint64_t dt = end - T_prev, nq = q_tail - q_head;
+    if (in_sys == 0) {
+      res->idle_us += dt;
+      res->win_idle_us += overlap(T_prev, end, cfg->w0_us, cfg->w1_us);
+      if (rows)
+        for (uint64_t s = T_prev / US; s * US < end && s < n_sec; ++s)
+          rows[s].idle_us += (uint32_t)overlap(T_prev, end, (int64_t)(s * US), (int64_t)((s + 1) * US));
+    }
+    res->int_system_us += (nq + in_sys) * dt;
+    res->int_queue_us += nq * dt;
+  }
+  res->end_us = end;
+  INGEST_UNTIL(end);
+  res->queued_end = q_tail - q_head;
+  res->inflight_end = in_sys;
+  if (res->queued_end + res->inflight_end > 0) res->flags |= ORC_FLAG_TRUNCATED;
+  finish_run(res, prof, e2e_v, n_e2e, ttft_v, n_ttft, rows, n_sec, end, n_series, rs, n_req, log);
+  rc = 0;
+out:
+  free(req); free(rs); free(rep); free(queue); free(ready); free(batch); free(e2e_v); free(ttft_v);
   free(sec_tbt_sum); free(sec_tbt_cnt); free(sec_e2e_sum); free(sec_e2e_cnt); free(sec_slo_cnt);
   free(sec_ttft_sum); free(sec_ttft_cnt); free(sec_in_sum); free(sec_in_any); free(sec_util_sum);
   free(sec_util_cnt);
@@ -1000,6 +1302,8 @@ static void scenario_cfg(const orc_inputs *in, uint64_t sid, orc_profile *p, orc
   p->prefill_mode = in->prof_prefill_mode[pi];
   p->kv_policy = in->prof_kv_policy[pi];
   p->tpw_q16 = in->prof_tpw[pi];
+  p->replicas = in->prof_replicas[pi];
+  p->route = in->prof_route[pi];
   memset(c, 0, sizeof(*c));
   c->law = in->ctrl_law[ci];
   c->signal = in->ctrl_signal[ci];

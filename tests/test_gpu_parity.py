@@ -202,7 +202,7 @@ def test_c5_full_size_stride64_and_strong_scaled_shard():
     torch.cuda.synchronize()
     sh = sim.stats_shard(5, 8)
     assert len(sh) == 131072
-    assert np.array_equal(sh.view(np.uint8), st[5::8].view(np.uint8))
+    assert np.array_equal(sh.view(np.uint8), np.ascontiguousarray(st[5::8]).view(np.uint8))
     sids = np.arange(5, w.n_scenarios, 64, dtype=np.uint64)
     rs = oracle.run_batch(oracle.Bound(cols), sids)
     bad = [(int(s), e) for s, o in zip(sids, rs) for e in [compare(sh[(int(s) - 5) // 8], o, int(s))] if e]

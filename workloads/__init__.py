@@ -337,6 +337,7 @@ class Workload:
             prof_prefill_mode=u32([p.get("prefill_mode", 0) for p in P]),
             prof_kv_policy=u32([p.get("kv_policy", 0) for p in P]),
             prof_tpw=u32([p.get("tpw_q16", 0) for p in P]),
+            prof_replicas=u32([p.get("replicas", 0) for p in P]), prof_route=u32([p.get("route", 0) for p in P]),
             ctrl_law=u32([c.law for c in C]), ctrl_signal=u32([c.signal for c in C]),
             ctrl_window=u32([c.window for c in C]), ctrl_rmin=u32([c.r_min_bp for c in C]),
             ctrl_rmax=u32([c.r_max_bp for c in C]), ctrl_rconst=u32([c.r_const_bp for c in C]),

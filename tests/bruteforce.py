@@ -339,3 +339,126 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
     return dict(admit=admit, first=first, done=done, R=R, r_bp=rbp, gaps=gaps, ticks=ticks,
                 words_out=words_out, end_us=end, served=sum(1 for s in st if s == "done"),
                 preemptions=preemptions, recompute_words=recompute_words, sum_queue_us=sum_queue)
+
+
+def simulate_replicas(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max=2000, window=5,
+                      r_const=0, rungs=(), horizon_s=0, w_lat=0, w_q=0, w_osc=0, step_bp=0):
+    """NEXT-4 multi-replica routing (reading R45), brute force: prof["replicas"]
+    engines of prof["max_batch"] slots share one FIFO queue.  At every instant
+    where something happened and some replica has no iteration running, the
+    closed seconds are ingested (TBT signal) and the arrived queue head goes to
+    an idle replica with a free slot, chosen least-loaded (fewest requests in
+    the replica, lowest index) or round robin (prof["route"] = 1); then every
+    idle replica with decode-ready requests starts an iteration.  Drain mode."""
+    tpw = prof.get("tpw_q16", 0)
+
+    def tok(w):
+        return w if not tpw else max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2)))
+
+    requests = [dict(q, input=tok(q["input"])) for q in requests]
+    n = len(requests)
+    NR = max(1, prof.get("replicas", 1))
+    st = ["future"] * n
+    rep = [None] * n
+    admit, pend, first, done, last = [None] * n, [None] * n, [None] * n, [None] * n, [None] * n
+    emitted, R, rbp = [0] * n, [0] * n, [0] * n
+    gaps = [[] for _ in range(n)]
+    queue = []
+    iter_end = [None] * NR
+    batch = [[] for _ in range(NR)]
+    rr = 0
+    ticks = 0
+    sec_sum, sec_cnt = {}, {}
+    ctl = _Law(law, t1, t2, r_min, r_max, window, rungs, horizon_s, w_lat, w_q, w_osc, step_bp)
+    r_cur = r_const if law == "const" else 0
+    ingested_upto = 0
+    last_event = 0
+    t = 0
+    while t < horizon_us:
+        anything = False
+        for q in range(NR):
+            if iter_end[q] == t:
+                anything = True
+                for m in batch[q]:
+                    g = t - last[m]
+                    gaps[m].append(g)
+                    sec_sum[t // 10**6] = sec_sum.get(t // 10**6, 0) + g
+                    sec_cnt[t // 10**6] = sec_cnt.get(t // 10**6, 0) + 1
+                    last[m] = t
+                    emitted[m] += 1
+                    if emitted[m] == R[m]:
+                        st[m], done[m] = "done", t
+                    else:
+                        st[m] = "ready"
+                batch[q] = []
+                iter_end[q] = None
+        for m in range(n):
+            if st[m] == "prefill" and pend[m] == t:
+                anything = True
+                first[m] = last[m] = t
+                emitted[m] = 1
+                if R[m] == 1:
+                    st[m], done[m] = "done", t
+                else:
+                    st[m] = "ready"
+        for m in range(n):
+            if st[m] == "future" and requests[m]["a_us"] == t:
+                anything = True
+                st[m] = "queued"
+                queue.append(m)
+        if anything:
+            last_event = t
+        idle = [q for q in range(NR) if iter_end[q] is None]
+        if anything and idle:
+            while (ingested_upto + 1) * 10**6 <= t:
+                s = ingested_upto
+                ingested_upto += 1
+                if sec_cnt.get(s, 0) and law in ("map", "step", "mpc", "bbr", "pcc"):
+                    r_cur = ctl.ingest(sec_sum[s] // sec_cnt[s], sec_cnt[s])
+            while queue:
+                load = {q: sum(1 for i in range(n) if rep[i] == q and st[i] in ("prefill", "ready", "decoding"))
+                        for q in idle}
+                ok = [q for q in idle if load[q] < prof["max_batch"]]
+                if not ok:
+                    break
+                if prof.get("route", 0) == 1:
+                    q = min(ok, key=lambda c: (c - rr) % NR)
+                    rr = (q + 1) % NR
+                else:
+                    q = min(ok, key=lambda c: (load[c], c))
+                m = queue.pop(0)
+                rep[m] = q
+                admit[m] = t
+                rbp[m] = r_cur
+                qq = requests[m]
+                if r_cur > 0:
+                    N = max(1, int(Fraction(qq.get("P", qq["U"])) * Fraction(10000 - r_cur, 10000) + Fraction(1, 2)))
+                    R[m] = max(1, int(Fraction(N) * Fraction(qq.get("fcomp_q16", 65536), 65536) + Fraction(1, 2)))
+                else:
+                    R[m] = qq["U"]
+                R[m] = tok(R[m])
+                pend[m] = t + max(1, prof["prefill_ns_per_word"] * qq["input"] // 1000)
+                st[m] = "prefill"
+            for q in idle:
+                mine = [m for m in range(n) if rep[m] == q and st[m] == "ready"]
+                if mine:
+                    B = len(mine)
+                    K = sum(requests[m]["input"] + emitted[m] for m in mine)
+                    d = prof["t0_us"] + prof["slope_us"] * max(0, B - prof["knee"]) + \
+                        prof.get("kv_ns_per_word", 0) * K // 1000
+                    for m in mine:
+                        st[m] = "decoding"
+                    batch[q] = mine
+                    iter_end[q] = t + d
+                    ticks += 1
+        t += 1
+        if all(s == "done" for s in st):
+            break
+        nxt = [e for e in iter_end if e is not None]
+        nxt += [pend[m] for m in range(n) if st[m] == "prefill"]
+        nxt += [requests[m]["a_us"] for m in range(n) if st[m] == "future"]
+        nxt = [x for x in nxt if x >= t]
+        t = min(nxt) if nxt else horizon_us
+    return dict(admit=admit, first=first, done=done, R=R, r_bp=rbp, gaps=gaps, ticks=ticks, rep=rep,
+                end_us=last_event if all(s == "done" for s in st) else horizon_us,
+                served=sum(1 for s in st if s == "done"))

@@ -158,14 +158,31 @@ typedef struct {
   /* NEXT-4 token-level costs (S:249 tokens_per_word; reading R44): tokens per
    * word in Q16, 0 = the engine counts words (SPEC's model).  Nonzero (16384 ..
    * 262144, i.e. 0.25 .. 4): a request's input and realized output of w words
-   * are max(1, floor((w tpw + 2^15) / 2^16)) tokens; the engine decodes one
+   * are clamp(floor((w tpw + 2^15) / 2^16), 1, 2^24) tokens; the engine decodes one
    * token per request per iteration (TBT gaps per token), and every per-unit
    * constant above and below (prefill and KV ns, KV capacity, energy, and the
    * words_in / words_out counters of the summary) is per token.  The rewrite
    * N and the similarity score stay in words.  Inputs must stay < 65536 tokens. */
   uint32_t tpw_q16;
   double e_in_j_per_word, e_out_j_per_word, p_idle_w;
-} bellman_profile; /* 64 bytes */
+  /* NEXT-4 multi-replica routing ("picks requests from the arrival
+   * queue and assigns to GPU servers"; reading R45): `replicas` engines (0 or
+   * 1 = one, <= 8) of max_batch slots each (replicas x max_batch <= 64) share
+   * the FIFO arrival queue.  At an instant where some replica has no iteration
+   * running, the arrived queue head is assigned to such a replica with a free
+   * slot chosen by `route`: BELLMAN_ROUTE_LEAST (fewest requests in the
+   * replica, ties to the lowest index) or BELLMAN_ROUTE_RR (the first at or
+   * after a cyclic pointer, which then moves past it); each replica iterates
+   * its own batch under the cost law above; every replica's words feed the
+   * controller's signal; idle = the whole node empty.  replicas > 1 requires
+   * prefill_mode 0 and kv_cap_words 0. */
+  uint32_t replicas;
+  uint32_t route;
+} bellman_profile; /* 72 bytes */
+
+#define BELLMAN_MAX_REPLICAS 8u
+#define BELLMAN_ROUTE_LEAST 0u
+#define BELLMAN_ROUTE_RR 1u
 
 #define BELLMAN_PREFILL_NONBLOCKING 0u
 #define BELLMAN_PREFILL_CONTENDING 1u

@@ -529,11 +529,12 @@ static void finish_run(orc_result *res, const orc_profile *prof, uint64_t *e2e_v
 
 /* NEXT-4 token-level costs ("tokens_per_word"; reading R44): with
  * tpw_q16 != 0 the engine works in tokens — a count of w words is
- * max(1, round(w tpw)) tokens (half-up, Q16) — and every per-unit constant of
+ * clamp(round(w tpw), 1, 2^24) tokens (half-up, Q16) — and every per-unit constant of
  * the profile (prefill and KV ns, KV capacity, energy per unit) is per token. */
 static uint32_t to_tokens(uint32_t words, uint32_t tpw_q16) {
   if (tpw_q16 == 0) return words;
   uint64_t t = ((uint64_t)words * tpw_q16 + (1u << 15)) >> 16;
+  if (t > (1u << 24)) t = 1u << 24; /* the realized-length bound (R11) holds in tokens too */
   return t < 1 ? 1u : (uint32_t)t;
 }
 

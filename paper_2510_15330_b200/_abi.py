@@ -27,7 +27,8 @@ TRACE = np.dtype([("knot_offset", "<u4"), ("n_knots", "<u4"), ("arrival_cap", "<
 ARRIVAL = np.dtype([("a_us", "<i8"), ("L_words", "<u4"), ("input_words", "<u4"), ("cls", "<u4"), ("_pad", "<u4")])
 PROFILE = np.dtype([("t0_us", "<u4"), ("knee", "<u4"), ("slope_us", "<u4"), ("kv_ns_per_word", "<u4"),
                     ("max_batch", "<u4"), ("prefill_ns_per_word", "<u4"), ("kv_cap_words", "<u4"), ("prefill_mode", "<u4"),
-                    ("kv_policy", "<u4"), ("tpw_q16", "<u4"), ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8")])
+                    ("kv_policy", "<u4"), ("tpw_q16", "<u4"), ("e_in_j_per_word", "<f8"), ("e_out_j_per_word", "<f8"), ("p_idle_w", "<f8"),
+                    ("replicas", "<u4"), ("route", "<u4")])
 CTRL = np.dtype([(n, "<u4") for n in ("law", "signal", "window", "r_min_bp", "r_max_bp", "r_const_bp", "t1", "t2",
                                        "slo_us", "calibrated", "n_rungs")] + [("rungs_bp", "<u4", (8,))] +
                 [("bypass_mask", "<u4"), ("min_words_bypass", "<u4")] +
@@ -54,7 +55,7 @@ CTRL_ROW = np.dtype([("second", "<u4"), ("sample", "<u4"), ("k", "<u4"), ("r_bp"
 RECORD_SIGNAL, RECORD_SECONDS = 0x1, 0x2
 assert SECOND_ROW.itemsize == 64 and CTRL_ROW.itemsize == 32
 assert ARRIVAL.itemsize == 24
-assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 64
+assert KNOT.itemsize == 16 and TRACE.itemsize == 16 and PROFILE.itemsize == 72
 assert CTRL.itemsize == 104 and SCENARIO.itemsize == 64 and STATS.itemsize == 272
 
 

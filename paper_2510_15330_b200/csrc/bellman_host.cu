@@ -148,6 +148,14 @@ static bellman_status validate(const bellman_sim_desc *d) {
     if (p.prefill_mode == BELLMAN_PREFILL_CONTENDING &&
         (uint64_t)p.max_batch * ((uint64_t)p.prefill_ns_per_word * 65535u / 1000u + 1u) >= (1ull << 30))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: contending prefill: max_batch x max prefill >= 2^30 us", i);
+    if (p.replicas > BELLMAN_MAX_REPLICAS) return fail(nullptr, BELLMAN_EINVAL, "profile %u: replicas > 8", i);
+    if (p.route > BELLMAN_ROUTE_RR) return fail(nullptr, BELLMAN_EINVAL, "profile %u: unknown route", i);
+    if (p.replicas > 1u) {
+      if (p.replicas * p.max_batch > BELLMAN_MAX_BATCH)
+        return fail(nullptr, BELLMAN_EINVAL, "profile %u: replicas x max_batch > 64", i);
+      if (p.prefill_mode != BELLMAN_PREFILL_NONBLOCKING || p.kv_cap_words != 0u)
+        return fail(nullptr, BELLMAN_EINVAL, "profile %u: replicas > 1 needs prefill_mode 0 and no KV capacity", i);
+    }
     if (p.tpw_q16 != 0u && (p.tpw_q16 < 16384u || p.tpw_q16 > 262144u))
       return fail(nullptr, BELLMAN_EINVAL, "profile %u: tpw_q16 not 0 or in 16384..262144 (0.25..4 tokens/word)", i);
     if (p.tpw_q16 != 0u) {  // inputs are 16-bit token counts on the device

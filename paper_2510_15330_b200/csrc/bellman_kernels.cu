@@ -310,12 +310,13 @@ __device__ __noinline__ uint4 leap_wide(uint32_t lane, uint32_t cb, uint32_t q, 
 }
 
 // prefill duration of a request with `in` input words (R6): >= 1 µs
-// NEXT-4 token-level costs (R44): w words are max(1, round(w tpw)) tokens
-// (half-up, Q16); tpw = 0 keeps words
+// NEXT-4 token-level costs (R44): w words are clamp(round(w tpw), 1, 2^24)
+// tokens (half-up, Q16; the realized-length bound of R11 holds in tokens too);
+// tpw = 0 keeps words
 __device__ __forceinline__ uint32_t to_tokens(uint32_t w, uint32_t tpw) {
   if (tpw == 0u) return w;
-  const uint32_t t = (uint32_t)(((uint64_t)w * tpw + (1u << 15)) >> 16);
-  return t < 1u ? 1u : t;
+  const uint64_t t = ((uint64_t)w * tpw + (1u << 15)) >> 16;
+  return t < 1u ? 1u : (t > (1u << 24) ? (1u << 24) : (uint32_t)t);
 }
 
 __device__ __forceinline__ uint32_t prefill_us(uint32_t pf_ns, uint32_t in) {
@@ -854,6 +855,12 @@ struct Sim {
   uint64_t sa[2];
   uint32_t sp[2];
   uint32_t sR[2], sin[2], sdn[2], sph[2];
+  // NEXT-4 multi-replica path (R45; generic instantiation only): the replica
+  // of each slot; lane q < nrep holds replica q's iteration end (INF32 idle);
+  // sdn counts a slot's words emitted there and sp its last word's instant
+  uint32_t srep[2];
+  uint32_t re;
+  uint32_t nrep, route, rrp;
   // ---- generator / queue head (a2)
   uint32_t buf_h, buf_n;  // consumed / filled entries of the shared arrival buffer
   uint32_t pmode;         // NEXT-4 prefill_mode (generic instantiation only)
@@ -940,6 +947,7 @@ struct Sim {
     if (sec_bound != INF32) sec_bound -= D;
     sp[0] -= D;
     sp[1] -= D;
+    if (!TBTO && nrep > 1u && re != INF32) re -= D;
     head_t = buf_h < buf_n ? rel(cold().q[buf_h].a) : INF32;
     Hr = rel(cold().H);
     update_window();
@@ -1463,6 +1471,251 @@ struct Sim {
     if (DBG) __syncwarp();
   }
 
+
+  // ------------------------------------------------------------------ NEXT-4 multi-replica (R45)
+  // P:130 "the request scheduler ... picks requests from the arrival queue and
+  // assigns to GPU servers": nrep engines share the FIFO queue.  A plain
+  // event-at-a-time loop (no leaping): per-replica state is lane-distributed,
+  // per-slot state as in the single engine; the controller, window, epoch,
+  // generator, counters and epilogue are the single engine's.
+
+  // words of the iteration ends of the replicas in endm (a5): every decoding
+  // slot of such a replica emits a word; a slot reaching its R completes
+  __device__ __forceinline__ void multi_end(uint32_t endm, WarpHist &h) {
+    const uint32_t Tn = T;
+    const uint64_t Ta = ab(Tn);
+    uint64_t gap_l = 0, e2e_l = 0;
+    uint32_t nw = 0, ndone = 0, nslo = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (sph[s] == PH_DEC && ((endm >> srep[s]) & 1u)) {
+        gap_l += Tn - sp[s];  // 32-bit offsets: exact modulo 2^32
+        sp[s] = Tn;
+        sdn[s]++;
+        nw++;
+        if (sdn[s] == sR[s]) {
+          const uint64_t e = Ta - sa[s];
+          e2e_l += e;
+          nslo += e > slo_us;
+          ndone++;
+          atomicAdd(&h.e2e[lat_bin_us(e)], 1u);
+          sph[s] = PH_EMPTY;
+        } else {
+          sph[s] = PH_READY;
+        }
+      }
+    }
+    const uint32_t W = __reduce_add_sync(FULL, nw);
+    const uint64_t G = warp_sum_split(gap_l);
+    words_out += W;
+    if (win_now) win_words_out += W;
+    if (sig(BELLMAN_SIG_TBT)) {
+      acc_sum += G;
+      acc_cnt += W;
+    } else if (sig(BELLMAN_SIG_UTIL)) {  // one sample per replica iteration end: its batch size
+      acc_sum += W;
+      acc_cnt += (uint32_t)__popc(endm);
+    }
+    if (DBG && dbg && lane == 0) {
+      bellman_second_row *w = row(Ta);
+      atomicAdd(&w->tbt_count, W);
+      atomicAdd(&w->words_out, W);
+      atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)G);
+    }
+    if (DBG) __syncwarp();
+    const uint32_t nd = __reduce_add_sync(FULL, ndone);
+    if (nd) {
+      const uint64_t se = warp_sum_split(e2e_l);
+      const uint32_t ns = __reduce_add_sync(FULL, nslo);
+      cadd(CT_SERVED, nd);
+      cadd(CT_SUM_E2E, se);
+      cadd(CT_SLO_VIOL, ns);
+      if (win_now) cadd(CT_WIN_SERVED, nd);
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Ta)->completions, nd);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_e2e_us, (unsigned long long)se);
+      }
+      if (DBG) __syncwarp();
+      in_sys -= nd;
+      complete_sig(se, nd, ns);
+    }
+    if ((endm >> lane) & 1u) re = INF32;
+  }
+
+  // admission point of the replicas without a running iteration (R45): the
+  // arrived queue head goes to one of them with a free slot, by the routing
+  // policy; rewrite, similarity and accounting as in admit()
+  __device__ __forceinline__ void multi_admit(const Params &p, WarpHist &h) {
+    const uint32_t Tn = T;
+    const uint64_t Ta = ab(Tn);
+    const uint32_t slots_per = maxb;
+    uint32_t n = 0, n_byp = 0;
+    while (head_t <= Tn) {
+      // requests in each replica (lane q keeps replica q's count)
+      uint32_t load = 0;
+      for (uint32_t q = 0; q < nrep; ++q) {
+        const bool a0 = sph[0] != PH_EMPTY && sph[0] != PH_OFF && srep[0] == q;
+        const bool a1 = sph[1] != PH_EMPTY && sph[1] != PH_OFF && srep[1] == q;
+        const uint32_t c = (uint32_t)(__popc(__ballot_sync(FULL, a0)) + __popc(__ballot_sync(FULL, a1)));
+        if (lane == q) load = c;
+      }
+      const bool el = lane < nrep && re == INF32 && load < slots_per;
+      const uint32_t em = __ballot_sync(FULL, el);
+      if (em == 0u) break;
+      uint32_t q;
+      if (route == BELLMAN_ROUTE_RR) {
+        const uint32_t hi = em & (0xFFFFFFFFu << rrp);
+        q = (uint32_t)__ffs(hi ? hi : em) - 1u;
+        rrp = q + 1u == nrep ? 0u : q + 1u;
+      } else {  // least loaded, ties to the lowest index
+        q = __reduce_min_sync(FULL, el ? (load << 3) | lane : 0xFFFFFFFFu) & 7u;
+      }
+      const QEnt &e = cold().q[buf_h];
+      const uint64_t a = e.a;
+      const uint32_t inc = e.in, Uq = e.U, P = e.P, fcq = e.fcq;
+      const uint32_t in = inc & 0xFFFFu, U = Uq & 0xFFFFFFu;
+      const bool byp = r > 0 && (inc >> 31);
+      const uint32_t ra = byp ? 0u : r;
+      uint32_t R = U, qb = Uq >> 24;
+      if (ra > 0) {
+        R = realized_len(p, U, P, fcq, ra);
+        int32_t base;
+        const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
+        if (num <= (int64_t)p.q_safe * den) {
+          base = (int32_t)p.q_active;
+        } else if (num >= (int64_t)p.q_end * den) {
+          base = (int32_t)p.q_floor;
+        } else {
+          base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
+                           (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
+        }
+        int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+        qb = (uint32_t)sc / 50u;
+      }
+      R = to_tokens(R, cold().tpw);
+      n_byp += byp;
+      cadd(CT_REWRITTEN, ra > 0 ? 1u : 0u);
+      if (lane == 0) {
+        if (ra > 0) atomicAdd(&h.r[ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1], 1u);
+        atomicAdd(ra > 0 ? &h.qa[qb] : &h.qi[qb], 1u);
+      }
+      const uint32_t pf = e.pf;
+      const uint32_t f0 = __ballot_sync(FULL, sph[0] == PH_EMPTY), f1 = __ballot_sync(FULL, sph[1] == PH_EMPTY);
+      const bool s1 = f0 == 0u;
+      const uint32_t sl = (uint32_t)__ffs(s1 ? f1 : f0) - 1u;
+      if (lane == sl) {  // explicit rows: a runtime index would put the slot arrays in local memory
+        if (!s1) {
+          sa[0] = a;
+          sp[0] = Tn + pf;
+          sR[0] = R;
+          sin[0] = in;
+          sdn[0] = 1u;  // the first word (at the prefill end) is certain
+          srep[0] = q;
+          sph[0] = PH_PREFILL;
+        } else {
+          sa[1] = a;
+          sp[1] = Tn + pf;
+          sR[1] = R;
+          sin[1] = in;
+          sdn[1] = 1u;
+          srep[1] = q;
+          sph[1] = PH_PREFILL;
+        }
+      }
+      if (Tn + pf < next_pf) next_pf = Tn + pf;
+      cadd(CT_WORDS_IN, in);
+      if (win_now) cadd(CT_WIN_WORDS_IN, in);
+      cadd(CT_SUM_QUEUE, Ta - a);
+      if (sig(BELLMAN_SIG_INPUT)) {
+        acc_sum += in;
+        acc_cnt = 1u;
+      }
+      if (DBG && dbg && lane == 0) {
+        atomicAdd(&row(Ta)->admitted, 1u);
+        atomicAdd(&row(Ta)->words_in, in);
+        atomicAdd((unsigned long long *)&row(Ta)->sum_queue_us, (unsigned long long)(Ta - a));
+      }
+      n++;
+      in_sys++;
+      last_j = e.j + 1u;
+      if (++buf_h < buf_n) {
+        head_t = rel(cold().q[buf_h].a);
+      } else if (!cold().gen_done) {
+        refill(p);
+      } else {
+        head_t = INF32;
+      }
+    }
+    cadd(CT_ADMITTED, n);
+    if (n_byp) {
+      if (lane == 0) cold().bypassed += n_byp;
+      __syncwarp();
+    }
+    if (DBG) __syncwarp();
+  }
+
+  // every replica without a running iteration and with decode-ready slots starts
+  // one with all of them: d = t0 + slope max(0, B - knee) + floor(kv K / 1000)
+  __device__ __forceinline__ void multi_start() {
+    const uint32_t Tn = T;
+    const uint32_t idle = __ballot_sync(FULL, lane < nrep && re == INF32);
+    for (uint32_t q = 0; q < nrep; ++q) {
+      if (!((idle >> q) & 1u)) continue;
+      uint32_t b = 0;
+      uint64_t kadd = 0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (sph[s] == PH_READY && srep[s] == q) {
+          sph[s] = PH_DEC;
+          b++;
+          kadd += (uint64_t)sin[s] + sdn[s];
+        }
+      }
+      const uint32_t Bq = __reduce_add_sync(FULL, b);
+      if (Bq == 0u) continue;
+      const uint64_t K = warp_sum_split(kadd);
+      const uint64_t d = (uint64_t)t0 + (uint64_t)slope * (Bq > knee ? Bq - knee : 0u) + (uint64_t)kv * K / 1000u;
+      if (lane == q) re = Tn + (uint32_t)d;
+      ticks++;
+    }
+  }
+
+  // the multi-replica event loop; returns true when no event remains (drained)
+  __device__ __forceinline__ bool multi_loop(const Params &p, WarpHist &h) {
+    for (;;) {
+      uint32_t tn = __reduce_min_sync(FULL, lane < nrep ? re : INF32);
+      if (next_pf < tn) tn = next_pf;
+      // an arrival matters only where a replica could take it at once
+      uint32_t load = 0;
+      for (uint32_t q = 0; q < nrep; ++q) {
+        const bool a0 = sph[0] != PH_EMPTY && sph[0] != PH_OFF && srep[0] == q;
+        const bool a1 = sph[1] != PH_EMPTY && sph[1] != PH_OFF && srep[1] == q;
+        const uint32_t c = (uint32_t)(__popc(__ballot_sync(FULL, a0)) + __popc(__ballot_sync(FULL, a1)));
+        if (lane == q) load = c;
+      }
+      if (__ballot_sync(FULL, lane < nrep && re == INF32 && load < maxb) && head_t < tn) tn = head_t;
+      if (tn == INF32) return true;
+      if (tn > kJumpCap) tn = kJumpCap;  // a far event: jump to the cap first; advance() rebases
+      if (tn >= Hr) return false;
+      if (in_sys == 0) {  // idle interval [T, tn) (R18)
+        cadd(CT_IDLE, tn - T);
+        const uint64_t a = ab(T), b = ab(tn);
+        const uint64_t lo = a > cold().w0 ? a : cold().w0, hi = b < cold().w1 ? b : cold().w1;
+        if (hi > lo) cadd(CT_WIN_IDLE, hi - lo);
+        dbg_idle(a, b);
+      }
+      advance(tn);  // rolls closed seconds into the controller (R21), window, epoch
+      tn = T;
+      const uint32_t endm = __ballot_sync(FULL, lane < nrep && re == tn);
+      if (endm) multi_end(endm, h);
+      if (next_pf == tn) prefill_end(h, tn + 1u);
+      if (__ballot_sync(FULL, lane < nrep && re == INF32) == 0u) continue;  // no replica at an admission point
+      if (head_t <= tn) multi_admit(p, h);
+      multi_start();
+    }
+  }
+
   // ------------------------------------------------------------------ a4/a5 leap
   // Execute in bulk the longest run of iterations whose ends are uneventful —
   // no completion (index < next_done), no prefill end, no admission (head
@@ -1767,12 +2020,18 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   S.kstep_q = S.kstep_r = 0;
   S.batch_changed();
   S.update_window();
+  // NEXT-4 multi-replica routing (R45): replicas x max_batch slots (generic instantiation)
+  S.nrep = (!TBTO && pr.replicas > 1u) ? pr.replicas : 1u;
+  S.route = pr.route;
+  S.rrp = 0;
+  S.re = INF32;
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     S.sa[s] = S.sp[s] = 0;
     S.sR[s] = S.sin[s] = S.sdn[s] = 0;
-    // slots beyond max_batch are never free
-    S.sph[s] = (lane + 32u * s < S.maxb) ? PH_EMPTY : PH_OFF;
+    S.srep[s] = 0;
+    // slots beyond max_batch (x replicas) are never free
+    S.sph[s] = (lane + 32u * s < S.maxb * S.nrep) ? PH_EMPTY : PH_OFF;
   }
   S.buf_h = S.buf_n = 0;
   S.pmode = pr.prefill_mode;
@@ -1806,7 +2065,11 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   const long long loop0_ = clock64();
 #endif
   bool finished = false;
+  if constexpr (!TBTO) {
+    if (S.nrep > 1u) finished = S.multi_loop(p, h);
+  }
   for (;;) {
+    if (!TBTO && S.nrep > 1u) break;  // the multi-replica loop ran above
     uint32_t tn;
     // a prefill end strictly inside the running iteration only emits first
     // words / R=1 completions (time-stamped at p): its trip does nothing
@@ -2079,7 +2342,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
-               (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0)) {
+               (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0) &&
+               p.profs[sc.profile].replicas <= 1u) {
       // TBT-only loop, specialised once more on a KV-free cost law (kv = 0)
       if (p.profs[sc.profile].kv_ns_per_word == 0)
         run_one<false, true, true>(p, sid, sc, cc, lane, h);

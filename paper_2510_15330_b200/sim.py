@@ -53,7 +53,8 @@ def pack(cols: dict, pinned: bool = False) -> dict:
     for f, c in (("t0_us", "prof_t0"), ("knee", "prof_knee"), ("slope_us", "prof_slope"),
                  ("kv_ns_per_word", "prof_kv"), ("max_batch", "prof_maxb"),
                  ("prefill_ns_per_word", "prof_prefill_ns"), ("kv_cap_words", "prof_kv_cap"), ("prefill_mode", "prof_prefill_mode"),
-                 ("kv_policy", "prof_kv_policy"), ("tpw_q16", "prof_tpw"),
+                 ("kv_policy", "prof_kv_policy"), ("tpw_q16", "prof_tpw"), ("replicas", "prof_replicas"),
+                 ("route", "prof_route"),
                  ("e_in_j_per_word", "prof_e_in"),
                  ("e_out_j_per_word", "prof_e_out"), ("p_idle_w", "prof_p_idle")):
         profs[:npf][f] = cols[c]

@@ -128,7 +128,7 @@ def simulate(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=500, r_max
     tpw = prof.get("tpw_q16", 0)
 
     def tok(w):  # NEXT-4 token-level costs (R44): round-half-up w * tpw, at least 1
-        return w if not tpw else max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2)))
+        return w if not tpw else min(1 << 24, max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2))))
 
     requests = [dict(q, input=tok(q["input"])) for q in requests]  # the engine counts input tokens
     n = len(requests)
@@ -353,7 +353,7 @@ def simulate_replicas(requests, prof, horizon_us, law="off", t1=0, t2=0, r_min=5
     tpw = prof.get("tpw_q16", 0)
 
     def tok(w):
-        return w if not tpw else max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2)))
+        return w if not tpw else min(1 << 24, max(1, int(Fraction(w * tpw, 65536) + Fraction(1, 2))))
 
     requests = [dict(q, input=tok(q["input"])) for q in requests]
     n = len(requests)

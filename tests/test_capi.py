@@ -144,3 +144,26 @@ def test_next3_law_validation():
     for c, msg in bad:
         with pytest.raises(A.BellmanError, match=msg):
             sim.workspace_bytes(sim.pack(cols(c)))
+
+
+def test_replica_validation():
+    """NEXT-4 multi-replica profiles: <= 8 replicas, replicas x max_batch <= 64,
+    known route, non-blocking prefill and no KV capacity."""
+    from paper_2510_15330_b200 import _abi as A, sim
+    import workloads as W
+
+    def cols(**prof):
+        c = W.config_c2(n_seeds=1, rates=[1.0]).columns()
+        for k, v in prof.items():
+            c[k] = c[k].copy()
+            c[k][0] = v
+        return c
+
+    assert sim.workspace_bytes(sim.pack(cols(prof_replicas=8, prof_maxb=8, prof_knee=1))) > 0
+    for kw, msg in ((dict(prof_replicas=9, prof_maxb=4, prof_knee=1), "replicas > 8"),
+                    (dict(prof_replicas=2, prof_maxb=33, prof_knee=1), "replicas x max_batch > 64"),
+                    (dict(prof_replicas=2, prof_maxb=8, prof_knee=1, prof_route=2), "unknown route"),
+                    (dict(prof_replicas=2, prof_maxb=8, prof_knee=1, prof_prefill_mode=1), "needs prefill_mode 0"),
+                    (dict(prof_replicas=2, prof_maxb=8, prof_knee=1, prof_kv_cap=10_000), "needs prefill_mode 0")):
+        with pytest.raises(A.BellmanError, match=msg):
+            sim.workspace_bytes(sim.pack(cols(**kw)))

@@ -611,3 +611,60 @@ def test_next4_token_level_costs():
     bad, st = check_all(W.custom(traces, profs, ctrls, sc).columns())
     _assert_ok(bad)
     assert int(st["served"].sum()) > 1000
+
+
+def _replicas_workload():
+    """NEXT-4 multi-replica routing (reading R45): 2-8 replicas sharing
+    the arrival queue under both routing policies, light to heavy load, with
+    token costs, every controller family, the UTIL / E2E / TTFT signals and a
+    replayed trace; every fifth scenario debug-recorded."""
+    T13 = round(1.3 * 65536)
+    traces = [W.paper_trace(), W.const_trace(4.0, 300), W.const_trace(9.0, 120), W.paper_trace(3.5, 180, 0.6),
+              {"replay": [(int(k * 250_000), 300 + 7 * k % 500, 1000 + 37 * k % 9000, k % 3) for k in range(400)]}]
+    profs = [dict(W.PROFILES["P24"], replicas=2, max_batch=32, route=0),
+             dict(W.PROFILES["P24"], replicas=4, max_batch=16, route=1),
+             dict(W.PROFILES["P24"], replicas=8, max_batch=8, knee=0, route=0),
+             dict(W.PROFILES["L8B"], replicas=3, max_batch=21, route=1, tpw_q16=T13),
+             dict(W.PROFILES["L8B"], replicas=2, max_batch=4, route=0),
+             dict(W.PROFILES["P24"], replicas=5, max_batch=1, knee=1, route=1)]
+    ctrls = [W.OFF, W.map_ctrl(24_000, 40_000), W.mpc_ctrl(24_000), W.bbr_ctrl(3_000), W.pcc_ctrl(24_000),
+             W.map_ctrl(5000, 9000, signal=W.SIG_UTIL, window=3), W.map_ctrl(6_000_000, 20_000_000, signal=W.SIG_E2E),
+             W.step_ctrl(500_000, 900_000, (500, 1000, 2000), signal=W.SIG_TTFT)]
+    sc = []
+    k = 0
+    for ti in range(len(traces)):
+        for pi in range(len(profs)):
+            for ci in range(len(ctrls)):
+                if (ti * 7 + pi * 3 + ci) % 2:
+                    continue
+                mode = (ti + pi + ci) % 2
+                rec = 2 if k % 5 == 0 else 0
+                sc.append(W.Scenario(k % 13, wid=ti, trace=ti, profile=pi, ctrl=ci, segment=0, mode=mode,
+                                     horizon_us=(1500 if mode else 700) * W.US, record=rec))
+                k += 1
+    return W.custom(traces, profs, ctrls, sc)
+
+
+def test_next4_multi_replica_routing():
+    """GPU parity of the multi-replica path: every summary field and histogram,
+    and for debug-recorded scenarios the per-second rows and controller log."""
+    import torch
+
+    from paper_2510_15330_b200 import Simulator
+
+    w = _replicas_workload()
+    cols = w.columns()
+    bad, st = check_all(cols)
+    _assert_ok(bad)
+    assert int(st["ticks"].sum()) > 10**5 and int(st["rewritten"].sum()) > 0
+    sim = Simulator(cols)
+    sim.run()
+    torch.cuda.synchronize()
+    b = oracle.Bound(cols)
+    for sid in [i for i, s in enumerate(w.scenarios) if s.record & 2]:
+        o = oracle.run_scenario(b, sid, rows_cap=100000, ctrl_log_cap=100000)
+        rows, ctrl = sim.series(sid)
+        for f in o["rows"].dtype.names:
+            assert np.array_equal(rows[f].astype(np.int64), o["rows"][f].astype(np.int64)), (sid, f)
+        assert [tuple(int(g[k]) for k in ("second", "sample", "k", "r_bp", "active", "A")) for g in ctrl] == \
+               [(e["second"], e["sample"], e["k"], e["r_bp"], e["active"], e["A"]) for e in o["ctrl_log"]], sid

@@ -1386,7 +1386,7 @@ struct Sim {
         sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
         qb = (uint32_t)sc / 50u;
       }
-      R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
+      if (!TBTO) R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
       const uint32_t kvcap = cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
@@ -2343,8 +2343,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
                (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0) &&
-               p.profs[sc.profile].replicas <= 1u) {
-      // TBT-only loop, specialised once more on a KV-free cost law (kv = 0)
+               p.profs[sc.profile].replicas <= 1u && p.profs[sc.profile].tpw_q16 == 0u) {
+      // TBT-only loop (one replica, words: no token conversion at admission),
+      // specialised once more on a KV-free cost law (kv = 0)
       if (p.profs[sc.profile].kv_ns_per_word == 0)
         run_one<false, true, true>(p, sid, sc, cc, lane, h);
       else

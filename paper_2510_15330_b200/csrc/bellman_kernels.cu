@@ -198,12 +198,6 @@ struct alignas(16) Cold {
   uint32_t bypass_mask, min_words, bypassed;  // NEXT-3
   uint32_t kv_cap;                            // NEXT-4 KV capacity in context words (0 = none)
   uint32_t pf_ns;                             // prefill ns per input word (token, tpw != 0)
-  uint32_t tpw;                               // NEXT-4 tokens per word Q16, 0 = words (R44)
-  // NEXT-3 MPC / BBR / PCC (P:213) parameters and state (ingest_ext only)
-  uint32_t hz, wlat, wq, wosc, step;          // horizon s, cost weights, step / delta bp
-  uint32_t rt_min, phase, rbase;              // BBR RTprop; PCC phase and r_base
-  uint64_t cost_a;                            // PCC: cost of the pair's first experiment
-  uint32_t wring[8];                          // BBR: decode words of the window's seconds
   // KV-free cost law: floor((2^32 - 1) / cost(B)) for B = 0..max_batch, filled
   // lane-parallel at scenario start; the leap divides by cost(B) with it
   uint32_t cbm_tab[68];
@@ -211,7 +205,13 @@ struct alignas(16) Cold {
   // entry i written by lane i at refill, read whole (two 16-byte broadcasts)
   // by every lane at admission
   QEnt q[32];
-
+  // round 2 additions, after the hot fields (their offsets unchanged)
+  uint32_t tpw;                               // NEXT-4 tokens per word Q16, 0 = words (R44)
+  // NEXT-3 MPC / BBR / PCC (P:213) parameters and state (ingest_ext only)
+  uint32_t hz, wlat, wq, wosc, step;          // horizon s, cost weights, step / delta bp
+  uint32_t rt_min, phase, rbase;              // BBR RTprop; PCC phase and r_base
+  uint64_t cost_a;                            // PCC: cost of the pair's first experiment
+  uint32_t wring[8];                          // BBR: decode words of the window's seconds
 };
 static_assert(offsetof(Cold, ringA) == 0 && offsetof(Cold, rung) == 16 && offsetof(Cold, first_act) == 32 &&
                   offsetof(Cold, t1) == 48 && offsetof(Cold, series) == 64 && offsetof(Cold, ring) == 80,
@@ -679,7 +679,7 @@ __device__ __noinline__ uint32_t ingest_ext(uint32_t wid, uint32_t lane, uint64_
 // runs once per simulated second, so it stays out of the event loop's
 // instruction-cache footprint.  All lanes compute; only lane 0 writes the
 // shared-memory state.
-template <bool DBG>
+template <bool DBG, bool EXT = true>
 __device__ __forceinline__ uint32_t ingest_body(uint32_t wid, uint32_t lane, uint64_t sec_bound, uint64_t acc_sum,
                                                uint32_t acc_cnt, uint32_t r_cur, bool dbg, uint32_t util_maxb) {
   Cold &c = g_cold[kWarpsPerBlock == 1 ? 0u : wid];
@@ -703,7 +703,7 @@ __device__ __forceinline__ uint32_t ingest_body(uint32_t wid, uint32_t lane, uin
   }
   const uint32_t law = g2.z, window = g2.w;
   if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP)
-    return law >= BELLMAN_LAW_MPC ? ingest_ext<DBG>(wid, lane, sec_bound, x, acc_cnt, r_cur, dbg) : r_cur;
+    return (EXT && law >= BELLMAN_LAW_MPC) ? ingest_ext<DBG>(wid, lane, sec_bound, x, acc_cnt, r_cur, dbg) : r_cur;
   const uint32_t pos = g0.w, t1 = g3.x, was_active = g1.y;
   uint32_t k = g0.z, rung = g1.x;
   uint64_t A = (uint64_t)g0.x | ((uint64_t)g0.y << 32);
@@ -892,8 +892,8 @@ struct Sim {
   __device__ __forceinline__ void ingest() {
     // the TBT loops take the controller inline (C5's paper-trace scenarios
     // ingest every second of long quiet stretches); the others call it
-    if (TBTO && !DBG)
-      r = ingest_body<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
+    if (TBTO && !DBG)  // the TBT loops run MAP / STEP / CONST / OFF only (no ingest_ext call site)
+      r = ingest_body<DBG, false>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
     else
       r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,
                            sig(BELLMAN_SIG_UTIL) ? maxb : 0u);
@@ -2343,8 +2343,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
                (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0) &&
-               p.profs[sc.profile].replicas <= 1u && p.profs[sc.profile].tpw_q16 == 0u) {
-      // TBT-only loop (one replica, words: no token conversion at admission),
+               p.profs[sc.profile].replicas <= 1u && p.profs[sc.profile].tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC) {
+      // TBT-only loop (one replica, words: no token conversion at admission;
+      // MAP / STEP / CONST / OFF: no NEXT-3 law call site),
       // specialised once more on a KV-free cost law (kv = 0)
       if (p.profs[sc.profile].kv_ns_per_word == 0)
         run_one<false, true, true>(p, sid, sc, cc, lane, h);

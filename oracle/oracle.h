@@ -20,9 +20,15 @@
  * (neglog), Decimal log2 table, SPEC worked examples, hand fixtures F1-F6
  * (tests/golden/), a brute-force microsecond-stepping simulator on tiny
  * traces, M/D/1 Pollaczek-Khinchine, the uncongested-regime bound, the
- * sample-path Little's law identity, controller law vs exact rationals.
- * "parity unpinned": the paper's directional outcomes (A4) and the saturation
- * capacity of P24/L8B (calibration outputs), see DESIGN.md §6.
+ * sample-path Little's law identity, controller law vs exact rationals;
+ * round 2: hand-worked controller sequences for STEP / MAP / MPC / BBR / PCC
+ * (tests/golden/controller_sequences.json), E2E / SLO signals and the
+ * transition log recomputed from the request / controller logs, histogram
+ * percentiles bracketing the exact nearest-rank values, token costs (S:207 in
+ * tokens, identities), multi-replica routing (one replica == orc_simulate, a
+ * hand-worked two-replica timeline, brute force), the A3 saturation brackets.
+ * "parity unpinned": the paper's directional outcomes (A4) and the exact
+ * saturation capacity of P24/L8B (calibration outputs), see DESIGN.md §6.
  */
 #ifndef BELLMAN_ORACLE_H
 #define BELLMAN_ORACLE_H

@@ -65,6 +65,9 @@ def _edge_workload():
         dict(W.PROFILES["P24"], max_batch=32, knee=32), dict(W.PROFILES["P24"], max_batch=33, knee=7),
         dict(W.PROFILES["L8B"], max_batch=63, kv_ns_per_word=900),
         dict(W.PROFILES["P24"], prefill_ns_per_word=0, t0_us=1, slope_us=0),  # 1 µs prefills, 1 µs iterations
+        dict(W.PROFILES["P24"], replicas=8, max_batch=8, route=0),         # round 2: all 64 slots in replicas
+        dict(W.PROFILES["L8B"], replicas=7, max_batch=9, knee=3, route=1),  # 63 slots, ragged
+        dict(W.PROFILES["P24"], replicas=2, max_batch=1, knee=0, prefill_ns_per_word=0, t0_us=1, slope_us=0),
     ]
     ctrls = [
         W.OFF,
@@ -400,12 +403,13 @@ def _long_workload():
     rep = [(0, 500, 9000, 0), (3 * US, 800, 4000, 1), (3 * US + (1 << 33), 600, 9000, 2),
            (4 * US + (1 << 33), 700, 12000, 0)]  # 2^33 µs between arrivals
     traces = [gap_trace, sparse, overload, {"replay": rep}]
-    profs = [W.PROFILES["P24"], W.PROFILES["L8B"], dict(W.PROFILES["L8B"], kv_cap_words=300_000)]
+    profs = [W.PROFILES["P24"], W.PROFILES["L8B"], dict(W.PROFILES["L8B"], kv_cap_words=300_000),
+             dict(W.PROFILES["P24"], replicas=3, max_batch=8, route=1)]  # round 2: replica ends across rebases
     ctrls = [W.OFF, W.map_ctrl(30_000, 60_000), W.map_ctrl(5_000_000, 900_000_000, signal=W.SIG_E2E, window=3),
              W.Ctrl(W.LAW_CONST, W.SIG_TBT, 5, 500, 2000, 1500)]
     sc = []
     for t in range(4):
-        for pi in range(3):
+        for pi in range(4):
             for ci in range(4):
                 for H, mode in ((11_000 * US, W.MODE_CUTOFF), (20_000 * US, W.MODE_DRAIN), (1 << 40, t % 2)):
                     rec = 2 if (H == 11_000 * US and ci == 1 and pi == 0) else 0

@@ -305,10 +305,16 @@ def outputs(st_all, seg_hist, n_segments):
         return edge(int(np.searchsorted(np.cumsum(h), k)))
 
     h = seg_hist[:, :896].sum(axis=0)
+    seg = st_all["segment"].astype(np.int64)
+    served = np.bincount(seg, weights=st_all["served"].astype(np.float64), minlength=n_segments)
+    energy = np.bincount(seg, weights=st_all["energy_j"], minlength=n_segments)
+    per_seg = [[g, nr(seg_hist[g, :896], 50), nr(seg_hist[g, :896], 99), int(served[g]), round(float(energy[g]), 1)]
+               for g in range(n_segments)]
     return {"e2e_p50_ms": nr(h, 50), "e2e_p99_ms": nr(h, 99), "served": int(st_all["served"].sum()),
             "energy_j": float(st_all["energy_j"].sum()), "win_energy_j": float(st_all["win_energy_j"].sum()),
-            "note": f"job totals over {len(st_all)} scenarios / {n_segments} segments; p50/p99 = lower edge of the "
-                    "merged E2E histogram bin holding the nearest rank (R13)"}
+            "segments": {"columns": ["segment", "e2e_p50_ms", "e2e_p99_ms", "served", "energy_j"], "rows": per_seg},
+            "note": f"job totals over {len(st_all)} scenarios / {n_segments} segments, and per segment; p50/p99 = "
+                    "lower edge of the merged E2E histogram bin holding the nearest rank (R13)"}
 
 
 def main():

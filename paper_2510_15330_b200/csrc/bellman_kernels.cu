@@ -1387,7 +1387,7 @@ struct Sim {
         qb = (uint32_t)sc / 50u;
       }
       if (!TBTO) R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
-      const uint32_t kvcap = cold().kv_cap;
+      const uint32_t kvcap = TBTO ? 0u : cold().kv_cap;  // the TBT loops run capacity-free profiles only
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
         // the contexts in the system; an oversized head enters an empty system.
@@ -2342,10 +2342,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
-               (p.profs[sc.profile].kv_policy != BELLMAN_KV_PREEMPT || p.profs[sc.profile].kv_cap_words == 0) &&
+               p.profs[sc.profile].kv_cap_words == 0 &&
                p.profs[sc.profile].replicas <= 1u && p.profs[sc.profile].tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC) {
-      // TBT-only loop (one replica, words: no token conversion at admission;
-      // MAP / STEP / CONST / OFF: no NEXT-3 law call site),
+      // TBT-only loop (one replica, no KV capacity, words: no token conversion
+      // at admission; MAP / STEP / CONST / OFF: no NEXT-3 law call site),
       // specialised once more on a KV-free cost law (kv = 0)
       if (p.profs[sc.profile].kv_ns_per_word == 0)
         run_one<false, true, true>(p, sid, sc, cc, lane, h);

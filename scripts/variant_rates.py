@@ -2,7 +2,9 @@
 scenarios, the same traces, seeds and controller grid), one launch each:
 the TBT-specialised KV-free loop (C5 as is), the generic loop (token costs),
 the NEXT-3 laws (MPC / BBR / PCC instead of the grid), and the multi-replica
-loop (4 replicas x 16 slots, least loaded).  Prints ticks/s per variant."""
+loop (4 replicas x 16 slots, least loaded).  Prints ticks/s per variant and
+the roofline fraction bench.py would report for it (SURVEY 8(d) algorithmic
+warp-instructions / kernel time / the nominal issue peak at 1965 MHz)."""
 import json
 import os
 import sys
@@ -14,6 +16,8 @@ import torch  # noqa: E402
 
 import workloads as W  # noqa: E402
 from paper_2510_15330_b200 import Simulator  # noqa: E402
+
+import bench  # noqa: E402  (the algorithmic-work formula of the bench line)
 
 
 def variant(name):
@@ -36,7 +40,7 @@ def variant(name):
 
 def main():
     out = {}
-    names = sys.argv[1:] or ["c5_as_is", "tokens", "next3_laws", "replicas4x16"]
+    names = sys.argv[1:] or ["c5_as_is", "tokens", "map_generic", "mpc", "bbr", "pcc", "replicas4x16"]
     for name in names:
         w = variant(name)
         sim = Simulator(w.columns())
@@ -49,8 +53,12 @@ def main():
             torch.cuda.synchronize()
             t = a.elapsed_time(b)
             best = t if best is None else min(best, t)
-        ticks = int(sim.stats()["ticks"].astype(np.int64).sum())
-        out[name] = {"ms": round(best, 2), "ticks": ticks, "ticks_per_s": ticks / (best / 1e3)}
+        st = sim.stats()
+        ticks = int(st["ticks"].astype(np.int64).sum())
+        ops = bench.algorithmic_ops(st)  # SURVEY 8(d) per-unit counts x units, as bench.py
+        peak = 148 * 4 * 1965e6  # nominal issue peak, warp-inst/s (bench.py's roofline denominator)
+        out[name] = {"ms": round(best, 2), "ticks": ticks, "ticks_per_s": ticks / (best / 1e3),
+                     "roofline_frac": ops / (best / 1e3) / peak}
         sim.close()
         print(name, out[name], flush=True)
     print(json.dumps(out))

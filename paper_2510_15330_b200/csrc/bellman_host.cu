@@ -25,8 +25,10 @@ struct bellman_sim {
   int grid = 0;
   uint32_t last_launches = 0;
   Params params{};
-  unsigned int *counters = nullptr;  // [4]: one per launch of a run
+  unsigned int *counters = nullptr;  // [8]: one per launch of a run
   bool has_dbg = false;
+  bool has_multi = false;            // a scenario whose profile has replicas > 1, not debug-recorded
+  bool has_multi_dbg = false;        // ... debug-recorded (the multi-replica kernels)
   std::vector<uint8_t> calibrated;   // per scenario: ctrl is calibrated
   std::vector<uint32_t> calib_src;
   std::vector<uint32_t> dbg_slot;    // per scenario: debug-record slot or NONE
@@ -389,7 +391,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dn = take(sizeof(uint32_t) * 2 * nd);
   L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
   L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
-  L.off_cnt = take(sizeof(unsigned int) * 4);
+  L.off_cnt = take(sizeof(unsigned int) * 8);
   L.zero_end = o;
   // written by the kernels before they are read
   L.off_series = take(sizeof(uint32_t) * h.series_words);
@@ -529,6 +531,11 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   sim->host_order = h.order;
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
+  for (uint64_t k = 0; k < desc->n_scenarios; ++k)
+    if (desc->profiles[desc->scenarios[k].profile].replicas > 1u) {
+      if (desc->scenarios[k].record & BELLMAN_RECORD_SECONDS) sim->has_multi_dbg = true;
+      else sim->has_multi = true;
+    }
   sim->dbg_off = h.dbg_off;
   sim->dbg_cap = h.dbg_cap;
 
@@ -635,32 +642,41 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
 #ifdef BELLMAN_AB_NOORDER
   P.order = nullptr;
 #endif
-  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 4 * sizeof(unsigned int), s));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 8 * sizeof(unsigned int), s));
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
   sim->last_launches = 0;
   // pass 1: non-calibrated scenarios (product kernel; debug-recorded ones in the DBG kernel)
-  P.pass = 1;
-  P.counter = sim->counters;
-  CUDA_TRY(sim, bellman_launch_tick(P, grid, false, s));
-  sim->last_launches++;
-  if (sim->has_dbg) {
-    P.counter = sim->counters + 1;
-    CUDA_TRY(sim, bellman_launch_tick(P, grid, true, s));
+  // one launch per kernel with work: product, debug-record, multi-replica (plain, debug)
+  auto pass = [&](uint32_t pass_no, unsigned int *ctr) -> bellman_status {
+    P.pass = pass_no;
+    P.counter = ctr;
+    CUDA_TRY(sim, bellman_launch_tick(P, grid, false, false, s));
     sim->last_launches++;
-  }
+    if (sim->has_dbg) {  // some debug-recorded scenario exists (its one-replica ones run here)
+      P.counter = ctr + 1;
+      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, false, s));
+      sim->last_launches++;
+    }
+    if (sim->has_multi) {
+      P.counter = ctr + 2;
+      CUDA_TRY(sim, bellman_launch_tick(P, grid, false, true, s));
+      sim->last_launches++;
+    }
+    if (sim->has_multi_dbg) {
+      P.counter = ctr + 3;
+      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, true, s));
+      sim->last_launches++;
+    }
+    return BELLMAN_OK;
+  };
+  bellman_status rc = pass(1, sim->counters);
+  if (rc != BELLMAN_OK) return rc;
   if (any_cal) {  // a10: calibration, then pass 2 over the calibrated scenarios
     CUDA_TRY(sim, bellman_launch_calibrate(P, sim->n_slots, s));
     sim->last_launches++;
-    P.pass = 2;
-    P.counter = sim->counters + 2;
-    CUDA_TRY(sim, bellman_launch_tick(P, grid, false, s));
-    sim->last_launches++;
-    if (sim->has_dbg) {
-      P.counter = sim->counters + 3;
-      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, s));
-      sim->last_launches++;
-    }
+    rc = pass(2, sim->counters + 4);
+    if (rc != BELLMAN_OK) return rc;
   }
   return BELLMAN_OK;
 }

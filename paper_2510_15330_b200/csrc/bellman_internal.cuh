@@ -96,6 +96,6 @@ struct Params {
 }  // namespace bellman
 
 // launchers (bellman_kernels.cu)
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream);
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, bool multi, cudaStream_t stream);
 cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream);
 int bellman_tick_grid(int device);

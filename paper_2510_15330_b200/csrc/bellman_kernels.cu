@@ -1681,6 +1681,90 @@ struct Sim {
     }
   }
 
+  // Bulk-execute every replica's uneventful iteration ends (KV-free cost law:
+  // a replica's iterations then last d_q = t0 + slope max(0, B_q - knee) until
+  // its batch changes).  The next real event bounds the run: a prefill end, a
+  // window / horizon / second boundary, the queue head's arrival while some
+  // replica has a free slot, and per replica its first completion end (or its
+  // next end if it holds decode-ready requests: they join there).  Every
+  // replica's ends strictly before that instant are executed in closed form:
+  // B_q words each, the TBT gaps (first gap of each slot from its last word,
+  // then d_q), ticks (each end starts the next iteration), window and signal
+  // accumulators; the instant itself is then an ordinary trip.
+  __device__ __forceinline__ void multi_leap() {
+    if (kv != 0u) return;
+    uint32_t stop = next_pf < stop_static ? next_pf : stop_static;
+    if (sec_bound < stop) stop = sec_bound;
+    if (kJumpCap < stop) stop = kJumpCap;
+    uint32_t Bq = 0, mq = 0xFFFFFFFFu, load = 0;
+    for (uint32_t q = 0; q < nrep; ++q) {
+      const bool d0 = sph[0] == PH_DEC && srep[0] == q, d1 = sph[1] == PH_DEC && srep[1] == q;
+      const bool r0 = sph[0] == PH_READY && srep[0] == q, r1 = sph[1] == PH_READY && srep[1] == q;
+      const bool i0 = sph[0] != PH_EMPTY && sph[0] != PH_OFF && srep[0] == q;
+      const bool i1 = sph[1] != PH_EMPTY && sph[1] != PH_OFF && srep[1] == q;
+      const uint32_t b = (uint32_t)(__popc(__ballot_sync(FULL, d0)) + __popc(__ballot_sync(FULL, d1)));
+      const uint32_t nr = (uint32_t)(__popc(__ballot_sync(FULL, r0)) + __popc(__ballot_sync(FULL, r1)));
+      const uint32_t ld = (uint32_t)(__popc(__ballot_sync(FULL, i0)) + __popc(__ballot_sync(FULL, i1)));
+      uint32_t m = 0xFFFFFFFFu;
+      if (d0) m = sR[0] - sdn[0];
+      if (d1) m = min(m, sR[1] - sdn[1]);
+      m = __reduce_min_sync(FULL, m);
+      if (lane == q) {
+        Bq = b;
+        mq = nr ? 1u : m;
+        load = ld;
+      }
+    }
+    if (__ballot_sync(FULL, lane < nrep && load < maxb) && head_t < stop) stop = head_t;
+    const bool run = lane < nrep && re != INF32 && Bq > 0u;
+    const uint32_t dq = run ? t0 + slope * (Bq > knee ? Bq - knee : 0u) : 1u;
+    uint32_t creal = INF32;
+    if (run) {
+      const uint64_t c = (uint64_t)re + (uint64_t)(mq - 1u) * dq;
+      creal = c < INF32 ? (uint32_t)c : INF32;
+    }
+    const uint32_t cm = __reduce_min_sync(FULL, creal);
+    if (cm < stop) stop = cm;
+    uint32_t n = 0;
+    if (run && re < stop) n = (stop - 1u - re) / dq + 1u;  // ends re, re + d, ... before stop
+    const uint32_t nt = __reduce_add_sync(FULL, n);
+    if (nt == 0u) return;
+    uint64_t gap_l = 0;
+    uint32_t nw = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const uint32_t nq = __shfl_sync(FULL, n, (int)srep[s]);
+      const uint32_t ds = __shfl_sync(FULL, dq, (int)srep[s]);
+      const uint32_t rs = __shfl_sync(FULL, re, (int)srep[s]);
+      if (sph[s] == PH_DEC && nq) {
+        gap_l += (uint64_t)(rs - sp[s]) + (uint64_t)(nq - 1u) * ds;  // 32-bit offsets: exact modulo 2^32
+        sp[s] = rs + (nq - 1u) * ds;
+        sdn[s] += nq;
+        nw += nq;
+      }
+    }
+    const uint32_t W = __reduce_add_sync(FULL, nw);
+    const uint64_t G = warp_sum_split(gap_l);
+    if (run) re += n * dq;
+    ticks += nt;
+    words_out += W;
+    if (win_now) win_words_out += W;
+    if (sig(BELLMAN_SIG_TBT)) {
+      acc_sum += G;
+      acc_cnt += W;
+    } else if (sig(BELLMAN_SIG_UTIL)) {
+      acc_sum += W;
+      acc_cnt += nt;
+    }
+    if (DBG && dbg && lane == 0) {  // every leaped end lies in the open second
+      bellman_second_row *w = row(ab(sec_bound) - kUs);
+      atomicAdd(&w->tbt_count, W);
+      atomicAdd(&w->words_out, W);
+      atomicAdd((unsigned long long *)&w->sum_tbt_us, (unsigned long long)G);
+    }
+    if (DBG) __syncwarp();
+  }
+
   // the multi-replica event loop; returns true when no event remains (drained)
   __device__ __forceinline__ bool multi_loop(const Params &p, WarpHist &h) {
     for (;;) {
@@ -1710,9 +1794,11 @@ struct Sim {
       const uint32_t endm = __ballot_sync(FULL, lane < nrep && re == tn);
       if (endm) multi_end(endm, h);
       if (next_pf == tn) prefill_end(h, tn + 1u);
-      if (__ballot_sync(FULL, lane < nrep && re == INF32) == 0u) continue;  // no replica at an admission point
-      if (head_t <= tn) multi_admit(p, h);
-      multi_start();
+      if (__ballot_sync(FULL, lane < nrep && re == INF32) != 0u) {  // some replica at an admission point
+        if (head_t <= tn) multi_admit(p, h);
+        multi_start();
+      }
+      multi_leap();
     }
   }
 
@@ -1904,8 +1990,9 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 }
 
 // One scenario, a1-a9.  TBTO: the scenario's signal is TBT (compile-time
-// specialisation of every signal test in the event loop).
-template <bool DBG, bool TBTO, bool KV0 = false>
+// specialisation of every signal test in the event loop).  MULTI: a
+// multi-replica profile (NEXT-4, R45), run by multi_loop in its own kernel.
+template <bool DBG, bool TBTO, bool KV0 = false, bool MULTI = false>
 __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, const bellman_scenario &sc,
                                         const bellman_ctrl &cc, const uint32_t lane, WarpHist &h) {
   // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
@@ -2021,7 +2108,7 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   S.batch_changed();
   S.update_window();
   // NEXT-4 multi-replica routing (R45): replicas x max_batch slots (generic instantiation)
-  S.nrep = (!TBTO && pr.replicas > 1u) ? pr.replicas : 1u;
+  S.nrep = MULTI ? pr.replicas : 1u;
   S.route = pr.route;
   S.rrp = 0;
   S.re = INF32;
@@ -2065,11 +2152,9 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   const long long loop0_ = clock64();
 #endif
   bool finished = false;
-  if constexpr (!TBTO) {
-    if (S.nrep > 1u) finished = S.multi_loop(p, h);
-  }
-  for (;;) {
-    if (!TBTO && S.nrep > 1u) break;  // the multi-replica loop ran above
+  if constexpr (MULTI) {
+    finished = S.multi_loop(p, h);
+  } else for (;;) {
     uint32_t tn;
     // a prefill end strictly inside the running iteration only emits first
     // words / R=1 completions (time-stamped at p): its trip does nothing
@@ -2317,7 +2402,11 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   __syncwarp();
 }
 
-template <bool DBG>
+// DBG: the debug-record instantiation; MULTI: the multi-replica kernels.  Each
+// scenario runs in exactly one of product <0,0>, debug <1,0>, multi-replica
+// <0,1> and multi-replica debug <1,1>, so the product kernel carries neither
+// the debug hooks nor the multi-replica loop.
+template <bool DBG, bool MULTI = false>
 #ifndef BELLMAN_MIN_BLOCKS
 #define BELLMAN_MIN_BLOCKS (16 / BELLMAN_WPB)
 #endif
@@ -2333,17 +2422,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     const bellman_scenario sc = p.sc[sid];
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
     if ((cc.calibrated != 0) != (p.pass == 2)) continue;
-    // debug-recorded scenarios run in the DBG instantiation, all others in the product one
+    if ((p.profs[sc.profile].replicas > 1u) != MULTI) continue;
+    // debug-recorded scenarios run in the DBG instantiations, all others in the product ones
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
 
 #ifdef BELLMAN_PROFILE_COUNTERS
     if (lane == 0 && sid < (1u << 16)) g_span[2 * sid] = gtimer();
 #endif
-    if constexpr (DBG) {
+    if constexpr (MULTI) {
+      run_one<DBG, false, false, true>(p, sid, sc, cc, lane, h);
+    } else if constexpr (DBG) {
       run_one<true, false>(p, sid, sc, cc, lane, h);
     } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
                p.profs[sc.profile].kv_cap_words == 0 &&
-               p.profs[sc.profile].replicas <= 1u && p.profs[sc.profile].tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC) {
+               p.profs[sc.profile].tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC) {
       // TBT-only loop (one replica, no KV capacity, words: no token conversion
       // at admission; MAP / STEP / CONST / OFF: no NEXT-3 law call site),
       // specialised once more on a KV-free cost law (kv = 0)
@@ -2419,8 +2511,12 @@ int bellman_tick_grid(int device) {
   return g;
 }
 
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, cudaStream_t stream) {
-  if (dbg)
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, bool multi, cudaStream_t stream) {
+  if (multi && dbg)
+    bellman::bellman_tick_kernel<true, true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
+  else if (multi)
+    bellman::bellman_tick_kernel<false, true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
+  else if (dbg)
     bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
   else
     bellman::bellman_tick_kernel<false><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);

@@ -351,11 +351,41 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
     h.slot_cap.push_back((uint32_t)cap);
     h.series_words += cap;
   }
-  std::vector<double> cost(d->n_scenarios);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) cost[s] = expected_arrivals(d, d->scenarios[s]);
+  // heavy-first order: a stable sort by decreasing expected arrivals.  The cost
+  // depends only on (trace, horizon), so it is evaluated once per distinct pair,
+  // and the order is a stable counting sort over the distinct costs (large sets
+  // have few: C5's 2^20 scenarios have 16)
+  std::vector<uint32_t> rank(d->n_scenarios);
+  std::vector<double> costs;  // distinct costs, in first-seen order
+  {
+    std::unordered_map<uint64_t, uint32_t> memo;  // (trace << 44 | horizon) -> index into costs
+    for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+      const bellman_scenario &sc = d->scenarios[s];
+      const uint64_t key = ((uint64_t)sc.trace << 44) | (uint64_t)sc.horizon_us;  // horizon <= 2^43 (validated)
+      auto it = memo.find(key);
+      if (it == memo.end()) {
+        it = memo.emplace(key, (uint32_t)costs.size()).first;
+        costs.push_back(expected_arrivals(d, sc));
+      }
+      rank[s] = it->second;
+    }
+  }
+  std::vector<uint32_t> by_cost(costs.size());  // distinct cost indices by decreasing cost
+  for (uint32_t i = 0; i < by_cost.size(); ++i) by_cost[i] = i;
+  std::sort(by_cost.begin(), by_cost.end(), [&](uint32_t a, uint32_t b) { return costs[a] > costs[b]; });
+  // equal costs (from different (trace, horizon) pairs) share one group, so ids
+  // of equal cost keep their id order (the stable sort's tie rule)
+  std::vector<uint32_t> group(costs.size());
+  uint32_t ng = 0;
+  for (uint32_t i = 0; i < by_cost.size(); ++i) {
+    if (i && costs[by_cost[i]] != costs[by_cost[i - 1]]) ng++;
+    group[by_cost[i]] = ng;
+  }
+  std::vector<uint64_t> next(costs.empty() ? 0 : ng + 2, 0);
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) next[group[rank[s]] + 1]++;
+  for (uint32_t g = 1; g < next.size(); ++g) next[g] += next[g - 1];
   h.order.resize(d->n_scenarios);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) h.order[s] = (uint32_t)s;
-  std::stable_sort(h.order.begin(), h.order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+  for (uint64_t s = 0; s < d->n_scenarios; ++s) h.order[next[group[rank[s]]]++] = (uint32_t)s;
 }
 
 static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
@@ -545,13 +575,17 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     return t;
   }();
   {
-    // every input region assembled in one pageable staging buffer laid out like
-    // the workspace's input prefix, then one H2D copy and one memset
-    std::vector<uint8_t> stage(L.in_end, 0);
+    // the scenario table (64 B per scenario, the one large input) is copied
+    // straight from the caller's array (a DMA when it is pinned); every other
+    // input region is assembled in one pageable staging buffer laid out like
+    // the rest of the workspace's input prefix: two H2D copies and one memset
+    static_assert(sizeof(bellman_scenario) == 64, "scenario record");
+    const size_t base = L.off_tr;  // the staging buffer starts here (off_sc = 0 precedes it)
+    std::vector<uint8_t> stage(L.in_end - base);
+    std::memset(stage.data(), 0, stage.size());
     auto put = [&](size_t off, const void *src, size_t bytes) {
-      if (bytes) std::memcpy(stage.data() + off, src, bytes);
+      if (bytes) std::memcpy(stage.data() + (off - base), src, bytes);
     };
-    put(L.off_sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios);
     put(L.off_tr, h.traces.data(), sizeof(DevTrace) * h.traces.size());
     put(L.off_seg, h.segs.data(), sizeof(DevSeg) * h.segs.size());
     put(L.off_prof, desc->profiles, sizeof(bellman_profile) * desc->n_profiles);
@@ -570,9 +604,13 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     put(L.off_arr, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
     put(L.off_ord, h.order.data(), sizeof(uint32_t) * desc->n_scenarios);
     auto body = [&]() -> bellman_status {
-      CUDA_TRY(nullptr, cudaMemcpyAsync(ws, stage.data(), L.in_end, cudaMemcpyHostToDevice, s));
+      if (desc->n_scenarios)
+        CUDA_TRY(nullptr, cudaMemcpyAsync(ws + L.off_sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios,
+                                          cudaMemcpyHostToDevice, s));
+      CUDA_TRY(nullptr, cudaMemcpyAsync(ws + base, stage.data(), L.in_end - base, cudaMemcpyHostToDevice, s));
       CUDA_TRY(nullptr, cudaMemsetAsync(ws + L.zero_beg, 0, L.zero_end - L.zero_beg, s));
-      CUDA_TRY(nullptr, cudaStreamSynchronize(s));  // the staging buffer is freed on return
+      CUDA_TRY(nullptr, cudaStreamSynchronize(s));  // the staging buffer is freed on return (and the
+                                                    // caller's scenario array may be reused)
       return BELLMAN_OK;
     };
     const bellman_status rc = body();

@@ -27,4 +27,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tick
   > $o/${tag}_ncu_C5sub.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tick_kernel --launch-skip 3 --launch-count 1 -f \
   -o $o/${tag}_C2 python bench.py --workload C2 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-peak > $o/${tag}_ncu_C2.log 2>&1
+
+bash scripts/sanitize.sh > $o/${tag}_sanitizer.txt 2>&1; grep -E "ERROR SUMMARY|RACECHECK SUMMARY" $o/${tag}_sanitizer.txt
 echo done

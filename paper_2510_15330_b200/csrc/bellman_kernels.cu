@@ -1681,9 +1681,9 @@ struct Sim {
     }
   }
 
-  // Bulk-execute every replica's uneventful iteration ends (KV-free cost law:
-  // a replica's iterations then last d_q = t0 + slope max(0, B_q - knee) until
-  // its batch changes).  The next real event bounds the run: a prefill end, a
+  // Bulk-execute every replica's uneventful iteration ends: with a fixed batch,
+  // a replica's k-th next iteration lasts t0 + slope max(0, B_q - knee) +
+  // floor(kv (K_q + k B_q) / 1000) (closed form when kv = 0, stepped otherwise).  The next real event bounds the run: a prefill end, a
   // window / horizon / second boundary, the queue head's arrival while some
   // replica has a free slot, and per replica its first completion end (or its
   // next end if it holds decode-ready requests: they join there).  Every
@@ -1692,11 +1692,10 @@ struct Sim {
   // then d_q), ticks (each end starts the next iteration), window and signal
   // accumulators; the instant itself is then an ordinary trip.
   __device__ __forceinline__ void multi_leap() {
-    if (kv != 0u) return;
     uint32_t stop = next_pf < stop_static ? next_pf : stop_static;
     if (sec_bound < stop) stop = sec_bound;
     if (kJumpCap < stop) stop = kJumpCap;
-    uint32_t Bq = 0, mq = 0xFFFFFFFFu, load = 0;
+    uint32_t Bq = 0, mq = 0xFFFFFFFFu, load = 0, Kq = 0;
     for (uint32_t q = 0; q < nrep; ++q) {
       const bool d0 = sph[0] == PH_DEC && srep[0] == q, d1 = sph[1] == PH_DEC && srep[1] == q;
       const bool r0 = sph[0] == PH_READY && srep[0] == q, r1 = sph[1] == PH_READY && srep[1] == q;
@@ -1705,28 +1704,63 @@ struct Sim {
       const uint32_t b = (uint32_t)(__popc(__ballot_sync(FULL, d0)) + __popc(__ballot_sync(FULL, d1)));
       const uint32_t nr = (uint32_t)(__popc(__ballot_sync(FULL, r0)) + __popc(__ballot_sync(FULL, r1)));
       const uint32_t ld = (uint32_t)(__popc(__ballot_sync(FULL, i0)) + __popc(__ballot_sync(FULL, i1)));
-      uint32_t m = 0xFFFFFFFFu;
-      if (d0) m = sR[0] - sdn[0];
-      if (d1) m = min(m, sR[1] - sdn[1]);
+      uint32_t m = 0xFFFFFFFFu, k = 0;
+      if (d0) {
+        m = sR[0] - sdn[0];
+        k += sin[0] + sdn[0];
+      }
+      if (d1) {
+        m = min(m, sR[1] - sdn[1]);
+        k += sin[1] + sdn[1];
+      }
       m = __reduce_min_sync(FULL, m);
+      if (kv) k = __reduce_add_sync(FULL, k);  // context words of the running iteration (<= 2^31)
       if (lane == q) {
         Bq = b;
         mq = nr ? 1u : m;
         load = ld;
+        Kq = k;
       }
     }
     if (__ballot_sync(FULL, lane < nrep && load < maxb) && head_t < stop) stop = head_t;
     const bool run = lane < nrep && re != INF32 && Bq > 0u;
-    const uint32_t dq = run ? t0 + slope * (Bq > knee ? Bq - knee : 0u) : 1u;
+    const uint32_t cb = run ? t0 + slope * (Bq > knee ? Bq - knee : 0u) : 1u;
+    // iteration k >= 1 after the running one: context K + k B, length cb + floor(kv (K + k B) / 1000)
+    auto dur = [&](uint32_t k) -> uint32_t {
+      return cb + (uint32_t)((uint64_t)kv * ((uint64_t)Kq + (uint64_t)k * Bq) / 1000u);
+    };
+    // this replica's completion end (its mq-th end from now) bounds everyone
     uint32_t creal = INF32;
     if (run) {
-      const uint64_t c = (uint64_t)re + (uint64_t)(mq - 1u) * dq;
-      creal = c < INF32 ? (uint32_t)c : INF32;
+      if (kv == 0u) {
+        const uint64_t c = (uint64_t)re + (uint64_t)(mq - 1u) * cb;
+        creal = c < INF32 ? (uint32_t)c : INF32;
+      } else {  // step through the ends before the static bound
+        uint32_t e = re, k = 0;
+        while (k + 1u < mq && e < stop) {
+          k++;
+          e += dur(k);
+        }
+        if (k + 1u == mq) creal = e;
+      }
     }
     const uint32_t cm = __reduce_min_sync(FULL, creal);
     if (cm < stop) stop = cm;
-    uint32_t n = 0;
-    if (run && re < stop) n = (stop - 1u - re) / dq + 1u;  // ends re, re + d, ... before stop
+    // the replica's ends before stop: n of them, the last at elast; next end enext
+    uint32_t n = 0, elast = 0, enext = re;
+    if (run && re < stop) {
+      if (kv == 0u) {
+        n = (stop - 1u - re) / cb + 1u;
+        elast = re + (n - 1u) * cb;
+        enext = elast + cb;
+      } else {  // enext: the end of index n (0-based) from now
+        while (n + 1u < mq && enext < stop) {
+          elast = enext;
+          n++;
+          enext += dur(n);
+        }
+      }
+    }
     const uint32_t nt = __reduce_add_sync(FULL, n);
     if (nt == 0u) return;
     uint64_t gap_l = 0;
@@ -1734,18 +1768,17 @@ struct Sim {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const uint32_t nq = __shfl_sync(FULL, n, (int)srep[s]);
-      const uint32_t ds = __shfl_sync(FULL, dq, (int)srep[s]);
-      const uint32_t rs = __shfl_sync(FULL, re, (int)srep[s]);
+      const uint32_t el = __shfl_sync(FULL, elast, (int)srep[s]);
       if (sph[s] == PH_DEC && nq) {
-        gap_l += (uint64_t)(rs - sp[s]) + (uint64_t)(nq - 1u) * ds;  // 32-bit offsets: exact modulo 2^32
-        sp[s] = rs + (nq - 1u) * ds;
+        gap_l += (uint64_t)(el - sp[s]);  // the slot's gaps telescope to last end - last word (exact mod 2^32)
+        sp[s] = el;
         sdn[s] += nq;
         nw += nq;
       }
     }
     const uint32_t W = __reduce_add_sync(FULL, nw);
     const uint64_t G = warp_sum_split(gap_l);
-    if (run) re += n * dq;
+    if (run && n) re = enext;
     ticks += nt;
     words_out += W;
     if (win_now) win_words_out += W;

@@ -35,12 +35,15 @@ def variant(name):
             w.profiles = [dict(p, tpw_q16=65536) for p in w.profiles]
     elif name == "replicas4x16":
         w.profiles = [dict(p, replicas=4, max_batch=16) for p in w.profiles]
+    elif name == "replicas4x16_kv":  # with a KV term (L8B's 50 ns per context word): the stepped leap
+        w.profiles = [dict(p, replicas=4, max_batch=16, kv_ns_per_word=50) for p in w.profiles]
     return w
 
 
 def main():
     out = {}
-    names = sys.argv[1:] or ["c5_as_is", "tokens", "map_generic", "mpc", "bbr", "pcc", "replicas4x16"]
+    names = sys.argv[1:] or ["c5_as_is", "tokens", "map_generic", "mpc", "bbr", "pcc", "replicas4x16",
+                             "replicas4x16_kv"]
     for name in names:
         w = variant(name)
         sim = Simulator(w.columns())

@@ -252,3 +252,48 @@ def test_bruteforce_controller_laws(orc, law):
                    (bf["admit"][i], bf["done"][i], bf["R"][i], bf["r_bp"][i]), (law, case, i)
         acted += any(r["r_bp"] > 0 for r in d["requests"])
     assert acted >= 2, law  # the law acted in the loop, not only stayed at r = 0
+
+
+def test_next3_law_invariants(orc):
+    """Properties the NEXT-3 readings imply, over random sample streams:
+    MPC (R41) — r in {0} U candidates; with no oscillation cost the chosen r is
+    non-decreasing in the load (every sample scaled up); BBR (R42) — r in {0} U
+    [r_min, r_max], one step per ingest at most, and it only rises at the
+    bandwidth plateau while congested; PCC (R43) — r in {0} U [r_min, r_max]
+    and, while active, consecutive experiments alternate above / below r_base."""
+    rng = np.random.default_rng(77)
+    for case in range(200):
+        n = int(rng.integers(3, 40))
+        x = [int(v) for v in rng.integers(10_000, 90_000, n)]
+        w = [int(v) for v in rng.integers(1, 200, n)]
+        # MPC
+        c = orc.make_ctrl(law=W.LAW_MPC, t1=40_000, window=int(rng.integers(1, 9)), horizon_s=int(rng.integers(0, 5)),
+                          w_lat=int(rng.integers(1, 20)), w_q=int(rng.integers(0, 5)), w_osc=0)
+        cands = {0} | {500 + i * 1500 // 30 for i in range(31)}
+        lo = orc.ctrl_trace(c, x)["r"]
+        hi = orc.ctrl_trace(c, [v * 5 // 4 for v in x])["r"]
+        assert set(lo) <= cands and set(hi) <= cands
+        assert all(b >= a for a, b in zip(lo, hi)), case
+        # BBR
+        step = int(rng.integers(50, 800))
+        c = orc.make_ctrl(law=W.LAW_BBR, t1=int(rng.integers(0, 20_000)), window=int(rng.integers(1, 9)), step_bp=step)
+        r = orc.ctrl_trace(c, x, words=w)["r"]
+        prev = 0
+        for v in r:
+            assert v == 0 or 500 <= v <= 2000
+            assert abs(v - prev) <= max(step, 500), (case, prev, v)  # 0 <-> r_min jumps, else one step
+            prev = v
+        # PCC
+        d = int(rng.integers(50, 800))
+        c = orc.make_ctrl(law=W.LAW_PCC, t1=40_000, window=int(rng.integers(1, 9)), w_lat=1, w_q=4, step_bp=d)
+        t = orc.ctrl_trace(c, x)
+        for v in t["r"]:
+            assert v == 0 or 500 <= v <= 2000
+        run = []
+        for v, a in zip(t["r"], t["active"]):
+            if not a:
+                run = []
+                continue
+            run.append(v)
+            if len(run) >= 2 and run[-1] != run[-2]:
+                assert (run[-1] > run[-2]) == (len(run) % 2 == 1) or min(run[-1], run[-2]) in (500, 2000)

@@ -25,10 +25,9 @@ struct bellman_sim {
   int grid = 0;
   uint32_t last_launches = 0;
   Params params{};
-  unsigned int *counters = nullptr;  // [8]: one per launch of a run
+  unsigned int *counters = nullptr;  // [16]: one per launch of a run
   bool has_dbg = false;
-  bool has_multi = false;            // a scenario whose profile has replicas > 1, not debug-recorded
-  bool has_multi_dbg = false;        // ... debug-recorded (the multi-replica kernels)
+  bool has_kind[2][3] = {};          // [debug-recorded][kind]: some scenario runs in that kernel
   std::vector<uint8_t> calibrated;   // per scenario: ctrl is calibrated
   std::vector<uint32_t> calib_src;
   std::vector<uint32_t> dbg_slot;    // per scenario: debug-record slot or NONE
@@ -421,7 +420,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dn = take(sizeof(uint32_t) * 2 * nd);
   L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
   L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
-  L.off_cnt = take(sizeof(unsigned int) * 8);
+  L.off_cnt = take(sizeof(unsigned int) * 16);
   L.zero_end = o;
   // written by the kernels before they are read
   L.off_series = take(sizeof(uint32_t) * h.series_words);
@@ -561,11 +560,11 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   sim->host_order = h.order;
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
-  for (uint64_t k = 0; k < desc->n_scenarios; ++k)
-    if (desc->profiles[desc->scenarios[k].profile].replicas > 1u) {
-      if (desc->scenarios[k].record & BELLMAN_RECORD_SECONDS) sim->has_multi_dbg = true;
-      else sim->has_multi = true;
-    }
+  for (uint64_t k = 0; k < desc->n_scenarios; ++k) {
+    const bellman_scenario &sc = desc->scenarios[k];
+    const uint32_t kind = bellman_scenario_kind(sc, desc->ctrls[sc.ctrl], desc->profiles[sc.profile]);
+    sim->has_kind[(sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0][kind] = true;
+  }
   sim->dbg_off = h.dbg_off;
   sim->dbg_cap = h.dbg_cap;
 
@@ -680,32 +679,24 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
 #ifdef BELLMAN_AB_NOORDER
   P.order = nullptr;
 #endif
-  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 8 * sizeof(unsigned int), s));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 16 * sizeof(unsigned int), s));
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
   sim->last_launches = 0;
   // pass 1: non-calibrated scenarios (product kernel; debug-recorded ones in the DBG kernel)
-  // one launch per kernel with work: product, debug-record, multi-replica (plain, debug)
+  // one launch per kernel with work (bellman_scenario_kind): TBT-specialised,
+  // generic and multi-replica engines, debug-recorded or not; the product
+  // kernel always (it also covers empty sets)
   auto pass = [&](uint32_t pass_no, unsigned int *ctr) -> bellman_status {
     P.pass = pass_no;
-    P.counter = ctr;
-    CUDA_TRY(sim, bellman_launch_tick(P, grid, false, false, s));
-    sim->last_launches++;
-    if (sim->has_dbg) {  // some debug-recorded scenario exists (its one-replica ones run here)
-      P.counter = ctr + 1;
-      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, false, s));
-      sim->last_launches++;
-    }
-    if (sim->has_multi) {
-      P.counter = ctr + 2;
-      CUDA_TRY(sim, bellman_launch_tick(P, grid, false, true, s));
-      sim->last_launches++;
-    }
-    if (sim->has_multi_dbg) {
-      P.counter = ctr + 3;
-      CUDA_TRY(sim, bellman_launch_tick(P, grid, true, true, s));
-      sim->last_launches++;
-    }
+    for (int dbg = 0; dbg < 2; ++dbg)
+      for (int kind = 0; kind < 3; ++kind) {
+        if (dbg == 1 && kind == 0) continue;  // debug-recorded one-engine scenarios are kind 1
+        if (!(dbg == 0 && kind == 0) && !sim->has_kind[dbg][kind]) continue;
+        P.counter = ctr + 3 * dbg + kind;
+        CUDA_TRY(sim, bellman_launch_tick(P, grid, dbg != 0, kind, s));
+        sim->last_launches++;
+      }
     return BELLMAN_OK;
   };
   bellman_status rc = pass(1, sim->counters);
@@ -713,7 +704,7 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   if (any_cal) {  // a10: calibration, then pass 2 over the calibrated scenarios
     CUDA_TRY(sim, bellman_launch_calibrate(P, sim->n_slots, s));
     sim->last_launches++;
-    rc = pass(2, sim->counters + 4);
+    rc = pass(2, sim->counters + 8);
     if (rc != BELLMAN_OK) return rc;
   }
   return BELLMAN_OK;

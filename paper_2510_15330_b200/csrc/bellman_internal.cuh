@@ -98,6 +98,10 @@ struct Params {
 }  // namespace bellman
 
 // launchers (bellman_kernels.cu)
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, bool multi, cudaStream_t stream);
+// one persistent launch over the run's scenarios of one kernel: dbg (debug-recorded
+// or not) x kind (0 TBT-specialised, 1 generic, 2 multi-replica; scenario_kind)
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, int kind, cudaStream_t stream);
+// the kind (as above) of one scenario, shared by the kernel's filter and the host
+uint32_t bellman_scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc, const bellman_profile &pf);
 cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream);
 int bellman_tick_grid(int device);

@@ -2435,11 +2435,23 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
   __syncwarp();
 }
 
-// DBG: the debug-record instantiation; MULTI: the multi-replica kernels.  Each
-// scenario runs in exactly one of product <0,0>, debug <1,0>, multi-replica
-// <0,1> and multi-replica debug <1,1>, so the product kernel carries neither
-// the debug hooks nor the multi-replica loop.
-template <bool DBG, bool MULTI = false>
+// Which kernel runs a scenario: debug-recorded (DBG) or not, and its code
+// path (KIND): 0 the TBT-specialised single engine (TBT signal, non-blocking
+// prefill, no KV capacity, word units, MAP / STEP / CONST / OFF: every
+// benchmark configuration), 1 the generic single engine, 2 multi-replica.
+// Debug-recorded single-engine scenarios take the generic path.  Each
+// scenario runs in exactly one kernel, so the product kernel <0,0> carries
+// only the specialised loops.
+__host__ __device__ __forceinline__ uint32_t scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc,
+                                                           const bellman_profile &pf) {
+  if (pf.replicas > 1u) return 2u;
+  if ((sc.record & BELLMAN_RECORD_SECONDS) != 0) return 1u;
+  const bool tbto = cc.signal == BELLMAN_SIG_TBT && pf.prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
+                    pf.kv_cap_words == 0 && pf.tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC;
+  return tbto ? 0u : 1u;
+}
+
+template <bool DBG, int KIND>
 #ifndef BELLMAN_MIN_BLOCKS
 #define BELLMAN_MIN_BLOCKS (16 / BELLMAN_WPB)
 #endif
@@ -2455,20 +2467,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     const bellman_scenario sc = p.sc[sid];
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
     if ((cc.calibrated != 0) != (p.pass == 2)) continue;
-    if ((p.profs[sc.profile].replicas > 1u) != MULTI) continue;
-    // debug-recorded scenarios run in the DBG instantiations, all others in the product ones
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
+    if (scenario_kind(sc, cc, p.profs[sc.profile]) != (uint32_t)KIND) continue;
 
 #ifdef BELLMAN_PROFILE_COUNTERS
     if (lane == 0 && sid < (1u << 16)) g_span[2 * sid] = gtimer();
 #endif
-    if constexpr (MULTI) {
+    if constexpr (KIND == 2) {
       run_one<DBG, false, false, true>(p, sid, sc, cc, lane, h);
-    } else if constexpr (DBG) {
-      run_one<true, false>(p, sid, sc, cc, lane, h);
-    } else if (cc.signal == BELLMAN_SIG_TBT && p.profs[sc.profile].prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
-               p.profs[sc.profile].kv_cap_words == 0 &&
-               p.profs[sc.profile].tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC) {
+    } else if constexpr (KIND == 1) {
+      run_one<DBG, false>(p, sid, sc, cc, lane, h);
+    } else {
       // TBT-only loop (one replica, no KV capacity, words: no token conversion
       // at admission; MAP / STEP / CONST / OFF: no NEXT-3 law call site),
       // specialised once more on a KV-free cost law (kv = 0)
@@ -2476,8 +2485,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
         run_one<false, true, true>(p, sid, sc, cc, lane, h);
       else
         run_one<false, true, false>(p, sid, sc, cc, lane, h);
-    } else {
-      run_one<false, false>(p, sid, sc, cc, lane, h);
     }
 #ifdef BELLMAN_PROFILE_COUNTERS
     if (lane == 0 && sid < (1u << 16)) g_span[2 * sid + 1] = gtimer();
@@ -2536,7 +2543,7 @@ int bellman_tick_grid(int device) {
   if (device >= 0 && device < 64 && cached[device] > 0) return cached[device];
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bellman::bellman_tick_kernel<false, 0>,
                                                     bellman::kWarpsPerBlock * 32, 0) != cudaSuccess)
     return -1;
   const int g = sms * (per_sm > 0 ? per_sm : 1);
@@ -2544,15 +2551,17 @@ int bellman_tick_grid(int device) {
   return g;
 }
 
-cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, bool multi, cudaStream_t stream) {
-  if (multi && dbg)
-    bellman::bellman_tick_kernel<true, true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
-  else if (multi)
-    bellman::bellman_tick_kernel<false, true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
-  else if (dbg)
-    bellman::bellman_tick_kernel<true><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
-  else
-    bellman::bellman_tick_kernel<false><<<grid, bellman::kWarpsPerBlock * 32, 0, stream>>>(p);
+uint32_t bellman_scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc, const bellman_profile &pf) {
+  return bellman::scenario_kind(sc, cc, pf);
+}
+
+cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, int kind, cudaStream_t stream) {
+  const int bs = bellman::kWarpsPerBlock * 32;
+  if (dbg && kind == 2) bellman::bellman_tick_kernel<true, 2><<<grid, bs, 0, stream>>>(p);
+  else if (dbg) bellman::bellman_tick_kernel<true, 1><<<grid, bs, 0, stream>>>(p);
+  else if (kind == 2) bellman::bellman_tick_kernel<false, 2><<<grid, bs, 0, stream>>>(p);
+  else if (kind == 1) bellman::bellman_tick_kernel<false, 1><<<grid, bs, 0, stream>>>(p);
+  else bellman::bellman_tick_kernel<false, 0><<<grid, bs, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -787,7 +787,10 @@ __device__ __noinline__ uint32_t ingest_sample(uint32_t wid, uint32_t lane, uint
 #define BELLMAN_LEAP_SHIFT 3
 #endif
 
-template <bool DBG, bool TBTO, bool KV0 = false>
+// XT (with TBTO): the TBT-specialised loop extended with the runtime features
+// the product loop leaves out — token units, NEXT-3 laws, KV-reserve capacity —
+// for the generic kernel's TBT scenarios (the product kernel never has XT).
+template <bool DBG, bool TBTO, bool KV0 = false, bool XT = false>
 struct Sim {
   __device__ explicit Sim(uint32_t w) : wid(w) {}
   // the selected signal is x: a compile-time answer in the TBT-only
@@ -893,7 +896,7 @@ struct Sim {
     // the TBT loops take the controller inline (C5's paper-trace scenarios
     // ingest every second of long quiet stretches); the others call it
     if (TBTO && !DBG)  // the TBT loops run MAP / STEP / CONST / OFF only (no ingest_ext call site)
-      r = ingest_body<DBG, false>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
+      r = ingest_body<DBG, XT>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, false, 0u);
     else
       r = ingest_sample<DBG>(wid, lane, ab(sec_bound), acc_sum, acc_cnt, r, DBG && dbg != nullptr,
                            sig(BELLMAN_SIG_UTIL) ? maxb : 0u);
@@ -1386,8 +1389,9 @@ struct Sim {
         sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
         qb = (uint32_t)sc / 50u;
       }
-      if (!TBTO) R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
-      const uint32_t kvcap = TBTO ? 0u : cold().kv_cap;  // the TBT loops run capacity-free profiles only
+      if (!TBTO || XT) R = to_tokens(R, cold().tpw);  // NEXT-4: the realized output decoded as tokens (R44)
+      // the product TBT loops run capacity-free profiles only
+      const uint32_t kvcap = (TBTO && !XT) ? 0u : cold().kv_cap;
       if (__builtin_expect(kvcap != 0, 0)) {
         // NEXT-4: the whole context (input + realized output) must fit beside
         // the contexts in the system; an oversized head enters an empty system.
@@ -2025,12 +2029,12 @@ __device__ void warp_percentiles(const uint32_t *hist, uint32_t nb, uint64_t n, 
 // One scenario, a1-a9.  TBTO: the scenario's signal is TBT (compile-time
 // specialisation of every signal test in the event loop).  MULTI: a
 // multi-replica profile (NEXT-4, R45), run by multi_loop in its own kernel.
-template <bool DBG, bool TBTO, bool KV0 = false, bool MULTI = false>
+template <bool DBG, bool TBTO, bool KV0 = false, bool MULTI = false, bool XT = false>
 __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, const bellman_scenario &sc,
                                         const bellman_ctrl &cc, const uint32_t lane, WarpHist &h) {
   // ---- a1: scenario decode.  Shared-memory (Cold) fields are written by
   // lane 0 only and read after the __syncwarp below.
-  Sim<DBG, TBTO, KV0> S(warp_in_block());
+  Sim<DBG, TBTO, KV0, XT> S(warp_in_block());
   S.lane = lane;
   const bellman_profile pr = p.profs[sc.profile];
   const DevTrace tr = p.traces[sc.trace];
@@ -2476,7 +2480,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     if constexpr (KIND == 2) {
       run_one<DBG, false, false, true>(p, sid, sc, cc, lane, h);
     } else if constexpr (KIND == 1) {
-      run_one<DBG, false>(p, sid, sc, cc, lane, h);
+      const bellman_profile &pf = p.profs[sc.profile];
+      if (!DBG && cc.signal == BELLMAN_SIG_TBT && pf.prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
+          (pf.kv_policy != BELLMAN_KV_PREEMPT || pf.kv_cap_words == 0)) {
+        // TBT scenarios with token units, a NEXT-3 law or a KV-reserve capacity:
+        // the TBT-specialised loop with those features at run time (XT)
+        if (pf.kv_ns_per_word == 0)
+          run_one<false, true, true, false, true>(p, sid, sc, cc, lane, h);
+        else
+          run_one<false, true, false, false, true>(p, sid, sc, cc, lane, h);
+      } else {
+        run_one<DBG, false>(p, sid, sc, cc, lane, h);
+      }
     } else {
       // TBT-only loop (one replica, no KV capacity, words: no token conversion
       // at admission; MAP / STEP / CONST / OFF: no NEXT-3 law call site),

@@ -8,8 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libbellman_sim.so")
 PEAK_OUT = os.path.join(HERE, "libbellman_peak.so")  # roofline microbenchmark (measurement only)
-SOURCES = ["bellman_kernels.cu", "bellman_host.cu"]
-DEPS = SOURCES + ["bellman_internal.cuh"]
+SOURCES = ["bellman_kernels.cu", "bellman_lane.cu", "bellman_host.cu"]
+DEPS = SOURCES + ["bellman_internal.cuh", "bellman_lane.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

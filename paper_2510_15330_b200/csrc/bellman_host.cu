@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -17,6 +18,32 @@
 
 using namespace bellman;
 
+// K2L (the lane-per-scenario kernel) is a throughput engine: 32 scenarios per
+// warp, one CTA of 5-7 warps per SM, so it needs several scenarios per lane
+// (B200: 23-33k lanes) to beat the warp engine, which runs each scenario's
+// serial chain faster.  A run takes K2L for the scenarios within its bounds
+// when it has at least kLaneMinScenarios of them in total (C5 and its 8-way
+// shards; C1-C4 stay on K2), unless the environment sets BELLMAN_LANE=0 (A/B
+// measurements), or BELLMAN_LANE=2 (every run, any size: parity tests of K2L
+// on small sets).  Read at workspace sizing, create and run.
+constexpr uint64_t kLaneMinScenarios = 65536;
+static uint32_t lane_mode() {
+  const char *e = std::getenv("BELLMAN_LANE");
+  return e ? (e[0] == '0' ? 0u : (e[0] == '2' ? 2u : 1u)) : 1u;
+}
+
+static uint32_t kind_of(const bellman_sim_desc *d, const bellman_scenario &sc, uint32_t lane_on) {
+  return scenario_kind_of(sc, d->ctrls[sc.ctrl], d->profiles[sc.profile], d->traces[sc.trace].kind, lane_on);
+}
+
+// whether a descriptor's workspace carries K2L's histograms
+static bool lane_possible(const bellman_sim_desc *d) {
+  if (lane_mode() == 0 || (lane_mode() == 1 && d->n_scenarios < kLaneMinScenarios)) return false;
+  for (uint64_t s = 0; s < d->n_scenarios; ++s)
+    if (kind_of(d, d->scenarios[s], 1u) >= 3u) return true;
+  return false;
+}
+
 struct bellman_sim {
   int device = 0;
   uint64_t n_scenarios = 0;
@@ -27,7 +54,9 @@ struct bellman_sim {
   Params params{};
   unsigned int *counters = nullptr;  // [16]: one per launch of a run
   bool has_dbg = false;
-  bool has_kind[2][3] = {};          // [debug-recorded][kind]: some scenario runs in that kernel
+  bool has_kind[2][2][5] = {};       // [K2L on][debug-recorded][kind]: some scenario runs in that kernel
+  int lane_grid = 0;                 // K2L CTAs (one per SM)
+  bool lane_ok = false;              // the workspace holds K2L's per-thread histograms
   std::vector<uint8_t> calibrated;   // per scenario: ctrl is calibrated
   std::vector<uint32_t> calib_src;
   std::vector<uint32_t> dbg_slot;    // per scenario: debug-record slot or NONE
@@ -250,7 +279,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, total;
+      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, off_lhist, total;
   size_t in_end;              // [0, in_end): host-filled inputs, one staging copy at create
   size_t zero_beg, zero_end;  // [zero_beg, zero_end): zeroed at create (counters, stats, histograms)
 };
@@ -420,7 +449,10 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dn = take(sizeof(uint32_t) * 2 * nd);
   L.off_stats = take(sizeof(bellman_scenario_stats) * d->n_scenarios);
   L.off_hist = take(sizeof(uint64_t) * kSegWords * d->n_segments);
-  L.off_cnt = take(sizeof(unsigned int) * 16);
+  L.off_cnt = take(sizeof(unsigned int) * 32);
+  // K2L per-thread histograms: all-zero between scenarios (each epilogue
+  // re-zeroes what its scenario touched), only when some scenario runs in K2L
+  L.off_lhist = take(lane_possible(d) ? sizeof(uint32_t) * kLaneHistWords * kLaneMaxThreads : 0);
   L.zero_end = o;
   // written by the kernels before they are read
   L.off_series = take(sizeof(uint32_t) * h.series_words);
@@ -493,6 +525,11 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     return fail(nullptr, BELLMAN_ECUDA, "occupancy query failed");
   }
   if (sim->grid > (int)kMaxPreCtas) sim->grid = (int)kMaxPreCtas;  // one preemption scratch per CTA
+  sim->lane_grid = bellman_lane_grid(device);
+  if (sim->lane_grid <= 0) {
+    delete sim;
+    return fail(nullptr, BELLMAN_ECUDA, "SM count query failed");
+  }
   sim->calibrated.assign(desc->n_scenarios, 0);
   sim->calib_src.assign(desc->n_scenarios, BELLMAN_NONE);
   for (uint64_t s = 0; s < desc->n_scenarios; ++s) {
@@ -555,6 +592,9 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.arrivals = (const bellman_arrival *)(ws + L.off_arr);
   P.order = nullptr;
   P.pre = (PreScratch *)(ws + L.off_pre);
+  P.lane_on = 0;  // set per run
+  P.lane_hist = (uint32_t *)(ws + L.off_lhist);
+  sim->lane_ok = lane_possible(desc);
   sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->shard_order = (uint32_t *)(ws + L.off_sord);
   sim->host_order = h.order;
@@ -562,8 +602,8 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   sim->has_dbg = !h.dbg_off.empty();
   for (uint64_t k = 0; k < desc->n_scenarios; ++k) {
     const bellman_scenario &sc = desc->scenarios[k];
-    const uint32_t kind = bellman_scenario_kind(sc, desc->ctrls[sc.ctrl], desc->profiles[sc.profile]);
-    sim->has_kind[(sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0][kind] = true;
+    for (uint32_t lo = 0; lo < 2; ++lo)
+      sim->has_kind[lo][(sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0][kind_of(desc, sc, lo)] = true;
   }
   sim->dbg_off = h.dbg_off;
   sim->dbg_cap = h.dbg_cap;
@@ -679,24 +719,32 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
 #ifdef BELLMAN_AB_NOORDER
   P.order = nullptr;
 #endif
-  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 16 * sizeof(unsigned int), s));
+  CUDA_TRY(sim, cudaMemsetAsync(sim->counters, 0, 32 * sizeof(unsigned int), s));
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
   sim->last_launches = 0;
-  // pass 1: non-calibrated scenarios (product kernel; debug-recorded ones in the DBG kernel)
-  // one launch per kernel with work (bellman_scenario_kind): TBT-specialised,
-  // generic and multi-replica engines, debug-recorded or not; the product
-  // kernel always (it also covers empty sets)
+  // pass 1: non-calibrated scenarios.  One launch per kernel with work
+  // (scenario_kind_of): K2L (kv = 0 / kv > 0), the TBT-specialised, generic and
+  // multi-replica warp engines, debug-recorded or not; if no kernel has work
+  // (an empty set) the TBT-specialised warp kernel runs once
+  P.lane_on = (sim->lane_ok && (lane_mode() == 2 || count >= kLaneMinScenarios)) ? 1u : 0u;
   auto pass = [&](uint32_t pass_no, unsigned int *ctr) -> bellman_status {
     P.pass = pass_no;
+    uint32_t n = 0;
     for (int dbg = 0; dbg < 2; ++dbg)
-      for (int kind = 0; kind < 3; ++kind) {
-        if (dbg == 1 && kind == 0) continue;  // debug-recorded one-engine scenarios are kind 1
-        if (!(dbg == 0 && kind == 0) && !sim->has_kind[dbg][kind]) continue;
-        P.counter = ctr + 3 * dbg + kind;
-        CUDA_TRY(sim, bellman_launch_tick(P, grid, dbg != 0, kind, s));
-        sim->last_launches++;
+      for (int kind = 0; kind < 5; ++kind) {
+        if (!sim->has_kind[P.lane_on][dbg][kind]) continue;
+        P.counter = ctr + 5 * dbg + kind;
+        if (kind >= 3) CUDA_TRY(sim, bellman_launch_lane(P, sim->lane_grid, kind, s));
+        else CUDA_TRY(sim, bellman_launch_tick(P, grid, dbg != 0, kind, s));
+        n++;
       }
+    if (n == 0) {
+      P.counter = ctr;
+      CUDA_TRY(sim, bellman_launch_tick(P, grid, false, 0, s));
+      n++;
+    }
+    sim->last_launches += n;
     return BELLMAN_OK;
   };
   bellman_status rc = pass(1, sim->counters);
@@ -704,7 +752,7 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   if (any_cal) {  // a10: calibration, then pass 2 over the calibrated scenarios
     CUDA_TRY(sim, bellman_launch_calibrate(P, sim->n_slots, s));
     sim->last_launches++;
-    rc = pass(2, sim->counters + 8);
+    rc = pass(2, sim->counters + 16);
     if (rc != BELLMAN_OK) return rc;
   }
   return BELLMAN_OK;
@@ -871,3 +919,92 @@ const char *bellman_status_string(bellman_status s) {
 const char *bellman_sim_last_error(const bellman_sim *sim) { return sim ? sim->err : g_err; }
 
 }  // extern "C"
+
+#ifdef BELLMAN_LANECHECK
+// ---------------------------------------------------------------------------
+// Development build only (-DBELLMAN_LANECHECK, never the product library): run
+// K2L's per-scenario code on the CPU over every scenario it would take, with
+// the calibration between the passes done here, so that the lane engine can be
+// compared with the oracle (scripts/lanecheck.py) without a GPU.
+namespace bellman {
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist);
+}
+extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_stats *out, unsigned long long *seg,
+                                 uint8_t *ran) {
+  if (validate(d) != BELLMAN_OK) return -1;
+  HostPrep h;
+  prepare(d, h);
+  static std::vector<uint2> l2;
+  if (l2.empty()) log2_table_build(l2);
+  Params P{};
+  P.sc = d->scenarios;
+  P.traces = h.traces.data();
+  P.segs = h.segs.data();
+  P.profs = d->profiles;
+  P.ctrls = d->ctrls;
+  P.tabL = d->models.L_words;
+  P.tabI = d->models.I_words;
+  P.tabF = d->models.fvar_q16;
+  P.tabN = d->models.noise;
+  P.tabC = d->models.fcomp_q16;
+  P.tabQ = d->models.qnoise;
+  P.log2tab = l2.data();
+  P.poly0 = d->models.poly_q16[0];
+  P.poly1 = d->models.poly_q16[1];
+  P.poly2 = d->models.poly_q16[2];
+  {
+    const int64_t *c = d->models.poly_q16;
+    const unsigned __int128 b = (unsigned __int128)(c[0] < 0 ? -c[0] : c[0]) +
+                                ((unsigned __int128)(c[1] < 0 ? -c[1] : c[1]) << 17) +
+                                ((unsigned __int128)(c[2] < 0 ? -c[2] : c[2]) << 34);
+    P.poly_fast = b < ((unsigned __int128)1 << 43) ? 1u : 0u;
+  }
+  P.q_inactive = d->models.quality[0];
+  P.q_active = d->models.quality[1];
+  P.q_floor = d->models.quality[2];
+  P.q_safe = d->models.quality[3];
+  P.q_end = d->models.quality[4];
+  P.class_cum0 = d->models.class_cum[0];
+  P.class_cum1 = d->models.class_cum[1];
+  P.class_cum2 = d->models.class_cum[2];
+  std::vector<uint32_t> series(h.series_words + 1), series_n(h.slot_off.size() + 1), calib(4 * h.slot_off.size() + 4);
+  P.series_slot = h.slot_of.data();
+  P.series_off = h.slot_off.data();
+  P.series_cap = h.slot_cap.data();
+  P.series_n = series_n.data();
+  P.series = series.data();
+  P.calib = calib.data();
+  P.stats = out;
+  P.seg_hist = seg;
+  P.lane_on = 1;
+  std::vector<uint32_t> smem(kLaneWarpWords<false>), hist(kLaneHistWords, 0);
+  for (uint32_t pass = 1; pass <= 2; ++pass) {
+    P.pass = pass;
+    for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+      const bellman_scenario &sc = d->scenarios[s];
+      if ((d->ctrls[sc.ctrl].calibrated != 0) != (pass == 2) || kind_of(d, sc, 1u) < 3u) continue;
+      lane_host_run(P, s, smem.data(), hist.data());
+      ran[s] = 1;
+    }
+    if (pass == 1)
+      for (size_t w = 0; w < h.slot_off.size(); ++w) {  // K5 on the host: nearest-rank p50 / p75
+        const uint32_t n = std::min(series_n[w], h.slot_cap[w]);
+        std::vector<uint32_t> x(series.begin() + h.slot_off[w], series.begin() + h.slot_off[w] + n);
+        std::sort(x.begin(), x.end());
+        uint32_t t1 = 0, t2 = 0, st = 1;
+        if (n >= 4) {
+          t1 = x[(50u * n + 99u) / 100u - 1u];
+          t2 = x[(75u * n + 99u) / 100u - 1u];
+          st = t1 == t2 ? 2u : 0u;
+        }
+        calib[4 * w] = t1;
+        calib[4 * w + 1] = t2;
+        calib[4 * w + 2] = st;
+        calib[4 * w + 3] = n;
+      }
+  }
+  for (uint32_t i = 0; i < kHistRing; ++i)
+    if (hist[i]) return -2;  // every scenario's epilogue must leave its histograms zeroed
+  return 0;
+}
+#endif

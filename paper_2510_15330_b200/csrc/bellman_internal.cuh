@@ -4,6 +4,7 @@
 #include <cstdint>
 
 #include "../../include/bellman_sim.h"
+#include "bellman_lane.cuh"
 
 namespace bellman {
 
@@ -93,15 +94,18 @@ struct Params {
   PreScratch *pre;               // [kMaxPreCtas] NEXT-4 preemption scratch (preempting profiles only)
   uint64_t first, count, stride;
   uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
+  uint32_t lane_on;    // 1: kind-0 scenarios within K2L's bounds run in K2L (scenario_kind_of)
+  uint32_t *lane_hist; // K2L per-thread histograms [kLaneMaxThreads][kLaneHistWords], all-zero between scenarios
 };
 
 }  // namespace bellman
 
-// launchers (bellman_kernels.cu)
+// launchers (bellman_kernels.cu, bellman_lane.cu)
 // one persistent launch over the run's scenarios of one kernel: dbg (debug-recorded
 // or not) x kind (0 TBT-specialised, 1 generic, 2 multi-replica; scenario_kind)
 cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, int kind, cudaStream_t stream);
-// the kind (as above) of one scenario, shared by the kernel's filter and the host
-uint32_t bellman_scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc, const bellman_profile &pf);
+// K2L (kind 3: kv = 0, kind 4: kv > 0), one CTA per SM
+cudaError_t bellman_launch_lane(const bellman::Params &p, int grid, int kind, cudaStream_t stream);
+int bellman_lane_grid(int device);
 cudaError_t bellman_launch_calibrate(const bellman::Params &p, uint32_t n_slots, cudaStream_t stream);
 int bellman_tick_grid(int device);

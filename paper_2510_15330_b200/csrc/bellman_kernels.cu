@@ -2440,19 +2440,16 @@ __device__ __forceinline__ void run_one(const Params &p, const uint64_t sid, con
 }
 
 // Which kernel runs a scenario: debug-recorded (DBG) or not, and its code
-// path (KIND): 0 the TBT-specialised single engine (TBT signal, non-blocking
-// prefill, no KV capacity, word units, MAP / STEP / CONST / OFF: every
-// benchmark configuration), 1 the generic single engine, 2 multi-replica.
+// path (KIND, scenario_kind_of in bellman_lane.cuh): 0 the TBT-specialised
+// single engine (TBT signal, non-blocking prefill, no KV capacity, word units,
+// MAP / STEP / CONST / OFF) when it is outside K2L's bounds, 1 the generic
+// single engine, 2 multi-replica; 3 / 4 run in K2L (bellman_lane.cu).
 // Debug-recorded single-engine scenarios take the generic path.  Each
 // scenario runs in exactly one kernel, so the product kernel <0,0> carries
 // only the specialised loops.
-__host__ __device__ __forceinline__ uint32_t scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc,
-                                                           const bellman_profile &pf) {
-  if (pf.replicas > 1u) return 2u;
-  if ((sc.record & BELLMAN_RECORD_SECONDS) != 0) return 1u;
-  const bool tbto = cc.signal == BELLMAN_SIG_TBT && pf.prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
-                    pf.kv_cap_words == 0 && pf.tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC;
-  return tbto ? 0u : 1u;
+__host__ __device__ __forceinline__ uint32_t scenario_kind(const Params &p, const bellman_scenario &sc,
+                                                           const bellman_ctrl &cc) {
+  return scenario_kind_of(sc, cc, p.profs[sc.profile], p.traces[sc.trace].kind, p.lane_on);
 }
 
 template <bool DBG, int KIND>
@@ -2472,7 +2469,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BELLMAN_MIN_BLOCKS) bellm
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
     if ((cc.calibrated != 0) != (p.pass == 2)) continue;
     if (((sc.record & BELLMAN_RECORD_SECONDS) != 0) != DBG) continue;
-    if (scenario_kind(sc, cc, p.profs[sc.profile]) != (uint32_t)KIND) continue;
+    if (scenario_kind(p, sc, cc) != (uint32_t)KIND) continue;
 
 #ifdef BELLMAN_PROFILE_COUNTERS
     if (lane == 0 && sid < (1u << 16)) g_span[2 * sid] = gtimer();
@@ -2564,10 +2561,6 @@ int bellman_tick_grid(int device) {
   const int g = sms * (per_sm > 0 ? per_sm : 1);
   if (device >= 0 && device < 64) cached[device] = g;
   return g;
-}
-
-uint32_t bellman_scenario_kind(const bellman_scenario &sc, const bellman_ctrl &cc, const bellman_profile &pf) {
-  return bellman::scenario_kind(sc, cc, pf);
 }
 
 cudaError_t bellman_launch_tick(const bellman::Params &p, int grid, bool dbg, int kind, cudaStream_t stream) {

@@ -1,0 +1,1231 @@
+// bellman_lane.cu — K2L, the lane-per-scenario product kernel (round 2).
+//
+// SURVEY §8(d) bounds the method twice: R_issue (one warp per scenario, every
+// scalar operation of the event loop takes a whole warp issue slot) and R_lane
+// (the integer lanes themselves, "design-independent; shows what
+// warp-per-scenario leaves on the table").  K2 (bellman_kernels.cu) runs one
+// scenario per warp and reaches ~0.6 of R_issue, i.e. ~2 % of R_lane.  K2L runs
+// one scenario per LANE: each thread owns a whole scenario — clock, batch,
+// controller, generator, counters in registers; its <= 64 request slots in
+// shared memory — and the 32 scenarios of a warp advance through the same
+// event loop, each lane handling its own next event (divergent handlers are
+// serialised by the SIMT stack, so a warp pays the union of the handlers its
+// lanes need per trip, not their sum).
+//
+// Scope (scenario_kind 3 / 4): the TBT-specialised single-engine
+// scenarios of the product kernel (TBT signal, non-blocking prefill, no KV
+// capacity, word units, MAP / STEP / CONST / OFF; every benchmark
+// configuration) on a Poisson trace with horizon < 2^31 µs and fewer than 2^25
+// possible iterations; kind 3 is the KV-free cost law (kv = 0), kind 4 has the
+// KV term.  Everything else stays on K2.  Semantics are K2's (and the oracle's)
+// step for step; only the data layout differs:
+//  * all instants are absolute 32-bit µs (horizon < 2^31, iteration and
+//    prefill durations < 2^31: no epoch, no rebase);
+//  * request slots: shared memory [field][slot][lane] (u32; the bank is the
+//    lane whatever the slot, so divergent slot indices never conflict): prefill
+//    end, arrival, realized length R (+ input words with a KV term);
+//  * decoding requests: a binary min-heap per lane of (completion iteration
+//    << 6 | slot) in shared memory (completion iteration < 2^26);
+//  * slot phases: free / prefilling / decode-ready bit masks (u64 registers);
+//  * the FIFO queue head: the next accepted arrival, generated lazily one
+//    candidate at a time (same Philox counters, thinning, crossing rule);
+//  * histograms (a9): per thread in global memory (L2-resident), bumped with
+//    fire-and-forget RED.ADD; a bit mask of the 32-bin groups each scenario
+//    touched bounds the epilogue's percentile scan, segment merge and
+//    re-zeroing to those groups.
+//
+// The per-scenario code is __host__ __device__: a development build
+// (-DBELLMAN_LANECHECK, bellman_host.cu) runs it on the CPU to compare with
+// the oracle before any GPU time is spent.  The product path is the kernel.
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "bellman_internal.cuh"
+#include "bellman_lane.cuh"
+
+namespace bellman {
+namespace lane {
+
+#define LHD __host__ __device__ __forceinline__
+
+constexpr uint32_t kInf = 0xffffffffu, kFar = 0xfffffffeu, FULL_MASK = 0xffffffffu;
+constexpr uint32_t kNone = BELLMAN_NONE;
+
+LHD uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+LHD uint32_t clz32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return (uint32_t)__clz(x);
+#else
+  return x ? (uint32_t)__builtin_clz(x) : 32u;
+#endif
+}
+LHD uint32_t ffs64(uint64_t x) {  // 1 + index of the lowest set bit, 0 if none
+#ifdef __CUDA_ARCH__
+  return (uint32_t)__ffsll((long long)x);
+#else
+  return (uint32_t)__builtin_ffsll((long long)x);
+#endif
+}
+LHD uint32_t ffs32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return (uint32_t)__ffs((int)x);
+#else
+  return (uint32_t)__builtin_ffs((int)x);
+#endif
+}
+LHD void red_add(uint32_t *a, uint32_t v) {  // fire-and-forget on the GPU (result unused: RED)
+#ifdef __CUDA_ARCH__
+  atomicAdd(a, v);
+#else
+  *a += v;
+#endif
+}
+LHD void seg_add(unsigned long long *a, unsigned long long v) {
+#ifdef __CUDA_ARCH__
+  atomicAdd(a, v);
+#else
+  *a += v;
+#endif
+}
+template <class T>
+LHD T ldg(const T *x) {
+#ifdef __CUDA_ARCH__
+  return __ldg(x);
+#else
+  return *x;
+#endif
+}
+
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+// Philox4x32-10 (Salmon et al. SC'11), counter (c0..c3), key (k0, k1).  Inline:
+// a call would wait for every load still in flight into a register the callee
+// may clobber (the head's table entries are loaded just before it).
+LHD U4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                           uint32_t c3) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c0 = n0;
+    c1 = (uint32_t)p1;
+    c2 = n2;
+    c3 = (uint32_t)p0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
+// -ln(U), U = (2u+1)/2^33, in Q32 (reading R33): log2 by table + interpolation.
+// Split in two so that the table entry can be loaded one candidate ahead:
+// the normalised mantissa bits x (table index x >> 20) and exponent e of
+// v = 2u + 1, then the interpolation with the entry t = tab[x >> 20].
+LHD uint32_t neglog_split(uint32_t u, uint32_t &e) {
+  if (u >= 0x80000000u) {
+    e = 32;
+    return 2u * u + 1u;
+  }
+  const uint32_t v = 2u * u + 1u;
+  e = 31u - clz32(v);
+  return (uint32_t)(((uint64_t)(v - (1u << e))) << (32u - e));
+}
+LHD uint64_t neglog_q32(uint32_t u, uint2 t) {
+  uint32_t e;
+  const uint32_t x = neglog_split(u, e);
+  const uint64_t f = x & 0xFFFFFu;
+  const uint64_t log2v = ((uint64_t)e << 32) + t.x + (((uint64_t)t.y * f) >> 20);
+  const uint64_t neg = (33ull << 32) - log2v;
+  const uint64_t lo = neg * 2977044472ull, hi = mulhi64(neg, 2977044472ull);  // round(ln 2 * 2^32)
+  return (hi << 32) | (lo >> 32);
+}
+
+// latency bin of a value in µs (a9): exact ms below 32, then 32 per octave.
+// Instants are < 2^32 here, so every latency fits 32 bits.
+LHD uint32_t lat_bin(uint32_t us) {
+  const uint32_t ms = us / 1000u;
+  if (ms < 32) return ms;
+  const uint32_t e = 31u - clz32(ms);
+  return 32u * (e - 4u) + ((ms >> (e - 5u)) & 31u);
+}
+LHD uint32_t lat_edge(uint32_t b) {
+  if (b < 32) return b;
+  const uint32_t e = b / 32u + 4u, s = b % 32u;
+  return (32u + s) << (e - 5u);
+}
+LHD uint64_t div_u64(uint64_t a, uint64_t b) {
+  if (((a | b) >> 32) == 0) return (uint32_t)a / (uint32_t)b;
+  return a / b;
+}
+// NEXT-2 similarity decay: q_active - floor((q_active - q_floor) X / D)
+__host__ __device__ __noinline__ int32_t sim_decay(uint32_t q_active, uint32_t q_floor, uint64_t X, uint64_t D) {
+  const uint64_t aX = (uint64_t)(q_active - q_floor) * X;
+#ifdef __CUDA_ARCH__
+  uint32_t q = (uint32_t)__fmul_rz((float)aX, __frcp_rn((float)D));  // estimate, then an exact fix-up
+  while (q && (uint64_t)q * D > aX) q--;
+  while ((uint64_t)(q + 1u) * D <= aX) q++;
+#else
+  const uint32_t q = (uint32_t)(aX / D);
+#endif
+  return (int32_t)q_active - (int32_t)q;
+}
+
+// a7 rewrite (R11), the 128-bit path (out of line)
+__host__ __device__ __noinline__ uint32_t rewrite_wide(int64_t poly0, int64_t poly1, int64_t poly2, uint32_t N,
+                                                       uint32_t fcq) {
+  const int32_t fc = (int32_t)(fcq & 0xFFFFFu);
+  const __int128 poly = (__int128)poly0 + (__int128)poly1 * N + (__int128)poly2 * N * N;
+  __int128 x = (poly * fc + ((__int128)1 << 31)) >> 32;
+  if (x < 1) x = 1;
+  if (x > (1 << 24)) x = 1 << 24;
+  return (uint32_t)x;
+}
+
+LHD uint32_t realized_len(const Params &p, uint32_t P, uint32_t fcq, uint32_t ra) {
+  uint32_t N = (P * (10000u - ra) + 5000u) / 10000u;  // P < 2^17
+  if (N < 1u) N = 1u;
+  if (p.poly_fast) {
+    const int64_t n = N;
+    const int64_t poly = p.poly0 + p.poly1 * n + p.poly2 * n * n;
+    int64_t x = (poly * (int32_t)(fcq & 0xFFFFFu) + (1ll << 31)) >> 32;
+    x = x < 1 ? 1 : (x > (1 << 24) ? (1 << 24) : x);
+    return (uint32_t)x;
+  }
+  return rewrite_wide(p.poly0, p.poly1, p.poly2, N, fcq);
+}
+
+// slot fields: word (f, s) of this lane at sm[(f * 64 + s) * 32]; the heap follows the fields
+constexpr uint32_t F_PF = 0, F_ARR = 1, F_R = 2, F_IN = 3;
+
+template <bool KV0>
+struct Lane {
+  static constexpr uint32_t kF = kFields<KV0>;
+  // ---- storage
+  uint32_t *sm;    // this lane's word 0 of its warp's slot region (stride 32 words)
+  uint32_t *hist;  // this thread's histograms (global, kLaneHistWords)
+  uint64_t sid;
+  // ---- profile / scenario constants
+  uint32_t t0, knee, slope, kv, maxb, slo_us, pf_ns;
+  uint32_t H;          // horizon (absolute µs, < 2^31)
+  uint32_t w0, w1;     // window [w0, w1), clamped to 32 bits
+  uint32_t drain;
+  // ---- controller (a6)
+  uint32_t law, window, t1, t2, rmin, rmax, nrungs;
+  uint32_t rk[4];  // the ladder, two 16-bit rungs per word (rungs <= 5000 bp)
+  uint32_t r;
+  uint64_t ringA;
+  uint32_t ring_n, ring_pos, rung, active, activations, active_ingests, first_act, last_deact;
+  // the window's samples live in the thread's global scratch (hist + kHistRing);
+  // ev_next is the sample the next full-window ingest evicts, loaded one ingest ahead
+  uint32_t ev_next;
+  uint32_t *series;
+  uint32_t series_n, series_cap, rslot;
+  // ---- clock and serving state (a4, a5, a7)
+  uint32_t T, busy, iter_end, iter_d, ticks, next_done, next_pf;
+  uint64_t iter_align;
+  uint32_t n_ready, B, in_sys, cbase, kq, kr, kstep_q, kstep_r;
+  uint32_t win_now, win_next, stop_static, sec_bound;
+  uint64_t acc_sum;
+  uint32_t acc_cnt;
+  uint64_t pa_sum, pb_sum;  // closed seconds waiting for ingest_pending (npend <= 2)
+  uint32_t pa_cnt, pb_cnt, pa_sec, pb_sec, npend;
+  uint64_t free_m, pf_m, rdy_m;
+  uint64_t rdy_sum;   // sum of the decode-ready slots' prefill ends (their join alignment)
+  uint32_t rdy_kadd;  // sum of their (input + 1) context words (KV term)
+  uint32_t nheap;
+  // ---- queue head (the next accepted arrival) and generator (a2, a3)
+  // the head's raw draws (its table entries, loaded at generation and consumed
+  // at admission, so their L2 latency is off the event loop's critical path):
+  // L, input, F_var, noise, F_comp, similarity noise, the class bits, its index
+  uint32_t head_t, h_L, h_I, h_F, h_N, h_C, h_Q, h_cls, h_j;
+  U4 nu;     // tag-0 block of candidate gen_j (computed one candidate ahead)
+  uint2 nt;  // its log2 table entry (loaded one candidate ahead)
+  uint32_t gen_seg, gen_j, gen_acc, gen_done, gen_fresh, gen_cap, n_seg, seg_off;
+  uint64_t gen_tau, s_ta, s_tb, s_span, s_M;
+  uint32_t s_la, s_lb, s_lmax;
+  uint32_t k0, wid_lo, wid_hi, bypass_mask, min_words;
+  // ---- accounting (a8)
+  uint64_t c_admitted, c_served, c_rewritten, c_slo, c_win_served, c_words_in, c_idle, c_win_words_in,
+      c_win_idle, c_sum_queue, c_sum_ttft, c_sum_e2e, words_out, win_words_out, n_ttft;
+  uint32_t last_j, bypassed, flags, finished;
+  // touched 32-bin groups of each histogram (epilogue scan bound)
+  uint32_t hm_e2e, hm_ttft, hm_r, hm_q;  // hm_q: qa groups in bits 0-7, qi in bits 8-15
+
+  LHD uint32_t &SL(uint32_t f, uint32_t s) const { return sm[(f * 64u + s) * 32u]; }
+  // decode heap: position i is byte i & 3 of heap word i >> 2 (slot indices,
+  // byte loads / stores; the bank is still the lane); the key of slot s is its
+  // completion iteration, kept in the slot's (by then unused) prefill-end word
+  LHD uint8_t &HB(uint32_t i) const { return reinterpret_cast<uint8_t *>(&sm[(kF * 64u + (i >> 2)) * 32u])[i & 3u]; }
+  LHD uint32_t key(uint32_t slot) const { return SL(F_PF, slot); }
+
+  LHD void hist_add(uint32_t off, uint32_t b, uint32_t &mask, uint32_t shift = 0) {
+    red_add(&hist[off + b], 1u);
+    mask |= 1u << ((b >> 5) + shift);
+  }
+
+  // ------------------------------------------------------------------ decode heap
+  // min-heap of the decoding slots by completion iteration (ties in any order:
+  // completions of one iteration are popped together)
+  LHD void heap_push(uint32_t slot, uint32_t k) {
+    uint32_t i = nheap++;
+    while (i > 0) {
+      const uint32_t par = (i - 1u) >> 1;
+      const uint32_t ps = HB(par);
+      if (key(ps) <= k) break;
+      HB(i) = (uint8_t)ps;
+      i = par;
+    }
+    HB(i) = (uint8_t)slot;
+  }
+  LHD uint32_t heap_pop() {
+    const uint32_t top = HB(0);
+    const uint32_t last = HB(--nheap);
+    const uint32_t n = nheap;
+    if (n) {
+      const uint32_t lk = key(last);
+      uint32_t i = 0;
+      for (;;) {
+        uint32_t c = 2u * i + 1u;
+        if (c >= n) break;
+        uint32_t cs = HB(c), ck = key(cs);
+        if (c + 1u < n) {
+          const uint32_t c2 = HB(c + 1u), k2 = key(c2);
+          if (k2 < ck) {
+            c++;
+            cs = c2;
+            ck = k2;
+          }
+        }
+        if (lk <= ck) break;
+        HB(i) = (uint8_t)cs;
+        i = c;
+      }
+      HB(i) = (uint8_t)last;
+    }
+    return top;
+  }
+
+  // ------------------------------------------------------------------ helpers
+  LHD uint32_t rung_at(uint32_t i) const {
+    uint32_t v = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) v = (i == k) ? (rk[k >> 1] >> (16u * (k & 1u))) & 0xFFFFu : v;
+    return v;
+  }
+  LHD void update_window() {
+    win_now = (T >= w0) & (T < w1);
+    win_next = T < w0 ? w0 : (T < w1 ? w1 : kInf);
+    stop_static = H < win_next ? H : win_next;
+  }
+  LHD void batch_changed() {
+    cbase = t0 + slope * (B > knee ? B - knee : 0u);
+    if (KV0) return;
+    const uint32_t ks = kv * B;
+    kstep_q = ks / 1000u;
+    kstep_r = ks - kstep_q * 1000u;
+  }
+  LHD void kv_add(uint64_t x) {
+    if (KV0) return;
+    const uint64_t q = x / 1000u;
+    kr += (uint32_t)(x - q * 1000u);
+    kq += (uint32_t)q;
+    if (kr >= 1000u) {
+      kr -= 1000u;
+      kq++;
+    }
+  }
+  LHD void kv_sub(uint64_t x) {
+    if (KV0) return;
+    const uint64_t q = x / 1000u;
+    const uint32_t rem = (uint32_t)(x - q * 1000u);
+    kq -= (uint32_t)q;
+    if (kr < rem) {
+      kr += 1000u;
+      kq--;
+    }
+    kr -= rem;
+  }
+  // idle interval [a, b) (R18)
+  LHD void idle(uint32_t a, uint32_t b) {
+    c_idle += b - a;
+    const uint32_t lo = a > w0 ? a : w0, hi = b < w1 ? b : w1;
+    if (hi > lo) c_win_idle += hi - lo;
+  }
+
+  // ------------------------------------------------------------------ a6
+  // one controller ingest of the closed second ending at `sec` with
+  // accumulator (sum, cnt) (R3-R5, R12, R21, R38)
+  LHD void ingest(uint64_t sum, uint32_t cnt, uint32_t sec) {
+    // the sample: floor(sum / cnt) truncated to 32 bits
+    const uint32_t x = (uint32_t)div_u64(sum, cnt);
+    if (series) {
+      if (series_n < series_cap) series[series_n] = x;
+      else flags |= BELLMAN_FLAG_SERIES_OVERFLOW;
+      series_n++;
+    }
+    if (law != BELLMAN_LAW_MAP && law != BELLMAN_LAW_STEP) return;
+    const uint32_t was = active;
+    uint32_t k = ring_n;
+    uint64_t A = ringA;
+    if (k < window) {
+      k++;
+      A += x;
+    } else {
+      A = A + x - ev_next;
+    }
+    const uint32_t act = A >= (uint64_t)k * t1 ? 1u : 0u;  // non-strict (R38)
+    uint32_t nr = 0;
+    if (act) {
+      if (law == BELLMAN_LAW_MAP) {
+        // r_min + floor((r_max - r_min)(A - k t1) / (k (t2 - t1))), capped at r_max
+        const uint64_t ex = A - (uint64_t)k * t1, den = (uint64_t)k * (t2 - t1);
+        if (ex >= den) {
+          nr = rmax;  // the quotient is >= r_max - r_min
+        } else {  // quotient < r_max - r_min <= 5000; den < 2^35
+          nr = rmin + (uint32_t)div_u64((uint64_t)(rmax - rmin) * ex, den);
+          if (nr > rmax) nr = rmax;
+        }
+        if (nrungs) {  // largest rung <= r (R5)
+          uint32_t best = rk[0] & 0xFFFFu;
+#pragma unroll
+          for (uint32_t i = 1; i < 8; ++i) {
+            const uint32_t g = (rk[i >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
+            if (i < nrungs && g <= nr) best = g;
+          }
+          nr = best;
+        }
+      } else {  // STEP: rung 0 on activation, one rung up per ingest while active
+        rung = was ? (rung + 1u < nrungs ? rung + 1u : rung) : 0u;
+        nr = rung_at(rung);
+      }
+    }
+    hist[kHistRing + ring_pos] = x;
+    ring_pos = ring_pos + 1u == window ? 0u : ring_pos + 1u;
+    ev_next = hist[kHistRing + ring_pos];  // read after the store (window 1: the same word)
+    ring_n = k;
+    ringA = A;
+    active = act;
+    activations += (act && !was) ? 1u : 0u;
+    active_ingests += act;
+    if (act != was) {  // the log is kept by second index (R21)
+      const uint32_t second = sec / 1000000u - 1u;
+      if (act) {
+        if (first_act == kNone) first_act = second;
+      } else {
+        last_deact = second;
+      }
+    }
+    r = nr;
+  }
+
+  // Closed seconds wait in a two-entry queue and are ingested, in order, at
+  // one site per trip (ingest_pending, right after advance): the controller's
+  // output r is read only at admissions, which come after that site, so the
+  // deferral changes nothing — but every lane's ingests run at the same place
+  // of the loop, not at two (advance and the leap), which halves the warp's
+  // divergent passes over the controller code.  A leap queues at most one
+  // second (it stops before a second crossing once the queue is not empty).
+  LHD void push_second(uint64_t sum, uint32_t cnt, uint32_t sec) {
+    if (npend == 0) {
+      pa_sum = sum;
+      pa_cnt = cnt;
+      pa_sec = sec;
+    } else {
+      pb_sum = sum;
+      pb_cnt = cnt;
+      pb_sec = sec;
+    }
+    npend++;
+  }
+  LHD void ingest_pending() {
+#pragma unroll 1
+    for (uint32_t i = 0; i < npend; ++i) {
+      if (i == 0) ingest(pa_sum, pa_cnt, pa_sec);
+      else ingest(pb_sum, pb_cnt, pb_sec);
+    }
+    npend = 0;
+  }
+  // close the open second (queued if it holds samples) and open the one containing t
+  LHD void roll_second(uint32_t t) {
+    if (t < sec_bound) return;
+    if (acc_cnt) push_second(acc_sum, acc_cnt, sec_bound);
+    acc_sum = 0;
+    acc_cnt = 0;
+    const uint32_t nb = sec_bound + 1000000u;
+    sec_bound = t < nb ? nb : (t / 1000000u + 1u) * 1000000u;
+  }
+
+  LHD void advance(uint32_t t) {
+    T = t;
+    const uint32_t b = sec_bound < win_next ? sec_bound : win_next;
+    if (t < b) return;
+    roll_second(t);
+    if (t >= win_next) update_window();
+  }
+
+  // ------------------------------------------------------------------ a2 + a3
+  LHD void load_seg(const Params &p) {
+    const DevSeg &S = p.segs[seg_off + gen_seg];
+    s_ta = S.ta;
+    s_tb = S.tb;
+    s_span = S.span;
+    s_M = S.M;
+    s_la = S.la;
+    s_lb = S.lb;
+    s_lmax = S.lmax;
+  }
+  // the tag-0 block of candidate gen_j and its log2 table entry
+  LHD void prefetch(const Params &p) {
+    nu = philox(k0, kSeedHi, gen_j, 0u, wid_lo, wid_hi);
+    uint32_t e;
+    nt = ldg(&p.log2tab[neglog_split(nu.x, e) >> 20]);
+  }
+  // Next candidate of the stream (P:183 Poisson, S:83 thinning; R17, R32, R33):
+  // returns false when the generator is exhausted, else the candidate's index
+  // j, time tau, its tag-0 block u and whether thinning accepted it.
+  LHD bool candidate(const Params &p, uint32_t &j, uint64_t &tau, U4 &u, bool &acc) {
+    for (;;) {
+      if (gen_seg >= n_seg) {
+        gen_done = 1;
+        return false;
+      }
+      if (gen_fresh) {
+        load_seg(p);
+        gen_tau = s_ta;
+        gen_fresh = 0;
+      }
+      j = gen_j++;
+      u = nu;
+      const uint2 t = nt;
+      prefetch(p);  // candidate j + 1
+      tau = gen_tau + mulhi64(neglog_q32(u.x, t), s_M);
+      if (tau >= s_tb) {  // the crossing candidate is consumed (R17)
+        gen_seg++;
+        gen_fresh = 1;
+        continue;
+      }
+      gen_tau = tau;
+      // thinning: u1 lmax span < (la (tb - tau) + lb (tau - ta)) 2^32, in 128 bits
+      const uint64_t x = (uint64_t)u.y * s_lmax;
+      const uint64_t lhs_hi = mulhi64(x, s_span), lhs_lo = x * s_span;
+      const uint64_t y = (uint64_t)s_la * (s_tb - tau) + (uint64_t)s_lb * (tau - s_ta);
+      const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
+      acc = lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
+      if (acc) {
+        gen_acc++;
+        if (gen_cap && gen_acc >= gen_cap) gen_done = 1;  // the capped arrival is still delivered
+      }
+      return true;
+    }
+  }
+  // the queue head becomes the next accepted arrival (or none: head_t = INF)
+  LHD void next_head(const Params &p) {
+    for (;;) {
+      if (gen_done) {
+        head_t = kInf;
+        return;
+      }
+      uint32_t j;
+      uint64_t tau;
+      U4 u;
+      bool acc;
+      if (!candidate(p, j, tau, u, acc)) {
+        head_t = kInf;
+        return;
+      }
+      if (!acc) continue;
+      // the request's attributes and its own draws (a3: tag-1 block): loads issued now, used at admission
+      h_L = (uint32_t)ldg(&p.tabL[u.z >> 20]);
+      h_I = (uint32_t)ldg(&p.tabI[u.w >> 20]);
+      h_cls = u.z & 0xFFFFFu;  // class draw (NEXT-3): the bits below L's index
+      const U4 v = philox(k0, kSeedHi, j, 1u, wid_lo, wid_hi);
+      h_F = (uint32_t)ldg(&p.tabF[v.x >> 20]);
+      h_N = (uint32_t)ldg(&p.tabN[v.y >> 20]);
+      h_C = (uint32_t)ldg(&p.tabC[v.z >> 20]);
+      h_Q = (uint32_t)ldg(&p.tabQ[v.w >> 20]);
+      h_j = j;
+      head_t = tau < kFar ? (uint32_t)tau : kFar;
+      return;
+    }
+  }
+
+  // ------------------------------------------------------------------ a1 scenario decode
+  LHD void init(const Params &p, uint64_t id, uint32_t *smem_lane, uint32_t *hist_lane) {
+    sm = smem_lane;
+    hist = hist_lane;
+    sid = id;
+    const bellman_scenario sc = p.sc[id];
+    const bellman_ctrl &cc = p.ctrls[sc.ctrl];
+    const bellman_profile &pr = p.profs[sc.profile];
+    const DevTrace tr = p.traces[sc.trace];
+    t0 = pr.t0_us;
+    knee = pr.knee;
+    slope = pr.slope_us;
+    kv = KV0 ? 0u : pr.kv_ns_per_word;
+    maxb = pr.max_batch;
+    pf_ns = pr.prefill_ns_per_word;
+    slo_us = cc.slo_us;
+    H = (uint32_t)sc.horizon_us;
+    w0 = sc.w0_us <= 0 ? 0u : (sc.w0_us >= (int64_t)kFar ? kFar : (uint32_t)sc.w0_us);
+    w1 = sc.w1_us <= 0 ? 0u : (sc.w1_us >= (int64_t)kFar ? kFar : (uint32_t)sc.w1_us);
+    drain = sc.mode == BELLMAN_MODE_DRAIN;
+    // a10: thresholds from the paired unbounded run's calibration
+    law = cc.law;
+    t1 = cc.t1;
+    t2 = cc.t2;
+    flags = 0;
+    if (cc.calibrated) {
+      const uint32_t *cb = p.calib + 4u * p.series_slot[sc.calib_src];
+      t1 = cb[0];
+      t2 = cb[1];
+      if (cb[2] != 0) {
+        law = BELLMAN_LAW_OFF;
+        flags |= BELLMAN_FLAG_DEGENERATE_CALIB;
+      }
+    }
+    window = cc.window;
+    rmin = cc.r_min_bp;
+    rmax = cc.r_max_bp;
+    nrungs = cc.n_rungs;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rk[k] = cc.rungs_bp[2 * k] | (cc.rungs_bp[2 * k + 1] << 16);
+    r = law == BELLMAN_LAW_CONST ? cc.r_const_bp : 0u;
+    ringA = 0;
+    ring_n = ring_pos = rung = active = activations = active_ingests = 0;
+    first_act = last_deact = kNone;
+    ev_next = 0;
+    rslot = p.series_slot[id];
+    series = rslot != kNone ? p.series + p.series_off[rslot] : nullptr;
+    series_cap = rslot != kNone ? p.series_cap[rslot] : 0u;
+    series_n = 0;
+    // the per-second signal feeds only the controller (MAP / STEP) and the recorder
+    sec_bound = (law >= BELLMAN_LAW_MAP || rslot != kNone) ? 1000000u : kInf;
+    acc_sum = 0;
+    acc_cnt = 0;
+    npend = 0;
+    pa_sum = pb_sum = 0;
+    pa_cnt = pb_cnt = pa_sec = pb_sec = 0;
+    T = 0;
+    busy = 0;
+    iter_end = kInf;
+    iter_d = 0;
+    iter_align = 0;
+    ticks = 0;
+    next_done = kInf;
+    next_pf = kInf;
+    n_ready = B = in_sys = 0;
+    kq = kr = kstep_q = kstep_r = 0;
+    batch_changed();
+    update_window();
+    free_m = maxb >= 64u ? ~0ull : ((1ull << maxb) - 1ull);
+    pf_m = rdy_m = 0;
+    rdy_sum = 0;
+    rdy_kadd = 0;
+    nheap = 0;
+    // generator
+    k0 = sc.seed_index;
+    wid_lo = (uint32_t)sc.wid;
+    wid_hi = (uint32_t)(sc.wid >> 32);
+    bypass_mask = cc.bypass_mask;
+    min_words = cc.min_words_bypass;
+    n_seg = tr.n_seg;
+    seg_off = tr.seg_off;
+    gen_cap = tr.cap;
+    gen_seg = gen_j = gen_acc = gen_done = 0;
+    gen_fresh = 1;
+    gen_tau = 0;
+    prefetch(p);  // candidate 0
+    c_admitted = c_served = c_rewritten = c_slo = c_win_served = c_words_in = c_idle = c_win_words_in = 0;
+    c_win_idle = c_sum_queue = c_sum_ttft = c_sum_e2e = words_out = win_words_out = n_ttft = 0;
+    last_j = bypassed = finished = 0;
+    hm_e2e = hm_ttft = hm_r = hm_q = 0;
+    next_head(p);
+  }
+
+  // ------------------------------------------------------------------ a5
+  LHD void iteration_words() {
+    words_out += B;
+    if (win_now) win_words_out += B;
+    acc_sum += (uint64_t)B * iter_d + iter_align;  // TBT: the B gaps of this end
+    acc_cnt += B;
+    if (!KV0) {
+      kr += kstep_r;
+      kq += kstep_q;
+      if (kr >= 1000u) {
+        kr -= 1000u;
+        kq++;
+      }
+    }
+  }
+
+  LHD void iteration_end() {
+    iteration_words();
+    const uint32_t it = ticks - 1u;
+    if (it == next_done) {
+      uint64_t se = 0;
+      uint32_t ndone = 0, nslo = 0, kd = 0;
+      do {
+        const uint32_t s = heap_pop();
+        const uint32_t e = T - SL(F_ARR, s);
+        se += e;
+        nslo += e > slo_us ? 1u : 0u;
+        ndone++;
+        if (!KV0) kd += SL(F_IN, s) + SL(F_R, s);
+        hist_add(kHistE2E, lat_bin(e), hm_e2e);
+        free_m |= 1ull << s;
+      } while (nheap && key(HB(0)) == it);
+      next_done = nheap ? key(HB(0)) : kInf;
+      if (!KV0) kv_sub((uint64_t)kv * kd);
+      c_served += ndone;
+      c_sum_e2e += se;
+      c_slo += nslo;
+      if (win_now) c_win_served += ndone;
+      in_sys -= ndone;
+      B -= ndone;
+      batch_changed();
+    }
+    busy = 0;
+  }
+
+  // prefill ends at instants in [T, lim): first words, R = 1 completions (R9)
+  LHD void prefill_end(uint32_t lim) {
+    uint64_t m = pf_m, st = 0, se = 0;
+    uint32_t mpf = kInf, nfirst = 0, n1 = 0, nslo = 0;
+    // software-pipelined over the prefilling slots: the next slot's fields are
+    // loaded before the current one is processed (pf_m is non-empty here)
+    uint32_t s = ffs64(m) - 1u;
+    m &= m - 1ull;
+    uint32_t key = SL(F_PF, s), arr = SL(F_ARR, s), R = SL(F_R, s);
+    for (;;) {
+      const bool more = m != 0;
+      uint32_t s2 = 0, key2 = 0, arr2 = 0, R2 = 0;
+      if (more) {
+        s2 = ffs64(m) - 1u;
+        m &= m - 1ull;
+        key2 = SL(F_PF, s2);
+        arr2 = SL(F_ARR, s2);
+        R2 = SL(F_R, s2);
+      }
+      if (key < lim) {
+        const uint32_t tt = key - arr;
+        const uint32_t lb = lat_bin(tt);
+        st += tt;
+        nfirst++;
+        hist_add(kHistTTFT, lb, hm_ttft);
+        const uint64_t bit = 1ull << s;
+        pf_m &= ~bit;
+        if (R == 1u) {  // R9: completes at the prefill end
+          se += tt;
+          nslo += tt > slo_us ? 1u : 0u;
+          n1++;
+          hist_add(kHistE2E, lb, hm_e2e);
+          free_m |= bit;
+        } else {
+          rdy_m |= bit;
+          rdy_sum += key;
+          if (!KV0) rdy_kadd += SL(F_IN, s) + 1u;
+          n_ready++;
+        }
+      } else if (key < mpf) {
+        mpf = key;
+      }
+      if (!more) break;
+      s = s2;
+      key = key2;
+      arr = arr2;
+      R = R2;
+    }
+    next_pf = mpf;
+    n_ttft += nfirst;
+    c_sum_ttft += st;
+    words_out += nfirst;
+    if (win_now) win_words_out += nfirst;
+    if (n1) {
+      c_served += n1;
+      c_sum_e2e += se;
+      c_slo += nslo;
+      if (win_now) c_win_served += n1;
+      in_sys -= n1;
+    }
+  }
+
+  // ------------------------------------------------------------------ a7 (+a3)
+  // FIFO admission at an admission point (R7).  Precondition: in_sys < maxb, head_t <= T.
+  LHD void admit(const Params &p) {
+    const uint32_t Tn = T;
+    uint32_t n = 0, n_byp = 0;
+    do {
+      // the head's draws (a3): U = max(1, round(L F_var)) (R14), P = max(1, L + noise)
+      // (S:121), F_comp | similarity noise, prefill max(1, floor(pf_ns in / 1000))
+      const uint32_t a = head_t, in = h_I, L = h_L;
+      const uint64_t U64 = ((uint64_t)L * h_F + 32768u) >> 16;
+      const uint32_t U = U64 < 1 ? 1u : (uint32_t)U64;
+      const int32_t P0 = (int32_t)L + (int32_t)h_N;
+      const uint32_t P = P0 < 1 ? 1u : (uint32_t)P0;
+      const uint32_t fcq = h_C | ((h_Q + 2048u) << 20);
+      const uint32_t pf0 = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
+      const uint32_t pf = pf0 < 1u ? 1u : pf0;
+      const uint32_t cls =
+          h_cls < p.class_cum0 ? 0u : (h_cls < p.class_cum1 ? 1u : (h_cls < p.class_cum2 ? 2u : 3u));
+      // r applied to this request: r unless a bypass rule holds (NEXT-3)
+      const bool byp = r > 0 && (((bypass_mask >> cls) & 1u) || P < min_words);
+      const uint32_t ra = byp ? 0u : r;
+      uint32_t R = U, qb;
+      if (ra > 0) {
+        R = realized_len(p, P, fcq, ra);
+        int32_t base;
+        const int64_t num = ((int64_t)U - (int64_t)R) * 10000, den = U;
+        if (num <= (int64_t)p.q_safe * den) {
+          base = (int32_t)p.q_active;
+        } else if (num >= (int64_t)p.q_end * den) {
+          base = (int32_t)p.q_floor;
+        } else {
+          base = sim_decay(p.q_active, p.q_floor, (uint64_t)(num - (int64_t)p.q_safe * den),
+                           (uint64_t)(p.q_end - p.q_safe) * (uint64_t)den);
+        }
+        int32_t sc = base + (int32_t)(fcq >> 20) - 2048;
+        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+        qb = (uint32_t)sc / 50u;
+        c_rewritten++;
+        hist_add(kHistR, ra / 10u < BELLMAN_HIST_R ? ra / 10u : BELLMAN_HIST_R - 1u, hm_r);
+        hist_add(kHistQA, qb, hm_q);
+      } else {  // not rewritten: the inactive base plus the noise
+        int32_t sc = (int32_t)p.q_inactive + (int32_t)(fcq >> 20) - 2048;
+        sc = sc < 0 ? 0 : (sc > 10000 ? 10000 : sc);
+        qb = (uint32_t)sc / 50u;
+        hist_add(kHistQI, qb, hm_q, 8u);
+      }
+      n_byp += byp ? 1u : 0u;
+      const uint32_t s = ffs64(free_m) - 1u;
+      const uint64_t bit = 1ull << s;
+      free_m &= ~bit;
+      pf_m |= bit;
+      const uint32_t pe = Tn + pf;
+      SL(F_PF, s) = pe;
+      SL(F_ARR, s) = a;
+      SL(F_R, s) = R;
+      if (!KV0) SL(F_IN, s) = in;
+      if (pe < next_pf) next_pf = pe;
+      c_words_in += in;
+      if (win_now) c_win_words_in += in;
+      c_sum_queue += Tn - a;
+      n++;
+      in_sys++;
+      last_j = h_j + 1u;
+      next_head(p);
+    } while (in_sys < maxb && head_t <= Tn);
+    c_admitted += n;
+    bypassed += n_byp;
+  }
+
+  // ------------------------------------------------------------------ a4/a5 leap
+  // the longest run of uneventful iterations in bulk (K2's leap, scalar)
+  LHD void leap() {
+    uint32_t stop = next_pf < stop_static ? next_pf : stop_static;
+    if (in_sys < maxb && head_t < stop) stop = head_t;
+    const uint32_t nmax = next_done - ticks;  // iterations ticks .. next_done-1 complete nobody
+    if (nmax == 0 || stop <= T + 1u) return;
+    const uint32_t cb = cbase, qs = kstep_q, rs = kstep_r;
+    uint32_t q = KV0 ? 0u : kq, rr = KV0 ? 0u : kr, done = 0;
+    for (;;) {
+      const uint32_t lim = stop < sec_bound ? stop : sec_bound;
+      const uint32_t room = lim - 1u - T;
+      const uint32_t left = nmax - done;
+      uint32_t n = 0, used = 0;
+      if (KV0) {
+        const uint32_t nn = room / cb;
+        n = nn < left ? nn : left;
+        used = n * cb;
+      } else {
+        while (n < left) {
+          const uint32_t d = cb + q;
+          if (d > room - used) break;
+          used += d;
+          rr += rs;
+          const uint32_t carry = rr >= 1000u ? 1u : 0u;
+          rr -= carry ? 1000u : 0u;
+          q += qs + carry;
+          n++;
+        }
+      }
+      const uint64_t words = (uint64_t)n * B;
+      ticks += n;
+      T += used;
+      words_out += words;
+      if (win_now) win_words_out += words;
+      acc_sum += (uint64_t)B * used;
+      acc_cnt += (uint32_t)words;
+      done += n;
+      const uint32_t tnext = T + (cb + q);
+      if ((done == nmax) | (tnext >= stop) | (tnext < sec_bound) | (npend != 0)) break;
+      roll_second(tnext);
+    }
+    if (!KV0) {
+      kq = q;
+      kr = rr;
+    }
+  }
+
+  // ------------------------------------------------------------------ a4
+  LHD void start_iteration() {
+    const uint32_t Tn = T;
+    uint64_t align = 0;
+    if (n_ready) {
+      const uint32_t it0 = ticks;
+      uint64_t m = rdy_m;
+      while (m) {
+        const uint32_t s = ffs64(m) - 1u;
+        m &= m - 1ull;
+        // words 2..R at the ends of iterations it0 .. it0 + R - 2
+        const uint32_t k = it0 + SL(F_R, s) - 2u;
+        SL(F_PF, s) = k;
+        heap_push(s, k);
+      }
+      rdy_m = 0;
+      align = (uint64_t)n_ready * Tn - rdy_sum;
+      rdy_sum = 0;
+      next_done = key(HB(0));
+      if (!KV0) {
+        kv_add((uint64_t)kv * rdy_kadd);
+        rdy_kadd = 0;
+      }
+      B += n_ready;
+      n_ready = 0;
+      batch_changed();
+    }
+    const uint32_t d = cbase + (KV0 ? 0u : kq);
+    iter_d = d;
+    iter_align = align;
+    iter_end = Tn + d;
+    busy = 1;
+    ticks++;
+  }
+
+  LHD bool quiet_end() {
+    const uint32_t te = iter_end;
+    uint32_t lim = stop_static < sec_bound ? stop_static : sec_bound;
+    lim = lim < next_pf ? lim : next_pf;
+    if ((te >= lim) | (ticks - 1u == next_done) | ((in_sys < maxb) & (head_t <= te))) return false;
+    T = te;
+    iteration_words();
+    busy = 0;
+    return true;
+  }
+
+  // ------------------------------------------------------------------ one event trip
+  // Returns true when the scenario's event loop is over (finished: drained).
+  LHD bool trip(const Params &p) {
+    uint32_t tn;
+    bool mid = false;
+    if (busy) {
+      // prefill ends due inside the running iteration, in the open second and
+      // window: handled now (order-free until the iteration end)
+      uint32_t lim = iter_end < stop_static ? iter_end : stop_static;
+      if (sec_bound < lim) lim = sec_bound;
+      if (next_pf < lim) prefill_end(lim);
+      mid = next_pf < iter_end;
+      tn = mid ? next_pf : iter_end;
+    } else {
+      tn = next_pf;
+      if (in_sys < maxb && head_t < tn) tn = head_t;
+      if (tn == kInf) {
+        finished = 1;
+        return true;
+      }
+    }
+    if ((tn >= H) | (in_sys == 0)) {
+      if (tn >= H) return true;
+      idle(T, tn);
+    }
+    advance(tn);
+    ingest_pending();
+    if (busy && !mid) iteration_end();
+    if (next_pf == tn) {
+      uint32_t lim = tn + 1u;
+      if (mid) {
+        lim = iter_end < stop_static ? iter_end : stop_static;
+        if (sec_bound < lim) lim = sec_bound;
+      }
+      prefill_end(lim);
+      if (mid) return false;
+    }
+    if (in_sys < maxb && head_t <= tn) admit(p);
+    if (n_ready + B > 0) {
+      bool join;
+      do {
+        join = n_ready != 0;
+        if (!join) leap();
+        start_iteration();
+      } while (join && quiet_end());
+    }
+    return false;
+  }
+
+  // ------------------------------------------------------------------ a9 histogram scan
+  // Walk the touched groups of one histogram in bin order: nearest-rank
+  // percentiles (k = ceil(p n / 100), the first bin whose
+  // cumulative count reaches k), the segment merge (integer atomics) and the
+  // re-zeroing of the groups for the thread's next scenario.
+  LHD void scan(uint32_t off, uint32_t nb, uint32_t mask, uint64_t n, uint32_t p0, uint32_t p1, uint32_t &b0,
+                uint32_t &b1, unsigned long long *seg) {
+    const uint64_t k0v = ((uint64_t)p0 * n + 99u) / 100u, k1v = ((uint64_t)p1 * n + 99u) / 100u;
+    const uint64_t ka = k0v < 1 ? 1 : k0v, kb = k1v < 1 ? 1 : k1v;
+    b0 = b1 = kNone;
+    uint64_t cum = 0;
+    while (mask) {
+      const uint32_t g = ffs32(mask) - 1u;
+      mask &= mask - 1u;
+      uint4 *v4 = reinterpret_cast<uint4 *>(hist + off + 32u * g);
+#pragma unroll 1
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint4 v = v4[i];
+        if ((v.x | v.y | v.z | v.w) == 0) continue;
+        const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          if (!c[k]) continue;
+          const uint32_t b = 32u * g + 4u * i + k;
+          cum += c[k];
+          seg_add(&seg[b], c[k]);
+          if (b0 == kNone && cum >= ka) b0 = b;
+          if (p1 && b1 == kNone && cum >= kb) b1 = b;
+        }
+        v4[i] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    (void)nb;
+    if (n == 0) b0 = b1 = kNone;
+  }
+
+  // ------------------------------------------------------------------ termination, a8, a9
+  LHD void finish(const Params &p) {
+    const bellman_scenario &sc = p.sc[sid];
+    const bellman_profile &pr = p.profs[sc.profile];
+    // R20: a drained run ends at its last event, a cutoff run at H
+    const uint32_t end = (drain && finished) ? T : H;
+    if (in_sys == 0) idle(T, end);
+    if (sec_bound != kInf && sec_bound <= end && acc_cnt) push_second(acc_sum, acc_cnt, sec_bound);
+    ingest_pending();
+    // queued at the end: accepted arrivals before `end` not admitted
+    uint64_t queued = 0;
+    if (head_t != kInf && head_t < end) {
+      queued = 1;
+      last_j = h_j + 1u;
+      while (!gen_done) {  // the rest of the stream is only counted (tag-0 draws, thinning)
+        uint32_t j;
+        uint64_t tau;
+        U4 u;
+        bool acc;
+        if (!candidate(p, j, tau, u, acc)) break;
+        if (!acc) continue;
+        if (tau >= end) break;
+        queued++;
+        last_j = j + 1u;
+      }
+    }
+    if (series) p.series_n[rslot] = series_n;
+    unsigned long long *seg = p.seg_hist + (uint64_t)sc.segment * kSegWords;
+    uint32_t e50, e99, f50, f99, rm, qa, qi, dummy;
+    scan(kHistE2E, BELLMAN_HIST_LAT, hm_e2e, c_served, 50u, 99u, e50, e99, seg);
+    scan(kHistTTFT, BELLMAN_HIST_LAT, hm_ttft, n_ttft, 50u, 99u, f50, f99, seg + BELLMAN_HIST_LAT);
+    scan(kHistR, BELLMAN_HIST_R, hm_r, c_rewritten, 50u, 0u, rm, dummy, seg + 2 * BELLMAN_HIST_LAT);
+    scan(kHistQA, BELLMAN_HIST_Q, hm_q & 0xFFu, c_rewritten, 50u, 0u, qa, dummy,
+         seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R);
+    scan(kHistQI, BELLMAN_HIST_Q, hm_q >> 8, c_admitted - c_rewritten, 50u, 0u, qi, dummy,
+         seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q);
+    bellman_scenario_stats o;
+    o.scenario_id = sid;
+    o.ticks = ticks;
+    o.candidates = last_j;
+    o.arrivals = c_admitted + queued;
+    o.admitted = c_admitted;
+    o.served = c_served;
+    o.rewritten = c_rewritten;
+    o.words_in = c_words_in;
+    o.words_out = words_out;
+    o.idle_us = c_idle;
+    o.end_us = end;
+    o.queued_end = queued;
+    o.inflight_end = in_sys;
+    o.win_served = c_win_served;
+    o.win_words_in = c_win_words_in;
+    o.win_words_out = win_words_out;
+    o.win_idle_us = c_win_idle;
+    o.sum_queue_us = c_sum_queue;
+    o.sum_ttft_us = c_sum_ttft;
+    o.sum_e2e_us = c_sum_e2e;
+    o.slo_violations = c_slo;
+    o.e2e_p50_ms = e50 == kNone ? kNone : lat_edge(e50);
+    o.e2e_p99_ms = e99 == kNone ? kNone : lat_edge(e99);
+    o.ttft_p50_ms = f50 == kNone ? kNone : lat_edge(f50);
+    o.ttft_p99_ms = f99 == kNone ? kNone : lat_edge(f99);
+    o.median_r_bp = rm == kNone ? kNone : rm * 10u;
+    o.t1 = t1;
+    o.t2 = t2;
+    o.activations = activations;
+    o.first_act_s = first_act;
+    o.last_deact_s = last_deact;
+    o.active_ingests = active_ingests;
+    uint32_t fl = flags | BELLMAN_FLAG_DONE;
+    if (queued + in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
+    o.flags = fl;
+    o.segment = sc.segment;
+    o.bypassed = bypassed;
+    // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
+#ifdef __CUDA_ARCH__
+    const double a = __dmul_rn(pr.e_in_j_per_word, (double)c_words_in);
+    const double b = __dmul_rn(pr.e_out_j_per_word, (double)words_out);
+    const double c = __dmul_rn(pr.p_idle_w, (double)c_idle);
+    o.energy_j = __dadd_rn(__dadd_rn(a, b), __ddiv_rn(c, 1e6));
+    const double wa = __dmul_rn(pr.e_in_j_per_word, (double)c_win_words_in);
+    const double wb = __dmul_rn(pr.e_out_j_per_word, (double)win_words_out);
+    const double wc = __dmul_rn(pr.p_idle_w, (double)c_win_idle);
+    o.win_energy_j = __dadd_rn(__dadd_rn(wa, wb), __ddiv_rn(wc, 1e6));
+#else
+    o.energy_j = (pr.e_in_j_per_word * (double)c_words_in + pr.e_out_j_per_word * (double)words_out) +
+                 (pr.p_idle_w * (double)c_idle) / 1e6;
+    o.win_energy_j = (pr.e_in_j_per_word * (double)c_win_words_in + pr.e_out_j_per_word * (double)win_words_out) +
+                     (pr.p_idle_w * (double)c_win_idle) / 1e6;
+#endif
+    o.sim_active_p50 = qa == kNone ? kNone : qa * 50u;
+    o.sim_inactive_p50 = qi == kNone ? kNone : qi * 50u;
+    o.scored_active = c_rewritten;
+    o.scored_inactive = c_admitted - c_rewritten;
+    o.preemptions = 0;
+    o._pad2 = 0;
+    o.recompute_words = 0;
+    p.stats[sid] = o;
+#ifdef __CUDA_ARCH__
+    if (p.n_peer) {  // fused exchange (§8(e)): the record to every rank's array over peer memory
+      const uint4 *src = reinterpret_cast<const uint4 *>(&o);
+      for (uint32_t g = 0; g < p.n_peer; ++g) {
+        uint4 *dst = reinterpret_cast<uint4 *>(&p.peer[g][sid]);
+#pragma unroll
+        for (uint32_t c2 = 0; c2 < sizeof(bellman_scenario_stats) / 16; ++c2) dst[c2] = src[c2];
+      }
+      __threadfence_system();
+    }
+#endif
+  }
+};
+
+// Whether scenario `sid` belongs to lane kernel `kind` (3 or 4) in this pass.
+LHD bool mine(const Params &p, uint64_t sid, uint32_t kind) {
+  const bellman_scenario &sc = p.sc[sid];
+  const bellman_ctrl &cc = p.ctrls[sc.ctrl];
+  if ((cc.calibrated != 0) != (p.pass == 2)) return false;
+  return scenario_kind_of(sc, cc, p.profs[sc.profile], p.traces[sc.trace].kind, p.lane_on) == kind;
+}
+
+}  // namespace lane
+
+// ---------------------------------------------------------------------------
+// K2L: persistent, one CTA of kLaneWarps<KV0> warps per SM; every lane fetches
+// scenario ids (warp-aggregated atomics on the launch's counter), heavy-first
+// through p.order, and runs them one after another.
+using lane::FULL_MASK;
+template <bool KV0>
+__global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(16) uint32_t lane_smem[];
+  uint32_t lane_id;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane_id));
+  uint32_t *smem = lane_smem + (threadIdx.x >> 5) * kLaneWarpWords<KV0> + lane_id;
+  uint32_t *hist = p.lane_hist + (uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * kLaneHistWords;
+  const uint32_t kind = KV0 ? 3u : 4u;
+  lane::Lane<KV0> L;
+  bool has = false, alive = true;
+  const uint32_t lt = (1u << lane_id) - 1u;
+  // Every iteration starts with a warp-wide vote, so the 32 lanes reconverge
+  // once per trip (otherwise lanes that finish a trip early run ahead into the
+  // next one and the warp splits into groups that issue separately).  Lanes
+  // without a scenario fetch one: warp-aggregated atomics on the counter.
+  for (;;) {
+    const uint32_t need = __ballot_sync(FULL_MASK, !has && alive);
+    if (need) {
+      uint32_t base = 0;
+      if (lane_id == (uint32_t)__ffs((int)need) - 1u) base = atomicAdd(p.counter, (unsigned)__popc(need));
+      base = __shfl_sync(FULL_MASK, base, __ffs((int)need) - 1);
+      if (!has && alive) {
+        const uint32_t kidx = base + (uint32_t)__popc(need & lt);
+        if ((uint64_t)kidx >= p.count) {
+          alive = false;
+        } else {
+          const uint64_t sid = p.order ? (uint64_t)p.order[kidx] : p.first + (uint64_t)kidx * p.stride;
+          if (lane::mine(p, sid, kind)) {
+            L.init(p, sid, smem, hist);
+            has = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(FULL_MASK, has || alive)) break;
+    if (has && L.trip(p)) {
+      L.finish(p);
+      has = false;
+    }
+  }
+}
+
+#ifdef BELLMAN_LANECHECK
+// Development only: the same per-scenario code on the CPU (one scenario at a time).
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist) {
+  const bellman_profile &pr = p.profs[p.sc[sid].profile];
+  if (pr.kv_ns_per_word == 0) {
+    lane::Lane<true> L;
+    L.init(p, sid, smem_warp, hist);
+    while (!L.trip(p)) {
+    }
+    L.finish(p);
+  } else {
+    lane::Lane<false> L;
+    L.init(p, sid, smem_warp, hist);
+    while (!L.trip(p)) {
+    }
+    L.finish(p);
+  }
+}
+#endif
+
+}  // namespace bellman
+
+int bellman_lane_grid(int device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return sms < (int)bellman::kLaneMaxCtas ? sms : (int)bellman::kLaneMaxCtas;
+}
+
+cudaError_t bellman_launch_lane(const bellman::Params &p, int grid, int kind, cudaStream_t stream) {
+  using namespace bellman;
+  if (kind == 3) {
+    const size_t smem = sizeof(uint32_t) * kLaneWarpWords<true> * kLaneWarps<true>;
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(bellman_lane_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    bellman_lane_kernel<true><<<grid, 32 * kLaneWarps<true>, smem, stream>>>(p);
+  } else {
+    const size_t smem = sizeof(uint32_t) * kLaneWarpWords<false> * kLaneWarps<false>;
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(bellman_lane_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    bellman_lane_kernel<false><<<grid, 32 * kLaneWarps<false>, smem, stream>>>(p);
+  }
+  return cudaGetLastError();
+}

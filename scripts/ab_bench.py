@@ -15,6 +15,7 @@ from paper_2510_15330_b200 import _abi, sim  # noqa: E402
 
 
 def main(paths, reps=15):
+    reps = int(os.environ.get("AB_REPS", reps))
     # AB_WL: Python expression over W building the workload (default C2)
     cols = eval(os.environ.get("AB_WL", "W.config_c2()"), {"W": W}).columns()
     pk = sim.pack(cols)

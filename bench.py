@@ -148,12 +148,14 @@ def latency_floor(w, pk, ws, local, stream, kernel_ms):
                     "serial-latency floor of the whole launch; frac = floor / measured kernel time"}
 
 
-def ncu_traffic(name: str):
-    """DRAM bytes (read + write) per tick-kernel launch of this workload, from
-    the committed summary of one `ncu --set full` capture (profiles/), or None."""
+def ncu_traffic(name: str, engine: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel (engine
+    "lane" = K2L, "warp" = the warp-per-scenario tick kernel) on this
+    workload, from the committed summary of one `ncu --set full` capture
+    (profiles/ncu_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f)[name]
+            t = json.load(f)[f"{name}/{engine}"]
         return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), t["source"]
     except Exception:
         return None, None
@@ -425,6 +427,8 @@ def main():
     ticks_all, ops_all = float(tt[0]), float(tt[1])
     value = ticks_all * args.steps / (tot_ms / 1e3)
     launches = sim.last_launches
+    engines = sim.last_engines
+    lane_engine = bool(engines & 0x18)  # BELLMAN_ENGINE_LANE_KV0 | BELLMAN_ENGINE_LANE_KV
     if world > 1:
         st_all = (full_dev if fused else PAR.gather_summaries(PAR.shard_rows(stats_dev, rank, world), n, rank,
                                                               world)).cpu().numpy().view(_abi.STATS).reshape(-1)
@@ -478,14 +482,32 @@ def main():
     clocks = clk.summary()
     mhz = pk_["sm_max_mhz"]
     kern_s = kern_tot / 1e3 / args.steps
-    achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G warp-inst/s
-    peak = 148 * 4 * mhz * 1e6 / 1e9
-    traffic, traffic_src = ncu_traffic(args.workload)
-    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time (max over ranks, per GPU); "
-                    f"peak = 148 SM x 4 issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM bytes "
-                    f"per launch ({traffic_src or 'no capture'})"}
+    achieved = ops_all / max(world, 1) / kern_s / 1e9  # per GPU, G algorithmic int ops/s
+    issue_peak = 148 * 4 * mhz * 1e6 / 1e9  # R_issue: 4 warp-instructions / clk / SM
+    # R_lane from the guide's unit counts: 4 SMSPs x (alu + fma pipes, each one
+    # warp-instruction / 2 clk) x 32 lanes = 128 integer lanes / clk / SM
+    lane_peak = 148 * 128 * mhz * 1e6 / 1e9
+    engine = "lane" if lane_engine else "warp"
+    traffic, traffic_src = ncu_traffic(args.workload, engine)
+    if lane_engine:
+        # K2L: one thread per scenario, so an algorithmic op is one lane-op and
+        # the binding roof is the SM's integer lanes (SURVEY 8(d) R_lane)
+        roof = {"bound": "alu", "achieved": achieved, "peak": lane_peak, "unit": "G int-lane-ops/s",
+                "frac": achieved / lane_peak, "traffic": traffic, "kernel": "bellman_lane_kernel (K2L)",
+                "note": f"survey 8(d) algorithmic integer ops per launch (per-unit counts x the units processed) / "
+                        f"kernel time (max over ranks, per GPU); K2L runs one scenario per lane, so the roof is R_lane "
+                        f"= 148 SM x 128 int lanes/clk (4 SMSP x alu + fma pipes x 16 lanes/clk, guide) x {mhz:.0f} "
+                        f"MHz ({pk_['src']} sm_max); traffic = DRAM bytes per launch ({traffic_src or 'no capture'})"}
+        roof["issue_model"] = {"peak": issue_peak, "unit": "Gwarp-inst/s", "frac": achieved / issue_peak,
+                               "note": "R_issue of SURVEY 8(d) (one warp per scenario: every algorithmic op takes a "
+                                       "warp issue slot); K2L issues one instruction for up to 32 scenarios, so it "
+                                       "runs above that ceiling"}
+    else:
+        roof = {"bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "Gwarp-inst/s",
+                "frac": achieved / issue_peak, "traffic": traffic, "kernel": "bellman_tick_kernel (K2)",
+                "note": f"survey 8(d) algorithmic warp-instructions per launch / kernel time (max over ranks, per "
+                        f"GPU); peak = 148 SM x 4 issue/clk x {mhz:.0f} MHz ({pk_['src']} sm_max); traffic = DRAM "
+                        f"bytes per launch ({traffic_src or 'no capture'})"}
     if not args.no_peak:
         # measured integer issue / lane throughput (microbenchmark, after the timed region)
         from paper_2510_15330_b200 import peak as PEAK
@@ -494,14 +516,13 @@ def main():
         best = max(v for k, v in mb.items() if "warp_inst" in k)
         issue_meas = 148 * best * mhz * 1e6 / 1e9
         l_int = max(mb["mixed_lanes_per_clk_sm"], mb["alu_lanes_per_clk_sm"], mb["fma_lanes_per_clk_sm"])
-        lane_peak = 148 * l_int * mhz * 1e6 / 1e9
+        lane_meas = 148 * l_int * mhz * 1e6 / 1e9
         roof["issue_measured"] = {"peak": issue_meas, "frac": achieved / issue_meas,
                                   "warp_inst_per_clk_sm": {k.split("_warp")[0]: round(v, 3) for k, v in mb.items()
                                                            if "warp_inst" in k},
                                   "note": "peak = the best measured integer issue rate x 148 SM x clock"}
-        roof["lane"] = {"L_int": l_int, "peak": lane_peak, "unit": "G int-lane-ops/s", "frac": achieved / lane_peak,
-                        "note": "R_lane (SURVEY 8(d)): every algorithmic op is one warp-instruction in the "
-                                "warp-per-scenario design, so achieved counts it once; L_int measured"}
+        roof["lane"] = {"L_int": l_int, "peak": lane_meas, "unit": "G int-lane-ops/s", "frac": achieved / lane_meas,
+                        "note": "R_lane (SURVEY 8(d)) with L_int measured (integer lanes / clk / SM, microbenchmark)"}
     # HBM (BASELINE north_star asks for achieved GB/s): algorithmic bytes = descriptor in + record out
     # per scenario of the launch; ncu bytes = the committed capture's DRAM read + write
     alg_bytes = (B_DESC + B_REC) * count
@@ -523,6 +544,7 @@ def main():
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches * args.steps,
+        "engines": {"mask": engines, "dominant": "K2L lane-per-scenario" if lane_engine else "K2 warp-per-scenario"},
         "clocks": clocks,
         "kernel_ms_per_step": kern_tot / args.steps,
         "outputs": outs,

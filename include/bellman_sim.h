@@ -401,6 +401,23 @@ bellman_status bellman_sim_set_peers(bellman_sim *sim, void *const *peer_stats, 
 /* Kernel launches issued by the most recent bellman_sim_run. */
 uint32_t bellman_sim_last_launches(const bellman_sim *sim);
 
+/* Which engines the most recent bellman_sim_run launched, as a bit mask over
+ * BELLMAN_ENGINE_*: the warp-per-scenario kernels (one warp simulates one
+ * scenario: the TBT-specialised, generic and multi-replica loops) and the
+ * lane-per-scenario kernel K2L (one thread simulates one scenario; DESIGN.md
+ * §5).  The results never depend on the engine: every engine computes the
+ * same records.  A run takes K2L for the scenarios within its bounds (TBT
+ * signal, non-blocking prefill, no KV capacity, word units, one replica,
+ * MAP / STEP / CONST / OFF, a Poisson trace, horizon < 2^31 µs) when it has at
+ * least 65,536 scenarios; the environment variable BELLMAN_LANE=0 turns K2L
+ * off, BELLMAN_LANE=2 takes it for runs of any size (read at every call). */
+#define BELLMAN_ENGINE_WARP_TBT 0x1u   /* warp per scenario, TBT-specialised loop */
+#define BELLMAN_ENGINE_WARP_GEN 0x2u   /* warp per scenario, generic loop */
+#define BELLMAN_ENGINE_WARP_MULTI 0x4u /* warp per scenario, multi-replica loop */
+#define BELLMAN_ENGINE_LANE_KV0 0x8u   /* lane per scenario, KV-free cost law */
+#define BELLMAN_ENGINE_LANE_KV 0x10u   /* lane per scenario, with the KV term */
+uint32_t bellman_sim_last_engines(const bellman_sim *sim);
+
 void bellman_sim_destroy(bellman_sim *sim);
 const char *bellman_status_string(bellman_status s);
 const char *bellman_sim_last_error(const bellman_sim *sim);

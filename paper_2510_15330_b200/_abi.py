@@ -90,6 +90,7 @@ EXPORTS = {
     "bellman_sim_series": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
                                      C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
     "bellman_sim_last_launches": (C.c_uint32, [C.c_void_p]),
+    "bellman_sim_last_engines": (C.c_uint32, [C.c_void_p]),
     "bellman_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
     "bellman_ipc_open": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "bellman_ipc_close": (C.c_int, [C.c_void_p]),

@@ -51,6 +51,7 @@ struct bellman_sim {
   bool has_calibrated = false;
   int grid = 0;
   uint32_t last_launches = 0;
+  uint32_t last_engines = 0;  // BELLMAN_ENGINE_* of the last run (bit k = scenario kind k)
   Params params{};
   unsigned int *counters = nullptr;  // [16]: one per launch of a run
   bool has_dbg = false;
@@ -279,7 +280,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, off_lhist, total;
+      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, off_lhist, off_lfifo, total;
   size_t in_end;              // [0, in_end): host-filled inputs, one staging copy at create
   size_t zero_beg, zero_end;  // [zero_beg, zero_end): zeroed at create (counters, stats, histograms)
 };
@@ -466,6 +467,8 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   for (uint32_t i = 0; i < d->n_profiles; ++i)
     pre = pre || (d->profiles[i].kv_policy == BELLMAN_KV_PREEMPT && d->profiles[i].kv_cap_words > 0);
   L.off_pre = take(pre ? sizeof(PreScratch) * kMaxPreCtas : 0);
+  // K2L per-thread arrival FIFOs (written before they are read)
+  L.off_lfifo = take(lane_possible(d) ? sizeof(uint4) * 128u * kLaneMaxThreads : 0);
   L.total = o;
   return L;
 }
@@ -594,6 +597,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.pre = (PreScratch *)(ws + L.off_pre);
   P.lane_on = 0;  // set per run
   P.lane_hist = (uint32_t *)(ws + L.off_lhist);
+  P.lane_fifo = (uint4 *)(ws + L.off_lfifo);
   sim->lane_ok = lane_possible(desc);
   sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->shard_order = (uint32_t *)(ws + L.off_sord);
@@ -666,6 +670,7 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   if (!sim) return fail(nullptr, BELLMAN_ESTATE, "sim is NULL");
   if (count == 0) {
     sim->last_launches = 0;
+    sim->last_engines = 0;
     return BELLMAN_OK;
   }
   if (stride == 0) return fail(sim, BELLMAN_ESTATE, "stride must be >= 1");
@@ -723,6 +728,7 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
   const uint64_t want = (count + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)(want < (uint64_t)sim->grid ? want : (uint64_t)sim->grid);
   sim->last_launches = 0;
+  sim->last_engines = 0;
   // pass 1: non-calibrated scenarios.  One launch per kernel with work
   // (scenario_kind_of): K2L (kv = 0 / kv > 0), the TBT-specialised, generic and
   // multi-replica warp engines, debug-recorded or not; if no kernel has work
@@ -737,11 +743,13 @@ bellman_status bellman_sim_run(bellman_sim *sim, uint64_t first, uint64_t count,
         P.counter = ctr + 5 * dbg + kind;
         if (kind >= 3) CUDA_TRY(sim, bellman_launch_lane(P, sim->lane_grid, kind, s));
         else CUDA_TRY(sim, bellman_launch_tick(P, grid, dbg != 0, kind, s));
+        sim->last_engines |= 1u << kind;
         n++;
       }
     if (n == 0) {
       P.counter = ctr;
       CUDA_TRY(sim, bellman_launch_tick(P, grid, false, 0, s));
+      sim->last_engines |= 1u;
       n++;
     }
     sim->last_launches += n;
@@ -900,6 +908,7 @@ bellman_status bellman_sim_set_peers(bellman_sim *sim, void *const *peer_stats, 
 }
 
 uint32_t bellman_sim_last_launches(const bellman_sim *sim) { return sim ? sim->last_launches : 0; }
+uint32_t bellman_sim_last_engines(const bellman_sim *sim) { return sim ? sim->last_engines : 0; }
 
 void bellman_sim_destroy(bellman_sim *sim) { delete sim; }
 
@@ -927,7 +936,7 @@ const char *bellman_sim_last_error(const bellman_sim *sim) { return sim ? sim->e
 // the calibration between the passes done here, so that the lane engine can be
 // compared with the oracle (scripts/lanecheck.py) without a GPU.
 namespace bellman {
-void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist);
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint4 *fifo);
 }
 extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_stats *out, unsigned long long *seg,
                                  uint8_t *ran) {
@@ -978,12 +987,13 @@ extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_sta
   P.seg_hist = seg;
   P.lane_on = 1;
   std::vector<uint32_t> smem(kLaneWarpWords<false>), hist(kLaneHistWords, 0);
+  std::vector<uint4> fifo(128);
   for (uint32_t pass = 1; pass <= 2; ++pass) {
     P.pass = pass;
     for (uint64_t s = 0; s < d->n_scenarios; ++s) {
       const bellman_scenario &sc = d->scenarios[s];
       if ((d->ctrls[sc.ctrl].calibrated != 0) != (pass == 2) || kind_of(d, sc, 1u) < 3u) continue;
-      lane_host_run(P, s, smem.data(), hist.data());
+      lane_host_run(P, s, smem.data(), hist.data(), fifo.data());
       ran[s] = 1;
     }
     if (pass == 1)

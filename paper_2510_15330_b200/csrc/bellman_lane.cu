@@ -128,9 +128,8 @@ LHD U4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
 }
 
 // -ln(U), U = (2u+1)/2^33, in Q32 (reading R33): log2 by table + interpolation.
-// Split in two so that the table entry can be loaded one candidate ahead:
-// the normalised mantissa bits x (table index x >> 20) and exponent e of
-// v = 2u + 1, then the interpolation with the entry t = tab[x >> 20].
+// neglog_split gives the normalised mantissa bits x of v = 2u + 1 (table index
+// x >> 20) and its exponent e; neglog_q32 interpolates with the entry t.
 LHD uint32_t neglog_split(uint32_t u, uint32_t &e) {
   if (u >= 0x80000000u) {
     e = 32;
@@ -139,6 +138,10 @@ LHD uint32_t neglog_split(uint32_t u, uint32_t &e) {
   const uint32_t v = 2u * u + 1u;
   e = 31u - clz32(v);
   return (uint32_t)(((uint64_t)(v - (1u << e))) << (32u - e));
+}
+LHD uint32_t neglog_index(uint32_t u) {
+  uint32_t e;
+  return neglog_split(u, e) >> 20;
 }
 LHD uint64_t neglog_q32(uint32_t u, uint2 t) {
   uint32_t e;
@@ -243,16 +246,17 @@ struct Lane {
   uint64_t rdy_sum;   // sum of the decode-ready slots' prefill ends (their join alignment)
   uint32_t rdy_kadd;  // sum of their (input + 1) context words (KV term)
   uint32_t nheap;
-  // ---- queue head (the next accepted arrival) and generator (a2, a3)
-  // the head's raw draws (its table entries, loaded at generation and consumed
-  // at admission, so their L2 latency is off the event loop's critical path):
-  // L, input, F_var, noise, F_comp, similarity noise, the class bits, its index
-  uint32_t head_t, h_L, h_I, h_F, h_N, h_C, h_Q, h_cls, h_j;
-  U4 nu;     // tag-0 block of candidate gen_j (computed one candidate ahead)
-  uint2 nt;  // its log2 table entry (loaded one candidate ahead)
+  // ---- the FIFO queue ahead of admission (a2, a3): the head and the next
+  // accepted arrival in registers, the ones after them in this thread's FIFO
+  // in global memory (fifo, a 64-entry ring: frd, fcnt), filled 32 candidates
+  // at a time by the whole warp (coop_refill).  An entry: arrival (clamped to
+  // 32 bits), input | class << 16, U, P, F_comp | similarity noise, index j.
+  uint32_t head_t, h_in, h_U, h_P, h_fcq, h_j;  // head_t = INF: no head
+  uint32_t n_t, n_in, n_U, n_P, n_fcq, n_j, n_ok;
+  uint4 *fifo;
+  uint32_t frd, fcnt;
   uint32_t gen_seg, gen_j, gen_acc, gen_done, gen_fresh, gen_cap, n_seg, seg_off;
-  uint64_t gen_tau, s_ta, s_tb, s_span, s_M;
-  uint32_t s_la, s_lb, s_lmax;
+  uint64_t gen_tau;
   uint32_t k0, wid_lo, wid_hi, bypass_mask, min_words;
   // ---- accounting (a8)
   uint64_t c_admitted, c_served, c_rewritten, c_slo, c_win_served, c_words_in, c_idle, c_win_words_in,
@@ -474,53 +478,57 @@ struct Lane {
   }
 
   // ------------------------------------------------------------------ a2 + a3
-  LHD void load_seg(const Params &p) {
-    const DevSeg &S = p.segs[seg_off + gen_seg];
-    s_ta = S.ta;
-    s_tb = S.tb;
-    s_span = S.span;
-    s_M = S.M;
-    s_la = S.la;
-    s_lb = S.lb;
-    s_lmax = S.lmax;
+  // One candidate from the tag-0 block u of candidate j (P:183 Poisson, S:83
+  // thinning; R17, R32, R33): its time tau = gen_tau + Exp draw, whether it
+  // crosses the segment's end, whether thinning accepts it.
+  // The request's attributes and own draws (tag-1 block): the FIFO entry.
+  __device__ __host__ static void make_entry(const Params &p, uint32_t key0, uint32_t wl, uint32_t wh, uint32_t j,
+                                             const U4 &u, uint64_t tau, uint32_t e[6]) {
+    const uint32_t L = (uint32_t)ldg(&p.tabL[u.z >> 20]);
+    const uint32_t xc = u.z & 0xFFFFFu;  // class draw (NEXT-3): the bits below L's index
+    const uint32_t cls = xc < p.class_cum0 ? 0u : (xc < p.class_cum1 ? 1u : (xc < p.class_cum2 ? 2u : 3u));
+    const uint32_t in = (uint32_t)ldg(&p.tabI[u.w >> 20]);
+    const U4 v = philox(key0, kSeedHi, j, 1u, wl, wh);
+    const uint64_t U = ((uint64_t)L * (uint32_t)ldg(&p.tabF[v.x >> 20]) + 32768u) >> 16;  // S:139, R14
+    const int32_t P0 = (int32_t)L + ldg(&p.tabN[v.y >> 20]);
+    e[0] = tau < kFar ? (uint32_t)tau : kFar;
+    e[1] = in | (cls << 16);
+    e[2] = U < 1 ? 1u : (uint32_t)U;
+    e[3] = P0 < 1 ? 1u : (uint32_t)P0;
+    e[4] = (uint32_t)ldg(&p.tabC[v.z >> 20]) | ((uint32_t)(ldg(&p.tabQ[v.w >> 20]) + 2048) << 20);
+    e[5] = j;
   }
-  // the tag-0 block of candidate gen_j and its log2 table entry
-  LHD void prefetch(const Params &p) {
-    nu = philox(k0, kSeedHi, gen_j, 0u, wid_lo, wid_hi);
-    uint32_t e;
-    nt = ldg(&p.log2tab[neglog_split(nu.x, e) >> 20]);
+  LHD static bool thin_accept(const DevSeg &S, uint32_t u1, uint64_t tau) {
+    // u1 lmax span < (la (tb - tau) + lb (tau - ta)) 2^32, in 128 bits
+    const uint64_t x = (uint64_t)u1 * S.lmax;
+    const uint64_t lhs_hi = mulhi64(x, S.span), lhs_lo = x * S.span;
+    const uint64_t y = (uint64_t)S.la * (S.tb - tau) + (uint64_t)S.lb * (tau - S.ta);
+    const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
+    return lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
   }
-  // Next candidate of the stream (P:183 Poisson, S:83 thinning; R17, R32, R33):
-  // returns false when the generator is exhausted, else the candidate's index
-  // j, time tau, its tag-0 block u and whether thinning accepted it.
+  // Scalar generation (the fallback when the FIFO is empty, and the epilogue's
+  // count): the next candidate; false when the generator is exhausted.
   LHD bool candidate(const Params &p, uint32_t &j, uint64_t &tau, U4 &u, bool &acc) {
     for (;;) {
       if (gen_seg >= n_seg) {
         gen_done = 1;
         return false;
       }
+      const DevSeg &S = p.segs[seg_off + gen_seg];
       if (gen_fresh) {
-        load_seg(p);
-        gen_tau = s_ta;
+        gen_tau = S.ta;
         gen_fresh = 0;
       }
       j = gen_j++;
-      u = nu;
-      const uint2 t = nt;
-      prefetch(p);  // candidate j + 1
-      tau = gen_tau + mulhi64(neglog_q32(u.x, t), s_M);
-      if (tau >= s_tb) {  // the crossing candidate is consumed (R17)
+      u = philox(k0, kSeedHi, j, 0u, wid_lo, wid_hi);
+      tau = gen_tau + mulhi64(neglog_q32(u.x, ldg(&p.log2tab[neglog_index(u.x)])), S.M);
+      if (tau >= S.tb) {  // the crossing candidate is consumed (R17)
         gen_seg++;
         gen_fresh = 1;
         continue;
       }
       gen_tau = tau;
-      // thinning: u1 lmax span < (la (tb - tau) + lb (tau - ta)) 2^32, in 128 bits
-      const uint64_t x = (uint64_t)u.y * s_lmax;
-      const uint64_t lhs_hi = mulhi64(x, s_span), lhs_lo = x * s_span;
-      const uint64_t y = (uint64_t)s_la * (s_tb - tau) + (uint64_t)s_lb * (tau - s_ta);
-      const uint64_t rhs_hi = y >> 32, rhs_lo = y << 32;
-      acc = lhs_hi < rhs_hi || (lhs_hi == rhs_hi && lhs_lo < rhs_lo);
+      acc = thin_accept(S, u.y, tau);
       if (acc) {
         gen_acc++;
         if (gen_cap && gen_acc >= gen_cap) gen_done = 1;  // the capped arrival is still delivered
@@ -528,41 +536,183 @@ struct Lane {
       return true;
     }
   }
-  // the queue head becomes the next accepted arrival (or none: head_t = INF)
-  LHD void next_head(const Params &p) {
+  // the next accepted arrival of the stream into e (false: none)
+  LHD bool scalar_next(const Params &p, uint32_t e[6]) {
     for (;;) {
-      if (gen_done) {
-        head_t = kInf;
-        return;
-      }
+      if (gen_done) return false;
       uint32_t j;
       uint64_t tau;
       U4 u;
       bool acc;
-      if (!candidate(p, j, tau, u, acc)) {
-        head_t = kInf;
-        return;
-      }
+      if (!candidate(p, j, tau, u, acc)) return false;
       if (!acc) continue;
-      // the request's attributes and its own draws (a3: tag-1 block): loads issued now, used at admission
-      h_L = (uint32_t)ldg(&p.tabL[u.z >> 20]);
-      h_I = (uint32_t)ldg(&p.tabI[u.w >> 20]);
-      h_cls = u.z & 0xFFFFFu;  // class draw (NEXT-3): the bits below L's index
-      const U4 v = philox(k0, kSeedHi, j, 1u, wid_lo, wid_hi);
-      h_F = (uint32_t)ldg(&p.tabF[v.x >> 20]);
-      h_N = (uint32_t)ldg(&p.tabN[v.y >> 20]);
-      h_C = (uint32_t)ldg(&p.tabC[v.z >> 20]);
-      h_Q = (uint32_t)ldg(&p.tabQ[v.w >> 20]);
-      h_j = j;
-      head_t = tau < kFar ? (uint32_t)tau : kFar;
-      return;
+      make_entry(p, k0, wid_lo, wid_hi, j, u, tau, e);
+      return true;
+    }
+  }
+  LHD void fifo_pop(uint32_t e[6]) {
+    const uint4 a = fifo[2u * frd], b = fifo[2u * frd + 1u];
+    e[0] = a.x;
+    e[1] = a.y;
+    e[2] = a.z;
+    e[3] = a.w;
+    e[4] = b.x;
+    e[5] = b.y;
+    frd = (frd + 1u) & 63u;
+    fcnt--;
+  }
+  // the head moves on: next -> head, the FIFO's front -> next (its loads are
+  // consumed at a later admission); scalar generation when both are empty
+  LHD void next_head(const Params &p) {
+    uint32_t e[6];
+    if (n_ok) {
+      head_t = n_t;
+      h_in = n_in;
+      h_U = n_U;
+      h_P = n_P;
+      h_fcq = n_fcq;
+      h_j = n_j;
+      n_ok = 0;
+    } else if (fcnt) {
+      fifo_pop(e);
+      head_t = e[0];
+      h_in = e[1];
+      h_U = e[2];
+      h_P = e[3];
+      h_fcq = e[4];
+      h_j = e[5];
+    } else if (scalar_next(p, e)) {
+      head_t = e[0];
+      h_in = e[1];
+      h_U = e[2];
+      h_P = e[3];
+      h_fcq = e[4];
+      h_j = e[5];
+    } else {
+      head_t = kInf;
+    }
+    refill_next();
+  }
+  LHD void refill_next() {
+    if (n_ok || !fcnt || head_t == kInf) return;
+    uint32_t e[6];
+    fifo_pop(e);
+    n_t = e[0];
+    n_in = e[1];
+    n_U = e[2];
+    n_P = e[3];
+    n_fcq = e[4];
+    n_j = e[5];
+    n_ok = 1;
+  }
+
+#ifdef __CUDA_ARCH__
+  // Warp-cooperative generation for lane `who` (every lane of the warp calls
+  // it, converged): its generator state is broadcast, lane l draws candidate
+  // j + l (tag-0 Philox block, -ln U, a warp prefix sum of the gaps), the
+  // crossing rule and thinning by ballot, and each accepted candidate's lane
+  // writes its FIFO entry (tag-1 draws) at its rank — K2's refill, per lane.
+  // Candidates after a segment crossing are discarded and redrawn in the next
+  // segment (the crossing one is consumed, R17), as in the scalar generator.
+  __device__ void coop_refill(const Params &p, uint32_t who, uint32_t lane, uint4 *fifo_warp) {
+    const uint32_t F = 0xffffffffu;
+    uint32_t gseg = __shfl_sync(F, gen_seg, who), gj = __shfl_sync(F, gen_j, who);
+    uint32_t gacc = __shfl_sync(F, gen_acc, who), gdone = __shfl_sync(F, gen_done, who);
+    uint32_t gfresh = __shfl_sync(F, gen_fresh, who);
+    uint64_t gtau = __shfl_sync(F, (unsigned long long)gen_tau, who);
+    const uint32_t nseg = __shfl_sync(F, n_seg, who), soff = __shfl_sync(F, seg_off, who);
+    const uint32_t gcap = __shfl_sync(F, gen_cap, who), key0 = __shfl_sync(F, k0, who);
+    const uint32_t wl = __shfl_sync(F, wid_lo, who), wh = __shfl_sync(F, wid_hi, who);
+    const uint32_t tail0 = (__shfl_sync(F, frd, who) + __shfl_sync(F, fcnt, who)) & 63u;
+    uint4 *fw = fifo_warp + 128u * who;
+    uint32_t added = 0;
+    while (!gdone && added == 0) {
+      if (gseg >= nseg) {
+        gdone = 1;
+        break;
+      }
+      const DevSeg S = p.segs[soff + gseg];
+      if (gfresh) {
+        gtau = S.ta;
+        gfresh = 0;
+      }
+      const uint32_t jj = gj + lane;
+      const U4 u = philox(key0, kSeedHi, jj, 0u, wl, wh);
+      uint64_t incl = mulhi64(neglog_q32(u.x, ldg(&p.log2tab[neglog_index(u.x)])), S.M);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(F, (unsigned long long)incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      const uint64_t tau = gtau + incl;
+      const uint32_t om = __ballot_sync(F, tau >= S.tb);
+      const uint32_t first_over = om ? (uint32_t)__ffs((int)om) - 1u : 32u;
+      const bool acc = lane < first_over && thin_accept(S, u.y, tau);
+      uint32_t am = __ballot_sync(F, acc);
+      if (gcap) {  // the arrival cap: keep the first `room` accepted
+        const uint32_t room = gcap - gacc;
+        if ((uint32_t)__popc(am) >= room) {
+          const uint32_t cut = room ? __fns(am, 0, (int)room) : 0u;
+          am = room ? (am & (0xffffffffu >> (31u - cut))) : 0u;
+          gdone = 1;
+        }
+      }
+      if ((am >> lane) & 1u) {
+        const uint32_t e = (uint32_t)__popc(am & ((1u << lane) - 1u));
+        uint32_t ent[6];
+        make_entry(p, key0, wl, wh, jj, u, tau, ent);
+        uint4 *f = fw + 2u * ((tail0 + added + e) & 63u);
+        f[0] = make_uint4(ent[0], ent[1], ent[2], ent[3]);
+        f[1] = make_uint4(ent[4], ent[5], 0u, 0u);
+      }
+      const uint32_t na = (uint32_t)__popc(am);
+      added += na;
+      gacc += na;
+      if (first_over < 32u) {
+        gj += first_over + 1u;
+        gseg++;
+        gfresh = 1;
+      } else {
+        gj += 32u;
+        gtau = __shfl_sync(F, (unsigned long long)tau, 31);
+      }
+    }
+    __syncwarp();  // the entries' stores precede lane `who`'s loads
+    if (lane == who) {
+      gen_seg = gseg;
+      gen_j = gj;
+      gen_acc = gacc;
+      gen_done = gdone;
+      gen_fresh = gfresh;
+      gen_tau = gtau;
+      fcnt += added;
+    }
+  }
+#endif
+  // the same FIFO contents one at a time (the CPU development build)
+  LHD void fill_host(const Params &p) {
+    uint32_t e[6];
+    while (fcnt < 32u && scalar_next(p, e)) {
+      uint4 *f = fifo + 2u * ((frd + fcnt) & 63u);
+      f[0] = make_uint4(e[0], e[1], e[2], e[3]);
+      f[1] = make_uint4(e[4], e[5], 0u, 0u);
+      fcnt++;
+    }
+  }
+  // after a refill: the head (a fresh scenario) or the next, from the FIFO
+  LHD void after_refill(const Params &p) {
+    if (head_t == kInf) {
+      if (fcnt || !gen_done) next_head(p);
+    } else {
+      refill_next();
     }
   }
 
   // ------------------------------------------------------------------ a1 scenario decode
-  LHD void init(const Params &p, uint64_t id, uint32_t *smem_lane, uint32_t *hist_lane) {
+  LHD void init(const Params &p, uint64_t id, uint32_t *smem_lane, uint32_t *hist_lane, uint4 *fifo_lane) {
     sm = smem_lane;
     hist = hist_lane;
+    fifo = fifo_lane;
     sid = id;
     const bellman_scenario sc = p.sc[id];
     const bellman_ctrl &cc = p.ctrls[sc.ctrl];
@@ -644,12 +794,13 @@ struct Lane {
     gen_seg = gen_j = gen_acc = gen_done = 0;
     gen_fresh = 1;
     gen_tau = 0;
-    prefetch(p);  // candidate 0
+    frd = fcnt = 0;
+    n_ok = 0;
+    head_t = kInf;  // the first refill (coop_refill, or fill_host) sets the head
     c_admitted = c_served = c_rewritten = c_slo = c_win_served = c_words_in = c_idle = c_win_words_in = 0;
     c_win_idle = c_sum_queue = c_sum_ttft = c_sum_e2e = words_out = win_words_out = n_ttft = 0;
     last_j = bypassed = finished = 0;
     hm_e2e = hm_ttft = hm_r = hm_q = 0;
-    next_head(p);
   }
 
   // ------------------------------------------------------------------ a5
@@ -765,19 +916,11 @@ struct Lane {
     const uint32_t Tn = T;
     uint32_t n = 0, n_byp = 0;
     do {
-      // the head's draws (a3): U = max(1, round(L F_var)) (R14), P = max(1, L + noise)
-      // (S:121), F_comp | similarity noise, prefill max(1, floor(pf_ns in / 1000))
-      const uint32_t a = head_t, in = h_I, L = h_L;
-      const uint64_t U64 = ((uint64_t)L * h_F + 32768u) >> 16;
-      const uint32_t U = U64 < 1 ? 1u : (uint32_t)U64;
-      const int32_t P0 = (int32_t)L + (int32_t)h_N;
-      const uint32_t P = P0 < 1 ? 1u : (uint32_t)P0;
-      const uint32_t fcq = h_C | ((h_Q + 2048u) << 20);
+      // the head (a3): U, P, F_comp | similarity noise drawn at generation; prefill
+      // max(1, floor(pf_ns in / 1000)); the bypass rule (NEXT-3)
+      const uint32_t a = head_t, in = h_in & 0xFFFFu, cls = h_in >> 16, U = h_U, P = h_P, fcq = h_fcq;
       const uint32_t pf0 = (uint32_t)(((uint64_t)pf_ns * in) / 1000u);
       const uint32_t pf = pf0 < 1u ? 1u : pf0;
-      const uint32_t cls =
-          h_cls < p.class_cum0 ? 0u : (h_cls < p.class_cum1 ? 1u : (h_cls < p.class_cum2 ? 2u : 3u));
-      // r applied to this request: r unless a bypass rule holds (NEXT-3)
       const bool byp = r > 0 && (((bypass_mask >> cls) & 1u) || P < min_words);
       const uint32_t ra = byp ? 0u : r;
       uint32_t R = U, qb;
@@ -1018,10 +1161,29 @@ struct Lane {
     ingest_pending();
     // queued at the end: accepted arrivals before `end` not admitted
     uint64_t queued = 0;
-    if (head_t != kInf && head_t < end) {
-      queued = 1;
-      last_j = h_j + 1u;
-      while (!gen_done) {  // the rest of the stream is only counted (tag-0 draws, thinning)
+    if (head_t != kInf) {  // the head, the next, the FIFO, then the rest of the stream (counted only)
+      bool more = head_t < end;
+      if (more) {
+        queued = 1;
+        last_j = h_j + 1u;
+      }
+      if (more && n_ok) {
+        more = n_t < end;
+        if (more) {
+          queued++;
+          last_j = n_j + 1u;
+        }
+      }
+      while (more && fcnt) {
+        uint32_t e[6];
+        fifo_pop(e);
+        more = e[0] < end;
+        if (more) {
+          queued++;
+          last_j = e[5] + 1u;
+        }
+      }
+      while (more && !gen_done) {  // tag-0 draws and thinning only
         uint32_t j;
         uint64_t tau;
         U4 u;
@@ -1140,7 +1302,9 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
   uint32_t lane_id;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane_id));
   uint32_t *smem = lane_smem + (threadIdx.x >> 5) * kLaneWarpWords<KV0> + lane_id;
-  uint32_t *hist = p.lane_hist + (uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * kLaneHistWords;
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t *hist = p.lane_hist + (uint64_t)gt * kLaneHistWords;
+  uint4 *fifo_warp = p.lane_fifo + (uint64_t)(gt - lane_id) * 128u;  // lane l's ring at + 128 l
   const uint32_t kind = KV0 ? 3u : 4u;
   lane::Lane<KV0> L;
   bool has = false, alive = true;
@@ -1162,13 +1326,25 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
         } else {
           const uint64_t sid = p.order ? (uint64_t)p.order[kidx] : p.first + (uint64_t)kidx * p.stride;
           if (lane::mine(p, sid, kind)) {
-            L.init(p, sid, smem, hist);
+            L.init(p, sid, smem, hist, fifo_warp + 128u * lane_id);
             has = true;
           }
         }
       }
     }
     if (!__any_sync(FULL_MASK, has || alive)) break;
+    // generation: every lane whose FIFO holds <= 31 entries gets 32 candidates
+    // drawn by the whole warp (one lane at a time)
+    uint32_t want = __ballot_sync(FULL_MASK, has && !L.gen_done && L.fcnt <= 31u);
+    if (want) {
+      const uint32_t w0 = want;
+      while (want) {
+        const uint32_t who = (uint32_t)__ffs((int)want) - 1u;
+        want &= want - 1u;
+        L.coop_refill(p, who, lane_id, fifo_warp);
+      }
+      if ((w0 >> lane_id) & 1u) L.after_refill(p);
+    }
     if (has && L.trip(p)) {
       L.finish(p);
       has = false;
@@ -1178,19 +1354,27 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
 
 #ifdef BELLMAN_LANECHECK
 // Development only: the same per-scenario code on the CPU (one scenario at a time).
-void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist) {
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint4 *fifo) {
   const bellman_profile &pr = p.profs[p.sc[sid].profile];
   if (pr.kv_ns_per_word == 0) {
     lane::Lane<true> L;
-    L.init(p, sid, smem_warp, hist);
-    while (!L.trip(p)) {
-    }
+    L.init(p, sid, smem_warp, hist, fifo);
+    do {
+      if (!L.gen_done && L.fcnt <= 31u) {
+        L.fill_host(p);
+        L.after_refill(p);
+      }
+    } while (!L.trip(p));
     L.finish(p);
   } else {
     lane::Lane<false> L;
-    L.init(p, sid, smem_warp, hist);
-    while (!L.trip(p)) {
-    }
+    L.init(p, sid, smem_warp, hist, fifo);
+    do {
+      if (!L.gen_done && L.fcnt <= 31u) {
+        L.fill_host(p);
+        L.after_refill(p);
+      }
+    } while (!L.trip(p));
     L.finish(p);
   }
 }

@@ -154,6 +154,12 @@ class Simulator:
     def last_launches(self) -> int:
         return int(A.lib().bellman_sim_last_launches(self.h))
 
+    @property
+    def last_engines(self) -> int:
+        """Bit mask of the engines the last run launched (BELLMAN_ENGINE_*: 1/2/4 the
+        warp-per-scenario loops, 8/16 the lane-per-scenario kernel K2L)."""
+        return int(A.lib().bellman_sim_last_engines(self.h))
+
     def stats_device(self, out: torch.Tensor, first: int = 0, count: int | None = None, stream=None):
         count = self.n_scenarios - first if count is None else count
         assert out.is_cuda and out.numel() * out.element_size() >= count * A.STATS.itemsize

@@ -30,3 +30,10 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_run.py 2>&1 | tail -6
   echo "exit $?"
 done
+# K2L (the lane-per-scenario kernel) on the same workloads: BELLMAN_LANE=2 takes
+# it for runs of any size (its scenarios; the rest stay in the warp engines)
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool (K2L)"
+  BELLMAN_LANE=2 timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_run.py 2>&1 | tail -6
+  echo "exit $?"
+done

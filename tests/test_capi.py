@@ -167,3 +167,34 @@ def test_replica_validation():
                     (dict(prof_replicas=2, prof_maxb=8, prof_knee=1, prof_kv_cap=10_000), "needs prefill_mode 0")):
         with pytest.raises(A.BellmanError, match=msg):
             sim.workspace_bytes(sim.pack(cols(**kw)))
+
+
+def test_lane_engine_workspace_and_sass(monkeypatch):
+    """K2L (the lane-per-scenario kernel): a descriptor with >= 65,536
+    scenarios in its bounds gets the per-thread histogram and FIFO regions in
+    its workspace, unless BELLMAN_LANE=0; BELLMAN_LANE=2 adds them to small
+    sets too.  Both K2L instantiations are in the library, built for sm_100a
+    with no local-memory spills."""
+    import workloads as W
+    from paper_2510_15330_b200 import build as B
+    from paper_2510_15330_b200 import sim
+
+    path = B.build()
+    lane_bytes = 40960 * (2760 * 4 + 128 * 16)  # kLaneMaxThreads x (histograms + FIFO)
+    big = sim.pack(W.config_c5(n_seeds=256).columns())  # 65,536 scenarios
+    small = sim.pack(W.config_c2(n_seeds=1).columns())
+    monkeypatch.delenv("BELLMAN_LANE", raising=False)
+    auto_big, auto_small = sim.workspace_bytes(big), sim.workspace_bytes(small)
+    monkeypatch.setenv("BELLMAN_LANE", "0")
+    off_big, off_small = sim.workspace_bytes(big), sim.workspace_bytes(small)
+    monkeypatch.setenv("BELLMAN_LANE", "2")
+    on_small = sim.workspace_bytes(small)
+    assert auto_big - off_big >= lane_bytes
+    assert auto_small == off_small and on_small - off_small >= lane_bytes
+    info = open(os.path.join(os.path.dirname(path), "ptxas_info.txt")).read()
+    blocks = info.split("Compiling entry function")
+    lane = [b for b in blocks if "bellman_lane_kernel" in b.split("\n")[0]]
+    assert len(lane) == 2, "two K2L instantiations (kv = 0, kv > 0)"
+    for b in lane:
+        assert "sm_100a" in b.split("\n")[0]
+        assert "0 bytes spill stores, 0 bytes spill loads" in b

@@ -468,7 +468,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
     pre = pre || (d->profiles[i].kv_policy == BELLMAN_KV_PREEMPT && d->profiles[i].kv_cap_words > 0);
   L.off_pre = take(pre ? sizeof(PreScratch) * kMaxPreCtas : 0);
   // K2L per-thread arrival FIFOs (written before they are read)
-  L.off_lfifo = take(lane_possible(d) ? sizeof(uint4) * 128u * kLaneMaxThreads : 0);
+  L.off_lfifo = take(lane_possible(d) ? sizeof(uint2) * 96u * kLaneMaxThreads : 0);
   L.total = o;
   return L;
 }
@@ -597,7 +597,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.pre = (PreScratch *)(ws + L.off_pre);
   P.lane_on = 0;  // set per run
   P.lane_hist = (uint32_t *)(ws + L.off_lhist);
-  P.lane_fifo = (uint4 *)(ws + L.off_lfifo);
+  P.lane_fifo = (uint2 *)(ws + L.off_lfifo);
   sim->lane_ok = lane_possible(desc);
   sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->shard_order = (uint32_t *)(ws + L.off_sord);
@@ -936,7 +936,7 @@ const char *bellman_sim_last_error(const bellman_sim *sim) { return sim ? sim->e
 // the calibration between the passes done here, so that the lane engine can be
 // compared with the oracle (scripts/lanecheck.py) without a GPU.
 namespace bellman {
-void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint4 *fifo);
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint2 *fifo);
 }
 extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_stats *out, unsigned long long *seg,
                                  uint8_t *ran) {
@@ -987,7 +987,7 @@ extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_sta
   P.seg_hist = seg;
   P.lane_on = 1;
   std::vector<uint32_t> smem(kLaneWarpWords<false>), hist(kLaneHistWords, 0);
-  std::vector<uint4> fifo(128);
+  std::vector<uint2> fifo(96);
   for (uint32_t pass = 1; pass <= 2; ++pass) {
     P.pass = pass;
     for (uint64_t s = 0; s < d->n_scenarios; ++s) {

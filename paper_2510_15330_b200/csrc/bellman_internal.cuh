@@ -96,7 +96,7 @@ struct Params {
   uint32_t pass;  // 1: non-calibrated scenarios, 2: calibrated scenarios
   uint32_t lane_on;    // 1: kind-0 scenarios within K2L's bounds run in K2L (scenario_kind_of)
   uint32_t *lane_hist; // K2L per-thread histograms [kLaneMaxThreads][kLaneHistWords], all-zero between scenarios
-  uint4 *lane_fifo;    // K2L per-thread arrival FIFOs [kLaneMaxThreads][64 entries x 2 uint4]
+  uint2 *lane_fifo;    // K2L per-thread arrival FIFOs [kLaneMaxThreads][32 entries x 3 uint2]
 };
 
 }  // namespace bellman

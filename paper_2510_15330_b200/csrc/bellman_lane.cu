@@ -248,12 +248,13 @@ struct Lane {
   uint32_t nheap;
   // ---- the FIFO queue ahead of admission (a2, a3): the head and the next
   // accepted arrival in registers, the ones after them in this thread's FIFO
-  // in global memory (fifo, a 64-entry ring: frd, fcnt), filled 32 candidates
-  // at a time by the whole warp (coop_refill).  An entry: arrival (clamped to
-  // 32 bits), input | class << 16, U, P, F_comp | similarity noise, index j.
+  // in global memory (fifo, a 32-entry ring of 24-byte entries: frd, fcnt),
+  // filled 32 candidates at a time by the whole warp (coop_refill) when it is
+  // empty.  An entry: arrival (clamped to 32 bits), input | class << 16, U, P,
+  // F_comp | similarity noise, index j.
   uint32_t head_t, h_in, h_U, h_P, h_fcq, h_j;  // head_t = INF: no head
   uint32_t n_t, n_in, n_U, n_P, n_fcq, n_j, n_ok;
-  uint4 *fifo;
+  uint2 *fifo;  // entry k: fifo[3k .. 3k+2]
   uint32_t frd, fcnt;
   uint32_t gen_seg, gen_j, gen_acc, gen_done, gen_fresh, gen_cap, n_seg, seg_off;
   uint64_t gen_tau;
@@ -551,15 +552,20 @@ struct Lane {
     }
   }
   LHD void fifo_pop(uint32_t e[6]) {
-    const uint4 a = fifo[2u * frd], b = fifo[2u * frd + 1u];
+    const uint2 a = fifo[3u * frd], b = fifo[3u * frd + 1u], c = fifo[3u * frd + 2u];
     e[0] = a.x;
     e[1] = a.y;
-    e[2] = a.z;
-    e[3] = a.w;
-    e[4] = b.x;
-    e[5] = b.y;
-    frd = (frd + 1u) & 63u;
+    e[2] = b.x;
+    e[3] = b.y;
+    e[4] = c.x;
+    e[5] = c.y;
+    frd = (frd + 1u) & 31u;
     fcnt--;
+#ifdef __CUDA_ARCH__
+    // the entry after it into L2 (no register waits on a prefetch): the pops
+    // come many trips after the refill wrote the ring
+    if (fcnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(fifo + 3u * frd));
+#endif
   }
   // the head moves on: next -> head, the FIFO's front -> next (its loads are
   // consumed at a later admission); scalar generation when both are empty
@@ -614,7 +620,7 @@ struct Lane {
   // writes its FIFO entry (tag-1 draws) at its rank — K2's refill, per lane.
   // Candidates after a segment crossing are discarded and redrawn in the next
   // segment (the crossing one is consumed, R17), as in the scalar generator.
-  __device__ void coop_refill(const Params &p, uint32_t who, uint32_t lane, uint4 *fifo_warp) {
+  __device__ void coop_refill(const Params &p, uint32_t who, uint32_t lane, uint2 *fifo_warp) {
     const uint32_t F = 0xffffffffu;
     uint32_t gseg = __shfl_sync(F, gen_seg, who), gj = __shfl_sync(F, gen_j, who);
     uint32_t gacc = __shfl_sync(F, gen_acc, who), gdone = __shfl_sync(F, gen_done, who);
@@ -623,8 +629,8 @@ struct Lane {
     const uint32_t nseg = __shfl_sync(F, n_seg, who), soff = __shfl_sync(F, seg_off, who);
     const uint32_t gcap = __shfl_sync(F, gen_cap, who), key0 = __shfl_sync(F, k0, who);
     const uint32_t wl = __shfl_sync(F, wid_lo, who), wh = __shfl_sync(F, wid_hi, who);
-    const uint32_t tail0 = (__shfl_sync(F, frd, who) + __shfl_sync(F, fcnt, who)) & 63u;
-    uint4 *fw = fifo_warp + 128u * who;
+    const uint32_t tail0 = (__shfl_sync(F, frd, who) + __shfl_sync(F, fcnt, who)) & 31u;
+    uint2 *fw = fifo_warp + 96u * who;
     uint32_t added = 0;
     while (!gdone && added == 0) {
       if (gseg >= nseg) {
@@ -661,9 +667,10 @@ struct Lane {
         const uint32_t e = (uint32_t)__popc(am & ((1u << lane) - 1u));
         uint32_t ent[6];
         make_entry(p, key0, wl, wh, jj, u, tau, ent);
-        uint4 *f = fw + 2u * ((tail0 + added + e) & 63u);
-        f[0] = make_uint4(ent[0], ent[1], ent[2], ent[3]);
-        f[1] = make_uint4(ent[4], ent[5], 0u, 0u);
+        uint2 *f = fw + 3u * ((tail0 + added + e) & 31u);
+        f[0] = make_uint2(ent[0], ent[1]);
+        f[1] = make_uint2(ent[2], ent[3]);
+        f[2] = make_uint2(ent[4], ent[5]);
       }
       const uint32_t na = (uint32_t)__popc(am);
       added += na;
@@ -693,9 +700,10 @@ struct Lane {
   LHD void fill_host(const Params &p) {
     uint32_t e[6];
     while (fcnt < 32u && scalar_next(p, e)) {
-      uint4 *f = fifo + 2u * ((frd + fcnt) & 63u);
-      f[0] = make_uint4(e[0], e[1], e[2], e[3]);
-      f[1] = make_uint4(e[4], e[5], 0u, 0u);
+      uint2 *f = fifo + 3u * ((frd + fcnt) & 31u);
+      f[0] = make_uint2(e[0], e[1]);
+      f[1] = make_uint2(e[2], e[3]);
+      f[2] = make_uint2(e[4], e[5]);
       fcnt++;
     }
   }
@@ -709,7 +717,7 @@ struct Lane {
   }
 
   // ------------------------------------------------------------------ a1 scenario decode
-  LHD void init(const Params &p, uint64_t id, uint32_t *smem_lane, uint32_t *hist_lane, uint4 *fifo_lane) {
+  LHD void init(const Params &p, uint64_t id, uint32_t *smem_lane, uint32_t *hist_lane, uint2 *fifo_lane) {
     sm = smem_lane;
     hist = hist_lane;
     fifo = fifo_lane;
@@ -1196,6 +1204,16 @@ struct Lane {
       }
     }
     if (series) p.series_n[rslot] = series_n;
+#ifdef __CUDA_ARCH__
+    {  // the touched histogram lines into L2 at once (the walks below then hit L2)
+      const uint32_t offs[5] = {kHistE2E, kHistTTFT, kHistR, kHistQA, kHistQI};
+      const uint32_t masks[5] = {hm_e2e, hm_ttft, hm_r, hm_q & 0xFFu, hm_q >> 8};
+#pragma unroll
+      for (int h5 = 0; h5 < 5; ++h5)
+        for (uint32_t m = masks[h5]; m; m &= m - 1u)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(hist + offs[h5] + 32u * (ffs32(m) - 1u)));
+    }
+#endif
     unsigned long long *seg = p.seg_hist + (uint64_t)sc.segment * kSegWords;
     uint32_t e50, e99, f50, f99, rm, qa, qi, dummy;
     scan(kHistE2E, BELLMAN_HIST_LAT, hm_e2e, c_served, 50u, 99u, e50, e99, seg);
@@ -1304,7 +1322,7 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
   uint32_t *smem = lane_smem + (threadIdx.x >> 5) * kLaneWarpWords<KV0> + lane_id;
   const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t *hist = p.lane_hist + (uint64_t)gt * kLaneHistWords;
-  uint4 *fifo_warp = p.lane_fifo + (uint64_t)(gt - lane_id) * 128u;  // lane l's ring at + 128 l
+  uint2 *fifo_warp = p.lane_fifo + (uint64_t)(gt - lane_id) * 96u;  // lane l's ring at + 96 l
   const uint32_t kind = KV0 ? 3u : 4u;
   lane::Lane<KV0> L;
   bool has = false, alive = true;
@@ -1326,16 +1344,16 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
         } else {
           const uint64_t sid = p.order ? (uint64_t)p.order[kidx] : p.first + (uint64_t)kidx * p.stride;
           if (lane::mine(p, sid, kind)) {
-            L.init(p, sid, smem, hist, fifo_warp + 128u * lane_id);
+            L.init(p, sid, smem, hist, fifo_warp + 96u * lane_id);
             has = true;
           }
         }
       }
     }
     if (!__any_sync(FULL_MASK, has || alive)) break;
-    // generation: every lane whose FIFO holds <= 31 entries gets 32 candidates
-    // drawn by the whole warp (one lane at a time)
-    uint32_t want = __ballot_sync(FULL_MASK, has && !L.gen_done && L.fcnt <= 31u);
+    // generation: every lane whose FIFO is empty gets 32 candidates drawn by
+    // the whole warp (one lane at a time); its head / next window covers the gap
+    uint32_t want = __ballot_sync(FULL_MASK, has && !L.gen_done && L.fcnt == 0u);
     if (want) {
       const uint32_t w0 = want;
       while (want) {
@@ -1354,13 +1372,13 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
 
 #ifdef BELLMAN_LANECHECK
 // Development only: the same per-scenario code on the CPU (one scenario at a time).
-void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint4 *fifo) {
+void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t *hist, uint2 *fifo) {
   const bellman_profile &pr = p.profs[p.sc[sid].profile];
   if (pr.kv_ns_per_word == 0) {
     lane::Lane<true> L;
     L.init(p, sid, smem_warp, hist, fifo);
     do {
-      if (!L.gen_done && L.fcnt <= 31u) {
+      if (!L.gen_done && L.fcnt == 0u) {
         L.fill_host(p);
         L.after_refill(p);
       }
@@ -1370,7 +1388,7 @@ void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t 
     lane::Lane<false> L;
     L.init(p, sid, smem_warp, hist, fifo);
     do {
-      if (!L.gen_done && L.fcnt <= 31u) {
+      if (!L.gen_done && L.fcnt == 0u) {
         L.fill_host(p);
         L.after_refill(p);
       }

@@ -180,7 +180,7 @@ def test_lane_engine_workspace_and_sass(monkeypatch):
     from paper_2510_15330_b200 import sim
 
     path = B.build()
-    lane_bytes = 40960 * (2760 * 4 + 128 * 16)  # kLaneMaxThreads x (histograms + FIFO)
+    lane_bytes = 40960 * (2760 * 4 + 96 * 8)  # kLaneMaxThreads x (histograms + FIFO)
     big = sim.pack(W.config_c5(n_seeds=256).columns())  # 65,536 scenarios
     small = sim.pack(W.config_c2(n_seeds=1).columns())
     monkeypatch.delenv("BELLMAN_LANE", raising=False)

@@ -108,10 +108,15 @@ struct U4 {
   uint32_t x, y, z, w;
 };
 
-// Philox4x32-10 (Salmon et al. SC'11), counter (c0..c3), key (k0, k1).  Inline:
-// a call would wait for every load still in flight into a register the callee
-// may clobber (the head's table entries are loaded just before it).
-LHD U4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+// Philox4x32-10 (Salmon et al. SC'11), counter (c0..c3), key (k0, k1).  Inline
+// (A/B on full C5, with the leap's integer division: 638 ms inline, 650 ms out
+// of line; code-layout effects in this kernel are not additive).
+#ifdef BELLMAN_AB_PHILOX_CALL
+__host__ __device__ __noinline__
+#else
+LHD
+#endif
+U4 philox(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
                                            uint32_t c3) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
@@ -334,6 +339,7 @@ struct Lane {
   }
   LHD void batch_changed() {
     cbase = t0 + slope * (B > knee ? B - knee : 0u);
+
     if (KV0) return;
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
@@ -454,9 +460,9 @@ struct Lane {
   }
   LHD void ingest_pending() {
 #pragma unroll 1
-    for (uint32_t i = 0; i < npend; ++i) {
-      if (i == 0) ingest(pa_sum, pa_cnt, pa_sec);
-      else ingest(pb_sum, pb_cnt, pb_sec);
+    for (uint32_t i = 0; i < npend; ++i) {  // one inlined copy of the controller
+      const bool b = i != 0;
+      ingest(b ? pb_sum : pa_sum, b ? pb_cnt : pa_cnt, b ? pb_sec : pa_sec);
     }
     npend = 0;
   }
@@ -467,7 +473,8 @@ struct Lane {
     acc_sum = 0;
     acc_cnt = 0;
     const uint32_t nb = sec_bound + 1000000u;
-    sec_bound = t < nb ? nb : (t / 1000000u + 1u) * 1000000u;
+    if (__builtin_expect(t < nb, 1)) sec_bound = nb;  // usually the next second (no division)
+    else sec_bound = (t / 1000000u + 1u) * 1000000u;
   }
 
   LHD void advance(uint32_t t) {
@@ -483,7 +490,12 @@ struct Lane {
   // thinning; R17, R32, R33): its time tau = gen_tau + Exp draw, whether it
   // crosses the segment's end, whether thinning accepts it.
   // The request's attributes and own draws (tag-1 block): the FIFO entry.
-  __device__ __host__ static void make_entry(const Params &p, uint32_t key0, uint32_t wl, uint32_t wh, uint32_t j,
+#ifdef BELLMAN_AB_ENTRY_CALL
+  __device__ __host__ __noinline__ static void make_entry(
+#else
+  __device__ __host__ static void make_entry(
+#endif
+      const Params &p, uint32_t key0, uint32_t wl, uint32_t wh, uint32_t j,
                                              const U4 &u, uint64_t tau, uint32_t e[6]) {
     const uint32_t L = (uint32_t)ldg(&p.tabL[u.z >> 20]);
     const uint32_t xc = u.z & 0xFFFFFu;  // class draw (NEXT-3): the bits below L's index
@@ -1204,7 +1216,7 @@ struct Lane {
       }
     }
     if (series) p.series_n[rslot] = series_n;
-#ifdef __CUDA_ARCH__
+#if defined(__CUDA_ARCH__) && !defined(BELLMAN_AB_NOHISTPF)
     {  // the touched histogram lines into L2 at once (the walks below then hit L2)
       const uint32_t offs[5] = {kHistE2E, kHistTTFT, kHistR, kHistQA, kHistQI};
       const uint32_t masks[5] = {hm_e2e, hm_ttft, hm_r, hm_q & 0xFFu, hm_q >> 8};

@@ -82,7 +82,15 @@ LHD uint32_t ffs32(uint32_t x) {
 #endif
 }
 LHD void red_add(uint32_t *a, uint32_t v) {  // fire-and-forget on the GPU (result unused: RED)
-#ifdef __CUDA_ARCH__
+#if defined(__CUDA_ARCH__) && defined(BELLMAN_AB_RED_EVICT_FIRST)
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+#elif defined(__CUDA_ARCH__) && !defined(BELLMAN_AB_ATOMG)
+  // explicit RED: ptxas emits ATOMG (with a destination register, whose
+  // scoreboard then stalls the next writer of that register) for atomicAdd
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+#elif defined(__CUDA_ARCH__)
   atomicAdd(a, v);
 #else
   *a += v;
@@ -90,7 +98,7 @@ LHD void red_add(uint32_t *a, uint32_t v) {  // fire-and-forget on the GPU (resu
 }
 LHD void seg_add(unsigned long long *a, unsigned long long v) {
 #ifdef __CUDA_ARCH__
-  atomicAdd(a, v);
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 #else
   *a += v;
 #endif

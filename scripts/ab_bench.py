@@ -28,6 +28,7 @@ def main(paths, reps=15):
     sims = []
     for p, L in zip(paths, libs):
         _abi._lib = L
+        pk.pop("_ws_bytes", None)  # builds may lay the workspace out differently
         sims.append(sim.Simulator(packed=pk))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for it in range(reps + 2):

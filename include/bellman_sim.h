@@ -5,8 +5,10 @@
  * an LLM serving node under the beLLMan output-length congestion controller
  * (arXiv 2510.15330).  It follows the paper's problem statement as SPEC.md
  * restates it: run_simulation(trace, server, models, controller?, seed) ->
- * RunResult, batched over scenarios.  One warp of a
- * persistent sm_100a kernel simulates one scenario.
+ * RunResult, batched over scenarios.  Persistent sm_100a
+ * kernels simulate one scenario per warp, or — for large runs of the
+ * benchmark-path scenarios — one scenario per lane (bellman_sim_last_engines);
+ * the records do not depend on the engine.
  *
  * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Rn = reading n in
  * DESIGN.md section 3.  Step names a1..a10 are DESIGN.md section 2.

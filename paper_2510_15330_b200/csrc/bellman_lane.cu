@@ -1099,10 +1099,13 @@ struct Lane {
     uint32_t tn;
     bool mid = false;
     if (busy) {
-      // prefill ends due inside the running iteration, in the open second and
-      // window: handled now (order-free until the iteration end)
+      // prefill ends due inside the running iteration and window: handled now
+      // (order-free until the iteration end; in the TBT-only loop a prefill
+      // end touches no per-second state, so a second boundary needs no split)
       uint32_t lim = iter_end < stop_static ? iter_end : stop_static;
+#ifdef BELLMAN_AB_PF_SECSPLIT
       if (sec_bound < lim) lim = sec_bound;
+#endif
       if (next_pf < lim) prefill_end(lim);
       mid = next_pf < iter_end;
       tn = mid ? next_pf : iter_end;
@@ -1125,7 +1128,9 @@ struct Lane {
       uint32_t lim = tn + 1u;
       if (mid) {
         lim = iter_end < stop_static ? iter_end : stop_static;
+#ifdef BELLMAN_AB_PF_SECSPLIT
         if (sec_bound < lim) lim = sec_bound;
+#endif
       }
       prefill_end(lim);
       if (mid) return false;

@@ -39,8 +39,10 @@ def build() -> str:
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(s) for s in deps):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    # LANECHECK_FLAGS: extra -D flags (a K2L variant under test)
+    extra = os.environ.get("LANECHECK_FLAGS", "").split()
     cmd = ["nvcc", "-DBELLMAN_LANECHECK", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", "-o", OUT] + srcs
+           "-Xcompiler", "-fPIC", "-shared", "-o", OUT] + extra + srcs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(r.stderr)

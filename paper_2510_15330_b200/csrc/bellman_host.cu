@@ -258,7 +258,8 @@ static bellman_status validate(const bellman_sim_desc *d) {
        // (a contending prefill-only iteration >= 1 µs), so ticks <= H / min_iter + 1 must stay < 2^32
       const bellman_profile &pf = d->profiles[sc.profile];
       const uint64_t min_iter = pf.prefill_mode == BELLMAN_PREFILL_CONTENDING ? 1u : pf.t0_us;
-      if ((uint64_t)sc.horizon_us / min_iter + 1u >= 0xFFFFFFFFull)
+      // horizon / min_iter + 1 >= 2^32 - 1, without a 64-bit division per scenario
+      if ((uint64_t)sc.horizon_us >= 0xFFFFFFFEull * min_iter)
         return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon / t0 allows >= 2^32 iterations",
                     (unsigned long long)s);
     }
@@ -354,23 +355,43 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
     }
     h.traces[t] = dt;
   }
-  // series slots: every recorded scenario and every calibration source
+  // One pass over the scenario table (64 B per scenario: at C5's 2^20 the passes
+  // are memory-bound, ~10 ms each): series slots (every recorded scenario and
+  // every calibration source), debug-record slots, and the heavy-first cost rank.
+  // The cost depends only on (trace, horizon): evaluated once per distinct pair.
   h.slot_of.assign(d->n_scenarios, BELLMAN_NONE);
-  std::vector<uint8_t> need(d->n_scenarios, 0);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
-    const bellman_scenario &sc = d->scenarios[s];
-    if (sc.record & BELLMAN_RECORD_SIGNAL) need[s] = 1;
-    const bellman_ctrl &c = d->ctrls[sc.ctrl];
-    if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) need[sc.calib_src] = 1;
-  }
   h.dbg_of.assign(d->n_scenarios, BELLMAN_NONE);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
-    if (!(d->scenarios[s].record & BELLMAN_RECORD_SECONDS)) continue;
-    h.dbg_of[s] = (uint32_t)h.dbg_off.size();
-    const uint64_t cap = (uint64_t)d->scenarios[s].horizon_us / kUs + 2;
-    h.dbg_off.push_back(h.dbg_rows);
-    h.dbg_cap.push_back((uint32_t)cap);
-    h.dbg_rows += cap;
+  std::vector<uint8_t> need(d->n_scenarios, 0);
+  std::vector<uint32_t> rank(d->n_scenarios);
+  std::vector<double> costs;  // distinct costs, in first-seen order
+  {
+    std::unordered_map<uint64_t, uint32_t> memo;  // (trace << 44 | horizon) -> index into costs
+    uint64_t last_key = ~0ull;  // consecutive scenarios usually share the key: skip the lookup
+    uint32_t last_rank = 0;
+    for (uint64_t s = 0; s < d->n_scenarios; ++s) {
+      const bellman_scenario &sc = d->scenarios[s];
+      if (sc.record & BELLMAN_RECORD_SIGNAL) need[s] = 1;
+      const bellman_ctrl &c = d->ctrls[sc.ctrl];
+      if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) need[sc.calib_src] = 1;
+      if (sc.record & BELLMAN_RECORD_SECONDS) {
+        h.dbg_of[s] = (uint32_t)h.dbg_off.size();
+        const uint64_t cap = (uint64_t)sc.horizon_us / kUs + 2;
+        h.dbg_off.push_back(h.dbg_rows);
+        h.dbg_cap.push_back((uint32_t)cap);
+        h.dbg_rows += cap;
+      }
+      const uint64_t key = ((uint64_t)sc.trace << 44) | (uint64_t)sc.horizon_us;  // horizon <= 2^43 (validated)
+      if (key != last_key) {
+        auto it = memo.find(key);
+        if (it == memo.end()) {
+          it = memo.emplace(key, (uint32_t)costs.size()).first;
+          costs.push_back(expected_arrivals(d, sc));
+        }
+        last_key = key;
+        last_rank = it->second;
+      }
+      rank[s] = last_rank;
+    }
   }
   for (uint64_t s = 0; s < d->n_scenarios; ++s) {
     if (!need[s]) continue;
@@ -379,25 +400,6 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
     h.slot_off.push_back(h.series_words);
     h.slot_cap.push_back((uint32_t)cap);
     h.series_words += cap;
-  }
-  // heavy-first order: a stable sort by decreasing expected arrivals.  The cost
-  // depends only on (trace, horizon), so it is evaluated once per distinct pair,
-  // and the order is a stable counting sort over the distinct costs (large sets
-  // have few: C5's 2^20 scenarios have 16)
-  std::vector<uint32_t> rank(d->n_scenarios);
-  std::vector<double> costs;  // distinct costs, in first-seen order
-  {
-    std::unordered_map<uint64_t, uint32_t> memo;  // (trace << 44 | horizon) -> index into costs
-    for (uint64_t s = 0; s < d->n_scenarios; ++s) {
-      const bellman_scenario &sc = d->scenarios[s];
-      const uint64_t key = ((uint64_t)sc.trace << 44) | (uint64_t)sc.horizon_us;  // horizon <= 2^43 (validated)
-      auto it = memo.find(key);
-      if (it == memo.end()) {
-        it = memo.emplace(key, (uint32_t)costs.size()).first;
-        costs.push_back(expected_arrivals(d, sc));
-      }
-      rank[s] = it->second;
-    }
   }
   std::vector<uint32_t> by_cost(costs.size());  // distinct cost indices by decreasing cost
   for (uint32_t i = 0; i < by_cost.size(); ++i) by_cost[i] = i;
@@ -533,15 +535,21 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     delete sim;
     return fail(nullptr, BELLMAN_ECUDA, "SM count query failed");
   }
+  // one pass over the scenario table: calibrated scenarios and which kernels have work
   sim->calibrated.assign(desc->n_scenarios, 0);
   sim->calib_src.assign(desc->n_scenarios, BELLMAN_NONE);
   for (uint64_t s = 0; s < desc->n_scenarios; ++s) {
-    const bellman_ctrl &c = desc->ctrls[desc->scenarios[s].ctrl];
+    const bellman_scenario &sc = desc->scenarios[s];
+    const bellman_ctrl &c = desc->ctrls[sc.ctrl];
     if (c.calibrated) {
       sim->calibrated[s] = 1;
       sim->has_calibrated = true;
-      sim->calib_src[s] = desc->scenarios[s].calib_src;
+      sim->calib_src[s] = sc.calib_src;
     }
+    const uint32_t k1 = kind_of(desc, sc, 1u);
+    const int dbg = (sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0;
+    sim->has_kind[1][dbg][k1] = true;
+    sim->has_kind[0][dbg][k1 >= 3u ? 0u : k1] = true;  // without K2L, its scenarios run in the TBT warp loop
   }
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)workspace;
@@ -604,11 +612,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   sim->host_order = h.order;
   sim->dbg_slot = h.dbg_of;
   sim->has_dbg = !h.dbg_off.empty();
-  for (uint64_t k = 0; k < desc->n_scenarios; ++k) {
-    const bellman_scenario &sc = desc->scenarios[k];
-    for (uint32_t lo = 0; lo < 2; ++lo)
-      sim->has_kind[lo][(sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0][kind_of(desc, sc, lo)] = true;
-  }
+
   sim->dbg_off = h.dbg_off;
   sim->dbg_cap = h.dbg_cap;
 

@@ -34,7 +34,7 @@ constexpr uint64_t kLaneMaxThreads = (uint64_t)kLaneMaxCtas * 32u * 8u;
 // the generic warp engine, 2 the multi-replica warp engine, 3 / 4 the
 // lane-per-scenario engine K2L (kv = 0 / kv > 0).  K2L takes the scenarios of
 // kind 0 on a Poisson trace whose instants fit 31 bits (horizon < 2^31 µs) and
-// whose iteration indices stay far from 2^32 (horizon / t0 < 2^31), unless lane_on is 0.
+// (so iteration indices stay below 2^31: t0 >= 1), unless lane_on is 0.
 __host__ __device__ __forceinline__ uint32_t scenario_kind_of(const bellman_scenario &sc, const bellman_ctrl &cc,
                                                               const bellman_profile &pf, uint32_t trace_kind,
                                                               uint32_t lane_on) {
@@ -43,8 +43,7 @@ __host__ __device__ __forceinline__ uint32_t scenario_kind_of(const bellman_scen
   const bool tbto = cc.signal == BELLMAN_SIG_TBT && pf.prefill_mode == BELLMAN_PREFILL_NONBLOCKING &&
                     pf.kv_cap_words == 0 && pf.tpw_q16 == 0u && cc.law < BELLMAN_LAW_MPC;
   if (!tbto) return 1u;
-  if (lane_on && trace_kind == 0u && sc.horizon_us < (1ll << 31) &&
-      (uint64_t)sc.horizon_us / pf.t0_us < (1ull << 31))
+  if (lane_on && trace_kind == 0u && sc.horizon_us < (1ll << 31))  // t0 >= 1: fewer than 2^31 iterations
     return pf.kv_ns_per_word == 0 ? 3u : 4u;
   return 0u;
 }

@@ -880,30 +880,19 @@ struct Lane {
   LHD void prefill_end(uint32_t lim) {
     uint64_t m = pf_m, st = 0, se = 0;
     uint32_t mpf = kInf, nfirst = 0, n1 = 0, nslo = 0;
-    // software-pipelined over the prefilling slots: the next slot's fields are
-    // loaded before the current one is processed (pf_m is non-empty here)
-    uint32_t s = ffs64(m) - 1u;
-    m &= m - 1ull;
-    uint32_t key = SL(F_PF, s), arr = SL(F_ARR, s), R = SL(F_R, s);
-    for (;;) {
-      const bool more = m != 0;
-      uint32_t s2 = 0, key2 = 0, arr2 = 0, R2 = 0;
-      if (more) {
-        s2 = ffs64(m) - 1u;
-        m &= m - 1ull;
-        key2 = SL(F_PF, s2);
-        arr2 = SL(F_ARR, s2);
-        R2 = SL(F_R, s2);
-      }
+    while (m) {
+      const uint32_t s = ffs64(m) - 1u;
+      m &= m - 1ull;
+      const uint32_t key = SL(F_PF, s);
       if (key < lim) {
-        const uint32_t tt = key - arr;
+        const uint32_t tt = key - SL(F_ARR, s);
         const uint32_t lb = lat_bin(tt);
         st += tt;
         nfirst++;
         hist_add(kHistTTFT, lb, hm_ttft);
         const uint64_t bit = 1ull << s;
         pf_m &= ~bit;
-        if (R == 1u) {  // R9: completes at the prefill end
+        if (SL(F_R, s) == 1u) {
           se += tt;
           nslo += tt > slo_us ? 1u : 0u;
           n1++;
@@ -918,11 +907,6 @@ struct Lane {
       } else if (key < mpf) {
         mpf = key;
       }
-      if (!more) break;
-      s = s2;
-      key = key2;
-      arr = arr2;
-      R = R2;
     }
     next_pf = mpf;
     n_ttft += nfirst;

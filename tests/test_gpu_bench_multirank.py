@@ -21,9 +21,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("extra", [[], ["--nccl-gather"]], ids=["fused", "gather"])
-def test_bench_two_ranks_one_gpu(extra):
-    env = dict(os.environ, BELLMAN_BENCH_SHARE_GPU="1")
+@pytest.mark.parametrize("extra,lane", [([], "1"), (["--nccl-gather"], "1"), ([], "2")],
+                         ids=["fused", "gather", "fused-K2L"])
+def test_bench_two_ranks_one_gpu(extra, lane):
+    """fused-K2L: the same with K2L forced at this size (BELLMAN_LANE=2): the
+    lane kernel's peer stores and bench.py's lane roofline."""
+    env = dict(os.environ, BELLMAN_BENCH_SHARE_GPU="1", BELLMAN_LANE=lane)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", "C2", "--seeds", "16", "--e2e-steps", "1", "--no-peak", "--no-cpu-baseline", *extra]
@@ -38,3 +41,5 @@ def test_bench_two_ranks_one_gpu(extra):
     want = "fused" if not extra else "NCCL all-gather"
     assert d["exchange"].startswith(want), d["exchange"]
     assert d["e2e"]["d2h_bytes_per_step"] == d["config"]["scenarios_per_gpu"] * 272  # the rank's shard only
+    if lane == "2":
+        assert d["engines"]["mask"] & 0x18 and d["roofline"]["unit"] == "G int-lane-ops/s"

@@ -55,7 +55,10 @@ def _rank_main(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_fused_exchange_two_ranks_one_gpu(tmp_path):
+@pytest.mark.parametrize("engine", ["warp", "lane"])
+def test_fused_exchange_two_ranks_one_gpu(tmp_path, monkeypatch, engine):
+    """Both engines store the records to the peers: the warp kernels (the default
+    at this size) and K2L (BELLMAN_LANE=2, inherited by the spawned ranks)."""
     import torch
     import torch.multiprocessing as mp
 
@@ -64,11 +67,13 @@ def test_fused_exchange_two_ranks_one_gpu(tmp_path):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
+    monkeypatch.setenv("BELLMAN_LANE", "2" if engine == "lane" else "0")
     mp.spawn(_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     w = _workload()
     ref = Simulator(w.columns(), device=0)
     ref.run()
     torch.cuda.synchronize()
+    assert (ref.last_engines & 0x18) != 0 if engine == "lane" else ref.last_engines == 1
     want = ref.stats().view(np.uint8).reshape(w.n_scenarios, -1)
     for r in range(2):
         got = np.load(tmp_path / f"full{r}.npy")

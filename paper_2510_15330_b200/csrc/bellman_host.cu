@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <unordered_map>
 #include <vector>
@@ -102,6 +103,59 @@ static bellman_status fail(bellman_sim *sim, bellman_status st, const char *fmt,
 // ---------------------------------------------------------------------------
 // validation (S:185 max_batch >= 1, knee <= max_batch; S:269 0 < r_min <= r_max < 1,
 // t1 < t2, window >= 1; S:51 positive durations, non-negative rates)
+// One scenario's descriptor checks; `report` writes the message (the caller's
+// thread only: the message buffer is thread-local).
+#define REPORT(...) (report ? fail(nullptr, BELLMAN_EINVAL, __VA_ARGS__) : BELLMAN_EINVAL)
+static bellman_status check_scenario(const bellman_sim_desc *d, uint64_t s, bool report) {
+  const bellman_scenario &sc = d->scenarios[s];
+  if (sc.trace >= d->n_traces || sc.profile >= d->n_profiles || sc.ctrl >= d->n_ctrls)
+    return REPORT("scenario %llu: index out of range", (unsigned long long)s);
+  if (sc.segment >= d->n_segments) return REPORT("scenario %llu: segment out of range", (unsigned long long)s);
+  if (sc.mode > BELLMAN_MODE_DRAIN) return REPORT("scenario %llu: bad mode", (unsigned long long)s);
+  if (sc.horizon_us <= 0 || sc.horizon_us > (1ll << 43))
+    return REPORT("scenario %llu: horizon out of range", (unsigned long long)s);
+  if (sc.w0_us > sc.w1_us) return REPORT("scenario %llu: w0 > w1", (unsigned long long)s);
+  {  // the kernel counts iterations in 32 bits: every iteration starts before H and lasts >= t0
+     // (a contending prefill-only iteration >= 1 µs), so ticks <= H / min_iter + 1 must stay < 2^32
+    const bellman_profile &pf = d->profiles[sc.profile];
+    const uint64_t min_iter = pf.prefill_mode == BELLMAN_PREFILL_CONTENDING ? 1u : pf.t0_us;
+    // horizon / min_iter + 1 >= 2^32 - 1, without a 64-bit division per scenario
+    if ((uint64_t)sc.horizon_us >= 0xFFFFFFFEull * min_iter)
+      return REPORT("scenario %llu: horizon / t0 allows >= 2^32 iterations",
+                  (unsigned long long)s);
+  }
+  const bellman_ctrl &c = d->ctrls[sc.ctrl];
+  if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) {
+    if (sc.calib_src >= d->n_scenarios) return REPORT("scenario %llu: calib_src out of range", (unsigned long long)s);
+    const bellman_scenario &src = d->scenarios[sc.calib_src];
+    const bellman_ctrl &sctl = d->ctrls[src.ctrl];
+    if (sctl.calibrated || sctl.law != BELLMAN_LAW_OFF)
+      return REPORT("scenario %llu: calibration source must be an OFF run", (unsigned long long)s);
+    if (sctl.signal != c.signal)
+      return REPORT("scenario %llu: calibration source records another signal", (unsigned long long)s);
+  }
+  return BELLMAN_OK;
+}
+#undef REPORT
+
+// Runs f(lo, hi, chunk) over [0, n) on up to 16 host threads (one chunk each);
+// sets under 32k elements run inline.
+static std::mutex g_par_mu;
+template <class F>
+static void parallel_chunks(uint64_t n, F f) {
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = nt < 1 ? 1 : (nt > 16 ? 16 : nt);
+  if (n < (1u << 15)) nt = 1;
+  const uint64_t step = (n + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) {
+    const uint64_t lo = t * step, hi = std::min<uint64_t>(n, lo + step);
+    if (lo < hi) th.emplace_back(f, lo, hi, t);
+  }
+  f(0, std::min<uint64_t>(n, step), 0u);
+  for (auto &x : th) x.join();
+}
+
 static bellman_status validate(const bellman_sim_desc *d) {
   if (!d) return fail(nullptr, BELLMAN_EINVAL, "desc is NULL");
   if (d->n_traces && (!d->traces || !d->knots)) return fail(nullptr, BELLMAN_EINVAL, "traces/knots NULL");
@@ -245,35 +299,18 @@ static bellman_status validate(const bellman_sim_desc *d) {
       }
     }
   }
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) {
-    const bellman_scenario &sc = d->scenarios[s];
-    if (sc.trace >= d->n_traces || sc.profile >= d->n_profiles || sc.ctrl >= d->n_ctrls)
-      return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: index out of range", (unsigned long long)s);
-    if (sc.segment >= d->n_segments) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: segment out of range", (unsigned long long)s);
-    if (sc.mode > BELLMAN_MODE_DRAIN) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: bad mode", (unsigned long long)s);
-    if (sc.horizon_us <= 0 || sc.horizon_us > (1ll << 43))
-      return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon out of range", (unsigned long long)s);
-    if (sc.w0_us > sc.w1_us) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: w0 > w1", (unsigned long long)s);
-    {  // the kernel counts iterations in 32 bits: every iteration starts before H and lasts >= t0
-       // (a contending prefill-only iteration >= 1 µs), so ticks <= H / min_iter + 1 must stay < 2^32
-      const bellman_profile &pf = d->profiles[sc.profile];
-      const uint64_t min_iter = pf.prefill_mode == BELLMAN_PREFILL_CONTENDING ? 1u : pf.t0_us;
-      // horizon / min_iter + 1 >= 2^32 - 1, without a 64-bit division per scenario
-      if ((uint64_t)sc.horizon_us >= 0xFFFFFFFEull * min_iter)
-        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: horizon / t0 allows >= 2^32 iterations",
-                    (unsigned long long)s);
-    }
-    const bellman_ctrl &c = d->ctrls[sc.ctrl];
-    if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) {
-      if (sc.calib_src >= d->n_scenarios) return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calib_src out of range", (unsigned long long)s);
-      const bellman_scenario &src = d->scenarios[sc.calib_src];
-      const bellman_ctrl &sctl = d->ctrls[src.ctrl];
-      if (sctl.calibrated || sctl.law != BELLMAN_LAW_OFF)
-        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calibration source must be an OFF run", (unsigned long long)s);
-      if (sctl.signal != c.signal)
-        return fail(nullptr, BELLMAN_EINVAL, "scenario %llu: calibration source records another signal", (unsigned long long)s);
-    }
-  }
+  // per-scenario checks on host threads (C5: 2^20 scenarios, a memory-bound
+  // pass over 64 MB); the message names the lowest failing scenario
+  uint64_t bad = ~0ull;
+  parallel_chunks(d->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t s = lo; s < hi; ++s)
+      if (check_scenario(d, s, false) != BELLMAN_OK) {
+        std::lock_guard<std::mutex> lk(g_par_mu);
+        if (s < bad) bad = s;
+        return;
+      }
+  });
+  if (bad != ~0ull) return check_scenario(d, bad, true);
   return BELLMAN_OK;
 }
 
@@ -330,6 +367,13 @@ static double expected_arrivals(const bellman_sim_desc *d, const bellman_scenari
 }
 
 static void prepare(const bellman_sim_desc *d, HostPrep &h) {
+  h.segs.clear();
+  h.slot_off.clear();
+  h.slot_cap.clear();
+  h.series_words = 0;
+  h.dbg_off.clear();
+  h.dbg_cap.clear();
+  h.dbg_rows = 0;
   h.traces.resize(d->n_traces);
   for (uint32_t t = 0; t < d->n_traces; ++t) {
     const bellman_trace &tr = d->traces[t];
@@ -361,37 +405,75 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
   // The cost depends only on (trace, horizon): evaluated once per distinct pair.
   h.slot_of.assign(d->n_scenarios, BELLMAN_NONE);
   h.dbg_of.assign(d->n_scenarios, BELLMAN_NONE);
-  std::vector<uint8_t> need(d->n_scenarios, 0);
-  std::vector<uint32_t> rank(d->n_scenarios);
+  // scratch reused across calls; bound to references here because the worker
+  // threads below would otherwise name their own thread_local instances
+  static thread_local std::vector<uint8_t> need_tls;
+  static thread_local std::vector<uint32_t> rank_tls;
+  std::vector<uint8_t> &need = need_tls;
+  std::vector<uint32_t> &rank = rank_tls;
+  need.assign(d->n_scenarios, 0);
+  rank.resize(d->n_scenarios);
   std::vector<double> costs;  // distinct costs, in first-seen order
   {
-    std::unordered_map<uint64_t, uint32_t> memo;  // (trace << 44 | horizon) -> index into costs
-    uint64_t last_key = ~0ull;  // consecutive scenarios usually share the key: skip the lookup
-    uint32_t last_rank = 0;
-    for (uint64_t s = 0; s < d->n_scenarios; ++s) {
-      const bellman_scenario &sc = d->scenarios[s];
-      if (sc.record & BELLMAN_RECORD_SIGNAL) need[s] = 1;
-      const bellman_ctrl &c = d->ctrls[sc.ctrl];
-      if (c.calibrated && (c.law == BELLMAN_LAW_MAP || c.law == BELLMAN_LAW_STEP)) need[sc.calib_src] = 1;
-      if (sc.record & BELLMAN_RECORD_SECONDS) {
+    // on host threads, one chunk of scenarios each: the chunk's distinct
+    // (trace << 44 | horizon) keys in first-seen order and chunk-local ranks;
+    // merged below in chunk order, so the result is the sequential pass's
+    struct Chunk {
+      std::vector<uint64_t> keys;    // distinct keys, first-seen order
+      std::vector<uint64_t> first;   // a scenario with that key
+      std::vector<uint64_t> calib;   // calibration sources named by the chunk
+      std::vector<uint64_t> dbg;     // debug-recorded scenarios of the chunk
+    };
+    std::vector<Chunk> ch(16);
+    parallel_chunks(d->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      Chunk &c = ch[t];
+      std::unordered_map<uint64_t, uint32_t> memo;
+      uint64_t last_key = ~0ull;  // consecutive scenarios usually share the key: skip the lookup
+      uint32_t last_rank = 0;
+      for (uint64_t s = lo; s < hi; ++s) {
+        const bellman_scenario &sc = d->scenarios[s];
+        if (sc.record & BELLMAN_RECORD_SIGNAL) need[s] = 1;
+        const bellman_ctrl &cc = d->ctrls[sc.ctrl];
+        if (cc.calibrated && (cc.law == BELLMAN_LAW_MAP || cc.law == BELLMAN_LAW_STEP)) c.calib.push_back(sc.calib_src);
+        if (sc.record & BELLMAN_RECORD_SECONDS) c.dbg.push_back(s);
+        const uint64_t key = ((uint64_t)sc.trace << 44) | (uint64_t)sc.horizon_us;  // horizon <= 2^43 (validated)
+        if (key != last_key) {
+          auto it = memo.find(key);
+          if (it == memo.end()) {
+            it = memo.emplace(key, (uint32_t)c.keys.size()).first;
+            c.keys.push_back(key);
+            c.first.push_back(s);
+          }
+          last_key = key;
+          last_rank = it->second;
+        }
+        rank[s] = last_rank;  // chunk-local for now
+      }
+    });
+    std::unordered_map<uint64_t, uint32_t> memo;  // key -> index into costs
+    std::vector<std::vector<uint32_t>> remap(ch.size());
+    for (size_t t = 0; t < ch.size(); ++t) {
+      for (size_t k = 0; k < ch[t].keys.size(); ++k) {
+        auto it = memo.find(ch[t].keys[k]);
+        if (it == memo.end()) {
+          it = memo.emplace(ch[t].keys[k], (uint32_t)costs.size()).first;
+          costs.push_back(expected_arrivals(d, d->scenarios[ch[t].first[k]]));
+        }
+        remap[t].push_back(it->second);
+      }
+      for (uint64_t src : ch[t].calib) need[src] = 1;
+      for (uint64_t s : ch[t].dbg) {
         h.dbg_of[s] = (uint32_t)h.dbg_off.size();
-        const uint64_t cap = (uint64_t)sc.horizon_us / kUs + 2;
+        const uint64_t cap = (uint64_t)d->scenarios[s].horizon_us / kUs + 2;
         h.dbg_off.push_back(h.dbg_rows);
         h.dbg_cap.push_back((uint32_t)cap);
         h.dbg_rows += cap;
       }
-      const uint64_t key = ((uint64_t)sc.trace << 44) | (uint64_t)sc.horizon_us;  // horizon <= 2^43 (validated)
-      if (key != last_key) {
-        auto it = memo.find(key);
-        if (it == memo.end()) {
-          it = memo.emplace(key, (uint32_t)costs.size()).first;
-          costs.push_back(expected_arrivals(d, sc));
-        }
-        last_key = key;
-        last_rank = it->second;
-      }
-      rank[s] = last_rank;
     }
+    parallel_chunks(d->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      const std::vector<uint32_t> &m = remap[t];
+      for (uint64_t s = lo; s < hi; ++s) rank[s] = m[rank[s]];
+    });
   }
   for (uint64_t s = 0; s < d->n_scenarios; ++s) {
     if (!need[s]) continue;
@@ -412,11 +494,28 @@ static void prepare(const bellman_sim_desc *d, HostPrep &h) {
     if (i && costs[by_cost[i]] != costs[by_cost[i - 1]]) ng++;
     group[by_cost[i]] = ng;
   }
-  std::vector<uint64_t> next(costs.empty() ? 0 : ng + 2, 0);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) next[group[rank[s]] + 1]++;
-  for (uint32_t g = 1; g < next.size(); ++g) next[g] += next[g - 1];
+  // counting sort by group, stable: per-chunk counts (host threads), the
+  // chunks' offsets in chunk order, then each chunk scatters its ids
   h.order.resize(d->n_scenarios);
-  for (uint64_t s = 0; s < d->n_scenarios; ++s) h.order[next[group[rank[s]]]++] = (uint32_t)s;
+  if (!costs.empty()) {
+    const uint32_t G = ng + 1;
+    std::vector<std::vector<uint64_t>> cnt(16, std::vector<uint64_t>(G, 0));
+    parallel_chunks(d->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      std::vector<uint64_t> &c = cnt[t];
+      for (uint64_t s = lo; s < hi; ++s) c[group[rank[s]]]++;
+    });
+    uint64_t at = 0;
+    for (uint32_t g = 0; g < G; ++g)
+      for (size_t t = 0; t < cnt.size(); ++t) {  // group-major, then chunk order: the stable order
+        const uint64_t n = cnt[t][g];
+        cnt[t][g] = at;
+        at += n;
+      }
+    parallel_chunks(d->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      std::vector<uint64_t> &c = cnt[t];
+      for (uint64_t s = lo; s < hi; ++s) h.order[c[group[rank[s]]]++] = (uint32_t)s;
+    });
+  }
 }
 
 static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
@@ -492,7 +591,7 @@ extern "C" {
 
 size_t bellman_sim_workspace_bytes(const bellman_sim_desc *desc) {
   if (validate(desc) != BELLMAN_OK) return 0;
-  HostPrep h;
+  static thread_local HostPrep h;  // buffers reused across calls (C5: ~20 MB of per-scenario arrays)
   prepare(desc, h);
   return layout(desc, h).total;
 }
@@ -503,7 +602,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   *out = nullptr;
   bellman_status st = validate(desc);
   if (st != BELLMAN_OK) return st;
-  HostPrep h;
+  static thread_local HostPrep h;  // buffers reused across calls (C5: ~20 MB of per-scenario arrays)
   prepare(desc, h);
   const Layout L = layout(desc, h);
   if (!workspace || ((uintptr_t)workspace & 255u))
@@ -535,21 +634,37 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     delete sim;
     return fail(nullptr, BELLMAN_ECUDA, "SM count query failed");
   }
-  // one pass over the scenario table: calibrated scenarios and which kernels have work
+  // one pass over the scenario table (host threads): calibrated scenarios and
+  // which kernels have work
   sim->calibrated.assign(desc->n_scenarios, 0);
   sim->calib_src.assign(desc->n_scenarios, BELLMAN_NONE);
-  for (uint64_t s = 0; s < desc->n_scenarios; ++s) {
-    const bellman_scenario &sc = desc->scenarios[s];
-    const bellman_ctrl &c = desc->ctrls[sc.ctrl];
-    if (c.calibrated) {
-      sim->calibrated[s] = 1;
-      sim->has_calibrated = true;
-      sim->calib_src[s] = sc.calib_src;
+  {
+    struct Flags {
+      bool cal = false, kind[2][2][5] = {};
+    };
+    std::vector<Flags> fl(16);
+    parallel_chunks(desc->n_scenarios, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      Flags &f = fl[t];
+      for (uint64_t s = lo; s < hi; ++s) {
+        const bellman_scenario &sc = desc->scenarios[s];
+        const bellman_ctrl &c = desc->ctrls[sc.ctrl];
+        if (c.calibrated) {
+          sim->calibrated[s] = 1;
+          f.cal = true;
+          sim->calib_src[s] = sc.calib_src;
+        }
+        const uint32_t k1 = kind_of(desc, sc, 1u);
+        const int dbg = (sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0;
+        f.kind[1][dbg][k1] = true;
+        f.kind[0][dbg][k1 >= 3u ? 0u : k1] = true;  // without K2L, its scenarios run in the TBT warp loop
+      }
+    });
+    for (const Flags &f : fl) {
+      sim->has_calibrated = sim->has_calibrated || f.cal;
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+          for (int k = 0; k < 5; ++k) sim->has_kind[a][b][k] = sim->has_kind[a][b][k] || f.kind[a][b][k];
     }
-    const uint32_t k1 = kind_of(desc, sc, 1u);
-    const int dbg = (sc.record & BELLMAN_RECORD_SECONDS) ? 1 : 0;
-    sim->has_kind[1][dbg][k1] = true;
-    sim->has_kind[0][dbg][k1 >= 3u ? 0u : k1] = true;  // without K2L, its scenarios run in the TBT warp loop
   }
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)workspace;
@@ -628,8 +743,8 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     // the rest of the workspace's input prefix: two H2D copies and one memset
     static_assert(sizeof(bellman_scenario) == 64, "scenario record");
     const size_t base = L.off_tr;  // the staging buffer starts here (off_sc = 0 precedes it)
-    std::vector<uint8_t> stage(L.in_end - base);
-    std::memset(stage.data(), 0, stage.size());
+    static thread_local std::vector<uint8_t> stage;  // reused across creates (no fresh pages per call)
+    stage.assign(L.in_end - base, 0);
     auto put = [&](size_t off, const void *src, size_t bytes) {
       if (bytes) std::memcpy(stage.data() + (off - base), src, bytes);
     };
@@ -945,7 +1060,7 @@ void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t 
 extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_stats *out, unsigned long long *seg,
                                  uint8_t *ran) {
   if (validate(d) != BELLMAN_OK) return -1;
-  HostPrep h;
+  static thread_local HostPrep h;  // buffers reused across calls (C5: ~20 MB of per-scenario arrays)
   prepare(d, h);
   static std::vector<uint2> l2;
   if (l2.empty()) log2_table_build(l2);

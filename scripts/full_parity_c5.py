@@ -24,6 +24,7 @@ def main():
     sim.run()
     torch.cuda.synchronize()
     st = sim.stats()
+    print(f"engines mask {sim.last_engines} (8/16 = K2L lane-per-scenario, 1 = K2 warp-per-scenario)", flush=True)
     b = oracle.Bound(cols)
     n = w.n_scenarios
     bad, t0, chunk = 0, time.time(), 1 << 15

@@ -15,24 +15,30 @@
 // Scope (scenario_kind 3 / 4): the TBT-specialised single-engine
 // scenarios of the product kernel (TBT signal, non-blocking prefill, no KV
 // capacity, word units, MAP / STEP / CONST / OFF; every benchmark
-// configuration) on a Poisson trace with horizon < 2^31 µs and fewer than 2^25
-// possible iterations; kind 3 is the KV-free cost law (kv = 0), kind 4 has the
-// KV term.  Everything else stays on K2.  Semantics are K2's (and the oracle's)
-// step for step; only the data layout differs:
+// configuration) on a Poisson trace with horizon < 2^31 µs, in runs of at
+// least 65,536 scenarios; kind 3 is the KV-free cost law (kv = 0), kind 4 has
+// the KV term.  Everything else stays on K2.  Semantics are K2's (and the
+// oracle's) step for step; only the data layout and the schedule differ:
 //  * all instants are absolute 32-bit µs (horizon < 2^31, iteration and
 //    prefill durations < 2^31: no epoch, no rebase);
 //  * request slots: shared memory [field][slot][lane] (u32; the bank is the
 //    lane whatever the slot, so divergent slot indices never conflict): prefill
-//    end, arrival, realized length R (+ input words with a KV term);
-//  * decoding requests: a binary min-heap per lane of (completion iteration
-//    << 6 | slot) in shared memory (completion iteration < 2^26);
-//  * slot phases: free / prefilling / decode-ready bit masks (u64 registers);
-//  * the FIFO queue head: the next accepted arrival, generated lazily one
-//    candidate at a time (same Philox counters, thinning, crossing rule);
+//    end (then the completion iteration), arrival, realized length R (+ input
+//    words with a KV term); slot phases as u64 bit masks in registers;
+//  * decoding requests: a binary min-heap per lane of one-byte slot indices
+//    (byte loads / stores, still one bank per lane) keyed by the completion
+//    iteration held in the slot's prefill-end word: 26 KB per warp, 8 warps
+//    (one CTA) per SM;
+//  * the FIFO queue ahead of admission: a head / next register window and a
+//    32-entry ring per lane in global memory, refilled 32 candidates at a time
+//    by the whole warp (coop_refill: K2's lane-parallel generator, for one lane
+//    at a time; same Philox counters, thinning and crossing rule);
+//  * the persistent loop starts every trip with a warp vote (reconvergence),
+//    and closed seconds are ingested at one site per trip;
 //  * histograms (a9): per thread in global memory (L2-resident), bumped with
-//    fire-and-forget RED.ADD; a bit mask of the 32-bin groups each scenario
-//    touched bounds the epilogue's percentile scan, segment merge and
-//    re-zeroing to those groups.
+//    fire-and-forget PTX `red` (atomicAdd compiles to ATOMG with a destination
+//    register); a bit mask of the 32-bin groups each scenario touched bounds
+//    the epilogue's percentile walk, segment merge and re-zeroing.
 //
 // The per-scenario code is __host__ __device__: a development build
 // (-DBELLMAN_LANECHECK, bellman_host.cu) runs it on the CPU to compare with

@@ -198,3 +198,27 @@ def test_lane_engine_workspace_and_sass(monkeypatch):
     for b in lane:
         assert "sm_100a" in b.split("\n")[0]
         assert "0 bytes spill stores, 0 bytes spill loads" in b
+
+
+def test_parallel_validation_names_the_lowest_bad_scenario():
+    """Per-scenario validation runs on host threads in chunks (bellman_host.cu
+    parallel_chunks): with invalid scenarios in several chunks the message must
+    still name the lowest one, as a sequential pass would, and workspace
+    sizing must be a pure function of the descriptor."""
+    import numpy as np
+
+    from paper_2510_15330_b200 import _abi as A, sim
+    import workloads as W
+
+    cols = W.config_c5(n_seeds=256).columns()  # 65,536 scenarios: chunked on any multi-core host
+    n = len(cols["sc_seed"])
+    pk = sim.pack(cols)
+    a, b = sim.workspace_bytes(pk), sim.workspace_bytes(sim.pack(cols))
+    assert a == b > 0
+    bad = dict(cols)
+    bad["sc_w0"] = np.asarray(cols["sc_w0"]).copy()
+    bad["sc_w1"] = np.asarray(cols["sc_w1"]).copy()
+    for s in (n - 5, n // 2 + 7, 40_000, 12_345):  # w0 > w1 in four different chunks
+        bad["sc_w0"][s], bad["sc_w1"][s] = 10, 5
+    with pytest.raises(A.BellmanError, match="scenario 12345: w0 > w1"):
+        sim.workspace_bytes(sim.pack(bad))

@@ -282,6 +282,10 @@ struct Lane {
   uint64_t c_admitted, c_served, c_rewritten, c_slo, c_win_served, c_words_in, c_idle, c_win_words_in,
       c_win_idle, c_sum_queue, c_sum_ttft, c_sum_e2e, words_out, win_words_out, n_ttft;
   uint32_t last_j, bypassed, flags, finished;
+  uint32_t segment;                       // the scenario's segment (a9 merge)
+  uint32_t fin_end;                       // end_us of the finished scenario (R20)
+  uint64_t fin_queued;                    // queued at the end
+  uint32_t r_e50, r_e99, r_f50, r_f99, r_rm, r_qa, r_qi;  // percentile bins (kNone: empty)
   // touched 32-bin groups of each histogram (epilogue scan bound)
   uint32_t hm_e2e, hm_ttft, hm_r, hm_q;  // hm_q: qa groups in bits 0-7, qi in bits 8-15
 
@@ -834,6 +838,7 @@ struct Lane {
     c_admitted = c_served = c_rewritten = c_slo = c_win_served = c_words_in = c_idle = c_win_words_in = 0;
     c_win_idle = c_sum_queue = c_sum_ttft = c_sum_e2e = words_out = win_words_out = n_ttft = 0;
     last_j = bypassed = finished = 0;
+    segment = sc.segment;
     hm_e2e = hm_ttft = hm_r = hm_q = 0;
   }
 
@@ -1174,9 +1179,10 @@ struct Lane {
   }
 
   // ------------------------------------------------------------------ termination, a8, a9
-  LHD void finish(const Params &p) {
-    const bellman_scenario &sc = p.sc[sid];
-    const bellman_profile &pr = p.profs[sc.profile];
+  // the end of a scenario: termination and the queue count (finish_pre), the
+  // histogram walks (scan_all on the host; coop_hists, the whole warp, on the
+  // GPU), the record (finish_post)
+  LHD void finish_pre(const Params &p) {
     // R20: a drained run ends at its last event, a cutoff run at H
     const uint32_t end = (drain && finished) ? T : H;
     if (in_sys == 0) idle(T, end);
@@ -1219,6 +1225,8 @@ struct Lane {
       }
     }
     if (series) p.series_n[rslot] = series_n;
+    fin_end = end;
+    fin_queued = queued;
 #if defined(__CUDA_ARCH__) && !defined(BELLMAN_AB_NOHISTPF)
     {  // the touched histogram lines into L2 at once (the walks below then hit L2)
       const uint32_t offs[5] = {kHistE2E, kHistTTFT, kHistR, kHistQA, kHistQI};
@@ -1229,15 +1237,122 @@ struct Lane {
           asm volatile("prefetch.global.L2 [%0];" ::"l"(hist + offs[h5] + 32u * (ffs32(m) - 1u)));
     }
 #endif
-    unsigned long long *seg = p.seg_hist + (uint64_t)sc.segment * kSegWords;
-    uint32_t e50, e99, f50, f99, rm, qa, qi, dummy;
-    scan(kHistE2E, BELLMAN_HIST_LAT, hm_e2e, c_served, 50u, 99u, e50, e99, seg);
-    scan(kHistTTFT, BELLMAN_HIST_LAT, hm_ttft, n_ttft, 50u, 99u, f50, f99, seg + BELLMAN_HIST_LAT);
-    scan(kHistR, BELLMAN_HIST_R, hm_r, c_rewritten, 50u, 0u, rm, dummy, seg + 2 * BELLMAN_HIST_LAT);
-    scan(kHistQA, BELLMAN_HIST_Q, hm_q & 0xFFu, c_rewritten, 50u, 0u, qa, dummy,
+  }
+
+  // the walks one lane at a time (the CPU development build)
+  LHD void scan_all(const Params &p) {
+    unsigned long long *seg = p.seg_hist + (uint64_t)segment * kSegWords;
+    uint32_t dummy;
+    scan(kHistE2E, BELLMAN_HIST_LAT, hm_e2e, c_served, 50u, 99u, r_e50, r_e99, seg);
+    scan(kHistTTFT, BELLMAN_HIST_LAT, hm_ttft, n_ttft, 50u, 99u, r_f50, r_f99, seg + BELLMAN_HIST_LAT);
+    scan(kHistR, BELLMAN_HIST_R, hm_r, c_rewritten, 50u, 0u, r_rm, dummy, seg + 2 * BELLMAN_HIST_LAT);
+    scan(kHistQA, BELLMAN_HIST_Q, hm_q & 0xFFu, c_rewritten, 50u, 0u, r_qa, dummy,
          seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R);
-    scan(kHistQI, BELLMAN_HIST_Q, hm_q >> 8, c_admitted - c_rewritten, 50u, 0u, qi, dummy,
+    scan(kHistQI, BELLMAN_HIST_Q, hm_q >> 8, c_admitted - c_rewritten, 50u, 0u, r_qi, dummy,
          seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q);
+  }
+
+#ifdef __CUDA_ARCH__
+  // One histogram of lane `who`, by the whole warp (converged): lane l takes
+  // the l-th touched 32-bin group (groups in bin order), sums it, merges its
+  // non-zero bins into the segment histogram; a warp prefix sum of the group
+  // counts finds, for each nearest-rank k = max(1, ceil(p n / 100)),
+  // the lane whose group holds the k-th count, which walks its 32 bins; then
+  // the groups are re-zeroed.  K2's warp_percentiles over the touched groups.
+  __device__ static void coop_one(uint32_t *h, uint32_t mask, uint64_t n, uint32_t p0, uint32_t p1, uint32_t &b0,
+                                  uint32_t &b1, unsigned long long *seg, uint32_t lane) {
+    const uint32_t F = 0xffffffffu;
+    const uint32_t ng = (uint32_t)__popc(mask);
+    const bool mine = lane < ng;
+    const uint32_t g = mine ? (uint32_t)__fns(mask, 0, (int)lane + 1) : 0u;
+    uint4 *v4 = reinterpret_cast<uint4 *>(h + 32u * g);
+    uint32_t csum = 0;
+    if (mine) {
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint4 v = v4[i];
+        const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k)
+          if (c[k]) seg_add(&seg[32u * g + 4u * i + k], c[k]);
+        csum += v.x + v.y + v.z + v.w;
+      }
+    }
+    uint32_t incl = csum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(F, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    b0 = b1 = kNone;
+    if (n != 0) {
+#pragma unroll 1
+      for (uint32_t q = 0; q < 2; ++q) {
+        const uint32_t pq = q ? p1 : p0;
+        if (!pq) break;
+        uint64_t k = ((uint64_t)pq * n + 99u) / 100u;
+        if (k < 1) k = 1;
+        const uint32_t bal = __ballot_sync(F, mine && (uint64_t)incl >= k);
+        const uint32_t L = (uint32_t)__ffs((int)bal) - 1u;
+        uint32_t res = 0;
+        if (lane == L) {
+          uint64_t cum = incl - csum;
+          const uint32_t *hb = h + 32u * g;
+#pragma unroll 1
+          for (uint32_t i = 0; i < 32; ++i) {
+            cum += hb[i];
+            if (cum >= k) {
+              res = 32u * g + i;
+              break;
+            }
+          }
+        }
+        res = __shfl_sync(F, res, (int)L);
+        if (q) b1 = res;
+        else b0 = res;
+      }
+    }
+    __syncwarp();  // every lane's reads of the groups precede the re-zeroing
+    if (mine) {
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) v4[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  // every histogram of lane `who` (a finished scenario), by the whole warp
+  __device__ void coop_hists(const Params &p, uint32_t who, uint32_t lane, uint32_t *hist_warp) {
+    const uint32_t F = 0xffffffffu;
+    uint32_t *hb = hist_warp + (uint64_t)who * kLaneHistWords;
+    const uint32_t me = __shfl_sync(F, hm_e2e, who), mt = __shfl_sync(F, hm_ttft, who);
+    const uint32_t mr = __shfl_sync(F, hm_r, who), mq = __shfl_sync(F, hm_q, who);
+    const uint64_t ne = __shfl_sync(F, (unsigned long long)c_served, who);
+    const uint64_t nt = __shfl_sync(F, (unsigned long long)n_ttft, who);
+    const uint64_t nr = __shfl_sync(F, (unsigned long long)c_rewritten, who);
+    const uint64_t na = __shfl_sync(F, (unsigned long long)c_admitted, who);
+    unsigned long long *seg = p.seg_hist + (uint64_t)__shfl_sync(F, segment, who) * kSegWords;
+    uint32_t o[7], dummy;
+    coop_one(hb + kHistE2E, me, ne, 50u, 99u, o[0], o[1], seg, lane);
+    coop_one(hb + kHistTTFT, mt, nt, 50u, 99u, o[2], o[3], seg + BELLMAN_HIST_LAT, lane);
+    coop_one(hb + kHistR, mr, nr, 50u, 0u, o[4], dummy, seg + 2 * BELLMAN_HIST_LAT, lane);
+    coop_one(hb + kHistQA, mq & 0xFFu, nr, 50u, 0u, o[5], dummy, seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R, lane);
+    coop_one(hb + kHistQI, mq >> 8, na - nr, 50u, 0u, o[6], dummy,
+             seg + 2 * BELLMAN_HIST_LAT + BELLMAN_HIST_R + BELLMAN_HIST_Q, lane);
+    if (lane == who) {
+      r_e50 = o[0];
+      r_e99 = o[1];
+      r_f50 = o[2];
+      r_f99 = o[3];
+      r_rm = o[4];
+      r_qa = o[5];
+      r_qi = o[6];
+    }
+  }
+#endif
+
+  // the summary record (a8) from the walks' percentiles
+  LHD void finish_post(const Params &p) {
+    const bellman_profile &pr = p.profs[p.sc[sid].profile];
+    const uint32_t end = fin_end, e50 = r_e50, e99 = r_e99, f50 = r_f50, f99 = r_f99, rm = r_rm, qa = r_qa, qi = r_qi;
+    const uint64_t queued = fin_queued;
     bellman_scenario_stats o;
     o.scenario_id = sid;
     o.ticks = ticks;
@@ -1274,7 +1389,7 @@ struct Lane {
     uint32_t fl = flags | BELLMAN_FLAG_DONE;
     if (queued + in_sys > 0) fl |= BELLMAN_FLAG_TRUNCATED;
     o.flags = fl;
-    o.segment = sc.segment;
+    o.segment = segment;
     o.bypassed = bypassed;
     // energy in fp64 with explicit round-to-nearest ops in a fixed order (R19)
 #ifdef __CUDA_ARCH__
@@ -1337,6 +1452,7 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
   uint32_t *smem = lane_smem + (threadIdx.x >> 5) * kLaneWarpWords<KV0> + lane_id;
   const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t *hist = p.lane_hist + (uint64_t)gt * kLaneHistWords;
+  uint32_t *hist_warp = p.lane_hist + (uint64_t)(gt - lane_id) * kLaneHistWords;  // lane l's at + l x words
   uint2 *fifo_warp = p.lane_fifo + (uint64_t)(gt - lane_id) * 96u;  // lane l's ring at + 96 l
   const uint32_t kind = KV0 ? 3u : 4u;
   lane::Lane<KV0> L;
@@ -1378,8 +1494,16 @@ __global__ void __launch_bounds__(32 * kLaneWarps<KV0>, 1) bellman_lane_kernel(c
       }
       if ((w0 >> lane_id) & 1u) L.after_refill(p);
     }
+    bool fin = false;
     if (has && L.trip(p)) {
-      L.finish(p);
+      L.finish_pre(p);
+      fin = true;
+    }
+    // the finished lanes' histogram walks, by the whole warp, one lane at a time
+    for (uint32_t fm = __ballot_sync(FULL_MASK, fin); fm; fm &= fm - 1u)
+      L.coop_hists(p, (uint32_t)__ffs((int)fm) - 1u, lane_id, hist_warp);
+    if (fin) {
+      L.finish_post(p);
       has = false;
     }
   }
@@ -1398,7 +1522,9 @@ void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t 
         L.after_refill(p);
       }
     } while (!L.trip(p));
-    L.finish(p);
+    L.finish_pre(p);
+    L.scan_all(p);
+    L.finish_post(p);
   } else {
     lane::Lane<false> L;
     L.init(p, sid, smem_warp, hist, fifo);
@@ -1408,7 +1534,9 @@ void lane_host_run(const Params &p, uint64_t sid, uint32_t *smem_warp, uint32_t 
         L.after_refill(p);
       }
     } while (!L.trip(p));
-    L.finish(p);
+    L.finish_pre(p);
+    L.scan_all(p);
+    L.finish_post(p);
   }
 }
 #endif

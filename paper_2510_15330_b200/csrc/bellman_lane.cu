@@ -25,10 +25,10 @@
 //    lane whatever the slot, so divergent slot indices never conflict): prefill
 //    end (then the completion iteration), arrival, realized length R (+ input
 //    words with a KV term); slot phases as u64 bit masks in registers;
-//  * decoding requests: a binary min-heap per lane of one-byte slot indices
-//    (byte loads / stores, still one bank per lane) keyed by the completion
-//    iteration held in the slot's prefill-end word: 26 KB per warp, 8 warps
-//    (one CTA) per SM;
+//  * decoding requests: a 4-ary min-heap per lane of one-byte slot indices
+//    (a node's four children are one 32-bit word; byte stores, still one bank
+//    per lane) keyed by the completion iteration held in the slot's
+//    prefill-end word: 26 KB per warp, 8 warps (one CTA) per SM;
 //  * the FIFO queue ahead of admission: a head / next register window and a
 //    32-entry ring per lane in global memory, refilled 32 candidates at a time
 //    by the whole warp (coop_refill: K2's lane-parallel generator, for one lane
@@ -295,6 +295,7 @@ struct Lane {
   // completion iteration, kept in the slot's (by then unused) prefill-end word
   LHD uint8_t &HB(uint32_t i) const { return reinterpret_cast<uint8_t *>(&sm[(kF * 64u + (i >> 2)) * 32u])[i & 3u]; }
   LHD uint32_t key(uint32_t slot) const { return SL(F_PF, slot); }
+  static constexpr uint32_t kHeapRoot = 3;  // the 4-ary heap's node 0 is byte 3
 
   LHD void hist_add(uint32_t off, uint32_t b, uint32_t &mask, uint32_t shift = 0) {
     red_add(&hist[off + b], 1u);
@@ -302,43 +303,51 @@ struct Lane {
   }
 
   // ------------------------------------------------------------------ decode heap
-  // min-heap of the decoding slots by completion iteration (ties in any order:
-  // completions of one iteration are popped together)
+  // 4-ary min-heap of the decoding slots by completion iteration (ties in any
+  // order: completions of one iteration are popped together).  Node i is heap
+  // byte i + 3, so the children 4i+1 .. 4i+4 of node i are the four bytes of
+  // heap word i + 1: one load per level, then four independent key loads
+  // (depth <= 3 for 64 slots).
+  LHD uint32_t HW(uint32_t w) const { return sm[(kF * 64u + w) * 32u]; }
   LHD void heap_push(uint32_t slot, uint32_t k) {
     uint32_t i = nheap++;
     while (i > 0) {
-      const uint32_t par = (i - 1u) >> 1;
-      const uint32_t ps = HB(par);
+      const uint32_t par = (i - 1u) >> 2;
+      const uint32_t ps = HB(par + 3u);
       if (key(ps) <= k) break;
-      HB(i) = (uint8_t)ps;
+      HB(i + 3u) = (uint8_t)ps;
       i = par;
     }
-    HB(i) = (uint8_t)slot;
+    HB(i + 3u) = (uint8_t)slot;
   }
   LHD uint32_t heap_pop() {
-    const uint32_t top = HB(0);
-    const uint32_t last = HB(--nheap);
+    const uint32_t top = HB(3u);
+    const uint32_t last = HB(--nheap + 3u);
     const uint32_t n = nheap;
     if (n) {
       const uint32_t lk = key(last);
       uint32_t i = 0;
       for (;;) {
-        uint32_t c = 2u * i + 1u;
-        if (c >= n) break;
-        uint32_t cs = HB(c), ck = key(cs);
-        if (c + 1u < n) {
-          const uint32_t c2 = HB(c + 1u), k2 = key(c2);
-          if (k2 < ck) {
-            c++;
-            cs = c2;
-            ck = k2;
+        const uint32_t c0 = 4u * i + 1u;
+        if (c0 >= n) break;
+        const uint32_t w = HW(i + 1u);  // the slot indices of children c0 .. c0 + 3
+        uint32_t bs = w & 0xFFu, bk = key(bs), bc = c0;
+#pragma unroll
+        for (uint32_t q = 1; q < 4; ++q) {
+          if (c0 + q < n) {
+            const uint32_t sq = (w >> (8u * q)) & 0xFFu, kq2 = key(sq);
+            if (kq2 < bk) {
+              bk = kq2;
+              bs = sq;
+              bc = c0 + q;
+            }
           }
         }
-        if (lk <= ck) break;
-        HB(i) = (uint8_t)cs;
-        i = c;
+        if (lk <= bk) break;
+        HB(i + 3u) = (uint8_t)bs;
+        i = bc;
       }
-      HB(i) = (uint8_t)last;
+      HB(i + 3u) = (uint8_t)last;
     }
     return top;
   }
@@ -873,8 +882,8 @@ struct Lane {
         if (!KV0) kd += SL(F_IN, s) + SL(F_R, s);
         hist_add(kHistE2E, lat_bin(e), hm_e2e);
         free_m |= 1ull << s;
-      } while (nheap && key(HB(0)) == it);
-      next_done = nheap ? key(HB(0)) : kInf;
+      } while (nheap && key(HB(kHeapRoot)) == it);
+      next_done = nheap ? key(HB(kHeapRoot)) : kInf;
       if (!KV0) kv_sub((uint64_t)kv * kd);
       c_served += ndone;
       c_sum_e2e += se;
@@ -1060,7 +1069,7 @@ struct Lane {
       rdy_m = 0;
       align = (uint64_t)n_ready * Tn - rdy_sum;
       rdy_sum = 0;
-      next_done = key(HB(0));
+      next_done = key(HB(kHeapRoot));
       if (!KV0) {
         kv_add((uint64_t)kv * rdy_kadd);
         rdy_kadd = 0;

@@ -14,7 +14,7 @@ namespace bellman {
 template <bool KV0>
 constexpr uint32_t kFields = KV0 ? 3u : 4u;
 template <bool KV0>
-constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 16u) * 32u;  // 26 KB / 34 KB
+constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 17u) * 32u;  // 26.1 KB / 34.1 KB (heap: 67 bytes)
 // one CTA per SM: 8 x 26 KB (kv = 0) or 6 x 34 KB of the 227 KB per CTA
 #ifndef BELLMAN_LANE_WARPS0
 #define BELLMAN_LANE_WARPS0 8

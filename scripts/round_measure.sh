@@ -30,5 +30,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tick
 
 for r in C5 C5sub C2; do python scripts/ncu_summary.py $o/${tag}_$r.ncu-rep > $o/${tag}_ncu_full_$r.txt 2>&1; done
 python scripts/ncu_funcs.py $o/${tag}_C5.ncu-rep > $o/${tag}_ncu_funcs_C5.txt 2>&1
-bash scripts/sanitize.sh > $o/${tag}_sanitizer.txt 2>&1; grep -E "ERROR SUMMARY|RACECHECK SUMMARY" $o/${tag}_sanitizer.txt
+# compute-sanitizer (scripts/sanitize.sh) is closed on the GPU pool since r02p: not run here
 echo done

@@ -318,7 +318,7 @@ static bellman_status validate(const bellman_sim_desc *d) {
 struct Layout {
   size_t off_sc, off_tr, off_seg, off_prof, off_ctrl, off_tab, off_log2, off_slot, off_soff, off_scap,
       off_sn, off_series, off_calib, off_stats, off_hist, off_cnt, off_dslot, off_doff, off_dcap, off_dn,
-      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, off_lhist, off_lfifo, total;
+      off_drows, off_dctrl, off_arr, off_ord, off_sord, off_pre, off_lhist, off_lfifo, off_cmag, total;
   size_t in_end;              // [0, in_end): host-filled inputs, one staging copy at create
   size_t zero_beg, zero_end;  // [zero_beg, zero_end): zeroed at create (counters, stats, histograms)
 };
@@ -544,6 +544,7 @@ static Layout layout(const bellman_sim_desc *d, const HostPrep &h) {
   L.off_dcap = take(sizeof(uint32_t) * nd);
   L.off_arr = take(sizeof(bellman_arrival) * d->n_arrivals);
   L.off_ord = take(sizeof(uint32_t) * d->n_scenarios);
+  L.off_cmag = take(sizeof(uint64_t) * kCostMagicB * d->n_profiles);
   L.in_end = o;
   // zeroed at create, contiguous: one memset
   L.zero_beg = o;
@@ -585,6 +586,18 @@ static void log2_table_build(std::vector<uint2> &out) {
     if (i > 0) out[i - 1] = make_uint2((uint32_t)prev, (uint32_t)(t - prev));
     prev = t;
   }
+}
+
+// K2L's leap reciprocals (bellman_internal.cuh): M = ceil(2^63 / c(B)) for
+// B = 0 .. 64 of every profile whose kv-free cost law stays in [1, 2^31); 0
+// elsewhere (such profiles never run in K2L's kv-free kernel).
+static void cost_magic_build(const bellman_profile *pr, uint32_t n, std::vector<uint64_t> &out) {
+  out.assign((size_t)kCostMagicB * n, 0);
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t b = 0; b < kCostMagicB; ++b) {
+      const uint64_t c = (uint64_t)pr[i].t0_us + (uint64_t)pr[i].slope_us * (b > pr[i].knee ? b - pr[i].knee : 0u);
+      if (c >= 1 && c < (1ull << 31)) out[(size_t)kCostMagicB * i + b] = ((1ull << 63) + c - 1) / c;
+    }
 }
 
 extern "C" {
@@ -721,6 +734,7 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
   P.lane_on = 0;  // set per run
   P.lane_hist = (uint32_t *)(ws + L.off_lhist);
   P.lane_fifo = (uint2 *)(ws + L.off_lfifo);
+  P.cost_magic = (const uint64_t *)(ws + L.off_cmag);
   sim->lane_ok = lane_possible(desc);
   sim->order = (const uint32_t *)(ws + L.off_ord);
   sim->shard_order = (uint32_t *)(ws + L.off_sord);
@@ -765,6 +779,11 @@ bellman_status bellman_sim_create(const bellman_sim_desc *desc, void *workspace,
     put(L.off_dcap, h.dbg_cap.data(), sizeof(uint32_t) * h.dbg_cap.size());
     put(L.off_arr, desc->arrivals, sizeof(bellman_arrival) * desc->n_arrivals);
     put(L.off_ord, h.order.data(), sizeof(uint32_t) * desc->n_scenarios);
+    {
+      std::vector<uint64_t> cm;
+      cost_magic_build(desc->profiles, desc->n_profiles, cm);
+      put(L.off_cmag, cm.data(), sizeof(uint64_t) * cm.size());
+    }
     auto body = [&]() -> bellman_status {
       if (desc->n_scenarios)
         CUDA_TRY(nullptr, cudaMemcpyAsync(ws + L.off_sc, desc->scenarios, sizeof(bellman_scenario) * desc->n_scenarios,
@@ -1077,6 +1096,9 @@ extern "C" int bellman_lanecheck(const bellman_sim_desc *d, bellman_scenario_sta
   P.tabC = d->models.fcomp_q16;
   P.tabQ = d->models.qnoise;
   P.log2tab = l2.data();
+  static thread_local std::vector<uint64_t> cm;
+  cost_magic_build(d->profiles, d->n_profiles, cm);
+  P.cost_magic = cm.data();
   P.poly0 = d->models.poly_q16[0];
   P.poly1 = d->models.poly_q16[1];
   P.poly2 = d->models.poly_q16[2];

@@ -97,7 +97,14 @@ struct Params {
   uint32_t lane_on;    // 1: kind-0 scenarios within K2L's bounds run in K2L (scenario_kind_of)
   uint32_t *lane_hist; // K2L per-thread histograms [kLaneMaxThreads][kLaneHistWords], all-zero between scenarios
   uint2 *lane_fifo;    // K2L per-thread arrival FIFOs [kLaneMaxThreads][32 entries x 3 uint2]
+  const uint64_t *cost_magic;  // K2L: [n_profiles][65] ceil(2^63 / cost(B)) of the kv-free cost law (0: unused)
 };
+
+// K2L's leap divides by the kv-free iteration cost c(B) = t0 + slope max(0, B - knee)
+// through a per-profile reciprocal table (cost_magic_build): floor(n / c) =
+// floor(M n / 2^63) with M = ceil(2^63 / c), exact for n < 2^32 and 1 <= c < 2^31
+// (M c - 2^63 = e < c, so e n < 2^63 keeps the error below one quotient step).
+constexpr uint32_t kCostMagicB = 65;  // B = 0 .. 64
 
 }  // namespace bellman
 

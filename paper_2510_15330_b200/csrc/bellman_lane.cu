@@ -28,7 +28,13 @@
 //  * decoding requests: a 4-ary min-heap per lane of one-byte slot indices
 //    (a node's four children are one 32-bit word; byte stores, still one bank
 //    per lane) keyed by the completion iteration held in the slot's
-//    prefill-end word: 26 KB per warp, 8 warps (one CTA) per SM;
+//    prefill-end word; every position past the heap's size holds a sentinel
+//    slot whose key is kInf (no bounds tests), and a pop returns the new least
+//    key: 27.5 KB per warp, 8 warps (one CTA) per SM;
+//  * the kv-free leap divides by the iteration cost through a per-profile
+//    reciprocal table (exact: bellman_internal.cuh);
+//  * one prefill-end site per trip, before the clock advance (a second one
+//    only for ends at or past a window / horizon boundary);
 //  * the FIFO queue ahead of admission: a head / next register window and a
 //    32-entry ring per lane in global memory, refilled 32 candidates at a time
 //    by the whole warp (coop_refill: K2's lane-parallel generator, for one lane
@@ -190,7 +196,14 @@ LHD uint64_t div_u64(uint64_t a, uint64_t b) {
   return a / b;
 }
 // NEXT-2 similarity decay: q_active - floor((q_active - q_floor) X / D)
-__host__ __device__ __noinline__ int32_t sim_decay(uint32_t q_active, uint32_t q_floor, uint64_t X, uint64_t D) {
+// inline: A/B on full C5 with the one-site prefill loop, 494.3 ms vs 502.6 ms
+// out of line (BELLMAN_AB_DECAY_CALL)
+#ifndef BELLMAN_AB_DECAY_CALL
+LHD
+#else
+__host__ __device__ __noinline__
+#endif
+int32_t sim_decay(uint32_t q_active, uint32_t q_floor, uint64_t X, uint64_t D) {
   const uint64_t aX = (uint64_t)(q_active - q_floor) * X;
 #ifdef __CUDA_ARCH__
   uint32_t q = (uint32_t)__fmul_rz((float)aX, __frcp_rn((float)D));  // estimate, then an exact fix-up
@@ -227,11 +240,21 @@ LHD uint32_t realized_len(const Params &p, uint32_t P, uint32_t fcq, uint32_t ra
 }
 
 // slot fields: word (f, s) of this lane at sm[(f * 64 + s) * 32]; the heap follows the fields
+#ifdef BELLMAN_AB_NOSENT
 constexpr uint32_t F_PF = 0, F_ARR = 1, F_R = 2, F_IN = 3;
+#endif
 
 template <bool KV0>
 struct Lane {
   static constexpr uint32_t kF = kFields<KV0>;
+#ifndef BELLMAN_AB_NOSENT
+  // the prefill-end / completion-key field last: its slot 64 is the sentinel
+  // word (kInf) that precedes the heap
+  static constexpr uint32_t F_ARR = 0, F_R = 1, F_IN = 2, F_PF = kF - 1u, kHeapW = kF * 64u + 1u;
+  static constexpr uint32_t kSent = 64;  // sentinel slot index: key(kSent) = kInf
+#else
+  static constexpr uint32_t kHeapW = kF * 64u;
+#endif
   // ---- storage
   uint32_t *sm;    // this lane's word 0 of its warp's slot region (stride 32 words)
   uint32_t *hist;  // this thread's histograms (global, kLaneHistWords)
@@ -256,6 +279,8 @@ struct Lane {
   uint32_t T, busy, iter_end, iter_d, ticks, next_done, next_pf;
   uint64_t iter_align;
   uint32_t n_ready, B, in_sys, cbase, kq, kr, kstep_q, kstep_r;
+  const uint64_t *cm;  // kv = 0: this profile's leap reciprocals ceil(2^63 / c(B)), B = 0 .. 64
+  uint64_t cmag;       // kv = 0: cm[B] (loaded at each batch change, used by the next leap)
   uint32_t win_now, win_next, stop_static, sec_bound;
   uint64_t acc_sum;
   uint32_t acc_cnt;
@@ -293,7 +318,7 @@ struct Lane {
   // decode heap: position i is byte i & 3 of heap word i >> 2 (slot indices,
   // byte loads / stores; the bank is still the lane); the key of slot s is its
   // completion iteration, kept in the slot's (by then unused) prefill-end word
-  LHD uint8_t &HB(uint32_t i) const { return reinterpret_cast<uint8_t *>(&sm[(kF * 64u + (i >> 2)) * 32u])[i & 3u]; }
+  LHD uint8_t &HB(uint32_t i) const { return reinterpret_cast<uint8_t *>(&sm[(kHeapW + (i >> 2)) * 32u])[i & 3u]; }
   LHD uint32_t key(uint32_t slot) const { return SL(F_PF, slot); }
   static constexpr uint32_t kHeapRoot = 3;  // the 4-ary heap's node 0 is byte 3
 
@@ -308,7 +333,7 @@ struct Lane {
   // byte i + 3, so the children 4i+1 .. 4i+4 of node i are the four bytes of
   // heap word i + 1: one load per level, then four independent key loads
   // (depth <= 3 for 64 slots).
-  LHD uint32_t HW(uint32_t w) const { return sm[(kF * 64u + w) * 32u]; }
+  LHD uint32_t HW(uint32_t w) const { return sm[(kHeapW + w) * 32u]; }
   LHD void heap_push(uint32_t slot, uint32_t k) {
     uint32_t i = nheap++;
     while (i > 0) {
@@ -320,7 +345,57 @@ struct Lane {
     }
     HB(i + 3u) = (uint8_t)slot;
   }
-  LHD uint32_t heap_pop() {
+#ifndef BELLMAN_AB_NOSENT
+  // Every position >= nheap (up to position 84, the last child of a depth-2
+  // node) holds the sentinel slot, whose key is kInf: no bounds tests in the
+  // sift-down, which stops when the moved key is <= the least child (kInf
+  // included) or at depth 3.
+  // Returns the popped slot; rk = the new root's key (kInf: empty), which the
+  // first level's comparison already decides (the moved key or the least child).
+  LHD uint32_t heap_pop(uint32_t &rk) {
+    const uint32_t top = HB(3u);
+    const uint32_t n = --nheap;
+    const uint32_t last = HB(n + 3u);
+    HB(n + 3u) = (uint8_t)kSent;
+    const uint32_t lk = key(last);
+    uint32_t i = 0;
+    rk = kInf;
+    if (n) {
+#pragma unroll
+      for (uint32_t lvl = 0; lvl < 3u; ++lvl) {  // depth <= 3: at most three levels down
+        const uint32_t c0 = 4u * i + 1u;
+        const uint32_t w = HW(i + 1u);  // the slot indices of children c0 .. c0 + 3
+        uint32_t bs = w & 0xFFu, bk = key(bs), bc = c0;
+#pragma unroll
+        for (uint32_t q = 1; q < 4; ++q) {
+          const uint32_t sq = (w >> (8u * q)) & 0xFFu, kq2 = key(sq);
+          if (kq2 < bk) {
+            bk = kq2;
+            bs = sq;
+            bc = c0 + q;
+          }
+        }
+#ifndef BELLMAN_AB_NOKEYTRACK
+        if (lvl == 0) rk = lk <= bk ? lk : bk;
+#endif
+        if (lk <= bk) break;
+        HB(i + 3u) = (uint8_t)bs;
+        i = bc;
+      }
+      HB(i + 3u) = (uint8_t)last;
+    }
+#ifdef BELLMAN_AB_NOKEYTRACK
+    rk = key(HB(kHeapRoot));
+#endif
+    return top;
+  }
+  LHD void heap_reset() {  // all positions sentinel, the sentinel key kInf
+    sm[(kHeapW - 1u) * 32u] = kInf;
+#pragma unroll
+    for (uint32_t w = 0; w < 22u; ++w) sm[(kHeapW + w) * 32u] = kSent * 0x01010101u;
+  }
+#else
+  LHD uint32_t heap_pop(uint32_t &rk) {
     const uint32_t top = HB(3u);
     const uint32_t last = HB(--nheap + 3u);
     const uint32_t n = nheap;
@@ -349,8 +424,12 @@ struct Lane {
       }
       HB(i + 3u) = (uint8_t)last;
     }
+    rk = nheap ? key(HB(kHeapRoot)) : kInf;
     return top;
   }
+
+  LHD void heap_reset() {}
+#endif
 
   // ------------------------------------------------------------------ helpers
   LHD uint32_t rung_at(uint32_t i) const {
@@ -366,7 +445,9 @@ struct Lane {
   }
   LHD void batch_changed() {
     cbase = t0 + slope * (B > knee ? B - knee : 0u);
-
+#ifndef BELLMAN_AB_LEAPDIV
+    if (KV0) cmag = ldg(cm + B);
+#endif
     if (KV0) return;
     const uint32_t ks = kv * B;
     kstep_q = ks / 1000u;
@@ -766,6 +847,7 @@ struct Lane {
     const bellman_profile &pr = p.profs[sc.profile];
     const DevTrace tr = p.traces[sc.trace];
     t0 = pr.t0_us;
+    cm = p.cost_magic + (uint64_t)kCostMagicB * sc.profile;
     knee = pr.knee;
     slope = pr.slope_us;
     kv = KV0 ? 0u : pr.kv_ns_per_word;
@@ -829,6 +911,7 @@ struct Lane {
     rdy_sum = 0;
     rdy_kadd = 0;
     nheap = 0;
+    heap_reset();
     // generator
     k0 = sc.seed_index;
     wid_lo = (uint32_t)sc.wid;
@@ -873,8 +956,9 @@ struct Lane {
     if (it == next_done) {
       uint64_t se = 0;
       uint32_t ndone = 0, nslo = 0, kd = 0;
+      uint32_t rk;
       do {
-        const uint32_t s = heap_pop();
+        const uint32_t s = heap_pop(rk);
         const uint32_t e = T - SL(F_ARR, s);
         se += e;
         nslo += e > slo_us ? 1u : 0u;
@@ -882,8 +966,8 @@ struct Lane {
         if (!KV0) kd += SL(F_IN, s) + SL(F_R, s);
         hist_add(kHistE2E, lat_bin(e), hm_e2e);
         free_m |= 1ull << s;
-      } while (nheap && key(HB(kHeapRoot)) == it);
-      next_done = nheap ? key(HB(kHeapRoot)) : kInf;
+      } while (rk == it);  // rk: the new root's key (kInf when empty)
+      next_done = rk;
       if (!KV0) kv_sub((uint64_t)kv * kd);
       c_served += ndone;
       c_sum_e2e += se;
@@ -1018,7 +1102,12 @@ struct Lane {
       const uint32_t left = nmax - done;
       uint32_t n = 0, used = 0;
       if (KV0) {
+#ifdef BELLMAN_AB_LEAPDIV
         const uint32_t nn = room / cb;
+#else
+        // floor(room / c(B)) by the profile's reciprocal (exact: bellman_internal.cuh)
+        const uint32_t nn = (uint32_t)mulhi64(cmag, (uint64_t)room << 1);
+#endif
         n = nn < left ? nn : left;
         used = n * cb;
       } else {
@@ -1065,11 +1154,16 @@ struct Lane {
         const uint32_t k = it0 + SL(F_R, s) - 2u;
         SL(F_PF, s) = k;
         heap_push(s, k);
+#ifndef BELLMAN_AB_NOKEYTRACK
+        next_done = k < next_done ? k : next_done;  // the heap's least key (pushes only add keys)
+#endif
       }
       rdy_m = 0;
       align = (uint64_t)n_ready * Tn - rdy_sum;
       rdy_sum = 0;
+#ifdef BELLMAN_AB_NOKEYTRACK
       next_done = key(HB(kHeapRoot));
+#endif
       if (!KV0) {
         kv_add((uint64_t)kv * rdy_kadd);
         rdy_kadd = 0;
@@ -1099,6 +1193,61 @@ struct Lane {
 
   // ------------------------------------------------------------------ one event trip
   // Returns true when the scenario's event loop is over (finished: drained).
+#ifndef BELLMAN_AB_PF2
+  // One prefill-end call site per trip for every lane: before the clock
+  // advance, the ends due before min(next event + 1, stop_static) — a busy
+  // lane's ends inside its running iteration and at its end, an idle lane's
+  // ends at its next event.  Order-free against the iteration end, the clock
+  // advance and the ingest of the same trip (disjoint state but commutative
+  // sums; the window flag cannot change below stop_static), so each lane's
+  // result is the two-site loop's; only ends at or past a window / horizon
+  // boundary (stop_static) keep the second, post-advance site (rare).
+  LHD bool trip(const Params &p) {
+    uint32_t tn, lim;
+    bool mid = false;
+    if (busy) {
+      tn = iter_end;
+      lim = iter_end + 1u < stop_static ? iter_end + 1u : stop_static;
+    } else {
+      tn = next_pf;
+      if (in_sys < maxb && head_t < tn) tn = head_t;
+      if (tn == kInf) {
+        finished = 1;
+        return true;
+      }
+      if ((tn >= H) | (in_sys == 0)) {
+        if (tn >= H) return true;
+        idle(T, tn);
+      }
+      lim = tn + 1u < stop_static ? tn + 1u : stop_static;
+    }
+    if (next_pf < lim) prefill_end(lim);
+    if (busy) {
+      mid = next_pf < iter_end;
+      if (mid) tn = next_pf;
+      if (tn >= H) return true;
+    }
+    advance(tn);
+    ingest_pending();
+    if (busy && !mid) iteration_end();
+    if (next_pf == tn) {  // at or past a window / horizon boundary only
+      uint32_t lim2 = tn + 1u;
+      if (mid) lim2 = iter_end < stop_static ? iter_end : stop_static;
+      prefill_end(lim2);
+      if (mid) return false;
+    }
+    if (in_sys < maxb && head_t <= tn) admit(p);
+    if (n_ready + B > 0) {
+      bool join;
+      do {
+        join = n_ready != 0;
+        if (!join) leap();
+        start_iteration();
+      } while (join && quiet_end());
+    }
+    return false;
+  }
+#else
   LHD bool trip(const Params &p) {
     uint32_t tn;
     bool mid = false;
@@ -1150,6 +1299,7 @@ struct Lane {
     }
     return false;
   }
+#endif
 
   // ------------------------------------------------------------------ a9 histogram scan
   // Walk the touched groups of one histogram in bin order: nearest-rank

@@ -13,8 +13,17 @@ namespace bellman {
 // words with a KV term).
 template <bool KV0>
 constexpr uint32_t kFields = KV0 ? 3u : 4u;
+#ifdef BELLMAN_AB_NOSENT
 template <bool KV0>
 constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 17u) * 32u;  // 26.1 KB / 34.1 KB (heap: 67 bytes)
+#else
+// + one sentinel word per lane after the last field (the key kInf of the
+// sentinel slot index 64 that fills every heap position >= the heap's size);
+// the heap spans 22 words: positions 0 .. 84, the children of every node of
+// depth <= 2 (a 4-ary heap of <= 64 slots has depth <= 3)
+template <bool KV0>
+constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 23u) * 32u;  // 27.5 KB / 35.7 KB
+#endif
 // one CTA per SM: 8 x 26 KB (kv = 0) or 6 x 34 KB of the 227 KB per CTA
 #ifndef BELLMAN_LANE_WARPS0
 #define BELLMAN_LANE_WARPS0 8

@@ -6,7 +6,10 @@ import subprocess
 import sys
 
 
-def main(rep, fname="bellman_lane.cu", top=45):
+def main(rep, fname="bellman_lane.cu", local=None, top=45):
+    """local: the source file the kernel was built from, when it differs from
+    the one the report imported (line texts are taken from it)."""
+    loc = open(local).read().split("\n") if local else None
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -31,8 +34,10 @@ def main(rep, fname="bellman_lane.cu", top=45):
     tt = sum(d[3] for d in data) or 1
     print(f"total samples {ts}  warp-instructions {ti / 1e6:.1f}M  thread-instructions/warp-inst {tt / ti:.2f}")
     for ln, s, i, t, src in sorted(data, key=lambda d: -d[2])[:top]:
+        if loc:
+            src = loc[ln - 1].strip()[:80]
         print(f"{ln:5d} {100 * s / ts:5.1f}% smp {100 * i / ti:5.1f}% ins {t / max(i, 1):5.1f} thr  {src}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], *(sys.argv[2:3] or ["bellman_lane.cu"]))
+    main(sys.argv[1], *(sys.argv[2:4] or ["bellman_lane.cu"]))

@@ -80,7 +80,7 @@ LHD uint32_t clz32(uint32_t x) {
 #endif
 }
 LHD uint32_t ffs64(uint64_t x) {  // 1 + index of the lowest set bit, 0 if none
-#ifdef __CUDA_ARCH__
+#if defined(__CUDA_ARCH__)  // (two 32-bit __ffs with a select measured 7 % slower on C5, r02x)
   return (uint32_t)__ffsll((long long)x);
 #else
   return (uint32_t)__builtin_ffsll((long long)x);
@@ -486,6 +486,8 @@ struct Lane {
   // accumulator (sum, cnt) (R3-R5, R12, R21, R38)
   LHD void ingest(uint64_t sum, uint32_t cnt, uint32_t sec) {
     // the sample: floor(sum / cnt) truncated to 32 bits
+    // (an fp32 estimate with an exact fix-up, as for the MAP quotient below,
+    // measured 5 % slower here: 496.4 vs 472.7 ms on C5, r02z)
     const uint32_t x = (uint32_t)div_u64(sum, cnt);
     if (series) {
       if (series_n < series_cap) series[series_n] = x;
@@ -511,7 +513,17 @@ struct Lane {
         if (ex >= den) {
           nr = rmax;  // the quotient is >= r_max - r_min
         } else {  // quotient < r_max - r_min <= 5000; den < 2^35
+#if defined(__CUDA_ARCH__)
+          // fp32 estimate (off by at most one: q < 5000), then the exact fix-up
+          // (A/B on full C5: 478.4 -> 474.1 ms against the integer division, r02y)
+          const uint64_t num = (uint64_t)(rmax - rmin) * ex;
+          uint32_t q = (uint32_t)__fmul_rz((float)num, __frcp_rn((float)den));
+          while (q && (uint64_t)q * den > num) q--;
+          while ((uint64_t)(q + 1u) * den <= num) q++;
+          nr = rmin + q;
+#else
           nr = rmin + (uint32_t)div_u64((uint64_t)(rmax - rmin) * ex, den);
+#endif
           if (nr > rmax) nr = rmax;
         }
         if (nrungs) {  // largest rung <= r (R5)
@@ -1069,9 +1081,9 @@ struct Lane {
         hist_add(kHistQI, qb, hm_q, 8u);
       }
       n_byp += byp ? 1u : 0u;
+      const uint64_t bit = free_m & (0ull - free_m);  // the lowest free slot (no 64-bit shift)
       const uint32_t s = ffs64(free_m) - 1u;
-      const uint64_t bit = 1ull << s;
-      free_m &= ~bit;
+      free_m ^= bit;
       pf_m |= bit;
       const uint32_t pe = Tn + pf;
       SL(F_PF, s) = pe;

@@ -42,8 +42,14 @@ def main(paths, reps=15):
             torch.cuda.synchronize()
             if it >= 2:
                 res[p].append(a.elapsed_time(b))
-    for p in paths:
-        print(f"{os.path.basename(p):40s} median {statistics.median(res[p]):7.3f} ms  min {min(res[p]):7.3f}")
+    # every build's records of the last run, byte for byte, against the first build's
+    recs = []
+    for p, L, s in zip(paths, libs, sims):
+        _abi._lib = L
+        recs.append(s.stats().view("u1"))
+    for p, r in zip(paths, recs):
+        same = "records == first build" if (r == recs[0]).all() else "RECORDS DIFFER from the first build"
+        print(f"{os.path.basename(p):40s} median {statistics.median(res[p]):7.3f} ms  min {min(res[p]):7.3f}  {same}")
 
 
 if __name__ == "__main__":

@@ -180,11 +180,13 @@ LHD uint64_t neglog_q32(uint32_t u, uint2 t) {
 
 // latency bin of a value in µs (a9): exact ms below 32, then 32 per octave.
 // Instants are < 2^32 here, so every latency fits 32 bits.
+// Branch-free (both values, then a select; A/B on full C5: 472.8 -> 465.6 ms
+// against an early return, r02zc): for ms >= 32, ms | 32 has ms's top bit.
 LHD uint32_t lat_bin(uint32_t us) {
   const uint32_t ms = us / 1000u;
-  if (ms < 32) return ms;
-  const uint32_t e = 31u - clz32(ms);
-  return 32u * (e - 4u) + ((ms >> (e - 5u)) & 31u);
+  const uint32_t e = 31u - clz32(ms | 32u);
+  const uint32_t big = 32u * (e - 4u) + ((ms >> (e - 5u)) & 31u);
+  return ms < 32u ? ms : big;
 }
 LHD uint32_t lat_edge(uint32_t b) {
   if (b < 32) return b;

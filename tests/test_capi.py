@@ -101,7 +101,8 @@ def test_sass_sm100a_warp_level_no_transcendentals():
     draws are integer tables): the only MUFU forms are the reciprocal seeds of
     integer / IEEE division (RCP, RCP64H), never EX2 / LG2 / SIN / COS / SQRT / RSQ.
     (Floating point that does appear: the energy epilogue's IEEE fp64 ops and
-    the quality decay's fp32 with an exact integer fix-up.)"""
+    the quality decay's and K2L's MAP-law quotient's fp32 estimates with an
+    exact integer fix-up.)"""
     import re as _re
     import subprocess
 

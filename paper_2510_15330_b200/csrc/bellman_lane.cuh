@@ -15,7 +15,7 @@ template <bool KV0>
 constexpr uint32_t kFields = KV0 ? 3u : 4u;
 #ifdef BELLMAN_AB_NOSENT
 template <bool KV0>
-constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 17u) * 32u;  // 26.1 KB / 34.1 KB (heap: 67 bytes)
+constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 17u) * 32u;  // A/B only: no sentinel (heap: 67 bytes)
 #else
 // + one sentinel word per lane after the last field (the key kInf of the
 // sentinel slot index 64 that fills every heap position >= the heap's size);
@@ -24,7 +24,7 @@ constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 17u) * 32u;  // 26.1 K
 template <bool KV0>
 constexpr uint32_t kLaneWarpWords = (kFields<KV0> * 64u + 23u) * 32u;  // 27.5 KB / 35.7 KB
 #endif
-// one CTA per SM: 8 x 26 KB (kv = 0) or 6 x 34 KB of the 227 KB per CTA
+// one CTA per SM: 8 x 27.5 KB (kv = 0) or 6 x 35.7 KB of the 227 KB per CTA
 #ifndef BELLMAN_LANE_WARPS0
 #define BELLMAN_LANE_WARPS0 8
 #endif
